@@ -1,0 +1,47 @@
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA B200 (runs through the C-ABI library)")
+    config.addinivalue_line("markers", "slow: long-running (full-size) case")
+
+
+def load_golden(name):
+    """Parse a tests/golden/*.txt fixture: '# comments', then 'key: values' lines."""
+    path = os.path.join(ROOT, "tests", "golden", name)
+    out = {}
+    with open(path) as f:
+        for line in f:
+            line = line.strip()
+            if not line or line.startswith("#"):
+                continue
+            key, val = line.split(":", 1)
+            out[key.strip()] = val.split()
+    n, d, m = int(out["n"][0]), int(out["d"][0]), int(out["m"][0])
+    X = np.array([float(v) for v in out["X"]], dtype=np.float32).reshape(n, d)
+    Z = np.array([float(v) for v in out["Z"]], dtype=np.float32).reshape(n, m)
+    Y = np.array([float(v) for v in out["Y"]], dtype=np.float64).reshape(n, m)
+    return X, Z, Y
+
+
+GOLDEN = ["q1_three_points.txt", "q2_identity.txt", "q20_two_dim.txt", "q21_ties_negative.txt"]
+
+
+def col_rel_l2(Y, Yref):
+    """Max over columns of ||Y[:,c]-Yref[:,c]||_2 / ||Yref[:,c]||_2 (abs floor 1e-12*n)."""
+    Y = np.asarray(Y, dtype=np.float64).reshape(Yref.shape[0], -1)
+    Yref = np.asarray(Yref, dtype=np.float64).reshape(Yref.shape[0], -1)
+    worst = 0.0
+    for c in range(Yref.shape[1]):
+        num = np.linalg.norm(Y[:, c] - Yref[:, c])
+        den = np.linalg.norm(Yref[:, c])
+        worst = max(worst, num / den if den > 0 else num / (1e-12 * Yref.shape[0]))
+    return worst
