@@ -1,0 +1,180 @@
+/*
+ * l1dm.h — C ABI of the B200-native l1 distance-matrix block product.
+ *
+ *   Y = A·Z,   A_ij = ||x_i - x_j||_1 = sum_k |x_ik - x_jk|      (§2)
+ *
+ * computed without forming A, by the paper's method: a one-time per-coordinate
+ * sort (Alg. 1) and, per query, prefix sums in sorted order plus one
+ * rank lookup per point and coordinate (Alg. 2; Thm "p=1").
+ * A block Z of m columns is m independent matvecs (Lemma matrixmult).
+ *
+ * Every entry point returns a status code; nothing crosses the ABI as an
+ * exception or abort.  A thread-local message for the last failure is available
+ * from l1dm_last_error().  There is no CPU fallback: without a usable sm_100
+ * device every call that needs one returns L1DM_EDEVICE.
+ *
+ * Pointers may be HOST or DEVICE memory unless a parameter says otherwise; the
+ * library classifies each with cudaPointerGetAttributes.  Host buffers are
+ * staged through library-owned device buffers and make the call synchronous.
+ *
+ * Layouts (all row-major, C order):
+ *   X  n x ld_x  fp32  (point i at X + i*ld_x; coordinates k_begin..k_end-1 used)
+ *   Z  n x ld_z  fp32  (query column c of point j at Z[j*ld_z + c], c < m)
+ *   Y  n x ld_y  fp64  (output, OVERWRITTEN, never accumulated into)
+ *
+ * Threads / streams: a handle is bound to the CUDA device current when it was
+ * prepared.  Calls on one handle must be serialised by the caller (its query
+ * workspace is shared); use one handle per concurrent stream.  Prepared state
+ * is immutable after l1dm_prepare returns, so handles may be queried from
+ * several streams only if each has its own handle.
+ */
+#ifndef L1DM_H
+#define L1DM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define L1DM_API __attribute__((visibility("default")))
+#else
+#define L1DM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct l1dm_ctx *l1dm_handle; /* opaque; owns every internal device buffer */
+
+typedef enum {
+  L1DM_OK = 0,
+  L1DM_EINVAL = -1,     /* null pointer, n/d/m < 1, n >= 2^32, bad leading dimension or range */
+  L1DM_ENONFINITE = -2, /* X holds a NaN or +-Inf (point sets are finite) */
+  L1DM_ENOMEM = -3,     /* a device or pinned-host allocation failed */
+  L1DM_ECUDA = -4,      /* a CUDA runtime error (message in l1dm_last_error) */
+  L1DM_EDEVICE = -5,    /* no sm_100 device, or the handle belongs to another device */
+  L1DM_ENOTIMPL = -6,
+  L1DM_ETIMEOUT = -7    /* a look-back wait exceeded its bound (never expected; results invalid) */
+} l1dm_status;
+
+/* ---------------------------------------------------------------------------
+ * Prepare — Alg. 1: for every coordinate k, a stable ascending
+ * sort of x_{.k}, kept as
+ *   sval[k][r] = x_{perm[k][r], k}   sorted values T_k
+ *   perm[k][r]                       the order pi^k induced by T_k
+ *   rank[k][i] = r with perm[k][r]=i "position of x_i(k) in T_k"
+ *   h[i]       = sum_k x_ik (fp64)   per-point coordinate sum (query epilogue)
+ * Ties are ordered by point index; -0.0 is ordered as +0.0.
+ * X: n x d fp32 (ld_x = d), host or device, BORROWED for the call only (the
+ * library copies what it needs).  Synchronous: returns when the state is
+ * complete.  Errors: EINVAL (X or out null, n < 1, d < 1, n >= 2^32),
+ * ENONFINITE, ENOMEM, ECUDA, EDEVICE.  On error *out is set to NULL.
+ * ------------------------------------------------------------------------- */
+L1DM_API l1dm_status l1dm_prepare(const float *X, int64_t n, int64_t d, l1dm_handle *out);
+
+/* Coordinate shard: prepare only coordinates [k_begin, k_end) of X (n x ld_x).
+ * Queries on the handle then return the shard's PARTIAL product
+ *   Y_g = sum_{k in [k_begin,k_end)} A^(k) Z,  A^(k)_ij = |x_ik - x_jk|,
+ * including the shard's own share of the epilogue, so that the sum of Y_g over
+ * a partition of [0, d) is A·Z exactly up to rounding (swap of sums).
+ * `stream` (a cudaStream_t, may be NULL for a library-created stream) is used for
+ * the prepare work and becomes the handle's default stream.  Synchronous. */
+L1DM_API l1dm_status l1dm_prepare_ex(const float *X, int64_t n, int64_t ld_x, int64_t k_begin,
+                            int64_t k_end, void *stream, l1dm_handle *out);
+
+/* ---------------------------------------------------------------------------
+ * Query — Alg. 2 for the m columns of Z at once:
+ *   y_i = sum_k [ x_ik (S3 - S4) + S2 - S1 ]  per column
+ * evaluated in the equivalent single-array form
+ *   y_i = 2 sum_k U^k_{rank_k(i)} + g - h_i S,  U^k_r = v_r P_r - Q_r,
+ * P, Q the exclusive prefix sums of z and x·z in sorted order, S = 1^T Z,
+ * g = h^T Z; fp64 accumulation of the fp32 inputs.
+ * Z: n x m fp32 (ld_z = m); Y: n x m fp64 (ld_y = m), OVERWRITTEN.
+ * Device Z/Y: stream-ordered on the handle's stream; Z and Y must stay valid
+ * until the stream reaches the end of the call.  Host Z/Y: synchronous.
+ * NaN/Inf in Z are not checked; they propagate into Y by IEEE rules.
+ * Errors: EINVAL (null, m < 1), EDEVICE, ENOMEM (workspace), ECUDA. */
+L1DM_API l1dm_status l1dm_matvec(l1dm_handle h, const float *Z, int64_t m, double *Y);
+
+/* As l1dm_matvec with explicit leading dimensions (ld_z >= m, ld_y >= m) and
+ * stream (NULL = the handle's stream). */
+L1DM_API l1dm_status l1dm_matvec_ex(l1dm_handle h, const float *Z, int64_t ld_z, int64_t m, double *Y,
+                           int64_t ld_y, void *stream);
+
+/* Release every buffer the handle owns.  NULL is a no-op.  Synchronises the
+ * handle's stream first. */
+L1DM_API void l1dm_free(l1dm_handle h);
+
+/* Wait for the handle's stream and report deferred errors: ECUDA for an
+ * asynchronous fault, ETIMEOUT if a look-back wait of an earlier call gave up
+ * (its Y is then invalid).  Stream-ordered device calls return before their
+ * kernels finish, so this is where such failures surface. */
+L1DM_API l1dm_status l1dm_sync(l1dm_handle h);
+
+/* ---------------------------------------------------------------------------
+ * Introspection and control (host-only, no compute).
+ * ------------------------------------------------------------------------- */
+
+/* Shape of a handle: points, local coordinate count, shard range. Any out may be NULL. */
+L1DM_API l1dm_status l1dm_shape(l1dm_handle h, int64_t *n, int64_t *d_local, int64_t *k_begin,
+                       int64_t *k_end);
+
+/* Upper bound on the query workspace (bytes) a query with m columns allocates. */
+L1DM_API size_t l1dm_workspace_bytes(l1dm_handle h, int64_t m);
+
+/* Cap the query workspace (bytes; 0 = automatic, a fraction of free memory).
+ * A smaller cap means more coordinate chunks (more Y read-modify-writes). */
+L1DM_API l1dm_status l1dm_set_workspace_limit(l1dm_handle h, size_t bytes);
+
+/* Query plan, a pure function of the sizes (testable without a GPU).
+ * mb = columns per scan segment; rows_per_tile = scan tile rows; kc = coordinates
+ * per chunk; chunks = ceil(d_local / kc); l2_resident = 1 when a chunk's U
+ * workspace is sized to stay in L2 (small n*m). */
+typedef struct {
+  int64_t mb;
+  int64_t col_blocks;
+  int64_t vec;
+  int64_t lanes_per_row;
+  int64_t rows_per_tile;
+  int64_t tiles_per_segment;
+  int64_t kc;
+  int64_t chunks;
+  int64_t l2_resident;
+  int64_t workspace_bytes;
+} l1dm_plan_t;
+L1DM_API l1dm_status l1dm_plan(int64_t n, int64_t d_local, int64_t m, int64_t l2_bytes,
+                      int64_t workspace_limit, l1dm_plan_t *out);
+
+/* Per-kernel device time (CUDA events on the launching stream).  While enabled,
+ * every launch of every kernel is bracketed by events; read accumulates the
+ * durations of completed launches (it synchronises the handle's stream). */
+typedef struct {
+  double prep_ms;           /* l1dm_prepare total (all prepare kernels) */
+  double colsums_ms;        /* K4: S = 1^T Z, g = h^T Z */
+  double scan_ms;           /* K5: gather + decoupled look-back scan, writes U */
+  double accumulate_ms;     /* K6: rank gather + register accumulation into Y */
+  double copy_ms;           /* host<->device staging (host-pointer calls) */
+  int64_t colsums_launches;
+  int64_t scan_launches;
+  int64_t accumulate_launches;
+  int64_t queries;
+  int64_t kernel_launches;  /* every kernel the library launched while enabled */
+} l1dm_timing_t;
+L1DM_API l1dm_status l1dm_timing_enable(l1dm_handle h, int enable);
+L1DM_API l1dm_status l1dm_timing_read(l1dm_handle h, l1dm_timing_t *out, int reset);
+
+/* Test-only: copy the prepared tables (each d_local x n, coordinate-major) and
+ * h (n) into caller buffers (host or device; any may be NULL). */
+L1DM_API l1dm_status l1dm_debug_export(l1dm_handle h, float *sval, uint32_t *perm, uint32_t *rank,
+                              double *hsum);
+
+/* Thread-local message describing the last non-OK status ("" if none). */
+L1DM_API const char *l1dm_last_error(void);
+
+/* Library version string. */
+L1DM_API const char *l1dm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* L1DM_H */

@@ -1,0 +1,245 @@
+"""Thin Python binding of the C ABI in include/l1dm.h (ctypes; argument marshalling only).
+
+Every step of the hot path runs in libl1dm.so's sm_100a kernels.  There is no CPU
+fallback: if the library is missing the import of this module's functions raises,
+and on a machine without an sm_100 device the library itself returns L1DM_EDEVICE.
+
+Names mirror the C entry points: l1dm_prepare / l1dm_matvec / l1dm_free (BASELINE.json
+north_star), plus the _ex shard/stream variants and the introspection calls.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libl1dm.so")
+
+STATUS = {
+    0: "L1DM_OK", -1: "L1DM_EINVAL", -2: "L1DM_ENONFINITE", -3: "L1DM_ENOMEM",
+    -4: "L1DM_ECUDA", -5: "L1DM_EDEVICE", -6: "L1DM_ENOTIMPL", -7: "L1DM_ETIMEOUT",
+}
+
+EXPORTS = [
+    "l1dm_prepare", "l1dm_prepare_ex", "l1dm_matvec", "l1dm_matvec_ex", "l1dm_free", "l1dm_sync",
+    "l1dm_shape", "l1dm_workspace_bytes", "l1dm_set_workspace_limit", "l1dm_plan",
+    "l1dm_timing_enable", "l1dm_timing_read", "l1dm_debug_export", "l1dm_last_error",
+    "l1dm_version",
+]
+
+
+class L1dmError(RuntimeError):
+    def __init__(self, status: int, where: str, msg: str):
+        super().__init__(f"{where}: {STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+class PlanT(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_int64) for f in (
+        "mb", "col_blocks", "vec", "lanes_per_row", "rows_per_tile", "tiles_per_segment", "kc",
+        "chunks", "l2_resident", "workspace_bytes")]
+
+
+class TimingT(ctypes.Structure):
+    _fields_ = [("prep_ms", ctypes.c_double), ("colsums_ms", ctypes.c_double),
+                ("scan_ms", ctypes.c_double), ("accumulate_ms", ctypes.c_double),
+                ("copy_ms", ctypes.c_double), ("colsums_launches", ctypes.c_int64),
+                ("scan_launches", ctypes.c_int64), ("accumulate_launches", ctypes.c_int64),
+                ("queries", ctypes.c_int64), ("kernel_launches", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libl1dm.so (built in-tree by __graft_entry__.build()).  Raises if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"libl1dm.so not found at {path}; run "
+                          "`python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+    st = ctypes.c_int
+    lib.l1dm_prepare.argtypes = [vp, i64, i64, ctypes.POINTER(vp)]
+    lib.l1dm_prepare_ex.argtypes = [vp, i64, i64, i64, i64, vp, ctypes.POINTER(vp)]
+    lib.l1dm_matvec.argtypes = [vp, vp, i64, vp]
+    lib.l1dm_matvec_ex.argtypes = [vp, vp, i64, i64, vp, i64, vp]
+    lib.l1dm_free.argtypes = [vp]
+    lib.l1dm_free.restype = None
+    lib.l1dm_sync.argtypes = [vp]
+    lib.l1dm_shape.argtypes = [vp] + [ctypes.POINTER(i64)] * 4
+    lib.l1dm_workspace_bytes.argtypes = [vp, i64]
+    lib.l1dm_workspace_bytes.restype = ctypes.c_size_t
+    lib.l1dm_set_workspace_limit.argtypes = [vp, ctypes.c_size_t]
+    lib.l1dm_plan.argtypes = [i64, i64, i64, i64, i64, ctypes.POINTER(PlanT)]
+    lib.l1dm_timing_enable.argtypes = [vp, i32]
+    lib.l1dm_timing_read.argtypes = [vp, ctypes.POINTER(TimingT), i32]
+    lib.l1dm_debug_export.argtypes = [vp, vp, vp, vp, vp]
+    lib.l1dm_last_error.argtypes = []
+    lib.l1dm_last_error.restype = ctypes.c_char_p
+    lib.l1dm_version.argtypes = []
+    lib.l1dm_version.restype = ctypes.c_char_p
+    for name in ("l1dm_prepare", "l1dm_prepare_ex", "l1dm_matvec", "l1dm_matvec_ex", "l1dm_sync",
+                 "l1dm_shape", "l1dm_set_workspace_limit", "l1dm_plan", "l1dm_timing_enable",
+                 "l1dm_timing_read", "l1dm_debug_export"):
+        getattr(lib, name).restype = st
+    _lib = lib
+    return lib
+
+
+def _check(rc: int, where: str):
+    if rc != 0:
+        raise L1dmError(rc, where, load_library().l1dm_last_error().decode())
+
+
+def _ptr(t) -> ctypes.c_void_p:
+    if isinstance(t, torch.Tensor):
+        return ctypes.c_void_p(t.data_ptr())
+    return t.ctypes.data_as(ctypes.c_void_p)
+
+
+def _stream_of(t, stream):
+    if stream is not None:
+        return ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+    if isinstance(t, torch.Tensor) and t.is_cuda:
+        return ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+    return ctypes.c_void_p(0)
+
+
+def _as_f32_2d(A, name):
+    if isinstance(A, np.ndarray):
+        A = torch.from_numpy(np.ascontiguousarray(A))
+    if A.dtype != torch.float32:
+        raise TypeError(f"{name} must be float32, got {A.dtype}")
+    if A.dim() == 1:
+        A = A.view(-1, 1)
+    if A.dim() != 2 or A.stride(1) != 1:
+        A = A.contiguous()
+    return A
+
+
+@dataclass
+class Handle:
+    """An l1dm_handle: prepared state for coordinates [k_begin, k_end) of n points."""
+    ptr: ctypes.c_void_p
+    n: int
+    d_local: int
+    k_begin: int
+    k_end: int
+    device: int
+
+    def __del__(self):
+        if self.ptr:
+            try:
+                load_library().l1dm_free(self.ptr)
+            except Exception:
+                pass
+            self.ptr = None
+
+
+def l1dm_prepare(X, k_begin: int = 0, k_end: int | None = None, stream=None) -> Handle:
+    """Alg. 1: sort every coordinate of X (n x d fp32; host or CUDA tensor)."""
+    lib = load_library()
+    X = _as_f32_2d(X, "X")
+    n, d = X.shape
+    if k_end is None:
+        k_end = d
+    out = ctypes.c_void_p()
+    if X.is_cuda:
+        with torch.cuda.device(X.device):
+            rc = lib.l1dm_prepare_ex(_ptr(X), n, X.stride(0), k_begin, k_end,
+                                     _stream_of(X, stream), ctypes.byref(out))
+        dev = X.device.index
+    else:
+        rc = lib.l1dm_prepare_ex(_ptr(X), n, X.stride(0), k_begin, k_end,
+                                 _stream_of(X, stream), ctypes.byref(out))
+        dev = torch.cuda.current_device() if torch.cuda.is_available() else -1
+    _check(rc, "l1dm_prepare")
+    return Handle(out, n, k_end - k_begin, k_begin, k_end, dev)
+
+
+def l1dm_matvec(h: Handle, Z, Y=None, stream=None):
+    """Alg. 2 for the m columns of Z: returns Y = A·Z (fp64, n x m).
+
+    CUDA tensors: stream-ordered on `stream` (default: torch's current stream).
+    Host tensors / numpy arrays: synchronous, staged through device buffers."""
+    lib = load_library()
+    squeeze = (Z.ndim == 1)
+    Z = _as_f32_2d(Z, "Z")
+    if Z.shape[0] != h.n:
+        raise ValueError(f"Z has {Z.shape[0]} rows, handle has n={h.n}")
+    m = Z.shape[1]
+    if Y is None:
+        Y = torch.empty((h.n, m), dtype=torch.float64, device=Z.device)
+    elif isinstance(Y, np.ndarray):
+        Y = torch.from_numpy(Y)
+    if Y.dtype != torch.float64 or Y.dim() != 2 or Y.shape != (h.n, m) or Y.stride(1) != 1:
+        raise ValueError("Y must be an n x m float64 row-major tensor")
+    if Z.is_cuda:
+        with torch.cuda.device(Z.device):
+            rc = lib.l1dm_matvec_ex(h.ptr, _ptr(Z), Z.stride(0), m, _ptr(Y), Y.stride(0),
+                                    _stream_of(Z, stream))
+    else:
+        rc = lib.l1dm_matvec_ex(h.ptr, _ptr(Z), Z.stride(0), m, _ptr(Y), Y.stride(0),
+                                _stream_of(Z, stream))
+    _check(rc, "l1dm_matvec")
+    return Y.view(-1) if squeeze else Y
+
+
+def l1dm_free(h: Handle):
+    if h is not None and h.ptr:
+        load_library().l1dm_free(h.ptr)
+        h.ptr = None
+
+
+def l1dm_sync(h: Handle):
+    _check(load_library().l1dm_sync(h.ptr), "l1dm_sync")
+
+
+def l1dm_set_workspace_limit(h: Handle, nbytes: int):
+    _check(load_library().l1dm_set_workspace_limit(h.ptr, int(nbytes)), "l1dm_set_workspace_limit")
+
+
+def l1dm_workspace_bytes(h: Handle, m: int) -> int:
+    return int(load_library().l1dm_workspace_bytes(h.ptr, m))
+
+
+def l1dm_plan(n: int, d_local: int, m: int, l2_bytes: int = 126 << 20, workspace_limit: int = 0):
+    p = PlanT()
+    _check(load_library().l1dm_plan(n, d_local, m, l2_bytes, workspace_limit, ctypes.byref(p)),
+           "l1dm_plan")
+    return {f: getattr(p, f) for f, _ in PlanT._fields_}
+
+
+def l1dm_timing_enable(h: Handle, enable: bool = True):
+    _check(load_library().l1dm_timing_enable(h.ptr, 1 if enable else 0), "l1dm_timing_enable")
+
+
+def l1dm_timing_read(h: Handle, reset: bool = False) -> dict:
+    t = TimingT()
+    _check(load_library().l1dm_timing_read(h.ptr, ctypes.byref(t), 1 if reset else 0),
+           "l1dm_timing_read")
+    return {f: getattr(t, f) for f, _ in TimingT._fields_}
+
+
+def l1dm_debug_export(h: Handle):
+    """Test-only: (sval, perm, rank) as d_local x n host arrays and hsum (n)."""
+    sval = np.empty((h.d_local, h.n), dtype=np.float32)
+    perm = np.empty((h.d_local, h.n), dtype=np.uint32)
+    rank = np.empty((h.d_local, h.n), dtype=np.uint32)
+    hs = np.empty(h.n, dtype=np.float64)
+    _check(load_library().l1dm_debug_export(h.ptr, _ptr(sval), _ptr(perm), _ptr(rank), _ptr(hs)),
+           "l1dm_debug_export")
+    return sval, perm, rank, hs
+
+
+def l1dm_version() -> str:
+    return load_library().l1dm_version().decode()

@@ -1,0 +1,678 @@
+// l1dm_api.cu — host runtime and the C ABI declared in include/l1dm.h.
+//
+// Owns the handle lifecycle, device buffers, the query planner, launch sequencing,
+// host<->device staging for host pointers, per-kernel event timing and error mapping.
+// Every compute step runs in the kernels of l1dm_prepare.cu / l1dm_query.cu; there
+// is no host (CPU) evaluation path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "l1dm.h"
+#include "l1dm_internal.h"
+
+using namespace l1dm;
+
+namespace {
+
+thread_local std::string g_err;
+
+l1dm_status fail(l1dm_status st, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define CUDA_TRY(expr)                                                                        \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess) {                                                                  \
+      l1dm_status st_ = (e_ == cudaErrorMemoryAllocation) ? L1DM_ENOMEM : L1DM_ECUDA;         \
+      return fail(st_, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__,      \
+                  __LINE__);                                                                  \
+    }                                                                                         \
+  } while (0)
+
+enum TimingKind { kPrep = 0, kColsums, kScan, kAcc, kCopy, kNumKinds };
+
+struct TimedPair {
+  int kind;
+  cudaEvent_t a, b;
+};
+
+template <typename T>
+struct DevBuf {
+  T *p = nullptr;
+  size_t count = 0;
+  cudaError_t ensure(size_t c, bool zero, cudaStream_t s) {
+    if (c <= count && p) return cudaSuccess;
+    if (p) {
+      cudaFree(p);
+      p = nullptr;
+      count = 0;
+    }
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(c, 1) * sizeof(T));
+    if (e != cudaSuccess) {
+      p = nullptr;
+      return e;
+    }
+    count = c;
+    if (zero) return cudaMemsetAsync(p, 0, std::max<size_t>(c, 1) * sizeof(T), s);
+    return cudaSuccess;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    count = 0;
+  }
+};
+
+bool is_device_pointer(const void *ptr) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();  // clear: unknown pointers are host memory
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+struct l1dm_ctx {
+  int device = -1;
+  int64_t n = 0, dl = 0, k_begin = 0, k_end = 0, ldn = 0;
+  int64_t l2_bytes = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  // prepared state (Alg. 1)
+  DevBuf<uint32_t> sval_bits;  // fp32 bits
+  DevBuf<uint32_t> perm;
+  DevBuf<uint32_t> rank;
+  DevBuf<double> hsum;
+  // query workspace
+  DevBuf<double> U;
+  DevBuf<uint32_t> flags;
+  DevBuf<double> agg, incl;
+  DevBuf<double> part, Sg;
+  DevBuf<unsigned> ctr;        // [0] colsum done counter, [1] timeout flag, [2..] scan tickets
+  size_t ws_limit = 0;
+  uint32_t epoch = 1;
+  // host staging
+  DevBuf<float> Zstage;
+  DevBuf<double> Ystage;
+  // plan cache
+  int64_t plan_m = -1;
+  size_t plan_ws = 0;
+  int plan_vec_cap = 0;
+  QueryPlan plan{};
+  // timing
+  bool timing = false;
+  std::vector<TimedPair> pending;
+  std::vector<cudaEvent_t> pool;
+  double prep_ms = 0.0;
+  double ms[kNumKinds] = {0, 0, 0, 0, 0};
+  int64_t launches[kNumKinds] = {0, 0, 0, 0, 0};
+  int64_t queries = 0;
+  int64_t kernel_launches = 0;
+};
+
+namespace {
+
+cudaEvent_t take_event(l1dm_ctx *h) {
+  if (!h->pool.empty()) {
+    cudaEvent_t e = h->pool.back();
+    h->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct TimedScope {
+  l1dm_ctx *h;
+  int kind;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr;
+  TimedScope(l1dm_ctx *h_, int kind_, cudaStream_t s_) : h(h_), kind(kind_), s(s_) {
+    if (h->timing) {
+      a = take_event(h);
+      cudaEventRecord(a, s);
+    }
+  }
+  ~TimedScope() {
+    if (a) {
+      cudaEvent_t b = take_event(h);
+      cudaEventRecord(b, s);
+      h->pending.push_back({kind, a, b});
+    }
+  }
+};
+
+l1dm_status check_device(l1dm_ctx *h) {
+  int cur = -1;
+  CUDA_TRY(cudaGetDevice(&cur));
+  if (cur != h->device)
+    return fail(L1DM_EDEVICE, "handle belongs to device %d but device %d is current", h->device,
+                cur);
+  return L1DM_OK;
+}
+
+l1dm_status check_arch(int *dev_out) {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return fail(L1DM_EDEVICE, "no CUDA device available (%s)",
+                e == cudaSuccess ? "0 devices" : cudaGetErrorString(e));
+  }
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  int major = 0, minor = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
+  if (major != 10 || minor != 0)
+    return fail(L1DM_EDEVICE, "library is built for sm_100a only; device %d is sm_%d%d", dev, major,
+                minor);
+  *dev_out = dev;
+  return L1DM_OK;
+}
+
+void destroy(l1dm_ctx *h) {
+  if (!h) return;
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (auto &p : h->pending) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  for (auto e : h->pool) cudaEventDestroy(e);
+  h->sval_bits.release();
+  h->perm.release();
+  h->rank.release();
+  h->hsum.release();
+  h->U.release();
+  h->flags.release();
+  h->agg.release();
+  h->incl.release();
+  h->part.release();
+  h->Sg.release();
+  h->ctr.release();
+  h->Zstage.release();
+  h->Ystage.release();
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+// --------------------------------------------------------------------- prepare
+l1dm_status prepare_impl(const float *X, int64_t n, int64_t ld_x, int64_t k_begin, int64_t k_end,
+                         void *stream, l1dm_ctx *h) {
+  int dev = 0;
+  l1dm_status st = check_arch(&dev);
+  if (st != L1DM_OK) return st;
+  h->device = dev;
+  h->n = n;
+  h->k_begin = k_begin;
+  h->k_end = k_end;
+  h->dl = k_end - k_begin;
+  h->ldn = (n + 31) / 32 * 32;
+  int l2 = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
+  h->l2_bytes = l2;
+  if (stream) {
+    h->stream = (cudaStream_t)stream;
+    h->own_stream = false;
+  } else {
+    CUDA_TRY(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    h->own_stream = true;
+  }
+  cudaStream_t s = h->stream;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  CUDA_TRY(cudaEventCreate(&ev0));
+  CUDA_TRY(cudaEventCreate(&ev1));
+  CUDA_TRY(cudaEventRecord(ev0, s));
+
+  const int64_t dl = h->dl, ldn = h->ldn;
+  const size_t elems = (size_t)dl * (size_t)ldn;
+
+  // X may live on the host: stage it (only the rows are needed, all columns copied).
+  const float *Xd = X;
+  DevBuf<float> Xstage;
+  if (!is_device_pointer(X)) {
+    CUDA_TRY(Xstage.ensure((size_t)n * (size_t)ld_x, false, s));
+    CUDA_TRY(cudaMemcpyAsync(Xstage.p, X, (size_t)n * (size_t)ld_x * sizeof(float),
+                             cudaMemcpyHostToDevice, s));
+    Xd = Xstage.p;
+  }
+  DevBuf<uint32_t> keyA, keyB, valA, valB, hist, dbase;
+  DevBuf<unsigned long long> status;
+  DevBuf<unsigned> ctrl;  // [0] nonfinite, [1] timeout, [2] ticket
+  CUDA_TRY(keyA.ensure(elems, false, s));
+  CUDA_TRY(h->rank.ensure(elems, false, s));
+  CUDA_TRY(h->hsum.ensure((size_t)n, false, s));
+  CUDA_TRY(hist.ensure((size_t)dl * 1024, true, s));
+  CUDA_TRY(ctrl.ensure(4, true, s));
+
+  launch_keys(Xd, n, ld_x, k_begin, dl, ldn, keyA.p, h->hsum.p, ctrl.p + 0, s);
+  h->kernel_launches++;
+  launch_hist(keyA.p, n, ldn, dl, hist.p, s);
+  h->kernel_launches++;
+  CUDA_TRY(cudaGetLastError());
+  std::vector<uint32_t> hh((size_t)dl * 1024);
+  unsigned flags_h[4];
+  CUDA_TRY(cudaMemcpyAsync(hh.data(), hist.p, hh.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                           s));
+  CUDA_TRY(cudaMemcpyAsync(flags_h, ctrl.p, sizeof(flags_h), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  Xstage.release();
+  if (flags_h[0]) {
+    keyA.release();
+    hist.release();
+    ctrl.release();
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    return fail(L1DM_ENONFINITE, "X holds a non-finite value in coordinates [%lld, %lld)",
+                (long long)k_begin, (long long)k_end);
+  }
+  // Passes whose digit is constant in every segment are the identity: skip them.
+  std::vector<int> passes;
+  for (int p = 0; p < 4; ++p) {
+    bool trivial_all = true;
+    for (int64_t k = 0; k < dl && trivial_all; ++k) {
+      const uint32_t *hk = &hh[(size_t)k * 1024 + (size_t)p * 256];
+      bool trivial = false;
+      for (int b = 0; b < 256; ++b)
+        if (hk[b] == (uint32_t)n) {
+          trivial = true;
+          break;
+        }
+      trivial_all = trivial;
+    }
+    if (!trivial_all) passes.push_back(p);
+  }
+  const int P = (int)passes.size();
+  if (P == 0) {
+    // keyA holds the keys; emit in place (sval bits over keyA), perm into valA.
+    CUDA_TRY(valA.ensure(elems, false, s));
+    launch_identity_emit(keyA.p, reinterpret_cast<float *>(keyA.p), valA.p, h->rank.p, n, ldn, dl,
+                         s);
+    h->kernel_launches++;
+    h->sval_bits.p = keyA.p;
+    h->sval_bits.count = keyA.count;
+    keyA.p = nullptr;
+    keyA.count = 0;
+    h->perm.p = valA.p;
+    h->perm.count = valA.count;
+    valA.p = nullptr;
+    valA.count = 0;
+  } else {
+    // digit bases: exclusive scan over digits of each segment's histogram, per pass
+    std::vector<uint32_t> db((size_t)dl * 1024);
+    for (int64_t k = 0; k < dl; ++k)
+      for (int p = 0; p < 4; ++p) {
+        uint32_t run = 0;
+        for (int b = 0; b < 256; ++b) {
+          db[(size_t)k * 1024 + (size_t)p * 256 + b] = run;
+          run += hh[(size_t)k * 1024 + (size_t)p * 256 + b];
+        }
+      }
+    // layout for launch: per pass a dl x 256 block
+    std::vector<uint32_t> dbp((size_t)4 * dl * 256);
+    for (int p = 0; p < 4; ++p)
+      for (int64_t k = 0; k < dl; ++k)
+        memcpy(&dbp[((size_t)p * dl + k) * 256], &db[(size_t)k * 1024 + (size_t)p * 256],
+               256 * sizeof(uint32_t));
+    CUDA_TRY(dbase.ensure(dbp.size(), false, s));
+    CUDA_TRY(cudaMemcpyAsync(dbase.p, dbp.data(), dbp.size() * sizeof(uint32_t),
+                             cudaMemcpyHostToDevice, s));
+    CUDA_TRY(keyB.ensure(elems, false, s));
+    CUDA_TRY(valB.ensure(elems, false, s));
+    if (P > 1) CUDA_TRY(valA.ensure(elems, false, s));
+    const int64_t tiles = (n + kSortTile - 1) / kSortTile;
+    CUDA_TRY(status.ensure((size_t)dl * tiles * 256, true, s));
+    uint32_t *kb[2] = {keyA.p, keyB.p};
+    uint32_t *vb[2] = {valA.p, valB.p};
+    for (int i = 0; i < P; ++i) {
+      const int p = passes[i];
+      CUDA_TRY(cudaMemsetAsync(ctrl.p + 2, 0, sizeof(unsigned), s));
+      const uint32_t ep = h->epoch++;
+      launch_sort_pass(i == 0, i == P - 1, kb[i & 1], vb[i & 1], kb[(i + 1) & 1], vb[(i + 1) & 1],
+                       h->rank.p, n, ldn, dl, 8 * p, dbase.p + (size_t)p * dl * 256, status.p, ep,
+                       ctrl.p + 2, ctrl.p + 1, s);
+      h->kernel_launches++;
+      CUDA_TRY(cudaGetLastError());
+    }
+    const int fin = P & 1;
+    DevBuf<uint32_t> *kbuf[2] = {&keyA, &keyB};
+    DevBuf<uint32_t> *vbuf[2] = {&valA, &valB};
+    std::swap(h->sval_bits.p, kbuf[fin]->p);
+    std::swap(h->sval_bits.count, kbuf[fin]->count);
+    std::swap(h->perm.p, vbuf[fin]->p);
+    std::swap(h->perm.count, vbuf[fin]->count);
+  }
+  CUDA_TRY(cudaEventRecord(ev1, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  CUDA_TRY(cudaMemcpy(flags_h, ctrl.p, sizeof(flags_h), cudaMemcpyDeviceToHost));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ev0, ev1);
+  h->prep_ms = ms;
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  keyA.release();
+  keyB.release();
+  valA.release();
+  valB.release();
+  hist.release();
+  dbase.release();
+  status.release();
+  ctrl.release();
+  if (flags_h[1]) return fail(L1DM_ETIMEOUT, "sort look-back wait exceeded its bound");
+  return L1DM_OK;
+}
+
+// --------------------------------------------------------------------- query
+int vec_cap_for(const float *Z, int64_t ldz) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(Z);
+  if (ldz % 4 == 0 && a % 16 == 0) return 4;
+  if (ldz % 2 == 0 && a % 8 == 0) return 2;
+  return 1;
+}
+
+l1dm_status ensure_plan(l1dm_ctx *h, int64_t m, int vec_cap) {
+  size_t ws = h->ws_limit;
+  if (ws == 0) {
+    size_t fr = 0, tot = 0;
+    CUDA_TRY(cudaMemGetInfo(&fr, &tot));
+    ws = (size_t)(0.5 * (double)(fr + h->U.count * sizeof(double) +
+                                 h->agg.count * sizeof(double) * 2));
+  }
+  if (h->plan_m == m && h->plan_ws == ws && h->plan_vec_cap == vec_cap) return L1DM_OK;
+  QueryPlan p;
+  if (!make_plan(h->n, h->dl, m, h->l2_bytes, (int64_t)ws, vec_cap, &p))
+    return fail(L1DM_EINVAL, "no query plan for n=%lld d=%lld m=%lld", (long long)h->n,
+                (long long)h->dl, (long long)m);
+  h->plan = p;
+  h->plan_m = m;
+  h->plan_ws = ws;
+  h->plan_vec_cap = vec_cap;
+  return L1DM_OK;
+}
+
+l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, double *Y,
+                          int64_t ldy, cudaStream_t s) {
+  l1dm_status st = ensure_plan(h, m, vec_cap_for(Z, ldz));
+  if (st != L1DM_OK) return st;
+  const QueryPlan &p = h->plan;
+  CUDA_TRY(h->U.ensure((size_t)p.kc * (size_t)h->n * (size_t)p.ldu, false, s));
+  CUDA_TRY(h->flags.ensure(p.lb_slots, true, s));
+  CUDA_TRY(h->agg.ensure(p.lb_slots * 2 * p.mb, false, s));
+  CUDA_TRY(h->incl.ensure(p.lb_slots * 2 * p.mb, false, s));
+  CUDA_TRY(h->part.ensure((size_t)kColsumBlocks * 2 * m, false, s));
+  CUDA_TRY(h->Sg.ensure((size_t)2 * m, false, s));
+  CUDA_TRY(h->ctr.ensure((size_t)2 + p.chunks, true, s));
+  // K4: column sums (and reset of the per-chunk scan tickets)
+  {
+    TimedScope ts(h, kColsums, s);
+    launch_colsums(Z, ldz, h->n, m, h->hsum.p, h->part.p, h->Sg.p, h->ctr.p + 0, h->ctr.p + 2,
+                   (int)p.chunks, s);
+    h->kernel_launches++;
+    h->launches[kColsums]++;
+  }
+  for (int64_t c = 0; c < p.chunks; ++c) {
+    const int64_t k_first = c * p.kc;
+    const int64_t kcc = std::min<int64_t>(p.kc, h->dl - k_first);
+    {
+      TimedScope ts(h, kScan, s);
+      const uint32_t ep = h->epoch++;
+      if (h->epoch >= (1u << 30)) h->epoch = 1;
+      launch_scan(p, h->perm.p, reinterpret_cast<const float *>(h->sval_bits.p), h->ldn, h->n, Z,
+                  ldz, m, h->U.p, k_first, kcc, h->flags.p, h->agg.p, h->incl.p, ep,
+                  h->ctr.p + 2 + c, h->ctr.p + 1, s);
+      h->kernel_launches++;
+      h->launches[kScan]++;
+    }
+    {
+      TimedScope ts(h, kAcc, s);
+      launch_accumulate(p, h->rank.p, h->ldn, h->n, h->U.p, k_first, kcc, h->hsum.p, h->Sg.p, Y,
+                        ldy, m, c == 0, s);
+      h->kernel_launches++;
+      h->launches[kAcc]++;
+    }
+  }
+  CUDA_TRY(cudaGetLastError());
+  h->queries++;
+  return L1DM_OK;
+}
+
+l1dm_status read_timeout(l1dm_ctx *h) {
+  if (!h->ctr.p) return L1DM_OK;
+  unsigned f = 0;
+  CUDA_TRY(cudaMemcpy(&f, h->ctr.p + 1, sizeof(unsigned), cudaMemcpyDeviceToHost));
+  if (f) {
+    unsigned zero = 0;
+    cudaMemcpy(h->ctr.p + 1, &zero, sizeof(unsigned), cudaMemcpyHostToDevice);
+    return fail(L1DM_ETIMEOUT, "scan look-back wait exceeded its bound; results invalid");
+  }
+  return L1DM_OK;
+}
+
+}  // namespace
+
+// ===================================================================== C ABI
+extern "C" {
+
+l1dm_status l1dm_prepare_ex(const float *X, int64_t n, int64_t ld_x, int64_t k_begin,
+                            int64_t k_end, void *stream, l1dm_handle *out) {
+  g_err.clear();
+  if (!out) return fail(L1DM_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!X) return fail(L1DM_EINVAL, "X is NULL");
+  if (n < 1 || n > (int64_t)0xFFFFFFFFLL)
+    return fail(L1DM_EINVAL, "n=%lld out of range [1, 2^32)", (long long)n);
+  if (k_begin < 0 || k_end <= k_begin || k_end > ld_x)
+    return fail(L1DM_EINVAL, "coordinate range [%lld,%lld) invalid for ld_x=%lld",
+                (long long)k_begin, (long long)k_end, (long long)ld_x);
+  l1dm_ctx *h = new (std::nothrow) l1dm_ctx();
+  if (!h) return fail(L1DM_ENOMEM, "host allocation failed");
+  l1dm_status st = prepare_impl(X, n, ld_x, k_begin, k_end, stream, h);
+  if (st != L1DM_OK) {
+    std::string keep = g_err;
+    destroy(h);
+    g_err = keep;
+    return st;
+  }
+  *out = h;
+  return L1DM_OK;
+}
+
+l1dm_status l1dm_prepare(const float *X, int64_t n, int64_t d, l1dm_handle *out) {
+  if (d < 1) {
+    if (out) *out = nullptr;
+    return fail(L1DM_EINVAL, "d=%lld < 1", (long long)d);
+  }
+  return l1dm_prepare_ex(X, n, d, 0, d, nullptr, out);
+}
+
+l1dm_status l1dm_matvec_ex(l1dm_handle h, const float *Z, int64_t ld_z, int64_t m, double *Y,
+                           int64_t ld_y, void *stream) {
+  g_err.clear();
+  if (!h) return fail(L1DM_EINVAL, "handle is NULL");
+  if (!Z || !Y) return fail(L1DM_EINVAL, "Z or Y is NULL");
+  if (m < 1 || ld_z < m || ld_y < m)
+    return fail(L1DM_EINVAL, "m=%lld ld_z=%lld ld_y=%lld invalid", (long long)m, (long long)ld_z,
+                (long long)ld_y);
+  l1dm_status st = check_device(h);
+  if (st != L1DM_OK) return st;
+  cudaStream_t s = stream ? (cudaStream_t)stream : h->stream;
+  const bool zdev = is_device_pointer(Z), ydev = is_device_pointer(Y);
+  // vector paths need aligned rows; fall back to staging only for host memory
+  if (zdev && ydev) return matvec_device(h, Z, ld_z, m, Y, ld_y, s);
+  // host buffers: stage through library-owned device memory; synchronous
+  const float *Zd = Z;
+  int64_t ldzd = ld_z;
+  if (!zdev) {
+    CUDA_TRY(h->Zstage.ensure((size_t)h->n * (size_t)m, false, s));
+    TimedScope ts(h, kCopy, s);
+    CUDA_TRY(cudaMemcpy2DAsync(h->Zstage.p, (size_t)m * sizeof(float), Z,
+                               (size_t)ld_z * sizeof(float), (size_t)m * sizeof(float),
+                               (size_t)h->n, cudaMemcpyHostToDevice, s));
+    Zd = h->Zstage.p;
+    ldzd = m;
+  }
+  double *Yd = Y;
+  int64_t ldyd = ld_y;
+  if (!ydev) {
+    CUDA_TRY(h->Ystage.ensure((size_t)h->n * (size_t)m, false, s));
+    Yd = h->Ystage.p;
+    ldyd = m;
+  }
+  st = matvec_device(h, Zd, ldzd, m, Yd, ldyd, s);
+  if (st != L1DM_OK) return st;
+  if (!ydev) {
+    TimedScope ts(h, kCopy, s);
+    CUDA_TRY(cudaMemcpy2DAsync(Y, (size_t)ld_y * sizeof(double), Yd, (size_t)m * sizeof(double),
+                               (size_t)m * sizeof(double), (size_t)h->n, cudaMemcpyDeviceToHost,
+                               s));
+  }
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return read_timeout(h);
+}
+
+l1dm_status l1dm_matvec(l1dm_handle h, const float *Z, int64_t m, double *Y) {
+  return l1dm_matvec_ex(h, Z, m, m, Y, m, nullptr);
+}
+
+void l1dm_free(l1dm_handle h) { destroy(h); }
+
+l1dm_status l1dm_sync(l1dm_handle h) {
+  g_err.clear();
+  if (!h) return fail(L1DM_EINVAL, "handle is NULL");
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return read_timeout(h);
+}
+
+l1dm_status l1dm_shape(l1dm_handle h, int64_t *n, int64_t *d_local, int64_t *k_begin,
+                       int64_t *k_end) {
+  if (!h) return fail(L1DM_EINVAL, "handle is NULL");
+  if (n) *n = h->n;
+  if (d_local) *d_local = h->dl;
+  if (k_begin) *k_begin = h->k_begin;
+  if (k_end) *k_end = h->k_end;
+  return L1DM_OK;
+}
+
+size_t l1dm_workspace_bytes(l1dm_handle h, int64_t m) {
+  if (!h || m < 1) return 0;
+  QueryPlan p;
+  int64_t ws = (int64_t)h->ws_limit;
+  if (ws == 0) {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return 0;
+    ws = (int64_t)(0.5 * (double)fr);
+  }
+  if (!make_plan(h->n, h->dl, m, h->l2_bytes, ws, 4, &p)) return 0;
+  return p.workspace_bytes;
+}
+
+l1dm_status l1dm_set_workspace_limit(l1dm_handle h, size_t bytes) {
+  if (!h) return fail(L1DM_EINVAL, "handle is NULL");
+  h->ws_limit = bytes;
+  h->plan_m = -1;
+  return L1DM_OK;
+}
+
+l1dm_status l1dm_plan(int64_t n, int64_t d_local, int64_t m, int64_t l2_bytes,
+                      int64_t workspace_limit, l1dm_plan_t *out) {
+  if (!out) return fail(L1DM_EINVAL, "out is NULL");
+  QueryPlan p;
+  if (!make_plan(n, d_local, m, l2_bytes, workspace_limit, 4, &p))
+    return fail(L1DM_EINVAL, "invalid sizes n=%lld d=%lld m=%lld", (long long)n,
+                (long long)d_local, (long long)m);
+  out->mb = p.mb;
+  out->col_blocks = p.col_blocks;
+  out->vec = p.vec;
+  out->lanes_per_row = p.lpr;
+  out->rows_per_tile = p.rows_per_tile;
+  out->tiles_per_segment = p.tiles_per_segment;
+  out->kc = p.kc;
+  out->chunks = p.chunks;
+  out->l2_resident = p.l2_resident;
+  out->workspace_bytes = (int64_t)p.workspace_bytes;
+  return L1DM_OK;
+}
+
+l1dm_status l1dm_timing_enable(l1dm_handle h, int enable) {
+  if (!h) return fail(L1DM_EINVAL, "handle is NULL");
+  h->timing = enable != 0;
+  return L1DM_OK;
+}
+
+l1dm_status l1dm_timing_read(l1dm_handle h, l1dm_timing_t *out, int reset) {
+  if (!h || !out) return fail(L1DM_EINVAL, "handle or out is NULL");
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  for (auto &tp : h->pending) {
+    float ms = 0.f;
+    cudaEventSynchronize(tp.b);
+    if (cudaEventElapsedTime(&ms, tp.a, tp.b) == cudaSuccess) h->ms[tp.kind] += ms;
+    h->pool.push_back(tp.a);
+    h->pool.push_back(tp.b);
+  }
+  h->pending.clear();
+  out->prep_ms = h->prep_ms;
+  out->colsums_ms = h->ms[kColsums];
+  out->scan_ms = h->ms[kScan];
+  out->accumulate_ms = h->ms[kAcc];
+  out->copy_ms = h->ms[kCopy];
+  out->colsums_launches = h->launches[kColsums];
+  out->scan_launches = h->launches[kScan];
+  out->accumulate_launches = h->launches[kAcc];
+  out->queries = h->queries;
+  out->kernel_launches = h->kernel_launches;
+  if (reset) {
+    for (int k = 0; k < kNumKinds; ++k) {
+      h->ms[k] = 0.0;
+      h->launches[k] = 0;
+    }
+    h->queries = 0;
+    h->kernel_launches = 0;
+  }
+  return L1DM_OK;
+}
+
+l1dm_status l1dm_debug_export(l1dm_handle h, float *sval, uint32_t *perm, uint32_t *rank,
+                              double *hsum) {
+  if (!h) return fail(L1DM_EINVAL, "handle is NULL");
+  l1dm_status st = check_device(h);
+  if (st != L1DM_OK) return st;
+  const size_t row = (size_t)h->n * sizeof(uint32_t);
+  const size_t pitch = (size_t)h->ldn * sizeof(uint32_t);
+  if (sval)
+    CUDA_TRY(cudaMemcpy2DAsync(sval, row, h->sval_bits.p, pitch, row, (size_t)h->dl,
+                               cudaMemcpyDefault, h->stream));
+  if (perm)
+    CUDA_TRY(cudaMemcpy2DAsync(perm, row, h->perm.p, pitch, row, (size_t)h->dl, cudaMemcpyDefault,
+                               h->stream));
+  if (rank)
+    CUDA_TRY(cudaMemcpy2DAsync(rank, row, h->rank.p, pitch, row, (size_t)h->dl, cudaMemcpyDefault,
+                               h->stream));
+  if (hsum)
+    CUDA_TRY(cudaMemcpyAsync(hsum, h->hsum.p, (size_t)h->n * sizeof(double), cudaMemcpyDefault,
+                             h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return L1DM_OK;
+}
+
+const char *l1dm_last_error(void) { return g_err.c_str(); }
+
+const char *l1dm_version(void) { return "l1dm 0.1.0 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,80 @@
+// l1dm_internal.h — host-side declarations shared by the library's translation units.
+// Product code only; never included by oracle/ (and vice versa).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace l1dm {
+
+// Look-back flag states (low 2 bits of an epoch-tagged word).
+constexpr uint32_t kFlagInvalid = 0;
+constexpr uint32_t kFlagAggregate = 1;
+constexpr uint32_t kFlagInclusive = 2;
+
+// Spin bound for every look-back wait: after this many polls the waiter gives up,
+// raises the handle's timeout flag and proceeds (results then invalid, status ETIMEOUT).
+constexpr uint32_t kSpinLimit = 1u << 26;
+
+// ---------------- prepare (Alg. 1) ----------------
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;                          // keys per thread per onesweep tile
+constexpr int kSortTile = kSortThreads * kSortItems;    // 4096 keys
+constexpr int kHistChunk = 16384;                       // keys per histogram CTA
+
+void launch_keys(const float *X, int64_t n, int64_t ldx, int64_t k0, int64_t dl, int64_t ldn,
+                 uint32_t *key, double *hsum, unsigned *nonfinite, cudaStream_t s);
+void launch_hist(const uint32_t *key, int64_t n, int64_t ldn, int64_t dl, uint32_t *hist,
+                 cudaStream_t s);
+// One stable LSD pass over all dl segments.  first: values are implicit point indices.
+// last: writes sval (decoded floats) to kout, perm to vout and rank[k][perm] = r.
+void launch_sort_pass(bool first, bool last, const uint32_t *kin, const uint32_t *vin,
+                      uint32_t *kout, uint32_t *vout, uint32_t *rank, int64_t n, int64_t ldn,
+                      int64_t dl, int shift, const uint32_t *digit_base,
+                      unsigned long long *status, uint32_t epoch, unsigned *ticket,
+                      unsigned *timeout_flag, cudaStream_t s);
+// No pass needed (every digit constant in every segment): identity order.
+void launch_identity_emit(const uint32_t *key, float *sval, uint32_t *perm, uint32_t *rank,
+                          int64_t n, int64_t ldn, int64_t dl, cudaStream_t s);
+
+// ---------------- query (Alg. 2) ----------------
+struct QueryPlan {
+  int vec;            // fp32 Z elements per lane in the scan (1, 2, 4)
+  int lpr;            // lanes per sorted row in the scan
+  int mb;             // columns per scan segment = vec * lpr
+  int col_blocks;     // ceil(m / mb)
+  int items;          // consecutive sorted rows per thread
+  int rows_per_tile;  // 8 warps * (32/lpr) * items
+  int64_t tiles_per_segment;
+  int64_t kc;         // coordinates per chunk
+  int64_t chunks;
+  int l2_resident;
+  int64_t ldu;        // U row length (doubles) = m
+  size_t u_bytes;     // kc * n * ldu * 8
+  size_t lb_slots;    // kc * col_blocks * tiles_per_segment
+  size_t workspace_bytes;
+  // accumulate kernel
+  int v6;             // doubles per lane (1 or 2)
+  int lpp;            // lanes per point
+  int col_groups;     // grid.y of the accumulate kernel
+};
+
+// vec_cap: widest fp32 vector the caller's Z allows (4: 16-B aligned rows, 2: 8-B, 1).
+bool make_plan(int64_t n, int64_t dl, int64_t m, int64_t l2_bytes, int64_t ws_limit,
+               int vec_cap, QueryPlan *p);
+
+constexpr int kColsumBlocks = 592;  // 4 x 148 SMs; fixed so the reduction order is fixed
+
+void launch_colsums(const float *Z, int64_t ldz, int64_t n, int64_t m, const double *hsum,
+                    double *part, double *Sg, unsigned *done_ctr, unsigned *tickets,
+                    int ntickets, cudaStream_t s);
+void launch_scan(const QueryPlan &p, const uint32_t *perm, const float *sval, int64_t ldn,
+                 int64_t n, const float *Z, int64_t ldz, int64_t m, double *U, int64_t k_first,
+                 int64_t kcc, uint32_t *flags, double *agg, double *incl, uint32_t epoch,
+                 unsigned *ticket, unsigned *timeout_flag, cudaStream_t s);
+void launch_accumulate(const QueryPlan &p, const uint32_t *rank, int64_t ldn, int64_t n,
+                       const double *U, int64_t k_first, int64_t kcc, const double *hsum,
+                       const double *Sg, double *Y, int64_t ldy, int64_t m, bool first_chunk,
+                       cudaStream_t s);
+
+}  // namespace l1dm

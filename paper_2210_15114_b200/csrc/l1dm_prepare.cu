@@ -1,0 +1,314 @@
+// l1dm_prepare.cu — Alg. 1 "Preprocessing" on sm_100a.
+//
+// For every coordinate k of the shard: a STABLE ascending sort of x_{.k}
+// producing sval[k][r] (T_k), perm[k][r] (the order pi^k) and
+// rank[k][i] ("position of x_i(k) in the order of T_k").  Layout is
+// coordinate-major with row stride ldn = round_up(n, 32) so every row is
+// 128-byte aligned.
+//
+//   K0 keys      X (row-major) -> key[k][i] orderable u32, h[i] = sum_k x_ik (fp64),
+//                non-finite flag.  Tiled smem transpose, coalesced both sides.
+//   K1 hist      one read of the keys -> all four 8-bit digit histograms per segment.
+//   K2 pass      onesweep LSD pass: warp multisplit ranking (match.any), per-digit
+//                decoupled look-back across tiles (one 64-bit word per digit holds
+//                flag | epoch | count), smem staging so the scatter is run-coalesced.
+//                Passes whose digit is constant in every segment are skipped.
+//                The last pass decodes sval, writes perm and scatters rank (K3 fused).
+//   emit         identity tables when no pass is needed.
+#include <cuda_runtime.h>
+
+#include "l1dm_device.cuh"
+#include "l1dm_internal.h"
+
+namespace l1dm {
+
+// ------------------------------------------------------------------ K0
+constexpr int kT0Points = 64;
+constexpr int kT0Coords = 32;
+
+__global__ void __launch_bounds__(256)
+    k0_keys(const float *__restrict__ X, int64_t n, int64_t ldx, int64_t k0, int64_t dl,
+            int64_t ldn, uint32_t *__restrict__ key, double *__restrict__ hsum,
+            unsigned *__restrict__ nonfinite) {
+  __shared__ float tile[kT0Points][kT0Coords + 1];
+  const int64_t i0 = (int64_t)blockIdx.x * kT0Points;
+  const int tid = threadIdx.x;
+  double hacc = 0.0;
+  int bad = 0;
+  for (int64_t kt = 0; kt < dl; kt += kT0Coords) {
+    for (int e = tid; e < kT0Points * kT0Coords; e += 256) {
+      const int p = e / kT0Coords, c = e % kT0Coords;
+      const int64_t i = i0 + p, k = kt + c;
+      float x = 0.0f;
+      if (i < n && k < dl) {
+        x = X[i * ldx + k0 + k];
+        if (!isfinite(x)) bad = 1;
+      }
+      tile[p][c] = x;
+    }
+    __syncthreads();
+    if (tid < kT0Points) {
+      const int kmax = (int)((dl - kt) < kT0Coords ? (dl - kt) : kT0Coords);
+      for (int c = 0; c < kmax; ++c) hacc += (double)tile[tid][c];  // fixed order k = 0..dl-1
+    }
+    for (int e = tid; e < kT0Points * kT0Coords; e += 256) {
+      const int c = e / kT0Points, p = e % kT0Points;
+      const int64_t i = i0 + p, k = kt + c;
+      if (i < n && k < dl) key[k * ldn + i] = float_to_key(tile[p][c]);
+    }
+    __syncthreads();
+  }
+  if (tid < kT0Points && i0 + tid < n) hsum[i0 + tid] = hacc;
+  if (__syncthreads_or(bad) && tid == 0) atomicOr(nonfinite, 1u);
+}
+
+void launch_keys(const float *X, int64_t n, int64_t ldx, int64_t k0, int64_t dl, int64_t ldn,
+                 uint32_t *key, double *hsum, unsigned *nonfinite, cudaStream_t s) {
+  dim3 grid((unsigned)((n + kT0Points - 1) / kT0Points));
+  k0_keys<<<grid, 256, 0, s>>>(X, n, ldx, k0, dl, ldn, key, hsum, nonfinite);
+}
+
+// ------------------------------------------------------------------ K1
+__global__ void __launch_bounds__(256)
+    k1_hist(const uint32_t *__restrict__ key, int64_t n, int64_t ldn,
+            uint32_t *__restrict__ hist) {
+  __shared__ uint32_t sh[4 * 256];
+  const int tid = threadIdx.x;
+  for (int b = tid; b < 1024; b += 256) sh[b] = 0;
+  __syncthreads();
+  const int64_t seg = blockIdx.y;
+  const uint32_t *kp = key + seg * ldn;
+  const int64_t r0 = (int64_t)blockIdx.x * kHistChunk;
+  const int64_t r1 = (r0 + kHistChunk < n) ? r0 + kHistChunk : n;
+  // r0 is a multiple of 4 and rows are 128-B aligned: vector body, scalar tail.
+  const int64_t body = r0 + ((r1 - r0) & ~(int64_t)3);
+  for (int64_t r = r0 + 4 * tid; r < body; r += 4 * 256) {
+    const uint4 q = *reinterpret_cast<const uint4 *>(kp + r);
+    const uint32_t v[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      atomicAdd(&sh[0 * 256 + (v[u] & 255u)], 1u);
+      atomicAdd(&sh[1 * 256 + ((v[u] >> 8) & 255u)], 1u);
+      atomicAdd(&sh[2 * 256 + ((v[u] >> 16) & 255u)], 1u);
+      atomicAdd(&sh[3 * 256 + (v[u] >> 24)], 1u);
+    }
+  }
+  for (int64_t r = body + tid; r < r1; r += 256) {
+    const uint32_t v = kp[r];
+    atomicAdd(&sh[0 * 256 + (v & 255u)], 1u);
+    atomicAdd(&sh[1 * 256 + ((v >> 8) & 255u)], 1u);
+    atomicAdd(&sh[2 * 256 + ((v >> 16) & 255u)], 1u);
+    atomicAdd(&sh[3 * 256 + (v >> 24)], 1u);
+  }
+  __syncthreads();
+  for (int b = tid; b < 1024; b += 256)
+    if (sh[b]) atomicAdd(&hist[seg * 1024 + b], sh[b]);
+}
+
+void launch_hist(const uint32_t *key, int64_t n, int64_t ldn, int64_t dl, uint32_t *hist,
+                 cudaStream_t s) {
+  dim3 grid((unsigned)((n + kHistChunk - 1) / kHistChunk), (unsigned)dl);
+  k1_hist<<<grid, 256, 0, s>>>(key, n, ldn, hist);
+}
+
+// ------------------------------------------------------------------ K2
+// Status word per (segment, tile, digit): [63:62] flag, [61:32] epoch (30 bits), [31:0] count.
+__device__ __forceinline__ unsigned long long pack_status(uint32_t flag, uint32_t epoch,
+                                                          uint32_t cnt) {
+  return ((unsigned long long)flag << 62) |
+         ((unsigned long long)(epoch & 0x3FFFFFFFu) << 32) | (unsigned long long)cnt;
+}
+
+template <bool FIRST, bool LAST>
+__global__ void __launch_bounds__(kSortThreads)
+    k2_pass(const uint32_t *__restrict__ kin, const uint32_t *__restrict__ vin,
+            uint32_t *__restrict__ kout, uint32_t *__restrict__ vout, uint32_t *__restrict__ rank,
+            int64_t n, int64_t ldn, int64_t tiles_per_seg, int shift,
+            const uint32_t *__restrict__ digit_base, unsigned long long *status, uint32_t epoch,
+            unsigned *ticket, unsigned *timeout_flag) {
+  constexpr int W = kSortThreads / 32;
+  __shared__ uint32_t s_keys[kSortTile];
+  __shared__ uint32_t s_vals[kSortTile];
+  __shared__ uint32_t s_whist[W][256];   // per-warp digit counts, then warp-exclusive offsets
+  __shared__ uint32_t s_tstart[256];     // tile-local start of each digit
+  __shared__ uint64_t s_gbase[256];      // global start of this tile's run of each digit
+  __shared__ uint32_t s_wsum[W];
+  __shared__ unsigned s_ticket;
+
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) s_ticket = atomicAdd(ticket, 1u);
+  for (int b = tid; b < W * 256; b += kSortThreads) (&s_whist[0][0])[b] = 0;
+  __syncthreads();
+  const int64_t t = s_ticket;
+  const int64_t seg = t / tiles_per_seg;
+  const int64_t tile = t - seg * tiles_per_seg;
+  const int64_t base = tile * kSortTile;
+  const int64_t seg_off = seg * ldn;
+  const int64_t tile_valid = (n - base < kSortTile) ? (n - base) : kSortTile;
+
+  // ---- load (warp-striped: warp w owns [w*32*ITEMS, (w+1)*32*ITEMS), item j at +j*32+lane)
+  uint32_t keys[kSortItems];
+  uint32_t vals[kSortItems];
+  uint16_t lrank[kSortItems];
+  const int64_t wbase = base + (int64_t)w * 32 * kSortItems;
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const int64_t idx = wbase + j * 32 + lane;
+    if (idx < n) {
+      keys[j] = kin[seg_off + idx];
+      vals[j] = FIRST ? (uint32_t)idx : vin[seg_off + idx];
+    } else {
+      keys[j] = 0u;
+      vals[j] = 0u;
+    }
+  }
+  // ---- warp multisplit: stable rank of each key among equal digits of its warp
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const int64_t idx = wbase + j * 32 + lane;
+    const bool valid = idx < n;
+    const uint32_t vmask = __ballot_sync(0xFFFFFFFFu, valid);
+    if (valid) {
+      const uint32_t dgt = (keys[j] >> shift) & 255u;
+      const uint32_t peers = __match_any_sync(vmask, dgt);
+      const int leader = __ffs(peers) - 1;
+      uint32_t old = 0;
+      if (lane == leader) {
+        old = s_whist[w][dgt];
+        s_whist[w][dgt] = old + __popc(peers);
+      }
+      old = __shfl_sync(peers, old, leader);
+      lrank[j] = (uint16_t)(old + __popc(peers & lt));
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+
+  // ---- per digit (thread d): warp-exclusive offsets and the tile count
+  const int dgt = tid;  // kSortThreads == 256 digits
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int ww = 0; ww < W; ++ww) {
+    const uint32_t c = s_whist[ww][dgt];
+    s_whist[ww][dgt] = cnt;
+    cnt += c;
+  }
+  // ---- decoupled look-back over earlier tiles of this segment, per digit
+  unsigned long long *st = status + (seg * tiles_per_seg) * 256;
+  uint64_t excl = 0;
+  if (tile == 0) {
+    st_release_u64(&st[dgt], pack_status(kFlagInclusive, epoch, cnt));
+  } else {
+    st_release_u64(&st[tile * 256 + dgt], pack_status(kFlagAggregate, epoch, cnt));
+    int64_t j = tile - 1;
+    uint32_t spins = 0;
+    for (;;) {
+      const unsigned long long sv = ld_acquire_u64(&st[j * 256 + dgt]);
+      const uint32_t f = (uint32_t)(sv >> 62);
+      const uint32_t ep = (uint32_t)(sv >> 32) & 0x3FFFFFFFu;
+      if (ep != (epoch & 0x3FFFFFFFu) || f == kFlagInvalid) {
+        if (++spins > kSpinLimit) {
+          atomicOr(timeout_flag, 1u);
+          break;
+        }
+        if (spins > 64) __nanosleep(64);
+        continue;
+      }
+      excl += (uint32_t)sv;
+      if (f == kFlagInclusive) break;
+      --j;
+    }
+    st_release_u64(&st[tile * 256 + dgt], pack_status(kFlagInclusive, epoch,
+                                                      (uint32_t)(excl + cnt)));
+  }
+  s_gbase[dgt] = (uint64_t)digit_base[seg * 256 + dgt] + excl;
+
+  // ---- block exclusive scan of the tile's digit counts -> s_tstart
+  uint32_t incl_scan = cnt;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl_scan, off);
+    if (lane >= off) incl_scan += y;
+  }
+  if (lane == 31) s_wsum[w] = incl_scan;
+  __syncthreads();
+  uint32_t wpre = 0;
+#pragma unroll
+  for (int ww = 0; ww < W; ++ww)
+    if (ww < w) wpre += s_wsum[ww];
+  s_tstart[dgt] = wpre + incl_scan - cnt;
+  __syncthreads();
+
+  // ---- stage the tile in digit order (stable: warp order, then item, then lane)
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const int64_t idx = wbase + j * 32 + lane;
+    if (idx < n) {
+      const uint32_t d = (keys[j] >> shift) & 255u;
+      const uint32_t lp = s_tstart[d] + s_whist[w][d] + lrank[j];
+      s_keys[lp] = keys[j];
+      s_vals[lp] = vals[j];
+    }
+  }
+  __syncthreads();
+
+  // ---- scatter: consecutive e inside a digit run go to consecutive global slots
+  for (int e = tid; e < tile_valid; e += kSortThreads) {
+    const uint32_t k = s_keys[e];
+    const uint32_t v = s_vals[e];
+    const uint32_t d = (k >> shift) & 255u;
+    const int64_t gpos = (int64_t)(s_gbase[d] + (uint64_t)(e - s_tstart[d]));
+    if (LAST) {
+      kout[seg_off + gpos] = __float_as_uint(key_to_float(k));  // sval
+      vout[seg_off + gpos] = v;                                 // perm
+      rank[seg_off + v] = (uint32_t)gpos;                       // rank = perm^-1 (K3 fused)
+    } else {
+      kout[seg_off + gpos] = k;
+      vout[seg_off + gpos] = v;
+    }
+  }
+}
+
+void launch_sort_pass(bool first, bool last, const uint32_t *kin, const uint32_t *vin,
+                      uint32_t *kout, uint32_t *vout, uint32_t *rank, int64_t n, int64_t ldn,
+                      int64_t dl, int shift, const uint32_t *digit_base,
+                      unsigned long long *status, uint32_t epoch, unsigned *ticket,
+                      unsigned *timeout_flag, cudaStream_t s) {
+  const int64_t tiles = (n + kSortTile - 1) / kSortTile;
+  dim3 grid((unsigned)(tiles * dl));
+#define L1DM_PASS(F, L)                                                                     \
+  k2_pass<F, L><<<grid, kSortThreads, 0, s>>>(kin, vin, kout, vout, rank, n, ldn, tiles, shift, \
+                                              digit_base, status, epoch, ticket, timeout_flag)
+  if (first && last)
+    L1DM_PASS(true, true);
+  else if (first)
+    L1DM_PASS(true, false);
+  else if (last)
+    L1DM_PASS(false, true);
+  else
+    L1DM_PASS(false, false);
+#undef L1DM_PASS
+}
+
+// ------------------------------------------------------------------ identity emit
+__global__ void __launch_bounds__(256)
+    k3_identity(const uint32_t *__restrict__ key, float *__restrict__ sval,
+                uint32_t *__restrict__ perm, uint32_t *__restrict__ rank, int64_t n, int64_t ldn) {
+  const int64_t seg = blockIdx.y;
+  for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (int64_t)gridDim.x * 256) {
+    sval[seg * ldn + i] = key_to_float(key[seg * ldn + i]);
+    perm[seg * ldn + i] = (uint32_t)i;
+    rank[seg * ldn + i] = (uint32_t)i;
+  }
+}
+
+void launch_identity_emit(const uint32_t *key, float *sval, uint32_t *perm, uint32_t *rank,
+                          int64_t n, int64_t ldn, int64_t dl, cudaStream_t s) {
+  int64_t bx = (n + 255) / 256;
+  if (bx > 4096) bx = 4096;
+  dim3 grid((unsigned)bx, (unsigned)dl);
+  k3_identity<<<grid, 256, 0, s>>>(key, sval, perm, rank, n, ldn);
+}
+
+}  // namespace l1dm

@@ -1,0 +1,169 @@
+"""Query parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar (BASELINE.json north_star): max over columns of the relative l2 error <= 1e-9 for float
+data; bit-exact for integer data (every partial sum is an integer < 2^53)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2210_15114_b200 as l1
+from conftest import GOLDEN, col_rel_l2, load_golden
+from gpu_util import gpu_matvec
+from paper_2210_15114_b200 import workloads as wl
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+@pytest.mark.parametrize("name", GOLDEN)
+def test_golden(name):
+    X, Z, Y = load_golden(name)
+    assert np.array_equal(gpu_matvec(X, Z), Y)
+    assert np.array_equal(gpu_matvec(X, Z, host=True), Y)
+
+
+# m values exercise every lane mapping (vec 1/2/4, lanes per row 1..32, >1 column block);
+# n values span several scan tiles (2048 rows at m=1 ... 64 rows at m=31) plus ragged tails.
+CASES = [(1, 1, 1), (2, 1, 3), (3, 2, 2), (100, 3, 1), (2049, 2, 1), (4097, 3, 2), (5000, 4, 3),
+         (1000, 5, 4), (3001, 3, 5), (700, 2, 8), (1029, 3, 16), (333, 2, 31), (777, 2, 32),
+         (1100, 3, 64), (200, 2, 65), (513, 2, 128), (257, 3, 6), (6000, 1, 12)]
+
+
+@pytest.mark.parametrize("n,d,m", CASES)
+def test_random_float_vs_brute(n, d, m):
+    rng = np.random.default_rng(n * 1000 + d * 10 + m)
+    X = rng.standard_normal((n, d)).astype(np.float32)
+    Z = rng.standard_normal((n, m)).astype(np.float32)
+    Yg = gpu_matvec(X, Z)
+    Yr = oracle.brute(X, Z)
+    assert col_rel_l2(Yg, Yr) <= TOL
+
+
+@pytest.mark.parametrize("n,d,m", [(4099, 3, 1), (3000, 4, 4), (2500, 2, 7), (1500, 3, 32)])
+def test_integer_ties_exact(n, d, m):
+    rng = np.random.default_rng(7 * n + m)
+    X = rng.integers(0, 5, size=(n, d)).astype(np.float32)
+    Z = rng.integers(-3, 4, size=(n, m)).astype(np.float32)
+    Yg = gpu_matvec(X, Z)
+    assert np.array_equal(Yg, oracle.hist(X, Z, M=4).astype(np.float64))
+
+
+def test_degenerate_cases():
+    rng = np.random.default_rng(1)
+    X = rng.standard_normal((300, 3)).astype(np.float32)
+    Z = rng.standard_normal((300, 2)).astype(np.float32)
+    assert np.all(gpu_matvec(X, np.zeros_like(Z)) == 0)                       # z = 0
+    # equal points: A = 0; the fp64 U-form cancels to rounding level (abs floor 1e-12 n)
+    Ye = gpu_matvec(np.tile(X[:1], (300, 1)), Z)
+    assert col_rel_l2(Ye, np.zeros_like(Ye)) <= 1e-9
+    assert np.all(gpu_matvec(X[:1], Z[:1]) == 0)                              # n = 1
+    E = np.eye(300, dtype=np.float32)[:, :64]
+    A = gpu_matvec(X, E)
+    assert np.all(np.abs(A[np.arange(64), np.arange(64)]) <= 1e-12 * np.abs(A).max())
+    D = np.abs(X[:, None, :].astype(np.float64) - X[None, :64, :].astype(np.float64)).sum(-1)
+    assert np.allclose(A, D, rtol=1e-12, atol=1e-12)                          # A e_j = column j
+
+
+def test_symmetry_linearity_on_gpu():
+    rng = np.random.default_rng(5)
+    X = rng.standard_normal((20000, 6)).astype(np.float32)
+    Z = rng.standard_normal((20000, 2)).astype(np.float32)
+    Y = gpu_matvec(X, Z)
+    a = float(Z[:, 0].astype(np.float64) @ Y[:, 1])
+    b = float(Z[:, 1].astype(np.float64) @ Y[:, 0])
+    assert abs(a - b) <= 1e-12 * max(abs(a), abs(b))
+
+
+def test_strided_query_and_host_pointers():
+    rng = np.random.default_rng(11)
+    X = rng.standard_normal((3000, 4)).astype(np.float32)
+    Zw = torch.from_numpy(rng.standard_normal((3000, 9)).astype(np.float32))
+    Z = Zw[:, 1:6]                      # ld_z = 9 > m = 5, misaligned base
+    Yr = oracle.brute(X, Z.contiguous().numpy())
+    h = l1.l1dm_prepare(torch.from_numpy(X).cuda())
+    Yg = l1.l1dm_matvec(h, Zw.cuda()[:, 1:6])
+    torch.cuda.synchronize()
+    assert col_rel_l2(Yg.cpu().numpy(), Yr) <= TOL
+    Yh = l1.l1dm_matvec(h, Z.contiguous().numpy())       # host in, host out
+    assert col_rel_l2(Yh.numpy(), Yr) <= TOL
+    l1.l1dm_free(h)
+
+
+@pytest.mark.parametrize("m", [1, 4, 32])
+def test_chunked_workspace_matches(m):
+    rng = np.random.default_rng(m)
+    X = rng.standard_normal((5000, 7)).astype(np.float32)
+    Z = rng.standard_normal((5000, m)).astype(np.float32)
+    Yr = oracle.brute(X, Z)
+    Y1 = gpu_matvec(X, Z, ws_limit=1)     # one coordinate per chunk: Y read-modify-write path
+    assert col_rel_l2(Y1, Yr) <= TOL
+
+
+def test_coordinate_shards_sum_to_whole():
+    rng = np.random.default_rng(15)
+    X = rng.integers(0, 9, size=(4000, 7)).astype(np.float32)
+    Z = rng.integers(-2, 3, size=(4000, 3)).astype(np.float32)
+    parts = [gpu_matvec(X, Z, a, b) for a, b in [(0, 2), (2, 3), (3, 7)]]
+    whole = oracle.hist(X, Z, M=8).astype(np.float64)
+    assert np.array_equal(sum(parts), whole)
+    assert np.array_equal(parts[1], oracle.hist(X[:, 2:3], Z, M=8).astype(np.float64))
+
+
+def test_repeated_queries_same_handle():
+    rng = np.random.default_rng(21)
+    X = rng.standard_normal((9000, 5)).astype(np.float32)
+    h = l1.l1dm_prepare(torch.from_numpy(X).cuda())
+    for m in (1, 8, 3, 8, 1):
+        Z = rng.standard_normal((9000, m)).astype(np.float32)
+        Y = l1.l1dm_matvec(h, torch.from_numpy(Z).cuda())
+        torch.cuda.synchronize()
+        assert col_rel_l2(Y.cpu().numpy(), oracle.brute(X, Z)) <= TOL
+    l1.l1dm_sync(h)
+    l1.l1dm_free(h)
+
+
+# ---- the five BASELINE.json workloads, value structure at reduced n, vs the oracle ----
+@pytest.mark.parametrize("name,n", [("c1", 2048), ("c2", 30000), ("c3", 6000), ("c4", 20000),
+                                    ("c5", 40000)])
+def test_workload_reduced(name, n):
+    w = wl.workload(name, n=n)
+    X = wl.make_points(w, "cuda")
+    Z = wl.make_query(w, 0, "cuda")
+    Yg = gpu_matvec(X, Z)
+    Xh, Zh = X.cpu().numpy(), Z.cpu().numpy()
+    if name == "c5":
+        assert np.array_equal(Yg, oracle.hist(Xh, Zh, M=255).astype(np.float64))
+    elif name == "c1":
+        assert col_rel_l2(Yg, oracle.brute(Xh, Zh)) <= TOL
+    else:
+        assert col_rel_l2(Yg, oracle.sort_based(Xh, Zh)) <= TOL
+
+
+def sample_rows(n, Y=None, count=24, seed=0):
+    rng = np.random.default_rng(seed)
+    r = set(rng.integers(0, n, size=count).tolist()) | {0, n - 1}
+    return np.array(sorted(r), dtype=np.int64)
+
+
+# ---- full BASELINE.json sizes, in the bench's launch configuration, on sampled rows ----
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_workload_full_size_sampled(name):
+    w = wl.workload(name)
+    X = wl.make_points(w, "cuda")
+    Z = wl.make_query(w, 0, "cuda")
+    h = l1.l1dm_prepare(X)
+    Y = l1.l1dm_matvec(h, Z)
+    torch.cuda.synchronize()
+    l1.l1dm_sync(h)
+    rows = sample_rows(w.n, count=16 if w.n > (1 << 22) else 32)
+    Yg = Y[torch.from_numpy(rows).cuda()].cpu().numpy()
+    Xh, Zh = X.cpu().numpy(), Z.cpu().numpy()
+    del Y
+    l1.l1dm_free(h)
+    Yr = oracle.rows(Xh, Zh, rows)
+    if name == "c5":
+        assert np.array_equal(Yg, Yr)        # integers < 2^53: exact on both sides
+    else:
+        assert col_rel_l2(Yg, Yr) <= TOL
