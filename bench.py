@@ -1,0 +1,333 @@
+#!/usr/bin/env python
+"""Benchmark: l1 distance-matrix block product Y = A·Z on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3] [--impl ours|reference]
+
+One STEP is one pass of the whole hot path over the
+workload: prepare (Alg. 1: keys, radix sort, ranks) once, then the workload's
+queries (Alg. 2: colsums, gather+scan, rank-gather accumulate; + the NCCL sum of
+the partial Y when N > 1).  Default workload c3 (n=2^20, d=128, m=64, prepare once,
+100 queries on one fixed Pi; DESIGN.md §7 says why c3).  value = n·d·m·queries /
+step time, whole job.  Inputs (1.5 GB prepared state, 256 MB Z) are larger than L2,
+so no flush is needed between steps.
+
+Rank 0 prints ONE JSON line.  --impl reference times the CPU oracle (oracle/, Alg. 1
++ Alg. 2 as written, long double) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--queries", type=int, default=None, help="queries per step (default: recipe)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--reduce", default="reduce", choices=["reduce", "allreduce"])
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- utils
+def load_peaks():
+    try:
+        with open(PEAKS_FILE) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for r in self.rows for j in range(4) if r[2 + j] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def model_b_bytes(n, d, m):
+    """SURVEY §8(d) Model B algorithmic bytes per query: n d (12 + 20 m) + n (12 m + 8)."""
+    return n * d * (12 + 20 * m) + n * (12 * m + 8)
+
+
+# --------------------------------------------------------------------------- reference arm
+def cpu_oracle_sample(w, queries, budget_dims=None):
+    """Time the oracle (as it stands) on a bounded sample: full n, d' coordinates, m' columns."""
+    import oracle
+    from paper_2210_15114_b200 import workloads as wl
+    cores = oracle.num_threads(0)
+    n = w.n
+    d_s = min(w.d, budget_dims[0] if budget_dims else 32)
+    m_s = min(w.m, budget_dims[1] if budget_dims else max(1, min(w.m, cores)))
+    ws = wl.workload(w.name, n=n, d=w.d, m=w.m)
+    X = wl.make_points(ws, "cpu")[:, :d_s].contiguous().numpy()
+    Z = wl.make_query(ws, 0, "cpu")[:, :m_s].contiguous().numpy()
+    t0 = time.perf_counter()
+    _, order = oracle.alg1(X)
+    t_prep = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    oracle.alg2(X, order, Z)
+    t_q = time.perf_counter() - t0
+    upd = n * d_s * m_s
+    value = upd * queries / (t_prep + queries * t_q)
+    return {"value": value, "unit": "updates/s", "cores": cores, "kind": "oracle",
+            "sample": (f"n={n} (full), d'={d_s} of {w.d} coords, m'={m_s} of {w.m} cols; Alg.1 "
+                       f"{t_prep:.2f}s + Alg.2 {t_q:.2f}s per query, step = prep + {queries} "
+                       f"queries (query time x{queries})"),
+            "prep_s": t_prep, "query_s": t_q}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from paper_2210_15114_b200 import workloads as wl
+    w = wl.workload(args.workload)
+    Q = args.queries or w.queries
+    vals = []
+    info = None
+    for i in range(args.warmup + args.steps):
+        info = cpu_oracle_sample(w, Q, budget_dims=(16, 16))
+        if i >= args.warmup:
+            vals.append(info["value"])
+    value = statistics.mean(vals)
+    ms = w.n * w.d * w.m * Q / value * 1e3
+    line = {
+        "impl": "reference", "metric": "l1 matvec throughput (n*d*m updates/s)", "value": value,
+        "unit": "updates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64 (long double accumulation) over f32 inputs", "data": "synthetic",
+        "config": {"workload": args.workload, "n": w.n, "d": w.d, "m": w.m, "queries": Q},
+        "cpu_baseline": {k: info[k] for k in ("kind", "cores", "sample")} | {"value": value,
+                                                                          "unit": "updates/s"},
+        "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# --------------------------------------------------------------------------- our arm
+def main_ours(args):
+    import torch.distributed as dist
+
+    import paper_2210_15114_b200 as l1
+    from paper_2210_15114_b200 import workloads as wl
+    from paper_2210_15114_b200.distributed import ShardedL1DM, shard_range
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    w = wl.workload(args.workload)
+    Q = args.queries or w.queries
+    n, d, m = w.n, w.d, w.m
+    stream = torch.cuda.current_stream(dev)
+
+    # inputs resident in HBM before timing: full X regenerated per rank from the seed
+    Xfull = wl.make_points(w, dev)
+    k0, k1 = shard_range(d, rank, world)
+    X = Xfull[:, k0:k1].contiguous() if world > 1 else Xfull
+    del Xfull
+    torch.cuda.empty_cache()
+    if w.fresh_queries:
+        Zs = [wl.make_query(w, t, dev) for t in range(Q)]
+    else:
+        Zs = [wl.make_query(w, 0, dev)]
+    Y = torch.empty((n, m), dtype=torch.float64, device=dev)
+    kr = (0, k1 - k0)
+
+    def one_step(timing=False):
+        sh = ShardedL1DM(X, k_range=kr, stream=stream)
+        sh.world = world
+        if timing and sh.handle is not None:
+            l1.l1dm_timing_enable(sh.handle, True)
+        for q in range(Q):
+            sh.matvec(Zs[q % len(Zs)], Y, root=None if args.reduce == "allreduce" else 0)
+        return sh
+
+    for _ in range(args.warmup):
+        sh = one_step()
+        torch.cuda.synchronize()
+        sh.close()
+    clocks = ClockSampler(local)
+    if rank == 0:
+        clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    timings = []
+    ev0.record(stream)
+    for s in range(args.steps):
+        sh = one_step(timing=True)
+        if sh.handle is not None:
+            timings.append(l1.l1dm_timing_read(sh.handle))  # syncs the stream (host only)
+        sh.close()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop() if rank == 0 else None
+    ms_total = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / args.steps
+    upd_step = n * d * m * Q
+    value = upd_step / (ms_step * 1e-3)
+
+    # per-kernel device times (events on the library stream), this rank
+    agg = {k: sum(tt[k] for tt in timings) for k in timings[0]} if timings else {}
+    prep_ms = statistics.mean(tt["prep_ms"] for tt in timings) if timings else None
+    scan_launch_ms = agg["scan_ms"] / max(agg["scan_launches"], 1) if agg else None
+    acc_launch_ms = agg["accumulate_ms"] / max(agg["accumulate_launches"], 1) if agg else None
+    query_kernel_ms = ((agg["colsums_ms"] + agg["scan_ms"] + agg["accumulate_ms"]) /
+                       max(agg["queries"], 1)) if agg else None
+    hbm_peak, peak_kind = load_peaks()
+    dl = k1 - k0
+    plan = l1.l1dm_plan(n, dl, m) if dl > 0 else None
+    kc = plan["kc"] if plan else dl
+    # algorithmic bytes per launch (SURVEY §8(d) Model B split by kernel)
+    scan_bytes = n * kc * (8 + 12 * m)
+    acc_bytes = n * kc * (4 + 8 * m) + n * (8 * m + 8)
+    scan_ach = scan_bytes / (scan_launch_ms * 1e-3) / 1e9 if scan_launch_ms else None
+    acc_ach = acc_bytes / (acc_launch_ms * 1e-3) / 1e9 if acc_launch_ms else None
+    dominant = "scan" if (agg.get("scan_ms", 0) >= agg.get("accumulate_ms", 0)) else "accumulate"
+    ach = scan_ach if dominant == "scan" else acc_ach
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.workload}.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(dominant)
+        except Exception:
+            traffic = None
+    qb = model_b_bytes(n, dl, m)
+    result = {
+        "metric": "l1 matvec throughput (n*d*m updates/s; HBM GB/s vs peak in roofline)",
+        "value": value, "unit": "updates/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64 accumulation over f32 inputs", "data": "synthetic",
+        "config": {"workload": args.workload, "n": n, "d": d, "m": m, "queries_per_step": Q,
+                   "fresh_queries": w.fresh_queries, "parallelism": f"coord-shard x{world}",
+                   "collective": (args.reduce if world > 1 else None),
+                   "l2": "inputs > L2 (prepared state 12*n*d B), no flush"},
+        "gpu_launches": int(agg.get("kernel_launches", 0)),
+        "prepare_ms": prep_ms,
+        "query_ms": (ms_step - (prep_ms or 0.0)) / Q,
+        "query_kernel_ms": query_kernel_ms,
+        "kernel_ms_per_launch": {"scan": scan_launch_ms, "accumulate": acc_launch_ms,
+                                 "colsums": agg["colsums_ms"] / max(agg["colsums_launches"], 1)
+                                 if agg else None},
+        "model_b_GBps_per_query": qb / (query_kernel_ms * 1e-3) / 1e9 if query_kernel_ms else None,
+        "roofline": {"bound": "hbm", "kernel": dominant, "achieved": ach, "peak": hbm_peak,
+                     "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": (ach / hbm_peak) if ach else None, "traffic": traffic,
+                     "frac_of_8TBps": (ach / 8000.0) if ach else None},
+        "clocks": clk,
+    }
+    # ---- e2e through the public API with HOST buffers (pinned), N=1 only
+    if world == 1 and not args.no_e2e:
+        Xh = X.cpu().pin_memory()
+        Zh = [z.cpu().pin_memory() for z in Zs]
+        Yh = torch.empty((n, m), dtype=torch.float64).pin_memory()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        h = l1.l1dm_prepare(Xh)
+        for q in range(Q):
+            l1.l1dm_matvec(h, Zh[q % len(Zh)], Yh)
+        l1.l1dm_free(h)
+        e2e_s = time.perf_counter() - t0
+        result["e2e"] = {"value": upd_step / e2e_s, "unit": "updates/s",
+                         "h2d_bytes_per_step": int(Xh.numel() * 4 + Q * n * m * 4),
+                         "d2h_bytes_per_step": int(Q * n * m * 8),
+                         "note": "l1dm_prepare(host X) + per query l1dm_matvec(host Z, host Y)"}
+        del Xh, Zh, Yh
+    # ---- CPU baseline: the oracle on the host cores, bounded sample, rank 0 at N=1
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cb = cpu_oracle_sample(w, Q, budget_dims=(16, 16))
+            result["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind",
+                                                         "sample")}
+        except Exception as e:  # the baseline is reported, never required
+            result["cpu_baseline"] = {"value": None, "error": str(e)}
+    if rank == 0:
+        print(json.dumps(result))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    a = parse()
+    sys.exit(run_reference(a) if a.impl == "reference" else main_ours(a))

@@ -77,8 +77,9 @@ L1DM_API l1dm_status l1dm_prepare(const float *X, int64_t n, int64_t d, l1dm_han
  *   Y_g = sum_{k in [k_begin,k_end)} A^(k) Z,  A^(k)_ij = |x_ik - x_jk|,
  * including the shard's own share of the epilogue, so that the sum of Y_g over
  * a partition of [0, d) is A·Z exactly up to rounding (swap of sums).
- * `stream` (a cudaStream_t, may be NULL for a library-created stream) is used for
- * the prepare work and becomes the handle's default stream.  Synchronous. */
+ * `stream` (a cudaStream_t; NULL = the legacy default stream, CUDA's convention) is
+ * used for the prepare work and becomes the handle's stream (used by l1dm_matvec,
+ * l1dm_sync, l1dm_free).  Synchronous. */
 L1DM_API l1dm_status l1dm_prepare_ex(const float *X, int64_t n, int64_t ld_x, int64_t k_begin,
                             int64_t k_end, void *stream, l1dm_handle *out);
 
@@ -90,14 +91,15 @@ L1DM_API l1dm_status l1dm_prepare_ex(const float *X, int64_t n, int64_t ld_x, in
  * P, Q the exclusive prefix sums of z and x·z in sorted order, S = 1^T Z,
  * g = h^T Z; fp64 accumulation of the fp32 inputs.
  * Z: n x m fp32 (ld_z = m); Y: n x m fp64 (ld_y = m), OVERWRITTEN.
- * Device Z/Y: stream-ordered on the handle's stream; Z and Y must stay valid
+ * Device Z/Y: stream-ordered on the handle's (prepare) stream; Z and Y must stay valid
  * until the stream reaches the end of the call.  Host Z/Y: synchronous.
  * NaN/Inf in Z are not checked; they propagate into Y by IEEE rules.
  * Errors: EINVAL (null, m < 1), EDEVICE, ENOMEM (workspace), ECUDA. */
 L1DM_API l1dm_status l1dm_matvec(l1dm_handle h, const float *Z, int64_t m, double *Y);
 
 /* As l1dm_matvec with explicit leading dimensions (ld_z >= m, ld_y >= m) and
- * stream (NULL = the handle's stream). */
+ * stream (NULL = the legacy default stream, CUDA's convention).  The work is
+ * ordered on that stream only: Z must be ready on it, Y is ready when it is. */
 L1DM_API l1dm_status l1dm_matvec_ex(l1dm_handle h, const float *Z, int64_t ld_z, int64_t m, double *Y,
                            int64_t ld_y, void *stream);
 

@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libl1dm.so")
+LIB_PATH = os.environ.get("L1DM_LIB") or os.path.join(_PKG, "lib", "libl1dm.so")
 
 STATUS = {
     0: "L1DM_OK", -1: "L1DM_EINVAL", -2: "L1DM_ENONFINITE", -3: "L1DM_ENOMEM",

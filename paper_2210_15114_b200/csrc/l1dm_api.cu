@@ -92,7 +92,8 @@ struct l1dm_ctx {
   int device = -1;
   int64_t n = 0, dl = 0, k_begin = 0, k_end = 0, ldn = 0;
   int64_t l2_bytes = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;       // prepare stream; default for l1dm_matvec
+  cudaStream_t last_stream = nullptr;  // stream of the latest l1dm_matvec_ex
   bool own_stream = false;
   // prepared state (Alg. 1)
   DevBuf<uint32_t> sval_bits;  // fp32 bits
@@ -190,7 +191,8 @@ l1dm_status check_arch(int *dev_out) {
 
 void destroy(l1dm_ctx *h) {
   if (!h) return;
-  if (h->stream) cudaStreamSynchronize(h->stream);
+  cudaStreamSynchronize(h->stream);
+  if (h->last_stream != h->stream) cudaStreamSynchronize(h->last_stream);
   for (auto &p : h->pending) {
     cudaEventDestroy(p.a);
     cudaEventDestroy(p.b);
@@ -228,13 +230,10 @@ l1dm_status prepare_impl(const float *X, int64_t n, int64_t ld_x, int64_t k_begi
   int l2 = 0;
   CUDA_TRY(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
   h->l2_bytes = l2;
-  if (stream) {
-    h->stream = (cudaStream_t)stream;
-    h->own_stream = false;
-  } else {
-    CUDA_TRY(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
-    h->own_stream = true;
-  }
+  // CUDA convention: a NULL stream is the legacy default stream (implicitly ordered
+  // with every blocking stream, e.g. torch's default stream).
+  h->stream = (cudaStream_t)stream;
+  h->own_stream = false;
   cudaStream_t s = h->stream;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   CUDA_TRY(cudaEventCreate(&ev0));
@@ -512,7 +511,8 @@ l1dm_status l1dm_matvec_ex(l1dm_handle h, const float *Z, int64_t ld_z, int64_t 
                 (long long)ld_y);
   l1dm_status st = check_device(h);
   if (st != L1DM_OK) return st;
-  cudaStream_t s = stream ? (cudaStream_t)stream : h->stream;
+  cudaStream_t s = (cudaStream_t)stream;  // NULL: legacy default stream
+  h->last_stream = s;
   const bool zdev = is_device_pointer(Z), ydev = is_device_pointer(Y);
   // vector paths need aligned rows; fall back to staging only for host memory
   if (zdev && ydev) return matvec_device(h, Z, ld_z, m, Y, ld_y, s);
@@ -548,7 +548,8 @@ l1dm_status l1dm_matvec_ex(l1dm_handle h, const float *Z, int64_t ld_z, int64_t 
 }
 
 l1dm_status l1dm_matvec(l1dm_handle h, const float *Z, int64_t m, double *Y) {
-  return l1dm_matvec_ex(h, Z, m, m, Y, m, nullptr);
+  if (!h) return fail(L1DM_EINVAL, "handle is NULL");
+  return l1dm_matvec_ex(h, Z, m, m, Y, m, (void *)h->stream);
 }
 
 void l1dm_free(l1dm_handle h) { destroy(h); }
@@ -557,6 +558,7 @@ l1dm_status l1dm_sync(l1dm_handle h) {
   g_err.clear();
   if (!h) return fail(L1DM_EINVAL, "handle is NULL");
   CUDA_TRY(cudaStreamSynchronize(h->stream));
+  if (h->last_stream != h->stream) CUDA_TRY(cudaStreamSynchronize(h->last_stream));
   return read_timeout(h);
 }
 
@@ -619,6 +621,7 @@ l1dm_status l1dm_timing_enable(l1dm_handle h, int enable) {
 l1dm_status l1dm_timing_read(l1dm_handle h, l1dm_timing_t *out, int reset) {
   if (!h || !out) return fail(L1DM_EINVAL, "handle or out is NULL");
   CUDA_TRY(cudaStreamSynchronize(h->stream));
+  if (h->last_stream != h->stream) CUDA_TRY(cudaStreamSynchronize(h->last_stream));
   for (auto &tp : h->pending) {
     float ms = 0.f;
     cudaEventSynchronize(tp.b);

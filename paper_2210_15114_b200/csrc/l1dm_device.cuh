@@ -44,18 +44,39 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 }
 
 // ---- streaming loads/stores with cache hints ----
-// Read-once streams (sorted tables): evict-first in L2, no L1 allocation.
+// Read-once streams (sorted tables): no L1 allocation.
 __device__ __forceinline__ uint4 ld_stream_u4(const void *p) {
   uint4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.u32 {%0,%1,%2,%3}, [%4];"
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                : "l"(p));
   return v;
 }
 __device__ __forceinline__ uint32_t ld_stream_u32(const void *p) {
   uint32_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
+
+}  // namespace l1dm
+
+namespace l1dm {
+
+// ---- cp.async (LDGSTS): BYTES in {4, 8, 16}; src_size 0 zero-fills the destination ----
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void *smem, const void *gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int src_size = valid ? BYTES : 0;
+  if constexpr (BYTES == 16) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(src_size)
+                 : "memory");
+  } else {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(s), "l"(gmem), "n"(BYTES),
+                 "r"(src_size)
+                 : "memory");
+  }
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 }  // namespace l1dm

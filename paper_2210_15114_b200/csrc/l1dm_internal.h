@@ -38,10 +38,19 @@ void launch_identity_emit(const uint32_t *key, float *sval, uint32_t *perm, uint
                           int64_t n, int64_t ldn, int64_t dl, cudaStream_t s);
 
 // ---------------- query (Alg. 2) ----------------
+// Rows per thread in a scan tile (8 warps, VC columns per lane): the tile stages about
+// 96 KB of perm/sval/Z in shared memory, so two CTAs fit per SM.
+__host__ __device__ constexpr int scan_items(int lpr, int vc) {
+  return (98304 / (1024 * vc + 2048 / lpr)) / 4 * 4 > 64 ? 64
+                                                          : (98304 / (1024 * vc + 2048 / lpr)) / 4 * 4;
+}
+// Independent (coordinate, column block) scan segments the planner aims for per chunk.
+constexpr int64_t kScanTargetSegments = 0;
 struct QueryPlan {
-  int vec;            // fp32 Z elements per lane in the scan (1, 2, 4)
-  int lpr;            // lanes per sorted row in the scan
-  int mb;             // columns per scan segment = vec * lpr
+  int vec;            // fp32 Z elements per cp.async gather chunk (1, 2, 4)
+  int lpr;            // lanes per sorted row in the scan = columns per segment
+  int vc;             // columns per lane (1, or 2 when 32 < m <= 64)
+  int mb;             // columns per scan segment (= lpr * vc)
   int col_blocks;     // ceil(m / mb)
   int items;          // consecutive sorted rows per thread
   int rows_per_tile;  // 8 warps * (32/lpr) * items

@@ -123,7 +123,7 @@ template <bool FIRST, bool LAST>
 __global__ void __launch_bounds__(kSortThreads)
     k2_pass(const uint32_t *__restrict__ kin, const uint32_t *__restrict__ vin,
             uint32_t *__restrict__ kout, uint32_t *__restrict__ vout, uint32_t *__restrict__ rank,
-            int64_t n, int64_t ldn, int64_t tiles_per_seg, int shift,
+            int64_t n, int64_t ldn, int64_t nseg, int64_t tiles_per_seg, int shift,
             const uint32_t *__restrict__ digit_base, unsigned long long *status, uint32_t epoch,
             unsigned *ticket, unsigned *timeout_flag) {
   constexpr int W = kSortThreads / 32;
@@ -139,9 +139,10 @@ __global__ void __launch_bounds__(kSortThreads)
   if (tid == 0) s_ticket = atomicAdd(ticket, 1u);
   for (int b = tid; b < W * 256; b += kSortThreads) (&s_whist[0][0])[b] = 0;
   __syncthreads();
+  // tickets interleave segments (seg fastest): a tile's predecessor is nseg tickets older
   const int64_t t = s_ticket;
-  const int64_t seg = t / tiles_per_seg;
-  const int64_t tile = t - seg * tiles_per_seg;
+  const int64_t tile = t / nseg;
+  const int64_t seg = t - tile * nseg;
   const int64_t base = tile * kSortTile;
   const int64_t seg_off = seg * ldn;
   const int64_t tile_valid = (n - base < kSortTile) ? (n - base) : kSortTile;
@@ -278,7 +279,7 @@ void launch_sort_pass(bool first, bool last, const uint32_t *kin, const uint32_t
   const int64_t tiles = (n + kSortTile - 1) / kSortTile;
   dim3 grid((unsigned)(tiles * dl));
 #define L1DM_PASS(F, L)                                                                     \
-  k2_pass<F, L><<<grid, kSortThreads, 0, s>>>(kin, vin, kout, vout, rank, n, ldn, tiles, shift, \
+  k2_pass<F, L><<<grid, kSortThreads, 0, s>>>(kin, vin, kout, vout, rank, n, ldn, dl, tiles, shift, \
                                               digit_base, status, epoch, ticket, timeout_flag)
   if (first && last)
     L1DM_PASS(true, true);

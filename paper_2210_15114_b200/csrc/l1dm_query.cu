@@ -17,6 +17,8 @@
 //                  and accumulate in registers (no atomics); epilogue writes Y.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "l1dm_device.cuh"
 #include "l1dm_internal.h"
 
@@ -29,19 +31,11 @@ static int pow2ceil(int64_t x) {
   return p;
 }
 
-bool make_plan(int64_t n, int64_t dl, int64_t m, int64_t l2_bytes, int64_t ws_limit,
-               int vec_cap, QueryPlan *p) {
-  if (n < 1 || dl < 1 || m < 1 || !p) return false;
-  QueryPlan q{};
-  q.vec = (m % 4 == 0) ? 4 : (m % 2 == 0) ? 2 : 1;
-  if (q.vec > vec_cap) q.vec = vec_cap >= 2 && m % 2 == 0 ? 2 : 1;
-  const int lpr_cap = (q.vec == 4) ? 16 : (q.vec == 2) ? 16 : 32;
-  int64_t need = (m + q.vec - 1) / q.vec;
-  q.lpr = pow2ceil(need);
-  if (q.lpr > lpr_cap) q.lpr = lpr_cap;
-  q.mb = q.vec * q.lpr;
+static void plan_sizes(QueryPlan &q, int64_t n, int64_t dl, int64_t m, int64_t l2_bytes,
+                       int64_t ws_limit) {
+  q.mb = q.lpr * q.vc;
   q.col_blocks = (int)((m + q.mb - 1) / q.mb);
-  q.items = 8;
+  q.items = scan_items(q.lpr, q.vc);
   q.rows_per_tile = 8 * (32 / q.lpr) * q.items;
   q.tiles_per_segment = (n + q.rows_per_tile - 1) / q.rows_per_tile;
   q.ldu = m;
@@ -64,6 +58,36 @@ bool make_plan(int64_t n, int64_t dl, int64_t m, int64_t l2_bytes, int64_t ws_li
   q.lb_slots = (size_t)q.kc * slots_per_coord;
   q.workspace_bytes = (size_t)q.kc * per_coord + (size_t)kColsumBlocks * 2 * m * sizeof(double) +
                       2 * m * sizeof(double);
+}
+
+bool make_plan(int64_t n, int64_t dl, int64_t m, int64_t l2_bytes, int64_t ws_limit,
+               int vec_cap, QueryPlan *p) {
+  if (n < 1 || dl < 1 || m < 1 || !p) return false;
+  QueryPlan q{};
+  // Columns per scan segment: the whole Z row when it fits one warp (two columns per lane
+  // for 32 < m <= 64) — random row gathers from DRAM are only efficient when wide
+  // (measured on B200: 64 B rows ~2.6 TB/s, 128 B ~4.5, 256 B ~5.5 of useful bandwidth).
+  q.vc = (m > 32 && m % 2 == 0) ? 2 : 1;
+  q.lpr = pow2ceil((m + q.vc - 1) / q.vc > 32 ? 32 : (m + q.vc - 1) / q.vc);
+  // gather chunk (floats per cp.async): 16 B when rows/columns allow it
+  auto pick_vec = [&](int mb) {
+    int v = (m % 4 == 0) ? 4 : (m % 2 == 0) ? 2 : 1;
+    if (v > vec_cap) v = (vec_cap >= 2 && m % 2 == 0) ? 2 : 1;
+    while (v > mb) v >>= 1;
+    return v;
+  };
+  q.vec = pick_vec(q.lpr * q.vc);
+  plan_sizes(q, n, dl, m, l2_bytes, ws_limit);
+  // Optional: split columns further (more, narrower segments) — off by default.
+  static const int64_t target = [] {
+    const char *e = getenv("L1DM_SCAN_SEGMENTS");  // tuning override
+    return e ? atoll(e) : kScanTargetSegments;
+  }();
+  while (q.lpr * q.vc > 8 && q.kc * (int64_t)q.col_blocks < target) {
+    if (q.vc == 2) q.vc = 1; else q.lpr /= 2;
+    q.vec = pick_vec(q.lpr * q.vc);
+    plan_sizes(q, n, dl, m, l2_bytes, ws_limit);
+  }
   q.v6 = (m % 2 == 0) ? 2 : 1;
   int64_t lanes = (m + q.v6 - 1) / q.v6;
   q.lpp = pow2ceil(lanes > 32 ? 32 : lanes);
@@ -139,294 +163,338 @@ void launch_colsums(const float *Z, int64_t ldz, int64_t n, int64_t m, const dou
 }
 
 // ------------------------------------------------------------------ K5
-template <int VEC>
-struct ZVec;
-template <>
-struct ZVec<1> {
-  static __device__ __forceinline__ void load(const float *p, float *o) { o[0] = __ldg(p); }
-};
-template <>
-struct ZVec<2> {
-  static __device__ __forceinline__ void load(const float *p, float *o) {
-    const float2 v = __ldg(reinterpret_cast<const float2 *>(p));
+// One large tile per CTA.  Tiles are claimed by atomic ticket when the CTA starts (segments
+// interleaved, so a tile's predecessor is nseg tickets older); a CTA never holds an
+// unpublished ticket while it waits, so look-back waits are bounded by one tile's load
+// latency.  perm/sval and the gathered Z rows of the tile are staged in shared memory with
+// cp.async (the whole tile's loads are in flight at once), then the tile is scanned straight
+// out of shared memory.
+//
+template <int VC>
+__device__ __forceinline__ void lds_cols(const float *p, float *o) {
+  if constexpr (VC == 1) {
+    o[0] = *p;
+  } else {
+    const float2 v = *reinterpret_cast<const float2 *>(p);
     o[0] = v.x;
     o[1] = v.y;
   }
-};
-template <>
-struct ZVec<4> {
-  static __device__ __forceinline__ void load(const float *p, float *o) {
-    const float4 v = __ldg(reinterpret_cast<const float4 *>(p));
-    o[0] = v.x;
-    o[1] = v.y;
-    o[2] = v.z;
-    o[3] = v.w;
-  }
-};
-
-template <int VEC>
-__device__ __forceinline__ void store_u(double *p, const double *u) {
-  if constexpr (VEC == 1) {
+}
+template <int VC>
+__device__ __forceinline__ void stcs_cols(double *p, const double *u) {
+  if constexpr (VC == 1) {
     __stcs(p, u[0]);
-  } else if constexpr (VEC == 2) {
-    __stcs(reinterpret_cast<double2 *>(p), make_double2(u[0], u[1]));
   } else {
     __stcs(reinterpret_cast<double2 *>(p), make_double2(u[0], u[1]));
-    __stcs(reinterpret_cast<double2 *>(p) + 1, make_double2(u[2], u[3]));
   }
 }
 
-template <int VEC, int LPR, int ITEMS>
-__global__ void __launch_bounds__(256)
+// Lane mapping: lane = rg * LPR + cl owns columns [cl*VC, cl*VC+VC) of the segment
+// (mb = LPR*VC columns) and,
+// for j = 0..ITEMS-1, sorted row  w*ROWS_W + j*RPW + rg.  At fixed j a warp covers RPW
+// consecutive rows x all mb columns: shared-memory reads are conflict-free and each warp
+// store writes RPW full mb*8-byte row pieces of U.  The scan along rows is a warp scan over
+// the RPW row groups per j plus a running carry across j.
+template <int LPR, int VC, int ITEMS>
+struct ScanCfg {
+  static constexpr int MB = LPR * VC;
+  static constexpr int NW = 8;
+  static constexpr int NT = 32 * NW;
+  static constexpr int RPW = 32 / LPR;
+  static constexpr int ROWS_W = RPW * ITEMS;
+  static constexpr int R = NW * ROWS_W;        // rows per tile
+  static constexpr int NP = 2 * MB;            // look-back payload: (s, t) per column
+  static constexpr int ZST = R * MB;           // floats of gathered Z per tile
+  // dynamic smem: Z stage | sval | perm (+ small static arrays)
+  static constexpr size_t SMEM = (size_t)ZST * 4 + (size_t)R * 4 * 2;
+};
+
+
+template <int LPR, int VC, int CH>
+__global__ void __launch_bounds__(256, 2)
     k5_scan(const uint32_t *__restrict__ perm, const float *__restrict__ sval, int64_t ldn,
             int64_t n, const float *__restrict__ Z, int64_t ldz, int64_t m,
-            double *__restrict__ U, int64_t ldu, int64_t k_first, int col_blocks,
-            int64_t tiles_per_seg, uint32_t *flags, double *agg, double *incl, uint32_t epoch,
-            unsigned *ticket, unsigned *timeout_flag) {
-  constexpr int MB = VEC * LPR;
-  constexpr int RPW = 32 / LPR;
-  constexpr int ROWS_W = RPW * ITEMS;
-  constexpr int ROWS_T = 8 * ROWS_W;
-  constexpr int NP = 2 * MB;  // payload: (s, t) per column
-  __shared__ double s_wt[8][NP];
+            double *__restrict__ U, int64_t ldu, int64_t k_first, int col_blocks, int64_t nseg,
+            int64_t total, uint32_t *flags, double *agg, double *incl, uint32_t epoch,
+            unsigned *ticket, unsigned *timeout_flag, int64_t tiles_per_seg) {
+  constexpr int ITEMS = scan_items(LPR, VC);
+  using C = ScanCfg<LPR, VC, ITEMS>;
+  constexpr int MB = C::MB, RPW = C::RPW, ROWS_W = C::ROWS_W, R = C::R, NP = C::NP, NW = C::NW;
+  constexpr int NT = C::NT;
+  constexpr int CPR = MB * 4 / CH;  // cp.async chunks per gathered row
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float *zb = reinterpret_cast<float *>(smem_raw);        // [R][MB]
+  float *vb = zb + C::ZST;                                 // [R]
+  uint32_t *pb = reinterpret_cast<uint32_t *>(vb + R);     // [R]
+  __shared__ double s_wt[NW * NP];  // per-warp totals, then warp-exclusive prefixes
   __shared__ double s_agg[NP];
   __shared__ double s_excl[NP];
-  __shared__ unsigned s_ticket;
+  __shared__ double s_red[NT];
+  __shared__ int64_t s_t;
+  __shared__ int64_t s_j;
+  __shared__ int s_q;
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int rg = lane / LPR, cl = lane % LPR;
-  if (tid == 0) s_ticket = atomicAdd(ticket, 1u);
+  const int rg = lane / LPR, cl = lane - (lane / LPR) * LPR;
+
+  if (tid == 0) s_t = atomicAdd(ticket, 1u);
   __syncthreads();
-  const int64_t t = s_ticket;
-  const int64_t seg = t / tiles_per_seg;
-  const int64_t tile = t - seg * tiles_per_seg;
+  const int64_t t = s_t;
+  const int64_t tile = t / nseg;
+  const int64_t seg = t - tile * nseg;
   const int64_t kk = seg / col_blocks;
   const int cb = (int)(seg - kk * col_blocks);
-  const int64_t k = k_first + kk;
-  const int64_t r0 = tile * ROWS_T + (int64_t)w * ROWS_W + (int64_t)rg * ITEMS;
-  const int col0 = cb * MB + cl * VEC;
-  const bool col_ok = col0 < m;  // VEC divides m, so a lane's columns are all in or all out
+  const int64_t row0 = tile * R;
+  const int64_t nrows = (n - row0 < R) ? (n - row0) : R;
 
-  // ---- sorted-order inputs of this thread's ITEMS consecutive rows
-  uint32_t p[ITEMS];
-  float v[ITEMS];
-  const uint32_t *pp = perm + k * ldn + r0;
-  const float *vp = sval + k * ldn + r0;
-  if (r0 + ITEMS <= n) {
-#pragma unroll
-    for (int j = 0; j < ITEMS; j += 4) {
-      const uint4 a = __ldg(reinterpret_cast<const uint4 *>(pp + j));
-      const float4 b = __ldg(reinterpret_cast<const float4 *>(vp + j));
-      p[j] = a.x; p[j + 1] = a.y; p[j + 2] = a.z; p[j + 3] = a.w;
-      v[j] = b.x; v[j + 1] = b.y; v[j + 2] = b.z; v[j + 3] = b.w;
+  // ---- stage perm + sval of the tile (rows in [n, ldn) are padding: loaded, unused)
+  {
+    const uint32_t *pp = perm + (k_first + kk) * ldn + row0;
+    const float *vp = sval + (k_first + kk) * ldn + row0;
+    for (int c = tid; c < R / 4; c += NT) {
+      const bool ok = row0 + 4 * c < ldn;
+      cp_async<16>(pb + 4 * c, ok ? (const void *)(pp + 4 * c) : (const void *)perm, ok);
+      cp_async<16>(vb + 4 * c, ok ? (const void *)(vp + 4 * c) : (const void *)sval, ok);
     }
-  } else {
-#pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
-      const bool ok = r0 + j < n;
-      p[j] = ok ? __ldg(pp + j) : 0u;
-      v[j] = ok ? __ldg(vp + j) : 0.0f;
-    }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
   }
   // ---- gather z rows into sorted order ("in the order induced by T_i")
-  float z[ITEMS][VEC];
-#pragma unroll
-  for (int j = 0; j < ITEMS; ++j) {
-    if (col_ok && r0 + j < n) {
-      ZVec<VEC>::load(Z + (int64_t)p[j] * ldz + col0, z[j]);
-    } else {
-#pragma unroll
-      for (int q = 0; q < VEC; ++q) z[j][q] = 0.0f;
+  {
+    const int64_t col_base = (int64_t)cb * MB;
+    for (int e = tid; e < R * CPR; e += NT) {
+      const int r = e / CPR, ch = e - (e / CPR) * CPR;
+      const int64_t col = col_base + ch * (CH / 4);
+      const bool ok = (r < nrows) && (col < m);
+      const float *src = ok ? Z + (int64_t)pb[r] * ldz + col : Z;
+      cp_async<CH>(zb + r * MB + ch * (CH / 4), src, ok);
     }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
   }
-  // ---- thread totals of s and t = v*s (exact in fp64)
-  double own_s[VEC], own_t[VEC];
+  const int64_t col = (int64_t)cb * MB + cl * VC;
+  const bool col_ok = col < m;  // VC divides m: a lane's columns are all in or all out
+  const int rbase = w * ROWS_W + rg;  // row of item j: rbase + j * RPW
+
+  // ---- phase 1: warp totals of s = z and t = v z (fp64; products exact)
+  double cs[VC], ct[VC];  // carry: sums over this warp's items so far (all row groups)
 #pragma unroll
-  for (int q = 0; q < VEC; ++q) {
-    own_s[q] = 0.0;
-    own_t[q] = 0.0;
+  for (int q = 0; q < VC; ++q) {
+    cs[q] = 0.0;
+    ct[q] = 0.0;
   }
-#pragma unroll
+#pragma unroll 4
   for (int j = 0; j < ITEMS; ++j) {
-    const double vj = (double)v[j];
+    const int r = rbase + j * RPW;
+    float zz[VC];
+    lds_cols<VC>(zb + r * MB + cl * VC, zz);     // zero-filled past n / past m
+    const double vj = (r < nrows) ? (double)vb[r] : 0.0;
 #pragma unroll
-    for (int q = 0; q < VEC; ++q) {
-      const double s = (double)z[j][q];
-      own_s[q] += s;
-      own_t[q] = fma(vj, s, own_t[q]);
-    }
-  }
-  // ---- warp inclusive scan across the RPW row groups of the same column lane
-  double ps[VEC], pt[VEC];
+    for (int q = 0; q < VC; ++q) {
+      double a = (double)zz[q], b = vj * (double)zz[q];
 #pragma unroll
-  for (int q = 0; q < VEC; ++q) {
-    ps[q] = own_s[q];
-    pt[q] = own_t[q];
-  }
-#pragma unroll
-  for (int off = 1; off < RPW; off <<= 1) {
-#pragma unroll
-    for (int q = 0; q < VEC; ++q) {
-      const double a = __shfl_up_sync(0xFFFFFFFFu, ps[q], off * LPR);
-      const double b = __shfl_up_sync(0xFFFFFFFFu, pt[q], off * LPR);
-      if (rg >= off) {
-        ps[q] += a;
-        pt[q] += b;
+      for (int off = 1; off < RPW; off <<= 1) {  // reduce across the RPW row groups
+        a += __shfl_xor_sync(0xFFFFFFFFu, a, off * LPR);
+        b += __shfl_xor_sync(0xFFFFFFFFu, b, off * LPR);
       }
+      cs[q] += a;
+      ct[q] += b;
     }
   }
-  if (rg == RPW - 1) {
+  if (rg == 0) {
 #pragma unroll
-    for (int q = 0; q < VEC; ++q) {
-      s_wt[w][2 * (cl * VEC + q)] = ps[q];
-      s_wt[w][2 * (cl * VEC + q) + 1] = pt[q];
+    for (int q = 0; q < VC; ++q) {
+      s_wt[w * NP + 2 * (cl * VC + q)] = cs[q];
+      s_wt[w * NP + 2 * (cl * VC + q) + 1] = ct[q];
     }
   }
   __syncthreads();
-  // ---- block: warp-exclusive prefixes in place, tile aggregate
-  if (tid < NP) {
+  if (tid < NP) {  // warp-exclusive prefixes in place, tile aggregate
     double run = 0.0;
 #pragma unroll
-    for (int ww = 0; ww < 8; ++ww) {
-      const double c = s_wt[ww][tid];
-      s_wt[ww][tid] = run;
+    for (int ww = 0; ww < NW; ++ww) {
+      const double c = s_wt[ww * NP + tid];
+      s_wt[ww * NP + tid] = run;
       run += c;
     }
     s_agg[tid] = run;
   }
   __syncthreads();
-  // ---- decoupled look-back across the tiles of this segment (warp 0)
-  if (w == 0) {
-    const int64_t slot0 = seg * tiles_per_seg;
-    const int64_t me = slot0 + tile;
-    double acc[(NP + 31) / 32];
-#pragma unroll
-    for (int u = 0; u < (NP + 31) / 32; ++u) acc[u] = 0.0;
-    if (tile == 0) {
-#pragma unroll
-      for (int u = 0; u < (NP + 31) / 32; ++u) {
-        const int comp = lane + 32 * u;
-        if (comp < NP) __stcg(&incl[me * NP + comp], s_agg[comp]);
-      }
+
+  // ---- decoupled look-back (Merrill & Garland) across the tiles of this segment
+  const int64_t slot0 = seg * tiles_per_seg;
+  const int64_t me = slot0 + tile;
+  if (tid < NP) s_excl[tid] = 0.0;
+  if (tile == 0) {
+    if (tid < NP) {
+      __stcg(&incl[me * NP + tid], s_agg[tid]);
       __threadfence();
-      __syncwarp();
-      if (lane == 0) st_release_u32(&flags[me], (epoch << 2) | kFlagInclusive);
-    } else {
-#pragma unroll
-      for (int u = 0; u < (NP + 31) / 32; ++u) {
-        const int comp = lane + 32 * u;
-        if (comp < NP) __stcg(&agg[me * NP + comp], s_agg[comp]);
-      }
+    }
+    __syncthreads();
+    if (tid == 0) {
       __threadfence();
-      __syncwarp();
-      if (lane == 0) st_release_u32(&flags[me], (epoch << 2) | kFlagAggregate);
-      int64_t j = tile - 1;
-      uint32_t spins = 0;
-      for (;;) {
-        uint32_t f = 0;
-        if (lane == 0) {
+      st_release_u32(&flags[me], (epoch << 2) | kFlagInclusive);
+    }
+  } else {
+    if (tid < NP) {
+      __stcg(&agg[me * NP + tid], s_agg[tid]);
+      __threadfence();
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      st_release_u32(&flags[me], (epoch << 2) | kFlagAggregate);
+    }
+    int64_t j = tile - 1;  // nearest predecessor not yet summed
+    for (;;) {
+      // warp 0: lane l examines predecessor j - l; q = nearest inclusive prefix in the window
+      if (w == 0) {
+        const int64_t jl = j - lane;
+        uint32_t f = (epoch << 2) | kFlagInclusive;  // jl < 0: empty prefix
+        if (jl >= 0) {
+          uint32_t spins = 0;
           for (;;) {
-            f = ld_acquire_u32(&flags[slot0 + j]);
+            f = ld_acquire_u32(&flags[slot0 + jl]);
             if ((f >> 2) == (epoch & 0x3FFFFFFFu) && (f & 3u) != kFlagInvalid) break;
             if (++spins > kSpinLimit) {
               atomicOr(timeout_flag, 1u);
-              f = 0xFFFFFFFFu;  // give up (results invalid; host reports ETIMEOUT)
+              f = (epoch << 2) | kFlagInclusive;  // give up (results invalid; ETIMEOUT)
               break;
             }
-            if (spins > 32) __nanosleep(32);
+            if (spins > 8) __nanosleep(32);
           }
         }
-        f = __shfl_sync(0xFFFFFFFFu, f, 0);
-        if (f == 0xFFFFFFFFu) break;
-        const bool inc = (f & 3u) == kFlagInclusive;
-        const double *src = (inc ? incl : agg) + (slot0 + j) * NP;
-#pragma unroll
-        for (int u = 0; u < (NP + 31) / 32; ++u) {
-          const int comp = lane + 32 * u;
-          if (comp < NP) acc[u] += __ldcg(src + comp);
+        const uint32_t inc_mask = __ballot_sync(0xFFFFFFFFu, (f & 3u) == kFlagInclusive);
+        if (lane == 0) {
+          s_q = inc_mask ? __ffs(inc_mask) - 1 : 32;
+          s_j = j;
         }
-        if (inc) break;
-        --j;
       }
+      __syncthreads();
+      const int q = s_q;
+      const int64_t jw = s_j;
+      const int cnt = q < 32 ? q + 1 : 32;  // tiles jw .. jw-cnt+1 (the last one INCL if q<32)
+      constexpr int GROUPS = NT / NP;       // all threads sum payloads, comp = tid % NP
+      double part = 0.0;
+      {
+        const int comp = tid % NP, g = tid / NP;
+        if (g < GROUPS) {
+          for (int b = g; b < cnt; b += GROUPS) {
+            const int64_t jj = jw - b;
+            if (jj < 0) break;
+            part += __ldcg((b == q ? incl : agg) + (slot0 + jj) * NP + comp);
+          }
+        }
+      }
+      s_red[tid] = part;
+      __syncthreads();
+      if (tid < NP) {
+        double sum = 0.0;
 #pragma unroll
-      for (int u = 0; u < (NP + 31) / 32; ++u) {
-        const int comp = lane + 32 * u;
-        if (comp < NP) __stcg(&incl[me * NP + comp], acc[u] + s_agg[comp]);
+        for (int g = 0; g < GROUPS; ++g) sum += s_red[g * NP + tid];
+        s_excl[tid] += sum;
       }
+      __syncthreads();
+      if (q < 32) break;
+      j = jw - 32;
+    }
+    if (tid < NP) {
+      __stcg(&incl[me * NP + tid], s_excl[tid] + s_agg[tid]);
       __threadfence();
-      __syncwarp();
-      if (lane == 0) st_release_u32(&flags[me], (epoch << 2) | kFlagInclusive);
     }
-#pragma unroll
-    for (int u = 0; u < (NP + 31) / 32; ++u) {
-      const int comp = lane + 32 * u;
-      if (comp < NP) s_excl[comp] = acc[u];
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      st_release_u32(&flags[me], (epoch << 2) | kFlagInclusive);
     }
   }
-  __syncthreads();
-  // ---- exclusive prefix at this thread's first row, then U along its rows
-  double P[VEC], Q[VEC];
+  // ---- phase 2: exclusive prefixes P, Q along the rows, U_r = v_r P_r - Q_r
+  double P[VC], Q[VC];
 #pragma unroll
-  for (int q = 0; q < VEC; ++q) {
-    const int c2 = 2 * (cl * VEC + q);
-    P[q] = s_excl[c2] + s_wt[w][c2] + (ps[q] - own_s[q]);
-    Q[q] = s_excl[c2 + 1] + s_wt[w][c2 + 1] + (pt[q] - own_t[q]);
+  for (int q = 0; q < VC; ++q) {
+    const int c2 = 2 * (cl * VC + q);
+    P[q] = s_excl[c2] + s_wt[w * NP + c2];
+    Q[q] = s_excl[c2 + 1] + s_wt[w * NP + c2 + 1];
   }
-  if (!col_ok) return;
-  double *up = U + kk * n * ldu + r0 * ldu + col0;
-#pragma unroll
+  double *ub = U + kk * n * ldu + (row0 + rbase) * ldu + col;
+#pragma unroll 4
   for (int j = 0; j < ITEMS; ++j) {
-    if (r0 + j < n) {
-      const double vj = (double)v[j];
-      double u[VEC];
+    const int r = rbase + j * RPW;
+    float zz[VC];
+    lds_cols<VC>(zb + r * MB + cl * VC, zz);
+    const double vj = (r < nrows) ? (double)vb[r] : 0.0;
+    double u[VC];
 #pragma unroll
-      for (int q = 0; q < VEC; ++q) {
-        const double s = (double)z[j][q];
-        u[q] = fma(vj, P[q], -Q[q]);  // U_r = v_r P_r - Q_r
-        P[q] += s;
-        Q[q] = fma(vj, s, Q[q]);
+    for (int q = 0; q < VC; ++q) {
+      const double s = (double)zz[q], tt = vj * s;
+      double a = s, b = tt;  // inclusive scan across the RPW row groups of this column
+#pragma unroll
+      for (int off = 1; off < RPW; off <<= 1) {
+        const double a2 = __shfl_up_sync(0xFFFFFFFFu, a, off * LPR);
+        const double b2 = __shfl_up_sync(0xFFFFFFFFu, b, off * LPR);
+        if (rg >= off) {
+          a += a2;
+          b += b2;
+        }
       }
-      store_u<VEC>(up + (int64_t)j * ldu, u);
+      u[q] = fma(vj, P[q] + (a - s), -(Q[q] + (b - tt)));  // exclusive prefixes at row r
+      // carry: this item's totals over all row groups (held by the last row group)
+      P[q] += __shfl_sync(0xFFFFFFFFu, a, (RPW - 1) * LPR + cl);
+      Q[q] += __shfl_sync(0xFFFFFFFFu, b, (RPW - 1) * LPR + cl);
     }
+    if (col_ok && r < nrows) stcs_cols<VC>(ub + (int64_t)j * RPW * ldu, u);
   }
 }
 
-template <int VEC, int LPR>
+template <int LPR, int VC, int CH>
 static void launch_scan_t(const QueryPlan &p, const uint32_t *perm, const float *sval,
                           int64_t ldn, int64_t n, const float *Z, int64_t ldz, int64_t m,
                           double *U, int64_t k_first, int64_t kcc, uint32_t *flags, double *agg,
                           double *incl, uint32_t epoch, unsigned *ticket, unsigned *timeout_flag,
                           cudaStream_t s) {
-  const int64_t blocks = kcc * p.col_blocks * p.tiles_per_segment;
-  k5_scan<VEC, LPR, 8><<<(unsigned)blocks, 256, 0, s>>>(
-      perm, sval, ldn, n, Z, ldz, m, U, p.ldu, k_first, p.col_blocks, p.tiles_per_segment, flags,
-      agg, incl, epoch, ticket, timeout_flag);
+  using C = ScanCfg<LPR, VC, scan_items(LPR, VC)>;
+  auto kern = k5_scan<LPR, VC, CH>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    attr = true;
+  }
+  const int64_t nseg = kcc * p.col_blocks;
+  const int64_t total = nseg * p.tiles_per_segment;
+  kern<<<(unsigned)total, C::NT, C::SMEM, s>>>(perm, sval, ldn, n, Z, ldz, m, U, p.ldu, k_first,
+                                               p.col_blocks, nseg, total, flags, agg, incl, epoch,
+                                               ticket, timeout_flag, p.tiles_per_segment);
 }
 
 void launch_scan(const QueryPlan &p, const uint32_t *perm, const float *sval, int64_t ldn,
                  int64_t n, const float *Z, int64_t ldz, int64_t m, double *U, int64_t k_first,
                  int64_t kcc, uint32_t *flags, double *agg, double *incl, uint32_t epoch,
                  unsigned *ticket, unsigned *timeout_flag, cudaStream_t s) {
-#define L1DM_SCAN(V, L)                                                                     \
-  launch_scan_t<V, L>(p, perm, sval, ldn, n, Z, ldz, m, U, k_first, kcc, flags, agg, incl, \
-                      epoch, ticket, timeout_flag, s)
-  switch (p.vec * 100 + p.lpr) {
-    case 101: L1DM_SCAN(1, 1); break;
-    case 102: L1DM_SCAN(1, 2); break;
-    case 104: L1DM_SCAN(1, 4); break;
-    case 108: L1DM_SCAN(1, 8); break;
-    case 116: L1DM_SCAN(1, 16); break;
-    case 132: L1DM_SCAN(1, 32); break;
-    case 201: L1DM_SCAN(2, 1); break;
-    case 202: L1DM_SCAN(2, 2); break;
-    case 204: L1DM_SCAN(2, 4); break;
-    case 208: L1DM_SCAN(2, 8); break;
-    case 216: L1DM_SCAN(2, 16); break;
-    case 401: L1DM_SCAN(4, 1); break;
-    case 402: L1DM_SCAN(4, 2); break;
-    case 404: L1DM_SCAN(4, 4); break;
-    case 408: L1DM_SCAN(4, 8); break;
-    case 416: L1DM_SCAN(4, 16); break;
+#define L1DM_SCAN(L, V, CH)                                                                 \
+  launch_scan_t<L, V, CH>(p, perm, sval, ldn, n, Z, ldz, m, U, k_first, kcc, flags, agg, incl, \
+                          epoch, ticket, timeout_flag, s)
+  // p.lpr lanes per row, p.mb / p.lpr columns per lane, p.vec floats per cp.async chunk
+  const int vc = p.mb / p.lpr;
+  switch (vc * 10000 + p.vec * 100 + p.lpr) {
+    case 10101: L1DM_SCAN(1, 1, 4); break;
+    case 10102: L1DM_SCAN(2, 1, 4); break;
+    case 10104: L1DM_SCAN(4, 1, 4); break;
+    case 10108: L1DM_SCAN(8, 1, 4); break;
+    case 10116: L1DM_SCAN(16, 1, 4); break;
+    case 10132: L1DM_SCAN(32, 1, 4); break;
+    case 10202: L1DM_SCAN(2, 1, 8); break;
+    case 10204: L1DM_SCAN(4, 1, 8); break;
+    case 10208: L1DM_SCAN(8, 1, 8); break;
+    case 10216: L1DM_SCAN(16, 1, 8); break;
+    case 10232: L1DM_SCAN(32, 1, 8); break;
+    case 10404: L1DM_SCAN(4, 1, 16); break;
+    case 10408: L1DM_SCAN(8, 1, 16); break;
+    case 10416: L1DM_SCAN(16, 1, 16); break;
+    case 10432: L1DM_SCAN(32, 1, 16); break;
+    case 20232: L1DM_SCAN(32, 2, 8); break;
+    case 20432: L1DM_SCAN(32, 2, 16); break;
     default: break;
   }
 #undef L1DM_SCAN

@@ -1,0 +1,78 @@
+"""Coordinate sharding over torch.distributed (one process per GPU; NCCL over NVLink).
+
+A = sum_k A^(k) with A^(k)_ij = |x_ik - x_jk| (the swap of sums in the proof of
+Thm "p=1"), so rank g prepares only its coordinate slice K_g and
+returns the partial Y_g = A^(K_g) Z (its own share of the g - h S epilogue
+included, reading R15).  One fp64 SUM collective combines the partials:
+reduce to a root (BASELINE.json north_star "NCCL reduce") or all-reduce when every
+rank needs Y (Krylov-style consumers).  Prepare is communication-free.
+
+The local compute is the C ABI (l1dm_prepare_ex / l1dm_matvec_ex).  For host-side
+tests of the sharding logic on CPU (gloo), `local_prepare` / `local_matvec` can be
+injected; the product default never runs anything but the CUDA library.
+"""
+from __future__ import annotations
+
+from typing import Callable, Optional
+
+import torch
+import torch.distributed as dist
+
+from . import binding
+
+
+def shard_range(d: int, rank: int, world: int) -> tuple[int, int]:
+    """Coordinates [floor(g d / G), floor((g+1) d / G)) for rank g of G."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError(f"bad rank {rank} of {world}")
+    return (rank * d) // world, ((rank + 1) * d) // world
+
+
+class ShardedL1DM:
+    """Per-rank handle over a coordinate shard, with the cross-rank sum of Y."""
+
+    def __init__(self, X: torch.Tensor, group=None, *, k_range=None,
+                 local_prepare: Optional[Callable] = None,
+                 local_matvec: Optional[Callable] = None, stream=None):
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        d = X.shape[1]
+        self.k_begin, self.k_end = k_range if k_range is not None else shard_range(
+            d, self.rank, self.world)
+        self._prepare = local_prepare or binding.l1dm_prepare
+        self._matvec = local_matvec or binding.l1dm_matvec
+        self.stream = stream
+        if self.k_end > self.k_begin:
+            self.handle = self._prepare(X, self.k_begin, self.k_end, stream=stream)
+        else:
+            self.handle = None  # more ranks than coordinates: this rank contributes zeros
+
+    def partial(self, Z: torch.Tensor, Y: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Y_g = A^(K_g) Z for this rank's coordinates (no communication)."""
+        n, m = Z.shape[0], (Z.shape[1] if Z.dim() == 2 else 1)
+        if self.handle is None:
+            if Y is None:
+                Y = torch.zeros((n, m), dtype=torch.float64, device=Z.device)
+            else:
+                Y.zero_()
+            return Y
+        return self._matvec(self.handle, Z, Y, stream=self.stream)
+
+    def matvec(self, Z: torch.Tensor, Y: Optional[torch.Tensor] = None, *, root: Optional[int] = 0,
+               async_op: bool = False):
+        """A·Z summed over ranks: on `root` only (reduce) or on every rank (root=None)."""
+        Y = self.partial(Z, Y)
+        if self.world == 1:
+            return (Y, None) if async_op else Y
+        if root is None:
+            work = dist.all_reduce(Y, op=dist.ReduceOp.SUM, group=self.group, async_op=async_op)
+        else:
+            work = dist.reduce(Y, dst=root, op=dist.ReduceOp.SUM, group=self.group,
+                               async_op=async_op)
+        return (Y, work) if async_op else Y
+
+    def close(self):
+        if self.handle is not None and self._prepare is binding.l1dm_prepare:
+            binding.l1dm_free(self.handle)
+        self.handle = None

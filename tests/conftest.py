@@ -35,13 +35,17 @@ def load_golden(name):
 GOLDEN = ["q1_three_points.txt", "q2_identity.txt", "q20_two_dim.txt", "q21_ties_negative.txt"]
 
 
-def col_rel_l2(Y, Yref):
-    """Max over columns of ||Y[:,c]-Yref[:,c]||_2 / ||Yref[:,c]||_2 (abs floor 1e-12*n)."""
+def col_rel_l2(Y, Yref, floor=0.0):
+    """Max over columns of ||Y[:,c]-Yref[:,c]||_2 / max(||Yref[:,c]||_2, floor).
+
+    A column whose reference is exactly zero (and floor == 0) scores 0 if Y matches
+    it exactly and inf otherwise."""
     Y = np.asarray(Y, dtype=np.float64).reshape(Yref.shape[0], -1)
     Yref = np.asarray(Yref, dtype=np.float64).reshape(Yref.shape[0], -1)
     worst = 0.0
     for c in range(Yref.shape[1]):
         num = np.linalg.norm(Y[:, c] - Yref[:, c])
         den = np.linalg.norm(Yref[:, c])
-        worst = max(worst, num / den if den > 0 else num / (1e-12 * Yref.shape[0]))
+        den = max(den, floor)
+        worst = max(worst, num / den if den > 0 else (0.0 if num == 0 else float("inf")))
     return worst

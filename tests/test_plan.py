@@ -6,15 +6,22 @@ import paper_2210_15114_b200 as l1
 L2 = 126 << 20
 
 
-@pytest.mark.parametrize("m,vec,lpr", [(1, 1, 1), (2, 2, 1), (3, 1, 4), (4, 4, 1), (5, 1, 8),
-                                       (8, 4, 2), (16, 4, 4), (31, 1, 32), (32, 4, 8),
-                                       (64, 4, 16), (65, 1, 32), (128, 4, 16), (6, 2, 4)])
-def test_lane_mapping(m, vec, lpr):
+def scan_items(lpr, vc):
+    it = (98304 // (1024 * vc + 2048 // lpr)) // 4 * 4
+    return min(it, 64)
+
+
+# (m, gather floats per cp.async, lanes per row, columns per segment)
+@pytest.mark.parametrize("m,vec,lpr,mb", [(1, 1, 1, 1), (2, 2, 2, 2), (3, 1, 4, 4), (4, 4, 4, 4),
+                                          (5, 1, 8, 8), (8, 4, 8, 8), (16, 4, 16, 16),
+                                          (31, 1, 32, 32), (32, 4, 32, 32), (64, 4, 32, 64),
+                                          (65, 1, 32, 32), (128, 4, 32, 64), (6, 2, 8, 8),
+                                          (34, 2, 32, 64)])
+def test_lane_mapping(m, vec, lpr, mb):
     p = l1.l1dm_plan(1 << 20, 64, m, L2, 64 << 30)
-    assert (p["vec"], p["lanes_per_row"]) == (vec, lpr)
-    assert p["mb"] == vec * lpr
+    assert (p["vec"], p["lanes_per_row"], p["mb"]) == (vec, lpr, mb)
     assert p["col_blocks"] == -(-m // p["mb"])
-    assert p["rows_per_tile"] == 8 * (32 // lpr) * 8
+    assert p["rows_per_tile"] == 8 * (32 // lpr) * scan_items(lpr, mb // lpr)
     assert p["tiles_per_segment"] == -(-(1 << 20) // p["rows_per_tile"])
 
 
@@ -30,7 +37,7 @@ def test_large_problem_uses_hbm_workspace():
     assert p["l2_resident"] == 0
     assert p["kc"] == 128 and p["chunks"] == 1
     p = l1.l1dm_plan(1 << 24, 128, 32, L2, 64 << 30)
-    assert p["kc"] == 15 and p["chunks"] == 9
+    assert p["kc"] == 15 and p["chunks"] == 9   # U per coordinate = 4 GiB (+ look-back state)
     assert p["workspace_bytes"] <= 64 << 30
 
 
