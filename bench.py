@@ -149,7 +149,7 @@ def run_reference(args):
     vals = []
     info = None
     for i in range(args.warmup + args.steps):
-        info = cpu_oracle_sample(w, Q, budget_dims=(16, 16))
+        info = cpu_oracle_sample(w, Q, budget_dims=(64, 16))
         if i >= args.warmup:
             vals.append(info["value"])
     value = statistics.mean(vals)
@@ -245,24 +245,31 @@ def main_ours(args):
     upd_step = n * d * m * Q
     value = upd_step / (ms_step * 1e-3)
 
-    # per-kernel device times (events on the library stream), this rank
+    # per-kernel device times (CUDA events on the library's stream), this rank
     agg = {k: sum(tt[k] for tt in timings) for k in timings[0]} if timings else {}
     prep_ms = statistics.mean(tt["prep_ms"] for tt in timings) if timings else None
-    scan_launch_ms = agg["scan_ms"] / max(agg["scan_launches"], 1) if agg else None
-    acc_launch_ms = agg["accumulate_ms"] / max(agg["accumulate_launches"], 1) if agg else None
-    query_kernel_ms = ((agg["colsums_ms"] + agg["scan_ms"] + agg["accumulate_ms"]) /
-                       max(agg["queries"], 1)) if agg else None
+    nq = max(agg.get("queries", 0), 1)
+    query_kernel_ms = ((agg["colsums_ms"] + agg["scan_ms"] + agg["accumulate_ms"]) / nq
+                       if agg else None)
     hbm_peak, peak_kind = load_peaks()
     dl = k1 - k0
-    plan = l1.l1dm_plan(n, dl, m) if dl > 0 else None
-    kc = plan["kc"] if plan else dl
-    # algorithmic bytes per launch (SURVEY §8(d) Model B split by kernel)
-    scan_bytes = n * kc * (8 + 12 * m)
-    acc_bytes = n * kc * (4 + 8 * m) + n * (8 * m + 8)
-    scan_ach = scan_bytes / (scan_launch_ms * 1e-3) / 1e9 if scan_launch_ms else None
-    acc_ach = acc_bytes / (acc_launch_ms * 1e-3) / 1e9 if acc_launch_ms else None
-    dominant = "scan" if (agg.get("scan_ms", 0) >= agg.get("accumulate_ms", 0)) else "accumulate"
-    ach = scan_ach if dominant == "scan" else acc_ach
+    # algorithmic bytes (SURVEY §8(d) Model B, split by kernel):
+    #   scan       per (point, coordinate): perm 4 + sval 4 + Z row 4m + U row 8m
+    #   accumulate per (point, coordinate): rank 4 + U row 8m; per point and query: Y 8m + h 8
+    scan_bytes = agg.get("scan_pairs", 0) * (8 + 12 * m)
+    acc_bytes = agg.get("accumulate_pairs", 0) * (4 + 8 * m) + agg.get("queries", 0) * n * (8 * m + 8)
+    kern = {
+        "scan": {"ms_total": agg.get("scan_ms"), "launches": agg.get("scan_launches"),
+                 "alg_bytes": scan_bytes},
+        "accumulate": {"ms_total": agg.get("accumulate_ms"),
+                       "launches": agg.get("accumulate_launches"), "alg_bytes": acc_bytes},
+    }
+    for kv in kern.values():
+        kv["ms_per_launch"] = kv["ms_total"] / max(kv["launches"] or 1, 1) if kv["ms_total"] else None
+        kv["achieved_GBps"] = (kv["alg_bytes"] / (kv["ms_total"] * 1e-3) / 1e9
+                               if kv["ms_total"] else None)
+    dominant = max(kern, key=lambda k: kern[k]["ms_total"] or 0.0)
+    ach = kern[dominant]["achieved_GBps"]
     traffic = None
     prof = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.workload}.json")
     if os.path.exists(prof):
@@ -285,13 +292,15 @@ def main_ours(args):
         "prepare_ms": prep_ms,
         "query_ms": (ms_step - (prep_ms or 0.0)) / Q,
         "query_kernel_ms": query_kernel_ms,
-        "kernel_ms_per_launch": {"scan": scan_launch_ms, "accumulate": acc_launch_ms,
-                                 "colsums": agg["colsums_ms"] / max(agg["colsums_launches"], 1)
-                                 if agg else None},
+        "kernels": kern,
+        "colsums_ms_per_launch": (agg["colsums_ms"] / max(agg["colsums_launches"], 1)
+                                  if agg else None),
         "model_b_GBps_per_query": qb / (query_kernel_ms * 1e-3) / 1e9 if query_kernel_ms else None,
         "roofline": {"bound": "hbm", "kernel": dominant, "achieved": ach, "peak": hbm_peak,
                      "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": (ach / hbm_peak) if ach else None, "traffic": traffic,
+                     "alg_bytes_per_launch": (kern[dominant]["alg_bytes"] /
+                                              max(kern[dominant]["launches"] or 1, 1)),
                      "frac_of_8TBps": (ach / 8000.0) if ach else None},
         "clocks": clk,
     }
@@ -315,7 +324,7 @@ def main_ours(args):
     # ---- CPU baseline: the oracle on the host cores, bounded sample, rank 0 at N=1
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cb = cpu_oracle_sample(w, Q, budget_dims=(16, 16))
+            cb = cpu_oracle_sample(w, Q, budget_dims=(64, 16))
             result["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind",
                                                          "sample")}
         except Exception as e:  # the baseline is reported, never required

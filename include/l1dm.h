@@ -124,7 +124,7 @@ L1DM_API l1dm_status l1dm_shape(l1dm_handle h, int64_t *n, int64_t *d_local, int
 /* Upper bound on the query workspace (bytes) a query with m columns allocates. */
 L1DM_API size_t l1dm_workspace_bytes(l1dm_handle h, int64_t m);
 
-/* Cap the query workspace (bytes; 0 = automatic, a fraction of free memory).
+/* Cap the query workspace (bytes; 0 = automatic: 75% of the free device memory).
  * A smaller cap means more coordinate chunks (more Y read-modify-writes). */
 L1DM_API l1dm_status l1dm_set_workspace_limit(l1dm_handle h, size_t bytes);
 
@@ -160,7 +160,10 @@ typedef struct {
   int64_t scan_launches;
   int64_t accumulate_launches;
   int64_t queries;
-  int64_t kernel_launches;  /* every kernel the library launched while enabled */
+  int64_t kernel_launches;  /* every kernel the library launched (prepare + queries) */
+  int64_t scan_pairs;       /* (point, coordinate) pairs the timed scan launches covered */
+  int64_t accumulate_pairs; /* (point, coordinate) pairs the timed accumulate launches covered */
+  int64_t m_last;           /* columns of the latest query */
 } l1dm_timing_t;
 L1DM_API l1dm_status l1dm_timing_enable(l1dm_handle h, int enable);
 L1DM_API l1dm_status l1dm_timing_read(l1dm_handle h, l1dm_timing_t *out, int reset);

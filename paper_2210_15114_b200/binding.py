@@ -50,7 +50,9 @@ class TimingT(ctypes.Structure):
                 ("scan_ms", ctypes.c_double), ("accumulate_ms", ctypes.c_double),
                 ("copy_ms", ctypes.c_double), ("colsums_launches", ctypes.c_int64),
                 ("scan_launches", ctypes.c_int64), ("accumulate_launches", ctypes.c_int64),
-                ("queries", ctypes.c_int64), ("kernel_launches", ctypes.c_int64)]
+                ("queries", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
+                ("scan_pairs", ctypes.c_int64), ("accumulate_pairs", ctypes.c_int64),
+                ("m_last", ctypes.c_int64)]
 
 
 _lib = None

@@ -125,6 +125,7 @@ struct l1dm_ctx {
   int64_t launches[kNumKinds] = {0, 0, 0, 0, 0};
   int64_t queries = 0;
   int64_t kernel_launches = 0;
+  int64_t scan_pairs = 0, acc_pairs = 0, m_last = 0;
 };
 
 namespace {
@@ -391,7 +392,7 @@ l1dm_status ensure_plan(l1dm_ctx *h, int64_t m, int vec_cap) {
   if (ws == 0) {
     size_t fr = 0, tot = 0;
     CUDA_TRY(cudaMemGetInfo(&fr, &tot));
-    ws = (size_t)(0.5 * (double)(fr + h->U.count * sizeof(double) +
+    ws = (size_t)(0.75 * (double)(fr + h->U.count * sizeof(double) +
                                  h->agg.count * sizeof(double) * 2));
   }
   if (h->plan_m == m && h->plan_ws == ws && h->plan_vec_cap == vec_cap) return L1DM_OK;
@@ -438,6 +439,7 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
                   h->ctr.p + 2 + c, h->ctr.p + 1, s);
       h->kernel_launches++;
       h->launches[kScan]++;
+      if (h->timing) h->scan_pairs += h->n * kcc;
     }
     {
       TimedScope ts(h, kAcc, s);
@@ -445,10 +447,12 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
                         ldy, m, c == 0, s);
       h->kernel_launches++;
       h->launches[kAcc]++;
+      if (h->timing) h->acc_pairs += h->n * kcc;
     }
   }
   CUDA_TRY(cudaGetLastError());
   h->queries++;
+  h->m_last = m;
   return L1DM_OK;
 }
 
@@ -579,7 +583,7 @@ size_t l1dm_workspace_bytes(l1dm_handle h, int64_t m) {
   if (ws == 0) {
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return 0;
-    ws = (int64_t)(0.5 * (double)fr);
+    ws = (int64_t)(0.75 * (double)fr);
   }
   if (!make_plan(h->n, h->dl, m, h->l2_bytes, ws, 4, &p)) return 0;
   return p.workspace_bytes;
@@ -640,7 +644,12 @@ l1dm_status l1dm_timing_read(l1dm_handle h, l1dm_timing_t *out, int reset) {
   out->accumulate_launches = h->launches[kAcc];
   out->queries = h->queries;
   out->kernel_launches = h->kernel_launches;
+  out->scan_pairs = h->scan_pairs;
+  out->accumulate_pairs = h->acc_pairs;
+  out->m_last = h->m_last;
   if (reset) {
+    h->scan_pairs = 0;
+    h->acc_pairs = 0;
     for (int k = 0; k < kNumKinds; ++k) {
       h->ms[k] = 0.0;
       h->launches[k] = 0;

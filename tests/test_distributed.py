@@ -1,0 +1,97 @@
+"""Coordinate-sharding host logic on CPU with gloo, world size 2.
+
+The local compute is injected from the oracle (the product path has no CPU compute), so
+these tests check the partition of coordinates, the per-shard partial products and the
+cross-rank SUM (reduce to root and all-reduce) — on integer data, exactly."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_2210_15114_b200.distributed import ShardedL1DM, shard_range
+
+
+def test_shard_range_partitions_coordinates():
+    for d in (1, 2, 7, 16, 96, 128):
+        for G in (1, 2, 3, 4, 8):
+            ranges = [shard_range(d, g, G) for g in range(G)]
+            assert ranges[0][0] == 0 and ranges[-1][1] == d
+            for (a, b), (c, e) in zip(ranges, ranges[1:]):
+                assert b == c and a <= b
+            sizes = [b - a for a, b in ranges]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        shard_range(8, 2, 2)
+
+
+class OracleShard:
+    """Stand-in for the C-ABI handle: Alg. 1 tables of the full X, Alg. 2 over [k0, k1)."""
+
+    def __init__(self, X, k0, k1):
+        self.X = X.numpy()
+        self.k0, self.k1 = k0, k1
+        _, self.order = oracle.alg1(self.X)
+
+
+def oracle_prepare(X, k0, k1, stream=None):
+    return OracleShard(X, k0, k1)
+
+
+def oracle_matvec(h, Z, Y=None, stream=None):
+    out = torch.from_numpy(oracle.alg2_range(h.X, h.order, h.k0, h.k1, Z.numpy()))
+    if Y is not None:
+        Y.copy_(out)
+        return Y
+    return out
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def worker(rank, world, port, d, results):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(123)
+        X = torch.from_numpy(rng.integers(0, 7, size=(300, d)).astype(np.float32))
+        Z = torch.from_numpy(rng.integers(-3, 4, size=(300, 4)).astype(np.float32))
+        sh = ShardedL1DM(X, local_prepare=oracle_prepare, local_matvec=oracle_matvec)
+        Yr = sh.matvec(Z.clone(), root=0)            # reduce to rank 0
+        Ya = sh.matvec(Z.clone(), root=None)         # all-reduce
+        part = sh.partial(Z.clone())
+        results[rank] = (sh.k_begin, sh.k_end, Yr.numpy().copy(), Ya.numpy().copy(),
+                         part.numpy().copy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("d", [5, 1])
+def test_two_rank_gloo_reduce_and_allreduce(d):
+    world = 2
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(worker, args=(world, free_port(), d, results), nprocs=world, join=True)
+    rng = np.random.default_rng(123)
+    X = rng.integers(0, 7, size=(300, d)).astype(np.float32)
+    Z = rng.integers(-3, 4, size=(300, 4)).astype(np.float32)
+    whole = oracle.hist(X, Z, M=6).astype(np.float64)
+    (a0, b0, Yr0, Ya0, p0), (a1, b1, Yr1, Ya1, p1) = results[0], results[1]
+    assert (a0, b1) == (0, d) and b0 == a1
+    assert np.array_equal(Yr0, whole)                 # root holds the sum
+    assert np.array_equal(Ya0, whole) and np.array_equal(Ya1, whole)
+    assert np.array_equal(p0 + p1, whole)             # partials are the coordinate shares
+    if b0 > a0:
+        assert np.array_equal(p0, oracle.hist(X[:, a0:b0], Z, M=6).astype(np.float64))
+    else:
+        assert np.all(p0 == 0)                        # more ranks than coordinates
