@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -339,6 +340,7 @@ l1dm_status prepare_impl(const float *X, int64_t n, int64_t ld_x, int64_t k_begi
     if (P > 1) CUDA_TRY(valA.ensure(elems, false, s));
     const int64_t tiles = (n + kSortTile - 1) / kSortTile;
     CUDA_TRY(status.ensure((size_t)dl * tiles * 256, true, s));
+    static const bool fused_rank = getenv("L1DM_FUSED_RANK") != nullptr;  // tuning switch
     uint32_t *kb[2] = {keyA.p, keyB.p};
     uint32_t *vb[2] = {valA.p, valB.p};
     for (int i = 0; i < P; ++i) {
@@ -346,10 +348,14 @@ l1dm_status prepare_impl(const float *X, int64_t n, int64_t ld_x, int64_t k_begi
       CUDA_TRY(cudaMemsetAsync(ctrl.p + 2, 0, sizeof(unsigned), s));
       const uint32_t ep = h->epoch++;
       launch_sort_pass(i == 0, i == P - 1, kb[i & 1], vb[i & 1], kb[(i + 1) & 1], vb[(i + 1) & 1],
-                       h->rank.p, n, ldn, dl, 8 * p, dbase.p + (size_t)p * dl * 256, status.p, ep,
-                       ctrl.p + 2, ctrl.p + 1, s);
+                       fused_rank ? h->rank.p : nullptr, n, ldn, dl, 8 * p,
+                       dbase.p + (size_t)p * dl * 256, status.p, ep, ctrl.p + 2, ctrl.p + 1, s);
       h->kernel_launches++;
       CUDA_TRY(cudaGetLastError());
+    }
+    if (!fused_rank) {
+      launch_rank(vb[P & 1], h->rank.p, n, ldn, dl, s);
+      h->kernel_launches++;
     }
     const int fin = P & 1;
     DevBuf<uint32_t> *kbuf[2] = {&keyA, &keyB};
@@ -416,35 +422,36 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
   CUDA_TRY(h->flags.ensure(p.lb_slots, true, s));
   CUDA_TRY(h->agg.ensure(p.lb_slots * 2 * p.mb, false, s));
   CUDA_TRY(h->incl.ensure(p.lb_slots * 2 * p.mb, false, s));
-  CUDA_TRY(h->part.ensure((size_t)kColsumBlocks * 2 * m, false, s));
+  CUDA_TRY(h->part.ensure((size_t)h->dl * 2 * m, false, s));  // per-segment totals
   CUDA_TRY(h->Sg.ensure((size_t)2 * m, false, s));
-  CUDA_TRY(h->ctr.ensure((size_t)2 + p.chunks, true, s));
-  // K4: column sums (and reset of the per-chunk scan tickets)
-  {
-    TimedScope ts(h, kColsums, s);
-    launch_colsums(Z, ldz, h->n, m, h->hsum.p, h->part.p, h->Sg.p, h->ctr.p + 0, h->ctr.p + 2,
-                   (int)p.chunks, s);
-    h->kernel_launches++;
-    h->launches[kColsums]++;
+  if (h->ctr.count < (size_t)2 + p.chunks) {
+    CUDA_TRY(h->ctr.ensure((size_t)2 + p.chunks, true, s));  // tickets start at 0
   }
   for (int64_t c = 0; c < p.chunks; ++c) {
     const int64_t k_first = c * p.kc;
     const int64_t kcc = std::min<int64_t>(p.kc, h->dl - k_first);
+    const bool last = (c == p.chunks - 1);
     {
       TimedScope ts(h, kScan, s);
       const uint32_t ep = h->epoch++;
       if (h->epoch >= (1u << 30)) h->epoch = 1;
       launch_scan(p, h->perm.p, reinterpret_cast<const float *>(h->sval_bits.p), h->ldn, h->n, Z,
                   ldz, m, h->U.p, k_first, kcc, h->flags.p, h->agg.p, h->incl.p, ep,
-                  h->ctr.p + 2 + c, h->ctr.p + 1, s);
+                  h->ctr.p + 2 + c, h->ctr.p + 1, h->part.p, s);
       h->kernel_launches++;
       h->launches[kScan]++;
       if (h->timing) h->scan_pairs += h->n * kcc;
     }
+    if (last) {
+      TimedScope ts(h, kColsums, s);
+      launch_totals(h->part.p, h->dl, m, h->Sg.p, s);  // S, g from the segment totals
+      h->kernel_launches++;
+      h->launches[kColsums]++;
+    }
     {
       TimedScope ts(h, kAcc, s);
       launch_accumulate(p, h->rank.p, h->ldn, h->n, h->U.p, k_first, kcc, h->hsum.p, h->Sg.p, Y,
-                        ldy, m, c == 0, s);
+                        ldy, m, c == 0, last, h->ctr.p + 2 + c, s);
       h->kernel_launches++;
       h->launches[kAcc]++;
       if (h->timing) h->acc_pairs += h->n * kcc;

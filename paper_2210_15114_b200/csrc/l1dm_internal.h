@@ -33,6 +33,9 @@ void launch_sort_pass(bool first, bool last, const uint32_t *kin, const uint32_t
                       int64_t dl, int shift, const uint32_t *digit_base,
                       unsigned long long *status, uint32_t epoch, unsigned *ticket,
                       unsigned *timeout_flag, cudaStream_t s);
+// rank[k][perm[k][r]] = r, segment-major (K3; used when the last pass does not scatter it).
+void launch_rank(const uint32_t *perm, uint32_t *rank, int64_t n, int64_t ldn, int64_t dl,
+                 cudaStream_t s);
 // No pass needed (every digit constant in every segment): identity order.
 void launch_identity_emit(const uint32_t *key, float *sval, uint32_t *perm, uint32_t *rank,
                           int64_t n, int64_t ldn, int64_t dl, cudaStream_t s);
@@ -40,9 +43,14 @@ void launch_identity_emit(const uint32_t *key, float *sval, uint32_t *perm, uint
 // ---------------- query (Alg. 2) ----------------
 // Rows per thread in a scan tile (8 warps, VC columns per lane): the tile stages about
 // 96 KB of perm/sval/Z in shared memory, so two CTAs fit per SM.
+#ifndef L1DM_M1_ITEMS
+#define L1DM_M1_ITEMS 32
+#endif
 __host__ __device__ constexpr int scan_items(int lpr, int vc) {
-  return (98304 / (1024 * vc + 2048 / lpr)) / 4 * 4 > 64 ? 64
-                                                          : (98304 / (1024 * vc + 2048 / lpr)) / 4 * 4;
+  return lpr == 1 ? L1DM_M1_ITEMS
+                  : ((98304 / (1024 * vc + 2048 / lpr)) / 4 * 4 > 64
+                         ? 64
+                         : (98304 / (1024 * vc + 2048 / lpr)) / 4 * 4);
 }
 // Independent (coordinate, column block) scan segments the planner aims for per chunk.
 constexpr int64_t kScanTargetSegments = 0;
@@ -72,18 +80,15 @@ struct QueryPlan {
 bool make_plan(int64_t n, int64_t dl, int64_t m, int64_t l2_bytes, int64_t ws_limit,
                int vec_cap, QueryPlan *p);
 
-constexpr int kColsumBlocks = 592;  // 4 x 148 SMs; fixed so the reduction order is fixed
-
-void launch_colsums(const float *Z, int64_t ldz, int64_t n, int64_t m, const double *hsum,
-                    double *part, double *Sg, unsigned *done_ctr, unsigned *tickets,
-                    int ntickets, cudaStream_t s);
+// S and g from the scan's per-segment totals (segtot: dl x m x 2 doubles).
+void launch_totals(const double *segtot, int64_t dl, int64_t m, double *Sg, cudaStream_t s);
 void launch_scan(const QueryPlan &p, const uint32_t *perm, const float *sval, int64_t ldn,
                  int64_t n, const float *Z, int64_t ldz, int64_t m, double *U, int64_t k_first,
                  int64_t kcc, uint32_t *flags, double *agg, double *incl, uint32_t epoch,
-                 unsigned *ticket, unsigned *timeout_flag, cudaStream_t s);
+                 unsigned *ticket, unsigned *timeout_flag, double *segtot, cudaStream_t s);
 void launch_accumulate(const QueryPlan &p, const uint32_t *rank, int64_t ldn, int64_t n,
                        const double *U, int64_t k_first, int64_t kcc, const double *hsum,
                        const double *Sg, double *Y, int64_t ldy, int64_t m, bool first_chunk,
-                       cudaStream_t s);
+                       bool last_chunk, unsigned *ticket, cudaStream_t s);
 
 }  // namespace l1dm

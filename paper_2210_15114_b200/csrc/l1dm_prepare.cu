@@ -199,13 +199,13 @@ __global__ void __launch_bounds__(kSortThreads)
   unsigned long long *st = status + (seg * tiles_per_seg) * 256;
   uint64_t excl = 0;
   if (tile == 0) {
-    st_release_u64(&st[dgt], pack_status(kFlagInclusive, epoch, cnt));
+    st_relaxed_u64(&st[dgt], pack_status(kFlagInclusive, epoch, cnt));
   } else {
-    st_release_u64(&st[tile * 256 + dgt], pack_status(kFlagAggregate, epoch, cnt));
+    st_relaxed_u64(&st[tile * 256 + dgt], pack_status(kFlagAggregate, epoch, cnt));
     int64_t j = tile - 1;
     uint32_t spins = 0;
     for (;;) {
-      const unsigned long long sv = ld_acquire_u64(&st[j * 256 + dgt]);
+      const unsigned long long sv = ld_relaxed_u64(&st[j * 256 + dgt]);
       const uint32_t f = (uint32_t)(sv >> 62);
       const uint32_t ep = (uint32_t)(sv >> 32) & 0x3FFFFFFFu;
       if (ep != (epoch & 0x3FFFFFFFu) || f == kFlagInvalid) {
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(kSortThreads)
       if (f == kFlagInclusive) break;
       --j;
     }
-    st_release_u64(&st[tile * 256 + dgt], pack_status(kFlagInclusive, epoch,
+    st_relaxed_u64(&st[tile * 256 + dgt], pack_status(kFlagInclusive, epoch,
                                                       (uint32_t)(excl + cnt)));
   }
   s_gbase[dgt] = (uint64_t)digit_base[seg * 256 + dgt] + excl;
@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(kSortThreads)
     if (LAST) {
       kout[seg_off + gpos] = __float_as_uint(key_to_float(k));  // sval
       vout[seg_off + gpos] = v;                                 // perm
-      rank[seg_off + v] = (uint32_t)gpos;                       // rank = perm^-1 (K3 fused)
+      if (rank) rank[seg_off + v] = (uint32_t)gpos;             // rank = perm^-1 (K3 fused)
     } else {
       kout[seg_off + gpos] = k;
       vout[seg_off + gpos] = v;
@@ -290,6 +290,36 @@ void launch_sort_pass(bool first, bool last, const uint32_t *kin, const uint32_t
   else
     L1DM_PASS(false, false);
 #undef L1DM_PASS
+}
+
+// ------------------------------------------------------------------ K3 rank
+// rank[k][perm[k][r]] = r.  Blocks are segment-major (x fastest), so the 4n-byte rank row of
+// one coordinate is written while it is L2-resident and leaves L2 as whole sectors.
+constexpr int kRankRows = 4096;
+__global__ void __launch_bounds__(256)
+    k3_rank(const uint32_t *__restrict__ perm, uint32_t *__restrict__ rank, int64_t n,
+            int64_t ldn) {
+  const int64_t seg = blockIdx.y;
+  const int64_t r0 = (int64_t)blockIdx.x * kRankRows;
+  const uint32_t *pp = perm + seg * ldn;
+  uint32_t *rp = rank + seg * ldn;
+  for (int64_t r = r0 + 4 * threadIdx.x; r < r0 + kRankRows && r < n; r += 4 * 256) {
+    if (r + 4 <= n) {
+      const uint4 q = ld_stream_u4(pp + r);
+      rp[q.x] = (uint32_t)r;
+      rp[q.y] = (uint32_t)(r + 1);
+      rp[q.z] = (uint32_t)(r + 2);
+      rp[q.w] = (uint32_t)(r + 3);
+    } else {
+      for (int64_t u = r; u < n; ++u) rp[pp[u]] = (uint32_t)u;
+    }
+  }
+}
+
+void launch_rank(const uint32_t *perm, uint32_t *rank, int64_t n, int64_t ldn, int64_t dl,
+                 cudaStream_t s) {
+  dim3 grid((unsigned)((n + kRankRows - 1) / kRankRows), (unsigned)dl);
+  k3_rank<<<grid, 256, 0, s>>>(perm, rank, n, ldn);
 }
 
 // ------------------------------------------------------------------ identity emit

@@ -56,7 +56,7 @@ static void plan_sizes(QueryPlan &q, int64_t n, int64_t dl, int64_t m, int64_t l
   q.chunks = (dl + q.kc - 1) / q.kc;
   q.u_bytes = (size_t)q.kc * u_per_coord;
   q.lb_slots = (size_t)q.kc * slots_per_coord;
-  q.workspace_bytes = (size_t)q.kc * per_coord + (size_t)kColsumBlocks * 2 * m * sizeof(double) +
+  q.workspace_bytes = (size_t)q.kc * per_coord + (size_t)dl * 2 * m * sizeof(double) +
                       2 * m * sizeof(double);
 }
 
@@ -97,69 +97,22 @@ bool make_plan(int64_t n, int64_t dl, int64_t m, int64_t l2_bytes, int64_t ws_li
 }
 
 // ------------------------------------------------------------------ K4
-// grid (kColsumBlocks, ceil(m/CW)); thread t: column cy*CW + t%CW, row lane t/CW.
+// Query totals from the scan's segment totals: S_c = sum_j z_jc (coordinate 0's segment),
+// g_c = sum_k T_kc = sum_j h_j z_jc, summed over the shard's coordinates in fixed order.
 __global__ void __launch_bounds__(256)
-    k4_colsums(const float *__restrict__ Z, int64_t ldz, int64_t n, int64_t m,
-               const double *__restrict__ hsum, double *__restrict__ part, double *__restrict__ Sg,
-               unsigned *done_ctr, unsigned *tickets, int ntickets) {
-  __shared__ double s_s[256];
-  __shared__ double s_g[256];
-  __shared__ bool s_last;
-  const int tid = threadIdx.x;
-  const int CW = (int)(m < 256 ? m : 256);
-  const int RP = 256 / CW;
-  const int ro = tid / CW;
-  const int64_t c = (int64_t)blockIdx.y * CW + tid % CW;
-  const int64_t rows_per_block = (n + gridDim.x - 1) / gridDim.x;
-  const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
-  const int64_t r1 = (r0 + rows_per_block < n) ? r0 + rows_per_block : n;
-  double s = 0.0, g = 0.0;
-  if (ro < RP && c < m) {
-    for (int64_t r = r0 + ro; r < r1; r += RP) {
-      const double z = (double)Z[r * ldz + c];
-      s += z;
-      g = fma(hsum[r], z, g);
-    }
+    k4_totals(const double *__restrict__ segtot, int64_t dl, int64_t m, double *__restrict__ Sg) {
+  for (int64_t c = (int64_t)blockIdx.x * 256 + threadIdx.x; c < m; c += (int64_t)gridDim.x * 256) {
+    double g = 0.0;
+    for (int64_t k = 0; k < dl; ++k) g += segtot[k * 2 * m + 2 * c + 1];
+    Sg[c] = segtot[2 * c];
+    Sg[m + c] = g;
   }
-  s_s[tid] = s;
-  s_g[tid] = g;
-  __syncthreads();
-  if (ro == 0 && c < m) {
-    for (int q = 1; q < RP; ++q) {
-      s += s_s[q * CW + tid];
-      g += s_g[q * CW + tid];
-    }
-    part[(int64_t)blockIdx.x * 2 * m + c] = s;
-    part[(int64_t)blockIdx.x * 2 * m + m + c] = g;
-  }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) {
-    const unsigned total = gridDim.x * gridDim.y;
-    s_last = (atomicAdd(done_ctr, 1u) == total - 1);
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  for (int64_t cc = tid; cc < m; cc += 256) {
-    double S = 0.0, G = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) {
-      S += __ldcg(&part[(int64_t)b * 2 * m + cc]);
-      G += __ldcg(&part[(int64_t)b * 2 * m + m + cc]);
-    }
-    Sg[cc] = S;
-    Sg[m + cc] = G;
-  }
-  for (int t = tid; t < ntickets; t += 256) tickets[t] = 0u;
-  if (tid == 0) *done_ctr = 0u;
 }
 
-void launch_colsums(const float *Z, int64_t ldz, int64_t n, int64_t m, const double *hsum,
-                    double *part, double *Sg, unsigned *done_ctr, unsigned *tickets,
-                    int ntickets, cudaStream_t s) {
-  const int64_t CW = m < 256 ? m : 256;
-  dim3 grid(kColsumBlocks, (unsigned)((m + CW - 1) / CW));
-  k4_colsums<<<grid, 256, 0, s>>>(Z, ldz, n, m, hsum, part, Sg, done_ctr, tickets, ntickets);
+void launch_totals(const double *segtot, int64_t dl, int64_t m, double *Sg, cudaStream_t s) {
+  int64_t blocks = (m + 255) / 256;
+  if (blocks > 148) blocks = 148;
+  k4_totals<<<(unsigned)blocks, 256, 0, s>>>(segtot, dl, m, Sg);
 }
 
 // ------------------------------------------------------------------ K5
@@ -216,7 +169,8 @@ __global__ void __launch_bounds__(256, 2)
             int64_t n, const float *__restrict__ Z, int64_t ldz, int64_t m,
             double *__restrict__ U, int64_t ldu, int64_t k_first, int col_blocks, int64_t nseg,
             int64_t total, uint32_t *flags, double *agg, double *incl, uint32_t epoch,
-            unsigned *ticket, unsigned *timeout_flag, int64_t tiles_per_seg) {
+            unsigned *ticket, unsigned *timeout_flag, int64_t tiles_per_seg,
+            double *__restrict__ segtot) {
   constexpr int ITEMS = scan_items(LPR, VC);
   using C = ScanCfg<LPR, VC, ITEMS>;
   constexpr int MB = C::MB, RPW = C::RPW, ROWS_W = C::ROWS_W, R = C::R, NP = C::NP, NW = C::NW;
@@ -410,6 +364,12 @@ __global__ void __launch_bounds__(256, 2)
       st_release_u32(&flags[me], (epoch << 2) | kFlagInclusive);
     }
   }
+  // ---- the segment's totals (S = sum z, T_k = sum x z: Alg. 2's B_i[n], C_i[n])
+  // feed the epilogue g - h_i S with g = sum_k T_k, so no extra pass over Z.
+  if (tile == tiles_per_seg - 1 && tid < NP) {
+    const int64_t c = (int64_t)cb * MB + tid / 2;
+    if (c < m) segtot[(k_first + kk) * 2 * m + 2 * c + (tid & 1)] = s_excl[tid] + s_agg[tid];
+  }
   // ---- phase 2: exclusive prefixes P, Q along the rows, U_r = v_r P_r - Q_r
   double P[VC], Q[VC];
 #pragma unroll
@@ -453,7 +413,7 @@ static void launch_scan_t(const QueryPlan &p, const uint32_t *perm, const float 
                           int64_t ldn, int64_t n, const float *Z, int64_t ldz, int64_t m,
                           double *U, int64_t k_first, int64_t kcc, uint32_t *flags, double *agg,
                           double *incl, uint32_t epoch, unsigned *ticket, unsigned *timeout_flag,
-                          cudaStream_t s) {
+                          double *segtot, cudaStream_t s) {
   using C = ScanCfg<LPR, VC, scan_items(LPR, VC)>;
   auto kern = k5_scan<LPR, VC, CH>;
   static bool attr = false;
@@ -465,16 +425,16 @@ static void launch_scan_t(const QueryPlan &p, const uint32_t *perm, const float 
   const int64_t total = nseg * p.tiles_per_segment;
   kern<<<(unsigned)total, C::NT, C::SMEM, s>>>(perm, sval, ldn, n, Z, ldz, m, U, p.ldu, k_first,
                                                p.col_blocks, nseg, total, flags, agg, incl, epoch,
-                                               ticket, timeout_flag, p.tiles_per_segment);
+                                               ticket, timeout_flag, p.tiles_per_segment, segtot);
 }
 
 void launch_scan(const QueryPlan &p, const uint32_t *perm, const float *sval, int64_t ldn,
                  int64_t n, const float *Z, int64_t ldz, int64_t m, double *U, int64_t k_first,
                  int64_t kcc, uint32_t *flags, double *agg, double *incl, uint32_t epoch,
-                 unsigned *ticket, unsigned *timeout_flag, cudaStream_t s) {
+                 unsigned *ticket, unsigned *timeout_flag, double *segtot, cudaStream_t s) {
 #define L1DM_SCAN(L, V, CH)                                                                 \
   launch_scan_t<L, V, CH>(p, perm, sval, ldn, n, Z, ldz, m, U, k_first, kcc, flags, agg, incl, \
-                          epoch, ticket, timeout_flag, s)
+                          epoch, ticket, timeout_flag, segtot, s)
   // p.lpr lanes per row, p.mb / p.lpr columns per lane, p.vec floats per cp.async chunk
   const int vc = p.mb / p.lpr;
   switch (vc * 10000 + p.vec * 100 + p.lpr) {
@@ -521,8 +481,11 @@ __global__ void __launch_bounds__(256)
     k6_accumulate(const uint32_t *__restrict__ rank, int64_t ldn, int64_t n,
                   const double *__restrict__ U, int64_t ldu, int64_t k_first, int64_t kcc,
                   const double *__restrict__ hsum, const double *__restrict__ Sg,
-                  double *__restrict__ Y, int64_t ldy, int64_t m, int first_chunk) {
+                  double *__restrict__ Y, int64_t ldy, int64_t m, int first_chunk,
+                  int last_chunk, unsigned *ticket) {
   constexpr int PPW = 32 / LPP;
+  // the chunk's scan has completed (stream order): re-arm its ticket for the next query
+  if (ticket && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *ticket = 0u;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t i = (int64_t)blockIdx.x * (8 * PPW) + (int64_t)w * PPW + lane / LPP;
   const int64_t c0 = (int64_t)blockIdx.y * (LPP * V6) + (int64_t)(lane % LPP) * V6;
@@ -546,33 +509,40 @@ __global__ void __launch_bounds__(256)
     UVec<V6>::add(ub + kk * ustride + (int64_t)r * ldu, acc);
   }
   double *yp = Y + i * ldy + c0;
-  if (first_chunk) {
+  double val[V6];
+#pragma unroll
+  for (int q = 0; q < V6; ++q) val[q] = 2.0 * acc[q];
+  if (!first_chunk) {
+#pragma unroll
+    for (int q = 0; q < V6; ++q) val[q] += yp[q];
+  }
+  if (last_chunk) {
     const double hi = hsum[i];
 #pragma unroll
-    for (int q = 0; q < V6; ++q) yp[q] = 2.0 * acc[q] + fma(-hi, Sg[c0 + q], Sg[m + c0 + q]);
-  } else {
-#pragma unroll
-    for (int q = 0; q < V6; ++q) yp[q] = yp[q] + 2.0 * acc[q];
+    for (int q = 0; q < V6; ++q) val[q] += fma(-hi, Sg[c0 + q], Sg[m + c0 + q]);  // g - h_i S
   }
+#pragma unroll
+  for (int q = 0; q < V6; ++q) yp[q] = val[q];
 }
 
 template <int V6, int LPP>
 static void launch_acc_t(const QueryPlan &p, const uint32_t *rank, int64_t ldn, int64_t n,
                          const double *U, int64_t k_first, int64_t kcc, const double *hsum,
                          const double *Sg, double *Y, int64_t ldy, int64_t m, bool first,
-                         cudaStream_t s) {
+                         bool last, unsigned *ticket, cudaStream_t s) {
   constexpr int PPB = 8 * (32 / LPP);
   dim3 grid((unsigned)((n + PPB - 1) / PPB), (unsigned)p.col_groups);
   k6_accumulate<V6, LPP, 8><<<grid, 256, 0, s>>>(rank, ldn, n, U, p.ldu, k_first, kcc, hsum, Sg,
-                                                 Y, ldy, m, first ? 1 : 0);
+                                                 Y, ldy, m, first ? 1 : 0, last ? 1 : 0, ticket);
 }
 
 void launch_accumulate(const QueryPlan &p, const uint32_t *rank, int64_t ldn, int64_t n,
                        const double *U, int64_t k_first, int64_t kcc, const double *hsum,
                        const double *Sg, double *Y, int64_t ldy, int64_t m, bool first_chunk,
-                       cudaStream_t s) {
-#define L1DM_ACC(V, L) \
-  launch_acc_t<V, L>(p, rank, ldn, n, U, k_first, kcc, hsum, Sg, Y, ldy, m, first_chunk, s)
+                       bool last_chunk, unsigned *ticket, cudaStream_t s) {
+#define L1DM_ACC(V, L)                                                                   \
+  launch_acc_t<V, L>(p, rank, ldn, n, U, k_first, kcc, hsum, Sg, Y, ldy, m, first_chunk, \
+                     last_chunk, ticket, s)
   switch (p.v6 * 100 + p.lpp) {
     case 101: L1DM_ACC(1, 1); break;
     case 102: L1DM_ACC(1, 2); break;
