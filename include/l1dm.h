@@ -131,7 +131,8 @@ L1DM_API l1dm_status l1dm_set_workspace_limit(l1dm_handle h, size_t bytes);
 /* Query plan, a pure function of the sizes (testable without a GPU).
  * mb = columns per scan segment; rows_per_tile = scan tile rows; kc = coordinates
  * per chunk; chunks = ceil(d_local / kc); l2_resident = 1 when a chunk's U
- * workspace is sized to stay in L2 (small n*m). */
+ * workspace is sized to stay in L2 (small n*m); scatter = 1 when the query runs in
+ * small-m mode (m == 1 and Y fits L2: no U workspace, no rank gather). */
 typedef struct {
   int64_t mb;
   int64_t col_blocks;
@@ -143,6 +144,7 @@ typedef struct {
   int64_t chunks;
   int64_t l2_resident;
   int64_t workspace_bytes;
+  int64_t scatter;      /* 1: small-m mode, the scan adds 2U into an L2-resident Y with atomics */
 } l1dm_plan_t;
 L1DM_API l1dm_status l1dm_plan(int64_t n, int64_t d_local, int64_t m, int64_t l2_bytes,
                       int64_t workspace_limit, l1dm_plan_t *out);

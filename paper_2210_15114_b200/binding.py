@@ -42,7 +42,7 @@ class L1dmError(RuntimeError):
 class PlanT(ctypes.Structure):
     _fields_ = [(f, ctypes.c_int64) for f in (
         "mb", "col_blocks", "vec", "lanes_per_row", "rows_per_tile", "tiles_per_segment", "kc",
-        "chunks", "l2_resident", "workspace_bytes")]
+        "chunks", "l2_resident", "workspace_bytes", "scatter")]
 
 
 class TimingT(ctypes.Structure):

@@ -106,6 +106,7 @@ struct l1dm_ctx {
   DevBuf<uint32_t> flags;
   DevBuf<double> agg, incl;
   DevBuf<double> part, Sg;
+  DevBuf<float> zs;            // m == 1: gathered z in sorted order (reduce -> apply pass)
   DevBuf<unsigned> ctr;        // [0] colsum done counter, [1] timeout flag, [2..] scan tickets
   size_t ws_limit = 0;
   uint32_t epoch = 1;
@@ -213,6 +214,7 @@ void destroy(l1dm_ctx *h) {
   h->ctr.release();
   h->Zstage.release();
   h->Ystage.release();
+  h->zs.release();
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }
@@ -418,7 +420,8 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
   l1dm_status st = ensure_plan(h, m, vec_cap_for(Z, ldz));
   if (st != L1DM_OK) return st;
   const QueryPlan &p = h->plan;
-  CUDA_TRY(h->U.ensure((size_t)p.kc * (size_t)h->n * (size_t)p.ldu, false, s));
+  if (!p.scatter) CUDA_TRY(h->U.ensure((size_t)p.kc * (size_t)h->n * (size_t)p.ldu, false, s));
+  if (p.mb == 1) CUDA_TRY(h->zs.ensure((size_t)p.kc * (size_t)h->ldn, false, s));
   CUDA_TRY(h->flags.ensure(p.lb_slots, true, s));
   CUDA_TRY(h->agg.ensure(p.lb_slots * 2 * p.mb, false, s));
   CUDA_TRY(h->incl.ensure(p.lb_slots * 2 * p.mb, false, s));
@@ -427,7 +430,36 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
   if (h->ctr.count < (size_t)2 + p.chunks) {
     CUDA_TRY(h->ctr.ensure((size_t)2 + p.chunks, true, s));  // tickets start at 0
   }
-  for (int64_t c = 0; c < p.chunks; ++c) {
+  if (p.scatter) {
+    // small-m mode: zero Y, one scan launch over every coordinate adding 2U into Y, epilogue
+    CUDA_TRY(cudaMemset2DAsync(Y, (size_t)ldy * sizeof(double), 0, (size_t)m * sizeof(double),
+                               (size_t)h->n, s));
+    {
+      TimedScope ts(h, kScan, s);
+      const uint32_t ep = h->epoch++;
+      if (h->epoch >= (1u << 30)) h->epoch = 1;
+      launch_scan(p, h->perm.p, reinterpret_cast<const float *>(h->sval_bits.p), h->ldn, h->n, Z,
+                  ldz, m, Y, 0, h->dl, h->flags.p, h->agg.p, h->incl.p, ep, h->ctr.p + 2,
+                  h->ctr.p + 1, h->part.p, h->zs.p, s);
+      h->kernel_launches += (p.mb == 1) ? 3 : 1;  // m == 1: reduce, prefix, apply
+      h->launches[kScan]++;
+      if (h->timing) h->scan_pairs += h->n * h->dl;
+    }
+    {
+      TimedScope ts(h, kColsums, s);
+      launch_totals(h->part.p, h->dl, m, h->Sg.p, s);
+      h->kernel_launches++;
+      h->launches[kColsums]++;
+    }
+    {
+      TimedScope ts(h, kAcc, s);
+      launch_epilogue(h->hsum.p, h->Sg.p, Y, ldy, h->n, m, s);
+      h->kernel_launches++;
+      h->launches[kAcc]++;
+    }
+    CUDA_TRY(cudaMemsetAsync(h->ctr.p + 2, 0, sizeof(unsigned), s));  // re-arm the ticket
+  }
+  for (int64_t c = 0; !p.scatter && c < p.chunks; ++c) {
     const int64_t k_first = c * p.kc;
     const int64_t kcc = std::min<int64_t>(p.kc, h->dl - k_first);
     const bool last = (c == p.chunks - 1);
@@ -437,8 +469,8 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
       if (h->epoch >= (1u << 30)) h->epoch = 1;
       launch_scan(p, h->perm.p, reinterpret_cast<const float *>(h->sval_bits.p), h->ldn, h->n, Z,
                   ldz, m, h->U.p, k_first, kcc, h->flags.p, h->agg.p, h->incl.p, ep,
-                  h->ctr.p + 2 + c, h->ctr.p + 1, h->part.p, s);
-      h->kernel_launches++;
+                  h->ctr.p + 2 + c, h->ctr.p + 1, h->part.p, h->zs.p, s);
+      h->kernel_launches += (p.mb == 1) ? 3 : 1;  // m == 1: reduce, prefix, apply
       h->launches[kScan]++;
       if (h->timing) h->scan_pairs += h->n * kcc;
     }
@@ -620,6 +652,7 @@ l1dm_status l1dm_plan(int64_t n, int64_t d_local, int64_t m, int64_t l2_bytes,
   out->chunks = p.chunks;
   out->l2_resident = p.l2_resident;
   out->workspace_bytes = (int64_t)p.workspace_bytes;
+  out->scatter = p.scatter;
   return L1DM_OK;
 }
 

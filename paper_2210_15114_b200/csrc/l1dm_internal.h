@@ -47,7 +47,7 @@ void launch_identity_emit(const uint32_t *key, float *sval, uint32_t *perm, uint
 #define L1DM_M1_ITEMS 32
 #endif
 __host__ __device__ constexpr int scan_items(int lpr, int vc) {
-  return lpr == 1 ? L1DM_M1_ITEMS
+  return (lpr == 1 && vc == 1) ? 16 : lpr == 1 ? L1DM_M1_ITEMS
                   : ((98304 / (1024 * vc + 2048 / lpr)) / 4 * 4 > 64
                          ? 64
                          : (98304 / (1024 * vc + 2048 / lpr)) / 4 * 4);
@@ -66,6 +66,7 @@ struct QueryPlan {
   int64_t kc;         // coordinates per chunk
   int64_t chunks;
   int l2_resident;
+  int scatter;        // 1: scan adds 2U into Y with L2 atomics (small m); 0: U + rank gather
   int64_t ldu;        // U row length (doubles) = m
   size_t u_bytes;     // kc * n * ldu * 8
   size_t lb_slots;    // kc * col_blocks * tiles_per_segment
@@ -80,12 +81,17 @@ struct QueryPlan {
 bool make_plan(int64_t n, int64_t dl, int64_t m, int64_t l2_bytes, int64_t ws_limit,
                int vec_cap, QueryPlan *p);
 
+// Scatter mode: Y[i][c] += g_c - h_i S_c.
+void launch_epilogue(const double *hsum, const double *Sg, double *Y, int64_t ldy, int64_t n,
+                     int64_t m, cudaStream_t s);
 // S and g from the scan's per-segment totals (segtot: dl x m x 2 doubles).
 void launch_totals(const double *segtot, int64_t dl, int64_t m, double *Sg, cudaStream_t s);
 void launch_scan(const QueryPlan &p, const uint32_t *perm, const float *sval, int64_t ldn,
                  int64_t n, const float *Z, int64_t ldz, int64_t m, double *U, int64_t k_first,
                  int64_t kcc, uint32_t *flags, double *agg, double *incl, uint32_t epoch,
-                 unsigned *ticket, unsigned *timeout_flag, double *segtot, cudaStream_t s);
+                 unsigned *ticket, unsigned *timeout_flag, double *segtot, float *zs,
+                 cudaStream_t s);
+// (zs: m == 1 only, kc x ldn floats: z in sorted order between the reduce and apply passes)
 void launch_accumulate(const QueryPlan &p, const uint32_t *rank, int64_t ldn, int64_t n,
                        const double *U, int64_t k_first, int64_t kcc, const double *hsum,
                        const double *Sg, double *Y, int64_t ldy, int64_t m, bool first_chunk,

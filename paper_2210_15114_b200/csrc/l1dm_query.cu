@@ -42,7 +42,8 @@ static void plan_sizes(QueryPlan &q, int64_t n, int64_t dl, int64_t m, int64_t l
   const size_t u_per_coord = (size_t)n * (size_t)q.ldu * sizeof(double);
   const size_t slots_per_coord = (size_t)q.col_blocks * (size_t)q.tiles_per_segment;
   const size_t lb_per_coord = slots_per_coord * (sizeof(uint32_t) + 2 * 2 * q.mb * sizeof(double));
-  const size_t per_coord = u_per_coord + lb_per_coord;
+  const size_t zs_per_coord = (q.mb == 1) ? (size_t)n * sizeof(float) : 0;  // m == 1 staging
+  const size_t per_coord = u_per_coord + lb_per_coord + zs_per_coord;
   if (l2_bytes > 0 && (int64_t)(4 * per_coord) <= l2_bytes) {
     // small n*m: size each chunk's workspace to stay resident in L2 between K5 and K6
     q.l2_resident = 1;
@@ -87,6 +88,24 @@ bool make_plan(int64_t n, int64_t dl, int64_t m, int64_t l2_bytes, int64_t ws_li
     if (q.vc == 2) q.vc = 1; else q.lpr /= 2;
     q.vec = pick_vec(q.lpr * q.vc);
     plan_sizes(q, n, dl, m, l2_bytes, ws_limit);
+  }
+  // Small-m mode: for m == 1 with an L2-resident Y the scan adds 2U straight into Y with L2
+  // atomics (one pass, no U workspace, no rank gather).  L1DM_SCATTER=0/1 overrides.
+  static const int scatter_env = [] {
+    const char *e = getenv("L1DM_SCATTER");
+    return e ? atoi(e) : -1;
+  }();
+  q.scatter = scatter_env >= 0 ? scatter_env
+                               : (m == 1 && l2_bytes > 0 && n * m * 8 * 2 <= l2_bytes) ? 1 : 0;
+  if (q.scatter) {
+    q.kc = dl;  // every coordinate in one launch: nothing to hold between scan and accumulate
+    q.chunks = 1;
+    q.l2_resident = 1;
+    q.u_bytes = 0;
+    q.lb_slots = (size_t)dl * q.col_blocks * q.tiles_per_segment;
+    q.workspace_bytes = q.lb_slots * (sizeof(uint32_t) + 2 * 2 * q.mb * sizeof(double)) +
+                        (size_t)dl * n * sizeof(float) + (size_t)dl * 2 * m * sizeof(double) +
+                        2 * m * sizeof(double);
   }
   q.v6 = (m % 2 == 0) ? 2 : 1;
   int64_t lanes = (m + q.v6 - 1) / q.v6;
@@ -163,7 +182,9 @@ struct ScanCfg {
 };
 
 
-template <int LPR, int VC, int CH>
+// SCATTER: instead of storing U in sorted order, add 2 U_r straight into Y[perm[r]] with L2
+// atomics (small-m mode: Y is L2-resident; no U round trip, no rank gather — DESIGN.md §6).
+template <int LPR, int VC, int CH, bool SCATTER>
 __global__ void __launch_bounds__(256, 2)
     k5_scan(const uint32_t *__restrict__ perm, const float *__restrict__ sval, int64_t ldn,
             int64_t n, const float *__restrict__ Z, int64_t ldz, int64_t m,
@@ -378,7 +399,7 @@ __global__ void __launch_bounds__(256, 2)
     P[q] = s_excl[c2] + s_wt[w * NP + c2];
     Q[q] = s_excl[c2 + 1] + s_wt[w * NP + c2 + 1];
   }
-  double *ub = U + kk * n * ldu + (row0 + rbase) * ldu + col;
+  double *ub = SCATTER ? U + col : U + kk * n * ldu + (row0 + rbase) * ldu + col;
 #pragma unroll 4
   for (int j = 0; j < ITEMS; ++j) {
     const int r = rbase + j * RPW;
@@ -404,21 +425,207 @@ __global__ void __launch_bounds__(256, 2)
       P[q] += __shfl_sync(0xFFFFFFFFu, a, (RPW - 1) * LPR + cl);
       Q[q] += __shfl_sync(0xFFFFFFFFu, b, (RPW - 1) * LPR + cl);
     }
-    if (col_ok && r < nrows) stcs_cols<VC>(ub + (int64_t)j * RPW * ldu, u);
+    if (col_ok && r < nrows) {
+      if constexpr (SCATTER) {
+        double *yp = ub + (int64_t)pb[r] * ldu;
+#pragma unroll
+        for (int q = 0; q < VC; ++q) atomicAdd(yp + q, 2.0 * u[q]);
+      } else {
+        stcs_cols<VC>(ub + (int64_t)j * RPW * ldu, u);
+      }
+    }
+  }
+}
+
+// Single-column variant (m == 1).  Here a tile is cheap (4 B of Z per row, gathered from
+// L2) and the decoupled look-back's latency dominates, so the scan is done as
+// reduce-then-scan with no inter-CTA waits at all:
+//   M1_REDUCE  per tile: (sum z, sum v z)                         -> m1agg[seg][tile]
+//   k5_m1_prefix  per segment: exclusive scan over its tiles       -> m1agg (in place), segtot
+//   M1_APPLY   per tile: U along the rows from the tile's prefix, stored (sorted order)
+//              or, in scatter mode, added as 2U into Y[perm[r]] with L2 atomics.
+// Each thread owns ITEMS *consecutive* sorted rows (thread-sequential scan, one warp scan per
+// tile); shared-memory rows are padded (4 floats every 32) so its 128-bit reads are
+// bank-conflict free.
+constexpr int kM1Items = 16;
+constexpr int kM1Rows = 256 * kM1Items;  // rows per tile
+__device__ __forceinline__ int m1_pad(int r) { return r + (r >> 5) * 4; }
+
+enum { M1_REDUCE = 0, M1_APPLY_STORE = 1, M1_APPLY_SCATTER = 2 };
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 4)
+    k5_scan_m1(const uint32_t *__restrict__ perm, const float *__restrict__ sval, int64_t ldn,
+               int64_t n, const float *__restrict__ Z, int64_t ldz, double *__restrict__ U,
+               int64_t ldu, int64_t k_first, int64_t nseg, int64_t tiles_per_seg,
+               double *__restrict__ m1agg, float *__restrict__ zs) {
+  constexpr int ITEMS = kM1Items, R = kM1Rows, NW = 8;
+  constexpr int RP = R + R / 8;  // padded length
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float *zb = reinterpret_cast<float *>(smem_raw);     // [RP]
+  float *vb = zb + RP;                                  // [RP]
+  uint32_t *pb = reinterpret_cast<uint32_t *>(vb + RP);  // [RP]
+  __shared__ double s_w[NW][2];
+
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t t = blockIdx.x;  // tiles are independent: no ticket, no waiting
+  const int64_t tile = t / nseg;
+  const int64_t seg = t - tile * nseg;  // local coordinate
+  const int64_t row0 = tile * R;
+  const int64_t nrows = (n - row0 < R) ? (n - row0) : R;
+  float *zsp = zs + seg * ldn + row0;  // z in sorted order, written by the reduce pass
+  {
+    const uint32_t *pp = perm + (k_first + seg) * ldn + row0;
+    const float *vp = sval + (k_first + seg) * ldn + row0;
+    for (int c = tid; c < R / 4; c += 256) {
+      const bool ok = row0 + 4 * c < ldn;
+      if (MODE == M1_REDUCE || MODE == M1_APPLY_SCATTER)
+        cp_async<16>(pb + m1_pad(4 * c), ok ? (const void *)(pp + 4 * c) : (const void *)perm, ok);
+      cp_async<16>(vb + m1_pad(4 * c), ok ? (const void *)(vp + 4 * c) : (const void *)sval, ok);
+      if (MODE != M1_REDUCE)  // the apply pass streams z back in sorted order: no second gather
+        cp_async<16>(zb + m1_pad(4 * c), ok ? (const void *)(zsp + 4 * c) : (const void *)zs, ok);
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    if constexpr (MODE == M1_REDUCE) {
+      for (int r = tid; r < R; r += 256) {  // gather z into sorted order
+        const bool ok = r < nrows;
+        cp_async<4>(zb + m1_pad(r), ok ? (const void *)(Z + (int64_t)pb[m1_pad(r)] * ldz) : Z, ok);
+      }
+      cp_async_commit();
+      cp_async_wait_all();
+      __syncthreads();
+      for (int c = tid; c < R / 4; c += 256)  // keep it for the apply pass (coalesced)
+        if (row0 + 4 * c < ldn)
+          __stcg(reinterpret_cast<float4 *>(zsp + 4 * c),
+                 *reinterpret_cast<const float4 *>(zb + m1_pad(4 * c)));
+    }
+  }
+  const int rl0 = tid * ITEMS;  // this thread's first row
+  const int b0 = m1_pad(rl0);   // padded start (16 rows never straddle a 32-row group)
+  const int nmine = (int)(nrows - rl0 < ITEMS ? (nrows - rl0 < 0 ? 0 : nrows - rl0) : ITEMS);
+  double os = 0.0, ot = 0.0;
+#pragma unroll
+  for (int q = 0; q < ITEMS / 4; ++q) {
+    const float4 a = *reinterpret_cast<const float4 *>(zb + b0 + 4 * q);
+    const float4 b = *reinterpret_cast<const float4 *>(vb + b0 + 4 * q);
+    const float zz[4] = {a.x, a.y, a.z, a.w}, vv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {  // padding rows: z is zero-filled
+      os += (double)zz[u];
+      ot = fma(4 * q + u < nmine ? (double)vv[u] : 0.0, (double)zz[u], ot);
+    }
+  }
+  double ps = os, pt = ot;  // warp inclusive scan of the thread totals
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const double a = __shfl_up_sync(0xFFFFFFFFu, ps, off);
+    const double b = __shfl_up_sync(0xFFFFFFFFu, pt, off);
+    if (lane >= off) {
+      ps += a;
+      pt += b;
+    }
+  }
+  if (lane == 31) {
+    s_w[w][0] = ps;
+    s_w[w][1] = pt;
+  }
+  __syncthreads();
+  double *ag = m1agg + (seg * tiles_per_seg + tile) * 2;
+  if constexpr (MODE == M1_REDUCE) {
+    if (tid < 2) {
+      double run = 0.0;
+#pragma unroll
+      for (int ww = 0; ww < NW; ++ww) run += s_w[ww][tid];
+      ag[tid] = run;
+    }
+    return;
+  } else {
+    // exclusive prefix of this thread's first row: tile prefix + earlier warps + earlier lanes
+    double P = __ldg(ag) + ps - os, Q = __ldg(ag + 1) + pt - ot;
+    for (int ww = 0; ww < w; ++ww) {
+      P += s_w[ww][0];
+      Q += s_w[ww][1];
+    }
+    double *up = U + seg * n * ldu + (row0 + rl0) * ldu;  // store mode: this thread's U rows
+#pragma unroll
+    for (int q = 0; q < ITEMS / 4; ++q) {
+      const float4 a = *reinterpret_cast<const float4 *>(zb + b0 + 4 * q);
+      const float4 b = *reinterpret_cast<const float4 *>(vb + b0 + 4 * q);
+      const uint4 c = *reinterpret_cast<const uint4 *>(pb + b0 + 4 * q);
+      const float zz[4] = {a.x, a.y, a.z, a.w}, vv[4] = {b.x, b.y, b.z, b.w};
+      const uint32_t pr[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = 4 * q + u;
+        const double vj = j < nmine ? (double)vv[u] : 0.0, sz = (double)zz[u];
+        const double uu = fma(vj, P, -Q);  // U_r = v_r P_r - Q_r
+        P += sz;
+        Q = fma(vj, sz, Q);
+        if (j < nmine) {
+          if constexpr (MODE == M1_APPLY_SCATTER) {
+            atomicAdd(U + (int64_t)pr[u] * ldu, 2.0 * uu);
+          } else {
+            __stcs(up + (int64_t)j * ldu, uu);
+          }
+        }
+      }
+    }
+  }
+}
+
+// Exclusive scan of each segment's tile aggregates (one warp per segment, in place), and the
+// segment totals for the epilogue.
+__global__ void __launch_bounds__(256)
+    k5_m1_prefix(double *__restrict__ m1agg, int64_t nseg, int64_t tiles_per_seg, int64_t k_first,
+                 double *__restrict__ segtot) {
+  const int lane = threadIdx.x & 31;
+  const int64_t seg = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (seg >= nseg) return;
+  double *ag = m1agg + seg * tiles_per_seg * 2;
+  double cs = 0.0, ct = 0.0;
+  for (int64_t base = 0; base < tiles_per_seg; base += 32) {
+    const int64_t j = base + lane;
+    const double s = j < tiles_per_seg ? ag[2 * j] : 0.0;
+    const double t = j < tiles_per_seg ? ag[2 * j + 1] : 0.0;
+    double a = s, b = t;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const double a2 = __shfl_up_sync(0xFFFFFFFFu, a, off);
+      const double b2 = __shfl_up_sync(0xFFFFFFFFu, b, off);
+      if (lane >= off) {
+        a += a2;
+        b += b2;
+      }
+    }
+    if (j < tiles_per_seg) {
+      ag[2 * j] = cs + a - s;
+      ag[2 * j + 1] = ct + b - t;
+    }
+    cs += __shfl_sync(0xFFFFFFFFu, a, 31);
+    ct += __shfl_sync(0xFFFFFFFFu, b, 31);
+  }
+  if (lane == 0) {
+    segtot[(k_first + seg) * 2] = cs;
+    segtot[(k_first + seg) * 2 + 1] = ct;
   }
 }
 
 template <int LPR, int VC, int CH>
-static void launch_scan_t(const QueryPlan &p, const uint32_t *perm, const float *sval,
+static void launch_scan_t(const QueryPlan &p, bool scatter, const uint32_t *perm, const float *sval,
                           int64_t ldn, int64_t n, const float *Z, int64_t ldz, int64_t m,
                           double *U, int64_t k_first, int64_t kcc, uint32_t *flags, double *agg,
                           double *incl, uint32_t epoch, unsigned *ticket, unsigned *timeout_flag,
                           double *segtot, cudaStream_t s) {
   using C = ScanCfg<LPR, VC, scan_items(LPR, VC)>;
-  auto kern = k5_scan<LPR, VC, CH>;
+  auto kern = scatter ? k5_scan<LPR, VC, CH, true> : k5_scan<LPR, VC, CH, false>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    cudaFuncSetAttribute(k5_scan<LPR, VC, CH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)C::SMEM);
+    cudaFuncSetAttribute(k5_scan<LPR, VC, CH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)C::SMEM);
     attr = true;
   }
   const int64_t nseg = kcc * p.col_blocks;
@@ -431,11 +638,41 @@ static void launch_scan_t(const QueryPlan &p, const uint32_t *perm, const float 
 void launch_scan(const QueryPlan &p, const uint32_t *perm, const float *sval, int64_t ldn,
                  int64_t n, const float *Z, int64_t ldz, int64_t m, double *U, int64_t k_first,
                  int64_t kcc, uint32_t *flags, double *agg, double *incl, uint32_t epoch,
-                 unsigned *ticket, unsigned *timeout_flag, double *segtot, cudaStream_t s) {
-#define L1DM_SCAN(L, V, CH)                                                                 \
-  launch_scan_t<L, V, CH>(p, perm, sval, ldn, n, Z, ldz, m, U, k_first, kcc, flags, agg, incl, \
-                          epoch, ticket, timeout_flag, segtot, s)
+                 unsigned *ticket, unsigned *timeout_flag, double *segtot, float *zs,
+                 cudaStream_t s) {
+#define L1DM_SCAN(L, V, CH)                                                                    \
+  launch_scan_t<L, V, CH>(p, p.scatter != 0, perm, sval, ldn, n, Z, ldz, m, U, k_first, kcc, flags, \
+                          agg, incl, epoch, ticket, timeout_flag, segtot, s)
   // p.lpr lanes per row, p.mb / p.lpr columns per lane, p.vec floats per cp.async chunk
+  if (p.mb == 1) {
+    // reduce-then-scan, no look-back (the agg workspace holds 2 doubles per tile)
+    const size_t smem = (size_t)(kM1Rows + kM1Rows / 8) * 4 * 3;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k5_scan_m1<M1_REDUCE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      cudaFuncSetAttribute(k5_scan_m1<M1_APPLY_STORE>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k5_scan_m1<M1_APPLY_SCATTER>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    const int64_t nseg = kcc;
+    const int64_t total = nseg * p.tiles_per_segment;
+    k5_scan_m1<M1_REDUCE><<<(unsigned)total, 256, smem, s>>>(
+        perm, sval, ldn, n, Z, ldz, U, p.ldu, k_first, nseg, p.tiles_per_segment, agg, zs);
+    k5_m1_prefix<<<(unsigned)((nseg + 7) / 8), 256, 0, s>>>(agg, nseg, p.tiles_per_segment,
+                                                             k_first, segtot);
+    auto kern = p.scatter ? k5_scan_m1<M1_APPLY_SCATTER> : k5_scan_m1<M1_APPLY_STORE>;
+    kern<<<(unsigned)total, 256, smem, s>>>(perm, sval, ldn, n, Z, ldz, U, p.ldu, k_first, nseg,
+                                            p.tiles_per_segment, agg, zs);
+    (void)flags;
+    (void)incl;
+    (void)epoch;
+    (void)ticket;
+    (void)timeout_flag;
+    return;
+  }
   const int vc = p.mb / p.lpr;
   switch (vc * 10000 + p.vec * 100 + p.lpr) {
     case 10101: L1DM_SCAN(1, 1, 4); break;
@@ -458,6 +695,26 @@ void launch_scan(const QueryPlan &p, const uint32_t *perm, const float *sval, in
     default: break;
   }
 #undef L1DM_SCAN
+}
+
+// ------------------------------------------------------------------ scatter-mode epilogue
+// Y[i][c] += g_c - h_i S_c after the scatter scans (Y was zeroed before them).
+__global__ void __launch_bounds__(256)
+    k7_epilogue(const double *__restrict__ hsum, const double *__restrict__ Sg,
+                double *__restrict__ Y, int64_t ldy, int64_t n, int64_t m) {
+  const int64_t total = n * m;
+  for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * 256) {
+    const int64_t i = e / m, c = e - (e / m) * m;
+    Y[i * ldy + c] += fma(-hsum[i], Sg[c], Sg[m + c]);
+  }
+}
+
+void launch_epilogue(const double *hsum, const double *Sg, double *Y, int64_t ldy, int64_t n,
+                     int64_t m, cudaStream_t s) {
+  int64_t blocks = (n * m + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k7_epilogue<<<(unsigned)blocks, 256, 0, s>>>(hsum, Sg, Y, ldy, n, m);
 }
 
 // ------------------------------------------------------------------ K6

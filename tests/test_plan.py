@@ -7,6 +7,8 @@ L2 = 126 << 20
 
 
 def scan_items(lpr, vc):
+    if lpr == 1 and vc == 1:
+        return 16                      # the single-column kernel: 16 consecutive rows per thread
     it = (98304 // (1024 * vc + 2048 // lpr)) // 4 * 4
     return min(it, 64)
 
@@ -26,10 +28,17 @@ def test_lane_mapping(m, vec, lpr, mb):
 
 
 def test_small_problem_is_l2_resident_and_chunked():
-    p = l1.l1dm_plan(1 << 20, 64, 1, L2, 64 << 30)
-    assert p["l2_resident"] == 1
-    assert p["kc"] * (1 << 20) * 8 <= 0.4 * L2
+    p = l1.l1dm_plan(1 << 20, 64, 2, L2, 64 << 30)
+    assert p["l2_resident"] == 1 and p["scatter"] == 0
+    assert p["kc"] * (1 << 20) * 2 * 8 <= 0.4 * L2
     assert p["chunks"] == -(-64 // p["kc"])
+
+
+def test_single_column_small_n_uses_scatter_mode():
+    p = l1.l1dm_plan(1 << 20, 64, 1, L2, 64 << 30)
+    assert p["scatter"] == 1 and p["chunks"] == 1 and p["kc"] == 64
+    p = l1.l1dm_plan(1 << 24, 64, 1, L2, 64 << 30)   # Y (128 MiB) does not fit L2
+    assert p["scatter"] == 0
 
 
 def test_large_problem_uses_hbm_workspace():
