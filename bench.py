@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--reduce", default="reduce", choices=["reduce", "allreduce"])
+    ap.add_argument("--overlap-blocks", type=int, default=4,
+                    help="N>1: point blocks whose reduce overlaps the remaining accumulate")
     return ap.parse_args()
 
 
@@ -210,7 +212,8 @@ def main_ours(args):
         if timing and sh.handle is not None:
             l1.l1dm_timing_enable(sh.handle, True)
         for q in range(Q):
-            sh.matvec(Zs[q % len(Zs)], Y, root=None if args.reduce == "allreduce" else 0)
+            sh.matvec(Zs[q % len(Zs)], Y, root=None if args.reduce == "allreduce" else 0,
+                      overlap_blocks=args.overlap_blocks)
         return sh
 
     for _ in range(args.warmup):
@@ -287,6 +290,7 @@ def main_ours(args):
         "config": {"workload": args.workload, "n": n, "d": d, "m": m, "queries_per_step": Q,
                    "fresh_queries": w.fresh_queries, "parallelism": f"coord-shard x{world}",
                    "collective": (args.reduce if world > 1 else None),
+                   "overlap_blocks": (args.overlap_blocks if world > 1 else None),
                    "l2": "inputs > L2 (prepared state 12*n*d B), no flush"},
         "gpu_launches": int(agg.get("kernel_launches", 0)),
         "prepare_ms": prep_ms,

@@ -103,6 +103,16 @@ L1DM_API l1dm_status l1dm_matvec(l1dm_handle h, const float *Z, int64_t m, doubl
 L1DM_API l1dm_status l1dm_matvec_ex(l1dm_handle h, const float *Z, int64_t ld_z, int64_t m, double *Y,
                            int64_t ld_y, void *stream);
 
+/* As l1dm_matvec_ex (device Z and Y only), for overlapping the cross-GPU sum of Y with the
+ * query: the pass that completes Y (the last accumulate) runs per contiguous point block
+ * b = 0..point_blocks-1 (rows [floor(b n / B), floor((b+1) n / B))), and block_events[b]
+ * (a cudaEvent_t created by the caller; NULL entries are skipped) is recorded on `stream`
+ * right after block b's rows of Y are final.  Errors as l1dm_matvec_ex, and EINVAL for
+ * point_blocks < 1 or > n. */
+L1DM_API l1dm_status l1dm_matvec_pipelined(l1dm_handle h, const float *Z, int64_t ld_z, int64_t m,
+                                           double *Y, int64_t ld_y, void *stream,
+                                           int64_t point_blocks, void *const *block_events);
+
 /* Release every buffer the handle owns.  NULL is a no-op.  Synchronises the
  * handle's stream first. */
 L1DM_API void l1dm_free(l1dm_handle h);

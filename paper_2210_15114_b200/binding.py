@@ -25,7 +25,8 @@ STATUS = {
 }
 
 EXPORTS = [
-    "l1dm_prepare", "l1dm_prepare_ex", "l1dm_matvec", "l1dm_matvec_ex", "l1dm_free", "l1dm_sync",
+    "l1dm_prepare", "l1dm_prepare_ex", "l1dm_matvec", "l1dm_matvec_ex", "l1dm_matvec_pipelined",
+    "l1dm_free", "l1dm_sync",
     "l1dm_shape", "l1dm_workspace_bytes", "l1dm_set_workspace_limit", "l1dm_plan",
     "l1dm_timing_enable", "l1dm_timing_read", "l1dm_debug_export", "l1dm_last_error",
     "l1dm_version",
@@ -74,6 +75,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.l1dm_prepare_ex.argtypes = [vp, i64, i64, i64, i64, vp, ctypes.POINTER(vp)]
     lib.l1dm_matvec.argtypes = [vp, vp, i64, vp]
     lib.l1dm_matvec_ex.argtypes = [vp, vp, i64, i64, vp, i64, vp]
+    lib.l1dm_matvec_pipelined.argtypes = [vp, vp, i64, i64, vp, i64, vp, i64,
+                                           ctypes.POINTER(vp)]
     lib.l1dm_free.argtypes = [vp]
     lib.l1dm_free.restype = None
     lib.l1dm_sync.argtypes = [vp]
@@ -89,7 +92,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.l1dm_last_error.restype = ctypes.c_char_p
     lib.l1dm_version.argtypes = []
     lib.l1dm_version.restype = ctypes.c_char_p
-    for name in ("l1dm_prepare", "l1dm_prepare_ex", "l1dm_matvec", "l1dm_matvec_ex", "l1dm_sync",
+    for name in ("l1dm_prepare", "l1dm_prepare_ex", "l1dm_matvec", "l1dm_matvec_ex",
+                 "l1dm_matvec_pipelined", "l1dm_sync",
                  "l1dm_shape", "l1dm_set_workspace_limit", "l1dm_plan", "l1dm_timing_enable",
                  "l1dm_timing_read", "l1dm_debug_export"):
         getattr(lib, name).restype = st
@@ -194,6 +198,35 @@ def l1dm_matvec(h: Handle, Z, Y=None, stream=None):
                                 _stream_of(Z, stream))
     _check(rc, "l1dm_matvec")
     return Y.view(-1) if squeeze else Y
+
+
+def point_blocks(n: int, nblocks: int):
+    """Row ranges [floor(b n / B), floor((b+1) n / B)) used by l1dm_matvec_pipelined."""
+    return [((n * b) // nblocks, (n * (b + 1)) // nblocks) for b in range(nblocks)]
+
+
+def l1dm_matvec_pipelined(h: Handle, Z: torch.Tensor, Y: torch.Tensor, events, stream=None):
+    """As l1dm_matvec (CUDA tensors), recording events[b] once rows point_blocks(n, B)[b]
+    of Y are final, so a collective on those rows can start while the rest is computed."""
+    lib = load_library()
+    Z = _as_f32_2d(Z, "Z")
+    m = Z.shape[1]
+    if not (Z.is_cuda and Y.is_cuda):
+        raise ValueError("l1dm_matvec_pipelined needs CUDA tensors")
+    if Y.dtype != torch.float64 or Y.shape != (h.n, m) or Y.stride(1) != 1:
+        raise ValueError("Y must be an n x m float64 row-major tensor")
+    st = _stream_of(Z, stream)
+    handles = []
+    for e in events:
+        if e.cuda_event == 0:  # torch creates the CUDA event lazily, on first record
+            e.record(torch.cuda.current_stream(Z.device) if stream is None else stream)
+        handles.append(ctypes.c_void_p(e.cuda_event))
+    arr = (ctypes.c_void_p * len(handles))(*handles)
+    with torch.cuda.device(Z.device):
+        rc = lib.l1dm_matvec_pipelined(h.ptr, _ptr(Z), Z.stride(0), m, _ptr(Y), Y.stride(0), st,
+                                       len(handles), arr)
+    _check(rc, "l1dm_matvec_pipelined")
+    return Y
 
 
 def l1dm_free(h: Handle):

@@ -415,8 +415,16 @@ l1dm_status ensure_plan(l1dm_ctx *h, int64_t m, int vec_cap) {
   return L1DM_OK;
 }
 
+// nblocks/events: the pass that completes Y (the last chunk's accumulate, or the scatter-mode
+// epilogue) is launched per contiguous point block, and events[b] is recorded after block b.
 l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, double *Y,
-                          int64_t ldy, cudaStream_t s) {
+                          int64_t ldy, cudaStream_t s, int64_t nblocks = 1,
+                          void *const *events = nullptr) {
+  if (nblocks < 1) nblocks = 1;
+  auto block_range = [&](int64_t b, int64_t &i0, int64_t &i1) {
+    i0 = (h->n * b) / nblocks;
+    i1 = (h->n * (b + 1)) / nblocks;
+  };
   l1dm_status st = ensure_plan(h, m, vec_cap_for(Z, ldz));
   if (st != L1DM_OK) return st;
   const QueryPlan &p = h->plan;
@@ -453,8 +461,13 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
     }
     {
       TimedScope ts(h, kAcc, s);
-      launch_epilogue(h->hsum.p, h->Sg.p, Y, ldy, h->n, m, s);
-      h->kernel_launches++;
+      for (int64_t b = 0; b < nblocks; ++b) {
+        int64_t i0, i1;
+        block_range(b, i0, i1);
+        launch_epilogue(h->hsum.p, h->Sg.p, Y, ldy, i0, i1, m, s);
+        h->kernel_launches++;
+        if (events && events[b]) CUDA_TRY(cudaEventRecord((cudaEvent_t)events[b], s));
+      }
       h->launches[kAcc]++;
     }
     CUDA_TRY(cudaMemsetAsync(h->ctr.p + 2, 0, sizeof(unsigned), s));  // re-arm the ticket
@@ -482,9 +495,16 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
     }
     {
       TimedScope ts(h, kAcc, s);
-      launch_accumulate(p, h->rank.p, h->ldn, h->n, h->U.p, k_first, kcc, h->hsum.p, h->Sg.p, Y,
-                        ldy, m, c == 0, last, h->ctr.p + 2 + c, s);
-      h->kernel_launches++;
+      const int64_t nb = last ? nblocks : 1;
+      for (int64_t b = 0; b < nb; ++b) {
+        int64_t i0 = 0, i1 = h->n;
+        if (last) block_range(b, i0, i1);
+        launch_accumulate(p, h->rank.p, h->ldn, h->n, h->U.p, k_first, kcc, h->hsum.p, h->Sg.p,
+                          Y, ldy, m, c == 0, last, b == 0 ? h->ctr.p + 2 + c : nullptr, i0, i1,
+                          s);
+        h->kernel_launches++;
+        if (last && events && events[b]) CUDA_TRY(cudaEventRecord((cudaEvent_t)events[b], s));
+      }
       h->launches[kAcc]++;
       if (h->timing) h->acc_pairs += h->n * kcc;
     }
@@ -588,6 +608,24 @@ l1dm_status l1dm_matvec_ex(l1dm_handle h, const float *Z, int64_t ld_z, int64_t 
   }
   CUDA_TRY(cudaStreamSynchronize(s));
   return read_timeout(h);
+}
+
+l1dm_status l1dm_matvec_pipelined(l1dm_handle h, const float *Z, int64_t ld_z, int64_t m,
+                                  double *Y, int64_t ld_y, void *stream, int64_t point_blocks,
+                                  void *const *block_events) {
+  g_err.clear();
+  if (!h) return fail(L1DM_EINVAL, "handle is NULL");
+  if (!Z || !Y) return fail(L1DM_EINVAL, "Z or Y is NULL");
+  if (m < 1 || ld_z < m || ld_y < m || point_blocks < 1 || point_blocks > h->n)
+    return fail(L1DM_EINVAL, "m=%lld ld_z=%lld ld_y=%lld point_blocks=%lld invalid", (long long)m,
+                (long long)ld_z, (long long)ld_y, (long long)point_blocks);
+  l1dm_status st = check_device(h);
+  if (st != L1DM_OK) return st;
+  if (!is_device_pointer(Z) || !is_device_pointer(Y))
+    return fail(L1DM_EINVAL, "l1dm_matvec_pipelined needs device Z and Y");
+  cudaStream_t s = (cudaStream_t)stream;
+  h->last_stream = s;
+  return matvec_device(h, Z, ld_z, m, Y, ld_y, s, point_blocks, block_events);
 }
 
 l1dm_status l1dm_matvec(l1dm_handle h, const float *Z, int64_t m, double *Y) {

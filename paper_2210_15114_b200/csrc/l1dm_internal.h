@@ -52,6 +52,8 @@ __host__ __device__ constexpr int scan_items(int lpr, int vc) {
                          ? 64
                          : (98304 / (1024 * vc + 2048 / lpr)) / 4 * 4);
 }
+// Largest query workspace chunk (U + look-back state) in bytes.
+constexpr size_t kMaxChunkBytes = (size_t)72 << 30;
 // Independent (coordinate, column block) scan segments the planner aims for per chunk.
 constexpr int64_t kScanTargetSegments = 0;
 struct QueryPlan {
@@ -82,8 +84,8 @@ bool make_plan(int64_t n, int64_t dl, int64_t m, int64_t l2_bytes, int64_t ws_li
                int vec_cap, QueryPlan *p);
 
 // Scatter mode: Y[i][c] += g_c - h_i S_c.
-void launch_epilogue(const double *hsum, const double *Sg, double *Y, int64_t ldy, int64_t n,
-                     int64_t m, cudaStream_t s);
+void launch_epilogue(const double *hsum, const double *Sg, double *Y, int64_t ldy, int64_t i0,
+                     int64_t i1, int64_t m, cudaStream_t s);
 // S and g from the scan's per-segment totals (segtot: dl x m x 2 doubles).
 void launch_totals(const double *segtot, int64_t dl, int64_t m, double *Sg, cudaStream_t s);
 void launch_scan(const QueryPlan &p, const uint32_t *perm, const float *sval, int64_t ldn,
@@ -95,6 +97,7 @@ void launch_scan(const QueryPlan &p, const uint32_t *perm, const float *sval, in
 void launch_accumulate(const QueryPlan &p, const uint32_t *rank, int64_t ldn, int64_t n,
                        const double *U, int64_t k_first, int64_t kcc, const double *hsum,
                        const double *Sg, double *Y, int64_t ldy, int64_t m, bool first_chunk,
-                       bool last_chunk, unsigned *ticket, cudaStream_t s);
+                       bool last_chunk, unsigned *ticket, int64_t i0, int64_t i1,
+                       cudaStream_t s);  // points [i0, i1)
 
 }  // namespace l1dm

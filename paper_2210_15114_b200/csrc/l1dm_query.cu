@@ -50,7 +50,11 @@ static void plan_sizes(QueryPlan &q, int64_t n, int64_t dl, int64_t m, int64_t l
     q.kc = (int64_t)((0.375 * (double)l2_bytes) / (double)per_coord);
   } else {
     q.l2_resident = 0;
-    q.kc = (ws_limit > 0) ? (int64_t)((size_t)ws_limit / per_coord) : dl;
+    // one chunk's U is also capped: measured on B200, the rank gather of K6 drops from ~5.8
+    // to ~3.2 TB/s when the chunk's U spans ~100 GB (c5, 96 coordinates), not at 64 GB.
+    const size_t lim = (ws_limit > 0 && (size_t)ws_limit < kMaxChunkBytes) ? (size_t)ws_limit
+                                                                           : kMaxChunkBytes;
+    q.kc = (int64_t)(lim / per_coord);
   }
   if (q.kc < 1) q.kc = 1;
   if (q.kc > dl) q.kc = dl;
@@ -701,20 +705,21 @@ void launch_scan(const QueryPlan &p, const uint32_t *perm, const float *sval, in
 // Y[i][c] += g_c - h_i S_c after the scatter scans (Y was zeroed before them).
 __global__ void __launch_bounds__(256)
     k7_epilogue(const double *__restrict__ hsum, const double *__restrict__ Sg,
-                double *__restrict__ Y, int64_t ldy, int64_t n, int64_t m) {
-  const int64_t total = n * m;
+                double *__restrict__ Y, int64_t ldy, int64_t i0, int64_t i1, int64_t m) {
+  const int64_t total = (i1 - i0) * m;
   for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * 256) {
-    const int64_t i = e / m, c = e - (e / m) * m;
+    const int64_t i = i0 + e / m, c = e - (e / m) * m;
     Y[i * ldy + c] += fma(-hsum[i], Sg[c], Sg[m + c]);
   }
 }
 
-void launch_epilogue(const double *hsum, const double *Sg, double *Y, int64_t ldy, int64_t n,
-                     int64_t m, cudaStream_t s) {
-  int64_t blocks = (n * m + 255) / 256;
+void launch_epilogue(const double *hsum, const double *Sg, double *Y, int64_t ldy, int64_t i0,
+                     int64_t i1, int64_t m, cudaStream_t s) {
+  if (i1 <= i0) return;
+  int64_t blocks = ((i1 - i0) * m + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  k7_epilogue<<<(unsigned)blocks, 256, 0, s>>>(hsum, Sg, Y, ldy, n, m);
+  k7_epilogue<<<(unsigned)blocks, 256, 0, s>>>(hsum, Sg, Y, ldy, i0, i1, m);
 }
 
 // ------------------------------------------------------------------ K6
@@ -739,14 +744,14 @@ __global__ void __launch_bounds__(256)
                   const double *__restrict__ U, int64_t ldu, int64_t k_first, int64_t kcc,
                   const double *__restrict__ hsum, const double *__restrict__ Sg,
                   double *__restrict__ Y, int64_t ldy, int64_t m, int first_chunk,
-                  int last_chunk, unsigned *ticket) {
+                  int last_chunk, unsigned *ticket, int64_t i_begin, int64_t i_end) {
   constexpr int PPW = 32 / LPP;
   // the chunk's scan has completed (stream order): re-arm its ticket for the next query
   if (ticket && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *ticket = 0u;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t i = (int64_t)blockIdx.x * (8 * PPW) + (int64_t)w * PPW + lane / LPP;
+  const int64_t i = i_begin + (int64_t)blockIdx.x * (8 * PPW) + (int64_t)w * PPW + lane / LPP;
   const int64_t c0 = (int64_t)blockIdx.y * (LPP * V6) + (int64_t)(lane % LPP) * V6;
-  if (i >= n || c0 >= m) return;
+  if (i >= i_end || c0 >= m) return;
   double acc[V6];
 #pragma unroll
   for (int q = 0; q < V6; ++q) acc[q] = 0.0;
@@ -786,20 +791,23 @@ template <int V6, int LPP>
 static void launch_acc_t(const QueryPlan &p, const uint32_t *rank, int64_t ldn, int64_t n,
                          const double *U, int64_t k_first, int64_t kcc, const double *hsum,
                          const double *Sg, double *Y, int64_t ldy, int64_t m, bool first,
-                         bool last, unsigned *ticket, cudaStream_t s) {
+                         bool last, unsigned *ticket, int64_t i0, int64_t i1, cudaStream_t s) {
   constexpr int PPB = 8 * (32 / LPP);
-  dim3 grid((unsigned)((n + PPB - 1) / PPB), (unsigned)p.col_groups);
+  dim3 grid((unsigned)((i1 - i0 + PPB - 1) / PPB), (unsigned)p.col_groups);
   k6_accumulate<V6, LPP, 8><<<grid, 256, 0, s>>>(rank, ldn, n, U, p.ldu, k_first, kcc, hsum, Sg,
-                                                 Y, ldy, m, first ? 1 : 0, last ? 1 : 0, ticket);
+                                                 Y, ldy, m, first ? 1 : 0, last ? 1 : 0, ticket,
+                                                 i0, i1);
 }
 
 void launch_accumulate(const QueryPlan &p, const uint32_t *rank, int64_t ldn, int64_t n,
                        const double *U, int64_t k_first, int64_t kcc, const double *hsum,
                        const double *Sg, double *Y, int64_t ldy, int64_t m, bool first_chunk,
-                       bool last_chunk, unsigned *ticket, cudaStream_t s) {
+                       bool last_chunk, unsigned *ticket, int64_t i0, int64_t i1,
+                       cudaStream_t s) {
+  if (i1 <= i0) return;
 #define L1DM_ACC(V, L)                                                                   \
   launch_acc_t<V, L>(p, rank, ldn, n, U, k_first, kcc, hsum, Sg, Y, ldy, m, first_chunk, \
-                     last_chunk, ticket, s)
+                     last_chunk, ticket, i0, i1, s)
   switch (p.v6 * 100 + p.lpp) {
     case 101: L1DM_ACC(1, 1); break;
     case 102: L1DM_ACC(1, 2); break;

@@ -60,8 +60,15 @@ class ShardedL1DM:
         return self._matvec(self.handle, Z, Y, stream=self.stream)
 
     def matvec(self, Z: torch.Tensor, Y: Optional[torch.Tensor] = None, *, root: Optional[int] = 0,
-               async_op: bool = False):
-        """A·Z summed over ranks: on `root` only (reduce) or on every rank (root=None)."""
+               async_op: bool = False, overlap_blocks: int = 1):
+        """A·Z summed over ranks: on `root` only (reduce) or on every rank (root=None).
+
+        overlap_blocks > 1 (CUDA, C-ABI handle): the last accumulate runs per point block and
+        each block's rows are reduced as soon as they are final, overlapping the collective with
+        the remaining blocks' compute."""
+        if (overlap_blocks > 1 and self.world > 1 and self.handle is not None and Z.is_cuda
+                and self._matvec is binding.l1dm_matvec):
+            return self._matvec_overlapped(Z, Y, root, async_op, overlap_blocks)
         Y = self.partial(Z, Y)
         if self.world == 1:
             return (Y, None) if async_op else Y
@@ -71,6 +78,35 @@ class ShardedL1DM:
             work = dist.reduce(Y, dst=root, op=dist.ReduceOp.SUM, group=self.group,
                                async_op=async_op)
         return (Y, work) if async_op else Y
+
+    def _matvec_overlapped(self, Z, Y, root, async_op, nblocks):
+        n, m = Z.shape[0], Z.shape[1]
+        if Y is None:
+            Y = torch.empty((n, m), dtype=torch.float64, device=Z.device)
+        events = [torch.cuda.Event() for _ in range(nblocks)]
+        main = torch.cuda.current_stream(Z.device)
+        if getattr(self, "_compute_stream", None) is None:
+            self._compute_stream = torch.cuda.Stream(device=Z.device)
+        cs = self._compute_stream
+        cs.wait_stream(main)                      # Z (and Y's previous users) are ready
+        binding.l1dm_matvec_pipelined(self.handle, Z, Y, events, stream=cs)
+        works = []
+        for (i0, i1), ev in zip(binding.point_blocks(n, nblocks), events):
+            # the main stream (which NCCL synchronises with) waits only for block b's rows, so
+            # block b's collective runs while the compute stream finishes blocks b+1..
+            main.wait_event(ev)
+            if root is None:
+                w = dist.all_reduce(Y[i0:i1], op=dist.ReduceOp.SUM, group=self.group,
+                                    async_op=True)
+            else:
+                w = dist.reduce(Y[i0:i1], dst=root, op=dist.ReduceOp.SUM, group=self.group,
+                                async_op=True)
+            works.append(w)
+        if async_op:
+            return Y, works
+        for w in works:
+            w.wait()
+        return Y
 
     def close(self):
         if self.handle is not None and self._prepare is binding.l1dm_prepare:

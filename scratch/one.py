@@ -9,6 +9,8 @@ w = wl.workload(name, d=d, m=m)
 X = wl.make_points(w, "cuda"); Z = wl.make_query(w, 0, "cuda")
 torch.cuda.synchronize()
 h = l1.l1dm_prepare(X)
+import os
+if os.environ.get('WS_GB'): l1.l1dm_set_workspace_limit(h, int(float(os.environ['WS_GB'])*(1<<30)))
 Y = torch.empty((w.n, w.m), dtype=torch.float64, device="cuda")
 l1.l1dm_matvec(h, Z, Y); torch.cuda.synchronize()
 l1.l1dm_timing_enable(h, True); l1.l1dm_timing_read(h, reset=True)

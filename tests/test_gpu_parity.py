@@ -170,3 +170,27 @@ def test_workload_full_size_sampled(name):
         assert np.array_equal(Yg, Yr)        # integers < 2^53: exact on both sides
     else:
         assert col_rel_l2(Yg, Yr) <= TOL
+
+
+@pytest.mark.parametrize("m,blocks", [(1, 3), (4, 5), (64, 4)])
+def test_pipelined_point_blocks(m, blocks):
+    """l1dm_matvec_pipelined: same Y, and each block's event fires once its rows are final."""
+    rng = np.random.default_rng(40 + m)
+    X = rng.standard_normal((7001, 5)).astype(np.float32)
+    Z = rng.standard_normal((7001, m)).astype(np.float32)
+    h = l1.l1dm_prepare(torch.from_numpy(X).cuda())
+    Zd = torch.from_numpy(Z).cuda()
+    Y = torch.full((7001, m), float("nan"), dtype=torch.float64, device="cuda")
+    evs = [torch.cuda.Event() for _ in range(blocks)]
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    l1.l1dm_matvec_pipelined(h, Zd, Y, evs, stream=side)
+    ranges = l1.point_blocks(7001, blocks)
+    assert ranges[0][0] == 0 and ranges[-1][1] == 7001
+    Yr = oracle.brute(X, Z)
+    for (i0, i1), ev in zip(ranges, evs):
+        ev.synchronize()
+        assert col_rel_l2(Y[i0:i1].cpu().numpy(), Yr[i0:i1]) <= TOL
+    torch.cuda.synchronize()
+    l1.l1dm_sync(h)
+    l1.l1dm_free(h)
