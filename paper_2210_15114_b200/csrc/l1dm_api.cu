@@ -446,8 +446,10 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
       TimedScope ts(h, kScan, s);
       const uint32_t ep = h->epoch++;
       if (h->epoch >= (1u << 30)) h->epoch = 1;
-      launch_scan(p, h->perm.p, reinterpret_cast<const float *>(h->sval_bits.p), h->ldn, h->n, Z,
-                  ldz, m, Y, 0, h->dl, h->flags.p, h->agg.p, h->incl.p, ep, h->ctr.p + 2,
+      QueryPlan ps = p;
+      ps.ldu = ldy;  // the scan adds straight into Y's rows
+      launch_scan(ps, h->perm.p, reinterpret_cast<const float *>(h->sval_bits.p), h->ldn, h->n,
+                  Z, ldz, m, Y, 0, h->dl, h->flags.p, h->agg.p, h->incl.p, ep, h->ctr.p + 2,
                   h->ctr.p + 1, h->part.p, h->zs.p, s);
       h->kernel_launches += (p.mb == 1) ? 3 : 1;  // m == 1: reduce, prefix, apply
       h->launches[kScan]++;
