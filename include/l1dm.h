@@ -185,6 +185,11 @@ L1DM_API l1dm_status l1dm_timing_read(l1dm_handle h, l1dm_timing_t *out, int res
 L1DM_API l1dm_status l1dm_debug_export(l1dm_handle h, float *sval, uint32_t *perm, uint32_t *rank,
                               double *hsum);
 
+/* Return the device blocks that freed handles left in the library's block cache (current
+ * device) to CUDA.  Handles recycle each other's memory through this cache (it holds at most
+ * half of the device memory and is flushed automatically when an allocation fails). */
+L1DM_API l1dm_status l1dm_release_cached(void);
+
 /* Thread-local message describing the last non-OK status ("" if none). */
 L1DM_API const char *l1dm_last_error(void);
 

@@ -28,8 +28,8 @@ EXPORTS = [
     "l1dm_prepare", "l1dm_prepare_ex", "l1dm_matvec", "l1dm_matvec_ex", "l1dm_matvec_pipelined",
     "l1dm_free", "l1dm_sync",
     "l1dm_shape", "l1dm_workspace_bytes", "l1dm_set_workspace_limit", "l1dm_plan",
-    "l1dm_timing_enable", "l1dm_timing_read", "l1dm_debug_export", "l1dm_last_error",
-    "l1dm_version",
+    "l1dm_timing_enable", "l1dm_timing_read", "l1dm_debug_export", "l1dm_release_cached",
+    "l1dm_last_error", "l1dm_version",
 ]
 
 
@@ -88,6 +88,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.l1dm_timing_enable.argtypes = [vp, i32]
     lib.l1dm_timing_read.argtypes = [vp, ctypes.POINTER(TimingT), i32]
     lib.l1dm_debug_export.argtypes = [vp, vp, vp, vp, vp]
+    lib.l1dm_release_cached.argtypes = []
+    lib.l1dm_release_cached.restype = st
     lib.l1dm_last_error.argtypes = []
     lib.l1dm_last_error.restype = ctypes.c_char_p
     lib.l1dm_version.argtypes = []
@@ -274,6 +276,11 @@ def l1dm_debug_export(h: Handle):
     _check(load_library().l1dm_debug_export(h.ptr, _ptr(sval), _ptr(perm), _ptr(rank), _ptr(hs)),
            "l1dm_debug_export")
     return sval, perm, rank, hs
+
+
+def l1dm_release_cached():
+    """Return cached device blocks of freed handles to CUDA (current device)."""
+    _check(load_library().l1dm_release_cached(), "l1dm_release_cached")
 
 
 def l1dm_version() -> str:

@@ -7,6 +7,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <map>
+#include <mutex>
+#include <unordered_map>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -51,6 +55,90 @@ struct TimedPair {
   cudaEvent_t a, b;
 };
 
+// Process-wide cache of device blocks released by handles (prepare transients, query
+// workspace), so that successive handles — one per bench step, one per shard — reuse memory
+// instead of paying cudaMalloc/cudaFree of tens of GB each time.  Blocks enter the cache only
+// after their stream has been synchronised; a request takes the smallest cached block of at
+// least the requested size (and at most 1.25x of it).  The cache holds at most half of the
+// device memory, is flushed when an allocation fails, and l1dm_release_cached() empties it.
+class BlockCache {
+ public:
+  static BlockCache &get() {
+    static BlockCache c;
+    return c;
+  }
+  cudaError_t alloc(void **p, size_t bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    bytes = (bytes + ((size_t)2 << 20) - 1) & ~(((size_t)2 << 20) - 1);  // 2 MiB granules
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      auto &m = free_[dev];
+      auto it = m.lower_bound(bytes);
+      if (it != m.end() && it->first <= bytes + bytes / 4) {
+        *p = it->second;
+        sizes_[*p] = it->first;
+        cached_[dev] -= it->first;
+        m.erase(it);
+        return cudaSuccess;
+      }
+    }
+    const size_t rounded = bytes;
+    cudaError_t e = cudaMalloc(p, rounded);
+    if (e == cudaErrorMemoryAllocation) {
+      cudaGetLastError();
+      release_all(dev);
+      e = cudaMalloc(p, rounded);
+    }
+    if (e == cudaSuccess) {
+      std::lock_guard<std::mutex> g(mu_);
+      sizes_[*p] = rounded;
+    }
+    return e;
+  }
+  // p must not be in use by any queued work (callers synchronise first)
+  void free(void *p) {
+    if (!p) return;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu_);
+    auto sz = sizes_.find(p);
+    if (sz == sizes_.end()) {
+      cudaFree(p);
+      return;
+    }
+    const size_t bytes = sz->second;
+    sizes_.erase(sz);
+    if (limit_[dev] == 0) {
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      limit_[dev] = tot / 2;
+    }
+    if (cached_[dev] + bytes > limit_[dev]) {
+      cudaFree(p);
+      return;
+    }
+    free_[dev].emplace(bytes, p);
+    cached_[dev] += bytes;
+  }
+  void release_all(int dev) {
+    std::lock_guard<std::mutex> g(mu_);
+    for (auto &kv : free_[dev]) cudaFree(kv.second);
+    free_[dev].clear();
+    cached_[dev] = 0;
+  }
+  size_t cached(int dev) {
+    std::lock_guard<std::mutex> g(mu_);
+    return cached_[dev];
+  }
+
+ private:
+  std::mutex mu_;
+  std::map<int, std::multimap<size_t, void *>> free_;
+  std::map<int, size_t> cached_, limit_;
+  std::unordered_map<void *, size_t> sizes_;
+};
+
 template <typename T>
 struct DevBuf {
   T *p = nullptr;
@@ -58,21 +146,24 @@ struct DevBuf {
   cudaError_t ensure(size_t c, bool zero, cudaStream_t s) {
     if (c <= count && p) return cudaSuccess;
     if (p) {
-      cudaFree(p);
+      cudaStreamSynchronize(s);  // queued work on s may still use the old block
+      BlockCache::get().free(p);
       p = nullptr;
       count = 0;
     }
-    cudaError_t e = cudaMalloc(&p, std::max<size_t>(c, 1) * sizeof(T));
+    void *q = nullptr;
+    cudaError_t e = BlockCache::get().alloc(&q, std::max<size_t>(c, 1) * sizeof(T));
     if (e != cudaSuccess) {
       p = nullptr;
       return e;
     }
+    p = static_cast<T *>(q);
     count = c;
     if (zero) return cudaMemsetAsync(p, 0, std::max<size_t>(c, 1) * sizeof(T), s);
     return cudaSuccess;
   }
-  void release() {
-    if (p) cudaFree(p);
+  void release() {  // callers synchronise the streams that used the block first
+    if (p) BlockCache::get().free(p);
     p = nullptr;
     count = 0;
   }
@@ -243,6 +334,15 @@ l1dm_status prepare_impl(const float *X, int64_t n, int64_t ld_x, int64_t k_begi
   CUDA_TRY(cudaEventCreate(&ev0));
   CUDA_TRY(cudaEventCreate(&ev1));
   CUDA_TRY(cudaEventRecord(ev0, s));
+  static const bool dbg = getenv("L1DM_DEBUG_PREP") != nullptr;  // phase timing to stderr
+  const auto t_start = std::chrono::steady_clock::now();
+  auto lap = [&](const char *what) {
+    if (!dbg) return;
+    cudaStreamSynchronize(s);
+    fprintf(stderr, "[l1dm prep] %-28s %8.3f ms\n", what,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start)
+                .count());
+  };
 
   const int64_t dl = h->dl, ldn = h->ldn;
   const size_t elems = (size_t)dl * (size_t)ldn;
@@ -265,6 +365,7 @@ l1dm_status prepare_impl(const float *X, int64_t n, int64_t ld_x, int64_t k_begi
   CUDA_TRY(hist.ensure((size_t)dl * 1024, true, s));
   CUDA_TRY(ctrl.ensure(4, true, s));
 
+  lap("alloc keyA/rank/hsum/hist");
   launch_keys(Xd, n, ld_x, k_begin, dl, ldn, keyA.p, h->hsum.p, ctrl.p + 0, s);
   h->kernel_launches++;
   launch_hist(keyA.p, n, ldn, dl, hist.p, s);
@@ -276,6 +377,7 @@ l1dm_status prepare_impl(const float *X, int64_t n, int64_t ld_x, int64_t k_begi
                            s));
   CUDA_TRY(cudaMemcpyAsync(flags_h, ctrl.p, sizeof(flags_h), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
+  lap("keys + hist + readback");
   Xstage.release();
   if (flags_h[0]) {
     keyA.release();
@@ -343,6 +445,7 @@ l1dm_status prepare_impl(const float *X, int64_t n, int64_t ld_x, int64_t k_begi
     const int64_t tiles = (n + kSortTile - 1) / kSortTile;
     CUDA_TRY(status.ensure((size_t)dl * tiles * 256, true, s));
     static const bool fused_rank = getenv("L1DM_FUSED_RANK") != nullptr;  // tuning switch
+    lap("alloc sort buffers");
     uint32_t *kb[2] = {keyA.p, keyB.p};
     uint32_t *vb[2] = {valA.p, valB.p};
     for (int i = 0; i < P; ++i) {
@@ -367,6 +470,7 @@ l1dm_status prepare_impl(const float *X, int64_t n, int64_t ld_x, int64_t k_begi
     std::swap(h->perm.p, vbuf[fin]->p);
     std::swap(h->perm.count, vbuf[fin]->count);
   }
+  lap("sort passes + rank");
   CUDA_TRY(cudaEventRecord(ev1, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   CUDA_TRY(cudaMemcpy(flags_h, ctrl.p, sizeof(flags_h), cudaMemcpyDeviceToHost));
@@ -383,6 +487,7 @@ l1dm_status prepare_impl(const float *X, int64_t n, int64_t ld_x, int64_t k_begi
   dbase.release();
   status.release();
   ctrl.release();
+  lap("release transients");
   if (flags_h[1]) return fail(L1DM_ETIMEOUT, "sort look-back wait exceeded its bound");
   return L1DM_OK;
 }
@@ -400,8 +505,8 @@ l1dm_status ensure_plan(l1dm_ctx *h, int64_t m, int vec_cap) {
   if (ws == 0) {
     size_t fr = 0, tot = 0;
     CUDA_TRY(cudaMemGetInfo(&fr, &tot));
-    ws = (size_t)(0.75 * (double)(fr + h->U.count * sizeof(double) +
-                                 h->agg.count * sizeof(double) * 2));
+    ws = (size_t)(0.75 * (double)(fr + BlockCache::get().cached(h->device) +
+                                 h->U.count * sizeof(double) + h->agg.count * sizeof(double) * 2));
   }
   if (h->plan_m == m && h->plan_ws == ws && h->plan_vec_cap == vec_cap) return L1DM_OK;
   QueryPlan p;
@@ -760,6 +865,13 @@ l1dm_status l1dm_debug_export(l1dm_handle h, float *sval, uint32_t *perm, uint32
     CUDA_TRY(cudaMemcpyAsync(hsum, h->hsum.p, (size_t)h->n * sizeof(double), cudaMemcpyDefault,
                              h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return L1DM_OK;
+}
+
+l1dm_status l1dm_release_cached(void) {
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  BlockCache::get().release_all(dev);
   return L1DM_OK;
 }
 
