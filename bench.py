@@ -32,7 +32,9 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+L2_PEAKS_FILE = os.path.join(ROOT, "profiles", "l2_peaks.json")  # tools/l2_probe.cu on a B200
 FALLBACK_HBM = 6650.0
+METRIC = "l1 matvec throughput: n\u00b7d\u00b7m updates/s and achieved HBM GB/s vs peak"  # BASELINE.json
 
 
 def parse():
@@ -46,6 +48,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--reduce", default="reduce", choices=["reduce", "allreduce"])
+    ap.add_argument("--mode", default="auto", choices=["auto", "gather", "scatter"],
+                    help="query strategy (include/l1dm.h l1dm_set_query_mode)")
     ap.add_argument("--overlap-blocks", type=int, default=4,
                     help="N>1: point blocks whose reduce overlaps the remaining accumulate")
     return ap.parse_args()
@@ -109,6 +113,14 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def load_l2_peaks():
+    try:
+        with open(L2_PEAKS_FILE) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
 def model_b_bytes(n, d, m):
     """SURVEY §8(d) Model B algorithmic bytes per query: n d (12 + 20 m) + n (12 m + 8)."""
     return n * d * (12 + 20 * m) + n * (12 * m + 8)
@@ -157,7 +169,7 @@ def run_reference(args):
     value = statistics.mean(vals)
     ms = w.n * w.d * w.m * Q / value * 1e3
     line = {
-        "impl": "reference", "metric": "l1 matvec throughput (n*d*m updates/s)", "value": value,
+        "impl": "reference", "metric": METRIC, "value": value,
         "unit": "updates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64 (long double accumulation) over f32 inputs", "data": "synthetic",
@@ -207,7 +219,7 @@ def main_ours(args):
     kr = (0, k1 - k0)
 
     def one_step(timing=False):
-        sh = ShardedL1DM(X, k_range=kr, stream=stream)
+        sh = ShardedL1DM(X, k_range=kr, stream=stream, mode=args.mode)
         sh.world = world
         if timing and sh.handle is not None:
             l1.l1dm_timing_enable(sh.handle, True)
@@ -256,33 +268,76 @@ def main_ours(args):
                        if agg else None)
     hbm_peak, peak_kind = load_peaks()
     dl = k1 - k0
-    # algorithmic bytes (SURVEY §8(d) Model B, split by kernel):
-    #   scan       per (point, coordinate): perm 4 + sval 4 + Z row 4m + U row 8m
-    #   accumulate per (point, coordinate): rank 4 + U row 8m; per point and query: Y 8m + h 8
-    scan_bytes = agg.get("scan_pairs", 0) * (8 + 12 * m)
-    acc_bytes = agg.get("accumulate_pairs", 0) * (4 + 8 * m) + agg.get("queries", 0) * n * (8 * m + 8)
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+    plan = l1.l1dm_plan(n, max(dl, 1), m, l2_bytes, 0, mode=args.mode)
+    qb = model_b_bytes(n, dl, m)
     kern = {
-        "scan": {"ms_total": agg.get("scan_ms"), "launches": agg.get("scan_launches"),
-                 "alg_bytes": scan_bytes},
+        "scan": {"ms_total": agg.get("scan_ms"), "launches": agg.get("scan_launches")},
         "accumulate": {"ms_total": agg.get("accumulate_ms"),
-                       "launches": agg.get("accumulate_launches"), "alg_bytes": acc_bytes},
+                       "launches": agg.get("accumulate_launches")},
     }
     for kv in kern.values():
         kv["ms_per_launch"] = kv["ms_total"] / max(kv["launches"] or 1, 1) if kv["ms_total"] else None
-        kv["achieved_GBps"] = (kv["alg_bytes"] / (kv["ms_total"] * 1e-3) / 1e9
-                               if kv["ms_total"] else None)
-    dominant = max(kern, key=lambda k: kern[k]["ms_total"] or 0.0)
-    ach = kern[dominant]["achieved_GBps"]
+    l2p = load_l2_peaks()
+    if plan["scatter"] and m > 1:
+        # scatter mode: per column block, "scan" = reduce + prefix (perm/sval
+        # streamed from HBM, one Zt row gathered from L2 per pair), "accumulate" = apply (the
+        # same gathers plus one fp64 L2 reduction per update).  The apply pass is bounded by the
+        # L2's fp64 reduction throughput: roofline in reductions/s against the measured probe.
+        mb = plan["mb"]
+        kern["scan"]["alg_bytes"] = agg.get("scan_pairs", 0) * (8 + 4 * mb)
+        kern["accumulate"]["alg_reductions"] = agg.get("queries", 0) * n * dl * m
+        kern["accumulate"]["alg_bytes"] = agg.get("accumulate_pairs", 0) * (8 + 4 * mb) + \
+            kern["accumulate"]["alg_reductions"] * 8
+        for kv in kern.values():
+            kv["achieved_GBps"] = (kv["alg_bytes"] / (kv["ms_total"] * 1e-3) / 1e9
+                                   if kv["ms_total"] else None)
+        acc = kern["accumulate"]
+        dominant = "accumulate"
+        ach = (acc["alg_reductions"] / (acc["ms_total"] * 1e-3) / 1e9) if acc["ms_total"] else None
+        peak = l2p.get("red_row8_adds_per_s", 5.88e11) / 1e9
+        roof = {"bound": "l2_fp64_reductions", "kernel": "apply (k5_scan_seq<mb,APPLY>)",
+                "achieved": ach, "peak": peak,
+                "peak_kind": "measured (tools/l2_probe.cu -> profiles/l2_peaks.json)"
+                if l2p else "fallback (earlier probe)",
+                "unit": "G fp64 reductions/s", "frac": (ach / peak) if ach else None,
+                "alg_reductions_per_launch": acc["alg_reductions"] / max(acc["launches"] or 1, 1)}
+    else:
+        # gather mode: algorithmic bytes (SURVEY §8(d) Model B, split by kernel)
+        #   scan       per (point, coordinate): perm 4 + sval 4 + Z row 4m + U row 8m
+        #   accumulate per (point, coordinate): rank 4 + U row 8m; per point and query: Y 8m + h 8
+        kern["scan"]["alg_bytes"] = agg.get("scan_pairs", 0) * (8 + 12 * m)
+        kern["accumulate"]["alg_bytes"] = (agg.get("accumulate_pairs", 0) * (4 + 8 * m) +
+                                           agg.get("queries", 0) * n * (8 * m + 8))
+        for kv in kern.values():
+            kv["achieved_GBps"] = (kv["alg_bytes"] / (kv["ms_total"] * 1e-3) / 1e9
+                                   if kv["ms_total"] else None)
+        dominant = max(kern, key=lambda k: kern[k]["ms_total"] or 0.0)
+        ach = kern[dominant]["achieved_GBps"]
+        roof = {"bound": "hbm", "kernel": dominant, "achieved": ach, "peak": hbm_peak,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": (ach / hbm_peak) if ach else None,
+                "alg_bytes_per_launch": (kern[dominant]["alg_bytes"] /
+                                         max(kern[dominant]["launches"] or 1, 1)),
+                "frac_of_8TBps": (ach / 8000.0) if ach else None}
+        if plan["scatter"]:  # m == 1: L2-sector bound (random z gathers + reductions into Y)
+            roof["note"] = ("m = 1 scatter mode: L2-resident z and Y, DRAM fraction is not the "
+                            "bound (DESIGN.md §6)")
     traffic = None
     prof = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.workload}.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(dominant)
+            tr = json.load(open(prof))
+            traffic = tr.get(f"{'scatter' if plan['scatter'] else 'gather'}_{dominant}",
+                             tr.get(dominant))
         except Exception:
             traffic = None
-    qb = model_b_bytes(n, dl, m)
+    roof["traffic"] = traffic
+    # the U-materialising design's HBM floor (Model B bytes) over the measured query time:
+    # above 1.0 means the query beats that design's roofline
+    roof["model_b_hbm_equivalent_frac"] = (qb / (query_kernel_ms * 1e-3) / 1e9 / hbm_peak
+                                           if query_kernel_ms else None)
     result = {
-        "metric": "l1 matvec throughput (n*d*m updates/s; HBM GB/s vs peak in roofline)",
+        "metric": METRIC,
         "value": value, "unit": "updates/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None,
@@ -291,6 +346,8 @@ def main_ours(args):
                    "fresh_queries": w.fresh_queries, "parallelism": f"coord-shard x{world}",
                    "collective": (args.reduce if world > 1 else None),
                    "overlap_blocks": (args.overlap_blocks if world > 1 else None),
+                   "mode": args.mode, "strategy": ("scatter" if plan["scatter"] else "gather"),
+                   "columns_per_block": plan["mb"],
                    "l2": "inputs > L2 (prepared state 12*n*d B), no flush"},
         "gpu_launches": int(agg.get("kernel_launches", 0)),
         "prepare_ms": prep_ms,
@@ -300,12 +357,7 @@ def main_ours(args):
         "colsums_ms_per_launch": (agg["colsums_ms"] / max(agg["colsums_launches"], 1)
                                   if agg else None),
         "model_b_GBps_per_query": qb / (query_kernel_ms * 1e-3) / 1e9 if query_kernel_ms else None,
-        "roofline": {"bound": "hbm", "kernel": dominant, "achieved": ach, "peak": hbm_peak,
-                     "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": (ach / hbm_peak) if ach else None, "traffic": traffic,
-                     "alg_bytes_per_launch": (kern[dominant]["alg_bytes"] /
-                                              max(kern[dominant]["launches"] or 1, 1)),
-                     "frac_of_8TBps": (ach / 8000.0) if ach else None},
+        "roofline": roof,
         "clocks": clk,
     }
     # ---- e2e through the public API with HOST buffers (pinned), N=1 only
@@ -316,6 +368,7 @@ def main_ours(args):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         h = l1.l1dm_prepare(Xh)
+        l1.l1dm_set_query_mode(h, args.mode)
         for q in range(Q):
             l1.l1dm_matvec(h, Zh[q % len(Zh)], Yh)
         l1.l1dm_free(h)

@@ -138,11 +138,22 @@ L1DM_API size_t l1dm_workspace_bytes(l1dm_handle h, int64_t m);
  * A smaller cap means more coordinate chunks (more Y read-modify-writes). */
 L1DM_API l1dm_status l1dm_set_workspace_limit(l1dm_handle h, size_t bytes);
 
+/* Query strategy.  Both compute the same Y = A*Z:
+ *   GATHER  the scan stores U = v*P - Q per (coordinate, sorted row) in a workspace and a
+ *           per-point pass gathers U at rank_k(i) for every k (Y written once, no atomics);
+ *   SCATTER the scan adds 2U straight into Y[perm_k(r)] with fp64 L2 atomics, one column
+ *           block of Y at a time (no U workspace, no rank gather; the order of the d terms
+ *           of y_i then varies run to run at the ulp level on float data — DESIGN.md R16).
+ * AUTO (the default) picks SCATTER when a column block of Y and Z fits in L2.
+ * Returns EINVAL for a NULL handle or an unknown mode.  Host-only. */
+enum { L1DM_MODE_AUTO = 0, L1DM_MODE_GATHER = 1, L1DM_MODE_SCATTER = 2 };
+L1DM_API l1dm_status l1dm_set_query_mode(l1dm_handle h, int mode);
+
 /* Query plan, a pure function of the sizes (testable without a GPU).
  * mb = columns per scan segment; rows_per_tile = scan tile rows; kc = coordinates
  * per chunk; chunks = ceil(d_local / kc); l2_resident = 1 when a chunk's U
  * workspace is sized to stay in L2 (small n*m); scatter = 1 when the query runs in
- * small-m mode (m == 1 and Y fits L2: no U workspace, no rank gather). */
+ * scatter mode (see l1dm_set_query_mode; mb is then the column block width). */
 typedef struct {
   int64_t mb;
   int64_t col_blocks;
@@ -154,10 +165,13 @@ typedef struct {
   int64_t chunks;
   int64_t l2_resident;
   int64_t workspace_bytes;
-  int64_t scatter;      /* 1: small-m mode, the scan adds 2U into an L2-resident Y with atomics */
+  int64_t scatter;      /* 1: scatter mode, the scan adds 2U into an L2-resident Y block with atomics */
 } l1dm_plan_t;
 L1DM_API l1dm_status l1dm_plan(int64_t n, int64_t d_local, int64_t m, int64_t l2_bytes,
                       int64_t workspace_limit, l1dm_plan_t *out);
+/* The same for an explicit query mode (L1DM_MODE_*); EINVAL for an unknown mode. */
+L1DM_API l1dm_status l1dm_plan_ex(int64_t n, int64_t d_local, int64_t m, int64_t l2_bytes,
+                         int64_t workspace_limit, int mode, l1dm_plan_t *out);
 
 /* Per-kernel device time (CUDA events on the launching stream).  While enabled,
  * every launch of every kernel is bracketed by events; read accumulates the

@@ -27,8 +27,8 @@ STATUS = {
 EXPORTS = [
     "l1dm_prepare", "l1dm_prepare_ex", "l1dm_matvec", "l1dm_matvec_ex", "l1dm_matvec_pipelined",
     "l1dm_free", "l1dm_sync",
-    "l1dm_shape", "l1dm_workspace_bytes", "l1dm_set_workspace_limit", "l1dm_plan",
-    "l1dm_timing_enable", "l1dm_timing_read", "l1dm_debug_export", "l1dm_release_cached",
+    "l1dm_shape", "l1dm_workspace_bytes", "l1dm_set_workspace_limit", "l1dm_set_query_mode",
+    "l1dm_plan", "l1dm_plan_ex", "l1dm_timing_enable", "l1dm_timing_read", "l1dm_debug_export", "l1dm_release_cached",
     "l1dm_last_error", "l1dm_version",
 ]
 
@@ -84,7 +84,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.l1dm_workspace_bytes.argtypes = [vp, i64]
     lib.l1dm_workspace_bytes.restype = ctypes.c_size_t
     lib.l1dm_set_workspace_limit.argtypes = [vp, ctypes.c_size_t]
+    lib.l1dm_set_query_mode.argtypes = [vp, i32]
     lib.l1dm_plan.argtypes = [i64, i64, i64, i64, i64, ctypes.POINTER(PlanT)]
+    lib.l1dm_plan_ex.argtypes = [i64, i64, i64, i64, i64, i32, ctypes.POINTER(PlanT)]
     lib.l1dm_timing_enable.argtypes = [vp, i32]
     lib.l1dm_timing_read.argtypes = [vp, ctypes.POINTER(TimingT), i32]
     lib.l1dm_debug_export.argtypes = [vp, vp, vp, vp, vp]
@@ -96,7 +98,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.l1dm_version.restype = ctypes.c_char_p
     for name in ("l1dm_prepare", "l1dm_prepare_ex", "l1dm_matvec", "l1dm_matvec_ex",
                  "l1dm_matvec_pipelined", "l1dm_sync",
-                 "l1dm_shape", "l1dm_set_workspace_limit", "l1dm_plan", "l1dm_timing_enable",
+                 "l1dm_shape", "l1dm_set_workspace_limit", "l1dm_set_query_mode", "l1dm_plan", "l1dm_plan_ex",
+                 "l1dm_timing_enable",
                  "l1dm_timing_read", "l1dm_debug_export"):
         getattr(lib, name).restype = st
     _lib = lib
@@ -245,14 +248,24 @@ def l1dm_set_workspace_limit(h: Handle, nbytes: int):
     _check(load_library().l1dm_set_workspace_limit(h.ptr, int(nbytes)), "l1dm_set_workspace_limit")
 
 
+MODES = {"auto": 0, "gather": 1, "scatter": 2}
+
+
+def l1dm_set_query_mode(h: Handle, mode):
+    """"auto" | "gather" | "scatter" (or 0/1/2): the query strategy, include/l1dm.h."""
+    _check(load_library().l1dm_set_query_mode(h.ptr, MODES.get(mode, mode)), "l1dm_set_query_mode")
+
+
 def l1dm_workspace_bytes(h: Handle, m: int) -> int:
     return int(load_library().l1dm_workspace_bytes(h.ptr, m))
 
 
-def l1dm_plan(n: int, d_local: int, m: int, l2_bytes: int = 126 << 20, workspace_limit: int = 0):
+def l1dm_plan(n: int, d_local: int, m: int, l2_bytes: int = 126 << 20, workspace_limit: int = 0,
+              mode="auto"):
+    """The query plan for these sizes (pure host function; mode "auto" | "gather" | "scatter")."""
     p = PlanT()
-    _check(load_library().l1dm_plan(n, d_local, m, l2_bytes, workspace_limit, ctypes.byref(p)),
-           "l1dm_plan")
+    _check(load_library().l1dm_plan_ex(n, d_local, m, l2_bytes, workspace_limit,
+                                       MODES.get(mode, mode), ctypes.byref(p)), "l1dm_plan")
     return {f: getattr(p, f) for f, _ in PlanT._fields_}
 
 

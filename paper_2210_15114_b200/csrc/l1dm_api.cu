@@ -198,8 +198,11 @@ struct l1dm_ctx {
   DevBuf<double> agg, incl;
   DevBuf<double> part, Sg;
   DevBuf<float> zs;            // m == 1: gathered z in sorted order (reduce -> apply pass)
+  DevBuf<float> zt;            // scatter mode, m > 1: column-block-major copy of Z
+  DevBuf<double> yt;           // scatter mode, m > 1: one column block's accumulator (n x mb)
   DevBuf<unsigned> ctr;        // [0] colsum done counter, [1] timeout flag, [2..] scan tickets
   size_t ws_limit = 0;
+  int mode = 0;  // L1DM_MODE_*
   uint32_t epoch = 1;
   // host staging
   DevBuf<float> Zstage;
@@ -306,6 +309,8 @@ void destroy(l1dm_ctx *h) {
   h->Zstage.release();
   h->Ystage.release();
   h->zs.release();
+  h->zt.release();
+  h->yt.release();
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }
@@ -510,7 +515,7 @@ l1dm_status ensure_plan(l1dm_ctx *h, int64_t m, int vec_cap) {
   }
   if (h->plan_m == m && h->plan_ws == ws && h->plan_vec_cap == vec_cap) return L1DM_OK;
   QueryPlan p;
-  if (!make_plan(h->n, h->dl, m, h->l2_bytes, (int64_t)ws, vec_cap, &p))
+  if (!make_plan(h->n, h->dl, m, h->l2_bytes, (int64_t)ws, vec_cap, h->mode, &p))
     return fail(L1DM_EINVAL, "no query plan for n=%lld d=%lld m=%lld", (long long)h->n,
                 (long long)h->dl, (long long)m);
   h->plan = p;
@@ -540,13 +545,18 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
   CUDA_TRY(h->incl.ensure(p.lb_slots * 2 * p.mb, false, s));
   CUDA_TRY(h->part.ensure((size_t)h->dl * 2 * m, false, s));  // per-segment totals
   CUDA_TRY(h->Sg.ensure((size_t)2 * m, false, s));
-  if (h->ctr.count < (size_t)2 + p.chunks) {
-    CUDA_TRY(h->ctr.ensure((size_t)2 + p.chunks, true, s));  // tickets start at 0
+  const size_t nticket = (size_t)p.chunks;
+  if (h->ctr.count < 2 + nticket) {
+    CUDA_TRY(h->ctr.ensure(2 + nticket, true, s));  // tickets start at 0
   }
-  if (p.scatter) {
-    // small-m mode: zero Y, one scan launch over every coordinate adding 2U into Y, epilogue
-    CUDA_TRY(cudaMemset2DAsync(Y, (size_t)ldy * sizeof(double), 0, (size_t)m * sizeof(double),
-                               (size_t)h->n, s));
+  if (p.zt_floats) {
+    CUDA_TRY(h->zt.ensure((size_t)p.zt_floats, false, s));
+    CUDA_TRY(h->yt.ensure((size_t)h->n * p.mb, false, s));
+  }
+  if (p.scatter && m == 1) {
+    // scatter mode, m == 1: zero Y, reduce/prefix/apply over every coordinate adding 2U into Y,
+    // then the epilogue g - h_i S
+    CUDA_TRY(cudaMemset2DAsync(Y, (size_t)ldy * sizeof(double), 0, sizeof(double), (size_t)h->n, s));
     {
       TimedScope ts(h, kScan, s);
       const uint32_t ep = h->epoch++;
@@ -555,14 +565,14 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
       ps.ldu = ldy;  // the scan adds straight into Y's rows
       launch_scan(ps, h->perm.p, reinterpret_cast<const float *>(h->sval_bits.p), h->ldn, h->n,
                   Z, ldz, m, Y, 0, h->dl, h->flags.p, h->agg.p, h->incl.p, ep, h->ctr.p + 2,
-                  h->ctr.p + 1, h->part.p, h->zs.p, s);
-      h->kernel_launches += (p.mb == 1) ? 3 : 1;  // m == 1: reduce, prefix, apply
+                  h->ctr.p + 1, h->part.p, 2 * m, h->zs.p, s);
+      h->kernel_launches += 3;  // reduce, prefix, apply
       h->launches[kScan]++;
       if (h->timing) h->scan_pairs += h->n * h->dl;
     }
     {
       TimedScope ts(h, kColsums, s);
-      launch_totals(h->part.p, h->dl, m, h->Sg.p, s);
+      launch_totals(h->part.p, 2 * m, h->dl, m, h->Sg.p, h->Sg.p + m, s);
       h->kernel_launches++;
       h->launches[kColsums]++;
     }
@@ -578,6 +588,56 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
       h->launches[kAcc]++;
     }
     CUDA_TRY(cudaMemsetAsync(h->ctr.p + 2, 0, sizeof(unsigned), s));  // re-arm the ticket
+  } else if (p.scatter) {
+    // scatter mode, m > 1: per column block of mb columns (Zt, the block's compact copy of Z),
+    // the reduce / prefix / apply scan adds 2U into a compact L2-resident accumulator Yt
+    // (n x mb), then Y's block columns = Yt + g - h_i S.  Timing kinds: scan =
+    // reduce + prefix (tile totals), accumulate = apply (U and the reductions into Yt),
+    // colsums = Zt, totals and the block write-out.
+    const float *sval = reinterpret_cast<const float *>(h->sval_bits.p);
+    {
+      TimedScope ts(h, kColsums, s);
+      launch_zt(Z, ldz, h->n, m, p.mb, h->zt.p, s);
+      h->kernel_launches++;
+      h->launches[kColsums]++;
+    }
+    for (int cb = 0; cb < p.col_blocks; ++cb) {
+      const int64_t c0 = (int64_t)cb * p.mb;
+      const int64_t mc = std::min<int64_t>(p.mb, m - c0);
+      const bool last = cb == p.col_blocks - 1;
+      const float *ztb = h->zt.p + (size_t)cb * h->n * p.mb;
+      {
+        TimedScope ts(h, kScan, s);
+        launch_scan_seq(p, h->perm.p, sval, h->ldn, h->n, ztb, mc, h->yt.p, h->dl, h->agg.p,
+                        h->part.p + 2 * c0, 2 * m, 0, s);
+        h->kernel_launches += 2;  // reduce, prefix
+        h->launches[kScan]++;
+        if (h->timing) h->scan_pairs += h->n * h->dl;
+      }
+      {
+        TimedScope ts(h, kAcc, s);
+        CUDA_TRY(cudaMemsetAsync(h->yt.p, 0, (size_t)h->n * p.mb * sizeof(double), s));
+        launch_scan_seq(p, h->perm.p, sval, h->ldn, h->n, ztb, mc, h->yt.p, h->dl, h->agg.p,
+                        h->part.p + 2 * c0, 2 * m, 1, s);
+        h->kernel_launches++;  // apply
+        h->launches[kAcc]++;
+        if (h->timing) h->acc_pairs += h->n * h->dl;
+      }
+      {
+        TimedScope ts(h, kColsums, s);
+        launch_totals(h->part.p + 2 * c0, 2 * m, h->dl, mc, h->Sg.p + c0, h->Sg.p + m + c0, s);
+        const int64_t nb = last ? nblocks : 1;
+        for (int64_t b = 0; b < nb; ++b) {
+          int64_t i0 = 0, i1 = h->n;
+          if (last) block_range(b, i0, i1);
+          launch_block_out(h->yt.p, p.mb, mc, h->hsum.p, h->Sg.p + c0, h->Sg.p + m + c0, Y + c0,
+                           ldy, i0, i1, s);
+          if (last && events && events[b]) CUDA_TRY(cudaEventRecord((cudaEvent_t)events[b], s));
+        }
+        h->kernel_launches += 1 + nb;  // totals, block out(s)
+        h->launches[kColsums]++;
+      }
+    }
   }
   for (int64_t c = 0; !p.scatter && c < p.chunks; ++c) {
     const int64_t k_first = c * p.kc;
@@ -589,14 +649,14 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
       if (h->epoch >= (1u << 30)) h->epoch = 1;
       launch_scan(p, h->perm.p, reinterpret_cast<const float *>(h->sval_bits.p), h->ldn, h->n, Z,
                   ldz, m, h->U.p, k_first, kcc, h->flags.p, h->agg.p, h->incl.p, ep,
-                  h->ctr.p + 2 + c, h->ctr.p + 1, h->part.p, h->zs.p, s);
+                  h->ctr.p + 2 + c, h->ctr.p + 1, h->part.p, 2 * m, h->zs.p, s);
       h->kernel_launches += (p.mb == 1) ? 3 : 1;  // m == 1: reduce, prefix, apply
       h->launches[kScan]++;
       if (h->timing) h->scan_pairs += h->n * kcc;
     }
     if (last) {
       TimedScope ts(h, kColsums, s);
-      launch_totals(h->part.p, h->dl, m, h->Sg.p, s);  // S, g from the segment totals
+      launch_totals(h->part.p, 2 * m, h->dl, m, h->Sg.p, h->Sg.p + m, s);  // S, g from the segment totals
       h->kernel_launches++;
       h->launches[kColsums]++;
     }
@@ -769,8 +829,17 @@ size_t l1dm_workspace_bytes(l1dm_handle h, int64_t m) {
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return 0;
     ws = (int64_t)(0.75 * (double)fr);
   }
-  if (!make_plan(h->n, h->dl, m, h->l2_bytes, ws, 4, &p)) return 0;
+  if (!make_plan(h->n, h->dl, m, h->l2_bytes, ws, 4, h->mode, &p)) return 0;
   return p.workspace_bytes;
+}
+
+l1dm_status l1dm_set_query_mode(l1dm_handle h, int mode) {
+  if (!h) return fail(L1DM_EINVAL, "handle is NULL");
+  if (mode < L1DM_MODE_AUTO || mode > L1DM_MODE_SCATTER)
+    return fail(L1DM_EINVAL, "unknown query mode %d", mode);
+  h->mode = mode;
+  h->plan_m = -1;
+  return L1DM_OK;
 }
 
 l1dm_status l1dm_set_workspace_limit(l1dm_handle h, size_t bytes) {
@@ -782,9 +851,16 @@ l1dm_status l1dm_set_workspace_limit(l1dm_handle h, size_t bytes) {
 
 l1dm_status l1dm_plan(int64_t n, int64_t d_local, int64_t m, int64_t l2_bytes,
                       int64_t workspace_limit, l1dm_plan_t *out) {
+  return l1dm_plan_ex(n, d_local, m, l2_bytes, workspace_limit, L1DM_MODE_AUTO, out);
+}
+
+l1dm_status l1dm_plan_ex(int64_t n, int64_t d_local, int64_t m, int64_t l2_bytes,
+                         int64_t workspace_limit, int mode, l1dm_plan_t *out) {
   if (!out) return fail(L1DM_EINVAL, "out is NULL");
+  if (mode < L1DM_MODE_AUTO || mode > L1DM_MODE_SCATTER)
+    return fail(L1DM_EINVAL, "unknown query mode %d", mode);
   QueryPlan p;
-  if (!make_plan(n, d_local, m, l2_bytes, workspace_limit, 4, &p))
+  if (!make_plan(n, d_local, m, l2_bytes, workspace_limit, 4, mode, &p))
     return fail(L1DM_EINVAL, "invalid sizes n=%lld d=%lld m=%lld", (long long)n,
                 (long long)d_local, (long long)m);
   out->mb = p.mb;

@@ -56,6 +56,12 @@ __host__ __device__ constexpr int scan_items(int lpr, int vc) {
 constexpr size_t kMaxChunkBytes = (size_t)72 << 30;
 // Independent (coordinate, column block) scan segments the planner aims for per chunk.
 constexpr int64_t kScanTargetSegments = 0;
+// Scatter mode for m > 1 (measured crossovers): a Y block plus its Z block
+// (12 n mb bytes) may be up to this multiple of L2; mb = 4 only for m <= kScatterNarrowM; and
+// n >= kScatterMinN (below it the per-block launches dominate).
+constexpr double kScatterL2Fraction = 1.25;
+constexpr int64_t kScatterNarrowM = 24;
+constexpr int64_t kScatterMinN = 1 << 17;
 struct QueryPlan {
   int vec;            // fp32 Z elements per cp.async gather chunk (1, 2, 4)
   int lpr;            // lanes per sorted row in the scan = columns per segment
@@ -68,7 +74,8 @@ struct QueryPlan {
   int64_t kc;         // coordinates per chunk
   int64_t chunks;
   int l2_resident;
-  int scatter;        // 1: scan adds 2U into Y with L2 atomics (small m); 0: U + rank gather
+  int scatter;        // 1: scan adds 2U into Y with L2 atomics (Y block fits L2); 0: U + rank gather
+  int64_t zt_floats;  // scatter with m > 1: column-block-major copy of Z (col_blocks x n x mb)
   int64_t ldu;        // U row length (doubles) = m
   size_t u_bytes;     // kc * n * ldu * 8
   size_t lb_slots;    // kc * col_blocks * tiles_per_segment
@@ -80,20 +87,38 @@ struct QueryPlan {
 };
 
 // vec_cap: widest fp32 vector the caller's Z allows (4: 16-B aligned rows, 2: 8-B, 1).
+// mode: 0 automatic, 1 gather (U + rank gather), 2 scatter (L2 atomics into Y).
 bool make_plan(int64_t n, int64_t dl, int64_t m, int64_t l2_bytes, int64_t ws_limit,
-               int vec_cap, QueryPlan *p);
+               int vec_cap, int mode, QueryPlan *p);
 
 // Scatter mode: Y[i][c] += g_c - h_i S_c.
 void launch_epilogue(const double *hsum, const double *Sg, double *Y, int64_t ldy, int64_t i0,
                      int64_t i1, int64_t m, cudaStream_t s);
-// S and g from the scan's per-segment totals (segtot: dl x m x 2 doubles).
-void launch_totals(const double *segtot, int64_t dl, int64_t m, double *Sg, cudaStream_t s);
+// S and g of mc columns from the scan's per-segment totals (coordinate rows of ld_seg doubles,
+// (S, T) pairs per column): S_c = coordinate 0's S, g_c = sum_k T_kc.
+void launch_totals(const double *segtot, int64_t ld_seg, int64_t dl, int64_t mc, double *S,
+                   double *g, cudaStream_t s);
+// Scatter mode, m > 1: Y[i][c] = Yt[i][c] + g_c - h_i S_c for points [i0, i1), mc columns.
+void launch_block_out(const double *yt, int mb, int64_t mc, const double *hsum, const double *S,
+                      const double *g, double *Y, int64_t ldy, int64_t i0, int64_t i1,
+                      cudaStream_t s);
+// segtot: per-coordinate rows of ld_seg doubles ((S, T) per column); zs: m == 1 only, kc x ldn
+// floats (z in sorted order between the reduce and apply passes).
 void launch_scan(const QueryPlan &p, const uint32_t *perm, const float *sval, int64_t ldn,
                  int64_t n, const float *Z, int64_t ldz, int64_t m, double *U, int64_t k_first,
                  int64_t kcc, uint32_t *flags, double *agg, double *incl, uint32_t epoch,
-                 unsigned *ticket, unsigned *timeout_flag, double *segtot, float *zs,
-                 cudaStream_t s);
-// (zs: m == 1 only, kc x ldn floats: z in sorted order between the reduce and apply passes)
+                 unsigned *ticket, unsigned *timeout_flag, double *segtot, int64_t ld_seg,
+                 float *zs, cudaStream_t s);
+// Scatter mode, m > 1: scan of one column block (mc <= mb columns of the compact Zt block) over
+// kcc coordinates as reduce / prefix / apply launches (agg: kcc x tiles x 2mb doubles), adding
+// 2U into the block accumulator yt (n x mb).  rows_per_tile = 1024.  phase: 0 reduce + prefix
+// (writes agg and segtot), 1 apply (reads agg, adds into yt), 2 both.
+void launch_scan_seq(const QueryPlan &p, const uint32_t *perm, const float *sval, int64_t ldn,
+                     int64_t n, const float *zt, int64_t mc, double *yt, int64_t kcc, double *agg,
+                     double *segtot, int64_t ld_seg, int phase, cudaStream_t s);
+// Zt[cb][i][0..mb) = Z[i][cb*mb + ..] (zero-padded past m): the scatter mode's per-block Z.
+void launch_zt(const float *Z, int64_t ldz, int64_t n, int64_t m, int mb, float *zt,
+               cudaStream_t s);
 void launch_accumulate(const QueryPlan &p, const uint32_t *rank, int64_t ldn, int64_t n,
                        const double *U, int64_t k_first, int64_t kcc, const double *hsum,
                        const double *Sg, double *Y, int64_t ldy, int64_t m, bool first_chunk,

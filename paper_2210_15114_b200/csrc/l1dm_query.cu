@@ -66,7 +66,7 @@ static void plan_sizes(QueryPlan &q, int64_t n, int64_t dl, int64_t m, int64_t l
 }
 
 bool make_plan(int64_t n, int64_t dl, int64_t m, int64_t l2_bytes, int64_t ws_limit,
-               int vec_cap, QueryPlan *p) {
+               int vec_cap, int mode, QueryPlan *p) {
   if (n < 1 || dl < 1 || m < 1 || !p) return false;
   QueryPlan q{};
   // Columns per scan segment: the whole Z row when it fits one warp (two columns per lane
@@ -93,23 +93,70 @@ bool make_plan(int64_t n, int64_t dl, int64_t m, int64_t l2_bytes, int64_t ws_li
     q.vec = pick_vec(q.lpr * q.vc);
     plan_sizes(q, n, dl, m, l2_bytes, ws_limit);
   }
-  // Small-m mode: for m == 1 with an L2-resident Y the scan adds 2U straight into Y with L2
-  // atomics (one pass, no U workspace, no rank gather).  L1DM_SCATTER=0/1 overrides.
-  static const int scatter_env = [] {
+  // Scatter mode: when a block of Y (n x mb fp64) and the matching block of Z fit in L2, the
+  // scan adds 2U straight into Y with L2 atomics (no U workspace round trip through HBM, no
+  // rank gather).  m == 1 uses the reduce-then-scan kernels; m > 1 runs one scan launch per
+  // column block of mb columns over a column-block-major copy of Z.
+  // mode (1 gather, 2 scatter), else L1DM_SCATTER=0/1, and L1DM_SCATTER_MB override.
+  static const int scatter_env_ = [] {
     const char *e = getenv("L1DM_SCATTER");
     return e ? atoi(e) : -1;
   }();
-  q.scatter = scatter_env >= 0 ? scatter_env
-                               : (m == 1 && l2_bytes > 0 && n * m * 8 * 2 <= l2_bytes) ? 1 : 0;
+  // an explicit per-handle mode (l1dm_set_query_mode) wins over the environment
+  const int scatter_env = mode == 1 ? 0 : mode == 2 ? 1 : scatter_env_;
+  static const int scatter_mb_env = [] {
+    const char *e = getenv("L1DM_SCATTER_MB");
+    return e ? atoi(e) : 0;
+  }();
+  int smb = 0;  // columns per scatter block (0: no scatter)
+  if (m == 1) {
+    smb = (scatter_env == 1 || (scatter_env < 0 && l2_bytes > 0 && n * 16 <= l2_bytes)) ? 1 : 0;
+  } else if (scatter_env != 0) {
+    if (scatter_mb_env > 0) {
+      smb = scatter_mb_env;
+    } else {
+      // Measured on B200: per (point, coordinate, column block) the scatter scan
+      // costs ~24 ps at mb = 8 and ~17-20 ps at mb = 4, i.e. ~3 and ~4.5-5 ps per update, against
+      // ~3.6 (m = 64) to ~5 (m = 16) ps per update for the gather path.  So mb = 8 wins whenever
+      // its Yt + Zt block (12 n mb bytes) roughly fits L2, mb = 4 only for narrow queries, and
+      // tiny n (launch-bound) stays on the gather path.
+      const double cap = kScatterL2Fraction * (double)l2_bytes;
+      if (l2_bytes > 0 && n >= kScatterMinN) {
+        if ((double)n * 8 * 12.0 <= cap) smb = 8;
+        else if ((double)n * 4 * 12.0 <= cap && m <= kScatterNarrowM) smb = 4;
+      }
+      if (!smb && scatter_env == 1) smb = 4;
+    }
+    if (smb > 0) {
+      if (smb > 16) smb = 16;
+      smb = pow2ceil(smb);
+      while (smb > 1 && smb >= 2 * m) smb >>= 1;
+    }
+  }
+  q.scatter = smb > 0 ? 1 : 0;
+  q.zt_floats = 0;
+  if (q.scatter && m > 1) {
+    q.vc = 1;
+    q.lpr = smb;
+    q.vec = smb >= 4 ? 4 : smb;  // Zt rows are smb floats, 16-B aligned blocks
+    plan_sizes(q, n, dl, m, l2_bytes, ws_limit);
+    q.items = 4 * smb;  // k5_scan_seq: 1024-row tiles, 4*mb consecutive rows per thread
+    q.rows_per_tile = 1024;
+    q.tiles_per_segment = (n + q.rows_per_tile - 1) / q.rows_per_tile;
+    q.zt_floats = (int64_t)q.col_blocks * n * smb;
+  }
   if (q.scatter) {
     q.kc = dl;  // every coordinate in one launch: nothing to hold between scan and accumulate
     q.chunks = 1;
     q.l2_resident = 1;
     q.u_bytes = 0;
-    q.lb_slots = (size_t)dl * q.col_blocks * q.tiles_per_segment;
+    // m > 1: one launch per column block, the look-back state is reused between launches
+    q.lb_slots = (size_t)dl * (m > 1 ? 1 : q.col_blocks) * q.tiles_per_segment;
     q.workspace_bytes = q.lb_slots * (sizeof(uint32_t) + 2 * 2 * q.mb * sizeof(double)) +
-                        (size_t)dl * n * sizeof(float) + (size_t)dl * 2 * m * sizeof(double) +
-                        2 * m * sizeof(double);
+                        (m == 1 ? (size_t)dl * n * sizeof(float) : 0) +
+                        (size_t)q.zt_floats * sizeof(float) +
+                        (m > 1 ? (size_t)n * q.mb * sizeof(double) : 0) +
+                        (size_t)dl * 2 * m * sizeof(double) + 2 * m * sizeof(double);
   }
   q.v6 = (m % 2 == 0) ? 2 : 1;
   int64_t lanes = (m + q.v6 - 1) / q.v6;
@@ -123,19 +170,21 @@ bool make_plan(int64_t n, int64_t dl, int64_t m, int64_t l2_bytes, int64_t ws_li
 // Query totals from the scan's segment totals: S_c = sum_j z_jc (coordinate 0's segment),
 // g_c = sum_k T_kc = sum_j h_j z_jc, summed over the shard's coordinates in fixed order.
 __global__ void __launch_bounds__(256)
-    k4_totals(const double *__restrict__ segtot, int64_t dl, int64_t m, double *__restrict__ Sg) {
-  for (int64_t c = (int64_t)blockIdx.x * 256 + threadIdx.x; c < m; c += (int64_t)gridDim.x * 256) {
-    double g = 0.0;
-    for (int64_t k = 0; k < dl; ++k) g += segtot[k * 2 * m + 2 * c + 1];
-    Sg[c] = segtot[2 * c];
-    Sg[m + c] = g;
+    k4_totals(const double *__restrict__ segtot, int64_t ld_seg, int64_t dl, int64_t mc,
+              double *__restrict__ S, double *__restrict__ g) {
+  for (int64_t c = (int64_t)blockIdx.x * 256 + threadIdx.x; c < mc; c += (int64_t)gridDim.x * 256) {
+    double gc = 0.0;
+    for (int64_t k = 0; k < dl; ++k) gc += segtot[k * ld_seg + 2 * c + 1];
+    S[c] = segtot[2 * c];
+    g[c] = gc;
   }
 }
 
-void launch_totals(const double *segtot, int64_t dl, int64_t m, double *Sg, cudaStream_t s) {
-  int64_t blocks = (m + 255) / 256;
+void launch_totals(const double *segtot, int64_t ld_seg, int64_t dl, int64_t mc, double *S,
+                   double *g, cudaStream_t s) {
+  int64_t blocks = (mc + 255) / 256;
   if (blocks > 148) blocks = 148;
-  k4_totals<<<(unsigned)blocks, 256, 0, s>>>(segtot, dl, m, Sg);
+  k4_totals<<<(unsigned)blocks, 256, 0, s>>>(segtot, ld_seg, dl, mc, S, g);
 }
 
 // ------------------------------------------------------------------ K5
@@ -186,6 +235,106 @@ struct ScanCfg {
 };
 
 
+// Decoupled look-back (Merrill & Garland) for tile `tile` of the segment whose slots start at
+// slot0: publishes the tile aggregate s_agg[NP] (epoch-tagged flag, release at gpu scope), sums
+// the predecessors' payloads into s_excl[NP] (warp 0 polls a 32-predecessor window, all NT
+// threads sum payloads), then publishes the inclusive prefix.  Waits are bounded by kSpinLimit
+// (then *timeout_flag is raised and the results are invalid).  Called by all NT threads.
+template <int NP, int NT>
+__device__ __forceinline__ void lookback(int64_t slot0, int64_t tile, uint32_t *flags, double *agg,
+                                         double *incl, uint32_t epoch, unsigned *timeout_flag,
+                                         const double *s_agg, double *s_excl, double *s_red,
+                                         int *s_q, int64_t *s_j) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t me = slot0 + tile;
+  // payloads are read back within a few tiles: keep them from displacing L2-resident data
+  const uint64_t pol = l2_policy_evict_first();
+  if (tid < NP) s_excl[tid] = 0.0;
+  if (tile == 0) {
+    if (tid < NP) {
+      st_f64_hint(&incl[me * NP + tid], s_agg[tid], pol);
+      __threadfence();
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      st_release_u32(&flags[me], (epoch << 2) | kFlagInclusive);
+    }
+  } else {
+    if (tid < NP) {
+      st_f64_hint(&agg[me * NP + tid], s_agg[tid], pol);
+      __threadfence();
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      st_release_u32(&flags[me], (epoch << 2) | kFlagAggregate);
+    }
+    int64_t j = tile - 1;  // nearest predecessor not yet summed
+    for (;;) {
+      // warp 0: lane l examines predecessor j - l; q = nearest inclusive prefix in the window
+      if (w == 0) {
+        const int64_t jl = j - lane;
+        uint32_t f = (epoch << 2) | kFlagInclusive;  // jl < 0: empty prefix
+        if (jl >= 0) {
+          uint32_t spins = 0;
+          for (;;) {
+            f = ld_acquire_u32(&flags[slot0 + jl]);
+            if ((f >> 2) == (epoch & 0x3FFFFFFFu) && (f & 3u) != kFlagInvalid) break;
+            if (++spins > kSpinLimit) {
+              atomicOr(timeout_flag, 1u);
+              f = (epoch << 2) | kFlagInclusive;  // give up (results invalid; ETIMEOUT)
+              break;
+            }
+            if (spins > 8) __nanosleep(32);
+          }
+        }
+        const uint32_t inc_mask = __ballot_sync(0xFFFFFFFFu, (f & 3u) == kFlagInclusive);
+        if (lane == 0) {
+          *s_q = inc_mask ? __ffs(inc_mask) - 1 : 32;
+          *s_j = j;
+        }
+      }
+      __syncthreads();
+      const int q = *s_q;
+      const int64_t jw = *s_j;
+      const int cnt = q < 32 ? q + 1 : 32;  // tiles jw .. jw-cnt+1 (the last one INCL if q<32)
+      constexpr int GROUPS = NT / NP;       // all threads sum payloads, comp = tid % NP
+      double part = 0.0;
+      {
+        const int comp = tid % NP, g = tid / NP;
+        if (g < GROUPS) {
+          for (int b = g; b < cnt; b += GROUPS) {
+            const int64_t jj = jw - b;
+            if (jj < 0) break;
+            part += __ldcg((b == q ? incl : agg) + (slot0 + jj) * NP + comp);
+          }
+        }
+      }
+      s_red[tid] = part;
+      __syncthreads();
+      if (tid < NP) {
+        double sum = 0.0;
+#pragma unroll
+        for (int g = 0; g < GROUPS; ++g) sum += s_red[g * NP + tid];
+        s_excl[tid] += sum;
+      }
+      __syncthreads();
+      if (q < 32) break;
+      j = jw - 32;
+    }
+    if (tid < NP) {
+      st_f64_hint(&incl[me * NP + tid], s_excl[tid] + s_agg[tid], pol);
+      __threadfence();
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      st_release_u32(&flags[me], (epoch << 2) | kFlagInclusive);
+    }
+  }
+}
+
 // SCATTER: instead of storing U in sorted order, add 2 U_r straight into Y[perm[r]] with L2
 // atomics (small-m mode: Y is L2-resident; no U round trip, no rank gather — DESIGN.md §6).
 template <int LPR, int VC, int CH, bool SCATTER>
@@ -195,7 +344,7 @@ __global__ void __launch_bounds__(256, 2)
             double *__restrict__ U, int64_t ldu, int64_t k_first, int col_blocks, int64_t nseg,
             int64_t total, uint32_t *flags, double *agg, double *incl, uint32_t epoch,
             unsigned *ticket, unsigned *timeout_flag, int64_t tiles_per_seg,
-            double *__restrict__ segtot) {
+            double *__restrict__ segtot, int64_t ld_seg) {
   constexpr int ITEMS = scan_items(LPR, VC);
   using C = ScanCfg<LPR, VC, ITEMS>;
   constexpr int MB = C::MB, RPW = C::RPW, ROWS_W = C::ROWS_W, R = C::R, NP = C::NP, NW = C::NW;
@@ -304,96 +453,13 @@ __global__ void __launch_bounds__(256, 2)
 
   // ---- decoupled look-back (Merrill & Garland) across the tiles of this segment
   const int64_t slot0 = seg * tiles_per_seg;
-  const int64_t me = slot0 + tile;
-  if (tid < NP) s_excl[tid] = 0.0;
-  if (tile == 0) {
-    if (tid < NP) {
-      __stcg(&incl[me * NP + tid], s_agg[tid]);
-      __threadfence();
-    }
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      st_release_u32(&flags[me], (epoch << 2) | kFlagInclusive);
-    }
-  } else {
-    if (tid < NP) {
-      __stcg(&agg[me * NP + tid], s_agg[tid]);
-      __threadfence();
-    }
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      st_release_u32(&flags[me], (epoch << 2) | kFlagAggregate);
-    }
-    int64_t j = tile - 1;  // nearest predecessor not yet summed
-    for (;;) {
-      // warp 0: lane l examines predecessor j - l; q = nearest inclusive prefix in the window
-      if (w == 0) {
-        const int64_t jl = j - lane;
-        uint32_t f = (epoch << 2) | kFlagInclusive;  // jl < 0: empty prefix
-        if (jl >= 0) {
-          uint32_t spins = 0;
-          for (;;) {
-            f = ld_acquire_u32(&flags[slot0 + jl]);
-            if ((f >> 2) == (epoch & 0x3FFFFFFFu) && (f & 3u) != kFlagInvalid) break;
-            if (++spins > kSpinLimit) {
-              atomicOr(timeout_flag, 1u);
-              f = (epoch << 2) | kFlagInclusive;  // give up (results invalid; ETIMEOUT)
-              break;
-            }
-            if (spins > 8) __nanosleep(32);
-          }
-        }
-        const uint32_t inc_mask = __ballot_sync(0xFFFFFFFFu, (f & 3u) == kFlagInclusive);
-        if (lane == 0) {
-          s_q = inc_mask ? __ffs(inc_mask) - 1 : 32;
-          s_j = j;
-        }
-      }
-      __syncthreads();
-      const int q = s_q;
-      const int64_t jw = s_j;
-      const int cnt = q < 32 ? q + 1 : 32;  // tiles jw .. jw-cnt+1 (the last one INCL if q<32)
-      constexpr int GROUPS = NT / NP;       // all threads sum payloads, comp = tid % NP
-      double part = 0.0;
-      {
-        const int comp = tid % NP, g = tid / NP;
-        if (g < GROUPS) {
-          for (int b = g; b < cnt; b += GROUPS) {
-            const int64_t jj = jw - b;
-            if (jj < 0) break;
-            part += __ldcg((b == q ? incl : agg) + (slot0 + jj) * NP + comp);
-          }
-        }
-      }
-      s_red[tid] = part;
-      __syncthreads();
-      if (tid < NP) {
-        double sum = 0.0;
-#pragma unroll
-        for (int g = 0; g < GROUPS; ++g) sum += s_red[g * NP + tid];
-        s_excl[tid] += sum;
-      }
-      __syncthreads();
-      if (q < 32) break;
-      j = jw - 32;
-    }
-    if (tid < NP) {
-      __stcg(&incl[me * NP + tid], s_excl[tid] + s_agg[tid]);
-      __threadfence();
-    }
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      st_release_u32(&flags[me], (epoch << 2) | kFlagInclusive);
-    }
-  }
+  lookback<NP, NT>(slot0, tile, flags, agg, incl, epoch, timeout_flag, s_agg, s_excl, s_red, &s_q,
+                   &s_j);
   // ---- the segment's totals (S = sum z, T_k = sum x z: Alg. 2's B_i[n], C_i[n])
   // feed the epilogue g - h_i S with g = sum_k T_k, so no extra pass over Z.
   if (tile == tiles_per_seg - 1 && tid < NP) {
     const int64_t c = (int64_t)cb * MB + tid / 2;
-    if (c < m) segtot[(k_first + kk) * 2 * m + 2 * c + (tid & 1)] = s_excl[tid] + s_agg[tid];
+    if (c < m) segtot[(k_first + kk) * ld_seg + 2 * c + (tid & 1)] = s_excl[tid] + s_agg[tid];
   }
   // ---- phase 2: exclusive prefixes P, Q along the rows, U_r = v_r P_r - Q_r
   double P[VC], Q[VC];
@@ -439,6 +505,209 @@ __global__ void __launch_bounds__(256, 2)
       }
     }
   }
+}
+
+// Scatter-mode scan for m > 1: one column block of MB columns, read from the compact Zt block
+// (row stride MB), with 2U added into the block accumulator Yt[perm[r]][c] (row stride MB) by
+// fp64 L2 reductions.  Reduce-then-scan, no inter-CTA waits (ncu showed the decoupled
+// look-back's barriers and fences dominating this L2-bound kernel):
+//   SEQ_REDUCE  per tile: column totals of (z, v z)                  -> agg[seg][tile][2 MB]
+//   k5_seq_prefix  per (segment, component): exclusive scan over tiles, segment totals
+//   SEQ_APPLY   per tile: the same totals again, CTA scan + tile prefix, U along the rows, REDs
+// Thread (g, c) owns ITEMS consecutive sorted rows of column c, so the row loop is a
+// thread-sequential scan; only per-thread totals are scanned across the CTA (shuffles over the
+// 32/MB groups of a warp, then across warps).  At each row step a warp adds 32/MB rows x MB
+// consecutive columns: every reduction request is one row segment of Yt.
+template <int MB>
+struct SeqCfg {
+  static constexpr int NT = 256, NW = 8;
+  static constexpr int G = NT / MB;           // row groups per tile
+  static constexpr int ITEMS = 4 * MB;        // consecutive rows per thread
+  static constexpr int R = G * ITEMS;         // 1024 rows per tile
+  static constexpr int GPW = 32 / MB;         // groups per warp
+  static constexpr int GS = ITEMS * MB + MB;  // padded floats per group of the Z stage
+  static constexpr int PS = ITEMS + 4;        // padded words per group of perm / sval
+  static constexpr int NP = 2 * MB;
+  static constexpr int CH = MB * 4 >= 16 ? 16 : MB * 4;  // bytes per cp.async of a Z row
+  static constexpr size_t SMEM = (size_t)G * GS * 4 + (size_t)G * PS * 4 * 2;
+};
+enum { SEQ_REDUCE = 0, SEQ_APPLY = 1 };
+
+template <int MB, int MODE>
+__global__ void __launch_bounds__(256)
+    k5_scan_seq(const uint32_t *__restrict__ perm, const float *__restrict__ sval, int64_t ldn,
+                int64_t n, const float *__restrict__ zt, int64_t mc, double *__restrict__ yt,
+                int64_t nseg, int64_t tiles_per_seg, double *__restrict__ agg) {
+  using C = SeqCfg<MB>;
+  constexpr int NT = C::NT, NW = C::NW, ITEMS = C::ITEMS, R = C::R, GPW = C::GPW, GS = C::GS,
+                PS = C::PS, NP = C::NP, CH = C::CH, CPR = MB * 4 / CH;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float *zb = reinterpret_cast<float *>(smem_raw);              // [G][GS]
+  float *vb = zb + C::G * GS;                                    // [G][PS]
+  uint32_t *pb = reinterpret_cast<uint32_t *>(vb + C::G * PS);  // [G][PS]
+  __shared__ double s_wt[NW * NP];
+
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int c = lane % MB, gl = lane / MB, g = w * GPW + gl;
+  const int64_t t = blockIdx.x;  // tiles are independent: no ticket, no waiting
+  const int64_t tile = t / nseg;
+  const int64_t kk = t - tile * nseg;  // segment = local coordinate
+  const int64_t row0 = tile * R;
+  const int64_t nrows = (n - row0 < R) ? (n - row0) : R;
+  // L2 priorities: the sorted tables stream through (evict first); the Zt block and the Yt
+  // accumulator are what must stay resident for the whole launch (evict last).
+  const uint64_t pol_stream = l2_policy_evict_first(), pol_keep = l2_policy_evict_last();
+  {
+    const uint32_t *pp = perm + kk * ldn + row0;
+    const float *vp = sval + kk * ldn + row0;
+    for (int q = tid; q < R / 4; q += NT) {  // 4 consecutive rows, always inside one group
+      const int r = 4 * q, dst = (r / ITEMS) * PS + (r % ITEMS);
+      const bool ok = row0 + r < ldn;
+      cp_async_hint<16>(pb + dst, ok ? (const void *)(pp + r) : (const void *)perm, ok, pol_stream);
+      cp_async_hint<16>(vb + dst, ok ? (const void *)(vp + r) : (const void *)sval, ok, pol_stream);
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    for (int e = tid; e < R * CPR; e += NT) {  // gather Zt rows into sorted order
+      const int r = e / CPR, ch = e - (e / CPR) * CPR;
+      const bool ok = r < nrows;
+      const float *src =
+          ok ? zt + (int64_t)pb[(r / ITEMS) * PS + (r % ITEMS)] * MB + ch * (CH / 4) : zt;
+      cp_async_hint<CH>(zb + (r / ITEMS) * GS + (r % ITEMS) * MB + ch * (CH / 4), src, ok,
+                        pol_keep);
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+  }
+  const int rl0 = g * ITEMS;  // first row of this thread
+  const int nmine = (int)(nrows - rl0 < ITEMS ? (nrows - rl0 < 0 ? 0 : nrows - rl0) : ITEMS);
+  const float *zg = zb + g * GS + c;
+  const float *vg = vb + g * PS;
+  const uint32_t *pg = pb + g * PS;
+  // ---- per-thread totals of s = z and t = v z (fp64; products of fp32 exact)
+  double os = 0.0, ot = 0.0;
+#pragma unroll 8
+  for (int j = 0; j < ITEMS; ++j) {
+    const double z = (double)zg[j * MB];  // zero-filled past n
+    const double v = j < nmine ? (double)vg[j] : 0.0;
+    os += z;
+    ot = fma(v, z, ot);
+  }
+  // ---- inclusive scan over the GPW groups of this warp (same column: lanes c + k*MB)
+  double ps = os, pt = ot;
+#pragma unroll
+  for (int off = 1; off < GPW; off <<= 1) {
+    const double a = __shfl_up_sync(0xFFFFFFFFu, ps, off * MB);
+    const double b = __shfl_up_sync(0xFFFFFFFFu, pt, off * MB);
+    if (gl >= off) {
+      ps += a;
+      pt += b;
+    }
+  }
+  if (gl == GPW - 1) {
+    s_wt[w * NP + 2 * c] = ps;
+    s_wt[w * NP + 2 * c + 1] = pt;
+  }
+  __syncthreads();
+  double *ag = agg + (kk * tiles_per_seg + tile) * NP;
+  if constexpr (MODE == SEQ_REDUCE) {
+    if (tid < NP) {
+      double run = 0.0;
+#pragma unroll
+      for (int ww = 0; ww < NW; ++ww) run += s_wt[ww * NP + tid];
+      ag[tid] = run;
+    }
+    return;
+  } else {
+    // exclusive prefix of this thread's first row: tile prefix + earlier warps + earlier groups
+    double P = __ldg(ag + 2 * c) + ps - os, Q = __ldg(ag + 2 * c + 1) + pt - ot;
+    for (int ww = 0; ww < w; ++ww) {
+      P += s_wt[ww * NP + 2 * c];
+      Q += s_wt[ww * NP + 2 * c + 1];
+    }
+    if (c < mc) {
+#pragma unroll 8
+      for (int j = 0; j < ITEMS; ++j) {
+        if (j >= nmine) break;
+        const double z = (double)zg[j * MB], v = (double)vg[j];
+        const double u = fma(v, P, -Q);  // U_r = v_r P_r - Q_r
+        P += z;
+        Q = fma(v, z, Q);
+        red_add_f64(yt + (int64_t)pg[j] * MB + c, 2.0 * u, pol_keep);
+      }
+    }
+  }
+}
+
+// Exclusive scan of each (segment, component) over the segment's tiles, in place (one warp per
+// (segment, component)), and the segment totals (S, T_k per column) for the epilogue.
+__global__ void __launch_bounds__(256)
+    k5_seq_prefix(double *__restrict__ agg, int64_t nseg, int64_t tiles_per_seg, int np,
+                  int64_t ncomp, double *__restrict__ segtot, int64_t ld_seg) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (wid >= nseg * np) return;
+  const int64_t seg = wid / np;
+  const int comp = (int)(wid - seg * np);
+  double *ag = agg + seg * tiles_per_seg * np + comp;
+  double carry = 0.0;
+  for (int64_t base = 0; base < tiles_per_seg; base += 32) {
+    const int64_t j = base + lane;
+    const double x = j < tiles_per_seg ? ag[j * np] : 0.0;
+    double a = x;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const double a2 = __shfl_up_sync(0xFFFFFFFFu, a, off);
+      if (lane >= off) a += a2;
+    }
+    if (j < tiles_per_seg) ag[j * np] = carry + a - x;
+    carry += __shfl_sync(0xFFFFFFFFu, a, 31);
+  }
+  if (lane == 0 && comp < ncomp) segtot[seg * ld_seg + comp] = carry;
+}
+
+template <int MB>
+static void launch_seq_t(const QueryPlan &p, const uint32_t *perm, const float *sval, int64_t ldn,
+                         int64_t n, const float *zt, int64_t mc, double *yt, int64_t kcc,
+                         double *agg, double *segtot, int64_t ld_seg, int phase, cudaStream_t s) {
+  using C = SeqCfg<MB>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k5_scan_seq<MB, SEQ_REDUCE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)C::SMEM);
+    cudaFuncSetAttribute(k5_scan_seq<MB, SEQ_APPLY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)C::SMEM);
+    attr = true;
+  }
+  const int64_t total = kcc * p.tiles_per_segment;
+  if (phase != 1) {
+    k5_scan_seq<MB, SEQ_REDUCE><<<(unsigned)total, C::NT, C::SMEM, s>>>(
+        perm, sval, ldn, n, zt, mc, yt, kcc, p.tiles_per_segment, agg);
+    const int64_t warps = kcc * C::NP;
+    k5_seq_prefix<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(agg, kcc, p.tiles_per_segment,
+                                                              C::NP, 2 * mc, segtot, ld_seg);
+  }
+  if (phase != 0) {
+    k5_scan_seq<MB, SEQ_APPLY><<<(unsigned)total, C::NT, C::SMEM, s>>>(
+        perm, sval, ldn, n, zt, mc, yt, kcc, p.tiles_per_segment, agg);
+  }
+}
+
+void launch_scan_seq(const QueryPlan &p, const uint32_t *perm, const float *sval, int64_t ldn,
+                     int64_t n, const float *zt, int64_t mc, double *yt, int64_t kcc, double *agg,
+                     double *segtot, int64_t ld_seg, int phase, cudaStream_t s) {
+#define L1DM_SEQ(MB) \
+  launch_seq_t<MB>(p, perm, sval, ldn, n, zt, mc, yt, kcc, agg, segtot, ld_seg, phase, s)
+  switch (p.mb) {
+    case 2: L1DM_SEQ(2); break;
+    case 4: L1DM_SEQ(4); break;
+    case 8: L1DM_SEQ(8); break;
+    case 16: L1DM_SEQ(16); break;
+    default: break;
+  }
+#undef L1DM_SEQ
 }
 
 // Single-column variant (m == 1).  Here a tile is cheap (4 B of Z per row, gathered from
@@ -621,7 +890,7 @@ static void launch_scan_t(const QueryPlan &p, bool scatter, const uint32_t *perm
                           int64_t ldn, int64_t n, const float *Z, int64_t ldz, int64_t m,
                           double *U, int64_t k_first, int64_t kcc, uint32_t *flags, double *agg,
                           double *incl, uint32_t epoch, unsigned *ticket, unsigned *timeout_flag,
-                          double *segtot, cudaStream_t s) {
+                          double *segtot, int64_t ld_seg, cudaStream_t s) {
   using C = ScanCfg<LPR, VC, scan_items(LPR, VC)>;
   auto kern = scatter ? k5_scan<LPR, VC, CH, true> : k5_scan<LPR, VC, CH, false>;
   static bool attr = false;
@@ -636,17 +905,18 @@ static void launch_scan_t(const QueryPlan &p, bool scatter, const uint32_t *perm
   const int64_t total = nseg * p.tiles_per_segment;
   kern<<<(unsigned)total, C::NT, C::SMEM, s>>>(perm, sval, ldn, n, Z, ldz, m, U, p.ldu, k_first,
                                                p.col_blocks, nseg, total, flags, agg, incl, epoch,
-                                               ticket, timeout_flag, p.tiles_per_segment, segtot);
+                                               ticket, timeout_flag, p.tiles_per_segment, segtot,
+                                               ld_seg);
 }
 
 void launch_scan(const QueryPlan &p, const uint32_t *perm, const float *sval, int64_t ldn,
                  int64_t n, const float *Z, int64_t ldz, int64_t m, double *U, int64_t k_first,
                  int64_t kcc, uint32_t *flags, double *agg, double *incl, uint32_t epoch,
-                 unsigned *ticket, unsigned *timeout_flag, double *segtot, float *zs,
-                 cudaStream_t s) {
+                 unsigned *ticket, unsigned *timeout_flag, double *segtot, int64_t ld_seg,
+                 float *zs, cudaStream_t s) {
 #define L1DM_SCAN(L, V, CH)                                                                    \
   launch_scan_t<L, V, CH>(p, p.scatter != 0, perm, sval, ldn, n, Z, ldz, m, U, k_first, kcc, flags, \
-                          agg, incl, epoch, ticket, timeout_flag, segtot, s)
+                          agg, incl, epoch, ticket, timeout_flag, segtot, ld_seg, s)
   // p.lpr lanes per row, p.mb / p.lpr columns per lane, p.vec floats per cp.async chunk
   if (p.mb == 1) {
     // reduce-then-scan, no look-back (the agg workspace holds 2 doubles per tile)
@@ -720,6 +990,72 @@ void launch_epilogue(const double *hsum, const double *Sg, double *Y, int64_t ld
   int64_t blocks = ((i1 - i0) * m + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   k7_epilogue<<<(unsigned)blocks, 256, 0, s>>>(hsum, Sg, Y, ldy, i0, i1, m);
+}
+
+// Scatter mode, m > 1: Y[i][c0 + c] = Yt[i][c] + g_c - h_i S_c for one column block (Yt is the
+// block's compact L2-resident accumulator, mb doubles per point).
+__global__ void __launch_bounds__(256)
+    k9_block_out(const double *__restrict__ yt, int mb, int64_t mc, const double *__restrict__ hsum,
+                 const double *__restrict__ S, const double *__restrict__ g, double *__restrict__ Y,
+                 int64_t ldy, int64_t i0, int64_t i1) {
+  const int64_t total = (i1 - i0) * mc;
+  for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * 256) {
+    const int64_t i = i0 + e / mc, c = e - (e / mc) * mc;
+    __stcs(Y + i * ldy + c, yt[i * mb + c] + fma(-hsum[i], S[c], g[c]));
+  }
+}
+
+void launch_block_out(const double *yt, int mb, int64_t mc, const double *hsum, const double *S,
+                      const double *g, double *Y, int64_t ldy, int64_t i0, int64_t i1,
+                      cudaStream_t s) {
+  if (i1 <= i0) return;
+  int64_t blocks = ((i1 - i0) * mc + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k9_block_out<<<(unsigned)blocks, 256, 0, s>>>(yt, mb, mc, hsum, S, g, Y, ldy, i0, i1);
+}
+
+// ------------------------------------------------------------------ scatter-mode Z blocks
+// Zt[cb][i][0..mb) = Z[i][cb*mb ..] zero-padded past m.  Thread e -> (row i = e / cb_count,
+// block cb = e % cb_count): a warp reads whole Z rows and writes full sectors of each block.
+template <int MB>
+__global__ void __launch_bounds__(256)
+    k8_zt(const float *__restrict__ Z, int64_t ldz, int64_t n, int64_t m, int64_t ncb,
+          float *__restrict__ zt, int vec4) {
+  const int64_t total = n * ncb;
+  for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * 256) {
+    const int64_t i = e / ncb, cb = e - (e / ncb) * ncb;
+    const int64_t c0 = cb * MB;
+    const float *src = Z + i * ldz + c0;
+    float *dst = zt + (cb * n + i) * MB;
+    if constexpr (MB % 4 == 0) {
+      if (vec4 && c0 + MB <= m) {
+#pragma unroll
+        for (int q = 0; q < MB; q += 4)
+          reinterpret_cast<float4 *>(dst)[q / 4] = __ldcs(reinterpret_cast<const float4 *>(src + q));
+        continue;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < MB; ++q) dst[q] = (c0 + q < m) ? __ldcs(src + q) : 0.0f;
+  }
+}
+
+void launch_zt(const float *Z, int64_t ldz, int64_t n, int64_t m, int mb, float *zt,
+               cudaStream_t s) {
+  const int64_t ncb = (m + mb - 1) / mb;
+  const int vec4 = (ldz % 4 == 0 && reinterpret_cast<uintptr_t>(Z) % 16 == 0) ? 1 : 0;
+  int64_t blocks = (n * ncb + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  switch (mb) {
+    case 2: k8_zt<2><<<(unsigned)blocks, 256, 0, s>>>(Z, ldz, n, m, ncb, zt, vec4); break;
+    case 4: k8_zt<4><<<(unsigned)blocks, 256, 0, s>>>(Z, ldz, n, m, ncb, zt, vec4); break;
+    case 8: k8_zt<8><<<(unsigned)blocks, 256, 0, s>>>(Z, ldz, n, m, ncb, zt, vec4); break;
+    case 16: k8_zt<16><<<(unsigned)blocks, 256, 0, s>>>(Z, ldz, n, m, ncb, zt, vec4); break;
+    case 32: k8_zt<32><<<(unsigned)blocks, 256, 0, s>>>(Z, ldz, n, m, ncb, zt, vec4); break;
+    default: break;
+  }
 }
 
 // ------------------------------------------------------------------ K6

@@ -33,7 +33,7 @@ class ShardedL1DM:
 
     def __init__(self, X: torch.Tensor, group=None, *, k_range=None,
                  local_prepare: Optional[Callable] = None,
-                 local_matvec: Optional[Callable] = None, stream=None):
+                 local_matvec: Optional[Callable] = None, stream=None, mode: str = "auto"):
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -45,6 +45,8 @@ class ShardedL1DM:
         self.stream = stream
         if self.k_end > self.k_begin:
             self.handle = self._prepare(X, self.k_begin, self.k_end, stream=stream)
+            if mode != "auto" and self._prepare is binding.l1dm_prepare:
+                binding.l1dm_set_query_mode(self.handle, mode)
         else:
             self.handle = None  # more ranks than coordinates: this rank contributes zeros
 

@@ -55,11 +55,26 @@ for r in rows[2:]:
     sc = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}
     rb = float(r[hdr.index("dram__bytes_read.sum")]) * sc[units[hdr.index("dram__bytes_read.sum")]]
     wb = float(r[hdr.index("dram__bytes_write.sum")]) * sc[units[hdr.index("dram__bytes_write.sum")]]
-    kind = ("scan" if "scan" in name else "accumulate" if "accumulate" in name else name.split("(")[0])
+    if "k5_scan_seq" in name:  # scatter mode: <mb, 0> reduce (timing kind scan), <mb, 1> apply
+        kind = "scatter_accumulate" if ", 1>" in name or ",1>" in name else "scatter_scan"
+    elif "k5_scan" in name or "k6_accumulate" in name:
+        kind = "gather_" + ("scan" if "scan" in name else "accumulate")
+    else:
+        kind = name.split("(")[0]
     traffic.setdefault(kind, rb + wb)
 open(f"profiles/{tag}_{w}_ncu_full.txt", "w").write("\n".join(lines) + "\n")
-json.dump({**traffic, "unit": "bytes per launch (dram read+write)",
-           "source": f"profiles/{tag}_{w}_ncu_full.txt"},
-          open(f"profiles/ncu_traffic_{w}.json", "w"), indent=1)
+out_json = f"profiles/ncu_traffic_{w}.json"
+try:
+    old = json.load(open(out_json))
+except Exception:
+    old = {}
+old.pop("scan", None)
+old.pop("accumulate", None)
+sources = old.pop("sources", {})
+for k in traffic:
+    sources[k] = f"profiles/{tag}_{w}_ncu_full.txt"
+json.dump({**{k: v for k, v in old.items() if k not in ("unit", "source")}, **traffic,
+           "unit": "bytes per launch (dram read+write)", "sources": sources},
+          open(out_json, "w"), indent=1)
 print("\n".join(out))
 print(json.dumps(traffic, indent=1))

@@ -151,12 +151,16 @@ def sample_rows(n, Y=None, count=24, seed=0):
 
 # ---- full BASELINE.json sizes, in the bench's launch configuration, on sampled rows ----
 @pytest.mark.slow
-@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
-def test_workload_full_size_sampled(name):
+@pytest.mark.parametrize("name,mode", [("c1", "auto"), ("c2", "auto"), ("c3", "auto"),
+                                       ("c4", "auto"), ("c5", "auto"), ("c3", "gather"),
+                                       ("c2", "gather")])
+def test_workload_full_size_sampled(name, mode):
+    """Auto is the bench's launch configuration (c2, c3: scatter mode; c4, c5: gather)."""
     w = wl.workload(name)
     X = wl.make_points(w, "cuda")
     Z = wl.make_query(w, 0, "cuda")
     h = l1.l1dm_prepare(X)
+    l1.l1dm_set_query_mode(h, mode)
     Y = l1.l1dm_matvec(h, Z)
     torch.cuda.synchronize()
     l1.l1dm_sync(h)

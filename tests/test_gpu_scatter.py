@@ -1,0 +1,125 @@
+"""Scatter-mode query (L1DM_MODE_SCATTER: per column block, the scan adds 2U into an
+L2-resident block accumulator with fp64 reductions; include/l1dm.h) against the CPU oracle.
+
+The planner picks this mode for n >= 2^17 when a block fits L2, so small
+parity cases force it per handle; the full-size c3 case runs it by default (bench config).
+Bar as in test_gpu_parity.py: per-column relative l2 <= 1e-9 on float data, bit-exact on
+integer data (every partial sum is an integer < 2^53)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2210_15114_b200 as l1
+from conftest import col_rel_l2
+from gpu_util import gpu_matvec
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+# m spans block widths 2 / 4 / 8 and ragged last blocks; n spans the 1024-row tiles' edges.
+CASES = [(1, 1, 2), (2, 1, 3), (3, 2, 2), (100, 3, 4), (1023, 2, 5), (1024, 3, 8), (1025, 2, 9),
+         (2047, 3, 16), (3073, 4, 7), (5000, 2, 17), (700, 5, 64), (1500, 3, 65), (4097, 2, 3)]
+
+
+@pytest.mark.parametrize("n,d,m", CASES)
+def test_scatter_random_float_vs_brute(n, d, m):
+    rng = np.random.default_rng(n * 977 + d * 31 + m)
+    X = rng.standard_normal((n, d)).astype(np.float32)
+    Z = rng.standard_normal((n, m)).astype(np.float32)
+    Yr = oracle.brute(X, Z)
+    Ys = gpu_matvec(X, Z, mode="scatter")
+    if n == 1:
+        assert np.all(Ys == 0)
+    else:
+        assert col_rel_l2(Ys, Yr) <= TOL
+
+
+@pytest.mark.parametrize("n,d,m", [(4099, 3, 2), (3000, 4, 4), (2500, 2, 7), (1500, 3, 32)])
+def test_scatter_integer_ties_exact(n, d, m):
+    rng = np.random.default_rng(7 * n + m + 1)
+    X = rng.integers(0, 5, size=(n, d)).astype(np.float32)
+    Z = rng.integers(-3, 4, size=(n, m)).astype(np.float32)
+    assert np.array_equal(gpu_matvec(X, Z, mode="scatter"),
+                          oracle.hist(X, Z, M=4).astype(np.float64))
+
+
+def test_scatter_and_gather_agree_on_one_handle():
+    """Switching the mode on a live handle reuses/reallocates the workspace correctly."""
+    rng = np.random.default_rng(3)
+    X = rng.standard_normal((6000, 5)).astype(np.float32)
+    h = l1.l1dm_prepare(torch.from_numpy(X).cuda())
+    for mode, m in [("scatter", 12), ("gather", 12), ("scatter", 3), ("auto", 12), ("scatter", 40)]:
+        Z = rng.standard_normal((6000, m)).astype(np.float32)
+        l1.l1dm_set_query_mode(h, mode)
+        Y = l1.l1dm_matvec(h, torch.from_numpy(Z).cuda())
+        torch.cuda.synchronize()
+        assert col_rel_l2(Y.cpu().numpy(), oracle.brute(X, Z)) <= TOL, mode
+    l1.l1dm_sync(h)
+    l1.l1dm_free(h)
+
+
+def test_scatter_strided_and_host_pointers():
+    rng = np.random.default_rng(12)
+    X = rng.standard_normal((3000, 4)).astype(np.float32)
+    Zw = torch.from_numpy(rng.standard_normal((3000, 13)).astype(np.float32))
+    Yr = oracle.brute(X, Zw[:, 1:11].contiguous().numpy())
+    h = l1.l1dm_prepare(torch.from_numpy(X).cuda())
+    l1.l1dm_set_query_mode(h, "scatter")
+    Yg = l1.l1dm_matvec(h, Zw.cuda()[:, 1:11])          # ld_z = 13, misaligned base
+    torch.cuda.synchronize()
+    assert col_rel_l2(Yg.cpu().numpy(), Yr) <= TOL
+    Yh = l1.l1dm_matvec(h, Zw[:, 1:11].contiguous().numpy())   # host in, host out
+    assert col_rel_l2(Yh.numpy(), Yr) <= TOL
+    import ctypes                                         # strided Y (ld_y = 14 > m = 10)
+    Yw = torch.full((3000, 14), float("nan"), dtype=torch.float64, device="cuda")
+    Zc = Zw[:, 1:11].contiguous().cuda()
+    rc = l1.load_library().l1dm_matvec_ex(
+        h.ptr, ctypes.c_void_p(Zc.data_ptr()), 10, 10, ctypes.c_void_p(Yw[:, 2:].data_ptr()), 14,
+        ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == 0
+    torch.cuda.synchronize()
+    l1.l1dm_sync(h)
+    assert col_rel_l2(Yw[:, 2:12].cpu().numpy(), Yr) <= TOL
+    assert torch.isnan(Yw[:, :2]).all() and torch.isnan(Yw[:, 12:]).all()
+    l1.l1dm_free(h)
+
+
+@pytest.mark.parametrize("m,blocks", [(4, 5), (20, 3)])
+def test_scatter_pipelined_point_blocks(m, blocks):
+    rng = np.random.default_rng(90 + m)
+    X = rng.standard_normal((7001, 5)).astype(np.float32)
+    Z = rng.standard_normal((7001, m)).astype(np.float32)
+    h = l1.l1dm_prepare(torch.from_numpy(X).cuda())
+    l1.l1dm_set_query_mode(h, "scatter")
+    Y = torch.full((7001, m), float("nan"), dtype=torch.float64, device="cuda")
+    evs = [torch.cuda.Event() for _ in range(blocks)]
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    l1.l1dm_matvec_pipelined(h, torch.from_numpy(Z).cuda(), Y, evs, stream=side)
+    Yr = oracle.brute(X, Z)
+    for (i0, i1), ev in zip(l1.point_blocks(7001, blocks), evs):
+        ev.synchronize()
+        assert col_rel_l2(Y[i0:i1].cpu().numpy(), Yr[i0:i1]) <= TOL
+    torch.cuda.synchronize()
+    l1.l1dm_sync(h)
+    l1.l1dm_free(h)
+
+
+def test_scatter_degenerate():
+    rng = np.random.default_rng(2)
+    X = rng.standard_normal((300, 3)).astype(np.float32)
+    Z = rng.standard_normal((300, 6)).astype(np.float32)
+    assert np.all(gpu_matvec(X, np.zeros_like(Z), mode="scatter") == 0)
+    E = np.eye(300, dtype=np.float32)[:, :16]
+    A = gpu_matvec(X, E, mode="scatter")
+    D = np.abs(X[:, None, :].astype(np.float64) - X[None, :16, :].astype(np.float64)).sum(-1)
+    assert np.allclose(A, D, rtol=1e-12, atol=1e-12)                  # A e_j = column j
+
+
+def test_scatter_sharded_coordinates_exact():
+    rng = np.random.default_rng(16)
+    X = rng.integers(0, 9, size=(4000, 7)).astype(np.float32)
+    Z = rng.integers(-2, 3, size=(4000, 10)).astype(np.float32)
+    parts = [gpu_matvec(X, Z, a, b, mode="scatter") for a, b in [(0, 2), (2, 3), (3, 7)]]
+    assert np.array_equal(sum(parts), oracle.hist(X, Z, M=8).astype(np.float64))

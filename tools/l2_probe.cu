@@ -1,0 +1,115 @@
+// l2_probe.cu — measures the L2-side ceilings that bound the scatter-mode query
+// on the local B200 and prints one JSON object (committed as profiles/l2_peaks.json):
+//   red_row8_adds_per_s   fp64 reductions, 8 consecutive doubles (one 64-B row) per request,
+//                         random rows of an L2-resident 64 MiB buffer (the apply pass's REDs)
+//   gather_sector_GBps    random 32-B sector reads of an L2-resident 32 MiB buffer (Zt gathers)
+//   stream_read_GBps      sequential reads of an L2-resident 32 MiB buffer
+// Row indices come from a streamed index array (4 B per row, like perm).  CUDA-event timed,
+// best of 5 after a warm-up launch.  Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__global__ void fill_idx(uint32_t *idx, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t x = (uint64_t)i * 0x9E3779B97F4A7C15ull;
+    x ^= x >> 29; x *= 0xBF58476D1CE4E5B9ull; x ^= x >> 32;
+    idx[i] = (uint32_t)x;
+  }
+}
+// 8 lanes per 64-B row, 4 rows per warp per step, 4 steps in flight
+__global__ void __launch_bounds__(256) red_rows(const uint32_t *idx, int64_t rows, double *y,
+                                                uint32_t yrows) {
+  const int lane = threadIdx.x & 31, c = lane & 7, g = lane >> 3;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = warp * 16; base < rows; base += nw * 16) {
+    uint32_t p[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) p[u] = __ldcs(idx + base + u * 4 + g);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) atomicAdd(y + (int64_t)(p[u] % yrows) * 8 + c, 1.0);
+  }
+}
+// one 32-B sector per row: 8 lanes x 4 B
+__global__ void __launch_bounds__(256) gather_sectors(const uint32_t *idx, int64_t rows,
+                                                      const float *z, uint32_t zrows,
+                                                      float *out) {
+  const int lane = threadIdx.x & 31, c = lane & 7, g = lane >> 3;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  float acc = 0.f;
+  for (int64_t base = warp * 16; base < rows; base += nw * 16) {
+    uint32_t p[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) p[u] = __ldcs(idx + base + u * 4 + g);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc += __ldcg(z + (int64_t)(p[u] % zrows) * 8 + c);
+  }
+  if (acc == 1.2345f) out[0] = acc;
+}
+__global__ void __launch_bounds__(256) stream_read(const float4 *z, int64_t n4, int reps,
+                                                   float *out) {
+  float acc = 0.f;
+  for (int r = 0; r < reps; ++r)
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const float4 v = __ldcg(z + i);
+      acc += v.x + v.y + v.z + v.w;
+    }
+  if (acc == 1.2345f) out[0] = acc;
+}
+template <typename F>
+static float best_ms(F f) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  f();
+  cudaDeviceSynchronize();
+  float best = 1e30f;
+  for (int i = 0; i < 5; ++i) {
+    cudaEventRecord(a);
+    f();
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (ms < best) best = ms;
+  }
+  return best;
+}
+int main() {
+  int dev = 0, sms = 0, l2 = 0, clk = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev);
+  const int64_t rows = 1ll << 27;
+  uint32_t *idx;
+  double *y;
+  float *z, *out;
+  if (cudaMalloc(&idx, rows * 4) || cudaMalloc(&y, 64ll << 20) || cudaMalloc(&z, 32ll << 20) ||
+      cudaMalloc(&out, 64)) {
+    printf("{\"error\": \"alloc\"}\n");
+    return 1;
+  }
+  cudaMemset(y, 0, 64ll << 20);
+  cudaMemset(z, 0, 32ll << 20);
+  fill_idx<<<sms * 8, 256>>>(idx, rows);
+  const int grid = sms * 8;
+  const uint32_t yrows = (uint32_t)((64ll << 20) / 64), zrows = (uint32_t)((32ll << 20) / 32);
+  const float t_red = best_ms([&] { red_rows<<<grid, 256>>>(idx, rows, y, yrows); });
+  const float t_gat = best_ms([&] { gather_sectors<<<grid, 256>>>(idx, rows, z, zrows, out); });
+  const int reps = 64;
+  const float t_str = best_ms([&] {
+    stream_read<<<grid, 256>>>(reinterpret_cast<const float4 *>(z), (32ll << 20) / 16, reps, out);
+  });
+  const cudaError_t e = cudaGetLastError();
+  printf("{\"red_row8_adds_per_s\": %.4g, \"gather_sector_GBps\": %.1f, "
+         "\"stream_read_GBps\": %.1f, \"sms\": %d, \"l2_bytes\": %d, \"sm_clock_khz\": %d, "
+         "\"status\": \"%s\", \"how\": \"tools/l2_probe.cu: 2^27 random rows, L2-resident "
+         "buffers (RED 64 MiB, gather 32 MiB), best of 5 CUDA-event timings\"}\n",
+         rows * 8.0 / (t_red * 1e-3), rows * 32.0 / (t_gat * 1e-3) / 1e9,
+         (32ll << 20) * (double)reps / (t_str * 1e-3) / 1e9, sms, l2, clk, cudaGetErrorString(e));
+  return e == cudaSuccess ? 0 : 1;
+}
