@@ -47,8 +47,12 @@ def _load():
         lib.oracle_alg2_range.argtypes = [vp, i64, i64, vp, i64, i64, vp, i64, vp, i32]
         lib.oracle_hist.argtypes = [vp, i64, i64, vp, i64, i64, vp, i32]
         lib.oracle_num_threads.argtypes = [i32]
+        lib.oracle_brute_lp.argtypes = [vp, i64, i64, vp, i64, i32, vp, i32]
+        lib.oracle_lp_sorted.argtypes = [vp, i64, i64, vp, vp, i64, i32, vp, i32]
+        lib.oracle_brute_tv.argtypes = [vp, i64, i64, vp, i64, vp, i32]
         for f in (lib.oracle_brute, lib.oracle_rows, lib.oracle_alg1, lib.oracle_alg2,
-                  lib.oracle_alg2_range, lib.oracle_hist, lib.oracle_num_threads):
+                  lib.oracle_alg2_range, lib.oracle_hist, lib.oracle_num_threads,
+                  lib.oracle_brute_lp, lib.oracle_lp_sorted, lib.oracle_brute_tv):
             f.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -150,4 +154,38 @@ def hist(X, Z, M: int = 255, nthreads: int = 0) -> np.ndarray:
     Z2 = _as2d(Z, n)
     Y = np.empty((n, Z2.shape[1]), dtype=np.int64)
     _check(_load().oracle_hist(_ptr(X), n, d, _ptr(Z2), Z2.shape[1], M, _ptr(Y), nthreads), "hist")
+    return Y.reshape(-1) if np.ndim(Z) == 1 else Y
+
+
+def brute_lp(X, Z, p: int, nthreads: int = 0) -> np.ndarray:
+    """l_p^p definition: Y[i,c] = sum_j Z[j,c] sum_k |x_ik - x_jk|^p (Thm. odd_p)."""
+    X = _f32(X)
+    n, d = X.shape
+    Z2 = _as2d(Z, n)
+    Y = np.empty((n, Z2.shape[1]), dtype=np.float64)
+    _check(_load().oracle_brute_lp(_ptr(X), n, d, _ptr(Z2), Z2.shape[1], int(p), _ptr(Y),
+                                   nthreads), "brute_lp")
+    return Y.reshape(-1) if np.ndim(Z) == 1 else Y
+
+
+def lp_sorted(X, Z, p: int, nthreads: int = 0) -> np.ndarray:
+    """Odd p with Alg. 1's sort: SPEC S:150-158's construction in Alg. 2's shape."""
+    X = _f32(X)
+    n, d = X.shape
+    _, order = alg1(X, nthreads)
+    Z2 = _as2d(Z, n)
+    Y = np.empty((n, Z2.shape[1]), dtype=np.float64)
+    _check(_load().oracle_lp_sorted(_ptr(X), n, d, _ptr(np.ascontiguousarray(order)), _ptr(Z2),
+                                    Z2.shape[1], int(p), _ptr(Y), nthreads), "lp_sorted")
+    return Y.reshape(-1) if np.ndim(Z) == 1 else Y
+
+
+def brute_tv(X, Z, nthreads: int = 0) -> np.ndarray:
+    """TV definition: Y[i,c] = sum_j Z[j,c] (1/2) sum_k |x_ik - x_jk| (Thm. tv)."""
+    X = _f32(X)
+    n, d = X.shape
+    Z2 = _as2d(Z, n)
+    Y = np.empty((n, Z2.shape[1]), dtype=np.float64)
+    _check(_load().oracle_brute_tv(_ptr(X), n, d, _ptr(Z2), Z2.shape[1], _ptr(Y), nthreads),
+           "brute_tv")
     return Y.reshape(-1) if np.ndim(Z) == 1 else Y

@@ -21,6 +21,13 @@
  *   oracle_hist       — integer alphabets only: the definition regrouped by
  *                       coordinate value, evaluated exactly in int64
  *   oracle_rows       — the definition for a chosen set of rows (full-size spot checks)
+ *   oracle_brute_lp   — l_p^p, the definition: sum_j z_j sum_k |x_ik - x_jk|^p
+ *                       ("A_ij = ||x_i - x_j||_p^p", Thm. odd_p)
+ *   oracle_lp_sorted  — odd p, SPEC S:150-158's construction over Alg. 1's order, written
+ *                       in Alg. 2's shape: per coordinate and power t, inclusive partial
+ *                       sums in sorted order of z_j x_j^(p-t); per point, below/above split
+ *                       at its position; y_k += sum_t C(p,t) (-1)^(p-t) x_k^t (below - above)
+ *   oracle_brute_tv   — TV(x, y) = (1/2) sum_k |x_k - y_k|, the definition (Thm. tv)
  *
  * Precision: inputs are fp32 (BASELINE.json); every sum is accumulated in
  * x86 80-bit long double ("fp64 or better", reading R6) and
@@ -350,5 +357,131 @@ int oracle_hist(const float *X, int64_t n, int64_t d, const float *Z, int64_t m,
   }
   hist_args a = {X, n, d, Z, m, M, Y};
   run_parallel(hist_columns, &a, m, 1, nthreads);
+  return ORACLE_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* l_p^p (A_ij = ||x_i - x_j||_p^p; Thm. odd_p P:485-487 for odd p; any p >= 1 here).
+ * The definition: Y[i][c] = sum_j Z[j][c] * sum_k |X[i][k] - X[j][k]|^p, long double.      */
+/* ------------------------------------------------------------------ */
+typedef struct {
+  const float *X; int64_t n, d;
+  const float *Z; int64_t m;
+  int p;
+  double scale;          /* 1 for l_p^p; 1/2 for TV (p = 1) */
+  double *Y;
+} lp_args;
+
+static acc_t powi_l(acc_t a, int p) {
+  acc_t r = 1.0L;
+  for (int q = 0; q < p; ++q) r *= a;
+  return r;
+}
+
+static void brute_lp_rows(void *pa, int64_t lo, int64_t hi) {
+  lp_args *a = (lp_args *)pa;
+  acc_t *acc = (acc_t *)malloc(sizeof(acc_t) * (size_t)a->m);
+  for (int64_t i = lo; i < hi; ++i) {
+    for (int64_t c = 0; c < a->m; ++c) acc[c] = 0.0L;
+    const float *xi = a->X + i * a->d;
+    for (int64_t j = 0; j < a->n; ++j) {
+      const float *xj = a->X + j * a->d;
+      acc_t dist = 0.0L;                                  /* ||x_i - x_j||_p^p */
+      for (int64_t k = 0; k < a->d; ++k) dist += powi_l(fabsl((acc_t)xi[k] - (acc_t)xj[k]), a->p);
+      dist *= (acc_t)a->scale;
+      const float *zj = a->Z + j * a->m;
+      for (int64_t c = 0; c < a->m; ++c) acc[c] += dist * (acc_t)zj[c];
+    }
+    for (int64_t c = 0; c < a->m; ++c) a->Y[i * a->m + c] = (double)acc[c];
+  }
+  free(acc);
+}
+
+int oracle_brute_lp(const float *X, int64_t n, int64_t d, const float *Z, int64_t m, int p,
+                    double *Y, int nthreads) {
+  if (!X || !Z || !Y || n < 1 || d < 1 || m < 1 || p < 1) return ORACLE_EINVAL;
+  lp_args a = {X, n, d, Z, m, p, 1.0, Y};
+  run_parallel(brute_lp_rows, &a, n, 4, nthreads);
+  return ORACLE_OK;
+}
+
+/* TV (Thm. tv): TV(x, y) = (1/2) ||x - y||_1 for distributions x, y. */
+int oracle_brute_tv(const float *X, int64_t n, int64_t d, const float *Z, int64_t m, double *Y,
+                    int nthreads) {
+  if (!X || !Z || !Y || n < 1 || d < 1 || m < 1) return ORACLE_EINVAL;
+  lp_args a = {X, n, d, Z, m, 1, 0.5, Y};
+  run_parallel(brute_lp_rows, &a, n, 4, nthreads);
+  return ORACLE_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* Odd p with the sort (the paper omits the proof).  For odd p,
+ * |a - b|^p = sign(a - b) (a - b)^p and (x_k - x_j)^p = sum_t C(p,t) x_k^t (-x_j)^(p-t), so
+ * with the points split at x_k's position in T_i (below: x_j <= x_k, above: x_j > x_k):
+ *   sum_j z_j |x_k(i) - x_j(i)|^p
+ *     = sum_t C(p,t) (-1)^(p-t) x_k(i)^t [ sum_below z_j x_j(i)^(p-t) - sum_above z_j x_j(i)^(p-t) ].
+ * In Alg. 2's shape: for each t, B_t[q] = inclusive partial sums over sorted
+ * positions 1..q of z_j x_j(i)^(p-t); q = position of x_k(i); below = B_t[q] (self included:
+ * it contributes (x_k - x_k)^p = 0), above = B_t[n] - B_t[q].  `order` is Alg. 1's output.  */
+/* ------------------------------------------------------------------ */
+typedef struct {
+  const float *X; int64_t n, d;
+  const uint32_t *order;
+  const float *Z; int64_t m;
+  int p;
+  double *Y;
+} lps_args;
+
+static void lp_sorted_columns(void *pa, int64_t lo, int64_t hi) {
+  lps_args *a = (lps_args *)pa;
+  const int64_t n = a->n;
+  const int p = a->p;
+  acc_t *B = (acc_t *)malloc(sizeof(acc_t) * (size_t)(n + 1) * (size_t)(p + 1));
+  uint32_t *pos = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)n);
+  acc_t *z = (acc_t *)malloc(sizeof(acc_t) * (size_t)n);
+  acc_t binom[16];
+  binom[0] = 1.0L;                                   /* C(p, t), t = 0..p */
+  for (int t = 1; t <= p; ++t) binom[t] = binom[t - 1] * (acc_t)(p - t + 1) / (acc_t)t;
+  for (int64_t c = lo; c < hi; ++c) {
+    for (int64_t k = 0; k < n; ++k) z[k] = 0.0L;
+    for (int64_t i = 0; i < a->d; ++i) {
+      const uint32_t *pi = a->order + i * n;
+      for (int t = 0; t <= p; ++t) B[(size_t)t * (n + 1)] = 0.0L;
+      for (int64_t q = 1; q <= n; ++q) {
+        int64_t j = pi[q - 1];                       /* point at sorted position q */
+        acc_t yj = (acc_t)a->Z[j * a->m + c];
+        acc_t xji = (acc_t)a->X[j * a->d + i];
+        for (int t = 0; t <= p; ++t) {
+          acc_t *Bt = B + (size_t)t * (n + 1);
+          Bt[q] = Bt[q - 1] + yj * powi_l(xji, p - t);
+        }
+        pos[j] = (uint32_t)q;
+      }
+      for (int64_t k = 0; k < n; ++k) {
+        int64_t q = pos[k];
+        acc_t xki = (acc_t)a->X[k * a->d + i];
+        acc_t sum = 0.0L;
+        for (int t = 0; t <= p; ++t) {
+          const acc_t *Bt = B + (size_t)t * (n + 1);
+          acc_t below = Bt[q], above = Bt[n] - Bt[q];
+          acc_t sgn = ((p - t) & 1) ? -1.0L : 1.0L;  /* (-1)^(p-t) */
+          sum += binom[t] * sgn * powi_l(xki, t) * (below - above);
+        }
+        z[k] += sum;
+      }
+    }
+    for (int64_t k = 0; k < n; ++k) a->Y[k * a->m + c] = (double)z[k];
+  }
+  free(B);
+  free(pos);
+  free(z);
+}
+
+int oracle_lp_sorted(const float *X, int64_t n, int64_t d, const uint32_t *order,
+                     const float *Z, int64_t m, int p, double *Y, int nthreads) {
+  if (!X || !order || !Z || !Y || n < 1 || d < 1 || m < 1 || p < 1 || p > 15 || !(p & 1))
+    return ORACLE_EINVAL;
+  lps_args a = {X, n, d, order, Z, m, p, Y};
+  run_parallel(lp_sorted_columns, &a, m, 1, nthreads);
   return ORACLE_OK;
 }

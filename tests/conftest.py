@@ -32,7 +32,18 @@ def load_golden(name):
     return X, Z, Y
 
 
+def golden_p(name):
+    """The fixture's exponent p (l_p^p fixtures carry a 'p:' line; l1 fixtures are p = 1)."""
+    path = os.path.join(ROOT, "tests", "golden", name)
+    for line in open(path):
+        if line.startswith("p:"):
+            return int(line.split(":", 1)[1])
+    return 1
+
+
 GOLDEN = ["q1_three_points.txt", "q2_identity.txt", "q20_two_dim.txt", "q21_ties_negative.txt"]
+GOLDEN_LP = ["lp3_three_points.txt", "lp5_two_dim.txt"]
+GOLDEN_TV = ["tv_two_points.txt"]
 
 
 def col_rel_l2(Y, Yref, floor=0.0):
