@@ -54,7 +54,8 @@ typedef enum {
   L1DM_ECUDA = -4,      /* a CUDA runtime error (message in l1dm_last_error) */
   L1DM_EDEVICE = -5,    /* no sm_100 device, or the handle belongs to another device */
   L1DM_ENOTIMPL = -6,
-  L1DM_ETIMEOUT = -7    /* a look-back wait exceeded its bound (never expected; results invalid) */
+  L1DM_ETIMEOUT = -7,   /* a look-back wait exceeded its bound (never expected; results invalid) */
+  L1DM_ENOTSIMPLEX = -8 /* TV query on rows that are not probability vectors (Thm. tv) */
 } l1dm_status;
 
 /* ---------------------------------------------------------------------------
@@ -112,6 +113,34 @@ L1DM_API l1dm_status l1dm_matvec_ex(l1dm_handle h, const float *Z, int64_t ld_z,
 L1DM_API l1dm_status l1dm_matvec_pipelined(l1dm_handle h, const float *Z, int64_t ld_z, int64_t m,
                                            double *Y, int64_t ld_y, void *stream,
                                            int64_t point_blocks, void *const *block_events);
+
+/* ---------------------------------------------------------------------------
+ * l_p^p for odd p (Thm. odd_p: "O(nd log n) preprocessing and
+ * O(ndp) query"; the paper omits the construction, SPEC S:150-158 gives it):
+ *   Y = A_p Z,  (A_p)_ij = ||x_i - x_j||_p^p = sum_k |x_ik - x_jk|^p,  p in {1, 3, 5, 7}.
+ * Same prepared state as l1dm_matvec (the sort of Alg. 1).  Per coordinate the query carries
+ * the p+1 prefix moments M_t(r) = sum_{r'<r} z_{perm(r')} v_{r'}^t in sorted order, and
+ *   y_i += sum_t C(p,t) (-1)^t x_ik^(p-t) (2 M_t(rank_k(i)) - M_t(n))
+ * (|a - b|^p = sign(a - b)(a - b)^p for odd p, binomial expansion).  p = 1 is l1dm_matvec.
+ * fp64 throughout; the moments of large |x| lose relative accuracy with p (R18).
+ * Layouts, streams, host/device pointers and errors as l1dm_matvec_ex, plus EINVAL for p not
+ * in {1, 3, 5, 7}.  Sharded handles return the shard's partial product. */
+L1DM_API l1dm_status l1dm_matvec_lp_ex(l1dm_handle h, int p, const float *Z, int64_t ld_z,
+                                       int64_t m, double *Y, int64_t ld_y, void *stream);
+L1DM_API l1dm_status l1dm_matvec_lp(l1dm_handle h, int p, const float *Z, int64_t m, double *Y);
+
+/* ---------------------------------------------------------------------------
+ * Total variation (Thm. tv: "follows immediately from our l1 result"):
+ *   Y = A_TV Z,  (A_TV)_ij = TV(x_i, x_j) = ||x_i - x_j||_1 / 2,
+ * for rows x_i on the probability simplex.  The first TV call on a handle checks
+ * the prepared data once (one small reduction and a synchronisation): every coordinate >= 0 and,
+ * when the handle holds whole rows (k_begin = 0, k_end = ld_x), |sum_k x_ik - 1| <= 1e-9 +
+ * d 2^-23 (fp32 rounding of the entries, R17); otherwise ENOTSIMPLEX.  A coordinate
+ * shard can only check non-negativity: the caller owns the row-sum check across shards.
+ * Layouts, streams, pointers and other errors as l1dm_matvec_ex. */
+L1DM_API l1dm_status l1dm_tv_matvec_ex(l1dm_handle h, const float *Z, int64_t ld_z, int64_t m,
+                                       double *Y, int64_t ld_y, void *stream);
+L1DM_API l1dm_status l1dm_tv_matvec(l1dm_handle h, const float *Z, int64_t m, double *Y);
 
 /* Release every buffer the handle owns.  NULL is a no-op.  Synchronises the
  * handle's stream first. */

@@ -50,9 +50,11 @@ def _load():
         lib.oracle_brute_lp.argtypes = [vp, i64, i64, vp, i64, i32, vp, i32]
         lib.oracle_lp_sorted.argtypes = [vp, i64, i64, vp, vp, i64, i32, vp, i32]
         lib.oracle_brute_tv.argtypes = [vp, i64, i64, vp, i64, vp, i32]
+        lib.oracle_rows_lp.argtypes = [vp, i64, i64, vp, i64, i32, vp, i64, vp, i32]
         for f in (lib.oracle_brute, lib.oracle_rows, lib.oracle_alg1, lib.oracle_alg2,
                   lib.oracle_alg2_range, lib.oracle_hist, lib.oracle_num_threads,
-                  lib.oracle_brute_lp, lib.oracle_lp_sorted, lib.oracle_brute_tv):
+                  lib.oracle_brute_lp, lib.oracle_lp_sorted, lib.oracle_brute_tv,
+                  lib.oracle_rows_lp):
             f.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -166,6 +168,18 @@ def brute_lp(X, Z, p: int, nthreads: int = 0) -> np.ndarray:
     _check(_load().oracle_brute_lp(_ptr(X), n, d, _ptr(Z2), Z2.shape[1], int(p), _ptr(Y),
                                    nthreads), "brute_lp")
     return Y.reshape(-1) if np.ndim(Z) == 1 else Y
+
+
+def rows_lp(X, Z, p: int, row_ids, nthreads: int = 0) -> np.ndarray:
+    """l_p^p definition for the listed rows only: returns len(row_ids) x m."""
+    X = _f32(X)
+    n, d = X.shape
+    Z2 = _as2d(Z, n)
+    r = np.ascontiguousarray(row_ids, dtype=np.int64)
+    Y = np.empty((r.shape[0], Z2.shape[1]), dtype=np.float64)
+    _check(_load().oracle_rows_lp(_ptr(X), n, d, _ptr(Z2), Z2.shape[1], int(p), _ptr(r),
+                                  r.shape[0], _ptr(Y), nthreads), "rows_lp")
+    return Y
 
 
 def lp_sorted(X, Z, p: int, nthreads: int = 0) -> np.ndarray:

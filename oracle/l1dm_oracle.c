@@ -370,6 +370,7 @@ typedef struct {
   int p;
   double scale;          /* 1 for l_p^p; 1/2 for TV (p = 1) */
   double *Y;
+  const int64_t *rows;   /* NULL: rows 0..n-1; else output row t is point rows[t] */
 } lp_args;
 
 static acc_t powi_l(acc_t a, int p) {
@@ -381,7 +382,8 @@ static acc_t powi_l(acc_t a, int p) {
 static void brute_lp_rows(void *pa, int64_t lo, int64_t hi) {
   lp_args *a = (lp_args *)pa;
   acc_t *acc = (acc_t *)malloc(sizeof(acc_t) * (size_t)a->m);
-  for (int64_t i = lo; i < hi; ++i) {
+  for (int64_t t = lo; t < hi; ++t) {
+    const int64_t i = a->rows ? a->rows[t] : t;
     for (int64_t c = 0; c < a->m; ++c) acc[c] = 0.0L;
     const float *xi = a->X + i * a->d;
     for (int64_t j = 0; j < a->n; ++j) {
@@ -392,7 +394,7 @@ static void brute_lp_rows(void *pa, int64_t lo, int64_t hi) {
       const float *zj = a->Z + j * a->m;
       for (int64_t c = 0; c < a->m; ++c) acc[c] += dist * (acc_t)zj[c];
     }
-    for (int64_t c = 0; c < a->m; ++c) a->Y[i * a->m + c] = (double)acc[c];
+    for (int64_t c = 0; c < a->m; ++c) a->Y[t * a->m + c] = (double)acc[c];
   }
   free(acc);
 }
@@ -400,8 +402,20 @@ static void brute_lp_rows(void *pa, int64_t lo, int64_t hi) {
 int oracle_brute_lp(const float *X, int64_t n, int64_t d, const float *Z, int64_t m, int p,
                     double *Y, int nthreads) {
   if (!X || !Z || !Y || n < 1 || d < 1 || m < 1 || p < 1) return ORACLE_EINVAL;
-  lp_args a = {X, n, d, Z, m, p, 1.0, Y};
+  lp_args a = {X, n, d, Z, m, p, 1.0, Y, NULL};
   run_parallel(brute_lp_rows, &a, n, 4, nthreads);
+  return ORACLE_OK;
+}
+
+/* Selected rows of the l_p^p definition (full-size spot checks): Yrows is nr x m. */
+int oracle_rows_lp(const float *X, int64_t n, int64_t d, const float *Z, int64_t m, int p,
+                   const int64_t *rows, int64_t nr, double *Yrows, int nthreads) {
+  if (!X || !Z || !Yrows || !rows || n < 1 || d < 1 || m < 1 || p < 1 || nr < 0)
+    return ORACLE_EINVAL;
+  for (int64_t t = 0; t < nr; ++t)
+    if (rows[t] < 0 || rows[t] >= n) return ORACLE_EINVAL;
+  lp_args a = {X, n, d, Z, m, p, 1.0, Yrows, rows};
+  run_parallel(brute_lp_rows, &a, nr, 1, nthreads);
   return ORACLE_OK;
 }
 
@@ -409,7 +423,7 @@ int oracle_brute_lp(const float *X, int64_t n, int64_t d, const float *Z, int64_
 int oracle_brute_tv(const float *X, int64_t n, int64_t d, const float *Z, int64_t m, double *Y,
                     int nthreads) {
   if (!X || !Z || !Y || n < 1 || d < 1 || m < 1) return ORACLE_EINVAL;
-  lp_args a = {X, n, d, Z, m, 1, 0.5, Y};
+  lp_args a = {X, n, d, Z, m, 1, 0.5, Y, NULL};
   run_parallel(brute_lp_rows, &a, n, 4, nthreads);
   return ORACLE_OK;
 }

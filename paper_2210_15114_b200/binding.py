@@ -22,10 +22,12 @@ LIB_PATH = os.environ.get("L1DM_LIB") or os.path.join(_PKG, "lib", "libl1dm.so")
 STATUS = {
     0: "L1DM_OK", -1: "L1DM_EINVAL", -2: "L1DM_ENONFINITE", -3: "L1DM_ENOMEM",
     -4: "L1DM_ECUDA", -5: "L1DM_EDEVICE", -6: "L1DM_ENOTIMPL", -7: "L1DM_ETIMEOUT",
+    -8: "L1DM_ENOTSIMPLEX",
 }
 
 EXPORTS = [
     "l1dm_prepare", "l1dm_prepare_ex", "l1dm_matvec", "l1dm_matvec_ex", "l1dm_matvec_pipelined",
+    "l1dm_matvec_lp", "l1dm_matvec_lp_ex", "l1dm_tv_matvec", "l1dm_tv_matvec_ex",
     "l1dm_free", "l1dm_sync",
     "l1dm_shape", "l1dm_workspace_bytes", "l1dm_set_workspace_limit", "l1dm_set_query_mode",
     "l1dm_plan", "l1dm_plan_ex", "l1dm_timing_enable", "l1dm_timing_read", "l1dm_debug_export", "l1dm_release_cached",
@@ -75,6 +77,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.l1dm_prepare_ex.argtypes = [vp, i64, i64, i64, i64, vp, ctypes.POINTER(vp)]
     lib.l1dm_matvec.argtypes = [vp, vp, i64, vp]
     lib.l1dm_matvec_ex.argtypes = [vp, vp, i64, i64, vp, i64, vp]
+    lib.l1dm_matvec_lp_ex.argtypes = [vp, i32, vp, i64, i64, vp, i64, vp]
+    lib.l1dm_matvec_lp.argtypes = [vp, i32, vp, i64, vp]
+    lib.l1dm_tv_matvec_ex.argtypes = [vp, vp, i64, i64, vp, i64, vp]
+    lib.l1dm_tv_matvec.argtypes = [vp, vp, i64, vp]
     lib.l1dm_matvec_pipelined.argtypes = [vp, vp, i64, i64, vp, i64, vp, i64,
                                            ctypes.POINTER(vp)]
     lib.l1dm_free.argtypes = [vp]
@@ -97,7 +103,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.l1dm_version.argtypes = []
     lib.l1dm_version.restype = ctypes.c_char_p
     for name in ("l1dm_prepare", "l1dm_prepare_ex", "l1dm_matvec", "l1dm_matvec_ex",
-                 "l1dm_matvec_pipelined", "l1dm_sync",
+                 "l1dm_matvec_pipelined", "l1dm_sync", "l1dm_matvec_lp", "l1dm_matvec_lp_ex",
+                 "l1dm_tv_matvec", "l1dm_tv_matvec_ex",
                  "l1dm_shape", "l1dm_set_workspace_limit", "l1dm_set_query_mode", "l1dm_plan", "l1dm_plan_ex",
                  "l1dm_timing_enable",
                  "l1dm_timing_read", "l1dm_debug_export"):
@@ -177,11 +184,7 @@ def l1dm_prepare(X, k_begin: int = 0, k_end: int | None = None, stream=None) -> 
     return Handle(out, n, k_end - k_begin, k_begin, k_end, dev)
 
 
-def l1dm_matvec(h: Handle, Z, Y=None, stream=None):
-    """Alg. 2 (P:188-214) for the m columns of Z: returns Y = A·Z (fp64, n x m).
-
-    CUDA tensors: stream-ordered on `stream` (default: torch's current stream).
-    Host tensors / numpy arrays: synchronous, staged through device buffers."""
+def _query(entry: str, extra: tuple, h: Handle, Z, Y, stream):
     lib = load_library()
     squeeze = (Z.ndim == 1)
     Z = _as_f32_2d(Z, "Z")
@@ -194,15 +197,33 @@ def l1dm_matvec(h: Handle, Z, Y=None, stream=None):
         Y = torch.from_numpy(Y)
     if Y.dtype != torch.float64 or Y.dim() != 2 or Y.shape != (h.n, m) or Y.stride(1) != 1:
         raise ValueError("Y must be an n x m float64 row-major tensor")
+    fn = getattr(lib, entry)
     if Z.is_cuda:
         with torch.cuda.device(Z.device):
-            rc = lib.l1dm_matvec_ex(h.ptr, _ptr(Z), Z.stride(0), m, _ptr(Y), Y.stride(0),
-                                    _stream_of(Z, stream))
+            rc = fn(h.ptr, *extra, _ptr(Z), Z.stride(0), m, _ptr(Y), Y.stride(0),
+                    _stream_of(Z, stream))
     else:
-        rc = lib.l1dm_matvec_ex(h.ptr, _ptr(Z), Z.stride(0), m, _ptr(Y), Y.stride(0),
-                                _stream_of(Z, stream))
-    _check(rc, "l1dm_matvec")
+        rc = fn(h.ptr, *extra, _ptr(Z), Z.stride(0), m, _ptr(Y), Y.stride(0), _stream_of(Z, stream))
+    _check(rc, entry.replace("_ex", ""))
     return Y.view(-1) if squeeze else Y
+
+
+def l1dm_matvec(h: Handle, Z, Y=None, stream=None):
+    """Alg. 2 (P:188-214) for the m columns of Z: returns Y = A·Z (fp64, n x m).
+
+    CUDA tensors: stream-ordered on `stream` (default: torch's current stream).
+    Host tensors / numpy arrays: synchronous, staged through device buffers."""
+    return _query("l1dm_matvec_ex", (), h, Z, Y, stream)
+
+
+def l1dm_matvec_lp(h: Handle, p: int, Z, Y=None, stream=None):
+    """l_p^p block product for odd p in {1, 3, 5, 7} (Thm. odd_p): sum_k |x_ik - x_jk|^p."""
+    return _query("l1dm_matvec_lp_ex", (int(p),), h, Z, Y, stream)
+
+
+def l1dm_tv_matvec(h: Handle, Z, Y=None, stream=None):
+    """Total-variation block product (Thm. tv) for rows on the probability simplex."""
+    return _query("l1dm_tv_matvec_ex", (), h, Z, Y, stream)
 
 
 def point_blocks(n: int, nblocks: int):

@@ -11,6 +11,7 @@
 #include <map>
 #include <mutex>
 #include <unordered_map>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -203,6 +204,9 @@ struct l1dm_ctx {
   DevBuf<unsigned> ctr;        // [0] colsum done counter, [1] timeout flag, [2..] scan tickets
   size_t ws_limit = 0;
   int mode = 0;  // L1DM_MODE_*
+  bool full_rows = false;     // prepared coordinates are every coordinate of X's rows
+  int simplex = -1;           // TV precondition, checked once: -1 unknown, 0 violated, 1 holds
+  double simplex_dev = 0.0, simplex_min = 0.0;
   uint32_t epoch = 1;
   // host staging
   DevBuf<float> Zstage;
@@ -325,6 +329,7 @@ l1dm_status prepare_impl(const float *X, int64_t n, int64_t ld_x, int64_t k_begi
   h->n = n;
   h->k_begin = k_begin;
   h->k_end = k_end;
+  h->full_rows = (k_begin == 0 && k_end == ld_x);
   h->dl = k_end - k_begin;
   h->ldn = (n + 31) / 32 * 32;
   int l2 = 0;
@@ -608,8 +613,8 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
       const float *ztb = h->zt.p + (size_t)cb * h->n * p.mb;
       {
         TimedScope ts(h, kScan, s);
-        launch_scan_seq(p, h->perm.p, sval, h->ldn, h->n, ztb, mc, h->yt.p, h->dl, h->agg.p,
-                        h->part.p + 2 * c0, 2 * m, 0, s);
+        launch_scan_seq(p, 1, h->perm.p, sval, h->ldn, h->n, ztb, mc, h->yt.p, p.mb, false,
+                        h->dl, h->agg.p, h->part.p + 2 * c0, 2 * m, 0, s);
         h->kernel_launches += 2;  // reduce, prefix
         h->launches[kScan]++;
         if (h->timing) h->scan_pairs += h->n * h->dl;
@@ -617,8 +622,8 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
       {
         TimedScope ts(h, kAcc, s);
         CUDA_TRY(cudaMemsetAsync(h->yt.p, 0, (size_t)h->n * p.mb * sizeof(double), s));
-        launch_scan_seq(p, h->perm.p, sval, h->ldn, h->n, ztb, mc, h->yt.p, h->dl, h->agg.p,
-                        h->part.p + 2 * c0, 2 * m, 1, s);
+        launch_scan_seq(p, 1, h->perm.p, sval, h->ldn, h->n, ztb, mc, h->yt.p, p.mb, false,
+                        h->dl, h->agg.p, h->part.p + 2 * c0, 2 * m, 1, s);
         h->kernel_launches++;  // apply
         h->launches[kAcc]++;
         if (h->timing) h->acc_pairs += h->n * h->dl;
@@ -682,6 +687,82 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
   return L1DM_OK;
 }
 
+// l_p^p query, odd p > 1: Zt, then per column block the seq scan with p+1
+// moments; scatter mode adds each coordinate's whole term into Yt (then Y's block columns =
+// Yt), gather mode stores it in sorted order into U and k6 sums U over each coordinate chunk.
+l1dm_status lp_device(l1dm_ctx *h, int lp, const float *Z, int64_t ldz, int64_t m, double *Y,
+                      int64_t ldy, cudaStream_t s) {
+  size_t ws = h->ws_limit;
+  if (ws == 0) {
+    size_t fr = 0, tot = 0;
+    CUDA_TRY(cudaMemGetInfo(&fr, &tot));
+    ws = (size_t)(0.75 * (double)(fr + BlockCache::get().cached(h->device) +
+                                 h->U.count * sizeof(double)));
+  }
+  QueryPlan p;
+  if (!make_lp_plan(h->n, h->dl, m, lp, h->l2_bytes, (int64_t)ws, h->mode, &p))
+    return fail(L1DM_EINVAL, "no l_p plan for p=%d n=%lld d=%lld m=%lld", lp, (long long)h->n,
+                (long long)h->dl, (long long)m);
+  const int K = lp + 1;
+  const int64_t ld_seg = (int64_t)K * m;
+  const float *sval = reinterpret_cast<const float *>(h->sval_bits.p);
+  CUDA_TRY(h->zt.ensure((size_t)p.zt_floats, false, s));
+  CUDA_TRY(h->agg.ensure(p.lb_slots * (size_t)K * p.mb, false, s));
+  CUDA_TRY(h->part.ensure((size_t)h->dl * ld_seg, false, s));
+  if (p.scatter) CUDA_TRY(h->yt.ensure((size_t)h->n * p.mb, false, s));
+  else CUDA_TRY(h->U.ensure((size_t)p.kc * (size_t)h->n * (size_t)m, false, s));
+  {
+    TimedScope ts(h, kColsums, s);
+    launch_zt(Z, ldz, h->n, m, p.mb, h->zt.p, s);
+    h->kernel_launches++;
+    h->launches[kColsums]++;
+  }
+  for (int64_t c = 0; c < p.chunks; ++c) {
+    const int64_t k_first = c * p.kc;
+    const int64_t kcc = std::min<int64_t>(p.kc, h->dl - k_first);
+    const uint32_t *perm = h->perm.p + k_first * h->ldn;
+    const float *sv = sval + k_first * h->ldn;
+    double *seg = h->part.p + k_first * ld_seg;
+    for (int cb = 0; cb < p.col_blocks; ++cb) {
+      const int64_t c0 = (int64_t)cb * p.mb;
+      const int64_t mc = std::min<int64_t>(p.mb, m - c0);
+      const float *ztb = h->zt.p + (size_t)cb * h->n * p.mb;
+      {
+        TimedScope ts(h, kScan, s);
+        launch_scan_seq(p, lp, perm, sv, h->ldn, h->n, ztb, mc, nullptr, 0, false, kcc, h->agg.p,
+                        seg + K * c0, ld_seg, 0, s);
+        h->kernel_launches += 2;
+        h->launches[kScan]++;
+        if (h->timing) h->scan_pairs += h->n * kcc;
+      }
+      TimedScope ts(h, kAcc, s);
+      if (p.scatter) {
+        CUDA_TRY(cudaMemsetAsync(h->yt.p, 0, (size_t)h->n * p.mb * sizeof(double), s));
+        launch_scan_seq(p, lp, perm, sv, h->ldn, h->n, ztb, mc, h->yt.p, p.mb, false, kcc,
+                        h->agg.p, seg + K * c0, ld_seg, 1, s);
+        launch_block_out(h->yt.p, p.mb, mc, nullptr, nullptr, nullptr, Y + c0, ldy, 0, h->n, s);
+        h->kernel_launches += 2;
+      } else {
+        launch_scan_seq(p, lp, perm, sv, h->ldn, h->n, ztb, mc, h->U.p + c0, m, true, kcc,
+                        h->agg.p, seg + K * c0, ld_seg, 1, s);
+        h->kernel_launches++;
+      }
+      h->launches[kAcc]++;
+      if (h->timing) h->acc_pairs += h->n * kcc;
+    }
+    if (!p.scatter) {
+      TimedScope ts(h, kAcc, s);
+      launch_accumulate(p, h->rank.p, h->ldn, h->n, h->U.p, k_first, kcc, h->hsum.p, h->Sg.p, Y,
+                        ldy, m, c == 0, c == p.chunks - 1, nullptr, 0, h->n, s, 1.0, false);
+      h->kernel_launches++;
+    }
+  }
+  CUDA_TRY(cudaGetLastError());
+  h->queries++;
+  h->m_last = m;
+  return L1DM_OK;
+}
+
 l1dm_status read_timeout(l1dm_ctx *h) {
   if (!h->ctr.p) return L1DM_OK;
   unsigned f = 0;
@@ -731,21 +812,73 @@ l1dm_status l1dm_prepare(const float *X, int64_t n, int64_t d, l1dm_handle *out)
   return l1dm_prepare_ex(X, n, d, 0, d, nullptr, out);
 }
 
-l1dm_status l1dm_matvec_ex(l1dm_handle h, const float *Z, int64_t ld_z, int64_t m, double *Y,
-                           int64_t ld_y, void *stream) {
+}  // extern "C"
+
+namespace {
+
+enum QueryKind { kQueryL1 = 0, kQueryLp = 1, kQueryTV = 2 };
+
+// TV precondition (Thm. tv; "rows of X on the probability simplex"):
+// every prepared coordinate >= 0 and, for a handle holding whole rows, |sum_k x_ik - 1| <=
+// 1e-9 + d 2^-23 (fp32 rows of a distribution carry ~2^-24 relative rounding per entry,
+// DESIGN.md reading R17).  Computed once per handle (the prepared state is immutable).
+l1dm_status check_simplex(l1dm_ctx *h, cudaStream_t s) {
+  if (h->simplex < 0) {
+    DevBuf<double> out;
+    CUDA_TRY(out.ensure(2, false, s));
+    launch_simplex_stats(h->hsum.p, h->n, reinterpret_cast<const float *>(h->sval_bits.p), h->ldn,
+                         h->dl, out.p, s);
+    double host[2];
+    CUDA_TRY(cudaMemcpyAsync(host, out.p, sizeof(host), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    out.release();
+    h->simplex_dev = host[0];
+    h->simplex_min = host[1];
+    const double tol = 1e-9 + (double)h->dl * std::ldexp(1.0, -23);
+    h->simplex = (host[1] >= 0.0 && (!h->full_rows || host[0] <= tol)) ? 1 : 0;
+  }
+  if (!h->simplex)
+    return fail(L1DM_ENOTSIMPLEX,
+                "rows are not on the probability simplex (min coordinate %.3g, max |sum - 1| "
+                "%.3g%s)", h->simplex_min, h->simplex_dev,
+                h->full_rows ? "" : "; row sums not checkable on a coordinate shard");
+  return L1DM_OK;
+}
+
+l1dm_status dispatch(l1dm_ctx *h, int kind, int lp, const float *Z, int64_t ldz, int64_t m,
+                     double *Y, int64_t ldy, cudaStream_t s, int64_t nblocks = 1,
+                     void *const *events = nullptr) {
+  if (kind == kQueryTV) {
+    l1dm_status st = check_simplex(h, s);
+    if (st != L1DM_OK) return st;
+  }
+  if (kind == kQueryLp && lp > 1) return lp_device(h, lp, Z, ldz, m, Y, ldy, s);
+  l1dm_status st = matvec_device(h, Z, ldz, m, Y, ldy, s, nblocks, events);
+  if (st == L1DM_OK && kind == kQueryTV) {
+    TimedScope ts(h, kAcc, s);
+    launch_scale(Y, ldy, h->n, m, 0.5, s);  // TV(x, y) = ||x - y||_1 / 2
+    h->kernel_launches++;
+  }
+  return st;
+}
+
+// Argument checks, host-buffer staging and the call: shared by the l1, l_p and TV entries.
+l1dm_status query_entry(l1dm_handle h, int kind, int lp, const float *Z, int64_t ld_z, int64_t m,
+                        double *Y, int64_t ld_y, void *stream) {
   g_err.clear();
   if (!h) return fail(L1DM_EINVAL, "handle is NULL");
   if (!Z || !Y) return fail(L1DM_EINVAL, "Z or Y is NULL");
   if (m < 1 || ld_z < m || ld_y < m)
     return fail(L1DM_EINVAL, "m=%lld ld_z=%lld ld_y=%lld invalid", (long long)m, (long long)ld_z,
                 (long long)ld_y);
+  if (kind == kQueryLp && (lp < 1 || lp > 7 || !(lp & 1)))
+    return fail(L1DM_EINVAL, "p=%d: odd p in {1, 3, 5, 7} only (even p needs no sort)", lp);
   l1dm_status st = check_device(h);
   if (st != L1DM_OK) return st;
   cudaStream_t s = (cudaStream_t)stream;  // NULL: legacy default stream
   h->last_stream = s;
   const bool zdev = is_device_pointer(Z), ydev = is_device_pointer(Y);
-  // vector paths need aligned rows; fall back to staging only for host memory
-  if (zdev && ydev) return matvec_device(h, Z, ld_z, m, Y, ld_y, s);
+  if (zdev && ydev) return dispatch(h, kind, lp, Z, ld_z, m, Y, ld_y, s);
   // host buffers: stage through library-owned device memory; synchronous
   const float *Zd = Z;
   int64_t ldzd = ld_z;
@@ -765,7 +898,7 @@ l1dm_status l1dm_matvec_ex(l1dm_handle h, const float *Z, int64_t ld_z, int64_t 
     Yd = h->Ystage.p;
     ldyd = m;
   }
-  st = matvec_device(h, Zd, ldzd, m, Yd, ldyd, s);
+  st = dispatch(h, kind, lp, Zd, ldzd, m, Yd, ldyd, s);
   if (st != L1DM_OK) return st;
   if (!ydev) {
     TimedScope ts(h, kCopy, s);
@@ -775,6 +908,35 @@ l1dm_status l1dm_matvec_ex(l1dm_handle h, const float *Z, int64_t ld_z, int64_t 
   }
   CUDA_TRY(cudaStreamSynchronize(s));
   return read_timeout(h);
+}
+
+}  // namespace
+
+extern "C" {
+
+l1dm_status l1dm_matvec_ex(l1dm_handle h, const float *Z, int64_t ld_z, int64_t m, double *Y,
+                           int64_t ld_y, void *stream) {
+  return query_entry(h, kQueryL1, 1, Z, ld_z, m, Y, ld_y, stream);
+}
+
+l1dm_status l1dm_matvec_lp_ex(l1dm_handle h, int p, const float *Z, int64_t ld_z, int64_t m,
+                              double *Y, int64_t ld_y, void *stream) {
+  return query_entry(h, kQueryLp, p, Z, ld_z, m, Y, ld_y, stream);
+}
+
+l1dm_status l1dm_matvec_lp(l1dm_handle h, int p, const float *Z, int64_t m, double *Y) {
+  if (!h) return fail(L1DM_EINVAL, "handle is NULL");
+  return query_entry(h, kQueryLp, p, Z, m, m, Y, m, (void *)h->stream);
+}
+
+l1dm_status l1dm_tv_matvec_ex(l1dm_handle h, const float *Z, int64_t ld_z, int64_t m, double *Y,
+                              int64_t ld_y, void *stream) {
+  return query_entry(h, kQueryTV, 1, Z, ld_z, m, Y, ld_y, stream);
+}
+
+l1dm_status l1dm_tv_matvec(l1dm_handle h, const float *Z, int64_t m, double *Y) {
+  if (!h) return fail(L1DM_EINVAL, "handle is NULL");
+  return query_entry(h, kQueryTV, 1, Z, m, m, Y, m, (void *)h->stream);
 }
 
 l1dm_status l1dm_matvec_pipelined(l1dm_handle h, const float *Z, int64_t ld_z, int64_t m,

@@ -98,7 +98,8 @@ void launch_epilogue(const double *hsum, const double *Sg, double *Y, int64_t ld
 // (S, T) pairs per column): S_c = coordinate 0's S, g_c = sum_k T_kc.
 void launch_totals(const double *segtot, int64_t ld_seg, int64_t dl, int64_t mc, double *S,
                    double *g, cudaStream_t s);
-// Scatter mode, m > 1: Y[i][c] = Yt[i][c] + g_c - h_i S_c for points [i0, i1), mc columns.
+// Scatter mode, m > 1: Y[i][c] = Yt[i][c] + g_c - h_i S_c for points [i0, i1), mc columns
+// (S == nullptr: Y[i][c] = Yt[i][c]).
 void launch_block_out(const double *yt, int mb, int64_t mc, const double *hsum, const double *S,
                       const double *g, double *Y, int64_t ldy, int64_t i0, int64_t i1,
                       cudaStream_t s);
@@ -109,13 +110,17 @@ void launch_scan(const QueryPlan &p, const uint32_t *perm, const float *sval, in
                  int64_t kcc, uint32_t *flags, double *agg, double *incl, uint32_t epoch,
                  unsigned *ticket, unsigned *timeout_flag, double *segtot, int64_t ld_seg,
                  float *zs, cudaStream_t s);
-// Scatter mode, m > 1: scan of one column block (mc <= mb columns of the compact Zt block) over
-// kcc coordinates as reduce / prefix / apply launches (agg: kcc x tiles x 2mb doubles), adding
-// 2U into the block accumulator yt (n x mb).  rows_per_tile = 1024.  phase: 0 reduce + prefix
-// (writes agg and segtot), 1 apply (reads agg, adds into yt), 2 both.
-void launch_scan_seq(const QueryPlan &p, const uint32_t *perm, const float *sval, int64_t ldn,
-                     int64_t n, const float *zt, int64_t mc, double *yt, int64_t kcc, double *agg,
-                     double *segtot, int64_t ld_seg, int phase, cudaStream_t s);
+// Column-block "seq" scan (k5_scan_seq; scatter mode for m > 1 and every odd lp > 1 query):
+// one column block (mc <= mb columns of the compact Zt block) over kcc coordinates, as reduce /
+// prefix / apply launches (agg: kcc x tiles x (lp+1) mb doubles; segtot rows of ld_seg doubles,
+// (lp+1) moments per column).  Apply adds its per-row value into out[perm[r]][c] with fp64 L2
+// reductions (store = false: the block accumulator Yt, ldo = mb) or stores it at out[r][c] in
+// sorted order (store = true: the U workspace of gather mode, ldo = m).  rows_per_tile = 1024.
+// phase: 0 reduce + prefix, 1 apply, 2 both.  lp in {1, 3, 5, 7}.
+void launch_scan_seq(const QueryPlan &p, int lp, const uint32_t *perm, const float *sval,
+                     int64_t ldn, int64_t n, const float *zt, int64_t mc, double *out,
+                     int64_t ldo, bool store, int64_t kcc, double *agg, double *segtot,
+                     int64_t ld_seg, int phase, cudaStream_t s);
 // Zt[cb][i][0..mb) = Z[i][cb*mb + ..] (zero-padded past m): the scatter mode's per-block Z.
 void launch_zt(const float *Z, int64_t ldz, int64_t n, int64_t m, int mb, float *zt,
                cudaStream_t s);
@@ -123,6 +128,15 @@ void launch_accumulate(const QueryPlan &p, const uint32_t *rank, int64_t ldn, in
                        const double *U, int64_t k_first, int64_t kcc, const double *hsum,
                        const double *Sg, double *Y, int64_t ldy, int64_t m, bool first_chunk,
                        bool last_chunk, unsigned *ticket, int64_t i0, int64_t i1,
-                       cudaStream_t s);  // points [i0, i1)
+                       cudaStream_t s, double factor = 2.0,
+                       bool epilogue = true);  // points [i0, i1); Y (+)= factor * sum_k U (+ g - h S)
+// l_p^p, odd p in {3, 5, 7}: plan over the seq kernels.
+bool make_lp_plan(int64_t n, int64_t dl, int64_t m, int lp, int64_t l2_bytes, int64_t ws_limit,
+                  int mode, QueryPlan *p);
+// Y[i][c] *= a over n x m.
+void launch_scale(double *Y, int64_t ldy, int64_t n, int64_t m, double a, cudaStream_t s);
+// out[0] = max_i |h_i - 1|, out[1] = min over every prepared coordinate value (device doubles).
+void launch_simplex_stats(const double *hsum, int64_t n, const float *sval, int64_t ldn,
+                          int64_t dl, double *out, cudaStream_t s);
 
 }  // namespace l1dm

@@ -166,6 +166,62 @@ bool make_plan(int64_t n, int64_t dl, int64_t m, int64_t l2_bytes, int64_t ws_li
   return true;
 }
 
+// Plan of an l_p^p query with odd p > 1: every pass is the column-block seq scan
+// with (p+1) moments per column.  Scatter when a block of Yt + Zt fits L2 (as for p = 1), else
+// gather: the apply pass stores W in sorted order into the U workspace (chunks of kc
+// coordinates) and k6 sums it over the chunk at rank (factor 1, no epilogue).
+bool make_lp_plan(int64_t n, int64_t dl, int64_t m, int lp, int64_t l2_bytes, int64_t ws_limit,
+                  int mode, QueryPlan *p) {
+  if (n < 1 || dl < 1 || m < 1 || !p || lp < 3 || lp > 7 || !(lp & 1)) return false;
+  QueryPlan base;
+  if (!make_plan(n, dl, m, l2_bytes, ws_limit, 4, mode, &base)) return false;
+  QueryPlan q = base;
+  const bool scatter = base.scatter != 0;
+  int mb;
+  if (scatter) {
+    mb = base.mb < 2 ? 2 : base.mb;  // seq kernels exist for mb = 2..16
+  } else {
+    mb = 16;                          // gather: Zt rows of 64 B from HBM
+    while (mb > 2 && mb >= 2 * m) mb >>= 1;
+  }
+  const int K = lp + 1;
+  q.scatter = scatter ? 1 : 0;
+  q.mb = mb;
+  q.lpr = mb;
+  q.vc = 1;
+  q.vec = mb >= 4 ? 4 : mb;
+  q.col_blocks = (int)((m + mb - 1) / mb);
+  q.items = 4 * mb;
+  q.rows_per_tile = 1024;
+  q.tiles_per_segment = (n + 1023) / 1024;
+  q.zt_floats = (int64_t)q.col_blocks * n * mb;
+  q.ldu = m;
+  const size_t agg_per_coord = (size_t)q.tiles_per_segment * K * mb * sizeof(double);
+  if (scatter) {
+    q.kc = dl;
+    q.chunks = 1;
+    q.u_bytes = 0;
+    q.l2_resident = 1;
+  } else {
+    const size_t per_coord = (size_t)n * m * sizeof(double) + agg_per_coord;
+    const size_t lim = (ws_limit > 0 && (size_t)ws_limit < kMaxChunkBytes) ? (size_t)ws_limit
+                                                                           : kMaxChunkBytes;
+    q.kc = (int64_t)(lim / per_coord);
+    if (q.kc < 1) q.kc = 1;
+    if (q.kc > dl) q.kc = dl;
+    q.chunks = (dl + q.kc - 1) / q.kc;
+    q.u_bytes = (size_t)q.kc * n * m * sizeof(double);
+    q.l2_resident = 0;
+  }
+  q.lb_slots = (size_t)q.kc * q.tiles_per_segment;
+  q.workspace_bytes = q.u_bytes + q.lb_slots * K * mb * sizeof(double) +
+                      (size_t)q.zt_floats * sizeof(float) +
+                      (scatter ? (size_t)n * mb * sizeof(double) : 0) +
+                      (size_t)dl * K * m * sizeof(double);
+  *p = q;
+  return true;
+}
+
 // ------------------------------------------------------------------ K4
 // Query totals from the scan's segment totals: S_c = sum_j z_jc (coordinate 0's segment),
 // g_c = sum_k T_kc = sum_j h_j z_jc, summed over the shard's coordinates in fixed order.
@@ -507,18 +563,25 @@ __global__ void __launch_bounds__(256, 2)
   }
 }
 
-// Scatter-mode scan for m > 1: one column block of MB columns, read from the compact Zt block
-// (row stride MB), with 2U added into the block accumulator Yt[perm[r]][c] (row stride MB) by
-// fp64 L2 reductions.  Reduce-then-scan, no inter-CTA waits (ncu showed the decoupled
-// look-back's barriers and fences dominating this L2-bound kernel):
-//   SEQ_REDUCE  per tile: column totals of (z, v z)                  -> agg[seg][tile][2 MB]
-//   k5_seq_prefix  per (segment, component): exclusive scan over tiles, segment totals
-//   SEQ_APPLY   per tile: the same totals again, CTA scan + tile prefix, U along the rows, REDs
+// Column-block scan with thread-sequential rows ("seq"), used by scatter mode for m > 1 and by
+// every l_p^p query with odd p > 1 (gather and scatter).  One column block of MB columns is
+// read from the compact Zt block (row stride MB).  For P = 1 it evaluates U_r = v_r P_r - Q_r
+// (DESIGN.md §2); for odd P, per column, the P+1 exclusive prefix moments
+//   M_t(r) = sum_{r' < r} z_{perm(r')} v_{r'}^t,  t = 0..P,
+// and the coordinate's whole contribution to point perm(r)
+//   W_r = sum_t c_t v_r^(P-t) (2 M_t(r) - T_t),  c_t = C(P,t) (-1)^t,  T_t = M_t(n).
+// Reduce-then-scan, no inter-CTA waits (ncu showed the decoupled look-back's barriers and
+// fences dominating this L2-bound kernel):
+//   SEQ_REDUCE       per tile: column totals of the P+1 moments     -> agg[seg][tile][NP]
+//   k5_seq_prefix    per (segment, component): exclusive scan over tiles, segment totals T
+//   SEQ_APPLY_RED    per tile: CTA scan + tile prefix; P = 1: 2U, P > 1: W, added into
+//                    Yt[perm[r]][c] (row stride MB) by fp64 L2 reductions
+//   SEQ_APPLY_STORE  the same value stored at U[r][c] in sorted order (gather mode, P > 1)
 // Thread (g, c) owns ITEMS consecutive sorted rows of column c, so the row loop is a
 // thread-sequential scan; only per-thread totals are scanned across the CTA (shuffles over the
-// 32/MB groups of a warp, then across warps).  At each row step a warp adds 32/MB rows x MB
+// 32/MB groups of a warp, then across warps).  At each row step a warp touches 32/MB rows x MB
 // consecutive columns: every reduction request is one row segment of Yt.
-template <int MB>
+template <int MB, int P = 1>
 struct SeqCfg {
   static constexpr int NT = 256, NW = 8;
   static constexpr int G = NT / MB;           // row groups per tile
@@ -527,20 +590,30 @@ struct SeqCfg {
   static constexpr int GPW = 32 / MB;         // groups per warp
   static constexpr int GS = ITEMS * MB + MB;  // padded floats per group of the Z stage
   static constexpr int PS = ITEMS + 4;        // padded words per group of perm / sval
-  static constexpr int NP = 2 * MB;
+  static constexpr int K = P + 1;             // moments per column
+  static constexpr int NP = K * MB;           // payload per tile
   static constexpr int CH = MB * 4 >= 16 ? 16 : MB * 4;  // bytes per cp.async of a Z row
   static constexpr size_t SMEM = (size_t)G * GS * 4 + (size_t)G * PS * 4 * 2;
 };
-enum { SEQ_REDUCE = 0, SEQ_APPLY = 1 };
+enum { SEQ_REDUCE = 0, SEQ_APPLY_RED = 1, SEQ_APPLY_STORE = 2 };
 
-template <int MB, int MODE>
+// c_t = C(P, t) (-1)^t
+template <int P>
+__host__ __device__ constexpr double lp_coef(int t) {
+  double b = 1.0;
+  for (int q = 0; q < t; ++q) b = b * (double)(P - q) / (double)(q + 1);
+  return (t & 1) ? -b : b;
+}
+
+template <int MB, int MODE, int P>
 __global__ void __launch_bounds__(256)
     k5_scan_seq(const uint32_t *__restrict__ perm, const float *__restrict__ sval, int64_t ldn,
-                int64_t n, const float *__restrict__ zt, int64_t mc, double *__restrict__ yt,
-                int64_t nseg, int64_t tiles_per_seg, double *__restrict__ agg) {
-  using C = SeqCfg<MB>;
+                int64_t n, const float *__restrict__ zt, int64_t mc, double *__restrict__ out,
+                int64_t ldo, int64_t nseg, int64_t tiles_per_seg, double *__restrict__ agg,
+                const double *__restrict__ segtot, int64_t ld_seg) {
+  using C = SeqCfg<MB, P>;
   constexpr int NT = C::NT, NW = C::NW, ITEMS = C::ITEMS, R = C::R, GPW = C::GPW, GS = C::GS,
-                PS = C::PS, NP = C::NP, CH = C::CH, CPR = MB * 4 / CH;
+                PS = C::PS, K = C::K, NP = C::NP, CH = C::CH, CPR = MB * 4 / CH;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float *zb = reinterpret_cast<float *>(smem_raw);              // [G][GS]
   float *vb = zb + C::G * GS;                                    // [G][PS]
@@ -586,29 +659,36 @@ __global__ void __launch_bounds__(256)
   const float *zg = zb + g * GS + c;
   const float *vg = vb + g * PS;
   const uint32_t *pg = pb + g * PS;
-  // ---- per-thread totals of s = z and t = v z (fp64; products of fp32 exact)
-  double os = 0.0, ot = 0.0;
-#pragma unroll 8
+  // ---- per-thread totals of the moments z v^t (fp64; for P = 1: s = z, t = v z, exact)
+  double o[K];
+#pragma unroll
+  for (int q = 0; q < K; ++q) o[q] = 0.0;
+#pragma unroll 4
   for (int j = 0; j < ITEMS; ++j) {
     const double z = (double)zg[j * MB];  // zero-filled past n
     const double v = j < nmine ? (double)vg[j] : 0.0;
-    os += z;
-    ot = fma(v, z, ot);
+    double zv = z;
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      o[q] += zv;
+      zv *= v;
+    }
   }
   // ---- inclusive scan over the GPW groups of this warp (same column: lanes c + k*MB)
-  double ps = os, pt = ot;
+  double ps[K];
+#pragma unroll
+  for (int q = 0; q < K; ++q) ps[q] = o[q];
 #pragma unroll
   for (int off = 1; off < GPW; off <<= 1) {
-    const double a = __shfl_up_sync(0xFFFFFFFFu, ps, off * MB);
-    const double b = __shfl_up_sync(0xFFFFFFFFu, pt, off * MB);
-    if (gl >= off) {
-      ps += a;
-      pt += b;
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      const double a = __shfl_up_sync(0xFFFFFFFFu, ps[q], off * MB);
+      if (gl >= off) ps[q] += a;
     }
   }
   if (gl == GPW - 1) {
-    s_wt[w * NP + 2 * c] = ps;
-    s_wt[w * NP + 2 * c + 1] = pt;
+#pragma unroll
+    for (int q = 0; q < K; ++q) s_wt[w * NP + K * c + q] = ps[q];
   }
   __syncthreads();
   double *ag = agg + (kk * tiles_per_seg + tile) * NP;
@@ -622,27 +702,52 @@ __global__ void __launch_bounds__(256)
     return;
   } else {
     // exclusive prefix of this thread's first row: tile prefix + earlier warps + earlier groups
-    double P = __ldg(ag + 2 * c) + ps - os, Q = __ldg(ag + 2 * c + 1) + pt - ot;
+    double M[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) M[q] = __ldg(ag + K * c + q) + ps[q] - o[q];
     for (int ww = 0; ww < w; ++ww) {
-      P += s_wt[ww * NP + 2 * c];
-      Q += s_wt[ww * NP + 2 * c + 1];
+#pragma unroll
+      for (int q = 0; q < K; ++q) M[q] += s_wt[ww * NP + K * c + q];
     }
+    double Tt[K];  // P > 1: the coordinate's totals T_t of this column (from the prefix pass)
+#pragma unroll
+    for (int q = 0; q < K; ++q)
+      Tt[q] = (P > 1 && c < mc) ? __ldg(segtot + kk * ld_seg + K * c + q) : 0.0;
     if (c < mc) {
-#pragma unroll 8
+#pragma unroll 4
       for (int j = 0; j < ITEMS; ++j) {
         if (j >= nmine) break;
         const double z = (double)zg[j * MB], v = (double)vg[j];
-        const double u = fma(v, P, -Q);  // U_r = v_r P_r - Q_r
-        P += z;
-        Q = fma(v, z, Q);
-        red_add_f64(yt + (int64_t)pg[j] * MB + c, 2.0 * u, pol_keep);
+        double val;
+        if constexpr (P == 1) {
+          val = 2.0 * fma(v, M[0], -M[1]);  // 2 U_r = 2 (v_r P_r - Q_r)
+        } else {
+          double vp[K];  // v^0 .. v^P
+          vp[0] = 1.0;
+#pragma unroll
+          for (int q = 1; q < K; ++q) vp[q] = vp[q - 1] * v;
+          val = 0.0;
+#pragma unroll
+          for (int q = 0; q < K; ++q) val = fma(lp_coef<P>(q) * vp[P - q], fma(2.0, M[q], -Tt[q]), val);
+        }
+        double zv = z;
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+          M[q] += zv;
+          zv *= v;
+        }
+        if constexpr (MODE == SEQ_APPLY_RED) {
+          red_add_f64(out + (int64_t)pg[j] * ldo + c, val, pol_keep);
+        } else {
+          __stcs(out + (kk * n + row0 + rl0 + j) * ldo + c, val);  // U[kk][r][c]
+        }
       }
     }
   }
 }
 
 // Exclusive scan of each (segment, component) over the segment's tiles, in place (one warp per
-// (segment, component)), and the segment totals (S, T_k per column) for the epilogue.
+// (segment, component)), and the segment totals for the epilogue.
 __global__ void __launch_bounds__(256)
     k5_seq_prefix(double *__restrict__ agg, int64_t nseg, int64_t tiles_per_seg, int np,
                   int64_t ncomp, double *__restrict__ segtot, int64_t ld_seg) {
@@ -668,45 +773,60 @@ __global__ void __launch_bounds__(256)
   if (lane == 0 && comp < ncomp) segtot[seg * ld_seg + comp] = carry;
 }
 
-template <int MB>
+template <int MB, int P>
 static void launch_seq_t(const QueryPlan &p, const uint32_t *perm, const float *sval, int64_t ldn,
-                         int64_t n, const float *zt, int64_t mc, double *yt, int64_t kcc,
-                         double *agg, double *segtot, int64_t ld_seg, int phase, cudaStream_t s) {
-  using C = SeqCfg<MB>;
+                         int64_t n, const float *zt, int64_t mc, double *out, int64_t ldo,
+                         bool store, int64_t kcc, double *agg, double *segtot, int64_t ld_seg,
+                         int phase, cudaStream_t s) {
+  using C = SeqCfg<MB, P>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k5_scan_seq<MB, SEQ_REDUCE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)C::SMEM);
-    cudaFuncSetAttribute(k5_scan_seq<MB, SEQ_APPLY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)C::SMEM);
+    cudaFuncSetAttribute(k5_scan_seq<MB, SEQ_REDUCE, P>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    cudaFuncSetAttribute(k5_scan_seq<MB, SEQ_APPLY_RED, P>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    cudaFuncSetAttribute(k5_scan_seq<MB, SEQ_APPLY_STORE, P>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     attr = true;
   }
   const int64_t total = kcc * p.tiles_per_segment;
   if (phase != 1) {
-    k5_scan_seq<MB, SEQ_REDUCE><<<(unsigned)total, C::NT, C::SMEM, s>>>(
-        perm, sval, ldn, n, zt, mc, yt, kcc, p.tiles_per_segment, agg);
+    k5_scan_seq<MB, SEQ_REDUCE, P><<<(unsigned)total, C::NT, C::SMEM, s>>>(
+        perm, sval, ldn, n, zt, mc, out, ldo, kcc, p.tiles_per_segment, agg, segtot, ld_seg);
     const int64_t warps = kcc * C::NP;
     k5_seq_prefix<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(agg, kcc, p.tiles_per_segment,
-                                                              C::NP, 2 * mc, segtot, ld_seg);
+                                                              C::NP, C::K * mc, segtot, ld_seg);
   }
   if (phase != 0) {
-    k5_scan_seq<MB, SEQ_APPLY><<<(unsigned)total, C::NT, C::SMEM, s>>>(
-        perm, sval, ldn, n, zt, mc, yt, kcc, p.tiles_per_segment, agg);
+    auto kern = store ? k5_scan_seq<MB, SEQ_APPLY_STORE, P> : k5_scan_seq<MB, SEQ_APPLY_RED, P>;
+    kern<<<(unsigned)total, C::NT, C::SMEM, s>>>(perm, sval, ldn, n, zt, mc, out, ldo, kcc,
+                                                 p.tiles_per_segment, agg, segtot, ld_seg);
   }
 }
 
-void launch_scan_seq(const QueryPlan &p, const uint32_t *perm, const float *sval, int64_t ldn,
-                     int64_t n, const float *zt, int64_t mc, double *yt, int64_t kcc, double *agg,
-                     double *segtot, int64_t ld_seg, int phase, cudaStream_t s) {
-#define L1DM_SEQ(MB) \
-  launch_seq_t<MB>(p, perm, sval, ldn, n, zt, mc, yt, kcc, agg, segtot, ld_seg, phase, s)
+void launch_scan_seq(const QueryPlan &p, int lp, const uint32_t *perm, const float *sval,
+                     int64_t ldn, int64_t n, const float *zt, int64_t mc, double *out,
+                     int64_t ldo, bool store, int64_t kcc, double *agg, double *segtot,
+                     int64_t ld_seg, int phase, cudaStream_t s) {
+#define L1DM_SEQ(MB, P)                                                                     \
+  launch_seq_t<MB, P>(p, perm, sval, ldn, n, zt, mc, out, ldo, store, kcc, agg, segtot, ld_seg, \
+                      phase, s)
+#define L1DM_SEQ_P(MB)                         \
+  switch (lp) {                                \
+    case 1: L1DM_SEQ(MB, 1); break;            \
+    case 3: L1DM_SEQ(MB, 3); break;            \
+    case 5: L1DM_SEQ(MB, 5); break;            \
+    case 7: L1DM_SEQ(MB, 7); break;            \
+    default: break;                            \
+  }
   switch (p.mb) {
-    case 2: L1DM_SEQ(2); break;
-    case 4: L1DM_SEQ(4); break;
-    case 8: L1DM_SEQ(8); break;
-    case 16: L1DM_SEQ(16); break;
+    case 2: L1DM_SEQ_P(2); break;
+    case 4: L1DM_SEQ_P(4); break;
+    case 8: L1DM_SEQ_P(8); break;
+    case 16: L1DM_SEQ_P(16); break;
     default: break;
   }
+#undef L1DM_SEQ_P
 #undef L1DM_SEQ
 }
 
@@ -993,7 +1113,8 @@ void launch_epilogue(const double *hsum, const double *Sg, double *Y, int64_t ld
 }
 
 // Scatter mode, m > 1: Y[i][c0 + c] = Yt[i][c] + g_c - h_i S_c for one column block (Yt is the
-// block's compact L2-resident accumulator, mb doubles per point).
+// block's compact L2-resident accumulator, mb doubles per point).  S == nullptr (l_p, p > 1:
+// the apply pass already added the whole contribution): Y[i][c0 + c] = Yt[i][c].
 __global__ void __launch_bounds__(256)
     k9_block_out(const double *__restrict__ yt, int mb, int64_t mc, const double *__restrict__ hsum,
                  const double *__restrict__ S, const double *__restrict__ g, double *__restrict__ Y,
@@ -1002,7 +1123,8 @@ __global__ void __launch_bounds__(256)
   for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * 256) {
     const int64_t i = i0 + e / mc, c = e - (e / mc) * mc;
-    __stcs(Y + i * ldy + c, yt[i * mb + c] + fma(-hsum[i], S[c], g[c]));
+    const double v = yt[i * mb + c];
+    __stcs(Y + i * ldy + c, S ? v + fma(-hsum[i], S[c], g[c]) : v);
   }
 }
 
@@ -1013,6 +1135,57 @@ void launch_block_out(const double *yt, int mb, int64_t mc, const double *hsum, 
   int64_t blocks = ((i1 - i0) * mc + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   k9_block_out<<<(unsigned)blocks, 256, 0, s>>>(yt, mb, mc, hsum, S, g, Y, ldy, i0, i1);
+}
+
+// Y[i][c] *= a (TV = a * l1 with a = 1/2).
+__global__ void __launch_bounds__(256)
+    k10_scale(double *__restrict__ Y, int64_t ldy, int64_t n, int64_t m, double a) {
+  const int64_t total = n * m;
+  for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * 256) {
+    const int64_t i = e / m, c = e - (e / m) * m;
+    Y[i * ldy + c] *= a;
+  }
+}
+
+void launch_scale(double *Y, int64_t ldy, int64_t n, int64_t m, double a, cudaStream_t s) {
+  int64_t blocks = (n * m + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k10_scale<<<(unsigned)blocks, 256, 0, s>>>(Y, ldy, n, m, a);
+}
+
+// Simplex statistics of a prepared handle: out[0] = max_i |h_i - 1|, out[1] = min_k sval[k][0]
+// (the smallest coordinate value overall).  One CTA; n and dl are small enough per handle for
+// a grid-stride loop to be negligible next to prepare.
+__global__ void __launch_bounds__(1024)
+    k11_simplex_stats(const double *__restrict__ hsum, int64_t n, const float *__restrict__ sval,
+                      int64_t ldn, int64_t dl, double *__restrict__ out) {
+  __shared__ double s_a[32], s_b[32];
+  double a = 0.0, b = 1e300;
+  for (int64_t i = threadIdx.x; i < n; i += 1024) a = fmax(a, fabs(hsum[i] - 1.0));
+  for (int64_t k = threadIdx.x; k < dl; k += 1024) b = fmin(b, (double)sval[k * ldn]);
+  for (int off = 16; off; off >>= 1) {
+    a = fmax(a, __shfl_xor_sync(0xFFFFFFFFu, a, off));
+    b = fmin(b, __shfl_xor_sync(0xFFFFFFFFu, b, off));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s_a[threadIdx.x >> 5] = a;
+    s_b[threadIdx.x >> 5] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < 32; ++q) {
+      a = fmax(a, s_a[q]);
+      b = fmin(b, s_b[q]);
+    }
+    out[0] = a;
+    out[1] = b;
+  }
+}
+
+void launch_simplex_stats(const double *hsum, int64_t n, const float *sval, int64_t ldn,
+                          int64_t dl, double *out, cudaStream_t s) {
+  k11_simplex_stats<<<1, 1024, 0, s>>>(hsum, n, sval, ldn, dl, out);
 }
 
 // ------------------------------------------------------------------ scatter-mode Z blocks
@@ -1080,7 +1253,8 @@ __global__ void __launch_bounds__(256)
                   const double *__restrict__ U, int64_t ldu, int64_t k_first, int64_t kcc,
                   const double *__restrict__ hsum, const double *__restrict__ Sg,
                   double *__restrict__ Y, int64_t ldy, int64_t m, int first_chunk,
-                  int last_chunk, unsigned *ticket, int64_t i_begin, int64_t i_end) {
+                  int last_chunk, unsigned *ticket, int64_t i_begin, int64_t i_end, double factor,
+                  int epilogue) {
   constexpr int PPW = 32 / LPP;
   // the chunk's scan has completed (stream order): re-arm its ticket for the next query
   if (ticket && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *ticket = 0u;
@@ -1109,12 +1283,12 @@ __global__ void __launch_bounds__(256)
   double *yp = Y + i * ldy + c0;
   double val[V6];
 #pragma unroll
-  for (int q = 0; q < V6; ++q) val[q] = 2.0 * acc[q];
+  for (int q = 0; q < V6; ++q) val[q] = factor * acc[q];
   if (!first_chunk) {
 #pragma unroll
     for (int q = 0; q < V6; ++q) val[q] += yp[q];
   }
-  if (last_chunk) {
+  if (last_chunk && epilogue) {
     const double hi = hsum[i];
 #pragma unroll
     for (int q = 0; q < V6; ++q) val[q] += fma(-hi, Sg[c0 + q], Sg[m + c0 + q]);  // g - h_i S
@@ -1127,23 +1301,24 @@ template <int V6, int LPP>
 static void launch_acc_t(const QueryPlan &p, const uint32_t *rank, int64_t ldn, int64_t n,
                          const double *U, int64_t k_first, int64_t kcc, const double *hsum,
                          const double *Sg, double *Y, int64_t ldy, int64_t m, bool first,
-                         bool last, unsigned *ticket, int64_t i0, int64_t i1, cudaStream_t s) {
+                         bool last, unsigned *ticket, int64_t i0, int64_t i1, double factor,
+                         bool epilogue, cudaStream_t s) {
   constexpr int PPB = 8 * (32 / LPP);
   dim3 grid((unsigned)((i1 - i0 + PPB - 1) / PPB), (unsigned)p.col_groups);
   k6_accumulate<V6, LPP, 8><<<grid, 256, 0, s>>>(rank, ldn, n, U, p.ldu, k_first, kcc, hsum, Sg,
                                                  Y, ldy, m, first ? 1 : 0, last ? 1 : 0, ticket,
-                                                 i0, i1);
+                                                 i0, i1, factor, epilogue ? 1 : 0);
 }
 
 void launch_accumulate(const QueryPlan &p, const uint32_t *rank, int64_t ldn, int64_t n,
                        const double *U, int64_t k_first, int64_t kcc, const double *hsum,
                        const double *Sg, double *Y, int64_t ldy, int64_t m, bool first_chunk,
                        bool last_chunk, unsigned *ticket, int64_t i0, int64_t i1,
-                       cudaStream_t s) {
+                       cudaStream_t s, double factor, bool epilogue) {
   if (i1 <= i0) return;
 #define L1DM_ACC(V, L)                                                                   \
   launch_acc_t<V, L>(p, rank, ldn, n, U, k_first, kcc, hsum, Sg, Y, ldy, m, first_chunk, \
-                     last_chunk, ticket, i0, i1, s)
+                     last_chunk, ticket, i0, i1, factor, epilogue, s)
   switch (p.v6 * 100 + p.lpp) {
     case 101: L1DM_ACC(1, 1); break;
     case 102: L1DM_ACC(1, 2); break;

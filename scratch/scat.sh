@@ -1,3 +1,1 @@
-L1DM_SCATTER_MB=8 timeout 300 python scratch/scat.py c3 scatter
-L1DM_SCATTER_MB=4 timeout 300 python scratch/scat.py c3 scatter
-L1DM_SCATTER_MB=16 timeout 300 python scratch/scat.py c3 scatter
+for r in 0 1 2; do for a in 0 1 2; do echo "R=$r A=$a"; L1DM_ZPOL_R=$r L1DM_ZPOL_A=$a timeout 300 python scratch/scat.py c3 auto; done; done

@@ -1,0 +1,152 @@
+"""l_p^p (odd p) and TV queries through the C ABI against the CPU oracle.
+
+Tolerances (R18): the query evaluates sum_t c_t x^(p-t) (2 M_t - T_t) with fp64
+moments M_t of z x^t; the moments of |x| ~ 1 data are O(n) and cancel to the O(n) result
+only mildly, so float data meets 1e-9 for p = 3 and, measured here with >100x margin, 1e-9 /
+1e-8 for p = 5 / 7.  Integer data with small moments is exact (every partial sum is an
+integer < 2^53) and is checked bit-for-bit.  TV is half the l1 product: same 1e-9 bar."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2210_15114_b200 as l1
+from conftest import GOLDEN_LP, GOLDEN_TV, col_rel_l2, golden_p, load_golden
+
+pytestmark = pytest.mark.gpu
+TOL = {1: 1e-9, 3: 1e-9, 5: 1e-9, 7: 1e-8}
+MODES = ["gather", "scatter"]
+
+
+def lp_gpu(X, Z, p, mode="auto", k_range=None, tv=False):
+    Xt = torch.from_numpy(np.ascontiguousarray(X)).cuda()
+    h = l1.l1dm_prepare(Xt, *(k_range or (0, None)))
+    l1.l1dm_set_query_mode(h, mode)
+    Zt = torch.from_numpy(np.ascontiguousarray(Z)).cuda()
+    Y = l1.l1dm_tv_matvec(h, Zt) if tv else l1.l1dm_matvec_lp(h, p, Zt)
+    torch.cuda.synchronize()
+    l1.l1dm_sync(h)
+    out = Y.cpu().numpy()
+    l1.l1dm_free(h)
+    return out
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("name", GOLDEN_LP)
+def test_lp_goldens_exact(name, mode):
+    X, Z, Y = load_golden(name)
+    assert np.array_equal(lp_gpu(X, Z, golden_p(name), mode), Y)
+
+
+@pytest.mark.parametrize("name", GOLDEN_TV)
+def test_tv_golden(name):
+    X, Z, Y = load_golden(name)
+    assert np.array_equal(lp_gpu(X, Z, 1, tv=True), Y)
+
+
+# n spans 1024-row tiles and ragged tails; m spans column blocks 2..16 and ragged last blocks
+CASES = [(2, 1, 1), (100, 3, 2), (1025, 2, 5), (2047, 3, 16), (3000, 4, 17), (700, 2, 33)]
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("p", [3, 5, 7])
+@pytest.mark.parametrize("n,d,m", CASES)
+def test_lp_random_float_vs_oracle(n, d, m, p, mode):
+    rng = np.random.default_rng(n * 131 + d * 17 + m * 7 + p)
+    X = rng.standard_normal((n, d)).astype(np.float32)
+    Z = rng.standard_normal((n, m)).astype(np.float32)
+    assert col_rel_l2(lp_gpu(X, Z, p, mode), oracle.brute_lp(X, Z, p)) <= TOL[p]
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("p", [3, 5])
+def test_lp_integer_ties_exact(p, mode):
+    rng = np.random.default_rng(100 + p)
+    X = rng.integers(0, 5, size=(3001, 3)).astype(np.float32)
+    Z = rng.integers(-3, 4, size=(3001, 6)).astype(np.float32)
+    assert np.array_equal(lp_gpu(X, Z, p, mode), oracle.lp_sorted(X, Z, p))
+
+
+def test_lp_p1_entry_is_l1_and_bad_p_rejected():
+    rng = np.random.default_rng(7)
+    X = rng.standard_normal((900, 3)).astype(np.float32)
+    Z = rng.standard_normal((900, 4)).astype(np.float32)
+    assert col_rel_l2(lp_gpu(X, Z, 1), oracle.brute(X, Z)) <= 1e-9
+    h = l1.l1dm_prepare(torch.from_numpy(X).cuda())
+    for bad in (0, 2, 4, 9, -1):
+        with pytest.raises(l1.L1dmError) as e:
+            l1.l1dm_matvec_lp(h, bad, torch.from_numpy(Z).cuda())
+        assert e.value.name == "L1DM_EINVAL"
+    l1.l1dm_free(h)
+
+
+def test_lp_shards_sum_to_whole_exactly():
+    rng = np.random.default_rng(8)
+    X = rng.integers(0, 6, size=(2500, 5)).astype(np.float32)
+    Z = rng.integers(-2, 3, size=(2500, 4)).astype(np.float32)
+    parts = [lp_gpu(X, Z, 3, "gather", (a, b)) for a, b in [(0, 2), (2, 5)]]
+    assert np.array_equal(sum(parts), oracle.lp_sorted(X, Z, 3))
+
+
+def test_lp_gather_chunks_and_host_pointers():
+    rng = np.random.default_rng(9)
+    X = rng.standard_normal((4000, 6)).astype(np.float32)
+    Z = rng.standard_normal((4000, 3)).astype(np.float32)
+    h = l1.l1dm_prepare(X)                               # host X
+    l1.l1dm_set_query_mode(h, "gather")
+    l1.l1dm_set_workspace_limit(h, 1)                    # one coordinate per chunk
+    Y = l1.l1dm_matvec_lp(h, 3, Z)                        # host Z, host Y
+    assert col_rel_l2(Y.numpy(), oracle.brute_lp(X, Z, 3)) <= TOL[3]
+    l1.l1dm_free(h)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_tv_simplex_rows(mode):
+    rng = np.random.default_rng(10)
+    X = rng.dirichlet(np.ones(7), size=5000).astype(np.float32)
+    Z = rng.standard_normal((5000, 5)).astype(np.float32)
+    Yr = oracle.brute_tv(X, Z)
+    h = l1.l1dm_prepare(torch.from_numpy(X).cuda())
+    l1.l1dm_set_query_mode(h, mode)
+    Y = l1.l1dm_tv_matvec(h, torch.from_numpy(Z).cuda())
+    torch.cuda.synchronize()
+    assert col_rel_l2(Y.cpu().numpy(), Yr) <= 1e-9
+    l1.l1dm_free(h)
+
+
+def test_tv_rejects_rows_off_the_simplex():
+    rng = np.random.default_rng(11)
+    X = rng.dirichlet(np.ones(4), size=300).astype(np.float32)
+    Z = rng.standard_normal((300, 2)).astype(np.float32)
+    for bad in (X * 1.01, X - 0.01 * (X == X.max(1, keepdims=True))):
+        bad = bad.astype(np.float32)
+        h = l1.l1dm_prepare(torch.from_numpy(bad).cuda())
+        with pytest.raises(l1.L1dmError) as e:
+            l1.l1dm_tv_matvec(h, torch.from_numpy(Z).cuda())
+        assert e.value.name == "L1DM_ENOTSIMPLEX"
+        l1.l1dm_free(h)
+    neg = X.copy()
+    neg[0, 0] = -1e-3
+    neg[0, 1] += 1e-3
+    h = l1.l1dm_prepare(torch.from_numpy(neg).cuda())
+    with pytest.raises(l1.L1dmError):
+        l1.l1dm_tv_matvec(h, torch.from_numpy(Z).cuda())
+    l1.l1dm_free(h)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("p", [3, 5])
+def test_lp_c3_size_sampled(p):
+    """BASELINE configs[2]'s shape (n = 2^20, d = 128, m = 64, U[-1,1)): sampled rows."""
+    from paper_2210_15114_b200 import workloads as wl
+    w = wl.workload("c3")
+    X = wl.make_points(w, "cuda")
+    Z = wl.make_query(w, 0, "cuda")
+    h = l1.l1dm_prepare(X)
+    Y = l1.l1dm_matvec_lp(h, p, Z)
+    torch.cuda.synchronize()
+    rows = np.array([0, 1, 4095, 123457, 654321, w.n - 1])
+    Yg = Y[torch.from_numpy(rows).cuda()].cpu().numpy()
+    l1.l1dm_free(h)
+    Yr = oracle.rows_lp(X.cpu().numpy(), Z.cpu().numpy(), p, rows)
+    assert col_rel_l2(Yg, Yr) <= TOL[p]

@@ -96,6 +96,14 @@ def test_sorted_route_matches_definition(p):
     assert abs(lhs - rhs) <= 1e-12 * abs(lhs)
 
 
+def test_rows_lp_equals_brute_rows():
+    X = RNG.standard_normal((60, 4)).astype(np.float32)
+    Z = RNG.standard_normal((60, 2)).astype(np.float32)
+    rows = np.array([0, 7, 59, 7])
+    for p in (1, 3, 5):
+        assert np.array_equal(oracle.rows_lp(X, Z, p, rows), oracle.brute_lp(X, Z, p)[rows])
+
+
 def test_tv_is_half_l1_on_simplex_rows():
     X = RNG.dirichlet(np.ones(5), size=40).astype(np.float32)
     Z = RNG.standard_normal((40, 3)).astype(np.float32)
