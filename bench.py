@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--reduce", default="reduce", choices=["reduce", "allreduce"])
+    ap.add_argument("--p", type=int, default=1, choices=[1, 3, 5, 7],
+                    help="l_p^p query for odd p (SURVEY §8(f) NEXT-1); 1 = the l1 north star")
     ap.add_argument("--mode", default="auto", choices=["auto", "gather", "scatter"],
                     help="query strategy (include/l1dm.h l1dm_set_query_mode)")
     ap.add_argument("--overlap-blocks", type=int, default=4,
@@ -219,7 +221,7 @@ def main_ours(args):
     kr = (0, k1 - k0)
 
     def one_step(timing=False):
-        sh = ShardedL1DM(X, k_range=kr, stream=stream, mode=args.mode)
+        sh = ShardedL1DM(X, k_range=kr, stream=stream, mode=args.mode, p=args.p)
         sh.world = world
         if timing and sh.handle is not None:
             l1.l1dm_timing_enable(sh.handle, True)
@@ -279,7 +281,32 @@ def main_ours(args):
     for kv in kern.values():
         kv["ms_per_launch"] = kv["ms_total"] / max(kv["launches"] or 1, 1) if kv["ms_total"] else None
     l2p = load_l2_peaks()
-    if plan["scatter"] and m > 1:
+    if args.p > 1:
+        # l_p^p, odd p: the seq scan with p+1 moments in both strategies.
+        # scatter: the apply pass's fp64 L2 reductions, one per update, as for p = 1.
+        # gather: HBM bytes per query = per (i,k): two passes of perm/sval (16) and Zt rows
+        # (8m) gathered from HBM, the U store (8m) and k6's rank + U gather (4 + 8m); Y 8m per
+        # point.  Reported against the HBM peak for the whole query (its kernels interleave).
+        for kv in kern.values():
+            kv["achieved_GBps"] = None
+        if plan["scatter"]:
+            red = agg.get("queries", 0) * n * dl * m
+            acc = kern["accumulate"]
+            dominant = "accumulate"
+            ach = (red / (acc["ms_total"] * 1e-3) / 1e9) if acc["ms_total"] else None
+            peak = l2p.get("red_row8_adds_per_s", 5.88e11) / 1e9
+            roof = {"bound": "l2_fp64_reductions", "kernel": f"apply (k5_scan_seq<mb,APPLY,{args.p}>)",
+                    "achieved": ach, "peak": peak, "unit": "G fp64 reductions/s",
+                    "peak_kind": "measured (tools/l2_probe.cu -> profiles/l2_peaks.json)",
+                    "frac": (ach / peak) if ach else None}
+        else:
+            qbytes = n * dl * (16 + 8 * m + 8 * m + 4 + 8 * m) + n * 8 * m
+            ach = qbytes / (query_kernel_ms * 1e-3) / 1e9 if query_kernel_ms else None
+            dominant = "query"
+            roof = {"bound": "hbm", "kernel": "whole query (seq reduce/apply-store + k6)",
+                    "achieved": ach, "peak": hbm_peak, "peak_kind": peak_kind, "unit": "GB/s",
+                    "frac": (ach / hbm_peak) if ach else None, "alg_bytes_per_query": qbytes}
+    elif plan["scatter"] and m > 1:
         # scatter mode: per column block, "scan" = reduce + prefix (perm/sval
         # streamed from HBM, one Zt row gathered from L2 per pair), "accumulate" = apply (the
         # same gathers plus one fp64 L2 reduction per update).  The apply pass is bounded by the
@@ -324,7 +351,7 @@ def main_ours(args):
                             "bound (DESIGN.md §6)")
     traffic = None
     prof = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.workload}.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and args.p == 1:
         try:
             tr = json.load(open(prof))
             traffic = tr.get(f"{'scatter' if plan['scatter'] else 'gather'}_{dominant}",
@@ -347,6 +374,7 @@ def main_ours(args):
                    "collective": (args.reduce if world > 1 else None),
                    "overlap_blocks": (args.overlap_blocks if world > 1 else None),
                    "mode": args.mode, "strategy": ("scatter" if plan["scatter"] else "gather"),
+                   "query": "l1" if args.p == 1 else f"lp^p, p={args.p}",
                    "columns_per_block": plan["mb"],
                    "l2": "inputs > L2 (prepared state 12*n*d B), no flush"},
         "gpu_launches": int(agg.get("kernel_launches", 0)),
@@ -370,7 +398,10 @@ def main_ours(args):
         h = l1.l1dm_prepare(Xh)
         l1.l1dm_set_query_mode(h, args.mode)
         for q in range(Q):
-            l1.l1dm_matvec(h, Zh[q % len(Zh)], Yh)
+            if args.p == 1:
+                l1.l1dm_matvec(h, Zh[q % len(Zh)], Yh)
+            else:
+                l1.l1dm_matvec_lp(h, args.p, Zh[q % len(Zh)], Yh)
         l1.l1dm_free(h)
         e2e_s = time.perf_counter() - t0
         result["e2e"] = {"value": upd_step / e2e_s, "unit": "updates/s",

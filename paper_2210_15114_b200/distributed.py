@@ -33,7 +33,8 @@ class ShardedL1DM:
 
     def __init__(self, X: torch.Tensor, group=None, *, k_range=None,
                  local_prepare: Optional[Callable] = None,
-                 local_matvec: Optional[Callable] = None, stream=None, mode: str = "auto"):
+                 local_matvec: Optional[Callable] = None, stream=None, mode: str = "auto",
+                 p: int = 1):
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -41,6 +42,9 @@ class ShardedL1DM:
         self.k_begin, self.k_end = k_range if k_range is not None else shard_range(
             d, self.rank, self.world)
         self._prepare = local_prepare or binding.l1dm_prepare
+        if local_matvec is None and p != 1:   # l_p^p, odd p (Thm. odd_p): same sharding, A = sum_k A^(k)
+            local_matvec = (lambda h, Z, Y=None, stream=None:
+                            binding.l1dm_matvec_lp(h, p, Z, Y, stream=stream))
         self._matvec = local_matvec or binding.l1dm_matvec
         self.stream = stream
         if self.k_end > self.k_begin:

@@ -1,10 +1,11 @@
 """l_p^p (odd p) and TV queries through the C ABI against the CPU oracle.
 
-Tolerances (R18): the query evaluates sum_t c_t x^(p-t) (2 M_t - T_t) with fp64
-moments M_t of z x^t; the moments of |x| ~ 1 data are O(n) and cancel to the O(n) result
-only mildly, so float data meets 1e-9 for p = 3 and, measured here with >100x margin, 1e-9 /
-1e-8 for p = 5 / 7.  Integer data with small moments is exact (every partial sum is an
-integer < 2^53) and is checked bit-for-bit.  TV is half the l1 product: same 1e-9 bar."""
+Tolerance (R18): the query evaluates sum_t c_t x^(p-t) (2 M_t - T_t) with fp64
+moments M_t of z x^t.  For |x| ~ 1 data the moments are O(n) and cancel to the O(n) result
+only mildly: measured max column relative l2 error ~6e-16 for p = 3, 5, 7 (scratch/lp_probe.py),
+so the l1 bar of 1e-9 holds with ~6 orders of margin.  Integer data with small moments is exact
+(every partial sum is an integer < 2^53) and is checked bit-for-bit.  TV is half the l1
+product: same 1e-9 bar."""
 import numpy as np
 import pytest
 import torch
@@ -14,7 +15,7 @@ import paper_2210_15114_b200 as l1
 from conftest import GOLDEN_LP, GOLDEN_TV, col_rel_l2, golden_p, load_golden
 
 pytestmark = pytest.mark.gpu
-TOL = {1: 1e-9, 3: 1e-9, 5: 1e-9, 7: 1e-8}
+TOL = {1: 1e-9, 3: 1e-9, 5: 1e-9, 7: 1e-9}
 MODES = ["gather", "scatter"]
 
 
