@@ -51,10 +51,11 @@ def _load():
         lib.oracle_lp_sorted.argtypes = [vp, i64, i64, vp, vp, i64, i32, vp, i32]
         lib.oracle_brute_tv.argtypes = [vp, i64, i64, vp, i64, vp, i32]
         lib.oracle_rows_lp.argtypes = [vp, i64, i64, vp, i64, i32, vp, i64, vp, i32]
+        lib.oracle_lp_even.argtypes = [vp, i64, i64, vp, i64, i32, vp, i32]
         for f in (lib.oracle_brute, lib.oracle_rows, lib.oracle_alg1, lib.oracle_alg2,
                   lib.oracle_alg2_range, lib.oracle_hist, lib.oracle_num_threads,
                   lib.oracle_brute_lp, lib.oracle_lp_sorted, lib.oracle_brute_tv,
-                  lib.oracle_rows_lp):
+                  lib.oracle_rows_lp, lib.oracle_lp_even):
             f.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -202,4 +203,15 @@ def brute_tv(X, Z, nthreads: int = 0) -> np.ndarray:
     Y = np.empty((n, Z2.shape[1]), dtype=np.float64)
     _check(_load().oracle_brute_tv(_ptr(X), n, d, _ptr(Z2), Z2.shape[1], _ptr(Y), nthreads),
            "brute_tv")
+    return Y.reshape(-1) if np.ndim(Z) == 1 else Y
+
+
+def lp_even(X, Z, p: int, nthreads: int = 0) -> np.ndarray:
+    """Even p: Alg. "query_p_even" with SPEC S:140-146's corrections."""
+    X = _f32(X)
+    n, d = X.shape
+    Z2 = _as2d(Z, n)
+    Y = np.empty((n, Z2.shape[1]), dtype=np.float64)
+    _check(_load().oracle_lp_even(_ptr(X), n, d, _ptr(Z2), Z2.shape[1], int(p), _ptr(Y),
+                                  nthreads), "lp_even")
     return Y.reshape(-1) if np.ndim(Z) == 1 else Y

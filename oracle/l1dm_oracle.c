@@ -28,6 +28,10 @@
  *                       sums in sorted order of z_j x_j^(p-t); per point, below/above split
  *                       at its position; y_k += sum_t C(p,t) (-1)^(p-t) x_k^t (below - above)
  *   oracle_brute_tv   — TV(x, y) = (1/2) sum_k |x_k - y_k|, the definition (Thm. tv)
+ *   oracle_lp_even    — even p, Alg. "query_p_even" step by step with the
+ *                       corrections of SPEC S:140-146 (the text drops y_j and C(p,t) and
+ *                       starts t at 1): S_{i,t} = C(p,t) (-1)^(p-t) sum_j y_j x_j(i)^(p-t),
+ *                       z(k) = sum_i sum_{t=0}^{p} x_k(i)^t S_{i,t}
  *
  * Precision: inputs are fp32 (BASELINE.json); every sum is accumulated in
  * x86 80-bit long double ("fp64 or better", reading R6) and
@@ -497,5 +501,51 @@ int oracle_lp_sorted(const float *X, int64_t n, int64_t d, const uint32_t *order
     return ORACLE_EINVAL;
   lps_args a = {X, n, d, order, Z, m, p, Y};
   run_parallel(lp_sorted_columns, &a, m, 1, nthreads);
+  return ORACLE_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* Even p: Alg. "query_p_even" with SPEC S:140-146's corrections, one column of Z
+ * at a time (Lemma matrixmult).  Line "Compute all the values S_{i,t}" then the loop over k.  */
+/* ------------------------------------------------------------------ */
+typedef struct {
+  const float *X; int64_t n, d;
+  const float *Z; int64_t m;
+  int p;
+  double *Y;
+} lpe_args;
+
+static void lp_even_columns(void *pa, int64_t lo, int64_t hi) {
+  lpe_args *a = (lpe_args *)pa;
+  const int p = a->p;
+  acc_t *S = (acc_t *)malloc(sizeof(acc_t) * (size_t)a->d * (size_t)(p + 1));
+  acc_t binom[32];
+  binom[0] = 1.0L;
+  for (int t = 1; t <= p; ++t) binom[t] = binom[t - 1] * (acc_t)(p - t + 1) / (acc_t)t;
+  for (int64_t c = lo; c < hi; ++c) {
+    for (int64_t i = 0; i < a->d; ++i)                 /* S_{i,t} for all i, t */
+      for (int t = 0; t <= p; ++t) {
+        acc_t sum = 0.0L;
+        for (int64_t j = 0; j < a->n; ++j)
+          sum += (acc_t)a->Z[j * a->m + c] * powi_l((acc_t)a->X[j * a->d + i], p - t);
+        acc_t sgn = ((p - t) & 1) ? -1.0L : 1.0L;
+        S[i * (p + 1) + t] = binom[t] * sgn * sum;
+      }
+    for (int64_t k = 0; k < a->n; ++k) {               /* z(k) = sum_i sum_t x_k(i)^t S_{i,t} */
+      acc_t z = 0.0L;
+      for (int64_t i = 0; i < a->d; ++i)
+        for (int t = 0; t <= p; ++t) z += powi_l((acc_t)a->X[k * a->d + i], t) * S[i * (p + 1) + t];
+      a->Y[k * a->m + c] = (double)z;
+    }
+  }
+  free(S);
+}
+
+int oracle_lp_even(const float *X, int64_t n, int64_t d, const float *Z, int64_t m, int p,
+                   double *Y, int nthreads) {
+  if (!X || !Z || !Y || n < 1 || d < 1 || m < 1 || p < 2 || p > 30 || (p & 1))
+    return ORACLE_EINVAL;
+  lpe_args a = {X, n, d, Z, m, p, Y};
+  run_parallel(lp_even_columns, &a, m, 1, nthreads);
   return ORACLE_OK;
 }

@@ -44,6 +44,7 @@ def golden_p(name):
 GOLDEN = ["q1_three_points.txt", "q2_identity.txt", "q20_two_dim.txt", "q21_ties_negative.txt"]
 GOLDEN_LP = ["lp3_three_points.txt", "lp5_two_dim.txt"]
 GOLDEN_TV = ["tv_two_points.txt"]
+GOLDEN_EVEN = ["l2sq_three_points.txt", "lp4_two_points.txt"]
 
 
 def col_rel_l2(Y, Yref, floor=0.0):

@@ -117,3 +117,44 @@ def test_lp_rejects_even_p_in_sorted_route():
     X = np.zeros((3, 1), dtype=np.float32)
     with pytest.raises(ValueError):
         oracle.lp_sorted(X, np.ones((3, 1), dtype=np.float32), 2)
+
+
+# ---- even p (NEXT-4): brute_lp (definition) and lp_even (Alg. query_p_even, corrected) ----
+from conftest import GOLDEN_EVEN  # noqa: E402
+
+
+@pytest.mark.parametrize("name", GOLDEN_EVEN)
+def test_even_goldens(name):
+    X, Z, Y = load_golden(name)
+    p = golden_p(name)
+    assert np.array_equal(oracle.brute_lp(X, Z, p), Y)
+    assert np.array_equal(oracle.lp_even(X, Z, p), Y)
+
+
+def test_l2sq_gram_identity_exact():
+    """||a - b||^2 = ||a||^2 + ||b||^2 - 2 a.b: A_2 Z = h (1^T Z) + 1 (h^T Z) - 2 X (X^T Z),
+    evaluated with numpy int64 matmul on integer data (a library routine, exact)."""
+    X = RNG.integers(-5, 6, size=(40, 7))
+    Z = RNG.integers(-3, 4, size=(40, 3))
+    h = (X * X).sum(1)
+    want = h[:, None] * Z.sum(0)[None, :] + (h @ Z)[None, :] - 2 * (X @ (X.T @ Z))
+    Xf, Zf = X.astype(np.float32), Z.astype(np.float32)
+    assert np.array_equal(oracle.brute_lp(Xf, Zf, 2), want.astype(np.float64))
+    assert np.array_equal(oracle.lp_even(Xf, Zf, 2), want.astype(np.float64))
+
+
+@pytest.mark.parametrize("p", [2, 4, 6])
+def test_even_routes_agree_and_collinear(p):
+    n = 17
+    u = np.array([2, -1], dtype=np.int64)
+    X = (np.arange(n)[:, None] * u[None, :]).astype(np.float32)
+    up = int(sum(abs(int(v)) ** p for v in u))
+    want = np.array([up * (sum(a ** p for a in range(1, i + 1)) + sum(a ** p for a in range(1, n - i)))
+                     for i in range(n)], dtype=np.float64)
+    ones = np.ones((n, 1), dtype=np.float32)
+    assert np.array_equal(oracle.brute_lp(X, ones, p)[:, 0], want)
+    assert np.array_equal(oracle.lp_even(X, ones, p)[:, 0], want)
+    Xf = RNG.standard_normal((30, 4)).astype(np.float32)
+    Zf = RNG.standard_normal((30, 2)).astype(np.float32)
+    a, b = oracle.lp_even(Xf, Zf, p), oracle.brute_lp(Xf, Zf, p)
+    assert np.abs(a - b).max() <= 1e-12 * np.abs(b).max()
