@@ -48,8 +48,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--reduce", default="reduce", choices=["reduce", "allreduce"])
-    ap.add_argument("--p", type=int, default=1, choices=[1, 3, 5, 7],
-                    help="l_p^p query for odd p (SURVEY §8(f) NEXT-1); 1 = the l1 north star")
+    ap.add_argument("--p", type=int, default=1, choices=[1, 2, 3, 4, 5, 6, 7],
+                    help="l_p^p query: odd p sort-based (NEXT-1), even p sort-free (NEXT-4); "
+                         "1 = the l1 north star")
     ap.add_argument("--mode", default="auto", choices=["auto", "gather", "scatter"],
                     help="query strategy (include/l1dm.h l1dm_set_query_mode)")
     ap.add_argument("--overlap-blocks", type=int, default=4,
@@ -223,7 +224,7 @@ def main_ours(args):
     def one_step(timing=False):
         sh = ShardedL1DM(X, k_range=kr, stream=stream, mode=args.mode, p=args.p)
         sh.world = world
-        if timing and sh.handle is not None:
+        if timing and sh.handle is not None and args.p % 2 == 1:
             l1.l1dm_timing_enable(sh.handle, True)
         for q in range(Q):
             sh.matvec(Zs[q % len(Zs)], Y, root=None if args.reduce == "allreduce" else 0,
@@ -246,7 +247,7 @@ def main_ours(args):
     ev0.record(stream)
     for s in range(args.steps):
         sh = one_step(timing=True)
-        if sh.handle is not None:
+        if sh.handle is not None and args.p % 2 == 1:
             timings.append(l1.l1dm_timing_read(sh.handle))  # syncs the stream (host only)
         sh.close()
     ev1.record(stream)
@@ -281,7 +282,21 @@ def main_ours(args):
     for kv in kern.values():
         kv["ms_per_launch"] = kv["ms_total"] / max(kv["launches"] or 1, 1) if kv["ms_total"] else None
     l2p = load_l2_peaks()
-    if args.p > 1:
+    if args.p % 2 == 0:
+        # even p (NEXT-4, sort-free): two fp64 FMA contractions (moment reduce + expand),
+        # 2 n d m (2p - 1) flops per query; bound: fp64 FMA on the CUDA cores, peak derived from
+        # the unit count (64 fp64 FMA/clk/SM x 148 SMs x 2 flops x the max SM clock)
+        for kv in kern.values():
+            kv["achieved_GBps"] = None
+        flops = 2.0 * n * dl * m * (2 * args.p - 1)
+        ach = flops / (ms_step * 1e-3 / Q) / 1e12
+        peak = 64 * 148 * 2 * 1.965e9 / 1e12
+        dominant = "query"
+        roof = {"bound": "alu", "kernel": "whole query (k12 reduce + k13 fold + k14 expand)",
+                "achieved": ach, "peak": peak, "unit": "TFLOP/s (fp64)",
+                "peak_kind": "derived: 64 fp64 FMA/clk/SM x 148 SMs x 2 x 1.965 GHz",
+                "frac": ach / peak, "alg_flops_per_query": flops}
+    elif args.p > 1:
         # l_p^p, odd p: the seq scan with p+1 moments in both strategies.
         # scatter: the apply pass's fp64 L2 reductions, one per update, as for p = 1.
         # gather: HBM bytes per query = per (i,k): two passes of perm/sval (16) and Zt rows
@@ -362,7 +377,7 @@ def main_ours(args):
     # the U-materialising design's HBM floor (Model B bytes) over the measured query time:
     # above 1.0 means the query beats that design's roofline
     roof["model_b_hbm_equivalent_frac"] = (qb / (query_kernel_ms * 1e-3) / 1e9 / hbm_peak
-                                           if query_kernel_ms else None)
+                                           if query_kernel_ms and args.p % 2 == 1 else None)
     result = {
         "metric": METRIC,
         "value": value, "unit": "updates/s", "n_gpus": world, "steps": args.steps,
@@ -395,17 +410,22 @@ def main_ours(args):
         Yh = torch.empty((n, m), dtype=torch.float64).pin_memory()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        h = l1.l1dm_prepare(Xh)
-        l1.l1dm_set_query_mode(h, args.mode)
-        for q in range(Q):
-            if args.p == 1:
-                l1.l1dm_matvec(h, Zh[q % len(Zh)], Yh)
-            else:
-                l1.l1dm_matvec_lp(h, args.p, Zh[q % len(Zh)], Yh)
-        l1.l1dm_free(h)
+        if args.p % 2 == 0:
+            for q in range(Q):
+                l1.l1dm_lpp_even_matvec(Xh, args.p, Zh[q % len(Zh)], Yh)
+        else:
+            h = l1.l1dm_prepare(Xh)
+            l1.l1dm_set_query_mode(h, args.mode)
+            for q in range(Q):
+                if args.p == 1:
+                    l1.l1dm_matvec(h, Zh[q % len(Zh)], Yh)
+                else:
+                    l1.l1dm_matvec_lp(h, args.p, Zh[q % len(Zh)], Yh)
+            l1.l1dm_free(h)
         e2e_s = time.perf_counter() - t0
         result["e2e"] = {"value": upd_step / e2e_s, "unit": "updates/s",
-                         "h2d_bytes_per_step": int(Xh.numel() * 4 + Q * n * m * 4),
+                         "h2d_bytes_per_step": int(Xh.numel() * 4 * (Q if args.p % 2 == 0 else 1)
+                                                   + Q * n * m * 4),
                          "d2h_bytes_per_step": int(Q * n * m * 8),
                          "note": "l1dm_prepare(host X) + per query l1dm_matvec(host Z, host Y)"}
         del Xh, Zh, Yh

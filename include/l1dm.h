@@ -142,6 +142,22 @@ L1DM_API l1dm_status l1dm_tv_matvec_ex(l1dm_handle h, const float *Z, int64_t ld
                                        double *Y, int64_t ld_y, void *stream);
 L1DM_API l1dm_status l1dm_tv_matvec(l1dm_handle h, const float *Z, int64_t m, double *Y);
 
+/* ---------------------------------------------------------------------------
+ * Sort-free l_p^p for even p (Alg. "query_p_even" and Thm. even_p,
+ * P:453-481, with the C(p,t) and y_j the text drops — SPEC S:140-146, R19; p = 2
+ * is the squared-Euclidean case of Alg. 3):
+ *   Y = A_p Z,  (A_p)_ij = sum_k (x_ik - x_jk)^p,  p in {2, 4, 6},
+ *   y_ic = sum_k sum_t C(p,t) (-1)^t x_ik^(p-t) W_t[k][c],  W_t[k][c] = sum_j x_jk^t z_jc.
+ * No preprocessing and no handle: X (n x ld_x fp32, d coordinates used), Z (n x ld_z fp32),
+ * Y (n x ld_y fp64, OVERWRITTEN).  Device pointers: stream-ordered on `stream` (scratch from
+ * the stream-ordered allocator); any host pointer makes the call synchronous (staged).
+ * fp64 accumulation of fp32 inputs; the moments of large |x| cancel (R18).
+ * Errors: EINVAL (null, sizes, leading dimensions, p not in {2, 4, 6}), EDEVICE, ENOMEM,
+ * ECUDA. */
+L1DM_API l1dm_status l1dm_lpp_even_matvec(const float *X, int64_t n, int64_t ld_x, int64_t d,
+                                          int p, const float *Z, int64_t ld_z, int64_t m,
+                                          double *Y, int64_t ld_y, void *stream);
+
 /* Release every buffer the handle owns.  NULL is a no-op.  Synchronises the
  * handle's stream first. */
 L1DM_API void l1dm_free(l1dm_handle h);

@@ -28,6 +28,7 @@ STATUS = {
 EXPORTS = [
     "l1dm_prepare", "l1dm_prepare_ex", "l1dm_matvec", "l1dm_matvec_ex", "l1dm_matvec_pipelined",
     "l1dm_matvec_lp", "l1dm_matvec_lp_ex", "l1dm_tv_matvec", "l1dm_tv_matvec_ex",
+    "l1dm_lpp_even_matvec",
     "l1dm_free", "l1dm_sync",
     "l1dm_shape", "l1dm_workspace_bytes", "l1dm_set_workspace_limit", "l1dm_set_query_mode",
     "l1dm_plan", "l1dm_plan_ex", "l1dm_timing_enable", "l1dm_timing_read", "l1dm_debug_export", "l1dm_release_cached",
@@ -81,6 +82,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.l1dm_matvec_lp.argtypes = [vp, i32, vp, i64, vp]
     lib.l1dm_tv_matvec_ex.argtypes = [vp, vp, i64, i64, vp, i64, vp]
     lib.l1dm_tv_matvec.argtypes = [vp, vp, i64, vp]
+    lib.l1dm_lpp_even_matvec.argtypes = [vp, i64, i64, i64, i32, vp, i64, i64, vp, i64, vp]
     lib.l1dm_matvec_pipelined.argtypes = [vp, vp, i64, i64, vp, i64, vp, i64,
                                            ctypes.POINTER(vp)]
     lib.l1dm_free.argtypes = [vp]
@@ -104,7 +106,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.l1dm_version.restype = ctypes.c_char_p
     for name in ("l1dm_prepare", "l1dm_prepare_ex", "l1dm_matvec", "l1dm_matvec_ex",
                  "l1dm_matvec_pipelined", "l1dm_sync", "l1dm_matvec_lp", "l1dm_matvec_lp_ex",
-                 "l1dm_tv_matvec", "l1dm_tv_matvec_ex",
+                 "l1dm_tv_matvec", "l1dm_tv_matvec_ex", "l1dm_lpp_even_matvec",
                  "l1dm_shape", "l1dm_set_workspace_limit", "l1dm_set_query_mode", "l1dm_plan", "l1dm_plan_ex",
                  "l1dm_timing_enable",
                  "l1dm_timing_read", "l1dm_debug_export"):
@@ -224,6 +226,33 @@ def l1dm_matvec_lp(h: Handle, p: int, Z, Y=None, stream=None):
 def l1dm_tv_matvec(h: Handle, Z, Y=None, stream=None):
     """Total-variation block product (Thm. tv) for rows on the probability simplex."""
     return _query("l1dm_tv_matvec_ex", (), h, Z, Y, stream)
+
+
+def l1dm_lpp_even_matvec(X, p: int, Z, Y=None, stream=None):
+    """Sort-free even-p l_p^p block product (p in {2, 4, 6}; p = 2: squared Euclidean).
+    No preprocessing: X (n x d) is read by the call."""
+    lib = load_library()
+    X = _as_f32_2d(X, "X")
+    squeeze = (Z.ndim == 1)
+    Z = _as_f32_2d(Z, "Z")
+    n, d = X.shape
+    if Z.shape[0] != n:
+        raise ValueError(f"Z has {Z.shape[0]} rows, X has {n}")
+    m = Z.shape[1]
+    if Y is None:
+        Y = torch.empty((n, m), dtype=torch.float64, device=Z.device)
+    if Y.dtype != torch.float64 or Y.shape != (n, m) or Y.stride(1) != 1:
+        raise ValueError("Y must be an n x m float64 row-major tensor")
+    dev = Z.device if Z.is_cuda else (X.device if X.is_cuda else None)
+    if dev is not None:
+        with torch.cuda.device(dev):
+            rc = lib.l1dm_lpp_even_matvec(_ptr(X), n, X.stride(0), d, int(p), _ptr(Z), Z.stride(0),
+                                          m, _ptr(Y), Y.stride(0), _stream_of(Z, stream))
+    else:
+        rc = lib.l1dm_lpp_even_matvec(_ptr(X), n, X.stride(0), d, int(p), _ptr(Z), Z.stride(0), m,
+                                      _ptr(Y), Y.stride(0), _stream_of(Z, stream))
+    _check(rc, "l1dm_lpp_even_matvec")
+    return Y.view(-1) if squeeze else Y
 
 
 def point_blocks(n: int, nblocks: int):

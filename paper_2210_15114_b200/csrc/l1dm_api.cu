@@ -939,6 +939,74 @@ l1dm_status l1dm_tv_matvec(l1dm_handle h, const float *Z, int64_t m, double *Y) 
   return query_entry(h, kQueryTV, 1, Z, m, m, Y, m, (void *)h->stream);
 }
 
+l1dm_status l1dm_lpp_even_matvec(const float *X, int64_t n, int64_t ld_x, int64_t d, int p,
+                                 const float *Z, int64_t ld_z, int64_t m, double *Y, int64_t ld_y,
+                                 void *stream) {
+  g_err.clear();
+  if (!X || !Z || !Y) return fail(L1DM_EINVAL, "X, Z or Y is NULL");
+  if (n < 1 || d < 1 || m < 1 || ld_x < d || ld_z < m || ld_y < m)
+    return fail(L1DM_EINVAL, "n=%lld d=%lld m=%lld ld_x=%lld ld_z=%lld ld_y=%lld invalid",
+                (long long)n, (long long)d, (long long)m, (long long)ld_x, (long long)ld_z,
+                (long long)ld_y);
+  if (p != 2 && p != 4 && p != 6) return fail(L1DM_EINVAL, "p=%d: even p in {2, 4, 6} only", p);
+  int dev = 0;
+  l1dm_status st = check_arch(&dev);
+  if (st != L1DM_OK) return st;
+  int sms = 148;
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool xdev = is_device_pointer(X), zdev = is_device_pointer(Z), ydev = is_device_pointer(Y);
+  // stream-ordered scratch (cudaMallocAsync): the call stays asynchronous for device buffers
+  const size_t wsb = lpp_even_workspace(n, d, m, p, nullptr, nullptr, sms);
+  void *ws = nullptr, *xs = nullptr, *zs = nullptr, *ys = nullptr;
+  auto release = [&]() {
+    if (ws) cudaFreeAsync(ws, s);
+    if (xs) cudaFreeAsync(xs, s);
+    if (zs) cudaFreeAsync(zs, s);
+    if (ys) cudaFreeAsync(ys, s);
+  };
+  cudaError_t e = cudaMallocAsync(&ws, wsb, s);
+  const float *Xd = X, *Zd = Z;
+  double *Yd = Y;
+  int64_t ldxd = ld_x, ldzd = ld_z, ldyd = ld_y;
+  if (e == cudaSuccess && !xdev) {
+    e = cudaMallocAsync(&xs, (size_t)n * d * sizeof(float), s);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(xs, (size_t)d * sizeof(float), X, (size_t)ld_x * sizeof(float),
+                            (size_t)d * sizeof(float), (size_t)n, cudaMemcpyHostToDevice, s);
+    Xd = static_cast<const float *>(xs);
+    ldxd = d;
+  }
+  if (e == cudaSuccess && !zdev) {
+    e = cudaMallocAsync(&zs, (size_t)n * m * sizeof(float), s);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(zs, (size_t)m * sizeof(float), Z, (size_t)ld_z * sizeof(float),
+                            (size_t)m * sizeof(float), (size_t)n, cudaMemcpyHostToDevice, s);
+    Zd = static_cast<const float *>(zs);
+    ldzd = m;
+  }
+  if (e == cudaSuccess && !ydev) {
+    e = cudaMallocAsync(&ys, (size_t)n * m * sizeof(double), s);
+    Yd = static_cast<double *>(ys);
+    ldyd = m;
+  }
+  if (e != cudaSuccess) {
+    release();
+    cudaGetLastError();
+    return fail(e == cudaErrorMemoryAllocation ? L1DM_ENOMEM : L1DM_ECUDA, "lpp_even setup: %s",
+                cudaGetErrorString(e));
+  }
+  launch_lpp_even(Xd, ldxd, Zd, ldzd, n, d, m, p, Yd, ldyd, static_cast<double *>(ws), sms, s);
+  e = cudaGetLastError();
+  if (e == cudaSuccess && !ydev)
+    e = cudaMemcpy2DAsync(Y, (size_t)ld_y * sizeof(double), Yd, (size_t)m * sizeof(double),
+                          (size_t)m * sizeof(double), (size_t)n, cudaMemcpyDeviceToHost, s);
+  release();
+  if (e == cudaSuccess && !(xdev && zdev && ydev)) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return fail(L1DM_ECUDA, "lpp_even: %s", cudaGetErrorString(e));
+  return L1DM_OK;
+}
+
 l1dm_status l1dm_matvec_pipelined(l1dm_handle h, const float *Z, int64_t ld_z, int64_t m,
                                   double *Y, int64_t ld_y, void *stream, int64_t point_blocks,
                                   void *const *block_events) {

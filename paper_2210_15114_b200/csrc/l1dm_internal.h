@@ -139,4 +139,13 @@ void launch_scale(double *Y, int64_t ldy, int64_t n, int64_t m, double a, cudaSt
 void launch_simplex_stats(const double *hsum, int64_t n, const float *sval, int64_t ldn,
                           int64_t dl, double *out, cudaStream_t s);
 
+// ---------------- sort-free products (l1dm_sortfree.cu, NEXT-4) ----------------
+// Even p in {2, 4, 6}: Y = A_p Z with (A_p)_ij = ||x_i - x_j||_p^p, no preprocessing.
+// ws: lpp_even_workspace() bytes of device memory.
+size_t lpp_even_workspace(int64_t n, int64_t d, int64_t m, int p, int64_t *nchunks_out,
+                          int64_t *chunk_out, int sms);
+void launch_lpp_even(const float *X, int64_t ldx, const float *Z, int64_t ldz, int64_t n,
+                     int64_t d, int64_t m, int p, double *Y, int64_t ldy, double *ws, int sms,
+                     cudaStream_t s);
+
 }  // namespace l1dm

@@ -41,10 +41,14 @@ class ShardedL1DM:
         d = X.shape[1]
         self.k_begin, self.k_end = k_range if k_range is not None else shard_range(
             d, self.rank, self.world)
-        self._prepare = local_prepare or binding.l1dm_prepare
-        if local_matvec is None and p != 1:   # l_p^p, odd p (Thm. odd_p): same sharding, A = sum_k A^(k)
+        if local_matvec is None and p % 2 == 1 and p != 1:  # odd l_p^p (Thm. odd_p): A = sum_k A^(k)
             local_matvec = (lambda h, Z, Y=None, stream=None:
                             binding.l1dm_matvec_lp(h, p, Z, Y, stream=stream))
+        if local_prepare is None and p % 2 == 0:  # even p (NEXT-4): sort-free, the "handle" is X_g
+            local_prepare = (lambda X_, k0, k1, stream=None: X_[:, k0:k1].contiguous())
+            local_matvec = (lambda h, Z, Y=None, stream=None:
+                            binding.l1dm_lpp_even_matvec(h, p, Z, Y, stream=stream))
+        self._prepare = local_prepare or binding.l1dm_prepare
         self._matvec = local_matvec or binding.l1dm_matvec
         self.stream = stream
         if self.k_end > self.k_begin:
