@@ -158,6 +158,15 @@ L1DM_API l1dm_status l1dm_lpp_even_matvec(const float *X, int64_t n, int64_t ld_
                                           int p, const float *Z, int64_t ld_z, int64_t m,
                                           double *Y, int64_t ld_y, void *stream);
 
+/* The bilinear form of Thm. maha (the paper's "Mahalanobis distance squared" is
+ * f(x, y) = x^T M y for a d x d matrix M, R20):
+ *   Y = A Z,  A_ij = x_i^T M x_j,  i.e. Y = X (M (X^T Z))   (Alg. 8: v = S y, z(k) = <x_k, v>,
+ * with Alg. 7's S = M X^T applied, not stored).  M: d x d fp64 row-major (host or device).
+ * No handle; pointers, streams and errors as l1dm_lpp_even_matvec (EINVAL for a NULL M). */
+L1DM_API l1dm_status l1dm_bilinear_matvec(const float *X, int64_t n, int64_t ld_x, int64_t d,
+                                          const double *M, const float *Z, int64_t ld_z, int64_t m,
+                                          double *Y, int64_t ld_y, void *stream);
+
 /* Release every buffer the handle owns.  NULL is a no-op.  Synchronises the
  * handle's stream first. */
 L1DM_API void l1dm_free(l1dm_handle h);

@@ -52,10 +52,13 @@ def _load():
         lib.oracle_brute_tv.argtypes = [vp, i64, i64, vp, i64, vp, i32]
         lib.oracle_rows_lp.argtypes = [vp, i64, i64, vp, i64, i32, vp, i64, vp, i32]
         lib.oracle_lp_even.argtypes = [vp, i64, i64, vp, i64, i32, vp, i32]
+        lib.oracle_brute_bilinear.argtypes = [vp, i64, i64, vp, vp, i64, vp, i32]
+        lib.oracle_bilinear_alg.argtypes = [vp, i64, i64, vp, vp, i64, vp]
         for f in (lib.oracle_brute, lib.oracle_rows, lib.oracle_alg1, lib.oracle_alg2,
                   lib.oracle_alg2_range, lib.oracle_hist, lib.oracle_num_threads,
                   lib.oracle_brute_lp, lib.oracle_lp_sorted, lib.oracle_brute_tv,
-                  lib.oracle_rows_lp, lib.oracle_lp_even):
+                  lib.oracle_rows_lp, lib.oracle_lp_even, lib.oracle_brute_bilinear,
+                  lib.oracle_bilinear_alg):
             f.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -215,3 +218,28 @@ def lp_even(X, Z, p: int, nthreads: int = 0) -> np.ndarray:
     _check(_load().oracle_lp_even(_ptr(X), n, d, _ptr(Z2), Z2.shape[1], int(p), _ptr(Y),
                                   nthreads), "lp_even")
     return Y.reshape(-1) if np.ndim(Z) == 1 else Y
+
+
+def brute_bilinear(X, M, Z, nthreads: int = 0) -> np.ndarray:
+    """Thm. maha's form, the definition: Y[i,c] = sum_j Z[j,c] x_i^T M x_j."""
+    X = _f32(X)
+    n, d = X.shape
+    M = np.ascontiguousarray(M, dtype=np.float64)
+    assert M.shape == (d, d)
+    Z2 = _as2d(Z, n)
+    Y = np.empty((n, Z2.shape[1]), dtype=np.float64)
+    _check(_load().oracle_brute_bilinear(_ptr(X), n, d, _ptr(M), _ptr(Z2), Z2.shape[1], _ptr(Y),
+                                         nthreads), "brute_bilinear")
+    return Y
+
+
+def bilinear_alg(X, M, Z) -> np.ndarray:
+    """Algs. 7-8 step by step: S = [M x_j]_j, v = S y, z(k) = <x_k, v>."""
+    X = _f32(X)
+    n, d = X.shape
+    M = np.ascontiguousarray(M, dtype=np.float64)
+    Z2 = _as2d(Z, n)
+    Y = np.empty((n, Z2.shape[1]), dtype=np.float64)
+    _check(_load().oracle_bilinear_alg(_ptr(X), n, d, _ptr(M), _ptr(Z2), Z2.shape[1], _ptr(Y)),
+           "bilinear_alg")
+    return Y

@@ -28,6 +28,9 @@
  *                       sums in sorted order of z_j x_j^(p-t); per point, below/above split
  *                       at its position; y_k += sum_t C(p,t) (-1)^(p-t) x_k^t (below - above)
  *   oracle_brute_tv   — TV(x, y) = (1/2) sum_k |x_k - y_k|, the definition (Thm. tv)
+ *   oracle_brute_bilinear — A_ij = x_i^T M x_j, the definition (Thm. maha)
+ *   oracle_bilinear_alg   — Algs. 7-8 step by step: S = [M x_j]_j (d x n), v = S y,
+ *                           z(k) = <x_k, v>
  *   oracle_lp_even    — even p, Alg. "query_p_even" step by step with the
  *                       corrections of SPEC S:140-146 (the text drops y_j and C(p,t) and
  *                       starts t at 1): S_{i,t} = C(p,t) (-1)^(p-t) sum_j y_j x_j(i)^(p-t),
@@ -547,5 +550,82 @@ int oracle_lp_even(const float *X, int64_t n, int64_t d, const float *Z, int64_t
     return ORACLE_EINVAL;
   lpe_args a = {X, n, d, Z, m, p, Y};
   run_parallel(lp_even_columns, &a, m, 1, nthreads);
+  return ORACLE_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* Thm. maha: f(x, y) = x^T M y.  The definition, row by row: Y[i][c] =
+ * sum_j Z[j][c] x_i^T M x_j (M: d x d, row-major, fp64).                                    */
+/* ------------------------------------------------------------------ */
+typedef struct {
+  const float *X; int64_t n, d;
+  const double *M;
+  const float *Z; int64_t m;
+  double *Y;
+} bil_args;
+
+static void bilinear_rows(void *pa, int64_t lo, int64_t hi) {
+  bil_args *a = (bil_args *)pa;
+  const int64_t d = a->d;
+  acc_t *xm = (acc_t *)malloc(sizeof(acc_t) * (size_t)d);   /* x_i^T M */
+  acc_t *acc = (acc_t *)malloc(sizeof(acc_t) * (size_t)a->m);
+  for (int64_t i = lo; i < hi; ++i) {
+    for (int64_t l = 0; l < d; ++l) {
+      acc_t s = 0.0L;
+      for (int64_t k = 0; k < d; ++k) s += (acc_t)a->X[i * d + k] * (acc_t)a->M[k * d + l];
+      xm[l] = s;
+    }
+    for (int64_t c = 0; c < a->m; ++c) acc[c] = 0.0L;
+    for (int64_t j = 0; j < a->n; ++j) {
+      acc_t f = 0.0L;                                     /* x_i^T M x_j */
+      for (int64_t l = 0; l < d; ++l) f += xm[l] * (acc_t)a->X[j * d + l];
+      for (int64_t c = 0; c < a->m; ++c) acc[c] += f * (acc_t)a->Z[j * a->m + c];
+    }
+    for (int64_t c = 0; c < a->m; ++c) a->Y[i * a->m + c] = (double)acc[c];
+  }
+  free(xm);
+  free(acc);
+}
+
+int oracle_brute_bilinear(const float *X, int64_t n, int64_t d, const double *M, const float *Z,
+                          int64_t m, double *Y, int nthreads) {
+  if (!X || !M || !Z || !Y || n < 1 || d < 1 || m < 1) return ORACLE_EINVAL;
+  bil_args a = {X, n, d, M, Z, m, Y};
+  run_parallel(bilinear_rows, &a, n, 4, nthreads);
+  return ORACLE_OK;
+}
+
+/* Algs. 7-8: Preprocessing S <- d x n matrix with j-th column M x_j; Query v <- S y,
+ * z(k) <- <x_k, v>.  One column of Z at a time (Lemma matrixmult).  Single-threaded: small n. */
+int oracle_bilinear_alg(const float *X, int64_t n, int64_t d, const double *M, const float *Z,
+                        int64_t m, double *Y) {
+  if (!X || !M || !Z || !Y || n < 1 || d < 1 || m < 1) return ORACLE_EINVAL;
+  acc_t *S = (acc_t *)malloc(sizeof(acc_t) * (size_t)d * (size_t)n);
+  acc_t *v = (acc_t *)malloc(sizeof(acc_t) * (size_t)d);
+  if (!S || !v) {
+    free(S);
+    free(v);
+    return ORACLE_ENOMEM;
+  }
+  for (int64_t j = 0; j < n; ++j)                 /* S[:, j] = M x_j */
+    for (int64_t k = 0; k < d; ++k) {
+      acc_t s = 0.0L;
+      for (int64_t l = 0; l < d; ++l) s += (acc_t)M[k * d + l] * (acc_t)X[j * d + l];
+      S[k * n + j] = s;
+    }
+  for (int64_t c = 0; c < m; ++c) {
+    for (int64_t k = 0; k < d; ++k) {             /* v = S y */
+      acc_t s = 0.0L;
+      for (int64_t j = 0; j < n; ++j) s += S[k * n + j] * (acc_t)Z[j * m + c];
+      v[k] = s;
+    }
+    for (int64_t kk = 0; kk < n; ++kk) {          /* z(k) = <x_k, v> */
+      acc_t s = 0.0L;
+      for (int64_t k = 0; k < d; ++k) s += (acc_t)X[kk * d + k] * v[k];
+      Y[kk * m + c] = (double)s;
+    }
+  }
+  free(S);
+  free(v);
   return ORACLE_OK;
 }

@@ -28,7 +28,7 @@ STATUS = {
 EXPORTS = [
     "l1dm_prepare", "l1dm_prepare_ex", "l1dm_matvec", "l1dm_matvec_ex", "l1dm_matvec_pipelined",
     "l1dm_matvec_lp", "l1dm_matvec_lp_ex", "l1dm_tv_matvec", "l1dm_tv_matvec_ex",
-    "l1dm_lpp_even_matvec",
+    "l1dm_lpp_even_matvec", "l1dm_bilinear_matvec",
     "l1dm_free", "l1dm_sync",
     "l1dm_shape", "l1dm_workspace_bytes", "l1dm_set_workspace_limit", "l1dm_set_query_mode",
     "l1dm_plan", "l1dm_plan_ex", "l1dm_timing_enable", "l1dm_timing_read", "l1dm_debug_export", "l1dm_release_cached",
@@ -83,6 +83,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.l1dm_tv_matvec_ex.argtypes = [vp, vp, i64, i64, vp, i64, vp]
     lib.l1dm_tv_matvec.argtypes = [vp, vp, i64, vp]
     lib.l1dm_lpp_even_matvec.argtypes = [vp, i64, i64, i64, i32, vp, i64, i64, vp, i64, vp]
+    lib.l1dm_bilinear_matvec.argtypes = [vp, i64, i64, i64, vp, vp, i64, i64, vp, i64, vp]
     lib.l1dm_matvec_pipelined.argtypes = [vp, vp, i64, i64, vp, i64, vp, i64,
                                            ctypes.POINTER(vp)]
     lib.l1dm_free.argtypes = [vp]
@@ -107,6 +108,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     for name in ("l1dm_prepare", "l1dm_prepare_ex", "l1dm_matvec", "l1dm_matvec_ex",
                  "l1dm_matvec_pipelined", "l1dm_sync", "l1dm_matvec_lp", "l1dm_matvec_lp_ex",
                  "l1dm_tv_matvec", "l1dm_tv_matvec_ex", "l1dm_lpp_even_matvec",
+                 "l1dm_bilinear_matvec",
                  "l1dm_shape", "l1dm_set_workspace_limit", "l1dm_set_query_mode", "l1dm_plan", "l1dm_plan_ex",
                  "l1dm_timing_enable",
                  "l1dm_timing_read", "l1dm_debug_export"):
@@ -252,6 +254,36 @@ def l1dm_lpp_even_matvec(X, p: int, Z, Y=None, stream=None):
         rc = lib.l1dm_lpp_even_matvec(_ptr(X), n, X.stride(0), d, int(p), _ptr(Z), Z.stride(0), m,
                                       _ptr(Y), Y.stride(0), _stream_of(Z, stream))
     _check(rc, "l1dm_lpp_even_matvec")
+    return Y.view(-1) if squeeze else Y
+
+
+def l1dm_bilinear_matvec(X, M, Z, Y=None, stream=None):
+    """Thm. maha's bilinear form A_ij = x_i^T M x_j (M: d x d float64): Y = X M X^T Z."""
+    lib = load_library()
+    X = _as_f32_2d(X, "X")
+    squeeze = (Z.ndim == 1)
+    Z = _as_f32_2d(Z, "Z")
+    M = torch.as_tensor(M)
+    n, d = X.shape
+    if M.dtype != torch.float64 or tuple(M.shape) != (d, d):
+        raise ValueError("M must be a d x d float64 matrix")
+    M = M.contiguous()
+    if Z.shape[0] != n:
+        raise ValueError(f"Z has {Z.shape[0]} rows, X has {n}")
+    m = Z.shape[1]
+    if Y is None:
+        Y = torch.empty((n, m), dtype=torch.float64, device=Z.device)
+    if Y.dtype != torch.float64 or Y.shape != (n, m) or Y.stride(1) != 1:
+        raise ValueError("Y must be an n x m float64 row-major tensor")
+    dev = Z.device if Z.is_cuda else (X.device if X.is_cuda else None)
+    args = (_ptr(X), n, X.stride(0), d, _ptr(M), _ptr(Z), Z.stride(0), m, _ptr(Y), Y.stride(0),
+            _stream_of(Z, stream))
+    if dev is not None:
+        with torch.cuda.device(dev):
+            rc = lib.l1dm_bilinear_matvec(*args)
+    else:
+        rc = lib.l1dm_bilinear_matvec(*args)
+    _check(rc, "l1dm_bilinear_matvec")
     return Y.view(-1) if squeeze else Y
 
 

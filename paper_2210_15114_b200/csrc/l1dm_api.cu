@@ -939,16 +939,24 @@ l1dm_status l1dm_tv_matvec(l1dm_handle h, const float *Z, int64_t m, double *Y) 
   return query_entry(h, kQueryTV, 1, Z, m, m, Y, m, (void *)h->stream);
 }
 
-l1dm_status l1dm_lpp_even_matvec(const float *X, int64_t n, int64_t ld_x, int64_t d, int p,
-                                 const float *Z, int64_t ld_z, int64_t m, double *Y, int64_t ld_y,
-                                 void *stream) {
+}  // extern "C"
+
+namespace {
+
+// Shared by the handle-free sort-free entries: argument checks, host staging through the
+// stream-ordered allocator, the launch, the copy back.  M (bilinear only): d x d fp64.
+l1dm_status sortfree_entry(const float *X, int64_t n, int64_t ld_x, int64_t d, int p,
+                           const double *M, const float *Z, int64_t ld_z, int64_t m, double *Y,
+                           int64_t ld_y, void *stream) {
   g_err.clear();
-  if (!X || !Z || !Y) return fail(L1DM_EINVAL, "X, Z or Y is NULL");
+  const bool bilinear = (p == 0);
+  if (!X || !Z || !Y || (bilinear && !M)) return fail(L1DM_EINVAL, "X, M, Z or Y is NULL");
   if (n < 1 || d < 1 || m < 1 || ld_x < d || ld_z < m || ld_y < m)
     return fail(L1DM_EINVAL, "n=%lld d=%lld m=%lld ld_x=%lld ld_z=%lld ld_y=%lld invalid",
                 (long long)n, (long long)d, (long long)m, (long long)ld_x, (long long)ld_z,
                 (long long)ld_y);
-  if (p != 2 && p != 4 && p != 6) return fail(L1DM_EINVAL, "p=%d: even p in {2, 4, 6} only", p);
+  if (!bilinear && p != 2 && p != 4 && p != 6)
+    return fail(L1DM_EINVAL, "p=%d: even p in {2, 4, 6} only", p);
   int dev = 0;
   l1dm_status st = check_arch(&dev);
   if (st != L1DM_OK) return st;
@@ -956,17 +964,18 @@ l1dm_status l1dm_lpp_even_matvec(const float *X, int64_t n, int64_t ld_x, int64_
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   cudaStream_t s = (cudaStream_t)stream;
   const bool xdev = is_device_pointer(X), zdev = is_device_pointer(Z), ydev = is_device_pointer(Y);
+  const bool mdev = bilinear && is_device_pointer(M);
   // stream-ordered scratch (cudaMallocAsync): the call stays asynchronous for device buffers
-  const size_t wsb = lpp_even_workspace(n, d, m, p, nullptr, nullptr, sms);
-  void *ws = nullptr, *xs = nullptr, *zs = nullptr, *ys = nullptr;
+  const size_t wsb = bilinear ? bilinear_workspace(n, d, m, sms)
+                              : lpp_even_workspace(n, d, m, p, nullptr, nullptr, sms);
+  void *ws = nullptr, *xs = nullptr, *zs = nullptr, *ys = nullptr, *ms = nullptr;
   auto release = [&]() {
-    if (ws) cudaFreeAsync(ws, s);
-    if (xs) cudaFreeAsync(xs, s);
-    if (zs) cudaFreeAsync(zs, s);
-    if (ys) cudaFreeAsync(ys, s);
+    for (void *q : {ws, xs, zs, ys, ms})
+      if (q) cudaFreeAsync(q, s);
   };
   cudaError_t e = cudaMallocAsync(&ws, wsb, s);
   const float *Xd = X, *Zd = Z;
+  const double *Md = M;
   double *Yd = Y;
   int64_t ldxd = ld_x, ldzd = ld_z, ldyd = ld_y;
   if (e == cudaSuccess && !xdev) {
@@ -985,6 +994,12 @@ l1dm_status l1dm_lpp_even_matvec(const float *X, int64_t n, int64_t ld_x, int64_
     Zd = static_cast<const float *>(zs);
     ldzd = m;
   }
+  if (e == cudaSuccess && bilinear && !mdev) {
+    e = cudaMallocAsync(&ms, (size_t)d * d * sizeof(double), s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(ms, M, (size_t)d * d * sizeof(double), cudaMemcpyHostToDevice, s);
+    Md = static_cast<const double *>(ms);
+  }
   if (e == cudaSuccess && !ydev) {
     e = cudaMallocAsync(&ys, (size_t)n * m * sizeof(double), s);
     Yd = static_cast<double *>(ys);
@@ -993,18 +1008,39 @@ l1dm_status l1dm_lpp_even_matvec(const float *X, int64_t n, int64_t ld_x, int64_
   if (e != cudaSuccess) {
     release();
     cudaGetLastError();
-    return fail(e == cudaErrorMemoryAllocation ? L1DM_ENOMEM : L1DM_ECUDA, "lpp_even setup: %s",
+    return fail(e == cudaErrorMemoryAllocation ? L1DM_ENOMEM : L1DM_ECUDA, "sort-free setup: %s",
                 cudaGetErrorString(e));
   }
-  launch_lpp_even(Xd, ldxd, Zd, ldzd, n, d, m, p, Yd, ldyd, static_cast<double *>(ws), sms, s);
+  if (bilinear)
+    launch_bilinear(Xd, ldxd, Md, Zd, ldzd, n, d, m, Yd, ldyd, static_cast<double *>(ws), sms, s);
+  else
+    launch_lpp_even(Xd, ldxd, Zd, ldzd, n, d, m, p, Yd, ldyd, static_cast<double *>(ws), sms, s);
   e = cudaGetLastError();
   if (e == cudaSuccess && !ydev)
     e = cudaMemcpy2DAsync(Y, (size_t)ld_y * sizeof(double), Yd, (size_t)m * sizeof(double),
                           (size_t)m * sizeof(double), (size_t)n, cudaMemcpyDeviceToHost, s);
   release();
-  if (e == cudaSuccess && !(xdev && zdev && ydev)) e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) return fail(L1DM_ECUDA, "lpp_even: %s", cudaGetErrorString(e));
+  if (e == cudaSuccess && !(xdev && zdev && ydev && (!bilinear || mdev)))
+    e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return fail(L1DM_ECUDA, "sort-free query: %s", cudaGetErrorString(e));
   return L1DM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+l1dm_status l1dm_lpp_even_matvec(const float *X, int64_t n, int64_t ld_x, int64_t d, int p,
+                                 const float *Z, int64_t ld_z, int64_t m, double *Y, int64_t ld_y,
+                                 void *stream) {
+  if (p == 0) return fail(L1DM_EINVAL, "p=0: even p in {2, 4, 6} only");
+  return sortfree_entry(X, n, ld_x, d, p, nullptr, Z, ld_z, m, Y, ld_y, stream);
+}
+
+l1dm_status l1dm_bilinear_matvec(const float *X, int64_t n, int64_t ld_x, int64_t d,
+                                 const double *M, const float *Z, int64_t ld_z, int64_t m,
+                                 double *Y, int64_t ld_y, void *stream) {
+  return sortfree_entry(X, n, ld_x, d, 0, M, Z, ld_z, m, Y, ld_y, stream);
 }
 
 l1dm_status l1dm_matvec_pipelined(l1dm_handle h, const float *Z, int64_t ld_z, int64_t m,

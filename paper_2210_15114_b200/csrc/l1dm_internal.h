@@ -148,4 +148,10 @@ void launch_lpp_even(const float *X, int64_t ldx, const float *Z, int64_t ldz, i
                      int64_t d, int64_t m, int p, double *Y, int64_t ldy, double *ws, int sms,
                      cudaStream_t s);
 
+// Thm. maha's bilinear form f(x, y) = x^T M y (M: d x d fp64 row-major, device): Y = X M X^T Z.
+size_t bilinear_workspace(int64_t n, int64_t d, int64_t m, int sms);
+void launch_bilinear(const float *X, int64_t ldx, const double *M, const float *Z, int64_t ldz,
+                     int64_t n, int64_t d, int64_t m, double *Y, int64_t ldy, double *ws, int sms,
+                     cudaStream_t s);
+
 }  // namespace l1dm

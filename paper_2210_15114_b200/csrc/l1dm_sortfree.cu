@@ -215,7 +215,55 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// V[k][c] = sum_l M[k][l] W[l][c] (d x d times d x m; tiny next to the two contractions).
+__global__ void __launch_bounds__(256)
+    k15_small_gemm(const double *__restrict__ M, const double *__restrict__ W, int64_t d,
+                   int64_t m, double *__restrict__ V) {
+  for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < d * m;
+       e += (int64_t)gridDim.x * 256) {
+    const int64_t k = e / m, c = e - (e / m) * m;
+    double s = 0.0;
+    for (int64_t l = 0; l < d; ++l) s = fma(M[k * d + l], W[l * m + c], s);
+    V[e] = s;
+  }
+}
+
+__global__ void k15_zero(double *__restrict__ a, int64_t count) {
+  for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < count;
+       e += (int64_t)gridDim.x * 256)
+    a[e] = 0.0;
+}
+
 }  // namespace
+
+size_t bilinear_workspace(int64_t n, int64_t d, int64_t m, int sms) {
+  // lpp_even's layout at p = 1 (partials | W | S | G) + V (d x m)
+  return lpp_even_workspace(n, d, m, 1, nullptr, nullptr, sms) + (size_t)d * m * sizeof(double);
+}
+
+// Thm. maha: f(x, y) = x^T M y, A = X M X^T, Y = X (M (X^T Z)): Alg. 7's S = M X^T
+// is never formed; W = X^T Z (k12 at p = 1), V = M W (k15), Y = X V (k14 with S = G = 0).
+void launch_bilinear(const float *X, int64_t ldx, const double *M, const float *Z, int64_t ldz,
+                     int64_t n, int64_t d, int64_t m, double *Y, int64_t ldy, double *ws, int sms,
+                     cudaStream_t s) {
+  int64_t nchunks = 1, chunk = n;
+  lpp_even_workspace(n, d, m, 1, &nchunks, &chunk, sms);
+  double *part = ws;
+  double *W = part + (size_t)nchunks * d * m;
+  double *S = W + (size_t)d * m;
+  double *G = S + m;
+  double *V = G + m;
+  dim3 g12((unsigned)((d + kTile - 1) / kTile), (unsigned)((m + kTile - 1) / kTile),
+           (unsigned)nchunks);
+  k12_moment_reduce<<<g12, 256, 0, s>>>(X, ldx, Z, ldz, n, d, m, 1, chunk, nchunks, part);
+  int64_t b13 = (d * m + 255) / 256;
+  if (b13 > 148 * 8) b13 = 148 * 8;
+  k13_moment_fold<<<(unsigned)b13, 256, 0, s>>>(part, nchunks, d, m, 1, W, G);
+  k15_small_gemm<<<(unsigned)b13, 256, 0, s>>>(M, W, d, m, V);
+  k15_zero<<<1, 256, 0, s>>>(S, 2 * m);  // S and G (adjacent): no h S or G term
+  dim3 g14((unsigned)((n + kTile - 1) / kTile), (unsigned)((m + kTile - 1) / kTile));
+  k14_moment_expand<2><<<g14, 256, 0, s>>>(X, ldx, n, d, m, V, S, G, Y, ldy);
+}
 
 size_t lpp_even_workspace(int64_t n, int64_t d, int64_t m, int p, int64_t *nchunks_out,
                           int64_t *chunk_out, int sms) {

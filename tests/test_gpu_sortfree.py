@@ -60,3 +60,33 @@ def test_even_rejects_bad_p():
     for bad in (0, 1, 3, 8):
         with pytest.raises(l1.L1dmError):
             l1.l1dm_lpp_even_matvec(X, bad, Z)
+
+
+# ---- Thm. maha's bilinear form ----------------------------------------------------------
+def test_bilinear_golden_and_identity():
+    X = np.array([[1, 0], [0, 2]], dtype=np.float32)
+    M = np.array([[1, 2], [3, 4]], dtype=np.float64)
+    Y = l1.l1dm_bilinear_matvec(torch.from_numpy(X).cuda(), torch.from_numpy(M).cuda(),
+                                torch.ones((2, 1), device="cuda"))
+    torch.cuda.synchronize()
+    assert np.array_equal(Y.cpu().numpy()[:, 0], [5.0, 22.0])
+    rng = np.random.default_rng(4)
+    Xi = rng.integers(-4, 5, size=(3000, 70)).astype(np.float32)
+    Zi = rng.integers(-3, 4, size=(3000, 9)).astype(np.float32)
+    Mi = rng.integers(-2, 3, size=(70, 70)).astype(np.float64)
+    Yg = l1.l1dm_bilinear_matvec(Xi, Mi, Zi)              # host in, host out: exact integers
+    assert np.array_equal(Yg.numpy(), oracle.brute_bilinear(Xi, Mi, Zi))
+
+
+@pytest.mark.parametrize("n,d,m", [(1, 1, 1), (65, 63, 65), (2000, 130, 17)])
+def test_bilinear_random_vs_oracle(n, d, m):
+    rng = np.random.default_rng(n + d + m)
+    X = rng.standard_normal((n, d)).astype(np.float32)
+    Z = rng.standard_normal((n, m)).astype(np.float32)
+    M = rng.standard_normal((d, d))
+    Yg = l1.l1dm_bilinear_matvec(torch.from_numpy(X).cuda(), torch.from_numpy(M).cuda(),
+                                 torch.from_numpy(Z).cuda())
+    torch.cuda.synchronize()
+    Yr = oracle.brute_bilinear(X, M, Z)
+    scale = float(np.abs(X).sum(1).max() ** 2 * np.abs(M).max() * np.abs(Z).sum(0).max())
+    assert col_rel_l2(Yg.cpu().numpy(), Yr, floor=1e-6 * scale) <= 1e-9

@@ -158,3 +158,31 @@ def test_even_routes_agree_and_collinear(p):
     Zf = RNG.standard_normal((30, 2)).astype(np.float32)
     a, b = oracle.lp_even(Xf, Zf, p), oracle.brute_lp(Xf, Zf, p)
     assert np.abs(a - b).max() <= 1e-12 * np.abs(b).max()
+
+
+# ---- Thm. maha's bilinear form x^T M y (NEXT-4) -----------------------------------------
+def test_bilinear_golden_hand_derived():
+    """x1 = (1,0), x2 = (0,2), M = [[1,2],[3,4]] (not symmetric), z = (1,1):
+    A11 = M00 = 1, A12 = 2 M01 = 4, A21 = 2 M10 = 6, A22 = 4 M11 = 16 -> y = (5, 22)."""
+    X = np.array([[1, 0], [0, 2]], dtype=np.float32)
+    M = np.array([[1, 2], [3, 4]], dtype=np.float64)
+    Z = np.ones((2, 1), dtype=np.float32)
+    assert np.array_equal(oracle.brute_bilinear(X, M, Z)[:, 0], [5.0, 22.0])
+    assert np.array_equal(oracle.bilinear_alg(X, M, Z)[:, 0], [5.0, 22.0])
+
+
+def test_bilinear_identity_is_gram_and_zero_and_routes_agree():
+    X = RNG.integers(-4, 5, size=(30, 5))
+    Z = RNG.integers(-3, 4, size=(30, 2))
+    want = (X @ (X.T @ Z)).astype(np.float64)          # M = I: the Gram matvec (SPEC S:199)
+    Xf, Zf = X.astype(np.float32), Z.astype(np.float32)
+    assert np.array_equal(oracle.brute_bilinear(Xf, np.eye(5), Zf), want)
+    assert np.array_equal(oracle.bilinear_alg(Xf, np.eye(5), Zf), want)
+    assert np.all(oracle.brute_bilinear(Xf, np.zeros((5, 5)), Zf) == 0)
+    Mi = RNG.integers(-2, 3, size=(5, 5))              # integer M: X M X^T Z exactly (int64)
+    assert np.array_equal(oracle.brute_bilinear(Xf, Mi.astype(np.float64), Zf),
+                          (X @ Mi @ (X.T @ Z)).astype(np.float64))
+    Mf = RNG.standard_normal((5, 5))
+    Xr = RNG.standard_normal((30, 5)).astype(np.float32)
+    a, b = oracle.bilinear_alg(Xr, Mf, Zf), oracle.brute_bilinear(Xr, Mf, Zf)
+    assert np.abs(a - b).max() <= 1e-12 * np.abs(b).max()
