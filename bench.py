@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--p", type=int, default=1, choices=[1, 2, 3, 4, 5, 6, 7],
                     help="l_p^p query: odd p sort-based (NEXT-1), even p sort-free (NEXT-4); "
                          "1 = the l1 north star")
+    ap.add_argument("--krylov", type=int, default=0,
+                    help="K > 0: time block-Krylov top-K singular values of the workload's A "
+                         "(NEXT-2) instead of the query loop; block = m/2 fp64 columns")
     ap.add_argument("--mode", default="auto", choices=["auto", "gather", "scatter"],
                     help="query strategy (include/l1dm.h l1dm_set_query_mode)")
     ap.add_argument("--overlap-blocks", type=int, default=4,
@@ -445,6 +448,54 @@ def main_ours(args):
     return 0
 
 
+def main_krylov(args):
+    """NEXT-2 measurement: prepare once, then block Krylov for the top-K singular values, every
+    product through the library (1 GPU).  value = updates/s over the products (n d columns)."""
+    import paper_2210_15114_b200 as l1
+    from paper_2210_15114_b200 import workloads as wl
+    from paper_2210_15114_b200.krylov import block_krylov, fp64_product
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    w = wl.workload(args.workload)
+    n, d, m = w.n, w.d, w.m
+    X = wl.make_points(w, dev)
+    b = max(1, m // 2)
+    k = min(args.krylov, b)
+    times = []
+    for step in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        h = l1.l1dm_prepare(X)
+        if args.p == 1:
+            mv = lambda V: l1.l1dm_matvec(h, V)
+        else:
+            mv = lambda V: l1.l1dm_matvec_lp(h, args.p, V)
+        r = block_krylov(mv, n, k, block=b, seed=step, device=dev)
+        e1.record()
+        torch.cuda.synchronize()
+        if step >= args.warmup:
+            times.append(e0.elapsed_time(e1))
+        AZ = fp64_product(mv, r.Z)
+        res = (torch.linalg.norm(AZ - r.Z * r.lam[None, :], dim=0) / r.sigma).cpu().tolist()
+        l1.l1dm_free(h)
+    ms = statistics.mean(times)
+    upd = n * d * r.columns
+    print(json.dumps({
+        "metric": "block-Krylov top-k singular values of the l1 distance matrix (NEXT-2)",
+        "value": upd / (ms * 1e-3), "unit": "updates/s (n*d*columns through the products)",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "dtype": "f64 accumulation over f32 inputs (hi|lo split)",
+        "data": "synthetic", "config": {"workload": args.workload, "n": n, "d": d, "k": k,
+                                        "block": b, "products": r.products,
+                                        "columns": r.columns, "p": args.p},
+        "sigma_top": r.sigma[:min(k, 8)].cpu().tolist(), "ritz_residuals": res[:min(k, 8)],
+    }))
+    return 0
+
+
 if __name__ == "__main__":
     a = parse()
+    if a.krylov > 0 and a.impl == "ours":
+        sys.exit(main_krylov(a))
     sys.exit(run_reference(a) if a.impl == "reference" else main_ours(a))

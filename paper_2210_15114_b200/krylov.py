@@ -68,7 +68,7 @@ def _orth_block(V: torch.Tensor, basis: list[torch.Tensor], gen, rtol: float = 1
     have = sum(B.shape[1] for B in basis) + Q.shape[1]
     lost = min(b - Q.shape[1], n - have)
     if lost > 0:
-        R = torch.randn((n, lost), generator=gen, dtype=V.dtype).to(V.device)
+        R = torch.randn((n, lost), generator=gen, dtype=V.dtype, device=gen.device)
         R = _project_out(R, basis + [Q])
         Qr = _eig_orth(R, rtol * float(torch.linalg.norm(R, dim=0).max()))
         Q = torch.cat([Q, Qr], dim=1)
@@ -103,9 +103,11 @@ def block_krylov(matvec: MatVec, n: int, k: int, *, block: Optional[int] = None,
         raise ValueError(f"need 1 <= k < n (k={k}, n={n})")
     b = block or min(n, k + 8)
     q = depth or max(4, math.ceil(math.log(max(n, 2)) / math.sqrt(eps)))
-    gen = torch.Generator(device="cpu").manual_seed(seed)
-    Pi = start if start is not None else torch.randn((n, b), generator=gen, dtype=dtype)
-    Pi = Pi.to(device=device, dtype=dtype)
+    gdev = torch.device(device) if device is not None else torch.device("cpu")
+    gen = torch.Generator(device=gdev).manual_seed(seed)
+    Pi = start if start is not None else torch.randn((n, b), generator=gen, dtype=dtype,
+                                                     device=gdev)
+    Pi = Pi.to(device=gdev, dtype=dtype)
     products = columns = 0
 
     def apply(V: torch.Tensor) -> torch.Tensor:
@@ -141,8 +143,8 @@ def lowrank_error(matvec: MatVec, Z: torch.Tensor, probes: int = 16, seed: int =
     """Hutchinson estimate of ||A (I - Z Z^T)||_F^2 using `probes` Gaussian vectors (only
     products with A): E ||A (I - Z Z^T) g||^2 = ||A (I - Z Z^T)||_F^2."""
     n = Z.shape[0]
-    gen = torch.Generator(device="cpu").manual_seed(seed)
-    G = torch.randn((n, probes), generator=gen, dtype=Z.dtype).to(Z.device)
+    gen = torch.Generator(device=Z.device).manual_seed(seed)
+    G = torch.randn((n, probes), generator=gen, dtype=Z.dtype, device=Z.device)
     P = G - Z @ (Z.T @ G)
     AP = fp64_product(matvec, P)
     return float((AP * AP).sum() / probes)
