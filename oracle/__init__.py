@@ -54,11 +54,13 @@ def _load():
         lib.oracle_lp_even.argtypes = [vp, i64, i64, vp, i64, i32, vp, i32]
         lib.oracle_brute_bilinear.argtypes = [vp, i64, i64, vp, vp, i64, vp, i32]
         lib.oracle_bilinear_alg.argtypes = [vp, i64, i64, vp, vp, i64, vp]
+        lib.oracle_l2_embed.argtypes = [vp, i64, i64, vp, i64, vp]
+        lib.oracle_brute_l2.argtypes = [vp, i64, i64, vp, i64, vp, i32]
         for f in (lib.oracle_brute, lib.oracle_rows, lib.oracle_alg1, lib.oracle_alg2,
                   lib.oracle_alg2_range, lib.oracle_hist, lib.oracle_num_threads,
                   lib.oracle_brute_lp, lib.oracle_lp_sorted, lib.oracle_brute_tv,
                   lib.oracle_rows_lp, lib.oracle_lp_even, lib.oracle_brute_bilinear,
-                  lib.oracle_bilinear_alg):
+                  lib.oracle_bilinear_alg, lib.oracle_l2_embed, lib.oracle_brute_l2):
             f.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -242,4 +244,27 @@ def bilinear_alg(X, M, Z) -> np.ndarray:
     Y = np.empty((n, Z2.shape[1]), dtype=np.float64)
     _check(_load().oracle_bilinear_alg(_ptr(X), n, d, _ptr(M), _ptr(Z2), Z2.shape[1], _ptr(Y)),
            "bilinear_alg")
+    return Y
+
+
+def l2_embed(X, G) -> np.ndarray:
+    """Thm. l2embed: X' = X G^T / (beta k), beta = sqrt(2/pi), rounded to fp32."""
+    X = _f32(X)
+    G = _f32(G)
+    n, d = X.shape
+    k = G.shape[0]
+    assert G.shape[1] == d
+    Xp = np.empty((n, k), dtype=np.float32)
+    _check(_load().oracle_l2_embed(_ptr(X), n, d, _ptr(G), k, _ptr(Xp)), "l2_embed")
+    return Xp
+
+
+def brute_l2(X, Z, nthreads: int = 0) -> np.ndarray:
+    """The exact l2 distance product: Y[i,c] = sum_j Z[j,c] ||x_i - x_j||_2."""
+    X = _f32(X)
+    n, d = X.shape
+    Z2 = _as2d(Z, n)
+    Y = np.empty((n, Z2.shape[1]), dtype=np.float64)
+    _check(_load().oracle_brute_l2(_ptr(X), n, d, _ptr(Z2), Z2.shape[1], _ptr(Y), nthreads),
+           "brute_l2")
     return Y

@@ -31,6 +31,9 @@
  *   oracle_brute_bilinear — A_ij = x_i^T M x_j, the definition (Thm. maha)
  *   oracle_bilinear_alg   — Algs. 7-8 step by step: S = [M x_j]_j (d x n), v = S y,
  *                           z(k) = <x_k, v>
+ *   oracle_l2_embed   — Thm. l2embed: X'[i][r] = (1/(beta k)) sum_j G[r][j] x_ij,
+ *                       beta = sqrt(2/pi), rounded to fp32 (the l1 engine's input type)
+ *   oracle_brute_l2   — sum_j z_j ||x_i - x_j||_2, the exact l2 product (definition)
  *   oracle_lp_even    — even p, Alg. "query_p_even" step by step with the
  *                       corrections of SPEC S:140-146 (the text drops y_j and C(p,t) and
  *                       starts t at 1): S_{i,t} = C(p,t) (-1)^(p-t) sum_j y_j x_j(i)^(p-t),
@@ -627,5 +630,50 @@ int oracle_bilinear_alg(const float *X, int64_t n, int64_t d, const double *M, c
   }
   free(S);
   free(v);
+  return ORACLE_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* Thm. l2embed: T(x)_r = (1 / (beta k)) sum_j G_rj x_j, beta = sqrt(2/pi), long
+ * double, rounded to fp32.  G is k x d (the caller's N(0,1) draws).                          */
+/* ------------------------------------------------------------------ */
+int oracle_l2_embed(const float *X, int64_t n, int64_t d, const float *G, int64_t k, float *Xp) {
+  if (!X || !G || !Xp || n < 1 || d < 1 || k < 1) return ORACLE_EINVAL;
+  const acc_t beta = sqrtl(2.0L / 3.14159265358979323846264338327950288L);
+  const acc_t scale = 1.0L / (beta * (acc_t)k);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t r = 0; r < k; ++r) {
+      acc_t s = 0.0L;
+      for (int64_t j = 0; j < d; ++j) s += (acc_t)G[r * d + j] * (acc_t)X[i * d + j];
+      Xp[i * k + r] = (float)(double)(s * scale);
+    }
+  return ORACLE_OK;
+}
+
+/* The exact l2 distance product: Y[i][c] = sum_j Z[j][c] ||x_i - x_j||_2 (definition). */
+static void brute_l2_rows(void *pa, int64_t lo, int64_t hi) {
+  lp_args *a = (lp_args *)pa;
+  acc_t *acc = (acc_t *)malloc(sizeof(acc_t) * (size_t)a->m);
+  for (int64_t i = lo; i < hi; ++i) {
+    for (int64_t c = 0; c < a->m; ++c) acc[c] = 0.0L;
+    for (int64_t j = 0; j < a->n; ++j) {
+      acc_t s = 0.0L;
+      for (int64_t k = 0; k < a->d; ++k) {
+        acc_t t = (acc_t)a->X[i * a->d + k] - (acc_t)a->X[j * a->d + k];
+        s += t * t;
+      }
+      const acc_t dist = sqrtl(s);
+      for (int64_t c = 0; c < a->m; ++c) acc[c] += dist * (acc_t)a->Z[j * a->m + c];
+    }
+    for (int64_t c = 0; c < a->m; ++c) a->Y[i * a->m + c] = (double)acc[c];
+  }
+  free(acc);
+}
+
+int oracle_brute_l2(const float *X, int64_t n, int64_t d, const float *Z, int64_t m, double *Y,
+                    int nthreads) {
+  if (!X || !Z || !Y || n < 1 || d < 1 || m < 1) return ORACLE_EINVAL;
+  lp_args a = {X, n, d, Z, m, 2, 1.0, Y, NULL};
+  run_parallel(brute_l2_rows, &a, n, 4, nthreads);
   return ORACLE_OK;
 }

@@ -115,3 +115,10 @@ def make_query(w: Workload, trial: int = 0, device="cpu") -> torch.Tensor:
         b = torch.randint(0, 2, (n, m), generator=g, device=device, dtype=torch.int32)
         return b.to(torch.float32).mul_(2.0).sub_(1.0)
     raise ValueError(w.z_dist)
+
+
+def gaussian_embedding(k: int, d: int, seed: int, device="cpu") -> torch.Tensor:
+    """G: k x d fp32 of i.i.d. N(0,1) draws — the random matrix of Thm. l2embed,
+    passed to both the library (l1dm_l2_embed) and the oracle as an input (RNG only here)."""
+    return torch.randn((k, d), generator=_gen(device, 7_000_003 + seed), device=device,
+                       dtype=torch.float32)
