@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--krylov", type=int, default=0,
                     help="K > 0: time block-Krylov top-K singular values of the workload's A "
                          "(NEXT-2) instead of the query loop; block = m/2 fp64 columns")
+    ap.add_argument("--l2approx", type=float, default=0.0,
+                    help="EPS > 0: approximate l2 product through the l1 engine (NEXT-3): "
+                         "embed to k = 12 ln n / EPS^2 coordinates, prepare, run the queries")
     ap.add_argument("--mode", default="auto", choices=["auto", "gather", "scatter"],
                     help="query strategy (include/l1dm.h l1dm_set_query_mode)")
     ap.add_argument("--overlap-blocks", type=int, default=4,
@@ -494,8 +497,53 @@ def main_krylov(args):
     return 0
 
 
+def main_l2approx(args):
+    """NEXT-3 measurement (1 GPU): a step = embed (Thm. l2embed GEMM) + l1 prepare on the k
+    embedded coordinates + the workload's queries.  value = n k m queries / step time."""
+    import paper_2210_15114_b200 as l1
+    from paper_2210_15114_b200 import workloads as wl
+    from paper_2210_15114_b200.l2approx import L2Approx
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    w = wl.workload(args.workload)
+    Q = args.queries or w.queries
+    X = wl.make_points(w, dev)
+    Zs = [wl.make_query(w, t, dev) for t in range(Q if w.fresh_queries else 1)]
+    Y = torch.empty((w.n, w.m), dtype=torch.float64, device=dev)
+    times, embed_ms = [], []
+    k = None
+    for step in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record()
+        eng = L2Approx(X, eps=args.l2approx, seed=step)
+        e1.record()
+        for q in range(Q):
+            eng.matvec(Zs[q % len(Zs)], Y)
+        e2.record()
+        torch.cuda.synchronize()
+        k = eng.k
+        eng.close()
+        if step >= args.warmup:
+            times.append(e0.elapsed_time(e2))
+            embed_ms.append(e0.elapsed_time(e1))
+    ms = statistics.mean(times)
+    print(json.dumps({
+        "metric": "approximate l2 distance-matrix product via the l1 engine (NEXT-3)",
+        "value": w.n * k * w.m * Q / (ms * 1e-3), "unit": "updates/s (n*k*m on the embedding)",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "dtype": "f64 accumulation over f32 inputs", "data": "synthetic",
+        "config": {"workload": args.workload, "n": w.n, "d": w.d, "m": w.m, "eps": args.l2approx,
+                   "k": k, "queries_per_step": Q},
+        "embed_plus_prepare_ms": statistics.mean(embed_ms),
+        "query_ms": (ms - statistics.mean(embed_ms)) / Q}))
+    return 0
+
+
 if __name__ == "__main__":
     a = parse()
+    if a.l2approx > 0 and a.impl == "ours":
+        sys.exit(main_l2approx(a))
     if a.krylov > 0 and a.impl == "ours":
         sys.exit(main_krylov(a))
     sys.exit(run_reference(a) if a.impl == "reference" else main_ours(a))

@@ -167,6 +167,19 @@ L1DM_API l1dm_status l1dm_bilinear_matvec(const float *X, int64_t n, int64_t ld_
                                           const double *M, const float *Z, int64_t ld_z, int64_t m,
                                           double *Y, int64_t ld_y, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * Approximate l2 through the l1 engine (Thm. l2embed P:623-631,
+ * Algs. "Preprocessing" for l2 and Thm. l2_approx):
+ *   Xp[i][r] = (1 / (beta k)) sum_j G[r][j] X[i][j],   beta = sqrt(2/pi),   r < k,
+ * G a k x d matrix of i.i.d. N(0,1) draws supplied by the caller (the method's random numbers
+ * are an input, R22), fp64 accumulation rounded to fp32.  Then l1dm_prepare(Xp)
+ * and l1dm_matvec give B Z with B_ij = ||Xp_i - Xp_j||_1 = (1 +- eps) ||x_i - x_j||_2 w.h.p.
+ * for k = O(log n / eps^2).  Device pointers only (X: n x ld_x, G: k x d dense, Xp: n x ld_p);
+ * stream-ordered.  Errors: EINVAL (null, sizes, host pointers), EDEVICE, ECUDA. */
+L1DM_API l1dm_status l1dm_l2_embed(const float *X, int64_t n, int64_t ld_x, int64_t d,
+                                   const float *G, int64_t k, float *Xp, int64_t ld_p,
+                                   void *stream);
+
 /* Release every buffer the handle owns.  NULL is a no-op.  Synchronises the
  * handle's stream first. */
 L1DM_API void l1dm_free(l1dm_handle h);

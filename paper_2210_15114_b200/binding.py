@@ -28,7 +28,7 @@ STATUS = {
 EXPORTS = [
     "l1dm_prepare", "l1dm_prepare_ex", "l1dm_matvec", "l1dm_matvec_ex", "l1dm_matvec_pipelined",
     "l1dm_matvec_lp", "l1dm_matvec_lp_ex", "l1dm_tv_matvec", "l1dm_tv_matvec_ex",
-    "l1dm_lpp_even_matvec", "l1dm_bilinear_matvec",
+    "l1dm_lpp_even_matvec", "l1dm_bilinear_matvec", "l1dm_l2_embed",
     "l1dm_free", "l1dm_sync",
     "l1dm_shape", "l1dm_workspace_bytes", "l1dm_set_workspace_limit", "l1dm_set_query_mode",
     "l1dm_plan", "l1dm_plan_ex", "l1dm_timing_enable", "l1dm_timing_read", "l1dm_debug_export", "l1dm_release_cached",
@@ -84,6 +84,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.l1dm_tv_matvec.argtypes = [vp, vp, i64, vp]
     lib.l1dm_lpp_even_matvec.argtypes = [vp, i64, i64, i64, i32, vp, i64, i64, vp, i64, vp]
     lib.l1dm_bilinear_matvec.argtypes = [vp, i64, i64, i64, vp, vp, i64, i64, vp, i64, vp]
+    lib.l1dm_l2_embed.argtypes = [vp, i64, i64, i64, vp, i64, vp, i64, vp]
     lib.l1dm_matvec_pipelined.argtypes = [vp, vp, i64, i64, vp, i64, vp, i64,
                                            ctypes.POINTER(vp)]
     lib.l1dm_free.argtypes = [vp]
@@ -108,7 +109,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     for name in ("l1dm_prepare", "l1dm_prepare_ex", "l1dm_matvec", "l1dm_matvec_ex",
                  "l1dm_matvec_pipelined", "l1dm_sync", "l1dm_matvec_lp", "l1dm_matvec_lp_ex",
                  "l1dm_tv_matvec", "l1dm_tv_matvec_ex", "l1dm_lpp_even_matvec",
-                 "l1dm_bilinear_matvec",
+                 "l1dm_bilinear_matvec", "l1dm_l2_embed",
                  "l1dm_shape", "l1dm_set_workspace_limit", "l1dm_set_query_mode", "l1dm_plan", "l1dm_plan_ex",
                  "l1dm_timing_enable",
                  "l1dm_timing_read", "l1dm_debug_export"):
@@ -285,6 +286,24 @@ def l1dm_bilinear_matvec(X, M, Z, Y=None, stream=None):
         rc = lib.l1dm_bilinear_matvec(*args)
     _check(rc, "l1dm_bilinear_matvec")
     return Y.view(-1) if squeeze else Y
+
+
+def l1dm_l2_embed(X: torch.Tensor, G: torch.Tensor, out=None, stream=None) -> torch.Tensor:
+    """Thm. l2embed: X' = X G^T / (beta k) (n x k fp32), X and G CUDA fp32 tensors."""
+    lib = load_library()
+    X = _as_f32_2d(X, "X")
+    G = _as_f32_2d(G, "G").contiguous()
+    n, d = X.shape
+    k = G.shape[0]
+    if G.shape[1] != d or not (X.is_cuda and G.is_cuda):
+        raise ValueError("G must be k x d and X, G CUDA tensors")
+    if out is None:
+        out = torch.empty((n, k), dtype=torch.float32, device=X.device)
+    with torch.cuda.device(X.device):
+        rc = lib.l1dm_l2_embed(_ptr(X), n, X.stride(0), d, _ptr(G), k, _ptr(out), out.stride(0),
+                               _stream_of(X, stream))
+    _check(rc, "l1dm_l2_embed")
+    return out
 
 
 def point_blocks(n: int, nblocks: int):

@@ -1043,6 +1043,24 @@ l1dm_status l1dm_bilinear_matvec(const float *X, int64_t n, int64_t ld_x, int64_
   return sortfree_entry(X, n, ld_x, d, 0, M, Z, ld_z, m, Y, ld_y, stream);
 }
 
+l1dm_status l1dm_l2_embed(const float *X, int64_t n, int64_t ld_x, int64_t d, const float *G,
+                          int64_t k, float *Xp, int64_t ld_p, void *stream) {
+  g_err.clear();
+  if (!X || !G || !Xp) return fail(L1DM_EINVAL, "X, G or Xp is NULL");
+  if (n < 1 || d < 1 || k < 1 || ld_x < d || ld_p < k)
+    return fail(L1DM_EINVAL, "n=%lld d=%lld k=%lld ld_x=%lld ld_p=%lld invalid", (long long)n,
+                (long long)d, (long long)k, (long long)ld_x, (long long)ld_p);
+  int dev = 0;
+  l1dm_status st = check_arch(&dev);
+  if (st != L1DM_OK) return st;
+  if (!is_device_pointer(X) || !is_device_pointer(G) || !is_device_pointer(Xp))
+    return fail(L1DM_EINVAL, "l1dm_l2_embed needs device X, G and Xp");
+  cudaStream_t s = (cudaStream_t)stream;
+  launch_embed(X, ld_x, n, d, G, d, k, Xp, ld_p, s);
+  CUDA_TRY(cudaGetLastError());
+  return L1DM_OK;
+}
+
 l1dm_status l1dm_matvec_pipelined(l1dm_handle h, const float *Z, int64_t ld_z, int64_t m,
                                   double *Y, int64_t ld_y, void *stream, int64_t point_blocks,
                                   void *const *block_events) {

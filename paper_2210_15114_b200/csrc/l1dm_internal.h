@@ -154,4 +154,8 @@ void launch_bilinear(const float *X, int64_t ldx, const double *M, const float *
                      int64_t n, int64_t d, int64_t m, double *Y, int64_t ldy, double *ws, int sms,
                      cudaStream_t s);
 
+// Thm. l2embed: Xp (n x k fp32, ldp) = X G^T / (beta k), beta = sqrt(2/pi); G: k x d fp32.
+void launch_embed(const float *X, int64_t ldx, int64_t n, int64_t d, const float *G, int64_t ldg,
+                  int64_t k, float *Xp, int64_t ldp, cudaStream_t s);
+
 }  // namespace l1dm

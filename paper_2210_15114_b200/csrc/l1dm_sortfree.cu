@@ -234,7 +234,65 @@ __global__ void k15_zero(double *__restrict__ a, int64_t count) {
     a[e] = 0.0;
 }
 
+// Thm. l2embed: X'[i][r] = (1 / (beta k)) sum_j G[r][j] x_ij, beta = sqrt(2/pi),
+// fp64 accumulation rounded once to fp32 (the l1 engine's input type).  grid: (point tiles,
+// embedding-row tiles); block 16 x 16 threads, outputs (ty + 16u, tx + 16v).
+__global__ void __launch_bounds__(256)
+    k16_embed(const float *__restrict__ X, int64_t ldx, int64_t n, int64_t d,
+              const float *__restrict__ G, int64_t ldg, int64_t k, double scale,
+              float *__restrict__ Xp, int64_t ldp) {
+  __shared__ double xs[kStepK][kTile + 1];  // [coordinate][point]
+  __shared__ double gs[kStepK][kTile + 1];  // [coordinate][embedding row]
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t i0 = (int64_t)blockIdx.x * kTile, r0 = (int64_t)blockIdx.y * kTile;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int64_t jb = 0; jb < d; jb += kStepK) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < kTile * kStepK; e += 256) {
+      const int row = e / kStepK, q = e - (e / kStepK) * kStepK;
+      const int64_t j = jb + q;
+      xs[q][row] = (i0 + row < n && j < d) ? (double)X[(i0 + row) * ldx + j] : 0.0;
+      gs[q][row] = (r0 + row < k && j < d) ? (double)G[(r0 + row) * ldg + j] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kStepK; ++q) {
+      double a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a[u] = xs[q][ty + 16 * u];
+        b[u] = gs[q][tx + 16 * u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int64_t i = i0 + ty + 16 * u;
+    if (i >= n) continue;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int64_t r = r0 + tx + 16 * v;
+      if (r < k) Xp[i * ldp + r] = (float)(acc[u][v] * scale);
+    }
+  }
+}
+
 }  // namespace
+
+void launch_embed(const float *X, int64_t ldx, int64_t n, int64_t d, const float *G, int64_t ldg,
+                  int64_t k, float *Xp, int64_t ldp, cudaStream_t s) {
+  const double beta = 0.79788456080286535588;  // sqrt(2 / pi)
+  dim3 grid((unsigned)((n + kTile - 1) / kTile), (unsigned)((k + kTile - 1) / kTile));
+  k16_embed<<<grid, 256, 0, s>>>(X, ldx, n, d, G, ldg, k, 1.0 / (beta * (double)k), Xp, ldp);
+}
 
 size_t bilinear_workspace(int64_t n, int64_t d, int64_t m, int sms) {
   // lpp_even's layout at p = 1 (partials | W | S | G) + V (d x m)

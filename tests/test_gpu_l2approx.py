@@ -1,0 +1,45 @@
+"""Approximate l2 through the l1 engine on the GPU.  Parity: the library's
+embedding equals the oracle's (same G from workloads.gaussian_embedding; fp64 accumulation on
+both sides, one fp32 rounding: equal up to an fp32 ulp where the fp64 and long-double sums
+round differently); the full chain B Z against oracle.brute on the oracle's X' (1e-9, the l1
+bar); and the approximation quality against the exact l2 product (Thm. l2_approx)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2210_15114_b200 as l1
+from conftest import col_rel_l2
+from paper_2210_15114_b200.l2approx import L2Approx, embedding_dim
+from paper_2210_15114_b200.workloads import gaussian_embedding
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("n,d,k", [(1, 1, 1), (100, 7, 65), (3001, 130, 200)])
+def test_embedding_matches_oracle(n, d, k):
+    rng = np.random.default_rng(n + d + k)
+    X = rng.standard_normal((n, d)).astype(np.float32)
+    G = gaussian_embedding(k, d, seed=5, device="cuda")
+    Xp = l1.l1dm_l2_embed(torch.from_numpy(X).cuda(), G)
+    torch.cuda.synchronize()
+    want = oracle.l2_embed(X, G.cpu().numpy())
+    got = Xp.cpu().numpy()
+    ulp = np.spacing(np.abs(want).astype(np.float32))
+    assert np.all(np.abs(got - want) <= ulp)
+
+
+def test_chain_parity_and_approximation_quality():
+    rng = np.random.default_rng(9)
+    n, d, eps = 1500, 10, 0.2
+    X = rng.standard_normal((n, d)).astype(np.float32)
+    Z = rng.standard_normal((n, 3)).astype(np.float32)
+    eng = L2Approx(torch.from_numpy(X).cuda(), eps=eps, seed=3)
+    assert eng.k == embedding_dim(n, eps)
+    Yg = eng.matvec(torch.from_numpy(Z).cuda())
+    torch.cuda.synchronize()
+    Xp = oracle.l2_embed(X, eng.G.cpu().numpy())
+    assert col_rel_l2(Yg.cpu().numpy(), oracle.brute(Xp, Z)) <= 1e-6   # fp32-ulp X' differences
+    exact = oracle.brute_l2(X, Z)
+    assert col_rel_l2(Yg.cpu().numpy(), exact) <= eps                   # ||(A - B) z|| <= eps-ish
+    eng.close()
