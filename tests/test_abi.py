@@ -14,7 +14,7 @@ from conftest import ROOT
 def header_symbols():
     src = open(os.path.join(ROOT, "include", "l1dm.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(l1dm_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(l1dm_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_library_loads_and_exports_every_declared_symbol():
