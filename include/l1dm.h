@@ -15,7 +15,11 @@
  *
  * Pointers may be HOST or DEVICE memory unless a parameter says otherwise; the
  * library classifies each with cudaPointerGetAttributes.  Host buffers are
- * staged through library-owned device buffers and make the call synchronous.
+ * staged through library-owned device buffers.  Pageable host buffers make the call
+ * synchronous.  A query whose Z and Y are both PINNED host memory (cudaHostAlloc /
+ * cudaHostRegister) is asynchronous like a device-pointer call: its H2D and D2H copies run
+ * on the handle's copy streams through two staging slots, so consecutive queries overlap
+ * their copies with each other's compute; call l1dm_sync before reading Y or reusing Z.
  *
  * Layouts (all row-major, C order):
  *   X  n x ld_x  fp32  (point i at X + i*ld_x; coordinates k_begin..k_end-1 used)

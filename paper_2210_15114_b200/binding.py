@@ -189,7 +189,7 @@ def l1dm_prepare(X, k_begin: int = 0, k_end: int | None = None, stream=None) -> 
     return Handle(out, n, k_end - k_begin, k_begin, k_end, dev)
 
 
-def _query(entry: str, extra: tuple, h: Handle, Z, Y, stream):
+def _query(entry: str, extra: tuple, h: Handle, Z, Y, stream, block=True):
     lib = load_library()
     squeeze = (Z.ndim == 1)
     Z = _as_f32_2d(Z, "Z")
@@ -209,21 +209,26 @@ def _query(entry: str, extra: tuple, h: Handle, Z, Y, stream):
                     _stream_of(Z, stream))
     else:
         rc = fn(h.ptr, *extra, _ptr(Z), Z.stride(0), m, _ptr(Y), Y.stride(0), _stream_of(Z, stream))
+        _check(rc, entry.replace("_ex", ""))
+        if block:  # pinned host buffers run asynchronously in the library (include/l1dm.h)
+            l1dm_sync(h)
     _check(rc, entry.replace("_ex", ""))
     return Y.view(-1) if squeeze else Y
 
 
-def l1dm_matvec(h: Handle, Z, Y=None, stream=None):
+def l1dm_matvec(h: Handle, Z, Y=None, stream=None, block=True):
     """Alg. 2 for the m columns of Z: returns Y = A·Z (fp64, n x m).
 
     CUDA tensors: stream-ordered on `stream` (default: torch's current stream).
-    Host tensors / numpy arrays: synchronous, staged through device buffers."""
-    return _query("l1dm_matvec_ex", (), h, Z, Y, stream)
+    Host tensors / numpy arrays: staged through device buffers; synchronous unless Z and Y are
+    pinned and block=False (then the copies of consecutive calls overlap the compute, and the
+    caller runs l1dm_sync before reading Y)."""
+    return _query("l1dm_matvec_ex", (), h, Z, Y, stream, block)
 
 
-def l1dm_matvec_lp(h: Handle, p: int, Z, Y=None, stream=None):
+def l1dm_matvec_lp(h: Handle, p: int, Z, Y=None, stream=None, block=True):
     """l_p^p block product for odd p in {1, 3, 5, 7} (Thm. odd_p): sum_k |x_ik - x_jk|^p."""
-    return _query("l1dm_matvec_lp_ex", (int(p),), h, Z, Y, stream)
+    return _query("l1dm_matvec_lp_ex", (int(p),), h, Z, Y, stream, block)
 
 
 def l1dm_tv_matvec(h: Handle, Z, Y=None, stream=None):

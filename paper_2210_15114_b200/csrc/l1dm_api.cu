@@ -208,9 +208,16 @@ struct l1dm_ctx {
   int simplex = -1;           // TV precondition, checked once: -1 unknown, 0 violated, 1 holds
   double simplex_dev = 0.0, simplex_min = 0.0;
   uint32_t epoch = 1;
-  // host staging
+  // host staging (synchronous path: pageable host buffers)
   DevBuf<float> Zstage;
   DevBuf<double> Ystage;
+  // asynchronous pinned-host pipeline: two staging slots, H2D / D2H on their own streams so
+  // query q's copies overlap query q-1's compute (DESIGN.md §7 e2e)
+  DevBuf<float> Zpin[2];
+  DevBuf<double> Ypin[2];
+  cudaStream_t cp_in = nullptr, cp_out = nullptr;
+  cudaEvent_t ev_in[2] = {}, ev_done[2] = {}, ev_out[2] = {};
+  unsigned pin_slot = 0;
   // plan cache
   int64_t plan_m = -1;
   size_t plan_ws = 0;
@@ -310,8 +317,18 @@ void destroy(l1dm_ctx *h) {
   h->part.release();
   h->Sg.release();
   h->ctr.release();
+  if (h->cp_in) cudaStreamSynchronize(h->cp_in);
+  if (h->cp_out) cudaStreamSynchronize(h->cp_out);
   h->Zstage.release();
   h->Ystage.release();
+  for (int q = 0; q < 2; ++q) {
+    h->Zpin[q].release();
+    h->Ypin[q].release();
+    for (cudaEvent_t e : {h->ev_in[q], h->ev_done[q], h->ev_out[q]})
+      if (e) cudaEventDestroy(e);
+  }
+  if (h->cp_in) cudaStreamDestroy(h->cp_in);
+  if (h->cp_out) cudaStreamDestroy(h->cp_out);
   h->zs.release();
   h->zt.release();
   h->yt.release();
@@ -862,6 +879,62 @@ l1dm_status dispatch(l1dm_ctx *h, int kind, int lp, const float *Z, int64_t ldz,
   return st;
 }
 
+bool is_pinned_host(const void *ptr) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// Pinned host Z and Y: asynchronous, stream-ordered like device buffers (l1dm_sync before
+// reading Y or reusing Z).  Slot q&1: H2D of Z on cp_in (after the compute that last read the
+// slot), the query on the handle's stream, D2H of Y on cp_out; consecutive calls overlap.
+l1dm_status pinned_pipeline(l1dm_ctx *h, int kind, int lp, const float *Z, int64_t ld_z, int64_t m,
+                            double *Y, int64_t ld_y, cudaStream_t s) {
+  if (!h->cp_in) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&h->cp_in, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&h->cp_out, cudaStreamNonBlocking));
+    for (int q = 0; q < 2; ++q) {
+      CUDA_TRY(cudaEventCreateWithFlags(&h->ev_in[q], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&h->ev_done[q], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&h->ev_out[q], cudaEventDisableTiming));
+    }
+  }
+  const unsigned q = h->pin_slot++ & 1u;
+  if (h->Zpin[q].count < (size_t)h->n * m || h->Ypin[q].count < (size_t)h->n * m) {
+    // (re)allocation: drain every user of the slot first
+    CUDA_TRY(cudaStreamSynchronize(h->cp_in));
+    CUDA_TRY(cudaStreamSynchronize(h->cp_out));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    CUDA_TRY(h->Zpin[q].ensure((size_t)h->n * (size_t)m, false, s));
+    CUDA_TRY(h->Ypin[q].ensure((size_t)h->n * (size_t)m, false, s));
+  }
+  CUDA_TRY(cudaStreamWaitEvent(h->cp_in, h->ev_done[q], 0));  // slot's Z no longer read
+  {
+    TimedScope ts(h, kCopy, h->cp_in);
+    CUDA_TRY(cudaMemcpy2DAsync(h->Zpin[q].p, (size_t)m * sizeof(float), Z,
+                               (size_t)ld_z * sizeof(float), (size_t)m * sizeof(float),
+                               (size_t)h->n, cudaMemcpyHostToDevice, h->cp_in));
+  }
+  CUDA_TRY(cudaEventRecord(h->ev_in[q], h->cp_in));
+  CUDA_TRY(cudaStreamWaitEvent(s, h->ev_in[q], 0));
+  CUDA_TRY(cudaStreamWaitEvent(s, h->ev_out[q], 0));  // slot's Y copied out
+  l1dm_status st = dispatch(h, kind, lp, h->Zpin[q].p, m, m, h->Ypin[q].p, m, s);
+  if (st != L1DM_OK) return st;
+  CUDA_TRY(cudaEventRecord(h->ev_done[q], s));
+  CUDA_TRY(cudaStreamWaitEvent(h->cp_out, h->ev_done[q], 0));
+  {
+    TimedScope ts(h, kCopy, h->cp_out);
+    CUDA_TRY(cudaMemcpy2DAsync(Y, (size_t)ld_y * sizeof(double), h->Ypin[q].p,
+                               (size_t)m * sizeof(double), (size_t)m * sizeof(double),
+                               (size_t)h->n, cudaMemcpyDeviceToHost, h->cp_out));
+  }
+  CUDA_TRY(cudaEventRecord(h->ev_out[q], h->cp_out));
+  return L1DM_OK;
+}
+
 // Argument checks, host-buffer staging and the call: shared by the l1, l_p and TV entries.
 l1dm_status query_entry(l1dm_handle h, int kind, int lp, const float *Z, int64_t ld_z, int64_t m,
                         double *Y, int64_t ld_y, void *stream) {
@@ -879,7 +952,8 @@ l1dm_status query_entry(l1dm_handle h, int kind, int lp, const float *Z, int64_t
   h->last_stream = s;
   const bool zdev = is_device_pointer(Z), ydev = is_device_pointer(Y);
   if (zdev && ydev) return dispatch(h, kind, lp, Z, ld_z, m, Y, ld_y, s);
-  // host buffers: stage through library-owned device memory; synchronous
+  if (is_pinned_host(Z) && is_pinned_host(Y)) return pinned_pipeline(h, kind, lp, Z, ld_z, m, Y, ld_y, s);
+  // pageable host buffers: stage through library-owned device memory; synchronous
   const float *Zd = Z;
   int64_t ldzd = ld_z;
   if (!zdev) {
@@ -1089,6 +1163,8 @@ void l1dm_free(l1dm_handle h) { destroy(h); }
 l1dm_status l1dm_sync(l1dm_handle h) {
   g_err.clear();
   if (!h) return fail(L1DM_EINVAL, "handle is NULL");
+  if (h->cp_in) CUDA_TRY(cudaStreamSynchronize(h->cp_in));
+  if (h->cp_out) CUDA_TRY(cudaStreamSynchronize(h->cp_out));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   if (h->last_stream != h->stream) CUDA_TRY(cudaStreamSynchronize(h->last_stream));
   return read_timeout(h);

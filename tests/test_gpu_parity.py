@@ -261,3 +261,22 @@ def test_single_column_gather_mode_subprocess():
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_pinned_host_pipeline_async_queries():
+    """Pinned host Z and Y: asynchronous calls with overlapped copies; results after l1dm_sync
+    equal the oracle for every query (staging slots alternate, Y buffers distinct)."""
+    rng = np.random.default_rng(123)
+    X = rng.standard_normal((5000, 6)).astype(np.float32)
+    h = l1.l1dm_prepare(torch.from_numpy(X).cuda())
+    Zs = [torch.from_numpy(rng.standard_normal((5000, 7)).astype(np.float32)).pin_memory()
+          for _ in range(5)]
+    Ys = [torch.empty((5000, 7), dtype=torch.float64).pin_memory() for _ in range(5)]
+    for Z, Y in zip(Zs, Ys):
+        l1.l1dm_matvec(h, Z, Y, block=False)
+    l1.l1dm_sync(h)
+    for Z, Y in zip(Zs, Ys):
+        assert col_rel_l2(Y.numpy(), oracle.brute(X, Z.numpy())) <= TOL
+    Yb = l1.l1dm_matvec(h, Zs[0], torch.empty((5000, 7), dtype=torch.float64).pin_memory())
+    assert col_rel_l2(Yb.numpy(), oracle.brute(X, Zs[0].numpy())) <= TOL   # block=True default
+    l1.l1dm_free(h)
