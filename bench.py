@@ -367,9 +367,20 @@ def main_ours(args):
                 "alg_bytes_per_launch": (kern[dominant]["alg_bytes"] /
                                          max(kern[dominant]["launches"] or 1, 1)),
                 "frac_of_8TBps": (ach / 8000.0) if ach else None}
-        if plan["scatter"]:  # m == 1: L2-sector bound (random z gathers + reductions into Y)
-            roof["note"] = ("m = 1 scatter mode: L2-resident z and Y, DRAM fraction is not the "
-                            "bound (DESIGN.md §6)")
+        if plan["scatter"]:
+            # m == 1 scatter mode: z (4 MB) and Y (8 MB) live in L2; per (point, coordinate) the
+            # query makes two random 32-byte sector accesses (the z gather of the reduce pass and
+            # the fp64 reduction into Y of the apply pass) — bound by the L2's random-sector
+            # rate, measured by tools/l2_probe.cu (profiles/l2_peaks.json gather_sector_GBps)
+            sc = kern["scan"]
+            secs = agg.get("scan_pairs", 0) * 2 * 32
+            ach = secs / (sc["ms_total"] * 1e-3) / 1e9 if sc["ms_total"] else None
+            peak = l2p.get("gather_sector_GBps", 5712.0)
+            roof = {"bound": "l2_random_sectors", "kernel": "scan (k5_scan_m1 reduce/prefix/apply)",
+                    "achieved": ach, "peak": peak, "unit": "GB/s (32-B sectors)",
+                    "peak_kind": "measured (tools/l2_probe.cu -> profiles/l2_peaks.json)",
+                    "frac": (ach / peak) if ach else None,
+                    "note": "m = 1: L2-resident z and Y; HBM carries only the sorted tables"}
     traffic = None
     prof = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.workload}.json")
     if os.path.exists(prof) and args.p == 1:
