@@ -222,6 +222,8 @@ struct l1dm_ctx {
   int64_t plan_m = -1;
   size_t plan_ws = 0;
   int plan_vec_cap = 0;
+  size_t plan_ws_limit = 0;
+  int plan_mode = -1;
   QueryPlan plan{};
   // timing
   bool timing = false;
@@ -528,6 +530,11 @@ int vec_cap_for(const float *Z, int64_t ldz) {
 }
 
 l1dm_status ensure_plan(l1dm_ctx *h, int64_t m, int vec_cap) {
+  // a cached plan for this (m, alignment, limit) stands: the free-memory probe below
+  // (cudaMemGetInfo) costs host time on every query otherwise
+  if (h->plan_m == m && h->plan_vec_cap == vec_cap && h->plan_ws_limit == h->ws_limit &&
+      h->plan_mode == h->mode)
+    return L1DM_OK;
   size_t ws = h->ws_limit;
   if (ws == 0) {
     size_t fr = 0, tot = 0;
@@ -544,6 +551,8 @@ l1dm_status ensure_plan(l1dm_ctx *h, int64_t m, int vec_cap) {
   h->plan_m = m;
   h->plan_ws = ws;
   h->plan_vec_cap = vec_cap;
+  h->plan_ws_limit = h->ws_limit;
+  h->plan_mode = h->mode;
   return L1DM_OK;
 }
 
