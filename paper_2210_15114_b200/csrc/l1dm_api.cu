@@ -888,6 +888,14 @@ l1dm_status dispatch(l1dm_ctx *h, int kind, int lp, const float *Z, int64_t ldz,
   return st;
 }
 
+// 2-D copy of `rows` rows of `width` bytes; a contiguous block (pitches == width) goes as one
+// 1-D copy (the 2-D engine path moves narrow rows one by one: ~100x slower for m = 1).
+cudaError_t copy_rows(void *dst, size_t dpitch, const void *src, size_t spitch, size_t width,
+                      size_t rows, cudaMemcpyKind kind, cudaStream_t s) {
+  if (dpitch == width && spitch == width) return cudaMemcpyAsync(dst, src, width * rows, kind, s);
+  return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, kind, s);
+}
+
 bool is_pinned_host(const void *ptr) {
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
@@ -923,9 +931,8 @@ l1dm_status pinned_pipeline(l1dm_ctx *h, int kind, int lp, const float *Z, int64
   CUDA_TRY(cudaStreamWaitEvent(h->cp_in, h->ev_done[q], 0));  // slot's Z no longer read
   {
     TimedScope ts(h, kCopy, h->cp_in);
-    CUDA_TRY(cudaMemcpy2DAsync(h->Zpin[q].p, (size_t)m * sizeof(float), Z,
-                               (size_t)ld_z * sizeof(float), (size_t)m * sizeof(float),
-                               (size_t)h->n, cudaMemcpyHostToDevice, h->cp_in));
+    CUDA_TRY(copy_rows(h->Zpin[q].p, (size_t)m * sizeof(float), Z, (size_t)ld_z * sizeof(float),
+                       (size_t)m * sizeof(float), (size_t)h->n, cudaMemcpyHostToDevice, h->cp_in));
   }
   CUDA_TRY(cudaEventRecord(h->ev_in[q], h->cp_in));
   CUDA_TRY(cudaStreamWaitEvent(s, h->ev_in[q], 0));
@@ -936,9 +943,9 @@ l1dm_status pinned_pipeline(l1dm_ctx *h, int kind, int lp, const float *Z, int64
   CUDA_TRY(cudaStreamWaitEvent(h->cp_out, h->ev_done[q], 0));
   {
     TimedScope ts(h, kCopy, h->cp_out);
-    CUDA_TRY(cudaMemcpy2DAsync(Y, (size_t)ld_y * sizeof(double), h->Ypin[q].p,
-                               (size_t)m * sizeof(double), (size_t)m * sizeof(double),
-                               (size_t)h->n, cudaMemcpyDeviceToHost, h->cp_out));
+    CUDA_TRY(copy_rows(Y, (size_t)ld_y * sizeof(double), h->Ypin[q].p, (size_t)m * sizeof(double),
+                       (size_t)m * sizeof(double), (size_t)h->n, cudaMemcpyDeviceToHost,
+                       h->cp_out));
   }
   CUDA_TRY(cudaEventRecord(h->ev_out[q], h->cp_out));
   return L1DM_OK;
@@ -968,9 +975,8 @@ l1dm_status query_entry(l1dm_handle h, int kind, int lp, const float *Z, int64_t
   if (!zdev) {
     CUDA_TRY(h->Zstage.ensure((size_t)h->n * (size_t)m, false, s));
     TimedScope ts(h, kCopy, s);
-    CUDA_TRY(cudaMemcpy2DAsync(h->Zstage.p, (size_t)m * sizeof(float), Z,
-                               (size_t)ld_z * sizeof(float), (size_t)m * sizeof(float),
-                               (size_t)h->n, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(copy_rows(h->Zstage.p, (size_t)m * sizeof(float), Z, (size_t)ld_z * sizeof(float),
+                       (size_t)m * sizeof(float), (size_t)h->n, cudaMemcpyHostToDevice, s));
     Zd = h->Zstage.p;
     ldzd = m;
   }
@@ -985,9 +991,8 @@ l1dm_status query_entry(l1dm_handle h, int kind, int lp, const float *Z, int64_t
   if (st != L1DM_OK) return st;
   if (!ydev) {
     TimedScope ts(h, kCopy, s);
-    CUDA_TRY(cudaMemcpy2DAsync(Y, (size_t)ld_y * sizeof(double), Yd, (size_t)m * sizeof(double),
-                               (size_t)m * sizeof(double), (size_t)h->n, cudaMemcpyDeviceToHost,
-                               s));
+    CUDA_TRY(copy_rows(Y, (size_t)ld_y * sizeof(double), Yd, (size_t)m * sizeof(double),
+                       (size_t)m * sizeof(double), (size_t)h->n, cudaMemcpyDeviceToHost, s));
   }
   CUDA_TRY(cudaStreamSynchronize(s));
   return read_timeout(h);
@@ -1064,16 +1069,16 @@ l1dm_status sortfree_entry(const float *X, int64_t n, int64_t ld_x, int64_t d, i
   if (e == cudaSuccess && !xdev) {
     e = cudaMallocAsync(&xs, (size_t)n * d * sizeof(float), s);
     if (e == cudaSuccess)
-      e = cudaMemcpy2DAsync(xs, (size_t)d * sizeof(float), X, (size_t)ld_x * sizeof(float),
-                            (size_t)d * sizeof(float), (size_t)n, cudaMemcpyHostToDevice, s);
+      e = copy_rows(xs, (size_t)d * sizeof(float), X, (size_t)ld_x * sizeof(float),
+                    (size_t)d * sizeof(float), (size_t)n, cudaMemcpyHostToDevice, s);
     Xd = static_cast<const float *>(xs);
     ldxd = d;
   }
   if (e == cudaSuccess && !zdev) {
     e = cudaMallocAsync(&zs, (size_t)n * m * sizeof(float), s);
     if (e == cudaSuccess)
-      e = cudaMemcpy2DAsync(zs, (size_t)m * sizeof(float), Z, (size_t)ld_z * sizeof(float),
-                            (size_t)m * sizeof(float), (size_t)n, cudaMemcpyHostToDevice, s);
+      e = copy_rows(zs, (size_t)m * sizeof(float), Z, (size_t)ld_z * sizeof(float),
+                    (size_t)m * sizeof(float), (size_t)n, cudaMemcpyHostToDevice, s);
     Zd = static_cast<const float *>(zs);
     ldzd = m;
   }
@@ -1100,8 +1105,8 @@ l1dm_status sortfree_entry(const float *X, int64_t n, int64_t ld_x, int64_t d, i
     launch_lpp_even(Xd, ldxd, Zd, ldzd, n, d, m, p, Yd, ldyd, static_cast<double *>(ws), sms, s);
   e = cudaGetLastError();
   if (e == cudaSuccess && !ydev)
-    e = cudaMemcpy2DAsync(Y, (size_t)ld_y * sizeof(double), Yd, (size_t)m * sizeof(double),
-                          (size_t)m * sizeof(double), (size_t)n, cudaMemcpyDeviceToHost, s);
+    e = copy_rows(Y, (size_t)ld_y * sizeof(double), Yd, (size_t)m * sizeof(double),
+                  (size_t)m * sizeof(double), (size_t)n, cudaMemcpyDeviceToHost, s);
   release();
   if (e == cudaSuccess && !(xdev && zdev && ydev && (!bilinear || mdev)))
     e = cudaStreamSynchronize(s);
