@@ -632,12 +632,28 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
       h->kernel_launches++;
       h->launches[kColsums]++;
     }
+    // tile totals: one pass over full Z rows for every column block at once (m <= 256), else a
+    // reduce pass per block over its Zt block
+    static const bool reduce_all_env = [] {
+      const char *e = getenv("L1DM_REDUCE_ALL");
+      return e ? atoi(e) != 0 : true;
+    }();
+    bool all = false;
+    if (reduce_all_env && m <= 256) {
+      TimedScope ts(h, kScan, s);
+      CUDA_TRY(h->agg.ensure((size_t)h->dl * p.tiles_per_segment * 2 * m, false, s));
+      all = launch_reduce_all(h->perm.p, sval, h->ldn, h->n, Z, ldz, m, h->dl,
+                              p.tiles_per_segment, h->agg.p, h->part.p, s);
+      h->kernel_launches += 2;  // reduce-all, prefix
+      h->launches[kScan]++;
+      if (h->timing) h->scan_pairs += h->n * h->dl * p.col_blocks;
+    }
     for (int cb = 0; cb < p.col_blocks; ++cb) {
       const int64_t c0 = (int64_t)cb * p.mb;
       const int64_t mc = std::min<int64_t>(p.mb, m - c0);
       const bool last = cb == p.col_blocks - 1;
       const float *ztb = h->zt.p + (size_t)cb * h->n * p.mb;
-      {
+      if (!all) {
         TimedScope ts(h, kScan, s);
         launch_scan_seq(p, 1, h->perm.p, sval, h->ldn, h->n, ztb, mc, h->yt.p, p.mb, false,
                         h->dl, h->agg.p, h->part.p + 2 * c0, 2 * m, 0, s);
@@ -649,7 +665,8 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
         TimedScope ts(h, kAcc, s);
         CUDA_TRY(cudaMemsetAsync(h->yt.p, 0, (size_t)h->n * p.mb * sizeof(double), s));
         launch_scan_seq(p, 1, h->perm.p, sval, h->ldn, h->n, ztb, mc, h->yt.p, p.mb, false,
-                        h->dl, h->agg.p, h->part.p + 2 * c0, 2 * m, 1, s);
+                        h->dl, all ? h->agg.p + 2 * c0 : h->agg.p, h->part.p + 2 * c0, 2 * m, 1,
+                        s, all ? 2 * m : 0);
         h->kernel_launches++;  // apply
         h->launches[kAcc]++;
         if (h->timing) h->acc_pairs += h->n * h->dl;

@@ -120,7 +120,14 @@ void launch_scan(const QueryPlan &p, const uint32_t *perm, const float *sval, in
 void launch_scan_seq(const QueryPlan &p, int lp, const uint32_t *perm, const float *sval,
                      int64_t ldn, int64_t n, const float *zt, int64_t mc, double *out,
                      int64_t ldo, bool store, int64_t kcc, double *agg, double *segtot,
-                     int64_t ld_seg, int phase, cudaStream_t s);
+                     int64_t ld_seg, int phase, cudaStream_t s, int64_t agg_ld = 0);
+// (agg_ld: the apply's stride between tiles in agg, 0 = the block's own payload (lp+1) mb.)
+// P = 1, m <= 256: tile totals of all m columns in one pass over full Z rows + the prefix
+// (agg: kcc x tiles x 2m, segtot rows of 2m).  The per-block apply then reads agg + 2 c0 with
+// agg_ld = 2m.  Returns false (nothing launched) for m > 256.
+bool launch_reduce_all(const uint32_t *perm, const float *sval, int64_t ldn, int64_t n,
+                       const float *Z, int64_t ldz, int64_t m, int64_t kcc, int64_t tiles_per_seg,
+                       double *agg, double *segtot, cudaStream_t s);
 // Zt[cb][i][0..mb) = Z[i][cb*mb + ..] (zero-padded past m): the scatter mode's per-block Z.
 void launch_zt(const float *Z, int64_t ldz, int64_t n, int64_t m, int mb, float *zt,
                cudaStream_t s);

@@ -610,7 +610,7 @@ __global__ void __launch_bounds__(256)
     k5_scan_seq(const uint32_t *__restrict__ perm, const float *__restrict__ sval, int64_t ldn,
                 int64_t n, const float *__restrict__ zt, int64_t mc, double *__restrict__ out,
                 int64_t ldo, int64_t nseg, int64_t tiles_per_seg, double *__restrict__ agg,
-                const double *__restrict__ segtot, int64_t ld_seg) {
+                int64_t agg_ld, const double *__restrict__ segtot, int64_t ld_seg) {
   using C = SeqCfg<MB, P>;
   constexpr int NT = C::NT, NW = C::NW, ITEMS = C::ITEMS, R = C::R, GPW = C::GPW, GS = C::GS,
                 PS = C::PS, K = C::K, NP = C::NP, CH = C::CH, CPR = MB * 4 / CH;
@@ -691,7 +691,7 @@ __global__ void __launch_bounds__(256)
     for (int q = 0; q < K; ++q) s_wt[w * NP + K * c + q] = ps[q];
   }
   __syncthreads();
-  double *ag = agg + (kk * tiles_per_seg + tile) * NP;
+  double *ag = agg + (kk * tiles_per_seg + tile) * agg_ld;  // tile totals (REDUCE: agg_ld = NP)
   if constexpr (MODE == SEQ_REDUCE) {
     if (tid < NP) {
       double run = 0.0;
@@ -776,8 +776,8 @@ __global__ void __launch_bounds__(256)
 template <int MB, int P>
 static void launch_seq_t(const QueryPlan &p, const uint32_t *perm, const float *sval, int64_t ldn,
                          int64_t n, const float *zt, int64_t mc, double *out, int64_t ldo,
-                         bool store, int64_t kcc, double *agg, double *segtot, int64_t ld_seg,
-                         int phase, cudaStream_t s) {
+                         bool store, int64_t kcc, double *agg, int64_t agg_ld, double *segtot,
+                         int64_t ld_seg, int phase, cudaStream_t s) {
   using C = SeqCfg<MB, P>;
   static bool attr = false;
   if (!attr) {
@@ -792,7 +792,8 @@ static void launch_seq_t(const QueryPlan &p, const uint32_t *perm, const float *
   const int64_t total = kcc * p.tiles_per_segment;
   if (phase != 1) {
     k5_scan_seq<MB, SEQ_REDUCE, P><<<(unsigned)total, C::NT, C::SMEM, s>>>(
-        perm, sval, ldn, n, zt, mc, out, ldo, kcc, p.tiles_per_segment, agg, segtot, ld_seg);
+        perm, sval, ldn, n, zt, mc, out, ldo, kcc, p.tiles_per_segment, agg, C::NP, segtot,
+        ld_seg);
     const int64_t warps = kcc * C::NP;
     k5_seq_prefix<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(agg, kcc, p.tiles_per_segment,
                                                               C::NP, C::K * mc, segtot, ld_seg);
@@ -800,17 +801,18 @@ static void launch_seq_t(const QueryPlan &p, const uint32_t *perm, const float *
   if (phase != 0) {
     auto kern = store ? k5_scan_seq<MB, SEQ_APPLY_STORE, P> : k5_scan_seq<MB, SEQ_APPLY_RED, P>;
     kern<<<(unsigned)total, C::NT, C::SMEM, s>>>(perm, sval, ldn, n, zt, mc, out, ldo, kcc,
-                                                 p.tiles_per_segment, agg, segtot, ld_seg);
+                                                 p.tiles_per_segment, agg,
+                                                 agg_ld > 0 ? agg_ld : C::NP, segtot, ld_seg);
   }
 }
 
 void launch_scan_seq(const QueryPlan &p, int lp, const uint32_t *perm, const float *sval,
                      int64_t ldn, int64_t n, const float *zt, int64_t mc, double *out,
                      int64_t ldo, bool store, int64_t kcc, double *agg, double *segtot,
-                     int64_t ld_seg, int phase, cudaStream_t s) {
-#define L1DM_SEQ(MB, P)                                                                     \
-  launch_seq_t<MB, P>(p, perm, sval, ldn, n, zt, mc, out, ldo, store, kcc, agg, segtot, ld_seg, \
-                      phase, s)
+                     int64_t ld_seg, int phase, cudaStream_t s, int64_t agg_ld) {
+#define L1DM_SEQ(MB, P)                                                                         \
+  launch_seq_t<MB, P>(p, perm, sval, ldn, n, zt, mc, out, ldo, store, kcc, agg, agg_ld, segtot, \
+                      ld_seg, phase, s)
 #define L1DM_SEQ_P(MB)                         \
   switch (lp) {                                \
     case 1: L1DM_SEQ(MB, 1); break;            \
@@ -828,6 +830,116 @@ void launch_scan_seq(const QueryPlan &p, int lp, const uint32_t *perm, const flo
   }
 #undef L1DM_SEQ_P
 #undef L1DM_SEQ
+}
+
+// Tile totals of every column at once for the P = 1 scatter scan (one pass over the sorted
+// tables and the full Z rows, instead of one reduce pass per column block): per (segment,
+// 1024-row tile) and column c, (sum z, sum v z) -> agg[seg][tile][2c + {0,1}], the same layout
+// the per-block reduce writes with NP = 2m.  Each warp sums 128 consecutive sorted rows: the
+// row's perm/sval are warp-uniform loads, the Z row (m floats) is read with lanes over columns
+// (coalesced), so the gathers are whole Z rows from HBM (c3: 256 B) — the efficient width.
+template <int NCL>
+__global__ void __launch_bounds__(256)
+    k5_reduce_all(const uint32_t *__restrict__ perm, const float *__restrict__ sval, int64_t ldn,
+                  int64_t n, const float *__restrict__ Z, int64_t ldz, int64_t m, int64_t nseg,
+                  int64_t tiles_per_seg, double *__restrict__ agg) {
+  constexpr int R = 1024, NW = 8, RW = R / NW;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double *s_part = reinterpret_cast<double *>(smem_raw);  // [NW][2m]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t t = blockIdx.x;
+  const int64_t tile = t / nseg;
+  const int64_t kk = t - tile * nseg;
+  const int64_t r0 = tile * R + (int64_t)w * RW;
+  const int64_t r1 = (r0 + RW < n) ? r0 + RW : n;
+  const uint32_t *pp = perm + kk * ldn;
+  const float *vp = sval + kk * ldn;
+  double cs[NCL], ct[NCL];
+#pragma unroll
+  for (int j = 0; j < NCL; ++j) {
+    cs[j] = 0.0;
+    ct[j] = 0.0;
+  }
+  int64_t r = r0;
+  for (; r + 4 <= r1; r += 4) {  // 4 rows in flight per warp
+    uint32_t pr[4];
+    float vr[4], zr[4][NCL];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      pr[u] = __ldg(pp + r + u);
+      vr[u] = __ldg(vp + r + u);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int j = 0; j < NCL; ++j) {
+        const int64_t c = lane + 32 * j;
+        zr[u][j] = (c < m) ? __ldg(Z + (int64_t)pr[u] * ldz + c) : 0.0f;
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int j = 0; j < NCL; ++j) {
+        const double z = (double)zr[u][j];
+        cs[j] += z;
+        ct[j] = fma((double)vr[u], z, ct[j]);
+      }
+  }
+  for (; r < r1; ++r) {
+    const uint32_t pr = __ldg(pp + r);
+    const double v = (double)__ldg(vp + r);
+#pragma unroll
+    for (int j = 0; j < NCL; ++j) {
+      const int64_t c = lane + 32 * j;
+      const double z = (c < m) ? (double)__ldg(Z + (int64_t)pr * ldz + c) : 0.0;
+      cs[j] += z;
+      ct[j] = fma(v, z, ct[j]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NCL; ++j) {
+    const int64_t c = lane + 32 * j;
+    if (c < m) {
+      s_part[w * 2 * m + 2 * c] = cs[j];
+      s_part[w * 2 * m + 2 * c + 1] = ct[j];
+    }
+  }
+  __syncthreads();
+  double *ag = agg + (kk * tiles_per_seg + tile) * 2 * m;
+  for (int64_t e = threadIdx.x; e < 2 * m; e += 256) {
+    double a = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < NW; ++ww) a += s_part[ww * 2 * m + e];
+    ag[e] = a;
+  }
+}
+
+bool launch_reduce_all(const uint32_t *perm, const float *sval, int64_t ldn, int64_t n,
+                       const float *Z, int64_t ldz, int64_t m, int64_t kcc, int64_t tiles_per_seg,
+                       double *agg, double *segtot, cudaStream_t s) {
+  if (m > 256) return false;
+  const int64_t total = kcc * tiles_per_seg;
+  const size_t smem = (size_t)8 * 2 * m * sizeof(double);
+#define L1DM_RA(NCL)                                                                            \
+  {                                                                                             \
+    static bool attr = false;                                                                   \
+    if (!attr) {                                                                                \
+      cudaFuncSetAttribute(k5_reduce_all<NCL>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                           32768);                                                              \
+      attr = true;                                                                              \
+    }                                                                                           \
+    k5_reduce_all<NCL><<<(unsigned)total, 256, smem, s>>>(perm, sval, ldn, n, Z, ldz, m, kcc,   \
+                                                          tiles_per_seg, agg);                  \
+  }
+  if (m <= 32) L1DM_RA(1)
+  else if (m <= 64) L1DM_RA(2)
+  else if (m <= 128) L1DM_RA(4)
+  else L1DM_RA(8)
+#undef L1DM_RA
+  const int64_t warps = kcc * 2 * m;
+  k5_seq_prefix<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(agg, kcc, tiles_per_seg, (int)(2 * m),
+                                                            2 * m, segtot, 2 * m);
+  return true;
 }
 
 // Single-column variant (m == 1).  Here a tile is cheap (4 B of Z per row, gathered from
