@@ -391,9 +391,7 @@ __device__ __forceinline__ void lookback(int64_t slot0, int64_t tile, uint32_t *
   }
 }
 
-// SCATTER: instead of storing U in sorted order, add 2 U_r straight into Y[perm[r]] with L2
-// atomics (small-m mode: Y is L2-resident; no U round trip, no rank gather — DESIGN.md §6).
-template <int LPR, int VC, int CH, bool SCATTER>
+template <int LPR, int VC, int CH>
 __global__ void __launch_bounds__(256, 2)
     k5_scan(const uint32_t *__restrict__ perm, const float *__restrict__ sval, int64_t ldn,
             int64_t n, const float *__restrict__ Z, int64_t ldz, int64_t m,
@@ -525,7 +523,7 @@ __global__ void __launch_bounds__(256, 2)
     P[q] = s_excl[c2] + s_wt[w * NP + c2];
     Q[q] = s_excl[c2 + 1] + s_wt[w * NP + c2 + 1];
   }
-  double *ub = SCATTER ? U + col : U + kk * n * ldu + (row0 + rbase) * ldu + col;
+  double *ub = U + kk * n * ldu + (row0 + rbase) * ldu + col;
 #pragma unroll 4
   for (int j = 0; j < ITEMS; ++j) {
     const int r = rbase + j * RPW;
@@ -552,13 +550,7 @@ __global__ void __launch_bounds__(256, 2)
       Q[q] += __shfl_sync(0xFFFFFFFFu, b, (RPW - 1) * LPR + cl);
     }
     if (col_ok && r < nrows) {
-      if constexpr (SCATTER) {
-        double *yp = ub + (int64_t)pb[r] * ldu;
-#pragma unroll
-        for (int q = 0; q < VC; ++q) atomicAdd(yp + q, 2.0 * u[q]);
-      } else {
-        stcs_cols<VC>(ub + (int64_t)j * RPW * ldu, u);
-      }
+      stcs_cols<VC>(ub + (int64_t)j * RPW * ldu, u);
     }
   }
 }
@@ -1118,18 +1110,16 @@ __global__ void __launch_bounds__(256)
 }
 
 template <int LPR, int VC, int CH>
-static void launch_scan_t(const QueryPlan &p, bool scatter, const uint32_t *perm, const float *sval,
+static void launch_scan_t(const QueryPlan &p, const uint32_t *perm, const float *sval,
                           int64_t ldn, int64_t n, const float *Z, int64_t ldz, int64_t m,
                           double *U, int64_t k_first, int64_t kcc, uint32_t *flags, double *agg,
                           double *incl, uint32_t epoch, unsigned *ticket, unsigned *timeout_flag,
                           double *segtot, int64_t ld_seg, cudaStream_t s) {
   using C = ScanCfg<LPR, VC, scan_items(LPR, VC)>;
-  auto kern = scatter ? k5_scan<LPR, VC, CH, true> : k5_scan<LPR, VC, CH, false>;
+  auto kern = k5_scan<LPR, VC, CH>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k5_scan<LPR, VC, CH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)C::SMEM);
-    cudaFuncSetAttribute(k5_scan<LPR, VC, CH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k5_scan<LPR, VC, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)C::SMEM);
     attr = true;
   }
@@ -1147,7 +1137,7 @@ void launch_scan(const QueryPlan &p, const uint32_t *perm, const float *sval, in
                  unsigned *ticket, unsigned *timeout_flag, double *segtot, int64_t ld_seg,
                  float *zs, cudaStream_t s) {
 #define L1DM_SCAN(L, V, CH)                                                                    \
-  launch_scan_t<L, V, CH>(p, p.scatter != 0, perm, sval, ldn, n, Z, ldz, m, U, k_first, kcc, flags, \
+  launch_scan_t<L, V, CH>(p, perm, sval, ldn, n, Z, ldz, m, U, k_first, kcc, flags,              \
                           agg, incl, epoch, ticket, timeout_flag, segtot, ld_seg, s)
   // p.lpr lanes per row, p.mb / p.lpr columns per lane, p.vec floats per cp.async chunk
   if (p.mb == 1) {
