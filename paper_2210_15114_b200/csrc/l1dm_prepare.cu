@@ -9,7 +9,7 @@
 //   K0 keys      X (row-major) -> key[k][i] orderable u32, h[i] = sum_k x_ik (fp64),
 //                non-finite flag.  Tiled smem transpose, coalesced both sides.
 //   K1 hist      one read of the keys -> all four 8-bit digit histograms per segment.
-//   K2 pass      onesweep LSD pass: warp multisplit ranking (match.any), per-digit
+//   K2 pass      onesweep LSD pass: warp multisplit ranking (8 ballots), per-digit
 //                decoupled look-back across tiles (one 64-bit word per digit holds
 //                flag | epoch | count), smem staging so the scatter is run-coalesced.
 //                Passes whose digit is constant in every segment are skipped.
@@ -170,9 +170,17 @@ __global__ void __launch_bounds__(kSortThreads)
     const int64_t idx = wbase + j * 32 + lane;
     const bool valid = idx < n;
     const uint32_t vmask = __ballot_sync(0xFFFFFFFFu, valid);
+    // lanes holding the same digit: 8 ballots (one per digit bit) — MATCH.ANY's latency made
+    // it the top stall of this kernel on sm_100a (ncu short_scoreboard)
+    const uint32_t dgt = (keys[j] >> shift) & 255u;
+    uint32_t peers = vmask;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const uint32_t bit = (dgt >> b) & 1u;
+      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, bit);
+      peers &= bit ? bal : ~bal;
+    }
     if (valid) {
-      const uint32_t dgt = (keys[j] >> shift) & 255u;
-      const uint32_t peers = __match_any_sync(vmask, dgt);
       const int leader = __ffs(peers) - 1;
       uint32_t old = 0;
       if (lane == leader) {
