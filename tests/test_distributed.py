@@ -95,3 +95,45 @@ def test_two_rank_gloo_reduce_and_allreduce(d):
         assert np.array_equal(p0, oracle.hist(X[:, a0:b0], Z, M=6).astype(np.float64))
     else:
         assert np.all(p0 == 0)                        # more ranks than coordinates
+
+
+def lp_worker(rank, world, port, p, results):
+    """Odd-p l_p^p (NEXT-1) and even-p (NEXT-4) share the coordinate sharding: A = sum_k A^(k)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(7)
+        X = torch.from_numpy(rng.integers(0, 5, size=(200, 5)).astype(np.float32))
+        Z = torch.from_numpy(rng.integers(-2, 3, size=(200, 3)).astype(np.float32))
+
+        def prep(X_, k0, k1, stream=None):
+            return X_[:, k0:k1].contiguous().numpy()
+
+        def mv(h, Z_, Y=None, stream=None):
+            return torch.from_numpy(oracle.lp_sorted(h, Z_.numpy(), p) if p % 2
+                                    else oracle.lp_even(h, Z_.numpy(), p))
+
+        sh = ShardedL1DM(X, local_prepare=prep, local_matvec=mv, p=p)
+        results[rank] = sh.matvec(Z.clone(), root=None).numpy().copy()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("p", [3, 2])
+def test_two_rank_gloo_lp(p):
+    ctx = mp.get_context("spawn")
+    results = ctx.Manager().dict()
+    port = free_port()
+    ctx_procs = [ctx.Process(target=lp_worker, args=(r, 2, port, p, results)) for r in range(2)]
+    for pr in ctx_procs:
+        pr.start()
+    for pr in ctx_procs:
+        pr.join(120)
+        assert pr.exitcode == 0
+    rng = np.random.default_rng(7)
+    X = rng.integers(0, 5, size=(200, 5)).astype(np.float32)
+    Z = rng.integers(-2, 3, size=(200, 3)).astype(np.float32)
+    want = oracle.brute_lp(X, Z, p)
+    for r in range(2):
+        assert np.array_equal(results[r], want)
