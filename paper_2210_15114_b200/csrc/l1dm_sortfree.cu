@@ -7,8 +7,8 @@
 //        = S_c hp_i + sum_{t=1}^{p-1} c_t (X^(p-t) W_t)_ic + G_c,
 //   S_c = sum_j z_jc,  hp_i = sum_k x_ik^p,  G_c = sum_k W_p[k][c]  (c_0 = c_p = 1 for even p).
 //
-// Two dense contractions, both fp64 FMAs on the CUDA cores (fp32 inputs, fp64 products and
-// sums; tensor-core formats below fp64 cannot hold the 1e-9 bar — DESIGN.md §6b):
+// Two dense contractions on the fp64 tensor cores (DMMA, mma.sync m8n8k4 f64: fp32 inputs,
+// fp64 products and sums; the tcgen05 kinds below fp64 cannot hold the 1e-9 bar):
 //   K12 moment reduce  W_t = (X^t)^T Z for t = 1..p, split over point chunks; each CTA owns a
 //                      64 x 64 (coordinate, column) tile of one power and a chunk of points,
 //                      staging X and Z sub-tiles in shared memory; partials per chunk
@@ -28,7 +28,6 @@ namespace l1dm {
 namespace {
 
 constexpr int kTile = 64;    // output tile (rows x columns) of K12 and K14
-constexpr int kStepN = 16;   // points per shared-memory step of K12
 constexpr int kStepK = 16;   // coordinates per shared-memory step of K14
 
 __device__ __forceinline__ double powi(double x, int t) {
@@ -37,62 +36,199 @@ __device__ __forceinline__ double powi(double x, int t) {
   return r;
 }
 
-// grid: (k tiles, c tiles, p * chunks); block 16 x 16 threads, outputs (ty + 16u, tx + 16v).
+// ---- fp64 tensor-core (DMMA, mma.sync m8n8k4 f64) versions of K12 / K14 -----------------
+// mma.sync.aligned.m8n8k4.row.col.f64: lane l holds A[l/4][l%4], B[l%4][l/4] and
+// D[l/4][2(l%4) + {0,1}].  One DMMA = 256 fp64 FMAs; measured 37.2 TFLOP/s on this B200
+// (tools/fp64_probe.cu) vs 34.2 for CUDA-core DFMA, and 8x fewer issue slots per FMA.
+__device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+constexpr int kDmmaKs = 32;          // points per shared-memory stage of K12
+constexpr int kDmmaPad = kTile + 8;  // padded row length (doubles): two wavefronts per fragment
+
+// K12 on DMMA: grid (k tiles, c tiles, p * chunks), 8 warps; warp w owns coordinate rows
+// 16 (w % 4) .. +16 (two 8-row groups) x columns 32 (w / 4) .. +32 (four 8-column tiles).
 __global__ void __launch_bounds__(256)
-    k12_moment_reduce(const float *__restrict__ X, int64_t ldx, const float *__restrict__ Z,
-                      int64_t ldz, int64_t n, int64_t d, int64_t m, int p, int64_t chunk,
-                      int64_t nchunks, double *__restrict__ part) {
-  // operands staged as fp64, x already raised to the CTA's power t: converted once per element
-  // (not once per use), so the inner loop is 8 shared loads and 16 FMAs per point
-  __shared__ double xs[kStepN][kTile];
-  __shared__ double zs[kStepN][kTile];
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    k12_moment_reduce_dmma(const float *__restrict__ X, int64_t ldx, const float *__restrict__ Z,
+                           int64_t ldz, int64_t n, int64_t d, int64_t m, int p, int64_t chunk,
+                           double *__restrict__ part) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double *xs = reinterpret_cast<double *>(smem_raw);  // [kDmmaKs][kDmmaPad]  x^t
+  double *zs = xs + kDmmaKs * kDmmaPad;                // [kDmmaKs][kDmmaPad]
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t k0 = (int64_t)blockIdx.x * kTile, c0 = (int64_t)blockIdx.y * kTile;
   const int t = 1 + (int)(blockIdx.z % p);
   const int64_t ch = blockIdx.z / p;
   const int64_t i0 = ch * chunk, i1 = (i0 + chunk < n) ? i0 + chunk : n;
-  double acc[4][4];
+  const int rw = 16 * (w % 4), cw = 32 * (w / 4);
+  double acc[2][4][2];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < 2; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-  for (int64_t base = i0; base < i1; base += kStepN) {
-    __syncthreads();
-    for (int e = threadIdx.x; e < kStepN * kTile; e += 256) {  // coalesced row pieces
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  // register double buffering: stage s+1's global loads are in flight while stage s computes
+  constexpr int PER = kDmmaKs * kTile / 256;  // elements of X and of Z per thread per stage
+  float xr[PER], zr[PER];
+  auto load = [&](int64_t base) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = tid + 256 * u;
       const int r = e / kTile, q = e - (e / kTile) * kTile;
       const int64_t i = base + r;
-      const float xv = (i < i1 && k0 + q < d) ? __ldcs(X + i * ldx + k0 + q) : 0.0f;
-      xs[r][q] = powi((double)xv, t);
-      zs[r][q] = (i < i1 && c0 + q < m) ? (double)__ldcs(Z + i * ldz + c0 + q) : 0.0;
+      xr[u] = (i < i1 && k0 + q < d) ? __ldcs(X + i * ldx + k0 + q) : 0.0f;
+      zr[u] = (i < i1 && c0 + q < m) ? __ldcs(Z + i * ldz + c0 + q) : 0.0f;
+    }
+  };
+  if (i0 < i1) load(i0);
+  for (int64_t base = i0; base < i1; base += kDmmaKs) {
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = tid + 256 * u;
+      const int r = e / kTile, q = e - (e / kTile) * kTile;
+      xs[r * kDmmaPad + q] = powi((double)xr[u], t);
+      zs[r * kDmmaPad + q] = (double)zr[u];
     }
     __syncthreads();
-#pragma unroll 4
-    for (int r = 0; r < kStepN; ++r) {
-      double a[4], b[4];
+    if (base + kDmmaKs < i1) load(base + kDmmaKs);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {  // rows ty + 16 q, columns tx + 16 q: conflict-free
-        a[q] = xs[r][ty + 16 * q];
-        b[q] = zs[r][tx + 16 * q];
-      }
+    for (int kk = 0; kk < kDmmaKs / 4; ++kk) {
+      const int pt = 4 * kk + (lane & 3);
+      double a[2], b[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int g = 0; g < 2; ++g) a[g] = xs[pt * kDmmaPad + rw + 8 * g + (lane >> 2)];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+      for (int j = 0; j < 4; ++j) b[j] = zs[pt * kDmmaPad + cw + 8 * j + (lane >> 2)];
+#pragma unroll
+      for (int g = 0; g < 2; ++g)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc[g][j][0], acc[g][j][1], a[g], b[j]);
     }
   }
-  // part[ch][t-1][k][c]
   double *out = part + ((ch * p + (t - 1)) * d) * m;
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int64_t k = k0 + ty + 16 * u;
+  for (int g = 0; g < 2; ++g) {
+    const int64_t k = k0 + rw + 8 * g + (lane >> 2);
     if (k >= d) continue;
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const int64_t c = c0 + tx + 16 * v;
-      if (c < m) out[k * m + c] = acc[u][v];
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t c = c0 + cw + 8 * j + 2 * (lane & 3) + h;
+        if (c < m) out[k * m + c] = acc[g][j][h];
+      }
+  }
+}
+
+// K14 on DMMA: grid (point tiles, column tiles), 8 warps; warp w owns points 16 (w % 4) .. +16
+// x columns 32 (w / 4) .. +32.  K = (P-1) d: for t = 1..P-1 the A operand is x^(P-t) (staged in
+// shared memory as fp64), B = c_t W_t.  hp_i = sum_k x_ik^P accumulates while staging.
+template <int P>
+__global__ void __launch_bounds__(256)
+    k14_moment_expand_dmma(const float *__restrict__ X, int64_t ldx, int64_t n, int64_t d,
+                           int64_t m, const double *__restrict__ Wc,
+                           const double *__restrict__ S, const double *__restrict__ G,
+                           double *__restrict__ Y, int64_t ldy) {
+  constexpr int KS = kStepK, XP = KS + 2, WP = kDmmaPad;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double *xp = reinterpret_cast<double *>(smem_raw);  // [P-1][kTile][XP]  slot t: x^(P-1-t)...
+  double *ws = xp + (P - 1) * kTile * XP;               // [P-1][KS][WP]    c_t W_t
+  __shared__ double s_hp[kTile];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t i0 = (int64_t)blockIdx.x * kTile, c0 = (int64_t)blockIdx.y * kTile;
+  const int rw = 16 * (w % 4), cw = 32 * (w / 4);
+  double acc[2][4][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  double hp = 0.0;  // threads 0..kTile-1: point i0 + tid
+  // register double buffering of the next k step's X and c_t W_t
+  constexpr int PX = kTile * KS / 256, PW = (P - 1) * KS * kTile / 256;
+  float xr[PX];
+  double wr[PW];
+  auto load = [&](int64_t kb) {
+#pragma unroll
+    for (int u = 0; u < PX; ++u) {
+      const int e = tid + 256 * u;
+      const int r = e / KS, q = e - (e / KS) * KS;
+      const int64_t i = i0 + r, k = kb + q;
+      xr[u] = (i < n && k < d) ? X[i * ldx + k] : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < PW; ++u) {
+      const int e = tid + 256 * u;
+      const int tt = e / (KS * kTile), rem = e - tt * (KS * kTile);
+      const int q = rem / kTile, cc = rem - (rem / kTile) * kTile;
+      const int64_t k = kb + q, c = c0 + cc;
+      wr[u] = (k < d && c < m) ? Wc[((int64_t)tt * d + k) * m + c] : 0.0;
+    }
+  };
+  load(0);
+  for (int64_t kb = 0; kb < d; kb += KS) {
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < PX; ++u) {
+      const int e = tid + 256 * u;
+      const int r = e / KS, q = e - (e / KS) * KS;
+      const double x = (double)xr[u];
+      double pw = x;  // slot tt (t = tt + 1) holds x^(P-t) = x^(P-1-tt)
+#pragma unroll
+      for (int e2 = 1; e2 < P; ++e2) {
+        xp[((P - 1 - e2) * kTile + r) * XP + q] = pw;
+        pw *= x;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < PW; ++u) {
+      const int e = tid + 256 * u;
+      const int tt = e / (KS * kTile), rem = e - tt * (KS * kTile);
+      const int q = rem / kTile, cc = rem - (rem / kTile) * kTile;
+      ws[(tt * KS + q) * WP + cc] = wr[u];
+    }
+    __syncthreads();
+    if (kb + KS < d) load(kb + KS);
+    if (tid < kTile) {  // x^P = x^(P-1) (slot 0) * x (slot P-2)
+#pragma unroll 4
+      for (int q = 0; q < KS; ++q)
+        hp = fma(xp[tid * XP + q], xp[((P - 2) * kTile + tid) * XP + q], hp);
+    }
+#pragma unroll
+    for (int tt = 0; tt < P - 1; ++tt) {
+#pragma unroll
+      for (int kk = 0; kk < KS / 4; ++kk) {
+        const int kq = 4 * kk + (lane & 3);
+        double a[2], b[4];
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+          a[g] = xp[(tt * kTile + rw + 8 * g + (lane >> 2)) * XP + kq];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = ws[(tt * KS + kq) * WP + cw + 8 * j + (lane >> 2)];
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma884(acc[g][j][0], acc[g][j][1], a[g], b[j]);
+      }
     }
   }
-  (void)nchunks;
+  if (tid < kTile) s_hp[tid] = hp;
+  __syncthreads();
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+    const int r = rw + 8 * g + (lane >> 2);
+    const int64_t i = i0 + r;
+    if (i >= n) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t c = c0 + cw + 8 * j + 2 * (lane & 3) + h;
+        if (c < m) Y[i * ldy + c] = fma(S[c], s_hp[r], acc[g][j][h] + G[c]);
+      }
+  }
 }
 
 // W[t][k][c] = c_t * sum_ch part[ch][t][k][c]  (t = 1..p-1, scaled for the expand), plus
@@ -140,78 +276,6 @@ __global__ void __launch_bounds__(256)
   if (threadIdx.x == 0) {
     S[c] = rs[0];
     G[c] = rg[0];
-  }
-}
-
-// grid: (point tiles, column tiles); block 16 x 16 threads, 4 points x 4 columns each.
-// Y[i][c] = S_c hp_i + G_c + sum_{t=1}^{p-1} sum_k x_ik^(p-t) Wc[t][k][c]  (Wc pre-scaled by c_t)
-template <int P>
-__global__ void __launch_bounds__(256)
-    k14_moment_expand(const float *__restrict__ X, int64_t ldx, int64_t n, int64_t d, int64_t m,
-                      const double *__restrict__ Wc, const double *__restrict__ S,
-                      const double *__restrict__ G, double *__restrict__ Y, int64_t ldy) {
-  constexpr int p = P;
-  __shared__ float xs[kTile][kStepK + 1];
-  __shared__ double ws[P - 1][kStepK][kTile];  // c_t W_t, t = 1..p-1
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const int64_t i0 = (int64_t)blockIdx.x * kTile, c0 = (int64_t)blockIdx.y * kTile;
-  double acc[4][4], hp[4];
-#pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    hp[a] = 0.0;
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-  }
-  for (int64_t kb = 0; kb < d; kb += kStepK) {
-    __syncthreads();
-    for (int e = threadIdx.x; e < kTile * kStepK; e += 256) {
-      const int r = e / kStepK, q = e - (e / kStepK) * kStepK;
-      const int64_t i = i0 + r, k = kb + q;
-      xs[r][q] = (i < n && k < d) ? X[i * ldx + k] : 0.0f;
-    }
-    for (int e = threadIdx.x; e < (p - 1) * kStepK * kTile; e += 256) {
-      const int tt = e / (kStepK * kTile), rem = e - tt * (kStepK * kTile);
-      const int q = rem / kTile, cc = rem - (rem / kTile) * kTile;
-      const int64_t k = kb + q, c = c0 + cc;
-      ws[tt][q][cc] = (k < d && c < m) ? Wc[((int64_t)tt * d + k) * m + c] : 0.0;
-    }
-    __syncthreads();
-    for (int q = 0; q < kStepK; ++q) {
-      double xp[4][P + 1];  // x^0 .. x^p of this thread's 4 points
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const double x = (double)xs[ty + 16 * u][q];
-        xp[u][0] = 1.0;
-#pragma unroll
-        for (int e = 1; e <= P; ++e) xp[u][e] = xp[u][e - 1] * x;
-      }
-      if (kb + q < d) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) hp[u] += xp[u][p];
-      }
-#pragma unroll
-      for (int tt = 1; tt < P; ++tt) {
-        double b[4];
-#pragma unroll
-        for (int v = 0; v < 4; ++v) b[v] = ws[tt - 1][q][tx + 16 * v];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const double a = xp[u][p - tt];
-#pragma unroll
-          for (int v = 0; v < 4; ++v) acc[u][v] = fma(a, b[v], acc[u][v]);
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int64_t i = i0 + ty + 16 * u;
-    if (i >= n) continue;
-#pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const int64_t c = c0 + tx + 16 * v;
-      if (c < m) Y[i * ldy + c] = fma(S[c], hp[u], acc[u][v] + G[c]);
-    }
   }
 }
 
@@ -313,14 +377,20 @@ void launch_bilinear(const float *X, int64_t ldx, const double *M, const float *
   double *V = G + m;
   dim3 g12((unsigned)((d + kTile - 1) / kTile), (unsigned)((m + kTile - 1) / kTile),
            (unsigned)nchunks);
-  k12_moment_reduce<<<g12, 256, 0, s>>>(X, ldx, Z, ldz, n, d, m, 1, chunk, nchunks, part);
+  const size_t sm12 = (size_t)2 * kDmmaKs * kDmmaPad * sizeof(double);
+  cudaFuncSetAttribute(k12_moment_reduce_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sm12);
+  k12_moment_reduce_dmma<<<g12, 256, sm12, s>>>(X, ldx, Z, ldz, n, d, m, 1, chunk, part);
   int64_t b13 = (d * m + 255) / 256;
   if (b13 > 148 * 8) b13 = 148 * 8;
   k13_moment_fold<<<(unsigned)b13, 256, 0, s>>>(part, nchunks, d, m, 1, W, G);
   k15_small_gemm<<<(unsigned)b13, 256, 0, s>>>(M, W, d, m, V);
   k15_zero<<<1, 256, 0, s>>>(S, 2 * m);  // S and G (adjacent): no h S or G term
   dim3 g14((unsigned)((n + kTile - 1) / kTile), (unsigned)((m + kTile - 1) / kTile));
-  k14_moment_expand<2><<<g14, 256, 0, s>>>(X, ldx, n, d, m, V, S, G, Y, ldy);
+  const size_t sm14 = ((size_t)kTile * (kStepK + 2) + (size_t)kStepK * kDmmaPad) * sizeof(double);
+  cudaFuncSetAttribute(k14_moment_expand_dmma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sm14);
+  k14_moment_expand_dmma<2><<<g14, 256, sm14, s>>>(X, ldx, n, d, m, V, S, G, Y, ldy);
 }
 
 size_t lpp_even_workspace(int64_t n, int64_t d, int64_t m, int p, int64_t *nchunks_out,
@@ -349,16 +419,25 @@ void launch_lpp_even(const float *X, int64_t ldx, const float *Z, int64_t ldz, i
   double *G = S + m;
   dim3 g12((unsigned)((d + kTile - 1) / kTile), (unsigned)((m + kTile - 1) / kTile),
            (unsigned)(p * nchunks));
-  k12_moment_reduce<<<g12, 256, 0, s>>>(X, ldx, Z, ldz, n, d, m, p, chunk, nchunks, part);
+  const size_t sm12 = (size_t)2 * kDmmaKs * kDmmaPad * sizeof(double);
+  cudaFuncSetAttribute(k12_moment_reduce_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sm12);
+  k12_moment_reduce_dmma<<<g12, 256, sm12, s>>>(X, ldx, Z, ldz, n, d, m, p, chunk, part);
   int64_t b13 = ((int64_t)p * d * m + 255) / 256;
   if (b13 > 148 * 8) b13 = 148 * 8;
   k13_moment_fold<<<(unsigned)b13, 256, 0, s>>>(part, nchunks, d, m, p, W, G);
   k13_colsum<<<(unsigned)m, 256, 0, s>>>(W + (size_t)(p - 1) * d * m, Z, ldz, n, d, m, S, G);
   dim3 g14((unsigned)((n + kTile - 1) / kTile), (unsigned)((m + kTile - 1) / kTile));
+  auto expand = [&](auto kern, int P) {
+    const size_t sm14 = ((size_t)(P - 1) * kTile * (kStepK + 2) +
+                         (size_t)(P - 1) * kStepK * kDmmaPad) * sizeof(double);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm14);
+    kern<<<g14, 256, sm14, s>>>(X, ldx, n, d, m, W, S, G, Y, ldy);
+  };
   switch (p) {
-    case 2: k14_moment_expand<2><<<g14, 256, 0, s>>>(X, ldx, n, d, m, W, S, G, Y, ldy); break;
-    case 4: k14_moment_expand<4><<<g14, 256, 0, s>>>(X, ldx, n, d, m, W, S, G, Y, ldy); break;
-    case 6: k14_moment_expand<6><<<g14, 256, 0, s>>>(X, ldx, n, d, m, W, S, G, Y, ldy); break;
+    case 2: expand(k14_moment_expand_dmma<2>, 2); break;
+    case 4: expand(k14_moment_expand_dmma<4>, 4); break;
+    case 6: expand(k14_moment_expand_dmma<6>, 6); break;
     default: break;
   }
 }
