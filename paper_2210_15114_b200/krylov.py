@@ -40,9 +40,13 @@ class KrylovResult:
 
 
 def _project_out(V: torch.Tensor, basis: list[torch.Tensor]) -> torch.Tensor:
-    for _ in range(2):  # two passes of block classical Gram-Schmidt
-        for B in basis:
-            V = V - B @ (B.T @ V)
+    """V minus its projection on the span of the (orthonormal) blocks: two passes of block
+    classical Gram-Schmidt against the concatenated basis (one pair of GEMMs per pass)."""
+    if not basis:
+        return V
+    B = basis[0] if len(basis) == 1 else torch.cat(basis, dim=1)
+    for _ in range(2):
+        V = V - B @ (B.T @ V)
     return V
 
 
@@ -116,21 +120,25 @@ def block_krylov(matvec: MatVec, n: int, k: int, *, block: Optional[int] = None,
         columns += V.shape[1] * (2 if split else 1)
         return fp64_product(matvec, V, split)
 
-    basis: list[torch.Tensor] = []   # orthonormal blocks Q_0 .. Q_{q-1}
-    AQ: list[torch.Tensor] = []      # A Q_j
+    # the basis and A times it live in preallocated n x (q b) buffers (views, no re-concatenation)
+    Qbuf = torch.empty((n, q * b), dtype=dtype, device=gdev)
+    AQbuf = torch.empty((n, q * b), dtype=dtype, device=gdev)
+    cols = 0
     W = apply(Pi)                    # A Pi: the first Krylov block
-    while len(basis) < q:
-        width = min(b, n - sum(B.shape[1] for B in basis))
+    for _ in range(q):
+        width = min(b, n - cols)
         if width <= 0:
             break
-        Q = _orth_block(W[:, :width], basis, gen)
+        Q = _orth_block(W[:, :width], [Qbuf[:, :cols]] if cols else [], gen)
         if Q is None:
             break
-        basis.append(Q)
+        w_ = Q.shape[1]
+        Qbuf[:, cols:cols + w_] = Q
         W = apply(Q)                 # A Q_j: Rayleigh-Ritz column block and next Krylov block
-        AQ.append(W)
-    Qm = torch.cat(basis, dim=1)
-    T = Qm.T @ torch.cat(AQ, dim=1)  # Rayleigh quotient Q^T A Q
+        AQbuf[:, cols:cols + w_] = W
+        cols += w_
+    Qm = Qbuf[:, :cols]
+    T = Qm.T @ AQbuf[:, :cols]       # Rayleigh quotient Q^T A Q
     T = 0.5 * (T + T.T)
     lam, V = torch.linalg.eigh(T)
     order = torch.argsort(lam.abs(), descending=True)[:k]
