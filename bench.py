@@ -403,7 +403,7 @@ def main_ours(args):
         "value": value, "unit": "updates/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None,
-        "dtype": "f64 accumulation over f32 inputs", "data": "synthetic",
+        "dtype": "f64", "input_dtype": "f32", "data": "synthetic",
         "config": {"workload": args.workload, "n": n, "d": d, "m": m, "queries_per_step": Q,
                    "fresh_queries": w.fresh_queries, "parallelism": f"coord-shard x{world}",
                    "collective": (args.reduce if world > 1 else None),

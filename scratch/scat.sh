@@ -1,3 +1,3 @@
 timeout 300 python scratch/scat.py c3 auto
-L1DM_REDUCE_ALL_V4=0 timeout 300 python scratch/scat.py c3 auto
+L1DM_REDUCE_ALL_ASYNC=0 timeout 300 python scratch/scat.py c3 auto
 timeout 300 python scratch/scat.py c3 auto
