@@ -18,7 +18,7 @@ constexpr uint32_t kSpinLimit = 1u << 26;
 
 // ---------------- prepare (Alg. 1) ----------------
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;                          // keys per thread per onesweep tile
+constexpr int kSortItems = 8;                           // keys per thread per onesweep tile
 constexpr int kSortTile = kSortThreads * kSortItems;    // 4096 keys
 constexpr int kHistChunk = 16384;                       // keys per histogram CTA
 
