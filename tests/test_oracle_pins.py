@@ -225,3 +225,39 @@ def test_thread_count_independent():
     b = oracle.sort_based(X, Z, nthreads=3)
     assert np.array_equal(a, b)
     assert np.array_equal(oracle.brute(X, Z, nthreads=1), oracle.brute(X, Z, nthreads=4))
+
+
+# ---- Q18: precision discriminator for the U-form (DESIGN.md §3 tolerance derivation) -------
+def test_u_form_precision_requires_fp64_storage():
+    """The U-form evaluated with numpy in fp64 meets the 1e-9 bar against the
+    oracle; the same with U rounded to fp32 before the point gather does not, which
+    is why the library keeps U (and every accumulator) in fp64."""
+    rng = np.random.default_rng(18)
+    n, d = 1 << 15, 4
+    centres = rng.uniform(-10, 10, size=(32, d))
+    X = (centres[rng.integers(0, 32, n)] + 0.5 * rng.standard_normal((n, d))).astype(np.float32)
+    z = rng.standard_normal(n).astype(np.float32)
+    rows = np.arange(0, n, 997)
+    ref = oracle.rows(X, z[:, None], rows)[:, 0]
+
+    def u_form(store):
+        y = np.zeros(n)
+        S = z.astype(np.float64).sum()
+        for k in range(d):
+            order = np.argsort(X[:, k], kind="stable")
+            v = X[order, k].astype(np.float64)
+            s = z[order].astype(np.float64)
+            P = np.concatenate([[0.0], np.cumsum(s)[:-1]])
+            Q = np.concatenate([[0.0], np.cumsum(v * s)[:-1]])
+            U = store(v * P - Q)
+            T = (v * s).sum()
+            contrib = np.empty(n)
+            contrib[order] = 2 * U + T - v * S
+            y += contrib
+        return y[rows]
+
+    err64 = np.linalg.norm(u_form(lambda u: u) - ref) / np.linalg.norm(ref)
+    err32 = np.linalg.norm(u_form(lambda u: u.astype(np.float32).astype(np.float64)) - ref) / \
+        np.linalg.norm(ref)
+    assert err64 <= 1e-12
+    assert err32 > 1e-9
