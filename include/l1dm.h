@@ -184,6 +184,24 @@ L1DM_API l1dm_status l1dm_l2_embed(const float *X, int64_t n, int64_t ld_x, int6
                                    const float *G, int64_t k, float *Xp, int64_t ld_p,
                                    void *stream);
 
+/* Column-block output for overlapping the cross-GPU sum in the scatter strategy, whose rows
+ * are final only after the last column block: the query writes Yb, a
+ * column-block-major array of col_blocks blocks of n x mb fp64 (block cb holds columns
+ * [cb mb, min(m, cb mb + mb)) of Y with rows contiguous; a ragged last block is padded to mb),
+ * and records block_events[cb] (caller-created cudaEvent_t; NULL entries skipped) on `stream`
+ * as soon as block cb is final, so a collective on block cb can run while later blocks are
+ * computed.  l1dm_query_layout reports the handle's strategy, mb and col_blocks for m (host
+ * only); l1dm_unblock converts Yb back to a row-major Y (n x ld_y).  Device pointers only.
+ * Errors: EINVAL (not the scatter strategy for this m, m < 2, nevents not 0 or col_blocks,
+ * host pointers), and as l1dm_matvec_ex. */
+L1DM_API l1dm_status l1dm_query_layout(l1dm_handle h, int64_t m, int64_t *scatter, int64_t *mb,
+                                       int64_t *col_blocks);
+L1DM_API l1dm_status l1dm_matvec_colblocks(l1dm_handle h, const float *Z, int64_t ld_z, int64_t m,
+                                           double *Yb, void *stream, int64_t nevents,
+                                           void *const *block_events);
+L1DM_API l1dm_status l1dm_unblock(const double *Yb, int64_t n, int64_t m, int64_t mb, double *Y,
+                                  int64_t ld_y, void *stream);
+
 /* Release every buffer the handle owns.  NULL is a no-op.  Synchronises the
  * handle's stream first. */
 L1DM_API void l1dm_free(l1dm_handle h);

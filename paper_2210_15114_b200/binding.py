@@ -28,7 +28,8 @@ STATUS = {
 EXPORTS = [
     "l1dm_prepare", "l1dm_prepare_ex", "l1dm_matvec", "l1dm_matvec_ex", "l1dm_matvec_pipelined",
     "l1dm_matvec_lp", "l1dm_matvec_lp_ex", "l1dm_tv_matvec", "l1dm_tv_matvec_ex",
-    "l1dm_lpp_even_matvec", "l1dm_bilinear_matvec", "l1dm_l2_embed",
+    "l1dm_lpp_even_matvec", "l1dm_bilinear_matvec", "l1dm_l2_embed", "l1dm_query_layout",
+    "l1dm_matvec_colblocks", "l1dm_unblock",
     "l1dm_free", "l1dm_sync",
     "l1dm_shape", "l1dm_workspace_bytes", "l1dm_set_workspace_limit", "l1dm_set_query_mode",
     "l1dm_plan", "l1dm_plan_ex", "l1dm_timing_enable", "l1dm_timing_read", "l1dm_debug_export", "l1dm_release_cached",
@@ -85,6 +86,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.l1dm_lpp_even_matvec.argtypes = [vp, i64, i64, i64, i32, vp, i64, i64, vp, i64, vp]
     lib.l1dm_bilinear_matvec.argtypes = [vp, i64, i64, i64, vp, vp, i64, i64, vp, i64, vp]
     lib.l1dm_l2_embed.argtypes = [vp, i64, i64, i64, vp, i64, vp, i64, vp]
+    lib.l1dm_query_layout.argtypes = [vp, i64, ctypes.POINTER(i64), ctypes.POINTER(i64),
+                                      ctypes.POINTER(i64)]
+    lib.l1dm_matvec_colblocks.argtypes = [vp, vp, i64, i64, vp, vp, i64, ctypes.POINTER(vp)]
+    lib.l1dm_unblock.argtypes = [vp, i64, i64, i64, vp, i64, vp]
     lib.l1dm_matvec_pipelined.argtypes = [vp, vp, i64, i64, vp, i64, vp, i64,
                                            ctypes.POINTER(vp)]
     lib.l1dm_free.argtypes = [vp]
@@ -109,7 +114,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     for name in ("l1dm_prepare", "l1dm_prepare_ex", "l1dm_matvec", "l1dm_matvec_ex",
                  "l1dm_matvec_pipelined", "l1dm_sync", "l1dm_matvec_lp", "l1dm_matvec_lp_ex",
                  "l1dm_tv_matvec", "l1dm_tv_matvec_ex", "l1dm_lpp_even_matvec",
-                 "l1dm_bilinear_matvec", "l1dm_l2_embed",
+                 "l1dm_bilinear_matvec", "l1dm_l2_embed", "l1dm_query_layout",
+                 "l1dm_matvec_colblocks", "l1dm_unblock",
                  "l1dm_shape", "l1dm_set_workspace_limit", "l1dm_set_query_mode", "l1dm_plan", "l1dm_plan_ex",
                  "l1dm_timing_enable",
                  "l1dm_timing_read", "l1dm_debug_export"):
@@ -309,6 +315,48 @@ def l1dm_l2_embed(X: torch.Tensor, G: torch.Tensor, out=None, stream=None) -> to
                                _stream_of(X, stream))
     _check(rc, "l1dm_l2_embed")
     return out
+
+
+def l1dm_query_layout(h: Handle, m: int):
+    """(scatter, mb, col_blocks) of the handle's plan for m columns."""
+    a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _check(load_library().l1dm_query_layout(h.ptr, m, ctypes.byref(a), ctypes.byref(b),
+                                            ctypes.byref(c)), "l1dm_query_layout")
+    return a.value, b.value, c.value
+
+
+def _event_handles(events, device, stream):
+    out = []
+    for e in events:
+        if e.cuda_event == 0:  # torch creates the CUDA event lazily, on first record
+            e.record(torch.cuda.current_stream(device) if stream is None else stream)
+        out.append(ctypes.c_void_p(e.cuda_event))
+    return (ctypes.c_void_p * len(out))(*out)
+
+
+def l1dm_matvec_colblocks(h: Handle, Z: torch.Tensor, Yb: torch.Tensor, events, stream=None):
+    """Scatter-strategy query into the column-block-major Yb (col_blocks x n x mb fp64, CUDA),
+    recording events[cb] once block cb is final (include/l1dm.h)."""
+    Z = _as_f32_2d(Z, "Z")
+    if not (Z.is_cuda and Yb.is_cuda) or Yb.dtype != torch.float64 or not Yb.is_contiguous():
+        raise ValueError("Z and Yb must be CUDA tensors; Yb contiguous float64")
+    arr = _event_handles(events, Z.device, stream)
+    with torch.cuda.device(Z.device):
+        rc = load_library().l1dm_matvec_colblocks(h.ptr, _ptr(Z), Z.stride(0), Z.shape[1],
+                                                  _ptr(Yb), _stream_of(Z, stream), len(events),
+                                                  arr)
+    _check(rc, "l1dm_matvec_colblocks")
+    return Yb
+
+
+def l1dm_unblock(Yb: torch.Tensor, m: int, Y: torch.Tensor, stream=None):
+    """Row-major Y (n x m) from the column-block-major Yb (col_blocks x n x mb)."""
+    n, mb = Yb.shape[1], Yb.shape[2]
+    with torch.cuda.device(Yb.device):
+        rc = load_library().l1dm_unblock(_ptr(Yb), n, m, mb, _ptr(Y), Y.stride(0),
+                                         _stream_of(Yb, stream))
+    _check(rc, "l1dm_unblock")
+    return Y
 
 
 def point_blocks(n: int, nblocks: int):

@@ -558,9 +558,11 @@ l1dm_status ensure_plan(l1dm_ctx *h, int64_t m, int vec_cap) {
 
 // nblocks/events: the pass that completes Y (the last chunk's accumulate, or the scatter-mode
 // epilogue) is launched per contiguous point block, and events[b] is recorded after block b.
+// blocked (scatter mode, m > 1 only): Y is column-block-major — block cb at Y + cb n mb with
+// row stride mb — and events[cb] is recorded once block cb is final (nblocks = col_blocks).
 l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, double *Y,
                           int64_t ldy, cudaStream_t s, int64_t nblocks = 1,
-                          void *const *events = nullptr) {
+                          void *const *events = nullptr, bool blocked = false) {
   if (nblocks < 1) nblocks = 1;
   auto block_range = [&](int64_t b, int64_t &i0, int64_t &i1) {
     i0 = (h->n * b) / nblocks;
@@ -675,7 +677,12 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
         TimedScope ts(h, kColsums, s);
         launch_totals(h->part.p + 2 * c0, 2 * m, h->dl, mc, h->Sg.p + c0, h->Sg.p + m + c0, s);
         const int64_t nb = last ? nblocks : 1;
-        for (int64_t b = 0; b < nb; ++b) {
+        if (blocked) {
+          launch_block_out(h->yt.p, p.mb, mc, h->hsum.p, h->Sg.p + c0, h->Sg.p + m + c0,
+                           Y + (size_t)cb * h->n * p.mb, p.mb, 0, h->n, s);
+          if (events && events[cb]) CUDA_TRY(cudaEventRecord((cudaEvent_t)events[cb], s));
+        }
+        for (int64_t b = 0; !blocked && b < nb; ++b) {
           int64_t i0 = 0, i1 = h->n;
           if (last) block_range(b, i0, i1);
           launch_block_out(h->yt.p, p.mb, mc, h->hsum.p, h->Sg.p + c0, h->Sg.p + m + c0, Y + c0,
@@ -1182,6 +1189,55 @@ l1dm_status l1dm_matvec_pipelined(l1dm_handle h, const float *Z, int64_t ld_z, i
   cudaStream_t s = (cudaStream_t)stream;
   h->last_stream = s;
   return matvec_device(h, Z, ld_z, m, Y, ld_y, s, point_blocks, block_events);
+}
+
+l1dm_status l1dm_query_layout(l1dm_handle h, int64_t m, int64_t *scatter, int64_t *mb,
+                              int64_t *col_blocks) {
+  g_err.clear();
+  if (!h || m < 1) return fail(L1DM_EINVAL, "handle is NULL or m < 1");
+  l1dm_status st = ensure_plan(h, m, 4);
+  if (st != L1DM_OK) return st;
+  if (scatter) *scatter = h->plan.scatter;
+  if (mb) *mb = h->plan.mb;
+  if (col_blocks) *col_blocks = h->plan.col_blocks;
+  return L1DM_OK;
+}
+
+l1dm_status l1dm_matvec_colblocks(l1dm_handle h, const float *Z, int64_t ld_z, int64_t m,
+                                  double *Yb, void *stream, int64_t nevents,
+                                  void *const *events) {
+  g_err.clear();
+  if (!h) return fail(L1DM_EINVAL, "handle is NULL");
+  if (!Z || !Yb || m < 2 || ld_z < m)
+    return fail(L1DM_EINVAL, "Z/Yb NULL, m < 2 or ld_z < m");
+  l1dm_status st = check_device(h);
+  if (st != L1DM_OK) return st;
+  if (!is_device_pointer(Z) || !is_device_pointer(Yb))
+    return fail(L1DM_EINVAL, "l1dm_matvec_colblocks needs device Z and Yb");
+  st = ensure_plan(h, m, vec_cap_for(Z, ld_z));
+  if (st != L1DM_OK) return st;
+  if (!h->plan.scatter)
+    return fail(L1DM_EINVAL, "column-block output needs the scatter strategy (plan is gather)");
+  if (nevents != 0 && nevents != h->plan.col_blocks)
+    return fail(L1DM_EINVAL, "nevents=%lld, plan has %d column blocks", (long long)nevents,
+                h->plan.col_blocks);
+  cudaStream_t s = (cudaStream_t)stream;
+  h->last_stream = s;
+  return matvec_device(h, Z, ld_z, m, Yb, h->plan.mb, s, h->plan.col_blocks,
+                       nevents ? events : nullptr, true);
+}
+
+l1dm_status l1dm_unblock(const double *Yb, int64_t n, int64_t m, int64_t mb, double *Y,
+                         int64_t ld_y, void *stream) {
+  g_err.clear();
+  if (!Yb || !Y || n < 1 || m < 1 || mb < 1 || ld_y < m)
+    return fail(L1DM_EINVAL, "invalid unblock arguments");
+  int dev = 0;
+  l1dm_status st = check_arch(&dev);
+  if (st != L1DM_OK) return st;
+  launch_unblock(Yb, n, m, mb, Y, ld_y, (cudaStream_t)stream);
+  CUDA_TRY(cudaGetLastError());
+  return L1DM_OK;
 }
 
 l1dm_status l1dm_matvec(l1dm_handle h, const float *Z, int64_t m, double *Y) {

@@ -140,6 +140,9 @@ void launch_accumulate(const QueryPlan &p, const uint32_t *rank, int64_t ldn, in
 // l_p^p, odd p in {3, 5, 7}: plan over the seq kernels.
 bool make_lp_plan(int64_t n, int64_t dl, int64_t m, int lp, int64_t l2_bytes, int64_t ws_limit,
                   int mode, QueryPlan *p);
+// Y (row-major, ldy) <- Yb (column-block-major blocks of n x mb).
+void launch_unblock(const double *Yb, int64_t n, int64_t m, int64_t mb, double *Y, int64_t ldy,
+                    cudaStream_t s);
 // Y[i][c] *= a over n x m.
 void launch_scale(double *Y, int64_t ldy, int64_t n, int64_t m, double a, cudaStream_t s);
 // out[0] = max_i |h_i - 1|, out[1] = min over every prepared coordinate value (device doubles).

@@ -1239,6 +1239,25 @@ void launch_block_out(const double *yt, int mb, int64_t mc, const double *hsum, 
   k9_block_out<<<(unsigned)blocks, 256, 0, s>>>(yt, mb, mc, hsum, S, g, Y, ldy, i0, i1);
 }
 
+// Y[i][c] = Yb[c / mb][i][c % mb]: column-block-major (l1dm_matvec_colblocks) to row-major.
+__global__ void __launch_bounds__(256)
+    k10_unblock(const double *__restrict__ Yb, int64_t n, int64_t m, int64_t mb,
+                double *__restrict__ Y, int64_t ldy) {
+  const int64_t total = n * m;
+  for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * 256) {
+    const int64_t i = e / m, c = e - (e / m) * m;
+    Y[i * ldy + c] = Yb[((c / mb) * n + i) * mb + (c % mb)];
+  }
+}
+
+void launch_unblock(const double *Yb, int64_t n, int64_t m, int64_t mb, double *Y, int64_t ldy,
+                    cudaStream_t s) {
+  int64_t blocks = (n * m + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k10_unblock<<<(unsigned)blocks, 256, 0, s>>>(Yb, n, m, mb, Y, ldy);
+}
+
 // Y[i][c] *= a (TV = a * l1 with a = 1/2).
 __global__ void __launch_bounds__(256)
     k10_scale(double *__restrict__ Y, int64_t ldy, int64_t n, int64_t m, double a) {

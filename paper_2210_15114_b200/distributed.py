@@ -93,30 +93,44 @@ class ShardedL1DM:
         n, m = Z.shape[0], Z.shape[1]
         if Y is None:
             Y = torch.empty((n, m), dtype=torch.float64, device=Z.device)
-        events = [torch.cuda.Event() for _ in range(nblocks)]
         main = torch.cuda.current_stream(Z.device)
         if getattr(self, "_compute_stream", None) is None:
             self._compute_stream = torch.cuda.Stream(device=Z.device)
         cs = self._compute_stream
         cs.wait_stream(main)                      # Z (and Y's previous users) are ready
+        scatter, mb, ncb = binding.l1dm_query_layout(self.handle, m)
+        if scatter and m > 1:
+            # scatter strategy: rows are final only after the last column block, so the sum runs
+            # per column block of a column-block-major staging copy
+            Yb = torch.empty((ncb, n, mb), dtype=torch.float64, device=Z.device)
+            events = [torch.cuda.Event() for _ in range(ncb)]
+            binding.l1dm_matvec_colblocks(self.handle, Z, Yb, events, stream=cs)
+            works = []
+            for b, ev in enumerate(events):
+                main.wait_event(ev)
+                works.append(self._collective(Yb[b], root))
+            for w in works:
+                w.wait()
+            binding.l1dm_unblock(Yb, m, Y, stream=main)
+            return (Y, []) if async_op else Y
+        events = [torch.cuda.Event() for _ in range(nblocks)]
         binding.l1dm_matvec_pipelined(self.handle, Z, Y, events, stream=cs)
         works = []
         for (i0, i1), ev in zip(binding.point_blocks(n, nblocks), events):
             # the main stream (which NCCL synchronises with) waits only for block b's rows, so
             # block b's collective runs while the compute stream finishes blocks b+1..
             main.wait_event(ev)
-            if root is None:
-                w = dist.all_reduce(Y[i0:i1], op=dist.ReduceOp.SUM, group=self.group,
-                                    async_op=True)
-            else:
-                w = dist.reduce(Y[i0:i1], dst=root, op=dist.ReduceOp.SUM, group=self.group,
-                                async_op=True)
-            works.append(w)
+            works.append(self._collective(Y[i0:i1], root))
         if async_op:
             return Y, works
         for w in works:
             w.wait()
         return Y
+
+    def _collective(self, T, root):
+        if root is None:
+            return dist.all_reduce(T, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+        return dist.reduce(T, dst=root, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
 
     def close(self):
         if self.handle is not None and self._prepare is binding.l1dm_prepare:

@@ -145,3 +145,34 @@ def test_scatter_per_block_reduce_subprocess():
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_colblocks_output_and_unblock():
+    """l1dm_matvec_colblocks: block cb of the column-block-major output is final when its event
+    fires; l1dm_unblock gives back the row-major Y (ragged last block included)."""
+    rng = np.random.default_rng(44)
+    X = rng.standard_normal((5000, 4)).astype(np.float32)
+    Z = rng.standard_normal((5000, 21)).astype(np.float32)
+    Yr = oracle.brute(X, Z)
+    h = l1.l1dm_prepare(torch.from_numpy(X).cuda())
+    l1.l1dm_set_query_mode(h, "scatter")
+    scatter, mb, ncb = l1.binding.l1dm_query_layout(h, 21)
+    assert scatter == 1 and ncb == -(-21 // mb)
+    Yb = torch.full((ncb, 5000, mb), float("nan"), dtype=torch.float64, device="cuda")
+    evs = [torch.cuda.Event() for _ in range(ncb)]
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    l1.binding.l1dm_matvec_colblocks(h, torch.from_numpy(Z).cuda(), Yb, evs, stream=side)
+    for cb, ev in enumerate(evs):
+        ev.synchronize()
+        c0, c1 = cb * mb, min(21, cb * mb + mb)
+        assert col_rel_l2(Yb[cb, :, :c1 - c0].cpu().numpy(), Yr[:, c0:c1]) <= TOL
+    Y = torch.empty((5000, 21), dtype=torch.float64, device="cuda")
+    l1.binding.l1dm_unblock(Yb, 21, Y, stream=side)
+    side.synchronize()
+    assert col_rel_l2(Y.cpu().numpy(), Yr) <= TOL
+    l1.l1dm_set_query_mode(h, "gather")
+    with pytest.raises(l1.L1dmError):
+        l1.binding.l1dm_matvec_colblocks(h, torch.from_numpy(Z).cuda(), Yb, evs)
+    l1.l1dm_sync(h)
+    l1.l1dm_free(h)
