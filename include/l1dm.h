@@ -233,9 +233,15 @@ L1DM_API l1dm_status l1dm_set_workspace_limit(l1dm_handle h, size_t bytes);
  *   SCATTER the scan adds 2U straight into Y[perm_k(r)] with fp64 L2 atomics, one column
  *           block of Y at a time (no U workspace, no rank gather; the order of the d terms
  *           of y_i then varies run to run at the ulp level on float data — DESIGN.md R16).
- * AUTO (the default) picks SCATTER when a column block of Y and Z fits in L2.
- * Returns EINVAL for a NULL handle or an unknown mode.  Host-only. */
-enum { L1DM_MODE_AUTO = 0, L1DM_MODE_GATHER = 1, L1DM_MODE_SCATTER = 2 };
+ *   RUNS    tie-heavy data only (every prepared coordinate takes <= 256 distinct values,
+ *           detected by prepare): Alg. 2 over the distinct values — per coordinate the run
+ *           sums of Z by fp64 L2 reductions in point order, a prefix over the runs, then each
+ *           point adds its run's value; no sorted-order gather at all.
+ * AUTO (the default) picks RUNS when the prepared data allows it, else SCATTER when a column
+ * block of Y and Z fits in L2, else GATHER.  l1_p, TV and the pipelined/column-block calls
+ * follow the same choice where they apply.  Returns EINVAL for a NULL handle, an unknown
+ * mode, or RUNS on data without runs tables.  Host-only. */
+enum { L1DM_MODE_AUTO = 0, L1DM_MODE_GATHER = 1, L1DM_MODE_SCATTER = 2, L1DM_MODE_RUNS = 3 };
 L1DM_API l1dm_status l1dm_set_query_mode(l1dm_handle h, int mode);
 
 /* Query plan, a pure function of the sizes (testable without a GPU).

@@ -402,7 +402,7 @@ def l1dm_set_workspace_limit(h: Handle, nbytes: int):
     _check(load_library().l1dm_set_workspace_limit(h.ptr, int(nbytes)), "l1dm_set_workspace_limit")
 
 
-MODES = {"auto": 0, "gather": 1, "scatter": 2}
+MODES = {"auto": 0, "gather": 1, "scatter": 2, "runs": 3}
 
 
 def l1dm_set_query_mode(h: Handle, mode):

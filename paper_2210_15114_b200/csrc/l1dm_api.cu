@@ -193,6 +193,12 @@ struct l1dm_ctx {
   DevBuf<uint32_t> perm;
   DevBuf<uint32_t> rank;
   DevBuf<double> hsum;
+  // runs of equal values (every coordinate <= 256 distinct values)
+  bool has_runs = false;
+  DevBuf<uint8_t> runid;   // [dl][ldn] run index of point i
+  DevBuf<float> rvals;     // [dl][256] distinct values, ascending
+  DevBuf<uint32_t> nruns;  // [dl]
+  DevBuf<double> rtab;     // [dl][256][m] query table: H, then U in place
   // query workspace
   DevBuf<double> U;
   DevBuf<uint32_t> flags;
@@ -311,6 +317,10 @@ void destroy(l1dm_ctx *h) {
   h->sval_bits.release();
   h->perm.release();
   h->rank.release();
+  h->runid.release();
+  h->rvals.release();
+  h->nruns.release();
+  h->rtab.release();
   h->hsum.release();
   h->U.release();
   h->flags.release();
@@ -407,8 +417,8 @@ l1dm_status prepare_impl(const float *X, int64_t n, int64_t ld_x, int64_t k_begi
   CUDA_TRY(cudaMemcpyAsync(flags_h, ctrl.p, sizeof(flags_h), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   lap("keys + hist + readback");
-  Xstage.release();
   if (flags_h[0]) {
+    Xstage.release();
     keyA.release();
     hist.release();
     ctrl.release();
@@ -500,6 +510,52 @@ l1dm_status prepare_impl(const float *X, int64_t n, int64_t ld_x, int64_t k_begi
     std::swap(h->perm.count, vbuf[fin]->count);
   }
   lap("sort passes + rank");
+  // runs: count run starts per tile; keep runid / rvals when every coordinate has <= 256
+  {
+    static const bool runs_env = [] {
+      const char *e = getenv("L1DM_RUNS");
+      return e ? atoi(e) != 0 : true;
+    }();
+    const int64_t rt = runs_tiles(n);
+    if (runs_env && n >= 2) {
+      DevBuf<uint32_t> rcnt;
+      CUDA_TRY(rcnt.ensure((size_t)dl * rt, false, s));
+      launch_runs_count(reinterpret_cast<const float *>(h->sval_bits.p), n, ldn, dl, rcnt.p, s);
+      h->kernel_launches++;
+      std::vector<uint32_t> cnt((size_t)dl * rt), off((size_t)dl * rt), nr((size_t)dl);
+      CUDA_TRY(cudaMemcpyAsync(cnt.data(), rcnt.p, cnt.size() * sizeof(uint32_t),
+                               cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaStreamSynchronize(s));
+      bool ok = true;
+      for (int64_t k = 0; k < dl; ++k) {
+        uint32_t run = 0;
+        for (int64_t t = 0; t < rt; ++t) {
+          off[(size_t)k * rt + t] = run;
+          run += cnt[(size_t)k * rt + t];
+        }
+        nr[(size_t)k] = run;
+        if (run > 256) ok = false;
+      }
+      if (ok) {
+        CUDA_TRY(rcnt.ensure((size_t)dl * rt, false, s));
+        CUDA_TRY(cudaMemcpyAsync(rcnt.p, off.data(), off.size() * sizeof(uint32_t),
+                                 cudaMemcpyHostToDevice, s));
+        CUDA_TRY(h->runid.ensure((size_t)dl * ldn, false, s));
+        CUDA_TRY(h->rvals.ensure((size_t)dl * 256, true, s));
+        CUDA_TRY(h->nruns.ensure((size_t)dl, false, s));
+        CUDA_TRY(cudaMemcpyAsync(h->nruns.p, nr.data(), nr.size() * sizeof(uint32_t),
+                                 cudaMemcpyHostToDevice, s));
+        launch_runs_emit(reinterpret_cast<const float *>(h->sval_bits.p), n, ldn, dl, rcnt.p,
+                         h->rvals.p, s);
+        launch_runs_ids(Xd, n, ld_x, k_begin, dl, ldn, h->rvals.p, h->nruns.p, h->runid.p, s);
+        h->kernel_launches += 2;
+        h->has_runs = true;
+      }
+      CUDA_TRY(cudaStreamSynchronize(s));  // rcnt and the host vectors go out of scope
+    }
+  }
+  lap("runs");
+  Xstage.release();  // (the runs ids read X)
   CUDA_TRY(cudaEventRecord(ev1, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   CUDA_TRY(cudaMemcpy(flags_h, ctrl.p, sizeof(flags_h), cudaMemcpyDeviceToHost));
@@ -558,6 +614,12 @@ l1dm_status ensure_plan(l1dm_ctx *h, int64_t m, int vec_cap) {
 
 // nblocks/events: the pass that completes Y (the last chunk's accumulate, or the scatter-mode
 // epilogue) is launched per contiguous point block, and events[b] is recorded after block b.
+// Runs mode is used when the prepared data has runs tables (every coordinate <= 256 distinct
+// values) and the mode is AUTO or RUNS.
+bool use_runs(const l1dm_ctx *h) {
+  return h->has_runs && (h->mode == L1DM_MODE_AUTO || h->mode == L1DM_MODE_RUNS);
+}
+
 // blocked (scatter mode, m > 1 only): Y is column-block-major — block cb at Y + cb n mb with
 // row stride mb — and events[cb] is recorded once block cb is final (nblocks = col_blocks).
 l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, double *Y,
@@ -568,6 +630,43 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
     i0 = (h->n * b) / nblocks;
     i1 = (h->n * (b + 1)) / nblocks;
   };
+  if (!blocked && use_runs(h)) {
+    // runs mode: tie-heavy coordinates, no sorted-order gather at all
+    CUDA_TRY(h->rtab.ensure((size_t)h->dl * 256 * m, false, s));
+    CUDA_TRY(h->part.ensure((size_t)h->dl * 2 * m, false, s));
+    CUDA_TRY(h->Sg.ensure((size_t)2 * m, false, s));
+    {
+      TimedScope ts(h, kScan, s);
+      launch_runs_query(h->runid.p, h->ldn, h->n, h->dl, h->rvals.p, h->nruns.p, Z, ldz, m,
+                        h->rtab.p, h->part.p, h->hsum.p, h->Sg.p, Y, ldy, 0, s);
+      h->kernel_launches += 2;
+      h->launches[kScan]++;
+      if (h->timing) h->scan_pairs += h->n * h->dl;
+    }
+    {
+      TimedScope ts(h, kColsums, s);
+      launch_totals(h->part.p, 2 * m, h->dl, m, h->Sg.p, h->Sg.p + m, s);
+      h->kernel_launches++;
+      h->launches[kColsums]++;
+    }
+    {
+      TimedScope ts(h, kAcc, s);
+      for (int64_t b = 0; b < nblocks; ++b) {
+        int64_t i0, i1;
+        block_range(b, i0, i1);
+        launch_runs_query(h->runid.p, h->ldn, h->n, h->dl, h->rvals.p, h->nruns.p, Z, ldz, m,
+                          h->rtab.p, h->part.p, h->hsum.p, h->Sg.p, Y, ldy, 1, s, i0, i1);
+        h->kernel_launches++;
+        if (events && events[b]) CUDA_TRY(cudaEventRecord((cudaEvent_t)events[b], s));
+      }
+      h->launches[kAcc]++;
+      if (h->timing) h->acc_pairs += h->n * h->dl;
+    }
+    CUDA_TRY(cudaGetLastError());
+    h->queries++;
+    h->m_last = m;
+    return L1DM_OK;
+  }
   l1dm_status st = ensure_plan(h, m, vec_cap_for(Z, ldz));
   if (st != L1DM_OK) return st;
   const QueryPlan &p = h->plan;
@@ -1197,7 +1296,7 @@ l1dm_status l1dm_query_layout(l1dm_handle h, int64_t m, int64_t *scatter, int64_
   if (!h || m < 1) return fail(L1DM_EINVAL, "handle is NULL or m < 1");
   l1dm_status st = ensure_plan(h, m, 4);
   if (st != L1DM_OK) return st;
-  if (scatter) *scatter = h->plan.scatter;
+  if (scatter) *scatter = use_runs(h) ? 0 : h->plan.scatter;  // runs: point-block overlap
   if (mb) *mb = h->plan.mb;
   if (col_blocks) *col_blocks = h->plan.col_blocks;
   return L1DM_OK;
@@ -1282,8 +1381,10 @@ size_t l1dm_workspace_bytes(l1dm_handle h, int64_t m) {
 
 l1dm_status l1dm_set_query_mode(l1dm_handle h, int mode) {
   if (!h) return fail(L1DM_EINVAL, "handle is NULL");
-  if (mode < L1DM_MODE_AUTO || mode > L1DM_MODE_SCATTER)
+  if (mode < L1DM_MODE_AUTO || mode > L1DM_MODE_RUNS)
     return fail(L1DM_EINVAL, "unknown query mode %d", mode);
+  if (mode == L1DM_MODE_RUNS && !h->has_runs)
+    return fail(L1DM_EINVAL, "runs mode needs <= 256 distinct values in every coordinate");
   h->mode = mode;
   h->plan_m = -1;
   return L1DM_OK;

@@ -40,6 +40,18 @@ void launch_rank(const uint32_t *perm, uint32_t *rank, int64_t n, int64_t ldn, i
 void launch_identity_emit(const uint32_t *key, float *sval, uint32_t *perm, uint32_t *rank,
                           int64_t n, int64_t ldn, int64_t dl, cudaStream_t s);
 
+// Runs of equal values (tie-heavy coordinates): run-start counts per 4096-row
+// tile (cnt: dl x runs_tiles(n)); then, given exclusive per-tile offsets, runid[k][i] (u8,
+// point order) and rvals[k][0..R_k) (the distinct values, ascending; R_k <= 256).
+int64_t runs_tiles(int64_t n);
+void launch_runs_count(const float *sval, int64_t n, int64_t ldn, int64_t dl, uint32_t *cnt,
+                       cudaStream_t s);
+void launch_runs_emit(const float *sval, int64_t n, int64_t ldn, int64_t dl,
+                      const uint32_t *tile_off, float *rvals, cudaStream_t s);
+// runid[k][i] from X (point-major, the prepare's input) by binary search in rvals.
+void launch_runs_ids(const float *X, int64_t n, int64_t ldx, int64_t k0, int64_t dl, int64_t ldn,
+                     const float *rvals, const uint32_t *nruns, uint8_t *runid, cudaStream_t s);
+
 // ---------------- query (Alg. 2) ----------------
 // Rows per thread in a scan tile (8 warps, VC columns per lane): the tile stages about
 // 96 KB of perm/sval/Z in shared memory, so two CTAs fit per SM.
@@ -140,6 +152,13 @@ void launch_accumulate(const QueryPlan &p, const uint32_t *rank, int64_t ldn, in
 // l_p^p, odd p in {3, 5, 7}: plan over the seq kernels.
 bool make_lp_plan(int64_t n, int64_t dl, int64_t m, int lp, int64_t l2_bytes, int64_t ws_limit,
                   int mode, QueryPlan *p);
+// Runs mode.  phase 0: H (dl x 256 x m, zeroed here) <- run sums of Z, then U
+// in place and segtot (rows of 2m: S, T_k); phase 1: Y = 2 sum_k U[k][runid] + g - h S with
+// Sg = (S, g) from launch_totals.
+void launch_runs_query(const uint8_t *runid, int64_t ldn, int64_t n, int64_t dl, const float *rvals,
+                       const uint32_t *nruns, const float *Z, int64_t ldz, int64_t m, double *H,
+                       double *segtot, const double *hsum, double *Sg, double *Y, int64_t ldy,
+                       int phase, cudaStream_t s, int64_t i0 = 0, int64_t i1 = -1);
 // Y (row-major, ldy) <- Yb (column-block-major blocks of n x mb).
 void launch_unblock(const double *Yb, int64_t n, int64_t m, int64_t mb, double *Y, int64_t ldy,
                     cudaStream_t s);

@@ -350,4 +350,123 @@ void launch_identity_emit(const uint32_t *key, float *sval, uint32_t *perm, uint
   k3_identity<<<grid, 256, 0, s>>>(key, sval, perm, rank, n, ldn);
 }
 
+// ------------------------------------------------------------------ runs (tie-heavy data)
+// A coordinate whose sorted values take few distinct values (P:173 / P:205: ties) is also kept
+// as runs: rvals[k][j] = the j-th distinct value (ascending), runid[k][i] = j for point i (u8,
+// so at most 256 runs).  K_r1 counts run starts per 4096-row tile; the host turns the counts
+// into per-tile offsets and decides (every coordinate needs <= 256 runs); K_r2 emits both.
+constexpr int kRunTile = 4096;
+
+__global__ void __launch_bounds__(256)
+    k_runs_count(const float *__restrict__ sval, int64_t n, int64_t ldn, int64_t tiles,
+                 uint32_t *__restrict__ cnt) {
+  const int64_t seg = blockIdx.y, tile = blockIdx.x;
+  const float *v = sval + seg * ldn;
+  const int64_t r0 = tile * kRunTile;
+  uint32_t c = 0;
+  for (int64_t r = r0 + threadIdx.x; r < r0 + kRunTile && r < n; r += 256)
+    c += (r == 0 || __float_as_uint(v[r]) != __float_as_uint(v[r - 1])) ? 1u : 0u;
+  for (int off = 16; off; off >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, off);
+  __shared__ uint32_t s_c[8];
+  if ((threadIdx.x & 31) == 0) s_c[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < 8; ++w) t += s_c[w];
+    cnt[seg * tiles + tile] = t;
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    k_runs_emit(const float *__restrict__ sval, int64_t n, int64_t ldn, int64_t tiles,
+                const uint32_t *__restrict__ tile_off, float *__restrict__ rvals) {
+  constexpr int ITEMS = kRunTile / 256;
+  const int64_t seg = blockIdx.y, tile = blockIdx.x;
+  const float *v = sval + seg * ldn;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t rt = tile * kRunTile + (int64_t)tid * ITEMS;  // this thread's consecutive rows
+  uint32_t f[ITEMS], cnt = 0;
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const int64_t r = rt + j;
+    f[j] = (r < n && (r == 0 || __float_as_uint(v[r]) != __float_as_uint(v[r - 1]))) ? 1u : 0u;
+    cnt += f[j];
+  }
+  if (!__syncthreads_or(cnt)) return;  // no run starts in this tile
+  uint32_t inc = cnt;  // block exclusive scan of the per-thread counts
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, off);
+    if (lane >= off) inc += y;
+  }
+  __shared__ uint32_t s_w[8];
+  if (lane == 31) s_w[w] = inc;
+  __syncthreads();
+  uint32_t run = tile_off[seg * tiles + tile] + inc - cnt;  // run starts before this thread
+  for (int ww = 0; ww < w; ++ww) run += s_w[ww];
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j)
+    if (f[j]) rvals[seg * 256 + run++] = v[rt + j];
+}
+
+// runid[k][i] = the index of x_ik among rvals[k][0..R_k) (binary search; -0.0 == +0.0 as in
+// the sort's key canonicalisation).  Tiles of 64 points x 32 coordinates of X staged in shared
+// memory (as K0), so X is read in whole rows and runid written in whole segments.
+__global__ void __launch_bounds__(256)
+    k_runs_ids(const float *__restrict__ X, int64_t n, int64_t ldx, int64_t k0, int64_t dl,
+               int64_t ldn, const float *__restrict__ rvals, const uint32_t *__restrict__ nruns,
+               uint8_t *__restrict__ runid) {
+  __shared__ float tile[kT0Points][kT0Coords + 1];
+  __shared__ float s_vals[kT0Coords][256];
+  __shared__ uint32_t s_nr[kT0Coords];
+  const int64_t i0 = (int64_t)blockIdx.x * kT0Points;
+  const int tid = threadIdx.x;
+  for (int64_t kt = 0; kt < dl; kt += kT0Coords) {
+    __syncthreads();
+    for (int e = tid; e < kT0Points * kT0Coords; e += 256) {
+      const int p = e / kT0Coords, c = e % kT0Coords;
+      const int64_t i = i0 + p, k = kt + c;
+      tile[p][c] = (i < n && k < dl) ? X[i * ldx + k0 + k] : 0.0f;
+    }
+    for (int e = tid; e < kT0Coords * 256; e += 256) {
+      const int c = e / 256, j = e % 256;
+      s_vals[c][j] = (kt + c < dl) ? rvals[(kt + c) * 256 + j] : 0.0f;
+    }
+    if (tid < kT0Coords) s_nr[tid] = (kt + tid < dl) ? nruns[kt + tid] : 1u;
+    __syncthreads();
+    for (int e = tid; e < kT0Points * kT0Coords; e += 256) {
+      const int c = e / kT0Points, p = e % kT0Points;
+      const int64_t i = i0 + p, k = kt + c;
+      if (i >= n || k >= dl) continue;
+      const float x = tile[p][c];
+      int lo = 0, hi = (int)s_nr[c] - 1;  // the largest j with rvals[j] <= x (== x: present)
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_vals[c][mid] <= x) lo = mid; else hi = mid - 1;
+      }
+      runid[k * ldn + i] = (uint8_t)lo;
+    }
+  }
+}
+
+int64_t runs_tiles(int64_t n) { return (n + kRunTile - 1) / kRunTile; }
+
+void launch_runs_count(const float *sval, int64_t n, int64_t ldn, int64_t dl, uint32_t *cnt,
+                       cudaStream_t s) {
+  dim3 grid((unsigned)runs_tiles(n), (unsigned)dl);
+  k_runs_count<<<grid, 256, 0, s>>>(sval, n, ldn, runs_tiles(n), cnt);
+}
+
+void launch_runs_emit(const float *sval, int64_t n, int64_t ldn, int64_t dl,
+                      const uint32_t *tile_off, float *rvals, cudaStream_t s) {
+  dim3 grid((unsigned)runs_tiles(n), (unsigned)dl);
+  k_runs_emit<<<grid, 256, 0, s>>>(sval, n, ldn, runs_tiles(n), tile_off, rvals);
+}
+
+void launch_runs_ids(const float *X, int64_t n, int64_t ldx, int64_t k0, int64_t dl, int64_t ldn,
+                     const float *rvals, const uint32_t *nruns, uint8_t *runid, cudaStream_t s) {
+  dim3 grid((unsigned)((n + kT0Points - 1) / kT0Points));
+  k_runs_ids<<<grid, 256, 0, s>>>(X, n, ldx, k0, dl, ldn, rvals, nruns, runid);
+}
+
 }  // namespace l1dm

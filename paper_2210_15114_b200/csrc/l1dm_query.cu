@@ -1239,6 +1239,134 @@ void launch_block_out(const double *yt, int mb, int64_t mc, const double *hsum, 
   k9_block_out<<<(unsigned)blocks, 256, 0, s>>>(yt, mb, mc, hsum, S, g, Y, ldy, i0, i1);
 }
 
+// ------------------------------------------------------------------ runs mode
+// For tie-heavy coordinates (<= 256 distinct values each) Alg. 2 collapses to its distinct
+// values: with H_j = sum of z over run j, P_j / Q_j the exclusive prefixes over runs of H and
+// v H, every point of run j sees U^k = v_j P_j - Q_j (the prefix at any row of a run differs
+// only by equal-value terms, which contribute 0 — P:173 / P:205), so
+//   y_i = 2 sum_k U^k[runid_k(i)] + g - h_i S,  U^k[j] = v_j P_j - Q_j
+// R1  H[k][j][c] += z_ic for j = runid[k][i] (fp64 L2 reductions into an L2-resident table,
+//     points read in point order: no sorted-order gather at all)
+// R2  per (k, c): the prefix over runs, U in place, segment totals (S, T_k) for k4_totals
+// R3  per point tile: U^k staged in shared memory per coordinate, y accumulated in registers.
+__global__ void __launch_bounds__(256)
+    k20_runs_hist(const uint8_t *__restrict__ runid, int64_t ldn, int64_t n, int64_t dl,
+                  const float *__restrict__ Z, int64_t ldz, int64_t m, int kg,
+                  double *__restrict__ H) {
+  // lane -> (point p within the warp's group of 32/L, column c), L = min(32, pow2 >= m)
+  const int L = m >= 32 ? 32 : (m > 16 ? 32 : m > 8 ? 16 : m > 4 ? 8 : m > 2 ? 4 : m > 1 ? 2 : 1);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int pg = lane / L, cl = lane - (lane / L) * L;
+  const int ppw = 32 / L;  // points per warp step
+  const int64_t k0 = (int64_t)blockIdx.y * kg;
+  const int64_t k1 = (k0 + kg < dl) ? k0 + kg : dl;
+  const int64_t pts_per_cta = 8 * ppw * 16;  // 16 steps per warp
+  const int64_t i_base = (int64_t)blockIdx.x * pts_per_cta + (int64_t)w * ppw * 16;
+  const uint64_t pol = l2_policy_evict_last();
+  for (int step = 0; step < 16; ++step) {
+    const int64_t i = i_base + (int64_t)step * ppw + pg;
+    if (i >= n) break;
+    for (int64_t c0 = 0; c0 < m; c0 += L) {
+      const int64_t c = c0 + cl;
+      if (c >= m) continue;
+      const float z = __ldg(Z + i * ldz + c);
+      for (int64_t k = k0; k < k1; ++k) {
+        const uint32_t j = __ldg(runid + k * ldn + i);
+        red_add_f64(H + ((k * 256 + j) * m + c), (double)z, pol);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    k21_runs_scan(double *__restrict__ H, const float *__restrict__ rvals,
+                  const uint32_t *__restrict__ nruns, int64_t dl, int64_t m,
+                  double *__restrict__ segtot) {
+  const int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (e >= dl * m) return;
+  const int64_t k = e / m, c = e - (e / m) * m;
+  const uint32_t R = nruns[k];
+  double P = 0.0, Q = 0.0;
+  for (uint32_t j = 0; j < R; ++j) {
+    double *hp = H + (k * 256 + j) * m + c;
+    const double h = *hp, v = (double)rvals[k * 256 + j];
+    *hp = fma(v, P, -Q);  // U at run j (exclusive prefixes)
+    P += h;
+    Q = fma(v, h, Q);
+  }
+  segtot[k * 2 * m + 2 * c] = P;      // S_c (every coordinate's total of z)
+  segtot[k * 2 * m + 2 * c + 1] = Q;  // T_kc
+}
+
+// grid: point tiles of 256 points x column chunks of MC; block 256 threads; thread (p, c):
+// p = tid / MC + (256 / MC) u for u < MC, c = c0 + tid % MC.
+template <int MC>
+__global__ void __launch_bounds__(256)
+    k22_runs_expand(const uint8_t *__restrict__ runid, int64_t ldn, int64_t n, int64_t dl,
+                    const double *__restrict__ U, const uint32_t *__restrict__ nruns, int64_t m,
+                    const double *__restrict__ hsum, const double *__restrict__ Sg,
+                    double *__restrict__ Y, int64_t ldy, int64_t i_begin) {
+  constexpr int PT = 256;               // points per CTA
+  constexpr int PPP = 256 / MC;         // points per pass of the CTA's threads
+  constexpr int NP = PT / PPP;          // points per thread (= MC)
+  __shared__ double us[256 * MC];       // U^k[j][c0 .. c0 + MC)
+  const int tid = threadIdx.x;
+  const int cl = tid % MC, pr = tid / MC;
+  const int64_t i0 = i_begin + (int64_t)blockIdx.x * PT, c0 = (int64_t)blockIdx.y * MC;
+  const int64_t c = c0 + cl;
+  double acc[NP];
+#pragma unroll
+  for (int u = 0; u < NP; ++u) acc[u] = 0.0;
+  for (int64_t k = 0; k < dl; ++k) {
+    const int R = (int)nruns[k];
+    __syncthreads();
+    for (int e = tid; e < R * MC; e += 256) {
+      const int j = e / MC, q = e - (e / MC) * MC;
+      us[e] = (c0 + q < m) ? __ldg(U + (k * 256 + j) * m + c0 + q) : 0.0;
+    }
+    __syncthreads();
+    const uint8_t *rk = runid + k * ldn;
+#pragma unroll
+    for (int u = 0; u < NP; ++u) {
+      const int64_t i = i0 + pr + (int64_t)PPP * u;
+      if (i < n) acc[u] += us[(int)__ldg(rk + i) * MC + cl];
+    }
+  }
+  if (c >= m) return;
+#pragma unroll
+  for (int u = 0; u < NP; ++u) {
+    const int64_t i = i0 + pr + (int64_t)PPP * u;
+    if (i < n) Y[i * ldy + c] = 2.0 * acc[u] + fma(-hsum[i], Sg[c], Sg[m + c]);
+  }
+}
+
+void launch_runs_query(const uint8_t *runid, int64_t ldn, int64_t n, int64_t dl, const float *rvals,
+                       const uint32_t *nruns, const float *Z, int64_t ldz, int64_t m, double *H,
+                       double *segtot, const double *hsum, double *Sg, double *Y, int64_t ldy,
+                       int phase, cudaStream_t s, int64_t i0, int64_t i1) {
+  if (phase == 0) {
+    cudaMemsetAsync(H, 0, (size_t)dl * 256 * m * sizeof(double), s);
+    const int L = m >= 32 ? 32 : (m > 16 ? 32 : m > 8 ? 16 : m > 4 ? 8 : m > 2 ? 4 : m > 1 ? 2 : 1);
+    const int64_t pts_per_cta = 8 * (32 / L) * 16;
+    const int kg = 8;
+    dim3 g1((unsigned)((n + pts_per_cta - 1) / pts_per_cta), (unsigned)((dl + kg - 1) / kg));
+    k20_runs_hist<<<g1, 256, 0, s>>>(runid, ldn, n, dl, Z, ldz, m, kg, H);
+    const int64_t t2 = dl * m;
+    k21_runs_scan<<<(unsigned)((t2 + 255) / 256), 256, 0, s>>>(H, rvals, nruns, dl, m, segtot);
+    return;
+  }
+  // phase 1: expand (Sg = S, g from the segment totals, computed by the caller)
+  if (i1 < 0) i1 = n;
+  if (i1 <= i0) return;
+  auto run = [&](auto kern, int MC) {  // points [i0, i1): the kernel bounds rows by i1 via n
+    dim3 g3((unsigned)((i1 - i0 + 255) / 256), (unsigned)((m + MC - 1) / MC));
+    kern<<<g3, 256, 0, s>>>(runid, ldn, i1, dl, H, nruns, m, hsum, Sg, Y, ldy, i0);
+  };
+  if (m <= 4) run(k22_runs_expand<4>, 4);
+  else if (m <= 8) run(k22_runs_expand<8>, 8);
+  else run(k22_runs_expand<16>, 16);
+}
+
 // Y[i][c] = Yb[c / mb][i][c % mb]: column-block-major (l1dm_matvec_colblocks) to row-major.
 __global__ void __launch_bounds__(256)
     k10_unblock(const double *__restrict__ Yb, int64_t n, int64_t m, int64_t mb,
