@@ -40,12 +40,13 @@ def test_random_float_vs_brute(n, d, m):
     assert col_rel_l2(Yg, Yr) <= TOL
 
 
+@pytest.mark.parametrize("mode", ["gather", "scatter", "runs", "auto"])
 @pytest.mark.parametrize("n,d,m", [(4099, 3, 1), (3000, 4, 4), (2500, 2, 7), (1500, 3, 32)])
-def test_integer_ties_exact(n, d, m):
+def test_integer_ties_exact(n, d, m, mode):
     rng = np.random.default_rng(7 * n + m)
     X = rng.integers(0, 5, size=(n, d)).astype(np.float32)
     Z = rng.integers(-3, 4, size=(n, m)).astype(np.float32)
-    Yg = gpu_matvec(X, Z)
+    Yg = gpu_matvec(X, Z, mode=mode)
     assert np.array_equal(Yg, oracle.hist(X, Z, M=4).astype(np.float64))
 
 
@@ -107,7 +108,7 @@ def test_coordinate_shards_sum_to_whole():
     rng = np.random.default_rng(15)
     X = rng.integers(0, 9, size=(4000, 7)).astype(np.float32)
     Z = rng.integers(-2, 3, size=(4000, 3)).astype(np.float32)
-    parts = [gpu_matvec(X, Z, a, b) for a, b in [(0, 2), (2, 3), (3, 7)]]
+    parts = [gpu_matvec(X, Z, a, b, mode="gather") for a, b in [(0, 2), (2, 3), (3, 7)]]
     whole = oracle.hist(X, Z, M=8).astype(np.float64)
     assert np.array_equal(sum(parts), whole)
     assert np.array_equal(parts[1], oracle.hist(X[:, 2:3], Z, M=8).astype(np.float64))
@@ -153,9 +154,9 @@ def sample_rows(n, Y=None, count=24, seed=0):
 @pytest.mark.slow
 @pytest.mark.parametrize("name,mode", [("c1", "auto"), ("c2", "auto"), ("c3", "auto"),
                                        ("c4", "auto"), ("c5", "auto"), ("c3", "gather"),
-                                       ("c2", "gather")])
+                                       ("c2", "gather"), ("c5", "gather")])
 def test_workload_full_size_sampled(name, mode):
-    """Auto is the bench's launch configuration (c2, c3: scatter mode; c4, c5: gather)."""
+    """Auto is the bench's launch configuration (c2, c3: scatter; c4: gather; c5: runs)."""
     w = wl.workload(name)
     X = wl.make_points(w, "cuda")
     Z = wl.make_query(w, 0, "cuda")
@@ -235,6 +236,7 @@ def test_scatter_mode_host_pointers_and_plan():
     p = l1.l1dm_plan(20000, 3, 1)
     assert p["scatter"] == 1
     h = l1.l1dm_prepare(X)                           # host X
+    l1.l1dm_set_query_mode(h, "scatter")            # (integer data would pick runs mode)
     Y = l1.l1dm_matvec(h, Z)                         # host Z, host Y
     assert np.array_equal(Y.numpy(), oracle.hist(X, Z, M=5).astype(np.float64))
     l1.l1dm_free(h)
@@ -245,7 +247,7 @@ def test_more_coordinates_than_one_chunk_exactly():
     rng = np.random.default_rng(78)
     X = rng.integers(0, 256, size=(30000, 9)).astype(np.float32)
     Z = (2 * rng.integers(0, 2, size=(30000, 16)) - 1).astype(np.float32)
-    Yg = gpu_matvec(X, Z, ws_limit=3 * 30000 * 16 * 8)
+    Yg = gpu_matvec(X, Z, ws_limit=3 * 30000 * 16 * 8, mode="gather")
     assert np.array_equal(Yg, oracle.hist(X, Z, M=255).astype(np.float64))
 
 
