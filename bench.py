@@ -250,6 +250,7 @@ def main_ours(args):
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     timings = []
+    hl0 = l1.l1dm_handleless_launches()
     ev0.record(stream)
     for s in range(args.steps):
         sh = one_step(timing=True)
@@ -257,6 +258,7 @@ def main_ours(args):
             timings.append(l1.l1dm_timing_read(sh.handle))  # syncs the stream (host only)
         sh.close()
     ev1.record(stream)
+    hl_launches = l1.l1dm_handleless_launches() - hl0
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -412,7 +414,7 @@ def main_ours(args):
                    "query": "l1" if args.p == 1 else f"lp^p, p={args.p}",
                    "columns_per_block": plan["mb"],
                    "l2": "inputs > L2 (prepared state 12*n*d B), no flush"},
-        "gpu_launches": int(agg.get("kernel_launches", 0)),
+        "gpu_launches": int(agg.get("kernel_launches", 0)) + hl_launches,
         "prepare_ms": prep_ms,
         "query_ms": (ms_step - (prep_ms or 0.0)) / Q,
         "query_kernel_ms": query_kernel_ms,

@@ -302,6 +302,11 @@ L1DM_API l1dm_status l1dm_release_cached(void);
 /* Thread-local message describing the last non-OK status ("" if none). */
 L1DM_API const char *l1dm_last_error(void);
 
+/* Kernels launched so far (this process, all devices) by the handle-free entries
+ * (l1dm_lpp_even_matvec, l1dm_bilinear_matvec, l1dm_l2_embed); handle-bound launches are
+ * counted per handle in l1dm_timing_t.kernel_launches.  Never fails. */
+L1DM_API int64_t l1dm_handleless_launches(void);
+
 /* Library version string. */
 L1DM_API const char *l1dm_version(void);
 

@@ -33,7 +33,7 @@ EXPORTS = [
     "l1dm_free", "l1dm_sync",
     "l1dm_shape", "l1dm_workspace_bytes", "l1dm_set_workspace_limit", "l1dm_set_query_mode",
     "l1dm_plan", "l1dm_plan_ex", "l1dm_timing_enable", "l1dm_timing_read", "l1dm_debug_export", "l1dm_release_cached",
-    "l1dm_last_error", "l1dm_version",
+    "l1dm_last_error", "l1dm_handleless_launches", "l1dm_version",
 ]
 
 
@@ -109,6 +109,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.l1dm_release_cached.restype = st
     lib.l1dm_last_error.argtypes = []
     lib.l1dm_last_error.restype = ctypes.c_char_p
+    lib.l1dm_handleless_launches.argtypes = []
+    lib.l1dm_handleless_launches.restype = i64
     lib.l1dm_version.argtypes = []
     lib.l1dm_version.restype = ctypes.c_char_p
     for name in ("l1dm_prepare", "l1dm_prepare_ex", "l1dm_matvec", "l1dm_matvec_ex",
@@ -448,6 +450,11 @@ def l1dm_debug_export(h: Handle):
 def l1dm_release_cached():
     """Return cached device blocks of freed handles to CUDA (current device)."""
     _check(load_library().l1dm_release_cached(), "l1dm_release_cached")
+
+
+def l1dm_handleless_launches() -> int:
+    """Kernels launched so far by the handle-free entries (even p, bilinear, l2 embed)."""
+    return int(load_library().l1dm_handleless_launches())
 
 
 def l1dm_version() -> str:

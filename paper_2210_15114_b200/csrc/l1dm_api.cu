@@ -4,6 +4,7 @@
 // host<->device staging for host pointers, per-kernel event timing and error mapping.
 // Every compute step runs in the kernels of l1dm_prepare.cu / l1dm_query.cu; there
 // is no host (CPU) evaluation path.
+#include <atomic>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1154,6 +1155,8 @@ l1dm_status l1dm_tv_matvec(l1dm_handle h, const float *Z, int64_t m, double *Y) 
 
 namespace {
 
+std::atomic<int64_t> g_handleless_launches{0};
+
 // Shared by the handle-free sort-free entries: argument checks, host staging through the
 // stream-ordered allocator, the launch, the copy back.  M (bilinear only): d x d fp64.
 l1dm_status sortfree_entry(const float *X, int64_t n, int64_t ld_x, int64_t d, int p,
@@ -1222,10 +1225,12 @@ l1dm_status sortfree_entry(const float *X, int64_t n, int64_t ld_x, int64_t d, i
     return fail(e == cudaErrorMemoryAllocation ? L1DM_ENOMEM : L1DM_ECUDA, "sort-free setup: %s",
                 cudaGetErrorString(e));
   }
-  if (bilinear)
-    launch_bilinear(Xd, ldxd, Md, Zd, ldzd, n, d, m, Yd, ldyd, static_cast<double *>(ws), sms, s);
-  else
-    launch_lpp_even(Xd, ldxd, Zd, ldzd, n, d, m, p, Yd, ldyd, static_cast<double *>(ws), sms, s);
+  g_handleless_launches +=
+      bilinear
+          ? launch_bilinear(Xd, ldxd, Md, Zd, ldzd, n, d, m, Yd, ldyd, static_cast<double *>(ws),
+                            sms, s)
+          : launch_lpp_even(Xd, ldxd, Zd, ldzd, n, d, m, p, Yd, ldyd, static_cast<double *>(ws),
+                            sms, s);
   e = cudaGetLastError();
   if (e == cudaSuccess && !ydev)
     e = copy_rows(Y, (size_t)ld_y * sizeof(double), Yd, (size_t)m * sizeof(double),
@@ -1267,7 +1272,7 @@ l1dm_status l1dm_l2_embed(const float *X, int64_t n, int64_t ld_x, int64_t d, co
   if (!is_device_pointer(X) || !is_device_pointer(G) || !is_device_pointer(Xp))
     return fail(L1DM_EINVAL, "l1dm_l2_embed needs device X, G and Xp");
   cudaStream_t s = (cudaStream_t)stream;
-  launch_embed(X, ld_x, n, d, G, d, k, Xp, ld_p, s);
+  g_handleless_launches += launch_embed(X, ld_x, n, d, G, d, k, Xp, ld_p, s);
   CUDA_TRY(cudaGetLastError());
   return L1DM_OK;
 }
@@ -1500,6 +1505,8 @@ l1dm_status l1dm_release_cached(void) {
 }
 
 const char *l1dm_last_error(void) { return g_err.c_str(); }
+
+int64_t l1dm_handleless_launches(void) { return g_handleless_launches.load(); }
 
 const char *l1dm_version(void) { return "l1dm 0.1.0 (sm_100a)"; }
 

@@ -173,18 +173,18 @@ void launch_simplex_stats(const double *hsum, int64_t n, const float *sval, int6
 // ws: lpp_even_workspace() bytes of device memory.
 size_t lpp_even_workspace(int64_t n, int64_t d, int64_t m, int p, int64_t *nchunks_out,
                           int64_t *chunk_out, int sms);
-void launch_lpp_even(const float *X, int64_t ldx, const float *Z, int64_t ldz, int64_t n,
+int launch_lpp_even(const float *X, int64_t ldx, const float *Z, int64_t ldz, int64_t n,
                      int64_t d, int64_t m, int p, double *Y, int64_t ldy, double *ws, int sms,
                      cudaStream_t s);
 
 // Thm. maha's bilinear form f(x, y) = x^T M y (M: d x d fp64 row-major, device): Y = X M X^T Z.
 size_t bilinear_workspace(int64_t n, int64_t d, int64_t m, int sms);
-void launch_bilinear(const float *X, int64_t ldx, const double *M, const float *Z, int64_t ldz,
+int launch_bilinear(const float *X, int64_t ldx, const double *M, const float *Z, int64_t ldz,
                      int64_t n, int64_t d, int64_t m, double *Y, int64_t ldy, double *ws, int sms,
                      cudaStream_t s);
 
 // Thm. l2embed: Xp (n x k fp32, ldp) = X G^T / (beta k), beta = sqrt(2/pi); G: k x d fp32.
-void launch_embed(const float *X, int64_t ldx, int64_t n, int64_t d, const float *G, int64_t ldg,
+int launch_embed(const float *X, int64_t ldx, int64_t n, int64_t d, const float *G, int64_t ldg,
                   int64_t k, float *Xp, int64_t ldp, cudaStream_t s);
 
 }  // namespace l1dm

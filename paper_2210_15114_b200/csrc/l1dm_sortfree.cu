@@ -351,11 +351,12 @@ __global__ void __launch_bounds__(256)
 
 }  // namespace
 
-void launch_embed(const float *X, int64_t ldx, int64_t n, int64_t d, const float *G, int64_t ldg,
-                  int64_t k, float *Xp, int64_t ldp, cudaStream_t s) {
+int launch_embed(const float *X, int64_t ldx, int64_t n, int64_t d, const float *G, int64_t ldg,
+                 int64_t k, float *Xp, int64_t ldp, cudaStream_t s) {
   const double beta = 0.79788456080286535588;  // sqrt(2 / pi)
   dim3 grid((unsigned)((n + kTile - 1) / kTile), (unsigned)((k + kTile - 1) / kTile));
   k16_embed<<<grid, 256, 0, s>>>(X, ldx, n, d, G, ldg, k, 1.0 / (beta * (double)k), Xp, ldp);
+  return 1;
 }
 
 size_t bilinear_workspace(int64_t n, int64_t d, int64_t m, int sms) {
@@ -365,9 +366,9 @@ size_t bilinear_workspace(int64_t n, int64_t d, int64_t m, int sms) {
 
 // Thm. maha: f(x, y) = x^T M y, A = X M X^T, Y = X (M (X^T Z)): Alg. 7's S = M X^T
 // is never formed; W = X^T Z (k12 at p = 1), V = M W (k15), Y = X V (k14 with S = G = 0).
-void launch_bilinear(const float *X, int64_t ldx, const double *M, const float *Z, int64_t ldz,
-                     int64_t n, int64_t d, int64_t m, double *Y, int64_t ldy, double *ws, int sms,
-                     cudaStream_t s) {
+int launch_bilinear(const float *X, int64_t ldx, const double *M, const float *Z, int64_t ldz,
+                    int64_t n, int64_t d, int64_t m, double *Y, int64_t ldy, double *ws, int sms,
+                    cudaStream_t s) {
   int64_t nchunks = 1, chunk = n;
   lpp_even_workspace(n, d, m, 1, &nchunks, &chunk, sms);
   double *part = ws;
@@ -391,6 +392,7 @@ void launch_bilinear(const float *X, int64_t ldx, const double *M, const float *
   cudaFuncSetAttribute(k14_moment_expand_dmma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sm14);
   k14_moment_expand_dmma<2><<<g14, 256, sm14, s>>>(X, ldx, n, d, m, V, S, G, Y, ldy);
+  return 5;  // k12, k13 fold, k15 gemm, k15 zero, k14
 }
 
 size_t lpp_even_workspace(int64_t n, int64_t d, int64_t m, int p, int64_t *nchunks_out,
@@ -408,9 +410,9 @@ size_t lpp_even_workspace(int64_t n, int64_t d, int64_t m, int p, int64_t *nchun
   return ((size_t)nchunks * p * d * m + (size_t)p * d * m + 2 * (size_t)m) * sizeof(double);
 }
 
-void launch_lpp_even(const float *X, int64_t ldx, const float *Z, int64_t ldz, int64_t n,
-                     int64_t d, int64_t m, int p, double *Y, int64_t ldy, double *ws, int sms,
-                     cudaStream_t s) {
+int launch_lpp_even(const float *X, int64_t ldx, const float *Z, int64_t ldz, int64_t n,
+                    int64_t d, int64_t m, int p, double *Y, int64_t ldy, double *ws, int sms,
+                    cudaStream_t s) {
   int64_t nchunks = 1, chunk = n;
   lpp_even_workspace(n, d, m, p, &nchunks, &chunk, sms);
   double *part = ws;
@@ -438,8 +440,9 @@ void launch_lpp_even(const float *X, int64_t ldx, const float *Z, int64_t ldz, i
     case 2: expand(k14_moment_expand_dmma<2>, 2); break;
     case 4: expand(k14_moment_expand_dmma<4>, 4); break;
     case 6: expand(k14_moment_expand_dmma<6>, 6); break;
-    default: break;
+    default: return 3;
   }
+  return 4;  // k12, k13 fold, k13 colsum, k14
 }
 
 }  // namespace l1dm

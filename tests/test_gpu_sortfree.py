@@ -90,3 +90,18 @@ def test_bilinear_random_vs_oracle(n, d, m):
     Yr = oracle.brute_bilinear(X, M, Z)
     scale = float(np.abs(X).sum(1).max() ** 2 * np.abs(M).max() * np.abs(Z).sum(0).max())
     assert col_rel_l2(Yg.cpu().numpy(), Yr, floor=1e-6 * scale) <= 1e-9
+
+
+def test_handleless_launch_counter():
+    """The handle-free entries count their kernels (bench.py's gpu_launches for even p)."""
+    X = torch.randn(300, 9, device="cuda")
+    Z = torch.randn(300, 4, device="cuda")
+    c0 = l1.l1dm_handleless_launches()
+    l1.l1dm_lpp_even_matvec(X, 2, Z)
+    c1 = l1.l1dm_handleless_launches()
+    l1.l1dm_bilinear_matvec(X, torch.eye(9, dtype=torch.float64, device="cuda"), Z)
+    c2 = l1.l1dm_handleless_launches()
+    l1.l1dm_l2_embed(X, torch.randn(16, 9, device="cuda"))
+    c3 = l1.l1dm_handleless_launches()
+    torch.cuda.synchronize()
+    assert (c1 - c0, c2 - c1, c3 - c2) == (4, 5, 1)
