@@ -58,11 +58,17 @@ void launch_runs_ids(const float *X, int64_t n, int64_t ldx, int64_t k0, int64_t
 #ifndef L1DM_M1_ITEMS
 #define L1DM_M1_ITEMS 32
 #endif
+// Stage budget (bytes of gathered Z + sval + perm per tile).  Measured on B200 (c4, c3 gather,
+// c5 gather): 64 KiB for one-row-per-warp-step tiles (lpr = 32: 3 CTAs per SM, fewer look-backs
+// than 4 smaller CTAs), 96 KiB otherwise.
+#ifndef L1DM_SCAN_SMEM
+#define L1DM_SCAN_SMEM(lpr) ((lpr) == 32 ? 65536 : 98304)
+#endif
 __host__ __device__ constexpr int scan_items(int lpr, int vc) {
   return (lpr == 1 && vc == 1) ? 16 : lpr == 1 ? L1DM_M1_ITEMS
-                  : ((98304 / (1024 * vc + 2048 / lpr)) / 4 * 4 > 64
+                  : ((L1DM_SCAN_SMEM(lpr) / (1024 * vc + 2048 / lpr)) / 4 * 4 > 64
                          ? 64
-                         : (98304 / (1024 * vc + 2048 / lpr)) / 4 * 4);
+                         : (L1DM_SCAN_SMEM(lpr) / (1024 * vc + 2048 / lpr)) / 4 * 4);
 }
 // Largest query workspace chunk (U + look-back state) in bytes.
 constexpr size_t kMaxChunkBytes = (size_t)72 << 30;

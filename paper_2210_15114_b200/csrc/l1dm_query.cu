@@ -524,6 +524,30 @@ __global__ void __launch_bounds__(256, 2)
     Q[q] = s_excl[c2 + 1] + s_wt[w * NP + c2 + 1];
   }
   double *ub = U + kk * n * ldu + (row0 + rbase) * ldu + col;
+  if constexpr (RPW == 1) {
+    // one row per warp step (a lane per column group): the exclusive prefixes are the carries
+    const int nmine = (int)(nrows - rbase < ITEMS ? (nrows - rbase < 0 ? 0 : nrows - rbase)
+                                                  : ITEMS);
+    const float *zr = zb + rbase * MB + cl * VC;
+    const float *vr = vb + rbase;
+    if (col_ok) {
+#pragma unroll 4
+      for (int j = 0; j < nmine; ++j) {
+        float zz[VC];
+        lds_cols<VC>(zr + j * MB, zz);
+        const double vj = (double)vr[j];
+        double u[VC];
+#pragma unroll
+        for (int q = 0; q < VC; ++q) {
+          const double sz = (double)zz[q];
+          u[q] = fma(vj, P[q], -Q[q]);  // U_r = v_r P_r - Q_r
+          P[q] += sz;
+          Q[q] = fma(vj, sz, Q[q]);     // v z is exact in fp64: same as Q + v z
+        }
+        stcs_cols<VC>(ub + (int64_t)j * ldu, u);
+      }
+    }
+  } else {
 #pragma unroll 4
   for (int j = 0; j < ITEMS; ++j) {
     const int r = rbase + j * RPW;
@@ -552,6 +576,7 @@ __global__ void __launch_bounds__(256, 2)
     if (col_ok && r < nrows) {
       stcs_cols<VC>(ub + (int64_t)j * RPW * ldu, u);
     }
+  }
   }
 }
 
