@@ -251,9 +251,12 @@ def main_ours(args):
     ev1 = torch.cuda.Event(enable_timing=True)
     timings = []
     hl0 = l1.l1dm_handleless_launches()
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
     ev0.record(stream)
     for s in range(args.steps):
+        step_ev[2 * s].record(stream)
         sh = one_step(timing=True)
+        step_ev[2 * s + 1].record(stream)
         if sh.handle is not None and args.p % 2 == 1:
             timings.append(l1.l1dm_timing_read(sh.handle))  # syncs the stream (host only)
         sh.close()
@@ -264,6 +267,7 @@ def main_ours(args):
         dist.barrier()
     clk = clocks.stop() if rank == 0 else None
     ms_total = ev0.elapsed_time(ev1)
+    step_ms = [step_ev[2 * s].elapsed_time(step_ev[2 * s + 1]) for s in range(args.steps)]
     t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -416,6 +420,14 @@ def main_ours(args):
                    "l2": "inputs > L2 (prepared state 12*n*d B), no flush"},
         "gpu_launches": int(agg.get("kernel_launches", 0)) + hl_launches,
         "prepare_ms": prep_ms,
+        # prepare as keys/s and GB/s against the 16-B compulsory and 76-B pass
+        # models (per key: X read + sval/perm/rank write; keys, histogram, 4 radix passes, ranks)
+        "prepare": ({"keys_per_s": n * dl / (prep_ms * 1e-3),
+                     "GBps_16B_model": 16.0 * n * dl / (prep_ms * 1e-3) / 1e9,
+                     "GBps_76B_model": 76.0 * n * dl / (prep_ms * 1e-3) / 1e9,
+                     "frac_76B_of_hbm_peak": 76.0 * n * dl / (prep_ms * 1e-3) / 1e9 / hbm_peak}
+                    if prep_ms else None),
+        "step_ms_each": step_ms,
         "query_ms": (ms_step - (prep_ms or 0.0)) / Q,
         "query_kernel_ms": query_kernel_ms,
         "kernels": kern,

@@ -69,6 +69,10 @@ class BlockCache {
     static BlockCache c;
     return c;
   }
+  static bool debug() {
+    static const bool d = getenv("L1DM_DEBUG_ALLOC") != nullptr;
+    return d;
+  }
   cudaError_t alloc(void **p, size_t bytes) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -86,7 +90,12 @@ class BlockCache {
       }
     }
     const size_t rounded = bytes;
+    const auto t0 = std::chrono::steady_clock::now();
     cudaError_t e = cudaMalloc(p, rounded);
+    if (debug())
+      fprintf(stderr, "[l1dm] cudaMalloc %zu B: %.3f ms\n", rounded,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                  .count());
     if (e == cudaErrorMemoryAllocation) {
       cudaGetLastError();
       release_all(dev);
@@ -117,6 +126,7 @@ class BlockCache {
       limit_[dev] = tot / 2;
     }
     if (cached_[dev] + bytes > limit_[dev]) {
+      if (debug()) fprintf(stderr, "[l1dm] cache full: cudaFree %zu B\n", bytes);
       cudaFree(p);
       return;
     }
@@ -145,9 +155,23 @@ template <typename T>
 struct DevBuf {
   T *p = nullptr;
   size_t count = 0;
+  cudaStream_t s_last = nullptr;  // stream of the latest ensure (the block's user)
+  DevBuf() = default;
+  DevBuf(const DevBuf &) = delete;
+  DevBuf &operator=(const DevBuf &) = delete;
+  // a block still held at scope exit (a function-local buffer, an early error return) goes
+  // back to the cache once its stream is idle — never leaked, never reused while in use
+  ~DevBuf() {
+    if (p) {
+      cudaStreamSynchronize(s_last);
+      release();
+    }
+  }
   cudaError_t ensure(size_t c, bool zero, cudaStream_t s) {
+    s_last = s;
     if (c <= count && p) return cudaSuccess;
     if (p) {
+      if (BlockCache::debug()) fprintf(stderr, "[l1dm] grow %zu -> %zu elems (sync)\n", count, c);
       cudaStreamSynchronize(s);  // queued work on s may still use the old block
       BlockCache::get().free(p);
       p = nullptr;
@@ -553,6 +577,7 @@ l1dm_status prepare_impl(const float *X, int64_t n, int64_t ld_x, int64_t k_begi
         h->has_runs = true;
       }
       CUDA_TRY(cudaStreamSynchronize(s));  // rcnt and the host vectors go out of scope
+      rcnt.release();
     }
   }
   lap("runs");
@@ -593,14 +618,25 @@ l1dm_status ensure_plan(l1dm_ctx *h, int64_t m, int vec_cap) {
       h->plan_mode == h->mode)
     return L1DM_OK;
   size_t ws = h->ws_limit;
+  QueryPlan p;
   if (ws == 0) {
-    size_t fr = 0, tot = 0;
-    CUDA_TRY(cudaMemGetInfo(&fr, &tot));
-    ws = (size_t)(0.75 * (double)(fr + BlockCache::get().cached(h->device) +
-                                 h->U.count * sizeof(double) + h->agg.count * sizeof(double) * 2));
+    // A plan whose whole workspace is small (scatter mode, runs, narrow gathers) does not depend
+    // on the free memory: take it without the probe — cudaMemGetInfo occasionally stalls the
+    // host for milliseconds (measured: up to 7 ms on B200), idling the GPU on a new handle's
+    // first query.  An allocation that still fails flushes the block cache and retries.
+    constexpr size_t kNoProbeBytes = (size_t)2 << 30;
+    if (make_plan(h->n, h->dl, m, h->l2_bytes, (int64_t)kNoProbeBytes, vec_cap, h->mode, &p) &&
+        p.chunks == 1 && p.workspace_bytes <= kNoProbeBytes) {
+      ws = kNoProbeBytes;
+    } else {
+      size_t fr = 0, tot = 0;
+      CUDA_TRY(cudaMemGetInfo(&fr, &tot));
+      ws = (size_t)(0.75 * (double)(fr + BlockCache::get().cached(h->device) +
+                                   h->U.count * sizeof(double) +
+                                   h->agg.count * sizeof(double) * 2));
+    }
   }
   if (h->plan_m == m && h->plan_ws == ws && h->plan_vec_cap == vec_cap) return L1DM_OK;
-  QueryPlan p;
   if (!make_plan(h->n, h->dl, m, h->l2_bytes, (int64_t)ws, vec_cap, h->mode, &p))
     return fail(L1DM_EINVAL, "no query plan for n=%lld d=%lld m=%lld", (long long)h->n,
                 (long long)h->dl, (long long)m);
@@ -668,8 +704,13 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
     h->m_last = m;
     return L1DM_OK;
   }
+  const auto dbg_t0 = std::chrono::steady_clock::now();
   l1dm_status st = ensure_plan(h, m, vec_cap_for(Z, ldz));
   if (st != L1DM_OK) return st;
+  if (BlockCache::debug())
+    fprintf(stderr, "[l1dm] ensure_plan %.3f ms\n",
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - dbg_t0)
+                .count());
   const QueryPlan &p = h->plan;
   if (!p.scatter) CUDA_TRY(h->U.ensure((size_t)p.kc * (size_t)h->n * (size_t)p.ldu, false, s));
   if (p.mb == 1) CUDA_TRY(h->zs.ensure((size_t)p.kc * (size_t)h->ldn, false, s));
@@ -686,6 +727,10 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
     CUDA_TRY(h->zt.ensure((size_t)p.zt_floats, false, s));
     CUDA_TRY(h->yt.ensure((size_t)h->n * p.mb, false, s));
   }
+  if (BlockCache::debug())
+    fprintf(stderr, "[l1dm] plan + workspace %.3f ms\n",
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - dbg_t0)
+                .count());
   if (p.scatter && m == 1) {
     // scatter mode, m == 1: zero Y, reduce/prefix/apply over every coordinate adding 2U into Y,
     // then the epilogue g - h_i S
@@ -843,13 +888,19 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
 l1dm_status lp_device(l1dm_ctx *h, int lp, const float *Z, int64_t ldz, int64_t m, double *Y,
                       int64_t ldy, cudaStream_t s) {
   size_t ws = h->ws_limit;
-  if (ws == 0) {
-    size_t fr = 0, tot = 0;
-    CUDA_TRY(cudaMemGetInfo(&fr, &tot));
-    ws = (size_t)(0.75 * (double)(fr + BlockCache::get().cached(h->device) +
-                                 h->U.count * sizeof(double)));
-  }
   QueryPlan p;
+  if (ws == 0) {  // the free-memory probe only when the workspace is large (see ensure_plan)
+    constexpr size_t kNoProbeBytes = (size_t)2 << 30;
+    if (make_lp_plan(h->n, h->dl, m, lp, h->l2_bytes, (int64_t)kNoProbeBytes, h->mode, &p) &&
+        p.chunks == 1 && p.workspace_bytes <= kNoProbeBytes) {
+      ws = kNoProbeBytes;
+    } else {
+      size_t fr = 0, tot = 0;
+      CUDA_TRY(cudaMemGetInfo(&fr, &tot));
+      ws = (size_t)(0.75 * (double)(fr + BlockCache::get().cached(h->device) +
+                                   h->U.count * sizeof(double)));
+    }
+  }
   if (!make_lp_plan(h->n, h->dl, m, lp, h->l2_bytes, (int64_t)ws, h->mode, &p))
     return fail(L1DM_EINVAL, "no l_p plan for p=%d n=%lld d=%lld m=%lld", lp, (long long)h->n,
                 (long long)h->dl, (long long)m);

@@ -18,7 +18,13 @@ constexpr uint32_t kSpinLimit = 1u << 26;
 
 // ---------------- prepare (Alg. 1) ----------------
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 8;                           // keys per thread per onesweep tile
+#ifndef L1DM_SORT_ITEMS
+#define L1DM_SORT_ITEMS 8
+#endif
+#ifndef L1DM_SORT_MINB
+#define L1DM_SORT_MINB 3  // 3 CTAs per SM (85 registers, no spills): ~10% faster passes on B200
+#endif
+constexpr int kSortItems = L1DM_SORT_ITEMS;             // keys per thread per onesweep tile
 constexpr int kSortTile = kSortThreads * kSortItems;    // 4096 keys
 constexpr int kHistChunk = 16384;                       // keys per histogram CTA
 

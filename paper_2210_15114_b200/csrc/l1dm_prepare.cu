@@ -120,7 +120,7 @@ __device__ __forceinline__ unsigned long long pack_status(uint32_t flag, uint32_
 }
 
 template <bool FIRST, bool LAST>
-__global__ void __launch_bounds__(kSortThreads)
+__global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
     k2_pass(const uint32_t *__restrict__ kin, const uint32_t *__restrict__ vin,
             uint32_t *__restrict__ kout, uint32_t *__restrict__ vout, uint32_t *__restrict__ rank,
             int64_t n, int64_t ldn, int64_t nseg, int64_t tiles_per_seg, int shift,
@@ -165,32 +165,33 @@ __global__ void __launch_bounds__(kSortThreads)
   }
   // ---- warp multisplit: stable rank of each key among equal digits of its warp
   const uint32_t lt = lanemask_lt();
+  // lanes holding the same digit: 8 ballots (one per digit bit) — MATCH.ANY's latency made it
+  // the top stall of this kernel on sm_100a (ncu short_scoreboard).  The ballots of all items
+  // are independent (issued back to back); only the per-warp digit counters form a chain.
+  uint32_t peers[kSortItems];
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
-    const int64_t idx = wbase + j * 32 + lane;
-    const bool valid = idx < n;
-    const uint32_t vmask = __ballot_sync(0xFFFFFFFFu, valid);
-    // lanes holding the same digit: 8 ballots (one per digit bit) — MATCH.ANY's latency made
-    // it the top stall of this kernel on sm_100a (ncu short_scoreboard)
+    const bool valid = wbase + j * 32 + lane < n;
     const uint32_t dgt = (keys[j] >> shift) & 255u;
-    uint32_t peers = vmask;
+    uint32_t pm = __ballot_sync(0xFFFFFFFFu, valid);
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
       const uint32_t bit = (dgt >> b) & 1u;
       const uint32_t bal = __ballot_sync(0xFFFFFFFFu, bit);
-      peers &= bit ? bal : ~bal;
+      pm &= bit ? bal : ~bal;
     }
-    if (valid) {
-      const int leader = __ffs(peers) - 1;
+    peers[j] = valid ? pm : 0u;
+  }
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    if (peers[j]) {
+      const uint32_t dgt = (keys[j] >> shift) & 255u;
+      const int leader = __ffs(peers[j]) - 1;
       uint32_t old = 0;
-      if (lane == leader) {
-        old = s_whist[w][dgt];
-        s_whist[w][dgt] = old + __popc(peers);
-      }
-      old = __shfl_sync(peers, old, leader);
-      lrank[j] = (uint16_t)(old + __popc(peers & lt));
+      if (lane == leader) old = atomicAdd(&s_whist[w][dgt], (uint32_t)__popc(peers[j]));
+      old = __shfl_sync(peers[j], old, leader);
+      lrank[j] = (uint16_t)(old + __popc(peers[j] & lt));
     }
-    __syncwarp();
   }
   __syncthreads();
 
@@ -210,23 +211,39 @@ __global__ void __launch_bounds__(kSortThreads)
     st_relaxed_u64(&st[dgt], pack_status(kFlagInclusive, epoch, cnt));
   } else {
     st_relaxed_u64(&st[tile * 256 + dgt], pack_status(kFlagAggregate, epoch, cnt));
+    // walk back from tile - 1, reading a window of kLB predecessors per round trip (the reads
+    // are independent; they are consumed in order and the walk resumes at the first one that
+    // is not published yet)
+    constexpr int kLB = 4;
     int64_t j = tile - 1;
     uint32_t spins = 0;
-    for (;;) {
-      const unsigned long long sv = ld_relaxed_u64(&st[j * 256 + dgt]);
-      const uint32_t f = (uint32_t)(sv >> 62);
-      const uint32_t ep = (uint32_t)(sv >> 32) & 0x3FFFFFFFu;
-      if (ep != (epoch & 0x3FFFFFFFu) || f == kFlagInvalid) {
+    bool done = false;
+    while (!done) {
+      unsigned long long sv[kLB];
+#pragma unroll
+      for (int q = 0; q < kLB; ++q)
+        sv[q] = (j - q >= 0) ? ld_relaxed_u64(&st[(j - q) * 256 + dgt])
+                             : pack_status(kFlagInclusive, epoch, 0);  // before tile 0: empty
+      int q = 0;
+      for (; q < kLB; ++q) {
+        const uint32_t f = (uint32_t)(sv[q] >> 62);
+        const uint32_t ep = (uint32_t)(sv[q] >> 32) & 0x3FFFFFFFu;
+        if (ep != (epoch & 0x3FFFFFFFu) || f == kFlagInvalid) break;
+        excl += (uint32_t)sv[q];
+        if (f == kFlagInclusive) {
+          done = true;
+          break;
+        }
+      }
+      if (done) break;
+      j -= q;
+      if (q == 0) {  // the nearest unsummed predecessor is not published yet
         if (++spins > kSpinLimit) {
           atomicOr(timeout_flag, 1u);
           break;
         }
         if (spins > 64) __nanosleep(64);
-        continue;
       }
-      excl += (uint32_t)sv;
-      if (f == kFlagInclusive) break;
-      --j;
     }
     st_relaxed_u64(&st[tile * 256 + dgt], pack_status(kFlagInclusive, epoch,
                                                       (uint32_t)(excl + cnt)));
