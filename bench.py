@@ -59,6 +59,9 @@ def parse():
                          "embed to k = 12 ln n / EPS^2 coordinates, prepare, run the queries")
     ap.add_argument("--mode", default="auto", choices=["auto", "gather", "scatter"],
                     help="query strategy (include/l1dm.h l1dm_set_query_mode)")
+    ap.add_argument("--collective", default="nccl", choices=["nccl", "peer"],
+                    help="N > 1: NCCL per point/column block, or this library's peer-memory sum "
+                         "(final pass stores into the owners' inboxes; DESIGN.md §8)")
     ap.add_argument("--overlap-blocks", type=int, default=4,
                     help="N>1: point blocks whose reduce overlaps the remaining accumulate")
     return ap.parse_args()
@@ -227,14 +230,21 @@ def main_ours(args):
     Y = torch.empty((n, m), dtype=torch.float64, device=dev)
     kr = (0, k1 - k0)
 
+    peer = {}  # collective="peer": the symmetric buffers are set up once, reused every step
+
     def one_step(timing=False):
-        sh = ShardedL1DM(X, k_range=kr, stream=stream, mode=args.mode, p=args.p)
+        if args.collective == "peer" and world > 1 and not peer:
+            from paper_2210_15114_b200.distributed import PeerGroup
+            peer["g"] = PeerGroup(n, m, result_ranks=(tuple(range(world))
+                                                      if args.reduce == "allreduce" else (0,)))
+        sh = ShardedL1DM(X, k_range=kr, stream=stream, mode=args.mode, p=args.p,
+                         peer_group=peer.get("g"))
         sh.world = world
         if timing and sh.handle is not None and args.p % 2 == 1:
             l1.l1dm_timing_enable(sh.handle, True)
         for q in range(Q):
             sh.matvec(Zs[q % len(Zs)], Y, root=None if args.reduce == "allreduce" else 0,
-                      overlap_blocks=args.overlap_blocks)
+                      overlap_blocks=args.overlap_blocks, collective=args.collective)
         return sh
 
     for _ in range(args.warmup):
@@ -412,7 +422,7 @@ def main_ours(args):
         "dtype": "f64", "input_dtype": "f32", "data": "synthetic",
         "config": {"workload": args.workload, "n": n, "d": d, "m": m, "queries_per_step": Q,
                    "fresh_queries": w.fresh_queries, "parallelism": f"coord-shard x{world}",
-                   "collective": (args.reduce if world > 1 else None),
+                   "collective": (f"{args.reduce} over {args.collective}" if world > 1 else None),
                    "overlap_blocks": (args.overlap_blocks if world > 1 else None),
                    "mode": args.mode, "strategy": ("scatter" if plan["scatter"] else "gather"),
                    "query": "l1" if args.p == 1 else f"lp^p, p={args.p}",

@@ -202,6 +202,60 @@ L1DM_API l1dm_status l1dm_matvec_colblocks(l1dm_handle h, const float *Z, int64_
 L1DM_API l1dm_status l1dm_unblock(const double *Yb, int64_t n, int64_t m, int64_t mb, double *Y,
                                   int64_t ld_y, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * Cross-GPU sum over peer memory.  The
+ * coordinate shards' partials add up to Y because A = sum_k A^(k).  One
+ * process per GPU; rows are owned in contiguous blocks (owner o: rows
+ * [floor(o n / G), floor((o+1) n / G))).  Buffers every rank allocates with
+ * l1dm_ipc_alloc and maps on every other rank with l1dm_ipc_open (handles
+ * exchanged by the caller, e.g. torch.distributed):
+ *   inbox  2 halves (epoch parity) of G slots of rows_o x m fp64 each (slot g of
+ *          epoch e at inbox + ((e & 1) G + g) rows_o m, row stride m)
+ *   flags  2G unsigned words, zero-initialised (arrivals [0, G), results [G, 2G))
+ *   ybuf   n x m fp64 result (row stride m), on ranks that receive the sum
+ * and one local device word for timeouts.  epoch: the caller's query counter,
+ * strictly increasing from 1 (a wait ends when a flag reaches at least it).
+ * Stream order per rank: l1dm_matvec_push, l1dm_peer_reduce, then (result ranks)
+ * l1dm_peer_wait; l1dm_peer_check reports a timed-out wait (the result is
+ * then invalid).  These calls wait on other GPUs' kernels: never run several
+ * ranks of one group on one GPU (nothing guarantees those kernels co-run); a
+ * single-GPU emulation must issue every rank's push before any reduce. */
+#define L1DM_MAX_PEERS 16
+typedef struct {
+  int world;                        /* G, 1..L1DM_MAX_PEERS */
+  int rank;                         /* this rank */
+  double *inbox[L1DM_MAX_PEERS];    /* owner o's inbox as mapped in this process */
+  unsigned *flags[L1DM_MAX_PEERS];  /* owner o's 2G flag words as mapped here */
+  double *ybuf[L1DM_MAX_PEERS];     /* rank t's result buffer as mapped here, or NULL */
+  unsigned *timeout;                /* this rank's timeout word (device, zeroed) */
+} l1dm_peer_t;
+/* bytes of device memory, zeroed, with its 64-byte CUDA IPC handle in handle[0..64). */
+L1DM_API l1dm_status l1dm_ipc_alloc(size_t bytes, void **dptr, void *handle);
+L1DM_API l1dm_status l1dm_ipc_free(void *dptr);
+/* Map another process's allocation (same node; peer access enabled lazily). */
+L1DM_API l1dm_status l1dm_ipc_open(const void *handle, void **dptr);
+L1DM_API l1dm_status l1dm_ipc_close(void *dptr);
+/* This rank's partial A^(K_g) Z (m columns of device Z) goes row by row into the owners'
+ * inbox slots — stored by the query's final pass itself (gather mode's last accumulate,
+ * scatter mode's block write-out: peer stores over NVLink that overlap the pass), or pushed
+ * after a local pass (m = 1 scatter, runs) — then rank g's arrival flag is raised at every
+ * owner.  Stream-ordered; Errors: EINVAL (arguments, epoch 0, unmapped peers), as
+ * l1dm_matvec_ex. */
+L1DM_API l1dm_status l1dm_matvec_push(l1dm_handle h, const float *Z, int64_t ld_z, int64_t m,
+                                      const l1dm_peer_t *peers, unsigned epoch, void *stream);
+/* Owner side (every rank): wait for the G arrivals of this epoch, sum the G slots of this
+ * rank's rows in rank order (deterministic) and store them into ybuf[t] of every rank t whose
+ * bit is set in targets (the root for a reduce, all ranks for an all-reduce), then raise this
+ * owner's result flag at each target. */
+L1DM_API l1dm_status l1dm_peer_reduce(const l1dm_peer_t *peers, int64_t n, int64_t m,
+                                      unsigned epoch, unsigned targets, void *stream);
+/* Result side: wait for every owner's rows of this epoch; then, if Y is not NULL, copy the
+ * n x m result from this rank's ybuf into Y (device, row stride ld_y). */
+L1DM_API l1dm_status l1dm_peer_wait(const l1dm_peer_t *peers, unsigned epoch, int64_t n, int64_t m,
+                                    double *Y, int64_t ld_y, void *stream);
+/* Synchronise the stream and report (then clear) a timed-out peer wait: ETIMEOUT. */
+L1DM_API l1dm_status l1dm_peer_check(const l1dm_peer_t *peers, void *stream);
+
 /* Release every buffer the handle owns.  NULL is a no-op.  Synchronises the
  * handle's stream first. */
 L1DM_API void l1dm_free(l1dm_handle h);

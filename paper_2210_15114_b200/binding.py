@@ -33,6 +33,8 @@ EXPORTS = [
     "l1dm_free", "l1dm_sync",
     "l1dm_shape", "l1dm_workspace_bytes", "l1dm_set_workspace_limit", "l1dm_set_query_mode",
     "l1dm_plan", "l1dm_plan_ex", "l1dm_timing_enable", "l1dm_timing_read", "l1dm_debug_export", "l1dm_release_cached",
+    "l1dm_ipc_alloc", "l1dm_ipc_free", "l1dm_ipc_open", "l1dm_ipc_close", "l1dm_matvec_push",
+    "l1dm_peer_reduce", "l1dm_peer_wait", "l1dm_peer_check",
     "l1dm_last_error", "l1dm_handleless_launches", "l1dm_version",
 ]
 
@@ -48,6 +50,16 @@ class PlanT(ctypes.Structure):
     _fields_ = [(f, ctypes.c_int64) for f in (
         "mb", "col_blocks", "vec", "lanes_per_row", "rows_per_tile", "tiles_per_segment", "kc",
         "chunks", "l2_resident", "workspace_bytes", "scatter")]
+
+
+MAX_PEERS = 16
+
+
+class PeerT(ctypes.Structure):
+    """l1dm_peer_t (include/l1dm.h): the peer buffers of one rank's group, as mapped here."""
+    _fields_ = [("world", ctypes.c_int), ("rank", ctypes.c_int),
+                ("inbox", ctypes.c_void_p * MAX_PEERS), ("flags", ctypes.c_void_p * MAX_PEERS),
+                ("ybuf", ctypes.c_void_p * MAX_PEERS), ("timeout", ctypes.c_void_p)]
 
 
 class TimingT(ctypes.Structure):
@@ -109,6 +121,18 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.l1dm_release_cached.restype = st
     lib.l1dm_last_error.argtypes = []
     lib.l1dm_last_error.restype = ctypes.c_char_p
+    lib.l1dm_ipc_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(vp), ctypes.c_char_p]
+    lib.l1dm_ipc_free.argtypes = [vp]
+    lib.l1dm_ipc_open.argtypes = [ctypes.c_char_p, ctypes.POINTER(vp)]
+    lib.l1dm_ipc_close.argtypes = [vp]
+    lib.l1dm_matvec_push.argtypes = [vp, vp, i64, i64, ctypes.POINTER(PeerT), ctypes.c_uint, vp]
+    lib.l1dm_peer_reduce.argtypes = [ctypes.POINTER(PeerT), i64, i64, ctypes.c_uint, ctypes.c_uint,
+                                     vp]
+    lib.l1dm_peer_wait.argtypes = [ctypes.POINTER(PeerT), ctypes.c_uint, i64, i64, vp, i64, vp]
+    lib.l1dm_peer_check.argtypes = [ctypes.POINTER(PeerT), vp]
+    for name in ("l1dm_ipc_alloc", "l1dm_ipc_free", "l1dm_ipc_open", "l1dm_ipc_close",
+                 "l1dm_matvec_push", "l1dm_peer_reduce", "l1dm_peer_wait", "l1dm_peer_check"):
+        getattr(lib, name).restype = st
     lib.l1dm_handleless_launches.argtypes = []
     lib.l1dm_handleless_launches.restype = i64
     lib.l1dm_version.argtypes = []
@@ -450,6 +474,66 @@ def l1dm_debug_export(h: Handle):
 def l1dm_release_cached():
     """Return cached device blocks of freed handles to CUDA (current device)."""
     _check(load_library().l1dm_release_cached(), "l1dm_release_cached")
+
+
+# ------------------------------------------------------------ peer-memory collective (§8)
+IPC_HANDLE_BYTES = 64
+
+
+def l1dm_ipc_alloc(nbytes: int) -> tuple[int, bytes]:
+    """Zeroed device allocation of nbytes on the current device and its CUDA IPC handle."""
+    p = ctypes.c_void_p()
+    hbuf = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+    _check(load_library().l1dm_ipc_alloc(int(nbytes), ctypes.byref(p), hbuf), "l1dm_ipc_alloc")
+    return int(p.value), bytes(hbuf.raw)
+
+
+def l1dm_ipc_free(ptr: int):
+    _check(load_library().l1dm_ipc_free(ctypes.c_void_p(ptr)), "l1dm_ipc_free")
+
+
+def l1dm_ipc_open(handle: bytes) -> int:
+    """Map another process's l1dm_ipc_alloc buffer (same node) into this one."""
+    p = ctypes.c_void_p()
+    _check(load_library().l1dm_ipc_open(handle, ctypes.byref(p)), "l1dm_ipc_open")
+    return int(p.value)
+
+
+def l1dm_ipc_close(ptr: int):
+    _check(load_library().l1dm_ipc_close(ctypes.c_void_p(ptr)), "l1dm_ipc_close")
+
+
+def l1dm_matvec_push(h: Handle, Z: torch.Tensor, peers: PeerT, epoch: int, stream=None):
+    """This rank's partial A^(K_g) Z into the owners' inboxes, then its arrival flags."""
+    Z = _as_f32_2d(Z, "Z")
+    if not Z.is_cuda:
+        raise ValueError("l1dm_matvec_push needs a CUDA Z")
+    with torch.cuda.device(Z.device):
+        rc = load_library().l1dm_matvec_push(h.ptr, _ptr(Z), Z.stride(0), Z.shape[1],
+                                             ctypes.byref(peers), int(epoch),
+                                             _stream_of(Z, stream))
+    _check(rc, "l1dm_matvec_push")
+
+
+def l1dm_peer_reduce(peers: PeerT, n: int, m: int, epoch: int, targets: int, stream=None):
+    """Owner side: sum this rank's rows over the G slots into every target's result buffer."""
+    _check(load_library().l1dm_peer_reduce(ctypes.byref(peers), n, m, int(epoch), int(targets),
+                                           _stream_of(None, stream)), "l1dm_peer_reduce")
+
+
+def l1dm_peer_wait(peers: PeerT, epoch: int, n: int, m: int, Y=None, stream=None):
+    """Result side: wait for every owner's rows; copy the result into Y (CUDA, n x m fp64)."""
+    yp, ldy = (ctypes.c_void_p(0), m) if Y is None else (_ptr(Y), Y.stride(0))
+    if Y is not None and (Y.dtype != torch.float64 or not Y.is_cuda or tuple(Y.shape) != (n, m)):
+        raise ValueError("Y must be a CUDA float64 n x m tensor")
+    _check(load_library().l1dm_peer_wait(ctypes.byref(peers), int(epoch), n, m, yp, ldy,
+                                         _stream_of(Y, stream)), "l1dm_peer_wait")
+
+
+def l1dm_peer_check(peers: PeerT, stream=None):
+    """Synchronise and raise L1dmError(ETIMEOUT) if a peer wait gave up."""
+    _check(load_library().l1dm_peer_check(ctypes.byref(peers), _stream_of(None, stream)),
+           "l1dm_peer_check")
 
 
 def l1dm_handleless_launches() -> int:

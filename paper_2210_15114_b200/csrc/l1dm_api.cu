@@ -242,6 +242,7 @@ struct l1dm_ctx {
   // host staging (synchronous path: pageable host buffers)
   DevBuf<float> Zstage;
   DevBuf<double> Ystage;
+  DevBuf<double> ypush;  // peer push: the partial Y when the final pass is not fused (or chunked)
   // asynchronous pinned-host pipeline: two staging slots, H2D / D2H on their own streams so
   // query q's copies overlap query q-1's compute (DESIGN.md §7 e2e)
   DevBuf<float> Zpin[2];
@@ -358,6 +359,7 @@ void destroy(l1dm_ctx *h) {
   if (h->cp_out) cudaStreamSynchronize(h->cp_out);
   h->Zstage.release();
   h->Ystage.release();
+  h->ypush.release();
   for (int q = 0; q < 2; ++q) {
     h->Zpin[q].release();
     h->Ypin[q].release();
@@ -659,9 +661,14 @@ bool use_runs(const l1dm_ctx *h) {
 
 // blocked (scatter mode, m > 1 only): Y is column-block-major — block cb at Y + cb n mb with
 // row stride mb — and events[cb] is recorded once block cb is final (nblocks = col_blocks).
+// pd (peer push): the final pass stores each finished row into its owner's inbox
+// slot instead of Y (gather mode's last accumulate, scatter mode's block write-out); Y is then
+// only the gather mode's scratch between coordinate chunks.  Callers pass pd only when
+// push_fusable() holds.
 l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, double *Y,
                           int64_t ldy, cudaStream_t s, int64_t nblocks = 1,
-                          void *const *events = nullptr, bool blocked = false) {
+                          void *const *events = nullptr, bool blocked = false,
+                          const PeerDst *pd = nullptr) {
   if (nblocks < 1) nblocks = 1;
   auto block_range = [&](int64_t b, int64_t &i0, int64_t &i1) {
     i0 = (h->n * b) / nblocks;
@@ -831,7 +838,7 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
           int64_t i0 = 0, i1 = h->n;
           if (last) block_range(b, i0, i1);
           launch_block_out(h->yt.p, p.mb, mc, h->hsum.p, h->Sg.p + c0, h->Sg.p + m + c0, Y + c0,
-                           ldy, i0, i1, s);
+                           ldy, i0, i1, s, pd, c0);
           if (last && events && events[b]) CUDA_TRY(cudaEventRecord((cudaEvent_t)events[b], s));
         }
         h->kernel_launches += 1 + nb;  // totals, block out(s)
@@ -868,7 +875,7 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
         if (last) block_range(b, i0, i1);
         launch_accumulate(p, h->rank.p, h->ldn, h->n, h->U.p, k_first, kcc, h->hsum.p, h->Sg.p,
                           Y, ldy, m, c == 0, last, b == 0 ? h->ctr.p + 2 + c : nullptr, i0, i1,
-                          s);
+                          s, 2.0, true, pd);
         h->kernel_launches++;
         if (last && events && events[b]) CUDA_TRY(cudaEventRecord((cudaEvent_t)events[b], s));
       }
@@ -1344,6 +1351,180 @@ l1dm_status l1dm_matvec_pipelined(l1dm_handle h, const float *Z, int64_t ld_z, i
   cudaStream_t s = (cudaStream_t)stream;
   h->last_stream = s;
   return matvec_device(h, Z, ld_z, m, Y, ld_y, s, point_blocks, block_events);
+}
+
+// ---------------------------------------------------------------- peer-memory collective
+l1dm_status l1dm_ipc_alloc(size_t bytes, void **dptr, void *handle) {
+  g_err.clear();
+  if (!dptr || !handle || bytes == 0) return fail(L1DM_EINVAL, "dptr/handle NULL or bytes == 0");
+  int dev = 0;
+  l1dm_status st = check_arch(&dev);
+  if (st != L1DM_OK) return st;
+  void *p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(e == cudaErrorMemoryAllocation ? L1DM_ENOMEM : L1DM_ECUDA, "cudaMalloc(%zu): %s",
+                bytes, cudaGetErrorString(e));
+  }
+  CUDA_TRY(cudaMemset(p, 0, bytes));
+  cudaIpcMemHandle_t hd;
+  e = cudaIpcGetMemHandle(&hd, p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    cudaGetLastError();
+    return fail(L1DM_ECUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+  }
+  memcpy(handle, &hd, sizeof(hd));
+  *dptr = p;
+  return L1DM_OK;
+}
+
+l1dm_status l1dm_ipc_free(void *dptr) {
+  g_err.clear();
+  if (dptr) CUDA_TRY(cudaFree(dptr));
+  return L1DM_OK;
+}
+
+l1dm_status l1dm_ipc_open(const void *handle, void **dptr) {
+  g_err.clear();
+  if (!handle || !dptr) return fail(L1DM_EINVAL, "handle or dptr is NULL");
+  cudaIpcMemHandle_t hd;
+  memcpy(&hd, handle, sizeof(hd));
+  CUDA_TRY(cudaIpcOpenMemHandle(dptr, hd, cudaIpcMemLazyEnablePeerAccess));
+  return L1DM_OK;
+}
+
+l1dm_status l1dm_ipc_close(void *dptr) {
+  g_err.clear();
+  if (dptr) CUDA_TRY(cudaIpcCloseMemHandle(dptr));
+  return L1DM_OK;
+}
+
+namespace {
+l1dm_status check_peers(const l1dm_peer_t *pr) {
+  if (!pr) return fail(L1DM_EINVAL, "peers is NULL");
+  if (pr->world < 1 || pr->world > L1DM_MAX_PEERS || pr->rank < 0 || pr->rank >= pr->world)
+    return fail(L1DM_EINVAL, "world=%d rank=%d invalid (1 <= world <= %d)", pr->world, pr->rank,
+                L1DM_MAX_PEERS);
+  for (int o = 0; o < pr->world; ++o)
+    if (!pr->inbox[o] || !pr->flags[o])
+      return fail(L1DM_EINVAL, "inbox/flags of rank %d not mapped", o);
+  if (!pr->timeout) return fail(L1DM_EINVAL, "timeout word is NULL");
+  return L1DM_OK;
+}
+}  // namespace
+
+l1dm_status l1dm_matvec_push(l1dm_handle h, const float *Z, int64_t ld_z, int64_t m,
+                             const l1dm_peer_t *peers, unsigned epoch, void *stream) {
+  g_err.clear();
+  if (!h || !Z) return fail(L1DM_EINVAL, "handle or Z is NULL");
+  if (m < 1 || ld_z < m) return fail(L1DM_EINVAL, "m=%lld ld_z=%lld invalid", (long long)m,
+                                     (long long)ld_z);
+  l1dm_status st = check_peers(peers);
+  if (st != L1DM_OK) return st;
+  if (epoch == 0) return fail(L1DM_EINVAL, "epoch 0 is reserved (the flags' initial value)");
+  st = check_device(h);
+  if (st != L1DM_OK) return st;
+  if (!is_device_pointer(Z)) return fail(L1DM_EINVAL, "l1dm_matvec_push needs a device Z");
+  cudaStream_t s = (cudaStream_t)stream;
+  h->last_stream = s;
+  const int G = peers->world, g = peers->rank;
+  PeerDst pd{};
+  pd.world = G;
+  pd.ld = m;
+  for (int o = 0; o <= G; ++o) pd.row0[o] = peer_row0(h->n, G, o);
+  const size_t par = epoch & 1u;  // inbox half of this epoch (double-buffered, see l1dm_peer.cu)
+  for (int o = 0; o < G; ++o)
+    pd.slot[o] = peers->inbox[o] +
+                 (par * G + (size_t)g) * (size_t)(pd.row0[o + 1] - pd.row0[o]) * m;
+  // fused when the final pass is k6 (gather) or k9 (scatter, m > 1); otherwise the partial is
+  // computed locally and pushed by k30
+  bool fused = false;
+  if (!use_runs(h)) {
+    st = ensure_plan(h, m, vec_cap_for(Z, ld_z));
+    if (st != L1DM_OK) return st;
+    fused = !(h->plan.scatter && m == 1);
+  }
+  const bool need_scratch = !fused || (!h->plan.scatter && h->plan.chunks > 1);
+  if (need_scratch) CUDA_TRY(h->ypush.ensure((size_t)h->n * (size_t)m, false, s));
+  if (fused) {
+    st = matvec_device(h, Z, ld_z, m, h->ypush.p, m, s, 1, nullptr, false, &pd);
+  } else {
+    st = matvec_device(h, Z, ld_z, m, h->ypush.p, m, s);
+    if (st == L1DM_OK) {
+      launch_push_rows(h->ypush.p, m, m, 0, h->n, pd, s);
+      h->kernel_launches++;
+    }
+  }
+  if (st != L1DM_OK) return st;
+  launch_peer_signal(peers->flags, G, g, epoch, s);  // arrival of rank g at every owner
+  h->kernel_launches++;
+  CUDA_TRY(cudaGetLastError());
+  return L1DM_OK;
+}
+
+l1dm_status l1dm_peer_reduce(const l1dm_peer_t *peers, int64_t n, int64_t m, unsigned epoch,
+                             unsigned targets, void *stream) {
+  g_err.clear();
+  l1dm_status st = check_peers(peers);
+  if (st != L1DM_OK) return st;
+  if (n < 1 || m < 1 || epoch == 0) return fail(L1DM_EINVAL, "n, m >= 1 and epoch > 0 required");
+  const int G = peers->world, g = peers->rank;
+  double *tp[L1DM_MAX_PEERS];
+  int64_t tl[L1DM_MAX_PEERS];
+  unsigned *tf[L1DM_MAX_PEERS];
+  int nt = 0;
+  for (int t = 0; t < G; ++t) {
+    if (!((targets >> t) & 1u)) continue;
+    if (!peers->ybuf[t]) return fail(L1DM_EINVAL, "target %d has no result buffer mapped", t);
+    tp[nt] = peers->ybuf[t];
+    tl[nt] = m;
+    tf[nt] = peers->flags[t];
+    ++nt;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t r0 = peer_row0(n, G, g), r1 = peer_row0(n, G, g + 1);
+  const double *half = peers->inbox[g] + (size_t)(epoch & 1u) * G * (size_t)(r1 - r0) * m;
+  launch_peer_reduce(peers->flags[g], G, epoch, half, r1 - r0, m, r0, tp, tl, nt,
+                     peers->timeout, s);
+  if (nt) launch_peer_signal(tf, nt, G + g, epoch, s);  // owner g's rows are at every target
+  CUDA_TRY(cudaGetLastError());
+  return L1DM_OK;
+}
+
+l1dm_status l1dm_peer_wait(const l1dm_peer_t *peers, unsigned epoch, int64_t n, int64_t m,
+                           double *Y, int64_t ld_y, void *stream) {
+  g_err.clear();
+  l1dm_status st = check_peers(peers);
+  if (st != L1DM_OK) return st;
+  if (epoch == 0) return fail(L1DM_EINVAL, "epoch 0 is reserved");
+  const int G = peers->world, g = peers->rank;
+  cudaStream_t s = (cudaStream_t)stream;
+  launch_peer_wait(peers->flags[g] + G, G, epoch, peers->timeout, s);
+  if (Y) {
+    if (!peers->ybuf[g]) return fail(L1DM_EINVAL, "this rank has no result buffer");
+    if (n < 1 || m < 1 || ld_y < m) return fail(L1DM_EINVAL, "n, m, ld_y invalid");
+    CUDA_TRY(copy_rows(Y, (size_t)ld_y * sizeof(double), peers->ybuf[g], (size_t)m * sizeof(double),
+                       (size_t)m * sizeof(double), (size_t)n, cudaMemcpyDeviceToDevice, s));
+  }
+  CUDA_TRY(cudaGetLastError());
+  return L1DM_OK;
+}
+
+l1dm_status l1dm_peer_check(const l1dm_peer_t *peers, void *stream) {
+  g_err.clear();
+  if (!peers || !peers->timeout) return fail(L1DM_EINVAL, "peers or timeout word is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned f = 0;
+  CUDA_TRY(cudaMemcpyAsync(&f, peers->timeout, sizeof(f), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  if (f) {
+    const unsigned zero = 0;
+    CUDA_TRY(cudaMemcpy(peers->timeout, &zero, sizeof(zero), cudaMemcpyHostToDevice));
+    return fail(L1DM_ETIMEOUT, "a peer flag wait exceeded its bound; the result is invalid");
+  }
+  return L1DM_OK;
 }
 
 l1dm_status l1dm_query_layout(l1dm_handle h, int64_t m, int64_t *scatter, int64_t *mb,

@@ -115,6 +115,42 @@ struct QueryPlan {
 bool make_plan(int64_t n, int64_t dl, int64_t m, int64_t l2_bytes, int64_t ws_limit,
                int vec_cap, int mode, QueryPlan *p);
 
+// ---------------- peer-memory collective (l1dm_peer.cu) ----------------
+// Row destinations of a rank's partial Y in the owners' inboxes: owner o holds rows
+// [row0[o], row0[o+1]) and this rank's slot in o's inbox is slot[o] (mapped in this process;
+// row stride ld = m).  world == 0: no push (the product writes its own Y).
+constexpr int kMaxPeers = 16;
+struct PeerDst {
+  int world;
+  int64_t ld;
+  int64_t row0[kMaxPeers + 1];
+  double *slot[kMaxPeers];
+};
+__device__ __forceinline__ double *peer_row(const PeerDst &d, int64_t i) {
+  int o = (int)((i * d.world) / d.row0[d.world]);  // even split: within one of the owner
+  if (o >= d.world) o = d.world - 1;
+  while (o > 0 && d.row0[o] > i) --o;
+  while (o + 1 < d.world && d.row0[o + 1] <= i) ++o;
+  return d.slot[o] + (i - d.row0[o]) * d.ld;
+}
+// rows [row0[o], row0[o+1]) of n for o = 0..world-1: floor(o n / world)
+inline int64_t peer_row0(int64_t n, int world, int o) { return (n * o) / world; }
+// dst rows <- src rows [i0, i1) (m doubles each, src row stride lds) at their owners.
+void launch_push_rows(const double *src, int64_t lds, int64_t m, int64_t i0, int64_t i1,
+                      const PeerDst &pd, cudaStream_t s);
+// flags[o][index] = epoch (system-scope release) for o = 0..world-1, after a system fence.
+void launch_peer_signal(unsigned *const *flags, int world, int index, unsigned epoch,
+                        cudaStream_t s);
+// Owner side: wait for flags[0..world) == epoch (bounded; *timeout |= 1 on expiry), then
+// out_t[(row0 + r) * ld_t + c] = sum_g slot_g[r][c] (g = 0..world-1, fixed order) for every
+// target t (targets[t], ld_t; mapped peer memory or local), rows r < rows, c < m.
+void launch_peer_reduce(const unsigned *flags, int world, unsigned epoch, const double *inbox,
+                        int64_t rows, int64_t m, int64_t row0, double *const *targets,
+                        const int64_t *ld_t, int ntargets, unsigned *timeout, cudaStream_t s);
+// Wait until flags[0..count) == epoch (bounded; *timeout |= 1 on expiry).
+void launch_peer_wait(const unsigned *flags, int count, unsigned epoch, unsigned *timeout,
+                      cudaStream_t s);
+
 // Scatter mode: Y[i][c] += g_c - h_i S_c.
 void launch_epilogue(const double *hsum, const double *Sg, double *Y, int64_t ldy, int64_t i0,
                      int64_t i1, int64_t m, cudaStream_t s);
@@ -126,7 +162,8 @@ void launch_totals(const double *segtot, int64_t ld_seg, int64_t dl, int64_t mc,
 // (S == nullptr: Y[i][c] = Yt[i][c]).
 void launch_block_out(const double *yt, int mb, int64_t mc, const double *hsum, const double *S,
                       const double *g, double *Y, int64_t ldy, int64_t i0, int64_t i1,
-                      cudaStream_t s);
+                      cudaStream_t s, const PeerDst *pd = nullptr, int64_t pc0 = 0);
+// (pd: the rows go to their owners' inbox slots at column pc0 instead of Y.)
 // segtot: per-coordinate rows of ld_seg doubles ((S, T) per column); zs: m == 1 only, kc x ldn
 // floats (z in sorted order between the reduce and apply passes).
 void launch_scan(const QueryPlan &p, const uint32_t *perm, const float *sval, int64_t ldn,
@@ -160,7 +197,8 @@ void launch_accumulate(const QueryPlan &p, const uint32_t *rank, int64_t ldn, in
                        const double *Sg, double *Y, int64_t ldy, int64_t m, bool first_chunk,
                        bool last_chunk, unsigned *ticket, int64_t i0, int64_t i1,
                        cudaStream_t s, double factor = 2.0,
-                       bool epilogue = true);  // points [i0, i1); Y (+)= factor * sum_k U (+ g - h S)
+                       bool epilogue = true,   // points [i0, i1); Y (+)= factor * sum_k U (+ g - h S)
+                       const PeerDst *pd = nullptr);  // last chunk: rows to their owners' slots
 // l_p^p, odd p in {3, 5, 7}: plan over the seq kernels.
 bool make_lp_plan(int64_t n, int64_t dl, int64_t m, int lp, int64_t l2_bytes, int64_t ws_limit,
                   int mode, QueryPlan *p);

@@ -1242,26 +1242,40 @@ void launch_epilogue(const double *hsum, const double *Sg, double *Y, int64_t ld
 // Scatter mode, m > 1: Y[i][c0 + c] = Yt[i][c] + g_c - h_i S_c for one column block (Yt is the
 // block's compact L2-resident accumulator, mb doubles per point).  S == nullptr (l_p, p > 1:
 // the apply pass already added the whole contribution): Y[i][c0 + c] = Yt[i][c].
+// PUSH: the row goes to its owner's inbox slot (peer memory over NVLink) at
+// column pc0 + c — the block's output pass is the collective's send.
+template <bool PUSH>
 __global__ void __launch_bounds__(256)
     k9_block_out(const double *__restrict__ yt, int mb, int64_t mc, const double *__restrict__ hsum,
                  const double *__restrict__ S, const double *__restrict__ g, double *__restrict__ Y,
-                 int64_t ldy, int64_t i0, int64_t i1) {
+                 int64_t ldy, int64_t i0, int64_t i1, PeerDst pd, int64_t pc0) {
   const int64_t total = (i1 - i0) * mc;
   for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * 256) {
     const int64_t i = i0 + e / mc, c = e - (e / mc) * mc;
     const double v = yt[i * mb + c];
-    __stcs(Y + i * ldy + c, S ? v + fma(-hsum[i], S[c], g[c]) : v);
+    const double out = S ? v + fma(-hsum[i], S[c], g[c]) : v;
+    if constexpr (PUSH) {
+      peer_row(pd, i)[pc0 + c] = out;
+    } else {
+      __stcs(Y + i * ldy + c, out);
+    }
   }
+  if constexpr (PUSH) __threadfence_system();  // the sends precede the signal kernel's flag
 }
 
 void launch_block_out(const double *yt, int mb, int64_t mc, const double *hsum, const double *S,
                       const double *g, double *Y, int64_t ldy, int64_t i0, int64_t i1,
-                      cudaStream_t s) {
+                      cudaStream_t s, const PeerDst *pd, int64_t pc0) {
   if (i1 <= i0) return;
   int64_t blocks = ((i1 - i0) * mc + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  k9_block_out<<<(unsigned)blocks, 256, 0, s>>>(yt, mb, mc, hsum, S, g, Y, ldy, i0, i1);
+  if (pd && pd->world > 0)
+    k9_block_out<true><<<(unsigned)blocks, 256, 0, s>>>(yt, mb, mc, hsum, S, g, Y, ldy, i0, i1,
+                                                        *pd, pc0);
+  else
+    k9_block_out<false><<<(unsigned)blocks, 256, 0, s>>>(yt, mb, mc, hsum, S, g, Y, ldy, i0, i1,
+                                                         PeerDst{}, 0);
 }
 
 // ------------------------------------------------------------------ runs mode
@@ -1521,21 +1535,24 @@ struct UVec<2> {
   }
 };
 
-template <int V6, int LPP, int UNR>
+template <int V6, int LPP, int UNR, bool PUSH>
 __global__ void __launch_bounds__(256)
     k6_accumulate(const uint32_t *__restrict__ rank, int64_t ldn, int64_t n,
                   const double *__restrict__ U, int64_t ldu, int64_t k_first, int64_t kcc,
                   const double *__restrict__ hsum, const double *__restrict__ Sg,
                   double *__restrict__ Y, int64_t ldy, int64_t m, int first_chunk,
                   int last_chunk, unsigned *ticket, int64_t i_begin, int64_t i_end, double factor,
-                  int epilogue) {
+                  int epilogue, PeerDst pd) {
   constexpr int PPW = 32 / LPP;
   // the chunk's scan has completed (stream order): re-arm its ticket for the next query
   if (ticket && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *ticket = 0u;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t i = i_begin + (int64_t)blockIdx.x * (8 * PPW) + (int64_t)w * PPW + lane / LPP;
   const int64_t c0 = (int64_t)blockIdx.y * (LPP * V6) + (int64_t)(lane % LPP) * V6;
-  if (i >= i_end || c0 >= m) return;
+  if (i >= i_end || c0 >= m) {
+    if constexpr (PUSH) __threadfence_system();
+    return;
+  }
   double acc[V6];
 #pragma unroll
   for (int q = 0; q < V6; ++q) acc[q] = 0.0;
@@ -1567,6 +1584,18 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int q = 0; q < V6; ++q) val[q] += fma(-hi, Sg[c0 + q], Sg[m + c0 + q]);  // g - h_i S
   }
+  if constexpr (PUSH) {
+    // last chunk: the finished partial row goes straight to its owner's inbox slot (peer
+    // stores over NVLink, overlapping the rest of the grid's gathers), then a system fence so
+    // the signal kernel's flag is ordered after every send
+    if (last_chunk) {
+      double *dp = peer_row(pd, i) + c0;
+#pragma unroll
+      for (int q = 0; q < V6; ++q) dp[q] = val[q];
+      __threadfence_system();
+      return;
+    }
+  }
 #pragma unroll
   for (int q = 0; q < V6; ++q) yp[q] = val[q];
 }
@@ -1576,23 +1605,28 @@ static void launch_acc_t(const QueryPlan &p, const uint32_t *rank, int64_t ldn, 
                          const double *U, int64_t k_first, int64_t kcc, const double *hsum,
                          const double *Sg, double *Y, int64_t ldy, int64_t m, bool first,
                          bool last, unsigned *ticket, int64_t i0, int64_t i1, double factor,
-                         bool epilogue, cudaStream_t s) {
+                         bool epilogue, const PeerDst *pd, cudaStream_t s) {
   constexpr int PPB = 8 * (32 / LPP);
   dim3 grid((unsigned)((i1 - i0 + PPB - 1) / PPB), (unsigned)p.col_groups);
-  k6_accumulate<V6, LPP, 8><<<grid, 256, 0, s>>>(rank, ldn, n, U, p.ldu, k_first, kcc, hsum, Sg,
-                                                 Y, ldy, m, first ? 1 : 0, last ? 1 : 0, ticket,
-                                                 i0, i1, factor, epilogue ? 1 : 0);
+  if (pd && pd->world > 0 && last)
+    k6_accumulate<V6, LPP, 8, true><<<grid, 256, 0, s>>>(
+        rank, ldn, n, U, p.ldu, k_first, kcc, hsum, Sg, Y, ldy, m, first ? 1 : 0, 1, ticket, i0,
+        i1, factor, epilogue ? 1 : 0, *pd);
+  else
+    k6_accumulate<V6, LPP, 8, false><<<grid, 256, 0, s>>>(
+        rank, ldn, n, U, p.ldu, k_first, kcc, hsum, Sg, Y, ldy, m, first ? 1 : 0, last ? 1 : 0,
+        ticket, i0, i1, factor, epilogue ? 1 : 0, PeerDst{});
 }
 
 void launch_accumulate(const QueryPlan &p, const uint32_t *rank, int64_t ldn, int64_t n,
                        const double *U, int64_t k_first, int64_t kcc, const double *hsum,
                        const double *Sg, double *Y, int64_t ldy, int64_t m, bool first_chunk,
                        bool last_chunk, unsigned *ticket, int64_t i0, int64_t i1,
-                       cudaStream_t s, double factor, bool epilogue) {
+                       cudaStream_t s, double factor, bool epilogue, const PeerDst *pd) {
   if (i1 <= i0) return;
 #define L1DM_ACC(V, L)                                                                   \
   launch_acc_t<V, L>(p, rank, ldn, n, U, k_first, kcc, hsum, Sg, Y, ldy, m, first_chunk, \
-                     last_chunk, ticket, i0, i1, factor, epilogue, s)
+                     last_chunk, ticket, i0, i1, factor, epilogue, pd, s)
   switch (p.v6 * 100 + p.lpp) {
     case 101: L1DM_ACC(1, 1); break;
     case 102: L1DM_ACC(1, 2); break;

@@ -28,13 +28,76 @@ def shard_range(d: int, rank: int, world: int) -> tuple[int, int]:
     return (rank * d) // world, ((rank + 1) * d) // world
 
 
+def peer_rows(n: int, world: int, owner: int) -> tuple[int, int]:
+    """Rows [floor(o n / G), floor((o+1) n / G)) owned by rank o in the peer sum."""
+    return (n * owner) // world, (n * (owner + 1)) // world
+
+
+class PeerGroup:
+    """The symmetric device buffers of the peer-memory sum (include/l1dm.h).
+
+    Every rank allocates its inbox (two epoch-parity halves of G slots of its rows x m fp64), 2G
+    flag words, a timeout word
+    and, on result ranks, an n x m result buffer with l1dm_ipc_alloc; the CUDA IPC handles are
+    exchanged with one all_gather_object and each rank maps every other rank's buffers with
+    l1dm_ipc_open.  `ipc` (alloc/open/close/free) can be injected for host-side tests."""
+
+    def __init__(self, n: int, m: int, group=None, *, result_ranks=(0,), ipc=None):
+        from types import SimpleNamespace
+        ipc = ipc or SimpleNamespace(alloc=binding.l1dm_ipc_alloc, open=binding.l1dm_ipc_open,
+                                     close=binding.l1dm_ipc_close, free=binding.l1dm_ipc_free)
+        self.ipc, self.n, self.m, self.group = ipc, n, m, group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if self.world > binding.MAX_PEERS:
+            raise ValueError(f"peer sum supports at most {binding.MAX_PEERS} ranks")
+        G, g = self.world, self.rank
+        self.result_ranks = sorted(set(result_ranks))
+        r0, r1 = peer_rows(n, G, g)
+        self.own = {"inbox": ipc.alloc(max(2 * G * (r1 - r0) * m * 8, 8)),  # 2 epoch halves
+                    "flags": ipc.alloc(2 * G * 4), "timeout": ipc.alloc(4),
+                    "ybuf": ipc.alloc(n * m * 8) if g in self.result_ranks else None}
+        mine = {k: (v[1] if v else None) for k, v in self.own.items() if k != "timeout"}
+        allh = [None] * G
+        if G > 1:
+            dist.all_gather_object(allh, mine, group=group)
+        else:
+            allh[0] = mine
+        self.mapped = []  # pointers this process opened (closed in close())
+        pt = binding.PeerT()
+        pt.world, pt.rank = G, g
+        for o in range(G):
+            for key, arr in (("inbox", pt.inbox), ("flags", pt.flags), ("ybuf", pt.ybuf)):
+                if o == g:
+                    arr[o] = self.own[key][0] if self.own[key] else None
+                elif allh[o][key] is not None:
+                    ptr = ipc.open(allh[o][key])
+                    self.mapped.append(ptr)
+                    arr[o] = ptr
+        pt.timeout = self.own["timeout"][0]
+        self.peers = pt
+        self.epoch = 0
+
+    def targets_mask(self) -> int:
+        return sum(1 << t for t in self.result_ranks)
+
+    def close(self):
+        for ptr in self.mapped:
+            self.ipc.close(ptr)
+        self.mapped = []
+        for v in self.own.values():
+            if v:
+                self.ipc.free(v[0])
+        self.own = {}
+
+
 class ShardedL1DM:
     """Per-rank handle over a coordinate shard, with the cross-rank sum of Y."""
 
     def __init__(self, X: torch.Tensor, group=None, *, k_range=None,
                  local_prepare: Optional[Callable] = None,
                  local_matvec: Optional[Callable] = None, stream=None, mode: str = "auto",
-                 p: int = 1):
+                 p: int = 1, peer_group: Optional["PeerGroup"] = None):
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -48,6 +111,8 @@ class ShardedL1DM:
             local_prepare = (lambda X_, k0, k1, stream=None: X_[:, k0:k1].contiguous())
             local_matvec = (lambda h, Z, Y=None, stream=None:
                             binding.l1dm_lpp_even_matvec(h, p, Z, Y, stream=stream))
+        self._peer = peer_group      # collective="peer" buffers (reused across handles if given)
+        self._peer_owned = peer_group is None
         self._prepare = local_prepare or binding.l1dm_prepare
         self._matvec = local_matvec or binding.l1dm_matvec
         self.stream = stream
@@ -70,12 +135,18 @@ class ShardedL1DM:
         return self._matvec(self.handle, Z, Y, stream=self.stream)
 
     def matvec(self, Z: torch.Tensor, Y: Optional[torch.Tensor] = None, *, root: Optional[int] = 0,
-               async_op: bool = False, overlap_blocks: int = 1):
+               async_op: bool = False, overlap_blocks: int = 1, collective: str = "nccl"):
         """A·Z summed over ranks: on `root` only (reduce) or on every rank (root=None).
 
         overlap_blocks > 1 (CUDA, C-ABI handle): the last accumulate runs per point block and
         each block's rows are reduced as soon as they are final, overlapping the collective with
-        the remaining blocks' compute."""
+        the remaining blocks' compute.
+        collective="peer" (CUDA, l1 handle): the sum runs over peer memory in this library's
+        kernels — the query's final pass stores rows straight into their owners' inboxes
+        (l1dm_matvec_push), owners reduce and store into the result ranks (l1dm_peer_reduce),
+        result ranks wait (l1dm_peer_wait); no NCCL on the data path."""
+        if collective == "peer":
+            return self._matvec_peer(Z, Y, root)
         if (overlap_blocks > 1 and self.world > 1 and self.handle is not None and Z.is_cuda
                 and self._matvec is binding.l1dm_matvec):
             return self._matvec_overlapped(Z, Y, root, async_op, overlap_blocks)
@@ -127,12 +198,40 @@ class ShardedL1DM:
             w.wait()
         return Y
 
+    def _matvec_peer(self, Z, Y, root):
+        if self.handle is None or self._matvec is not binding.l1dm_matvec or not Z.is_cuda:
+            raise ValueError("collective='peer' needs a CUDA Z and an l1 C-ABI handle on every rank")
+        n, m = Z.shape[0], Z.shape[1]
+        results = tuple(range(self.world)) if root is None else (root,)
+        pg = getattr(self, "_peer", None)
+        if pg is None or pg.m != m or pg.n != n or tuple(pg.result_ranks) != results:
+            if pg is not None and self._peer_owned:
+                torch.cuda.synchronize(Z.device)
+                pg.close()
+            pg = self._peer = PeerGroup(n, m, self.group, result_ranks=results)
+            self._peer_owned = True
+        pg.epoch += 1
+        stream = self.stream
+        binding.l1dm_matvec_push(self.handle, Z, pg.peers, pg.epoch, stream=stream)
+        binding.l1dm_peer_reduce(pg.peers, n, m, pg.epoch, pg.targets_mask(),
+                                 stream=stream if stream is not None
+                                 else torch.cuda.current_stream(Z.device))
+        if self.rank in results:
+            if Y is None:
+                Y = torch.empty((n, m), dtype=torch.float64, device=Z.device)
+            binding.l1dm_peer_wait(pg.peers, pg.epoch, n, m, Y, stream=stream)
+        return Y
+
     def _collective(self, T, root):
         if root is None:
             return dist.all_reduce(T, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
         return dist.reduce(T, dst=root, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
 
     def close(self):
+        if getattr(self, "_peer", None) is not None and self._peer_owned:
+            torch.cuda.synchronize()
+            self._peer.close()
+        self._peer = None
         if self.handle is not None and self._prepare is binding.l1dm_prepare:
             binding.l1dm_free(self.handle)
         self.handle = None

@@ -137,3 +137,82 @@ def test_two_rank_gloo_lp(p):
     want = oracle.brute_lp(X, Z, p)
     for r in range(2):
         assert np.array_equal(results[r], want)
+
+
+# ---------------------------------------------------------------- peer-sum buffer exchange
+class FakeIPC:
+    """Stands in for l1dm_ipc_* on CPU: 'pointers' are integers, a handle names its owner."""
+
+    def __init__(self, rank):
+        self.rank, self.count, self.opened, self.closed, self.freed = rank, 0, [], [], []
+
+    def alloc(self, nbytes):
+        self.count += 1
+        ptr = 1_000_000 * (self.rank + 1) + self.count
+        return ptr, f"{ptr}:{nbytes}".encode().ljust(64, b"\0")
+
+    def open(self, handle):
+        ptr = int(handle.rstrip(b"\0").split(b":")[0])
+        self.opened.append(ptr)
+        return ptr + 7  # a mapping is a different address of the same buffer
+
+    def close(self, ptr):
+        self.closed.append(ptr)
+
+    def free(self, ptr):
+        self.freed.append(ptr)
+
+
+def peer_worker(rank, world, port, results):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2210_15114_b200.distributed import PeerGroup, peer_rows
+        ipc = FakeIPC(rank)
+        n, m = 1001, 3
+        pg = PeerGroup(n, m, result_ranks=(0, 2), ipc=ipc)
+        pt = pg.peers
+        own = {k: (v[0] if v else None) for k, v in pg.own.items()}
+        rows = [peer_rows(n, world, o) for o in range(world)]
+        out = {
+            "world_rank": (pt.world, pt.rank), "inbox": list(pt.inbox[:world]),
+            "flags": list(pt.flags[:world]), "ybuf": list(pt.ybuf[:world]),
+            "timeout": pt.timeout, "own": own, "mask": pg.targets_mask(), "rows": rows,
+            "inbox_bytes": int(pg.own["inbox"][1].rstrip(b"\0").split(b":")[1]),
+        }
+        pg.close()
+        out["closed"] = sorted(ipc.closed)
+        out["opened"] = sorted(ipc.opened)
+        out["freed"] = sorted(ipc.freed)
+        results[rank] = out  # (a manager dict stores copies: assign once, complete)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_group_exchange_three_ranks():
+    """Every rank maps every other rank's inbox, flags and (result ranks only) result buffer;
+    its own buffers stay unmapped; owners' rows partition [0, n); close() unmaps and frees."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    results = ctx.Manager().dict()
+    mp.start_processes(peer_worker, args=(world, free_port(), results), nprocs=world, join=True,
+                       start_method="spawn")
+    r = {g: results[g] for g in range(world)}
+    assert r[0]["rows"] == [(0, 333), (333, 667), (667, 1001)]
+    for g in range(world):
+        assert r[g]["world_rank"] == (world, g) and r[g]["mask"] == 0b101
+        assert r[g]["timeout"] == r[g]["own"]["timeout"]
+        lo, hi = r[g]["rows"][g]
+        assert r[g]["inbox_bytes"] == 2 * world * (hi - lo) * 3 * 8  # two epoch halves
+        for o in range(world):
+            for key in ("inbox", "flags"):
+                want = r[o]["own"][key] if o == g else r[o]["own"][key] + 7
+                assert r[g][key][o] == want
+            if o in (0, 2):
+                want = r[o]["own"]["ybuf"] if o == g else r[o]["own"]["ybuf"] + 7
+                assert r[g]["ybuf"][o] == want
+            else:
+                assert r[g]["ybuf"][o] is None
+        assert [p + 7 for p in r[g]["opened"]] == r[g]["closed"]
+        assert len(r[g]["freed"]) == (4 if g in (0, 2) else 3)
