@@ -522,6 +522,7 @@ l1dm_status prepare_impl(const float *X, int64_t n, int64_t ld_x, int64_t k_begi
                        fused_rank ? h->rank.p : nullptr, n, ldn, dl, 8 * p,
                        dbase.p + (size_t)p * dl * 256, status.p, ep, ctrl.p + 2, ctrl.p + 1, s);
       h->kernel_launches++;
+      sort_prof_print(s);  // no-op unless built with L1DM_SORT_PROF
       CUDA_TRY(cudaGetLastError());
     }
     if (!fused_rank) {

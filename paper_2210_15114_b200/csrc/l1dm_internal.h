@@ -19,13 +19,13 @@ constexpr uint32_t kSpinLimit = 1u << 26;
 // ---------------- prepare (Alg. 1) ----------------
 constexpr int kSortThreads = 256;
 #ifndef L1DM_SORT_ITEMS
-#define L1DM_SORT_ITEMS 8
+#define L1DM_SORT_ITEMS 12
 #endif
 #ifndef L1DM_SORT_MINB
-#define L1DM_SORT_MINB 3  // 3 CTAs per SM (85 registers, no spills): ~10% faster passes on B200
+#define L1DM_SORT_MINB 2  // with 12 items per thread: 2 CTAs per SM, measured best on B200
 #endif
 constexpr int kSortItems = L1DM_SORT_ITEMS;             // keys per thread per onesweep tile
-constexpr int kSortTile = kSortThreads * kSortItems;    // 4096 keys
+constexpr int kSortTile = kSortThreads * kSortItems;    // 3072 keys
 constexpr int kHistChunk = 16384;                       // keys per histogram CTA
 
 void launch_keys(const float *X, int64_t n, int64_t ldx, int64_t k0, int64_t dl, int64_t ldn,
@@ -34,6 +34,7 @@ void launch_hist(const uint32_t *key, int64_t n, int64_t ldn, int64_t dl, uint32
                  cudaStream_t s);
 // One stable LSD pass over all dl segments.  first: values are implicit point indices.
 // last: writes sval (decoded floats) to kout, perm to vout and rank[k][perm] = r.
+void sort_prof_print(cudaStream_t s);  // debug builds (L1DM_SORT_PROF) only
 void launch_sort_pass(bool first, bool last, const uint32_t *kin, const uint32_t *vin,
                       uint32_t *kout, uint32_t *vout, uint32_t *rank, int64_t n, int64_t ldn,
                       int64_t dl, int shift, const uint32_t *digit_base,

@@ -17,6 +17,8 @@
 //   emit         identity tables when no pass is needed.
 #include <cuda_runtime.h>
 
+#include <cstdio>
+
 #include "l1dm_device.cuh"
 #include "l1dm_internal.h"
 
@@ -112,6 +114,32 @@ void launch_hist(const uint32_t *key, int64_t n, int64_t ldn, int64_t dl, uint32
 }
 
 // ------------------------------------------------------------------ K2
+#ifdef L1DM_SORT_PROF
+// debug build only: per-phase SM cycles of k2_pass summed over CTAs (thread 0's view)
+__device__ unsigned long long g_sort_prof[8];
+#define SORT_T(k)                                                        \
+  do {                                                                   \
+    if (threadIdx.x == 0) {                                              \
+      const long long now = clock64();                                   \
+      atomicAdd(&g_sort_prof[k], (unsigned long long)(now - prof_last)); \
+      prof_last = now;                                                   \
+    }                                                                    \
+  } while (0)
+__global__ void k_sort_prof_print() {
+  printf("[sort prof] ticket %llu load+ballots %llu chain %llu digits+lookback %llu scan %llu "
+         "stage %llu scatter %llu\n",
+         g_sort_prof[0], g_sort_prof[1], g_sort_prof[2], g_sort_prof[3], g_sort_prof[4],
+         g_sort_prof[5], g_sort_prof[6]);
+  for (int i = 0; i < 8; ++i) g_sort_prof[i] = 0;
+}
+void sort_prof_print(cudaStream_t s) { k_sort_prof_print<<<1, 1, 0, s>>>(); }
+#else
+#define SORT_T(k) \
+  do {            \
+  } while (0)
+void sort_prof_print(cudaStream_t) {}
+#endif
+
 // Status word per (segment, tile, digit): [63:62] flag, [61:32] epoch (30 bits), [31:0] count.
 __device__ __forceinline__ unsigned long long pack_status(uint32_t flag, uint32_t epoch,
                                                           uint32_t cnt) {
@@ -119,6 +147,13 @@ __device__ __forceinline__ unsigned long long pack_status(uint32_t flag, uint32_
          ((unsigned long long)(epoch & 0x3FFFFFFFu) << 32) | (unsigned long long)cnt;
 }
 
+// Persistent onesweep pass: each CTA loops over tiles claimed by an atomic ticket, and the
+// next tile's keys/values are already in flight (cp.async into the other half of a shared
+// double buffer) while the current one is ranked, looked back and scattered — ncu/clock64
+// showed the one-tile-per-CTA version spending ~4 of its ~12 us per tile waiting for the
+// ticket and its loads.  A CTA claims tickets in increasing order and processes them in that
+// order, so the smallest unfinished ticket always belongs to a tile being processed whose
+// predecessors are done: the look-back waits cannot deadlock.
 template <bool FIRST, bool LAST>
 __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
     k2_pass(const uint32_t *__restrict__ kin, const uint32_t *__restrict__ vin,
@@ -127,173 +162,225 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
             const uint32_t *__restrict__ digit_base, unsigned long long *status, uint32_t epoch,
             unsigned *ticket, unsigned *timeout_flag) {
   constexpr int W = kSortThreads / 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t *s_in = reinterpret_cast<uint32_t *>(smem_raw);  // [2][2][kSortTile] keys | vals
   __shared__ uint32_t s_keys[kSortTile];
   __shared__ uint32_t s_vals[kSortTile];
   __shared__ uint32_t s_whist[W][256];   // per-warp digit counts, then warp-exclusive offsets
   __shared__ uint32_t s_tstart[256];     // tile-local start of each digit
   __shared__ uint64_t s_gbase[256];      // global start of this tile's run of each digit
   __shared__ uint32_t s_wsum[W];
-  __shared__ unsigned s_ticket;
+  __shared__ unsigned s_tk[2];
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  if (tid == 0) s_ticket = atomicAdd(ticket, 1u);
-  for (int b = tid; b < W * 256; b += kSortThreads) (&s_whist[0][0])[b] = 0;
+  const int64_t total = nseg * tiles_per_seg;
+  // stage tile t (keys, and values unless FIRST) into half b of the input buffer
+  auto issue = [&](int64_t t, int b) {
+    if (t < total) {
+      const int64_t tile = t / nseg, seg = t - (t / nseg) * nseg;
+      const int64_t base = tile * kSortTile, off = seg * ldn + base;
+      uint32_t *dk = s_in + (size_t)b * 2 * kSortTile, *dv = dk + kSortTile;
+      for (int c = tid; c < kSortTile / 4; c += kSortThreads) {
+        const bool ok = base + 4 * c < ldn;  // rows are padded to ldn (multiple of 32)
+        cp_async<16>(dk + 4 * c, ok ? (const void *)(kin + off + 4 * c) : (const void *)kin, ok);
+        if (!FIRST)
+          cp_async<16>(dv + 4 * c, ok ? (const void *)(vin + off + 4 * c) : (const void *)vin, ok);
+      }
+    }
+    cp_async_commit();  // (an empty group past the last ticket keeps the group count uniform)
+  };
+  if (tid == 0) {
+    s_tk[0] = atomicAdd(ticket, 1u);
+    s_tk[1] = atomicAdd(ticket, 1u);
+  }
   __syncthreads();
-  // tickets interleave segments (seg fastest): a tile's predecessor is nseg tickets older
-  const int64_t t = s_ticket;
-  const int64_t tile = t / nseg;
-  const int64_t seg = t - tile * nseg;
-  const int64_t base = tile * kSortTile;
-  const int64_t seg_off = seg * ldn;
-  const int64_t tile_valid = (n - base < kSortTile) ? (n - base) : kSortTile;
+  int64_t t_cur = s_tk[0], t_nxt = s_tk[1];
+  issue(t_cur, 0);
+  issue(t_nxt, 1);
+  int cur = 0;
+#ifdef L1DM_SORT_PROF
+  long long prof_last = clock64();
+#endif
+  while (t_cur < total) {
+    cp_async_wait_group<1>();  // t_cur's group (t_nxt's may still be in flight)
+    for (int b = tid; b < W * 256; b += kSortThreads) (&s_whist[0][0])[b] = 0;
+    __syncthreads();
+    SORT_T(0);
+    const int64_t tile = t_cur / nseg;
+    const int64_t seg = t_cur - tile * nseg;
+    const int64_t base = tile * kSortTile;
+    const int64_t seg_off = seg * ldn;
+    const int64_t tile_valid = (n - base < kSortTile) ? (n - base) : kSortTile;
 
-  // ---- load (warp-striped: warp w owns [w*32*ITEMS, (w+1)*32*ITEMS), item j at +j*32+lane)
-  uint32_t keys[kSortItems];
-  uint32_t vals[kSortItems];
-  uint16_t lrank[kSortItems];
-  const int64_t wbase = base + (int64_t)w * 32 * kSortItems;
+    // ---- items (warp-striped: warp w owns [w*32*ITEMS, (w+1)*32*ITEMS), item j at +j*32+lane)
+    uint32_t keys[kSortItems];
+    uint32_t vals[kSortItems];
+    uint16_t lrank[kSortItems];
+    const int64_t wbase = base + (int64_t)w * 32 * kSortItems;
+    {
+      const uint32_t *sk = s_in + (size_t)cur * 2 * kSortTile, *sv = sk + kSortTile;
 #pragma unroll
-  for (int j = 0; j < kSortItems; ++j) {
-    const int64_t idx = wbase + j * 32 + lane;
-    if (idx < n) {
-      keys[j] = kin[seg_off + idx];
-      vals[j] = FIRST ? (uint32_t)idx : vin[seg_off + idx];
-    } else {
-      keys[j] = 0u;
-      vals[j] = 0u;
+      for (int j = 0; j < kSortItems; ++j) {
+        const int e = w * 32 * kSortItems + j * 32 + lane;
+        const bool valid = base + e < n;
+        keys[j] = valid ? sk[e] : 0u;
+        vals[j] = FIRST ? (uint32_t)(base + e) : (valid ? sv[e] : 0u);
+      }
     }
-  }
-  // ---- warp multisplit: stable rank of each key among equal digits of its warp
-  const uint32_t lt = lanemask_lt();
-  // lanes holding the same digit: 8 ballots (one per digit bit) — MATCH.ANY's latency made it
-  // the top stall of this kernel on sm_100a (ncu short_scoreboard).  The ballots of all items
-  // are independent (issued back to back); only the per-warp digit counters form a chain.
-  uint32_t peers[kSortItems];
+    // ---- warp multisplit: stable rank of each key among equal digits of its warp
+    const uint32_t lt = lanemask_lt();
+    // lanes holding the same digit: 8 ballots (one per digit bit) — MATCH.ANY's latency made it
+    // the top stall of this kernel on sm_100a (ncu short_scoreboard).  The ballots of all items
+    // are independent (issued back to back); only the per-warp digit counters form a chain.
+    uint32_t peers[kSortItems];
 #pragma unroll
-  for (int j = 0; j < kSortItems; ++j) {
-    const bool valid = wbase + j * 32 + lane < n;
-    const uint32_t dgt = (keys[j] >> shift) & 255u;
-    uint32_t pm = __ballot_sync(0xFFFFFFFFu, valid);
-#pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      const uint32_t bit = (dgt >> b) & 1u;
-      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, bit);
-      pm &= bit ? bal : ~bal;
-    }
-    peers[j] = valid ? pm : 0u;
-  }
-#pragma unroll
-  for (int j = 0; j < kSortItems; ++j) {
-    if (peers[j]) {
+    for (int j = 0; j < kSortItems; ++j) {
+      const bool valid = wbase + j * 32 + lane < n;
       const uint32_t dgt = (keys[j] >> shift) & 255u;
-      const int leader = __ffs(peers[j]) - 1;
+#ifdef L1DM_SORT_MATCH
+      // invalid lanes match only themselves (256 + lane is no digit)
+      const uint32_t pm = __match_any_sync(0xFFFFFFFFu, valid ? dgt : 256u + lane);
+#else
+      uint32_t pm = __ballot_sync(0xFFFFFFFFu, valid);
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const uint32_t bit = (dgt >> b) & 1u;
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, bit);
+        pm &= bit ? bal : ~bal;
+      }
+#endif
+      peers[j] = valid ? pm : 0u;
+    }
+    SORT_T(1);
+    // the leader of each digit group bumps the warp's counter; one full-warp shuffle hands
+    // every lane its leader's old count (a shuffle per peer-group mask would serialise groups)
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+      const uint32_t pm = peers[j];
+      const int leader = pm ? __ffs(pm) - 1 : lane;
       uint32_t old = 0;
-      if (lane == leader) old = atomicAdd(&s_whist[w][dgt], (uint32_t)__popc(peers[j]));
-      old = __shfl_sync(peers[j], old, leader);
-      lrank[j] = (uint16_t)(old + __popc(peers[j] & lt));
+      if (pm && lane == leader)
+        old = atomicAdd(&s_whist[w][(keys[j] >> shift) & 255u], (uint32_t)__popc(pm));
+      old = __shfl_sync(0xFFFFFFFFu, old, leader);
+      lrank[j] = (uint16_t)(old + __popc(pm & lt));
     }
-  }
-  __syncthreads();
+    __syncthreads();  // every thread has its items: half `cur` is free for the tile after next
+    SORT_T(2);
 
-  // ---- per digit (thread d): warp-exclusive offsets and the tile count
-  const int dgt = tid;  // kSortThreads == 256 digits
-  uint32_t cnt = 0;
+    // ---- per digit (thread d): warp-exclusive offsets and the tile count
+    const int dgt = tid;  // kSortThreads == 256 digits
+    uint32_t cnt = 0;
 #pragma unroll
-  for (int ww = 0; ww < W; ++ww) {
-    const uint32_t c = s_whist[ww][dgt];
-    s_whist[ww][dgt] = cnt;
-    cnt += c;
-  }
-  // ---- decoupled look-back over earlier tiles of this segment, per digit
-  unsigned long long *st = status + (seg * tiles_per_seg) * 256;
-  uint64_t excl = 0;
-  if (tile == 0) {
-    st_relaxed_u64(&st[dgt], pack_status(kFlagInclusive, epoch, cnt));
-  } else {
-    st_relaxed_u64(&st[tile * 256 + dgt], pack_status(kFlagAggregate, epoch, cnt));
-    // walk back from tile - 1, reading a window of kLB predecessors per round trip (the reads
-    // are independent; they are consumed in order and the walk resumes at the first one that
-    // is not published yet)
-    constexpr int kLB = 4;
-    int64_t j = tile - 1;
-    uint32_t spins = 0;
-    bool done = false;
-    while (!done) {
-      unsigned long long sv[kLB];
-#pragma unroll
-      for (int q = 0; q < kLB; ++q)
-        sv[q] = (j - q >= 0) ? ld_relaxed_u64(&st[(j - q) * 256 + dgt])
-                             : pack_status(kFlagInclusive, epoch, 0);  // before tile 0: empty
-      int q = 0;
-      for (; q < kLB; ++q) {
-        const uint32_t f = (uint32_t)(sv[q] >> 62);
-        const uint32_t ep = (uint32_t)(sv[q] >> 32) & 0x3FFFFFFFu;
-        if (ep != (epoch & 0x3FFFFFFFu) || f == kFlagInvalid) break;
-        excl += (uint32_t)sv[q];
-        if (f == kFlagInclusive) {
-          done = true;
-          break;
-        }
-      }
-      if (done) break;
-      j -= q;
-      if (q == 0) {  // the nearest unsummed predecessor is not published yet
-        if (++spins > kSpinLimit) {
-          atomicOr(timeout_flag, 1u);
-          break;
-        }
-        if (spins > 64) __nanosleep(64);
-      }
+    for (int ww = 0; ww < W; ++ww) {
+      const uint32_t c = s_whist[ww][dgt];
+      s_whist[ww][dgt] = cnt;
+      cnt += c;
     }
-    st_relaxed_u64(&st[tile * 256 + dgt], pack_status(kFlagInclusive, epoch,
-                                                      (uint32_t)(excl + cnt)));
-  }
-  s_gbase[dgt] = (uint64_t)digit_base[seg * 256 + dgt] + excl;
-
-  // ---- block exclusive scan of the tile's digit counts -> s_tstart
-  uint32_t incl_scan = cnt;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl_scan, off);
-    if (lane >= off) incl_scan += y;
-  }
-  if (lane == 31) s_wsum[w] = incl_scan;
-  __syncthreads();
-  uint32_t wpre = 0;
-#pragma unroll
-  for (int ww = 0; ww < W; ++ww)
-    if (ww < w) wpre += s_wsum[ww];
-  s_tstart[dgt] = wpre + incl_scan - cnt;
-  __syncthreads();
-
-  // ---- stage the tile in digit order (stable: warp order, then item, then lane)
-#pragma unroll
-  for (int j = 0; j < kSortItems; ++j) {
-    const int64_t idx = wbase + j * 32 + lane;
-    if (idx < n) {
-      const uint32_t d = (keys[j] >> shift) & 255u;
-      const uint32_t lp = s_tstart[d] + s_whist[w][d] + lrank[j];
-      s_keys[lp] = keys[j];
-      s_vals[lp] = vals[j];
-    }
-  }
-  __syncthreads();
-
-  // ---- scatter: consecutive e inside a digit run go to consecutive global slots
-  for (int e = tid; e < tile_valid; e += kSortThreads) {
-    const uint32_t k = s_keys[e];
-    const uint32_t v = s_vals[e];
-    const uint32_t d = (k >> shift) & 255u;
-    const int64_t gpos = (int64_t)(s_gbase[d] + (uint64_t)(e - s_tstart[d]));
-    if (LAST) {
-      kout[seg_off + gpos] = __float_as_uint(key_to_float(k));  // sval
-      vout[seg_off + gpos] = v;                                 // perm
-      if (rank) rank[seg_off + v] = (uint32_t)gpos;             // rank = perm^-1 (K3 fused)
+    // ---- decoupled look-back over earlier tiles of this segment, per digit
+    unsigned long long *st = status + (seg * tiles_per_seg) * 256;
+    uint64_t excl = 0;
+    if (tile == 0) {
+      st_relaxed_u64(&st[dgt], pack_status(kFlagInclusive, epoch, cnt));
     } else {
-      kout[seg_off + gpos] = k;
-      vout[seg_off + gpos] = v;
+      st_relaxed_u64(&st[tile * 256 + dgt], pack_status(kFlagAggregate, epoch, cnt));
+      // walk back from tile - 1, reading a window of kLB predecessors per round trip (the
+      // reads are independent; they are consumed in order and the walk resumes at the first
+      // one that is not published yet)
+      constexpr int kLB = 4;
+      int64_t j = tile - 1;
+      uint32_t spins = 0;
+      bool done = false;
+      while (!done) {
+        unsigned long long sv[kLB];
+#pragma unroll
+        for (int q = 0; q < kLB; ++q)
+          sv[q] = (j - q >= 0) ? ld_relaxed_u64(&st[(j - q) * 256 + dgt])
+                               : pack_status(kFlagInclusive, epoch, 0);  // before tile 0: empty
+        int q = 0;
+        for (; q < kLB; ++q) {
+          const uint32_t f = (uint32_t)(sv[q] >> 62);
+          const uint32_t ep = (uint32_t)(sv[q] >> 32) & 0x3FFFFFFFu;
+          if (ep != (epoch & 0x3FFFFFFFu) || f == kFlagInvalid) break;
+          excl += (uint32_t)sv[q];
+          if (f == kFlagInclusive) {
+            done = true;
+            break;
+          }
+        }
+        if (done) break;
+        j -= q;
+        if (q == 0) {  // the nearest unsummed predecessor is not published yet
+          if (++spins > kSpinLimit) {
+            atomicOr(timeout_flag, 1u);
+            break;
+          }
+          if (spins > 64) __nanosleep(64);
+        }
+      }
+      st_relaxed_u64(&st[tile * 256 + dgt], pack_status(kFlagInclusive, epoch,
+                                                        (uint32_t)(excl + cnt)));
     }
+    s_gbase[dgt] = (uint64_t)digit_base[seg * 256 + dgt] + excl;
+    SORT_T(3);
+
+    // ---- block exclusive scan of the tile's digit counts -> s_tstart
+    uint32_t incl_scan = cnt;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl_scan, off);
+      if (lane >= off) incl_scan += y;
+    }
+    if (lane == 31) s_wsum[w] = incl_scan;
+    __syncthreads();
+    uint32_t wpre = 0;
+#pragma unroll
+    for (int ww = 0; ww < W; ++ww)
+      if (ww < w) wpre += s_wsum[ww];
+    s_tstart[dgt] = wpre + incl_scan - cnt;
+    __syncthreads();
+    SORT_T(4);
+
+    // ---- stage the tile in digit order (stable: warp order, then item, then lane)
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+      const int64_t idx = wbase + j * 32 + lane;
+      if (idx < n) {
+        const uint32_t d = (keys[j] >> shift) & 255u;
+        const uint32_t lp = s_tstart[d] + s_whist[w][d] + lrank[j];
+        s_keys[lp] = keys[j];
+        s_vals[lp] = vals[j];
+      }
+    }
+    __syncthreads();
+    SORT_T(5);
+
+    // ---- scatter: consecutive e inside a digit run go to consecutive global slots
+    for (int e = tid; e < tile_valid; e += kSortThreads) {
+      const uint32_t k = s_keys[e];
+      const uint32_t v = s_vals[e];
+      const uint32_t d = (k >> shift) & 255u;
+      const int64_t gpos = (int64_t)(s_gbase[d] + (uint64_t)(e - s_tstart[d]));
+      if (LAST) {
+        kout[seg_off + gpos] = __float_as_uint(key_to_float(k));  // sval
+        vout[seg_off + gpos] = v;                                 // perm
+        if (rank) rank[seg_off + v] = (uint32_t)gpos;             // rank = perm^-1 (K3 fused)
+      } else {
+        kout[seg_off + gpos] = k;
+        vout[seg_off + gpos] = v;
+      }
+    }
+    SORT_T(6);
+    // claim the tile after next only now: a CTA holds at most two tickets (the one it works on
+    // and the one in flight), which keeps the tiles a look-back may wait for close behind
+    if (tid == 0) s_tk[0] = atomicAdd(ticket, 1u);
+    __syncthreads();  // s_keys / s_vals / s_gbase / s_tstart are reused by the next tile
+    const int64_t t_nn = s_tk[0];
+    issue(t_nn, cur);
+    t_cur = t_nxt;
+    t_nxt = t_nn;
+    cur ^= 1;
   }
+  cp_async_wait_all();
 }
 
 void launch_sort_pass(bool first, bool last, const uint32_t *kin, const uint32_t *vin,
@@ -302,10 +389,26 @@ void launch_sort_pass(bool first, bool last, const uint32_t *kin, const uint32_t
                       unsigned long long *status, uint32_t epoch, unsigned *ticket,
                       unsigned *timeout_flag, cudaStream_t s) {
   const int64_t tiles = (n + kSortTile - 1) / kSortTile;
-  dim3 grid((unsigned)(tiles * dl));
+  // persistent grid: every CTA resident (the look-back needs no more), at most one per tile
+  static int ctas = 0;
+  const size_t smem = (size_t)4 * kSortTile * sizeof(uint32_t);  // 2 halves x (keys | vals)
+  if (!ctas) {
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k2_pass<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k2_pass<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k2_pass<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k2_pass<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k2_pass<false, false>, kSortThreads, smem);
+    ctas = sms * (per > 0 ? per : 1);
+  }
+  const int64_t work = tiles * dl;
+  dim3 grid((unsigned)(work < ctas ? work : ctas));
 #define L1DM_PASS(F, L)                                                                     \
-  k2_pass<F, L><<<grid, kSortThreads, 0, s>>>(kin, vin, kout, vout, rank, n, ldn, dl, tiles, shift, \
-                                              digit_base, status, epoch, ticket, timeout_flag)
+  k2_pass<F, L><<<grid, kSortThreads, smem, s>>>(kin, vin, kout, vout, rank, n, ldn, dl, tiles, \
+                                                 shift, digit_base, status, epoch, ticket,   \
+                                                 timeout_flag)
   if (first && last)
     L1DM_PASS(true, true);
   else if (first)
