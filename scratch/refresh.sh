@@ -1,0 +1,11 @@
+set -x
+B="timeout 900 python bench.py"
+$B > gpurun_out/r_c3.log 2>&1
+$B --impl reference > gpurun_out/r_c3_ref.log 2>&1
+$B --workload c2 --steps 10 > gpurun_out/r_c2.log 2>&1
+$B --workload c4 --steps 2 > gpurun_out/r_c4.log 2>&1
+$B --workload c5 --steps 3 > gpurun_out/r_c5.log 2>&1
+$B --p 3 --steps 2 --no-cpu-baseline > gpurun_out/r_c3_p3.log 2>&1
+$B --workload c5 --p 3 --steps 2 --no-cpu-baseline > gpurun_out/r_c5_p3.log 2>&1
+bash profiles/run_profile.sh c3 "k5_scan_seq|k5_reduce_all"
+bash profiles/run_profile.sh c4 "k5_scan|k6_accumulate"
