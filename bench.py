@@ -208,10 +208,17 @@ def main_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # test-only overrides (a dry run of the N > 1 path as processes sharing one GPU with gloo:
+    # the NCCL-collective path's kernels never wait on each other, so that is safe)
+    local = int(os.environ.get("L1DM_BENCH_DEVICE", local))
+    backend = os.environ.get("L1DM_BENCH_BACKEND", "nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     w = wl.workload(args.workload)
     Q = args.queries or w.queries
     n, d, m = w.n, w.d, w.m
@@ -476,6 +483,39 @@ def main_ours(args):
                                  "pinned host Y), copies overlapped across queries, one "
                                  "l1dm_sync at the end (inside the timed region)"}
         del Xh, Zh, Yh
+    elif world > 1 and not args.no_e2e:
+        # N > 1: every rank uploads its coordinate shard of X and each query's Z from pinned
+        # host memory, the sharded query + collective runs as in the timed step, and the root
+        # reads every Y back into pinned host memory; wall time, max over ranks
+        Xh = X.cpu().pin_memory()
+        Zh = [z.cpu().pin_memory() for z in Zs]
+        Yh = torch.empty((n, m), dtype=torch.float64).pin_memory() if rank == 0 else None
+        Zd = torch.empty((n, m), dtype=torch.float32, device=dev)
+        root = None if args.reduce == "allreduce" else 0
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        Xd = Xh.to(dev, non_blocking=True)
+        sh = ShardedL1DM(Xd, k_range=kr, stream=stream, mode=args.mode, p=args.p,
+                         peer_group=peer.get("g"))
+        for q in range(Q):
+            Zd.copy_(Zh[q % len(Zh)], non_blocking=True)
+            sh.matvec(Zd, Y, root=root, overlap_blocks=args.overlap_blocks,
+                      collective=args.collective)
+            if rank == 0:
+                Yh.copy_(Y, non_blocking=True)
+        torch.cuda.synchronize()
+        sh.close()
+        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        e2e_s = float(dt.item())
+        result["e2e"] = {"value": upd_step / e2e_s, "unit": "updates/s",
+                         "h2d_bytes_per_step": int(n * d * 4 + world * Q * n * m * 4),
+                         "d2h_bytes_per_step": int(Q * n * m * 8),
+                         "note": "per rank: pinned host X shard + each query's Z uploaded, "
+                                 "sharded query + collective, root reads Y into pinned host "
+                                 "memory; wall time, max over ranks"}
+        del Xh, Zh, Yh, Xd, Zd
     # ---- CPU baseline: the oracle on the host cores, bounded sample, rank 0 at N=1
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
