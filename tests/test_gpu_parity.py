@@ -150,7 +150,7 @@ def sample_rows(n, Y=None, count=24, seed=0):
     return np.array(sorted(r), dtype=np.int64)
 
 
-# ---- full BASELINE.json sizes, in the bench's launch configuration, on sampled rows ----
+# ---- Q12: full BASELINE.json sizes, in the bench's launch configuration, on sampled rows ----
 @pytest.mark.slow
 @pytest.mark.parametrize("name,mode", [("c1", "auto"), ("c2", "auto"), ("c3", "auto"),
                                        ("c4", "auto"), ("c5", "auto"), ("c3", "gather"),

@@ -261,3 +261,29 @@ def test_u_form_precision_requires_fp64_storage():
         np.linalg.norm(ref)
     assert err64 <= 1e-12
     assert err32 > 1e-9
+
+
+# ---- Q19: the U-form scan identity the CUDA path evaluates ------
+def test_u_form_scan_identity_against_direct_sums():
+    """Per coordinate: U_r = sum_{j: rho(j) < r} z_j (v_r - x_jk) written as a direct O(n^2) sum
+    equals v_r P_r - Q_r from exclusive prefixes, and sum_j z_j |x_ik - x_jk| equals
+    2 U_rho(i) + T - x_ik S for every point — with ties (integer coordinates), where either side
+    of a tie may hold the equal values.  Exact in rationals on integer data."""
+    rng = np.random.default_rng(19)
+    for trial in range(40):
+        n = int(rng.integers(1, 40))
+        x = rng.integers(-4, 5, size=n).astype(np.int64)
+        z = rng.integers(-3, 4, size=n).astype(np.int64)
+        order = np.argsort(x, kind="stable")
+        rho = np.empty(n, dtype=np.int64)
+        rho[order] = np.arange(n)
+        v, s = x[order], z[order]
+        P = np.concatenate([[0], np.cumsum(s)[:-1]])
+        Q = np.concatenate([[0], np.cumsum(v * s)[:-1]])
+        U = v * P - Q
+        U_direct = np.array([sum(z[j] * (v[r] - x[j]) for j in range(n) if rho[j] < r)
+                             for r in range(n)], dtype=np.int64)
+        assert np.array_equal(U, U_direct)
+        S, T = z.sum(), (x * z).sum()
+        lhs = np.array([sum(z[j] * abs(x[i] - x[j]) for j in range(n)) for i in range(n)])
+        assert np.array_equal(lhs, 2 * U[rho] + T - x * S)
