@@ -483,7 +483,44 @@ def main_ours(args):
                                  "pinned host Y), copies overlapped across queries, one "
                                  "l1dm_sync at the end (inside the timed region)"}
         del Xh, Zh, Yh
-    elif world > 1 and not args.no_e2e:
+    if world > 1:
+        # SURVEY §8(d) multi-GPU protocol: the per-query compute without the collective, and
+        # the collective alone at the same message size (bus bandwidth), device-timed, max over
+        # ranks
+        sh = ShardedL1DM(X, k_range=kr, stream=stream, mode=args.mode, p=args.p)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        nq = min(Q, 5)
+        dist.barrier()
+        torch.cuda.synchronize()
+        a.record(stream)
+        for q in range(nq):
+            sh.partial(Zs[q % len(Zs)], Y)
+        b.record(stream)
+        torch.cuda.synchronize()
+        comp = a.elapsed_time(b) / nq
+        sh.close()
+        dist.barrier()
+        a.record(stream)
+        for _ in range(nq):
+            if args.reduce == "allreduce":
+                dist.all_reduce(Y, op=dist.ReduceOp.SUM)
+            else:
+                dist.reduce(Y, dst=0, op=dist.ReduceOp.SUM)
+        b.record(stream)
+        torch.cuda.synchronize()
+        coll = a.elapsed_time(b) / nq
+        tt = torch.tensor([comp, coll], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        comp, coll = (float(v) for v in tt.tolist())
+        msg = n * m * 8
+        factor = 2.0 * (world - 1) / world if args.reduce == "allreduce" else (world - 1) / world
+        result["multi_gpu"] = {
+            "compute_only_ms_per_query": comp, "collective_alone_ms": coll,
+            "message_bytes": msg, "collective": args.reduce,
+            "bus_GBps": factor * msg / (coll * 1e-3) / 1e9 if coll > 0 else None,
+            "note": "partial A^(K_g) Z per rank (no collective) and the collective alone on an "
+                    "n x m fp64 buffer; device-timed, max over ranks; NCCL bus-bandwidth factor"}
+    if world > 1 and not args.no_e2e:
         # N > 1: every rank uploads its coordinate shard of X and each query's Z from pinned
         # host memory, the sharded query + collective runs as in the timed step, and the root
         # reads every Y back into pinned host memory; wall time, max over ranks

@@ -63,3 +63,6 @@ def test_ours_two_rank_dry_run_line():
             env={"L1DM_BENCH_DEVICE": "0", "L1DM_BENCH_BACKEND": "gloo"})
     check_ours(d, 2)
     assert d["config"]["parallelism"] == "coord-shard x2"
+    mg = d["multi_gpu"]
+    assert mg["compute_only_ms_per_query"] > 0 and mg["collective_alone_ms"] > 0
+    assert mg["message_bytes"] == 2048 * 1 * 8
