@@ -196,6 +196,13 @@ L1DM_API l1dm_status l1dm_l2_embed(const float *X, int64_t n, int64_t ld_x, int6
  * host pointers), and as l1dm_matvec_ex. */
 L1DM_API l1dm_status l1dm_query_layout(l1dm_handle h, int64_t m, int64_t *scatter, int64_t *mb,
                                        int64_t *col_blocks);
+/* The strategy an m-column l1 query on h runs (the planner's choice under the handle's mode):
+ * gather (U + rank gather, HBM-bound), scatter (L2 reductions into a resident output block) or
+ * runs (tie-heavy data).  Errors: EINVAL. */
+#define L1DM_STRATEGY_GATHER 0
+#define L1DM_STRATEGY_SCATTER 1
+#define L1DM_STRATEGY_RUNS 2
+L1DM_API l1dm_status l1dm_query_strategy(l1dm_handle h, int64_t m, int *strategy);
 L1DM_API l1dm_status l1dm_matvec_colblocks(l1dm_handle h, const float *Z, int64_t ld_z, int64_t m,
                                            double *Yb, void *stream, int64_t nevents,
                                            void *const *block_events);

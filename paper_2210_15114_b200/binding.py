@@ -29,6 +29,7 @@ EXPORTS = [
     "l1dm_prepare", "l1dm_prepare_ex", "l1dm_matvec", "l1dm_matvec_ex", "l1dm_matvec_pipelined",
     "l1dm_matvec_lp", "l1dm_matvec_lp_ex", "l1dm_tv_matvec", "l1dm_tv_matvec_ex",
     "l1dm_lpp_even_matvec", "l1dm_bilinear_matvec", "l1dm_l2_embed", "l1dm_query_layout",
+    "l1dm_query_strategy",
     "l1dm_matvec_colblocks", "l1dm_unblock",
     "l1dm_free", "l1dm_sync",
     "l1dm_shape", "l1dm_workspace_bytes", "l1dm_set_workspace_limit", "l1dm_set_query_mode",
@@ -98,6 +99,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.l1dm_lpp_even_matvec.argtypes = [vp, i64, i64, i64, i32, vp, i64, i64, vp, i64, vp]
     lib.l1dm_bilinear_matvec.argtypes = [vp, i64, i64, i64, vp, vp, i64, i64, vp, i64, vp]
     lib.l1dm_l2_embed.argtypes = [vp, i64, i64, i64, vp, i64, vp, i64, vp]
+    lib.l1dm_query_strategy.argtypes = [vp, i64, ctypes.POINTER(i32)]
+    lib.l1dm_query_strategy.restype = st
     lib.l1dm_query_layout.argtypes = [vp, i64, ctypes.POINTER(i64), ctypes.POINTER(i64),
                                       ctypes.POINTER(i64)]
     lib.l1dm_matvec_colblocks.argtypes = [vp, vp, i64, i64, vp, vp, i64, ctypes.POINTER(vp)]
@@ -534,6 +537,17 @@ def l1dm_peer_check(peers: PeerT, stream=None):
     """Synchronise and raise L1dmError(ETIMEOUT) if a peer wait gave up."""
     _check(load_library().l1dm_peer_check(ctypes.byref(peers), _stream_of(None, stream)),
            "l1dm_peer_check")
+
+
+STRATEGIES = {0: "gather", 1: "scatter", 2: "runs"}
+
+
+def l1dm_query_strategy(h: Handle, m: int) -> str:
+    """'gather', 'scatter' or 'runs': what an m-column l1 query on h runs."""
+    v = ctypes.c_int()
+    _check(load_library().l1dm_query_strategy(h.ptr, int(m), ctypes.byref(v)),
+           "l1dm_query_strategy")
+    return STRATEGIES[v.value]
 
 
 def l1dm_handleless_launches() -> int:

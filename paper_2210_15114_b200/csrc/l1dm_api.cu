@@ -1540,6 +1540,19 @@ l1dm_status l1dm_query_layout(l1dm_handle h, int64_t m, int64_t *scatter, int64_
   return L1DM_OK;
 }
 
+l1dm_status l1dm_query_strategy(l1dm_handle h, int64_t m, int *strategy) {
+  g_err.clear();
+  if (!h || m < 1 || !strategy) return fail(L1DM_EINVAL, "handle/strategy NULL or m < 1");
+  if (use_runs(h)) {
+    *strategy = L1DM_STRATEGY_RUNS;
+    return L1DM_OK;
+  }
+  l1dm_status st = ensure_plan(h, m, 4);
+  if (st != L1DM_OK) return st;
+  *strategy = h->plan.scatter ? L1DM_STRATEGY_SCATTER : L1DM_STRATEGY_GATHER;
+  return L1DM_OK;
+}
+
 l1dm_status l1dm_matvec_colblocks(l1dm_handle h, const float *Z, int64_t ld_z, int64_t m,
                                   double *Yb, void *stream, int64_t nevents,
                                   void *const *events) {
