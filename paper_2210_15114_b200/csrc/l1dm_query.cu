@@ -1379,6 +1379,52 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Expansion without staging: a point's V lanes sum U^k[runid][c0 .. c0 + V) straight from the
+// L2-resident table (dl x 256 x m fp64) — the staged kernel above copies each coordinate's
+// table into shared memory once per 256 points, i.e. as many L2 bytes as the points read.
+template <int V, int LPP, int UNR>
+__global__ void __launch_bounds__(256)
+    k22_runs_gather(const uint8_t *__restrict__ runid, int64_t ldn, int64_t n, int64_t dl,
+                    const double *__restrict__ U, int64_t m, const double *__restrict__ hsum,
+                    const double *__restrict__ Sg, double *__restrict__ Y, int64_t ldy,
+                    int64_t i_begin) {
+  constexpr int PPW = 32 / LPP;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t i = i_begin + (int64_t)blockIdx.x * (8 * PPW) + (int64_t)w * PPW + lane / LPP;
+  const int64_t c0 = (int64_t)blockIdx.y * (LPP * V) + (int64_t)(lane % LPP) * V;
+  if (i >= n || c0 >= m) return;
+  double acc[V];
+#pragma unroll
+  for (int q = 0; q < V; ++q) acc[q] = 0.0;
+  const uint8_t *rp = runid + i;
+  const double *ub = U + c0;
+  int64_t k = 0;
+  for (; k + UNR <= dl; k += UNR) {
+    uint32_t r[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) r[u] = __ldg(rp + (k + u) * ldn);
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const double *p = ub + ((k + u) * 256 + r[u]) * m;
+      if constexpr (V == 2) {
+        const double2 v = __ldg(reinterpret_cast<const double2 *>(p));
+        acc[0] += v.x;
+        acc[1] += v.y;
+      } else {
+        acc[0] += __ldg(p);
+      }
+    }
+  }
+  for (; k < dl; ++k) {
+    const double *p = ub + (k * 256 + __ldg(rp + k * ldn)) * m;
+#pragma unroll
+    for (int q = 0; q < V; ++q) acc[q] += __ldg(p + q);
+  }
+#pragma unroll
+  for (int q = 0; q < V; ++q)
+    Y[i * ldy + c0 + q] = 2.0 * acc[q] + fma(-hsum[i], Sg[c0 + q], Sg[m + c0 + q]);
+}
+
 void launch_runs_query(const uint8_t *runid, int64_t ldn, int64_t n, int64_t dl, const float *rvals,
                        const uint32_t *nruns, const float *Z, int64_t ldz, int64_t m, double *H,
                        double *segtot, const double *hsum, double *Sg, double *Y, int64_t ldy,
@@ -1401,6 +1447,36 @@ void launch_runs_query(const uint8_t *runid, int64_t ldn, int64_t n, int64_t dl,
     dim3 g3((unsigned)((i1 - i0 + 255) / 256), (unsigned)((m + MC - 1) / MC));
     kern<<<g3, 256, 0, s>>>(runid, ldn, i1, dl, H, nruns, m, hsum, Sg, Y, ldy, i0);
   };
+  static const int gather_env = [] {
+    const char *e = getenv("L1DM_RUNS_GATHER");
+    return e ? atoi(e) : -1;
+  }();
+  // default: the unstaged gather (measured on B200, c5: expand 19.2 -> 8.5 ms); lanes cover
+  // V = 2 columns (even m) or 1, LPP lanes per point, wide m in several column groups
+  if (gather_env != 0) {
+    auto g = [&](auto kern, int LPP, int V) {
+      const int ppb = 8 * (32 / LPP);
+      dim3 grid((unsigned)((i1 - i0 + ppb - 1) / ppb), (unsigned)((m + V * LPP - 1) / (V * LPP)));
+      kern<<<grid, 256, 0, s>>>(runid, ldn, i1, dl, H, m, hsum, Sg, Y, ldy, i0);
+    };
+    if (m % 2 == 0) {
+      const int64_t lpp = m / 2;
+      if (lpp <= 1) g(k22_runs_gather<2, 1, 8>, 1, 2);
+      else if (lpp <= 2) g(k22_runs_gather<2, 2, 8>, 2, 2);
+      else if (lpp <= 4) g(k22_runs_gather<2, 4, 8>, 4, 2);
+      else if (lpp <= 8) g(k22_runs_gather<2, 8, 8>, 8, 2);
+      else if (lpp <= 16) g(k22_runs_gather<2, 16, 8>, 16, 2);
+      else g(k22_runs_gather<2, 32, 8>, 32, 2);
+    } else {
+      if (m <= 1) g(k22_runs_gather<1, 1, 8>, 1, 1);
+      else if (m <= 2) g(k22_runs_gather<1, 2, 8>, 2, 1);
+      else if (m <= 4) g(k22_runs_gather<1, 4, 8>, 4, 1);
+      else if (m <= 8) g(k22_runs_gather<1, 8, 8>, 8, 1);
+      else if (m <= 16) g(k22_runs_gather<1, 16, 8>, 16, 1);
+      else g(k22_runs_gather<1, 32, 8>, 32, 1);
+    }
+    return;
+  }
   if (m <= 4) run(k22_runs_expand<4>, 4);
   else if (m <= 8) run(k22_runs_expand<8>, 8);
   else run(k22_runs_expand<16>, 16);

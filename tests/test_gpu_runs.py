@@ -15,7 +15,8 @@ TOL = 1e-9
 
 
 @pytest.mark.parametrize("n,d,m", [(2, 1, 1), (1000, 3, 1), (40000, 12, 16), (5001, 4, 3),
-                                   (3000, 5, 17), (2500, 2, 40)])
+                                   (3000, 5, 17), (2500, 2, 40), (1500, 3, 66), (1200, 2, 71),
+                                   (777, 9, 2)])
 def test_runs_integer_exact(n, d, m):
     rng = np.random.default_rng(n + 7 * m)
     X = rng.integers(0, 256, size=(n, d)).astype(np.float32)
@@ -23,6 +24,28 @@ def test_runs_integer_exact(n, d, m):
     want = oracle.hist(X, Z, M=255).astype(np.float64)
     assert np.array_equal(gpu_matvec(X, Z, mode="runs"), want)
     assert np.array_equal(gpu_matvec(X, Z), want)                    # auto picks runs
+
+
+@pytest.mark.parametrize("m", [2, 16, 33])
+def test_runs_staged_expand_still_exact(m, monkeypatch):
+    """The shared-memory-staged expansion (L1DM_RUNS_GATHER=0) stays correct; run in a fresh
+    process so the environment switch takes effect."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, oracle, sys; sys.path.insert(0, 'tests');"
+        "from gpu_util import gpu_matvec;"
+        f"rng = np.random.default_rng({m});"
+        "X = rng.integers(0, 256, size=(3000, 4)).astype(np.float32);"
+        f"Z = rng.integers(-2, 3, size=(3000, {m})).astype(np.float32);"
+        "w = oracle.hist(X, Z, M=255).astype(np.float64);"
+        "assert np.array_equal(gpu_matvec(X, Z, mode='runs'), w)")
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, L1DM_RUNS_GATHER="0", PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
 
 
 def test_runs_float_values_and_constant_coordinate():
