@@ -165,6 +165,22 @@ def cpu_oracle_sample(w, queries, budget_dims=None):
             "prep_s": t_prep, "query_s": t_q}
 
 
+def mix_ceiling(read_fraction):
+    """Measured HBM streaming rate (GB/s) at a read fraction of the bytes, piecewise linear
+    between the probe's mixes (profiles/hbm_mix.json); None without the probe's file."""
+    try:
+        h = json.load(open(os.path.join(ROOT, "profiles", "hbm_mix.json")))
+        pts = [(0.0, h["write_GBps"]), (1 / 3, h["mix_1r2w_GBps"]), (0.5, h["copy_1r1w_GBps"]),
+               (2 / 3, h["mix_2r1w_GBps"]), (1.0, h["read_GBps"])]
+    except Exception:
+        return None
+    x = min(max(read_fraction, 0.0), 1.0)
+    for (x0, y0), (x1, y1) in zip(pts, pts[1:]):
+        if x <= x1:
+            return y0 + (y1 - y0) * (x - x0) / (x1 - x0)
+    return pts[-1][1]
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -419,6 +435,16 @@ def main_ours(args):
                 "alg_bytes_per_launch": (kern[dominant]["alg_bytes"] /
                                          max(kern[dominant]["launches"] or 1, 1)),
                 "frac_of_8TBps": (ach / 8000.0) if ach else None}
+        # HBM rate depends on the read:write mix (tools/hbm_mix_probe.cu -> profiles/hbm_mix.json:
+        # 1 read : 2 writes streams at ~4.9 TB/s, reads alone at ~7.1); the scan reads
+        # 8 + 4m and writes 8m bytes per pair, the accumulate almost only reads
+        rfrac = {"scan": (8 + 4 * m) / (8 + 12 * m),
+                 "accumulate": (4 + 8 * m) / (4 + 8 * m + 16.0 * m / max(dl, 1))}[dominant]
+        mixc = mix_ceiling(rfrac)
+        if mixc and ach:
+            roof["mix_ceiling_GBps"] = mixc
+            roof["frac_of_mix_ceiling"] = ach / mixc
+            roof["read_fraction"] = rfrac
         if plan["scatter"]:
             # m == 1 scatter mode: z (4 MB) and Y (8 MB) live in L2; per (point, coordinate) the
             # query makes two random 32-byte sector accesses (the z gather of the reduce pass and
