@@ -49,36 +49,49 @@ __device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double
 constexpr int kDmmaKs = 32;          // points per shared-memory stage of K12
 constexpr int kDmmaPad = kTile + 8;  // padded row length (doubles): two wavefronts per fragment
 
-// K12 on DMMA: grid (k tiles, c tiles, p * chunks), 8 warps; warp w owns coordinate rows
-// 16 (w % 4) .. +16 (two 8-row groups) x columns 32 (w / 4) .. +32 (four 8-column tiles).
+// K12 on DMMA: grid (k tiles, c tiles, p * chunks), 8 warps; a CTA owns 32 G coordinates x 64
+// columns, warp w the coordinate rows 8 G (w % 4) .. +8 G (G 8-row groups) x columns
+// 32 (w / 4) .. +32 (four 8-column tiles): G = 4 gives 16 DMMAs per 8 fragment loads (the
+// d >= 128 tile), G = 2 the narrow one.  colpart (t = 1, first coordinate tile only): the
+// chunk's column sums of Z, S_c's partials (folded by k13_colsum in fixed order).
+template <int G>
 __global__ void __launch_bounds__(256)
     k12_moment_reduce_dmma(const float *__restrict__ X, int64_t ldx, const float *__restrict__ Z,
                            int64_t ldz, int64_t n, int64_t d, int64_t m, int p, int64_t chunk,
-                           double *__restrict__ part) {
+                           double *__restrict__ part, double *__restrict__ colpart) {
+  constexpr int TK = 32 * G, XPAD = TK + 8;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double *xs = reinterpret_cast<double *>(smem_raw);  // [kDmmaKs][kDmmaPad]  x^t
-  double *zs = xs + kDmmaKs * kDmmaPad;                // [kDmmaKs][kDmmaPad]
+  double *xs = reinterpret_cast<double *>(smem_raw);  // [kDmmaKs][XPAD]  x^t
+  double *zs = xs + kDmmaKs * XPAD;                    // [kDmmaKs][kDmmaPad]
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int64_t k0 = (int64_t)blockIdx.x * kTile, c0 = (int64_t)blockIdx.y * kTile;
+  const int64_t k0 = (int64_t)blockIdx.x * TK, c0 = (int64_t)blockIdx.y * kTile;
   const int t = 1 + (int)(blockIdx.z % p);
   const int64_t ch = blockIdx.z / p;
   const int64_t i0 = ch * chunk, i1 = (i0 + chunk < n) ? i0 + chunk : n;
-  const int rw = 16 * (w % 4), cw = 32 * (w / 4);
-  double acc[2][4][2];
+  const int rw = 8 * G * (w % 4), cw = 32 * (w / 4);
+  const bool colsum = colpart && t == 1 && blockIdx.x == 0;
+  double csum = 0.0;  // threads 0..63: column c0 + tid
+  double acc[G][4][2];
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+  for (int a = 0; a < G; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
   // register double buffering: stage s+1's global loads are in flight while stage s computes
-  constexpr int PER = kDmmaKs * kTile / 256;  // elements of X and of Z per thread per stage
-  float xr[PER], zr[PER];
+  constexpr int PX = kDmmaKs * TK / 256, PZ = kDmmaKs * kTile / 256;
+  float xr[PX], zr[PZ];
   auto load = [&](int64_t base) {
 #pragma unroll
-    for (int u = 0; u < PER; ++u) {
+    for (int u = 0; u < PX; ++u) {
+      const int e = tid + 256 * u;
+      const int r = e / TK, q = e - (e / TK) * TK;
+      const int64_t i = base + r;
+      xr[u] = (i < i1 && k0 + q < d) ? __ldcs(X + i * ldx + k0 + q) : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < PZ; ++u) {
       const int e = tid + 256 * u;
       const int r = e / kTile, q = e - (e / kTile) * kTile;
       const int64_t i = base + r;
-      xr[u] = (i < i1 && k0 + q < d) ? __ldcs(X + i * ldx + k0 + q) : 0.0f;
       zr[u] = (i < i1 && c0 + q < m) ? __ldcs(Z + i * ldz + c0 + q) : 0.0f;
     }
   };
@@ -86,31 +99,41 @@ __global__ void __launch_bounds__(256)
   for (int64_t base = i0; base < i1; base += kDmmaKs) {
     __syncthreads();
 #pragma unroll
-    for (int u = 0; u < PER; ++u) {
+    for (int u = 0; u < PX; ++u) {
+      const int e = tid + 256 * u;
+      const int r = e / TK, q = e - (e / TK) * TK;
+      xs[r * XPAD + q] = powi((double)xr[u], t);
+    }
+#pragma unroll
+    for (int u = 0; u < PZ; ++u) {
       const int e = tid + 256 * u;
       const int r = e / kTile, q = e - (e / kTile) * kTile;
-      xs[r * kDmmaPad + q] = powi((double)xr[u], t);
       zs[r * kDmmaPad + q] = (double)zr[u];
     }
     __syncthreads();
     if (base + kDmmaKs < i1) load(base + kDmmaKs);
+    if (colsum && tid < kTile) {
+#pragma unroll 8
+      for (int r = 0; r < kDmmaKs; ++r) csum += zs[r * kDmmaPad + tid];  // rows past i1 are 0
+    }
 #pragma unroll
     for (int kk = 0; kk < kDmmaKs / 4; ++kk) {
       const int pt = 4 * kk + (lane & 3);
-      double a[2], b[4];
+      double a[G], b[4];
 #pragma unroll
-      for (int g = 0; g < 2; ++g) a[g] = xs[pt * kDmmaPad + rw + 8 * g + (lane >> 2)];
+      for (int g = 0; g < G; ++g) a[g] = xs[pt * XPAD + rw + 8 * g + (lane >> 2)];
 #pragma unroll
       for (int j = 0; j < 4; ++j) b[j] = zs[pt * kDmmaPad + cw + 8 * j + (lane >> 2)];
 #pragma unroll
-      for (int g = 0; g < 2; ++g)
+      for (int g = 0; g < G; ++g)
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma884(acc[g][j][0], acc[g][j][1], a[g], b[j]);
     }
   }
+  if (colsum && tid < kTile && c0 + tid < m) colpart[ch * m + c0 + tid] = csum;
   double *out = part + ((ch * p + (t - 1)) * d) * m;
 #pragma unroll
-  for (int g = 0; g < 2; ++g) {
+  for (int g = 0; g < G; ++g) {
     const int64_t k = k0 + rw + 8 * g + (lane >> 2);
     if (k >= d) continue;
 #pragma unroll
@@ -120,6 +143,29 @@ __global__ void __launch_bounds__(256)
         const int64_t c = c0 + cw + 8 * j + 2 * (lane & 3) + h;
         if (c < m) out[k * m + c] = acc[g][j][h];
       }
+  }
+}
+
+// the k12 variant for d coordinates, its CTA coordinate tile and dynamic shared memory
+static int k12_g(int64_t d) { return d > 64 ? 4 : 2; }
+static size_t k12_smem(int G) {
+  return ((size_t)kDmmaKs * (32 * G + 8) + (size_t)kDmmaKs * kDmmaPad) * sizeof(double);
+}
+static void launch_k12(const float *X, int64_t ldx, const float *Z, int64_t ldz, int64_t n,
+                       int64_t d, int64_t m, int p, int64_t chunk, int64_t nchunks, double *part,
+                       double *colpart, cudaStream_t s) {
+  const int G = k12_g(d);
+  const size_t sm = k12_smem(G);
+  dim3 g((unsigned)((d + 32 * G - 1) / (32 * G)), (unsigned)((m + kTile - 1) / kTile),
+         (unsigned)(p * nchunks));
+  if (G == 4) {
+    cudaFuncSetAttribute(k12_moment_reduce_dmma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
+    k12_moment_reduce_dmma<4><<<g, 256, sm, s>>>(X, ldx, Z, ldz, n, d, m, p, chunk, part, colpart);
+  } else {
+    cudaFuncSetAttribute(k12_moment_reduce_dmma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
+    k12_moment_reduce_dmma<2><<<g, 256, sm, s>>>(X, ldx, Z, ldz, n, d, m, p, chunk, part, colpart);
   }
 }
 
@@ -254,14 +300,14 @@ __global__ void __launch_bounds__(256)
 }
 
 __global__ void __launch_bounds__(256)
-    k13_colsum(const double *__restrict__ Wp, const float *__restrict__ Z, int64_t ldz, int64_t n,
+    k13_colsum(const double *__restrict__ Wp, const double *__restrict__ colpart, int64_t nchunks,
                int64_t d, int64_t m, double *__restrict__ S, double *__restrict__ G) {
-  // one CTA per column: S_c = sum_i z_ic, G_c = sum_k W_p[k][c] (fixed order per thread, then
-  // a fixed-shape tree)
+  // one CTA per column: S_c = sum over chunks of K12's column partials, G_c = sum_k W_p[k][c]
+  // (fixed order per thread, then a fixed-shape tree)
   __shared__ double rs[256], rg[256];
   const int64_t c = blockIdx.x;
   double s = 0.0, g = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += 256) s += (double)Z[i * ldz + c];
+  for (int64_t ch = threadIdx.x; ch < nchunks; ch += 256) s += colpart[ch * m + c];
   for (int64_t k = threadIdx.x; k < d; k += 256) g += Wp[k * m + c];
   rs[threadIdx.x] = s;
   rg[threadIdx.x] = g;
@@ -376,12 +422,7 @@ int launch_bilinear(const float *X, int64_t ldx, const double *M, const float *Z
   double *S = W + (size_t)d * m;
   double *G = S + m;
   double *V = G + m;
-  dim3 g12((unsigned)((d + kTile - 1) / kTile), (unsigned)((m + kTile - 1) / kTile),
-           (unsigned)nchunks);
-  const size_t sm12 = (size_t)2 * kDmmaKs * kDmmaPad * sizeof(double);
-  cudaFuncSetAttribute(k12_moment_reduce_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)sm12);
-  k12_moment_reduce_dmma<<<g12, 256, sm12, s>>>(X, ldx, Z, ldz, n, d, m, 1, chunk, part);
+  launch_k12(X, ldx, Z, ldz, n, d, m, 1, chunk, nchunks, part, nullptr, s);
   int64_t b13 = (d * m + 255) / 256;
   if (b13 > 148 * 8) b13 = 148 * 8;
   k13_moment_fold<<<(unsigned)b13, 256, 0, s>>>(part, nchunks, d, m, 1, W, G);
@@ -397,7 +438,8 @@ int launch_bilinear(const float *X, int64_t ldx, const double *M, const float *Z
 
 size_t lpp_even_workspace(int64_t n, int64_t d, int64_t m, int p, int64_t *nchunks_out,
                           int64_t *chunk_out, int sms) {
-  const int64_t tiles = ((d + kTile - 1) / kTile) * ((m + kTile - 1) / kTile) * p;
+  const int64_t tk = 32 * k12_g(d);
+  const int64_t tiles = ((d + tk - 1) / tk) * ((m + kTile - 1) / kTile) * p;
   int64_t nchunks = (4 * (int64_t)sms + tiles - 1) / tiles;  // ~4 CTAs per SM over all tiles
   const int64_t min_pts = 1024;
   if (nchunks * min_pts > n) nchunks = (n + min_pts - 1) / min_pts;
@@ -406,8 +448,9 @@ size_t lpp_even_workspace(int64_t n, int64_t d, int64_t m, int p, int64_t *nchun
   nchunks = (n + chunk - 1) / chunk;
   if (nchunks_out) *nchunks_out = nchunks;
   if (chunk_out) *chunk_out = chunk;
-  // partials | W (p x d x m) | S (m) | G (m)
-  return ((size_t)nchunks * p * d * m + (size_t)p * d * m + 2 * (size_t)m) * sizeof(double);
+  // partials | W (p x d x m) | S (m) | G (m) | column partials (nchunks x m)
+  return ((size_t)nchunks * p * d * m + (size_t)p * d * m + 2 * (size_t)m +
+          (size_t)nchunks * m) * sizeof(double);
 }
 
 int launch_lpp_even(const float *X, int64_t ldx, const float *Z, int64_t ldz, int64_t n,
@@ -419,16 +462,13 @@ int launch_lpp_even(const float *X, int64_t ldx, const float *Z, int64_t ldz, in
   double *W = part + (size_t)nchunks * p * d * m;
   double *S = W + (size_t)p * d * m;
   double *G = S + m;
-  dim3 g12((unsigned)((d + kTile - 1) / kTile), (unsigned)((m + kTile - 1) / kTile),
-           (unsigned)(p * nchunks));
-  const size_t sm12 = (size_t)2 * kDmmaKs * kDmmaPad * sizeof(double);
-  cudaFuncSetAttribute(k12_moment_reduce_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)sm12);
-  k12_moment_reduce_dmma<<<g12, 256, sm12, s>>>(X, ldx, Z, ldz, n, d, m, p, chunk, part);
+  double *colpart = G + m;
+  launch_k12(X, ldx, Z, ldz, n, d, m, p, chunk, nchunks, part, colpart, s);
   int64_t b13 = ((int64_t)p * d * m + 255) / 256;
   if (b13 > 148 * 8) b13 = 148 * 8;
   k13_moment_fold<<<(unsigned)b13, 256, 0, s>>>(part, nchunks, d, m, p, W, G);
-  k13_colsum<<<(unsigned)m, 256, 0, s>>>(W + (size_t)(p - 1) * d * m, Z, ldz, n, d, m, S, G);
+  k13_colsum<<<(unsigned)m, 256, 0, s>>>(W + (size_t)(p - 1) * d * m, colpart, nchunks, d, m, S,
+                                          G);
   dim3 g14((unsigned)((n + kTile - 1) / kTile), (unsigned)((m + kTile - 1) / kTile));
   auto expand = [&](auto kern, int P) {
     const size_t sm14 = ((size_t)(P - 1) * kTile * (kStepK + 2) +
