@@ -29,6 +29,12 @@ namespace {
 
 constexpr int kTile = 64;    // output tile (rows x columns) of K12 and K14
 constexpr int kStepK = 16;   // coordinates per shared-memory step of K14
+#ifndef L1DM_K14_P2_G
+#define L1DM_K14_P2_G 4
+#endif
+#ifndef L1DM_K14_P2_KS
+#define L1DM_K14_P2_KS 16
+#endif
 
 __device__ __forceinline__ double powi(double x, int t) {
   double r = 1.0;
@@ -172,28 +178,29 @@ static void launch_k12(const float *X, int64_t ldx, const float *Z, int64_t ldz,
 // K14 on DMMA: grid (point tiles, column tiles), 8 warps; warp w owns points 16 (w % 4) .. +16
 // x columns 32 (w / 4) .. +32.  K = (P-1) d: for t = 1..P-1 the A operand is x^(P-t) (staged in
 // shared memory as fp64), B = c_t W_t.  hp_i = sum_k x_ik^P accumulates while staging.
-template <int P>
+template <int P, int G, int KS>
 __global__ void __launch_bounds__(256)
     k14_moment_expand_dmma(const float *__restrict__ X, int64_t ldx, int64_t n, int64_t d,
                            int64_t m, const double *__restrict__ Wc,
-                           const double *__restrict__ S, const double *__restrict__ G,
+                           const double *__restrict__ S, const double *__restrict__ G_,
                            double *__restrict__ Y, int64_t ldy) {
-  constexpr int KS = kStepK, XP = KS + 2, WP = kDmmaPad;
+  constexpr int TR = 32 * G;  // points per CTA (warp w: rows 8 G (w % 4) .. +8 G)
+  constexpr int XP = KS + 2, WP = kDmmaPad;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double *xp = reinterpret_cast<double *>(smem_raw);  // [P-1][kTile][XP]  slot t: x^(P-1-t)...
-  double *ws = xp + (P - 1) * kTile * XP;               // [P-1][KS][WP]    c_t W_t
-  __shared__ double s_hp[kTile];
+  double *xp = reinterpret_cast<double *>(smem_raw);  // [P-1][TR][XP]  slot t: x^(P-1-t)...
+  double *ws = xp + (P - 1) * TR * XP;                  // [P-1][KS][WP]  c_t W_t
+  __shared__ double s_hp[TR];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int64_t i0 = (int64_t)blockIdx.x * kTile, c0 = (int64_t)blockIdx.y * kTile;
-  const int rw = 16 * (w % 4), cw = 32 * (w / 4);
-  double acc[2][4][2];
+  const int64_t i0 = (int64_t)blockIdx.x * TR, c0 = (int64_t)blockIdx.y * kTile;
+  const int rw = 8 * G * (w % 4), cw = 32 * (w / 4);
+  double acc[G][4][2];
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+  for (int a = 0; a < G; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-  double hp = 0.0;  // threads 0..kTile-1: point i0 + tid
+  double hp = 0.0;  // threads 0..TR-1: point i0 + tid
   // register double buffering of the next k step's X and c_t W_t
-  constexpr int PX = kTile * KS / 256, PW = (P - 1) * KS * kTile / 256;
+  constexpr int PX = TR * KS / 256, PW = (P - 1) * KS * kTile / 256;
   float xr[PX];
   double wr[PW];
   auto load = [&](int64_t kb) {
@@ -224,7 +231,7 @@ __global__ void __launch_bounds__(256)
       double pw = x;  // slot tt (t = tt + 1) holds x^(P-t) = x^(P-1-tt)
 #pragma unroll
       for (int e2 = 1; e2 < P; ++e2) {
-        xp[((P - 1 - e2) * kTile + r) * XP + q] = pw;
+        xp[((P - 1 - e2) * TR + r) * XP + q] = pw;
         pw *= x;
       }
     }
@@ -237,33 +244,33 @@ __global__ void __launch_bounds__(256)
     }
     __syncthreads();
     if (kb + KS < d) load(kb + KS);
-    if (tid < kTile) {  // x^P = x^(P-1) (slot 0) * x (slot P-2)
+    if (tid < TR) {  // x^P = x^(P-1) (slot 0) * x (slot P-2)
 #pragma unroll 4
       for (int q = 0; q < KS; ++q)
-        hp = fma(xp[tid * XP + q], xp[((P - 2) * kTile + tid) * XP + q], hp);
+        hp = fma(xp[tid * XP + q], xp[((P - 2) * TR + tid) * XP + q], hp);
     }
 #pragma unroll
     for (int tt = 0; tt < P - 1; ++tt) {
 #pragma unroll
       for (int kk = 0; kk < KS / 4; ++kk) {
         const int kq = 4 * kk + (lane & 3);
-        double a[2], b[4];
+        double a[G], b[4];
 #pragma unroll
-        for (int g = 0; g < 2; ++g)
-          a[g] = xp[(tt * kTile + rw + 8 * g + (lane >> 2)) * XP + kq];
+        for (int g = 0; g < G; ++g)
+          a[g] = xp[(tt * TR + rw + 8 * g + (lane >> 2)) * XP + kq];
 #pragma unroll
         for (int j = 0; j < 4; ++j) b[j] = ws[(tt * KS + kq) * WP + cw + 8 * j + (lane >> 2)];
 #pragma unroll
-        for (int g = 0; g < 2; ++g)
+        for (int g = 0; g < G; ++g)
 #pragma unroll
           for (int j = 0; j < 4; ++j) dmma884(acc[g][j][0], acc[g][j][1], a[g], b[j]);
       }
     }
   }
-  if (tid < kTile) s_hp[tid] = hp;
+  if (tid < TR) s_hp[tid] = hp;
   __syncthreads();
 #pragma unroll
-  for (int g = 0; g < 2; ++g) {
+  for (int g = 0; g < G; ++g) {
     const int r = rw + 8 * g + (lane >> 2);
     const int64_t i = i0 + r;
     if (i >= n) continue;
@@ -272,9 +279,27 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int64_t c = c0 + cw + 8 * j + 2 * (lane & 3) + h;
-        if (c < m) Y[i * ldy + c] = fma(S[c], s_hp[r], acc[g][j][h] + G[c]);
+        if (c < m) Y[i * ldy + c] = fma(S[c], s_hp[r], acc[g][j][h] + G_[c]);
       }
   }
+}
+
+// launch K14 for P with (G, KS): 32 G points x 64 columns per CTA, KS coordinates per stage
+template <int P, int G, int KS>
+static void launch_k14(const float *X, int64_t ldx, int64_t n, int64_t d, int64_t m,
+                       const double *Wc, const double *S, const double *Gc, double *Y,
+                       int64_t ldy, cudaStream_t s) {
+  constexpr int TR = 32 * G;
+  const size_t sm = ((size_t)(P - 1) * TR * (KS + 2) + (size_t)(P - 1) * KS * kDmmaPad) *
+                    sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k14_moment_expand_dmma<P, G, KS>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = true;
+  }
+  dim3 g((unsigned)((n + TR - 1) / TR), (unsigned)((m + kTile - 1) / kTile));
+  k14_moment_expand_dmma<P, G, KS><<<g, 256, sm, s>>>(X, ldx, n, d, m, Wc, S, Gc, Y, ldy);
 }
 
 // W[t][k][c] = c_t * sum_ch part[ch][t][k][c]  (t = 1..p-1, scaled for the expand), plus
@@ -428,11 +453,7 @@ int launch_bilinear(const float *X, int64_t ldx, const double *M, const float *Z
   k13_moment_fold<<<(unsigned)b13, 256, 0, s>>>(part, nchunks, d, m, 1, W, G);
   k15_small_gemm<<<(unsigned)b13, 256, 0, s>>>(M, W, d, m, V);
   k15_zero<<<1, 256, 0, s>>>(S, 2 * m);  // S and G (adjacent): no h S or G term
-  dim3 g14((unsigned)((n + kTile - 1) / kTile), (unsigned)((m + kTile - 1) / kTile));
-  const size_t sm14 = ((size_t)kTile * (kStepK + 2) + (size_t)kStepK * kDmmaPad) * sizeof(double);
-  cudaFuncSetAttribute(k14_moment_expand_dmma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)sm14);
-  k14_moment_expand_dmma<2><<<g14, 256, sm14, s>>>(X, ldx, n, d, m, V, S, G, Y, ldy);
+  launch_k14<2, 4, 32>(X, ldx, n, d, m, V, S, G, Y, ldy, s);
   return 5;  // k12, k13 fold, k15 gemm, k15 zero, k14
 }
 
@@ -469,17 +490,10 @@ int launch_lpp_even(const float *X, int64_t ldx, const float *Z, int64_t ldz, in
   k13_moment_fold<<<(unsigned)b13, 256, 0, s>>>(part, nchunks, d, m, p, W, G);
   k13_colsum<<<(unsigned)m, 256, 0, s>>>(W + (size_t)(p - 1) * d * m, colpart, nchunks, d, m, S,
                                           G);
-  dim3 g14((unsigned)((n + kTile - 1) / kTile), (unsigned)((m + kTile - 1) / kTile));
-  auto expand = [&](auto kern, int P) {
-    const size_t sm14 = ((size_t)(P - 1) * kTile * (kStepK + 2) +
-                         (size_t)(P - 1) * kStepK * kDmmaPad) * sizeof(double);
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm14);
-    kern<<<g14, 256, sm14, s>>>(X, ldx, n, d, m, W, S, G, Y, ldy);
-  };
   switch (p) {
-    case 2: expand(k14_moment_expand_dmma<2>, 2); break;
-    case 4: expand(k14_moment_expand_dmma<4>, 4); break;
-    case 6: expand(k14_moment_expand_dmma<6>, 6); break;
+    case 2: launch_k14<2, L1DM_K14_P2_G, L1DM_K14_P2_KS>(X, ldx, n, d, m, W, S, G, Y, ldy, s); break;
+    case 4: launch_k14<4, 4, 16>(X, ldx, n, d, m, W, S, G, Y, ldy, s); break;
+    case 6: launch_k14<6, 2, kStepK>(X, ldx, n, d, m, W, S, G, Y, ldy, s); break;
     default: return 3;
   }
   return 4;  // k12, k13 fold, k13 colsum, k14
