@@ -64,7 +64,8 @@ template <int G>
 __global__ void __launch_bounds__(256)
     k12_moment_reduce_dmma(const float *__restrict__ X, int64_t ldx, const float *__restrict__ Z,
                            int64_t ldz, int64_t n, int64_t d, int64_t m, int p, int64_t chunk,
-                           double *__restrict__ part, double *__restrict__ colpart) {
+                           double *__restrict__ part, double *__restrict__ colpart,
+                           double *__restrict__ gpart, int pg) {
   constexpr int TK = 32 * G, XPAD = TK + 8;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double *xs = reinterpret_cast<double *>(smem_raw);  // [kDmmaKs][XPAD]  x^t
@@ -76,7 +77,10 @@ __global__ void __launch_bounds__(256)
   const int64_t i0 = ch * chunk, i1 = (i0 + chunk < n) ? i0 + chunk : n;
   const int rw = 8 * G * (w % 4), cw = 32 * (w / 4);
   const bool colsum = colpart && t == 1 && blockIdx.x == 0;
-  double csum = 0.0;  // threads 0..63: column c0 + tid
+  // G_c's partial sum_j hp_j z_jc (hp_j = sum_k x_jk^pg) when the tile holds every coordinate
+  const bool gsum = colsum && gpart && gridDim.x == 1;
+  __shared__ double s_hp[kDmmaKs];
+  double csum = 0.0, gsumc = 0.0;  // threads 0..63: column c0 + tid
   double acc[G][4][2];
 #pragma unroll
   for (int a = 0; a < G; ++a)
@@ -118,9 +122,26 @@ __global__ void __launch_bounds__(256)
     }
     __syncthreads();
     if (base + kDmmaKs < i1) load(base + kDmmaKs);
+    if (gsum) {  // hp of the stage's 32 points: 8 threads per point, 4 G coordinates each
+      const int r = tid >> 3, q0 = (tid & 7) * (TK / 8);
+      double h = 0.0;
+#pragma unroll
+      for (int q = 0; q < TK / 8; ++q) {
+        const double x = xs[r * XPAD + q0 + q];  // x^1 (t == 1); zero past d and past i1
+        h += powi(x, pg);
+      }
+#pragma unroll
+      for (int off = 4; off; off >>= 1) h += __shfl_xor_sync(0xFFFFFFFFu, h, off);
+      if ((tid & 7) == 0) s_hp[r] = h;
+      __syncthreads();
+    }
     if (colsum && tid < kTile) {
 #pragma unroll 8
       for (int r = 0; r < kDmmaKs; ++r) csum += zs[r * kDmmaPad + tid];  // rows past i1 are 0
+      if (gsum) {
+#pragma unroll 8
+        for (int r = 0; r < kDmmaKs; ++r) gsumc = fma(s_hp[r], zs[r * kDmmaPad + tid], gsumc);
+      }
     }
 #pragma unroll
     for (int kk = 0; kk < kDmmaKs / 4; ++kk) {
@@ -137,6 +158,7 @@ __global__ void __launch_bounds__(256)
     }
   }
   if (colsum && tid < kTile && c0 + tid < m) colpart[ch * m + c0 + tid] = csum;
+  if (gsum && tid < kTile && c0 + tid < m) gpart[ch * m + c0 + tid] = gsumc;
   double *out = part + ((ch * p + (t - 1)) * d) * m;
 #pragma unroll
   for (int g = 0; g < G; ++g) {
@@ -159,7 +181,7 @@ static size_t k12_smem(int G) {
 }
 static void launch_k12(const float *X, int64_t ldx, const float *Z, int64_t ldz, int64_t n,
                        int64_t d, int64_t m, int p, int64_t chunk, int64_t nchunks, double *part,
-                       double *colpart, cudaStream_t s) {
+                       double *colpart, double *gpart, int pg, cudaStream_t s) {
   const int G = k12_g(d);
   const size_t sm = k12_smem(G);
   dim3 g((unsigned)((d + 32 * G - 1) / (32 * G)), (unsigned)((m + kTile - 1) / kTile),
@@ -167,11 +189,13 @@ static void launch_k12(const float *X, int64_t ldx, const float *Z, int64_t ldz,
   if (G == 4) {
     cudaFuncSetAttribute(k12_moment_reduce_dmma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sm);
-    k12_moment_reduce_dmma<4><<<g, 256, sm, s>>>(X, ldx, Z, ldz, n, d, m, p, chunk, part, colpart);
+    k12_moment_reduce_dmma<4><<<g, 256, sm, s>>>(X, ldx, Z, ldz, n, d, m, p, chunk, part, colpart,
+                                                  gpart, pg);
   } else {
     cudaFuncSetAttribute(k12_moment_reduce_dmma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sm);
-    k12_moment_reduce_dmma<2><<<g, 256, sm, s>>>(X, ldx, Z, ldz, n, d, m, p, chunk, part, colpart);
+    k12_moment_reduce_dmma<2><<<g, 256, sm, s>>>(X, ldx, Z, ldz, n, d, m, p, chunk, part, colpart,
+                                                  gpart, pg);
   }
 }
 
@@ -306,8 +330,8 @@ static void launch_k14(const float *X, int64_t ldx, int64_t n, int64_t d, int64_
 // S_c = sum_i z_ic (fixed-order two-level sum over point blocks) and G_c = sum_k W_p[k][c].
 __global__ void __launch_bounds__(256)
     k13_moment_fold(const double *__restrict__ part, int64_t nchunks, int64_t d, int64_t m,
-                    int p, double *__restrict__ W, double *__restrict__ G) {
-  const int64_t total = (int64_t)p * d * m;
+                    int T, int p, double *__restrict__ W) {
+  const int64_t total = (int64_t)T * d * m;
   for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * 256) {
     double s = 0.0;
@@ -318,22 +342,68 @@ __global__ void __launch_bounds__(256)
       for (int q = 0; q < t; ++q) coef = coef * (double)(p - q) / (double)(q + 1);
       W[e] = (t & 1) ? -coef * s : coef * s;
     } else {
-      W[e] = s;  // raw W_p, folded into G below
+      W[e] = s;  // raw (bilinear: W = X^T Z)
     }
   }
-  (void)G;
+}
+
+// G_c = sum_k W_p[k][c] = sum_j hp_j z_jc with hp_j = sum_k x_jk^p: a GEMV over the points, not
+// a d x m moment (K12 skips t = p).  Per point chunk (one CTA): warp per point, lanes over
+// coordinates for hp (fixed shuffle tree) and over columns for the products; the CTA's partial
+// goes to gpart[ch][c] (folded in fixed order by k13_colsum).
+__global__ void __launch_bounds__(256)
+    k13_gpart(const float *__restrict__ X, int64_t ldx, const float *__restrict__ Z, int64_t ldz,
+              int64_t n, int64_t d, int64_t m, int p, int64_t chunk, double *__restrict__ gpart) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double *acc = reinterpret_cast<double *>(smem_raw);  // [8][m]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t e = threadIdx.x; e < 8 * m; e += 256) acc[e] = 0.0;
+  __syncthreads();
+  const int64_t ch = blockIdx.x;
+  const int64_t i0 = ch * chunk, i1 = (i0 + chunk < n) ? i0 + chunk : n;
+  double *aw = acc + w * m;
+  for (int64_t ib = i0 + w; ib < i1; ib += 32) {  // 4 points per warp step (independent loads)
+    double hp[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = ib + 8 * u;
+      hp[u] = 0.0;
+      if (i < i1)
+        for (int64_t k = lane; k < d; k += 32) hp[u] += powi((double)__ldg(X + i * ldx + k), p);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int off = 16; off; off >>= 1) hp[u] += __shfl_xor_sync(0xFFFFFFFFu, hp[u], off);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = ib + 8 * u;
+      if (i >= i1) break;
+      for (int64_t c = lane; c < m; c += 32)
+        aw[c] = fma(hp[u], (double)__ldg(Z + i * ldz + c), aw[c]);
+    }
+  }
+  __syncthreads();
+  for (int64_t c = threadIdx.x; c < m; c += 256) {
+    double g = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < 8; ++ww) g += acc[ww * m + c];
+    gpart[ch * m + c] = g;
+  }
 }
 
 __global__ void __launch_bounds__(256)
-    k13_colsum(const double *__restrict__ Wp, const double *__restrict__ colpart, int64_t nchunks,
-               int64_t d, int64_t m, double *__restrict__ S, double *__restrict__ G) {
-  // one CTA per column: S_c = sum over chunks of K12's column partials, G_c = sum_k W_p[k][c]
-  // (fixed order per thread, then a fixed-shape tree)
+    k13_colsum(const double *__restrict__ gpart, const double *__restrict__ colpart,
+               int64_t nchunks, int64_t m, double *__restrict__ S, double *__restrict__ G) {
+  // one CTA per column: S_c and G_c from the chunks' partials (K12's column sums, k13_gpart)
+  // in fixed order per thread, then a fixed-shape tree
   __shared__ double rs[256], rg[256];
   const int64_t c = blockIdx.x;
   double s = 0.0, g = 0.0;
-  for (int64_t ch = threadIdx.x; ch < nchunks; ch += 256) s += colpart[ch * m + c];
-  for (int64_t k = threadIdx.x; k < d; k += 256) g += Wp[k * m + c];
+  for (int64_t ch = threadIdx.x; ch < nchunks; ch += 256) {
+    s += colpart[ch * m + c];
+    g += gpart[ch * m + c];
+  }
   rs[threadIdx.x] = s;
   rg[threadIdx.x] = g;
   __syncthreads();
@@ -447,10 +517,10 @@ int launch_bilinear(const float *X, int64_t ldx, const double *M, const float *Z
   double *S = W + (size_t)d * m;
   double *G = S + m;
   double *V = G + m;
-  launch_k12(X, ldx, Z, ldz, n, d, m, 1, chunk, nchunks, part, nullptr, s);
+  launch_k12(X, ldx, Z, ldz, n, d, m, 1, chunk, nchunks, part, nullptr, nullptr, 0, s);
   int64_t b13 = (d * m + 255) / 256;
   if (b13 > 148 * 8) b13 = 148 * 8;
-  k13_moment_fold<<<(unsigned)b13, 256, 0, s>>>(part, nchunks, d, m, 1, W, G);
+  k13_moment_fold<<<(unsigned)b13, 256, 0, s>>>(part, nchunks, d, m, 1, 1, W);
   k15_small_gemm<<<(unsigned)b13, 256, 0, s>>>(M, W, d, m, V);
   k15_zero<<<1, 256, 0, s>>>(S, 2 * m);  // S and G (adjacent): no h S or G term
   launch_k14<2, 4, 32>(X, ldx, n, d, m, V, S, G, Y, ldy, s);
@@ -460,7 +530,8 @@ int launch_bilinear(const float *X, int64_t ldx, const double *M, const float *Z
 size_t lpp_even_workspace(int64_t n, int64_t d, int64_t m, int p, int64_t *nchunks_out,
                           int64_t *chunk_out, int sms) {
   const int64_t tk = 32 * k12_g(d);
-  const int64_t tiles = ((d + tk - 1) / tk) * ((m + kTile - 1) / kTile) * p;
+  const int T = p > 1 ? p - 1 : 1;  // moments through DMMA: t = 1 .. p-1 (bilinear: 1)
+  const int64_t tiles = ((d + tk - 1) / tk) * ((m + kTile - 1) / kTile) * T;
   int64_t nchunks = (4 * (int64_t)sms + tiles - 1) / tiles;  // ~4 CTAs per SM over all tiles
   const int64_t min_pts = 1024;
   if (nchunks * min_pts > n) nchunks = (n + min_pts - 1) / min_pts;
@@ -469,9 +540,10 @@ size_t lpp_even_workspace(int64_t n, int64_t d, int64_t m, int p, int64_t *nchun
   nchunks = (n + chunk - 1) / chunk;
   if (nchunks_out) *nchunks_out = nchunks;
   if (chunk_out) *chunk_out = chunk;
-  // partials | W (p x d x m) | S (m) | G (m) | column partials (nchunks x m)
-  return ((size_t)nchunks * p * d * m + (size_t)p * d * m + 2 * (size_t)m +
-          (size_t)nchunks * m) * sizeof(double);
+  // partials (nchunks x T x d x m) | W (T x d x m) | S (m) | G (m) | column partials |
+  // G partials (nchunks x m each)
+  return ((size_t)nchunks * T * d * m + (size_t)T * d * m + 2 * (size_t)m +
+          2 * (size_t)nchunks * m) * sizeof(double);
 }
 
 int launch_lpp_even(const float *X, int64_t ldx, const float *Z, int64_t ldz, int64_t n,
@@ -479,24 +551,35 @@ int launch_lpp_even(const float *X, int64_t ldx, const float *Z, int64_t ldz, in
                     cudaStream_t s) {
   int64_t nchunks = 1, chunk = n;
   lpp_even_workspace(n, d, m, p, &nchunks, &chunk, sms);
+  const int T = p - 1;  // even p >= 2: W_1 .. W_{p-1} on DMMA; W_p enters only through G
   double *part = ws;
-  double *W = part + (size_t)nchunks * p * d * m;
-  double *S = W + (size_t)p * d * m;
+  double *W = part + (size_t)nchunks * T * d * m;
+  double *S = W + (size_t)T * d * m;
   double *G = S + m;
   double *colpart = G + m;
-  launch_k12(X, ldx, Z, ldz, n, d, m, p, chunk, nchunks, part, colpart, s);
-  int64_t b13 = ((int64_t)p * d * m + 255) / 256;
+  double *gpart = colpart + (size_t)nchunks * m;
+  launch_k12(X, ldx, Z, ldz, n, d, m, T, chunk, nchunks, part, colpart, gpart, p, s);
+  const bool fused_g = d <= 32 * k12_g(d);  // one coordinate tile: K12 summed hp z itself
+  if (!fused_g) {
+    const size_t smg = (size_t)8 * m * sizeof(double);
+    static bool gattr = false;
+    if (!gattr) {
+      cudaFuncSetAttribute(k13_gpart, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      gattr = true;
+    }
+    k13_gpart<<<(unsigned)nchunks, 256, smg, s>>>(X, ldx, Z, ldz, n, d, m, p, chunk, gpart);
+  }
+  int64_t b13 = ((int64_t)T * d * m + 255) / 256;
   if (b13 > 148 * 8) b13 = 148 * 8;
-  k13_moment_fold<<<(unsigned)b13, 256, 0, s>>>(part, nchunks, d, m, p, W, G);
-  k13_colsum<<<(unsigned)m, 256, 0, s>>>(W + (size_t)(p - 1) * d * m, colpart, nchunks, d, m, S,
-                                          G);
+  k13_moment_fold<<<(unsigned)b13, 256, 0, s>>>(part, nchunks, d, m, T, p, W);
+  k13_colsum<<<(unsigned)m, 256, 0, s>>>(gpart, colpart, nchunks, m, S, G);
   switch (p) {
     case 2: launch_k14<2, L1DM_K14_P2_G, L1DM_K14_P2_KS>(X, ldx, n, d, m, W, S, G, Y, ldy, s); break;
     case 4: launch_k14<4, 4, 16>(X, ldx, n, d, m, W, S, G, Y, ldy, s); break;
     case 6: launch_k14<6, 2, kStepK>(X, ldx, n, d, m, W, S, G, Y, ldy, s); break;
     default: return 3;
   }
-  return 4;  // k12, k13 fold, k13 colsum, k14
+  return fused_g ? 4 : 5;  // k12, (k13 G partials), k13 fold, k13 colsum, k14
 }
 
 }  // namespace l1dm
