@@ -331,12 +331,14 @@ def main_ours(args):
         kv["ms_per_launch"] = kv["ms_total"] / max(kv["launches"] or 1, 1) if kv["ms_total"] else None
     l2p = load_l2_peaks()
     if args.p % 2 == 0:
-        # even p (NEXT-4, sort-free): two fp64 FMA contractions (moment reduce + expand),
-        # 2 n d m (2p - 1) flops per query; bound: fp64 FMA on the CUDA cores, peak derived from
-        # the unit count (64 fp64 FMA/clk/SM x 148 SMs x 2 flops x the max SM clock)
+        # even p (NEXT-4, sort-free): two fp64 contractions on DMMA (moment reduce + expand);
+        # bound: the fp64 tensor rate measured by tools/fp64_probe.cu (fallback: derived from
+        # the unit count, 64 fp64 FMA/clk/SM x 148 SMs x 2 flops x the max SM clock)
         for kv in kern.values():
             kv["achieved_GBps"] = None
-        flops = 2.0 * n * dl * m * (2 * args.p - 1)
+        # the contractions the method needs: W_t = (X^t)^T Z for t = 1..p-1 and the expansion
+        # sum_t X^(p-t) W_t, 2 n d m flops each per power (S, G and hp are O(n (d + m)))
+        flops = 4.0 * n * dl * m * (args.p - 1)
         ach = flops / (ms_step * 1e-3 / Q) / 1e12
         try:
             fp = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
