@@ -293,8 +293,8 @@ def main_ours(args):
         step_ev[2 * s + 1].record(stream)
         if sh.handle is not None and args.p % 2 == 1:
             timings.append(l1.l1dm_timing_read(sh.handle))  # syncs the stream (host only)
-        if sh.handle is not None and args.p == 1:
-            strategy = l1.l1dm_query_strategy(sh.handle, m)
+        if sh.handle is not None and args.p % 2 == 1:
+            strategy = l1.l1dm_query_strategy(sh.handle, m)  # (runs serves every odd p)
         sh.close()
     ev1.record(stream)
     hl_launches = l1.l1dm_handleless_launches() - hl0
@@ -349,6 +349,30 @@ def main_ours(args):
         roof = {"bound": "tensor", "kernel": "whole query (k12 reduce + k13 fold + k14 expand)",
                 "achieved": ach, "peak": peak, "unit": "TFLOP/s (fp64 DMMA)", "peak_kind": pk,
                 "frac": ach / peak, "alg_flops_per_query": flops}
+    elif strategy == "runs":
+        # runs mode (DESIGN.md §2f, tie-heavy data): "scan" = the run histogram (one fp64 L2
+        # reduction per update into the L2-resident (coordinate, run, column) table, run ids
+        # and Z rows streamed in point order) + the prefix over runs; "accumulate" = the
+        # expansion (per pair a run id from HBM and a U row from the L2-resident table).  HBM
+        # moves only 2 n d (run ids) + n m (4 + 8) bytes per query, so the histogram's
+        # reductions bound the query: roofline in reductions/s against the measured probe.
+        red = agg.get("queries", 0) * n * dl * m
+        sc = kern["scan"]
+        kern["scan"]["alg_reductions"] = red
+        hbm_q = 2 * n * dl + n * m * 12 + n * 8
+        for kv in kern.values():
+            kv["achieved_GBps"] = None
+        dominant = "scan"
+        ach = (red / (sc["ms_total"] * 1e-3) / 1e9) if sc["ms_total"] else None
+        peak = l2p.get("red_row8_adds_per_s", 5.88e11) / 1e9
+        roof = {"bound": "l2_fp64_reductions",
+                "kernel": "run histogram (k20_runs_hist + the scan over runs)",
+                "achieved": ach, "peak": peak, "unit": "G fp64 reductions/s",
+                "peak_kind": "measured (tools/l2_probe.cu -> profiles/l2_peaks.json)",
+                "frac": (ach / peak) if ach else None,
+                "alg_reductions_per_launch": red / max(sc["launches"] or 1, 1),
+                "hbm_bytes_per_query": hbm_q,
+                "hbm_GBps": (hbm_q / (query_kernel_ms * 1e-3) / 1e9) if query_kernel_ms else None}
     elif args.p > 1:
         # l_p^p, odd p: the seq scan with p+1 moments in both strategies.
         # scatter: the apply pass's fp64 L2 reductions, one per update, as for p = 1.
@@ -374,29 +398,6 @@ def main_ours(args):
             roof = {"bound": "hbm", "kernel": "whole query (seq reduce/apply-store + k6)",
                     "achieved": ach, "peak": hbm_peak, "peak_kind": peak_kind, "unit": "GB/s",
                     "frac": (ach / hbm_peak) if ach else None, "alg_bytes_per_query": qbytes}
-    elif strategy == "runs":
-        # runs mode (DESIGN.md §2f, tie-heavy data): "scan" = the run histogram (one fp64 L2
-        # reduction per update into the L2-resident (coordinate, run, column) table, run ids
-        # and Z rows streamed in point order) + the prefix over runs; "accumulate" = the
-        # expansion (per pair a run id from HBM and a U row from the L2-resident table).  HBM
-        # moves only 2 n d (run ids) + n m (4 + 8) bytes per query, so the histogram's
-        # reductions bound the query: roofline in reductions/s against the measured probe.
-        red = agg.get("queries", 0) * n * dl * m
-        sc = kern["scan"]
-        kern["scan"]["alg_reductions"] = red
-        hbm_q = 2 * n * dl + n * m * 12 + n * 8
-        for kv in kern.values():
-            kv["achieved_GBps"] = None
-        dominant = "scan"
-        ach = (red / (sc["ms_total"] * 1e-3) / 1e9) if sc["ms_total"] else None
-        peak = l2p.get("red_row8_adds_per_s", 5.88e11) / 1e9
-        roof = {"bound": "l2_fp64_reductions", "kernel": "run histogram (k20_runs_hist + prefix)",
-                "achieved": ach, "peak": peak, "unit": "G fp64 reductions/s",
-                "peak_kind": "measured (tools/l2_probe.cu -> profiles/l2_peaks.json)",
-                "frac": (ach / peak) if ach else None,
-                "alg_reductions_per_launch": red / max(sc["launches"] or 1, 1),
-                "hbm_bytes_per_query": hbm_q,
-                "hbm_GBps": (hbm_q / (query_kernel_ms * 1e-3) / 1e9) if query_kernel_ms else None}
     elif plan["scatter"] and m > 1:
         # scatter mode: per column block, "scan" = reduce + prefix (perm/sval
         # streamed from HBM, one Zt row gathered from L2 per pair), "accumulate" = apply (the

@@ -895,6 +895,28 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
 // Yt), gather mode stores it in sorted order into U and k6 sums U over each coordinate chunk.
 l1dm_status lp_device(l1dm_ctx *h, int lp, const float *Z, int64_t ldz, int64_t m, double *Y,
                       int64_t ldy, cudaStream_t s) {
+  if (use_runs(h)) {  // tie-heavy data: the run-level form serves every odd p
+    CUDA_TRY(h->rtab.ensure((size_t)h->dl * 256 * m, false, s));
+    {
+      TimedScope ts(h, kScan, s);
+      launch_runs_lp(h->runid.p, h->ldn, h->n, h->dl, h->rvals.p, h->nruns.p, Z, ldz, m, lp,
+                     h->rtab.p, Y, ldy, 0, s);
+      h->kernel_launches += 2;  // histogram, p-moment scan
+      h->launches[kScan]++;
+    }
+    {
+      TimedScope ts(h, kAcc, s);
+      launch_runs_lp(h->runid.p, h->ldn, h->n, h->dl, h->rvals.p, h->nruns.p, Z, ldz, m, lp,
+                     h->rtab.p, Y, ldy, 1, s);
+      h->kernel_launches++;  // expansion
+      h->launches[kAcc]++;
+      if (h->timing) h->acc_pairs += h->n * h->dl;
+    }
+    CUDA_TRY(cudaGetLastError());
+    h->queries++;
+    h->m_last = m;
+    return L1DM_OK;
+  }
   size_t ws = h->ws_limit;
   QueryPlan p;
   if (ws == 0) {  // the free-memory probe only when the workspace is large (see ensure_plan)

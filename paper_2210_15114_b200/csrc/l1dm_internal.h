@@ -210,6 +210,12 @@ void launch_runs_query(const uint8_t *runid, int64_t ldn, int64_t n, int64_t dl,
                        const uint32_t *nruns, const float *Z, int64_t ldz, int64_t m, double *H,
                        double *segtot, const double *hsum, double *Sg, double *Y, int64_t ldy,
                        int phase, cudaStream_t s, int64_t i0 = 0, int64_t i1 = -1);
+// Runs mode for odd p in {3, 5, 7}: Y = sum_k W^k[runid_k(i)] with W^k the whole per-run
+// l_p^p term (histogram, p-moment scan over runs, expansion); H: dl x 256 x m fp64 scratch.
+void launch_runs_lp(const uint8_t *runid, int64_t ldn, int64_t n, int64_t dl, const float *rvals,
+                    const uint32_t *nruns, const float *Z, int64_t ldz, int64_t m, int lp,
+                    double *H, double *Y, int64_t ldy, int phase, cudaStream_t s);
+// (phase 0: histogram + p-moment scan; phase 1: expansion.)
 // Y (row-major, ldy) <- Yb (column-block-major blocks of n x mb).
 void launch_unblock(const double *Yb, int64_t n, int64_t m, int64_t mb, double *Y, int64_t ldy,
                     cudaStream_t s);

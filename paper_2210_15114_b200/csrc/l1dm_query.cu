@@ -1382,7 +1382,7 @@ __global__ void __launch_bounds__(256)
 // Expansion without staging: a point's V lanes sum U^k[runid][c0 .. c0 + V) straight from the
 // L2-resident table (dl x 256 x m fp64) — the staged kernel above copies each coordinate's
 // table into shared memory once per 256 points, i.e. as many L2 bytes as the points read.
-template <int V, int LPP, int UNR>
+template <int V, int LPP, int UNR, bool LP = false>
 __global__ void __launch_bounds__(256)
     k22_runs_gather(const uint8_t *__restrict__ runid, int64_t ldn, int64_t n, int64_t dl,
                     const double *__restrict__ U, int64_t m, const double *__restrict__ hsum,
@@ -1422,7 +1422,101 @@ __global__ void __launch_bounds__(256)
   }
 #pragma unroll
   for (int q = 0; q < V; ++q)
-    Y[i * ldy + c0 + q] = 2.0 * acc[q] + fma(-hsum[i], Sg[c0 + q], Sg[m + c0 + q]);
+    Y[i * ldy + c0 + q] = LP ? acc[q]  // l_p^p: the table holds each coordinate's whole term
+                             : 2.0 * acc[q] + fma(-hsum[i], Sg[c0 + q], Sg[m + c0 + q]);
+}
+
+// Odd p (DESIGN.md §2b over runs, §2f): with H_j = sum of z over run j (the histogram), per
+// (coordinate, column) the totals T_t = sum_j v_j^t H_j, then in run order the exclusive
+// moments M_t(j) and W_j = sum_t c_t v_j^(P-t) (2 M_t(j) - T_t) in place of H — the same value
+// every row of run j gets in the sorted scan (rows of the run itself contribute |v - v|^p = 0).
+template <int P>
+__global__ void __launch_bounds__(256)
+    k21_runs_scan_lp(double *__restrict__ H, const float *__restrict__ rvals,
+                     const uint32_t *__restrict__ nruns, int64_t dl, int64_t m) {
+  constexpr int K = P + 1;
+  const int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (e >= dl * m) return;
+  const int64_t k = e / m, c = e - (e / m) * m;
+  const uint32_t R = nruns[k];
+  double T[K], M[K];
+#pragma unroll
+  for (int t = 0; t < K; ++t) T[t] = M[t] = 0.0;
+  for (uint32_t j = 0; j < R; ++j) {
+    const double h = H[(k * 256 + j) * m + c], v = (double)rvals[k * 256 + j];
+    double hv = h;
+#pragma unroll
+    for (int t = 0; t < K; ++t) {
+      T[t] += hv;
+      hv *= v;
+    }
+  }
+  for (uint32_t j = 0; j < R; ++j) {
+    double *hp = H + (k * 256 + j) * m + c;
+    const double h = *hp, v = (double)rvals[k * 256 + j];
+    double vp[K];
+    vp[0] = 1.0;
+#pragma unroll
+    for (int t = 1; t < K; ++t) vp[t] = vp[t - 1] * v;
+    double w = 0.0;
+#pragma unroll
+    for (int t = 0; t < K; ++t) {
+      double b = 1.0;  // c_t = C(P, t) (-1)^t
+      for (int q = 0; q < t; ++q) b = b * (double)(P - q) / (double)(q + 1);
+      w = fma(((t & 1) ? -b : b) * vp[P - t], fma(2.0, M[t], -T[t]), w);
+    }
+    *hp = w;
+    double hv = h;
+#pragma unroll
+    for (int t = 0; t < K; ++t) {
+      M[t] += hv;
+      hv *= v;
+    }
+  }
+}
+
+void launch_runs_lp(const uint8_t *runid, int64_t ldn, int64_t n, int64_t dl, const float *rvals,
+                    const uint32_t *nruns, const float *Z, int64_t ldz, int64_t m, int lp,
+                    double *H, double *Y, int64_t ldy, int phase, cudaStream_t s) {
+  // phase 0: R1 as for l1 (the run sums of z), then the p-moment scan over runs in place of
+  // the l1 prefix; phase 1: the expansion without the l1 epilogue (no g - h S for p > 1)
+  if (phase == 0) {
+    cudaMemsetAsync(H, 0, (size_t)dl * 256 * m * sizeof(double), s);
+    const int L = m >= 32 ? 32 : (m > 16 ? 32 : m > 8 ? 16 : m > 4 ? 8 : m > 2 ? 4 : m > 1 ? 2 : 1);
+    const int64_t pts_per_cta = 8 * (32 / L) * 16;
+    const int kg = 8;
+    dim3 g1((unsigned)((n + pts_per_cta - 1) / pts_per_cta), (unsigned)((dl + kg - 1) / kg));
+    k20_runs_hist<<<g1, 256, 0, s>>>(runid, ldn, n, dl, Z, ldz, m, kg, H);
+    const unsigned g2 = (unsigned)((dl * m + 255) / 256);
+    switch (lp) {
+      case 3: k21_runs_scan_lp<3><<<g2, 256, 0, s>>>(H, rvals, nruns, dl, m); break;
+      case 5: k21_runs_scan_lp<5><<<g2, 256, 0, s>>>(H, rvals, nruns, dl, m); break;
+      case 7: k21_runs_scan_lp<7><<<g2, 256, 0, s>>>(H, rvals, nruns, dl, m); break;
+      default: break;
+    }
+    return;
+  }
+  auto g = [&](auto kern, int LPP, int V) {
+    const int ppb = 8 * (32 / LPP);
+    dim3 grid((unsigned)((n + ppb - 1) / ppb), (unsigned)((m + V * LPP - 1) / (V * LPP)));
+    kern<<<grid, 256, 0, s>>>(runid, ldn, n, dl, H, m, nullptr, nullptr, Y, ldy, 0);
+  };
+  if (m % 2 == 0) {
+    const int64_t lpp = m / 2;
+    if (lpp <= 1) g(k22_runs_gather<2, 1, 8, true>, 1, 2);
+    else if (lpp <= 2) g(k22_runs_gather<2, 2, 8, true>, 2, 2);
+    else if (lpp <= 4) g(k22_runs_gather<2, 4, 8, true>, 4, 2);
+    else if (lpp <= 8) g(k22_runs_gather<2, 8, 8, true>, 8, 2);
+    else if (lpp <= 16) g(k22_runs_gather<2, 16, 8, true>, 16, 2);
+    else g(k22_runs_gather<2, 32, 8, true>, 32, 2);
+  } else {
+    if (m <= 1) g(k22_runs_gather<1, 1, 8, true>, 1, 1);
+    else if (m <= 2) g(k22_runs_gather<1, 2, 8, true>, 2, 1);
+    else if (m <= 4) g(k22_runs_gather<1, 4, 8, true>, 4, 1);
+    else if (m <= 8) g(k22_runs_gather<1, 8, 8, true>, 8, 1);
+    else if (m <= 16) g(k22_runs_gather<1, 16, 8, true>, 16, 1);
+    else g(k22_runs_gather<1, 32, 8, true>, 32, 1);
+  }
 }
 
 void launch_runs_query(const uint8_t *runid, int64_t ldn, int64_t n, int64_t dl, const float *rvals,

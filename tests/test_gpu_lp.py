@@ -32,7 +32,7 @@ def lp_gpu(X, Z, p, mode="auto", k_range=None, tv=False):
     return out
 
 
-@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("mode", MODES + ["runs"])
 @pytest.mark.parametrize("name", GOLDEN_LP)
 def test_lp_goldens_exact(name, mode):
     X, Z, Y = load_golden(name)
@@ -59,13 +59,24 @@ def test_lp_random_float_vs_oracle(n, d, m, p, mode):
     assert col_rel_l2(lp_gpu(X, Z, p, mode), oracle.brute_lp(X, Z, p)) <= TOL[p]
 
 
-@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("mode", MODES + ["runs", "auto"])
 @pytest.mark.parametrize("p", [3, 5])
 def test_lp_integer_ties_exact(p, mode):
     rng = np.random.default_rng(100 + p)
     X = rng.integers(0, 5, size=(3001, 3)).astype(np.float32)
     Z = rng.integers(-3, 4, size=(3001, 6)).astype(np.float32)
     assert np.array_equal(lp_gpu(X, Z, p, mode), oracle.lp_sorted(X, Z, p))
+
+
+# runs mode (<= 256 distinct values per coordinate) for odd p: float values,
+# ragged n, m across the expansion's lane layouts (even / odd, > 32)
+@pytest.mark.parametrize("p", [3, 5, 7])
+@pytest.mark.parametrize("n,d,m", [(2, 1, 1), (999, 3, 2), (4097, 5, 7), (2500, 2, 40)])
+def test_lp_runs_float_few_values(n, d, m, p):
+    rng = np.random.default_rng(n + 3 * d + 11 * m + p)
+    X = (rng.integers(-40, 41, size=(n, d)) / 9.0).astype(np.float32)
+    Z = rng.standard_normal((n, m)).astype(np.float32)
+    assert col_rel_l2(lp_gpu(X, Z, p, "runs"), oracle.brute_lp(X, Z, p)) <= TOL[p]
 
 
 def test_lp_p1_entry_is_l1_and_bad_p_rejected():
