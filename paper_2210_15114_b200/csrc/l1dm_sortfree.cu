@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "l1dm_device.cuh"
 #include "l1dm_internal.h"
@@ -179,9 +180,134 @@ static int k12_g(int64_t d) { return d > 64 ? 4 : 2; }
 static size_t k12_smem(int G) {
   return ((size_t)kDmmaKs * (32 * G + 8) + (size_t)kDmmaKs * kDmmaPad) * sizeof(double);
 }
+// K12 with fp32 operand tiles streamed by cp.async through a 3-stage shared-memory ring (one
+// barrier per 32-point stage, no register staging), converted to fp64 (and raised to t) at
+// fragment load.  Needs 16-byte aligned rows and full 128-coordinate tiles (d % 128 == 0) and
+// 64-column tiles (m % 64 == 0 or the last tile zero-filled by chunk); K12<G> covers the rest.
+constexpr int kRing = 3;
+constexpr int kXs = 128 + 4, kZs = 64 + 4;  // padded fp32 row lengths (bank spread)
+__global__ void __launch_bounds__(256)
+    k12_moment_reduce_ring(const float *__restrict__ X, int64_t ldx, const float *__restrict__ Z,
+                           int64_t ldz, int64_t n, int64_t d, int64_t m, int p, int64_t chunk,
+                           double *__restrict__ part, double *__restrict__ colpart,
+                           double *__restrict__ gpart, int pg) {
+  constexpr int G = 4, TK = 128;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float *xs = reinterpret_cast<float *>(smem_raw);  // [kRing][kDmmaKs][kXs]
+  float *zs = xs + kRing * kDmmaKs * kXs;            // [kRing][kDmmaKs][kZs]
+  __shared__ double s_hp[kDmmaKs];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t k0 = (int64_t)blockIdx.x * TK, c0 = (int64_t)blockIdx.y * kTile;
+  const int t = 1 + (int)(blockIdx.z % p);
+  const int64_t ch = blockIdx.z / p;
+  const int64_t i0 = ch * chunk, i1 = (i0 + chunk < n) ? i0 + chunk : n;
+  const int rw = 8 * G * (w % 4), cw = 32 * (w / 4);
+  const bool colsum = colpart && t == 1 && blockIdx.x == 0;
+  const bool gsum = colsum && gpart && gridDim.x == 1;
+  double csum = 0.0, gsumc = 0.0;
+  double acc[G][4][2];
+#pragma unroll
+  for (int a = 0; a < G; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const int64_t nst = (i1 - i0 + kDmmaKs - 1) / kDmmaKs;
+  auto issue = [&](int64_t st) {
+    if (st < nst) {
+      const int64_t base = i0 + st * kDmmaKs;
+      float *xb = xs + (st % kRing) * kDmmaKs * kXs, *zb = zs + (st % kRing) * kDmmaKs * kZs;
+      // X: 32 rows x 32 chunks of 16 B; Z: 32 rows x 16 chunks
+      for (int e = tid; e < kDmmaKs * 32; e += 256) {
+        const int r = e >> 5, q = e & 31;
+        const bool ok = base + r < i1;
+        cp_async<16>(xb + r * kXs + 4 * q, ok ? (const void *)(X + (base + r) * ldx + k0 + 4 * q)
+                                              : (const void *)X, ok);
+      }
+      for (int e = tid; e < kDmmaKs * 16; e += 256) {
+        const int r = e >> 4, q = e & 15;
+        const bool ok = base + r < i1 && c0 + 4 * q < m;
+        cp_async<16>(zb + r * kZs + 4 * q, ok ? (const void *)(Z + (base + r) * ldz + c0 + 4 * q)
+                                              : (const void *)Z, ok);
+      }
+    }
+    cp_async_commit();
+  };
+  for (int st = 0; st < kRing - 1; ++st) issue(st);
+  for (int64_t st = 0; st < nst; ++st) {
+    cp_async_wait_group<kRing - 2>();
+    __syncthreads();  // stage st landed for every thread; stage st-1's buffer is free
+    issue(st + kRing - 1);
+    const float *xb = xs + (st % kRing) * kDmmaKs * kXs, *zb = zs + (st % kRing) * kDmmaKs * kZs;
+    if (gsum) {
+      const int r = tid >> 3, q0 = (tid & 7) * (TK / 8);
+      double h = 0.0;
+#pragma unroll
+      for (int q = 0; q < TK / 8; ++q) h += powi((double)xb[r * kXs + q0 + q], pg);
+#pragma unroll
+      for (int off = 4; off; off >>= 1) h += __shfl_xor_sync(0xFFFFFFFFu, h, off);
+      if ((tid & 7) == 0) s_hp[r] = h;
+      __syncthreads();
+    }
+    if (colsum && tid < kTile) {
+#pragma unroll 8
+      for (int r = 0; r < kDmmaKs; ++r) csum += (double)zb[r * kZs + tid];  // zero-filled rows
+      if (gsum) {
+#pragma unroll 8
+        for (int r = 0; r < kDmmaKs; ++r) gsumc = fma(s_hp[r], (double)zb[r * kZs + tid], gsumc);
+      }
+    }
+#pragma unroll
+    for (int kk = 0; kk < kDmmaKs / 4; ++kk) {
+      const int pt = 4 * kk + (lane & 3);
+      double a[G], b[4];
+#pragma unroll
+      for (int g = 0; g < G; ++g) a[g] = powi((double)xb[pt * kXs + rw + 8 * g + (lane >> 2)], t);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = (double)zb[pt * kZs + cw + 8 * j + (lane >> 2)];
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc[g][j][0], acc[g][j][1], a[g], b[j]);
+    }
+    if (gsum) __syncthreads();  // s_hp is rewritten by the next stage
+  }
+  cp_async_wait_all();
+  if (colsum && tid < kTile && c0 + tid < m) colpart[ch * m + c0 + tid] = csum;
+  if (gsum && tid < kTile && c0 + tid < m) gpart[ch * m + c0 + tid] = gsumc;
+  double *out = part + ((ch * p + (t - 1)) * d) * m;
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int64_t k = k0 + rw + 8 * g + (lane >> 2);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t c = c0 + cw + 8 * j + 2 * (lane & 3) + h;
+        if (c < m) out[k * m + c] = acc[g][j][h];
+      }
+  }
+}
+
 static void launch_k12(const float *X, int64_t ldx, const float *Z, int64_t ldz, int64_t n,
                        int64_t d, int64_t m, int p, int64_t chunk, int64_t nchunks, double *part,
                        double *colpart, double *gpart, int pg, cudaStream_t s) {
+  static const bool ring_env = [] {
+    const char *e = getenv("L1DM_K12_RING");
+    return e ? atoi(e) != 0 : true;
+  }();
+  if (ring_env && d % 128 == 0 && m % 4 == 0 && ldx % 4 == 0 && ldz % 4 == 0 &&
+      (uintptr_t)X % 16 == 0 && (uintptr_t)Z % 16 == 0) {
+    const size_t sm = (size_t)kRing * kDmmaKs * (kXs + kZs) * sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k12_moment_reduce_ring, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sm);
+      attr = true;
+    }
+    dim3 g((unsigned)(d / 128), (unsigned)((m + kTile - 1) / kTile), (unsigned)(p * nchunks));
+    k12_moment_reduce_ring<<<g, 256, sm, s>>>(X, ldx, Z, ldz, n, d, m, p, chunk, part, colpart,
+                                              gpart, pg);
+    return;
+  }
   const int G = k12_g(d);
   const size_t sm = k12_smem(G);
   dim3 g((unsigned)((d + 32 * G - 1) / (32 * G)), (unsigned)((m + kTile - 1) / kTile),

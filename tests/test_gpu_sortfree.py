@@ -24,7 +24,8 @@ def test_even_goldens_exact(name):
 # tiles of 64 points / 64 coordinates / 64 columns, ragged in every dimension
 @pytest.mark.parametrize("p", [2, 4, 6])
 @pytest.mark.parametrize("n,d,m", [(1, 1, 1), (5, 3, 2), (65, 63, 65), (1000, 7, 3),
-                                   (3001, 130, 17), (20000, 16, 64)])
+                                   (3001, 130, 17), (20000, 16, 64),
+                                   (3001, 128, 20), (1500, 256, 68)])  # cp.async ring K12
 def test_even_random_vs_oracle(n, d, m, p):
     rng = np.random.default_rng(n + 10 * d + 100 * m + p)
     X = rng.standard_normal((n, d)).astype(np.float32)
