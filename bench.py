@@ -474,8 +474,8 @@ def main_ours(args):
     if os.path.exists(prof) and args.p == 1:
         try:
             tr = json.load(open(prof))
-            traffic = tr.get(f"{'scatter' if plan['scatter'] else 'gather'}_{dominant}",
-                             tr.get(dominant))
+            strat = strategy or ("scatter" if plan["scatter"] else "gather")
+            traffic = tr.get(f"{strat}_{dominant}", tr.get(dominant))
         except Exception:
             traffic = None
     roof["traffic"] = traffic

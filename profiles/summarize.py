@@ -59,6 +59,10 @@ for r in rows[2:]:
         kind = "scatter_scan"
     elif "k5_scan_seq" in name:  # scatter mode: <mb, 0> reduce (timing kind scan), <mb, 1> apply
         kind = "scatter_accumulate" if ", 1>" in name or ",1>" in name else "scatter_scan"
+    elif "k20_runs_hist" in name:  # runs mode: the histogram (timing kind scan)
+        kind = "runs_scan"
+    elif "k22_runs" in name:  # runs mode: the expansion (timing kind accumulate)
+        kind = "runs_accumulate"
     elif "k5_scan" in name or "k6_accumulate" in name:
         kind = "gather_" + ("scan" if "scan" in name else "accumulate")
     else:
