@@ -88,3 +88,27 @@ def test_runs_shards_and_pipelined_blocks():
         assert np.array_equal(Y[i0:i1].cpu().numpy(), whole[i0:i1])
     l1.l1dm_sync(h)
     l1.l1dm_free(h)
+
+
+def test_query_strategy_reports_the_planner_choice():
+    """l1dm_query_strategy: runs on <= 256 distinct values (AUTO/RUNS), else the planner's
+    gather/scatter choice under the handle's mode."""
+    rng = np.random.default_rng(21)
+    Xi = torch.from_numpy(rng.integers(0, 50, size=(3000, 4)).astype(np.float32)).cuda()
+    h = l1.l1dm_prepare(Xi)
+    try:
+        assert l1.l1dm_query_strategy(h, 8) == "runs"
+        l1.l1dm_set_query_mode(h, "gather")
+        assert l1.l1dm_query_strategy(h, 8) == "gather"
+        l1.l1dm_set_query_mode(h, "scatter")
+        assert l1.l1dm_query_strategy(h, 8) == "scatter"
+    finally:
+        l1.l1dm_free(h)
+    Xf = torch.from_numpy(rng.standard_normal((1 << 17, 3)).astype(np.float32)).cuda()
+    h = l1.l1dm_prepare(Xf)
+    try:
+        assert l1.l1dm_query_strategy(h, 16) == "scatter"  # n >= 2^17, a block fits L2
+        with pytest.raises(l1.L1dmError):
+            l1.l1dm_set_query_mode(h, "runs")  # > 256 distinct values: no runs tables
+    finally:
+        l1.l1dm_free(h)
