@@ -162,3 +162,28 @@ def test_lp_c3_size_sampled(p):
     l1.l1dm_free(h)
     Yr = oracle.rows_lp(X.cpu().numpy(), Z.cpu().numpy(), p, rows)
     assert col_rel_l2(Yg, Yr) <= TOL[p]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("p", [3, 5])
+def test_lp_c5_size_runs_sampled_exact(p):
+    """BASELINE configs[4]'s shape (n = 2^23, d = 96, 8-bit integer coordinates, m = 16 of
+    +-1): runs mode for odd p.  At p = 3 every moment is an integer below 2^53 (255^3 n), so
+    sampled rows must equal the definition exactly; at p = 5 the moments exceed 2^53 and the
+    1e-9 bar applies."""
+    from paper_2210_15114_b200 import workloads as wl
+    w = wl.workload("c5")
+    X = wl.make_points(w, "cuda")
+    Z = wl.make_query(w, 0, "cuda")
+    h = l1.l1dm_prepare(X)
+    assert l1.l1dm_query_strategy(h, w.m) == "runs"
+    Y = l1.l1dm_matvec_lp(h, p, Z)
+    torch.cuda.synchronize()
+    rows = np.array([0, 1, 777, 4194305, w.n - 1])
+    Yg = Y[torch.from_numpy(rows).cuda()].cpu().numpy()
+    l1.l1dm_free(h)
+    Yr = oracle.rows_lp(X.cpu().numpy(), Z.cpu().numpy(), p, rows)
+    if p == 3:
+        assert np.array_equal(Yg, Yr)
+    else:
+        assert col_rel_l2(Yg, Yr) <= TOL[p]
