@@ -110,6 +110,18 @@ __device__ __forceinline__ void cp_async_hint(void *smem, const void *gmem, bool
                  : "memory");
   }
 }
+__device__ __forceinline__ uint4 ld_stream_u4_hint(const void *p, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_u32_hint(uint32_t *p, uint32_t v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v),
+               "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void st_f64_hint(double *p, double v, uint64_t pol) {
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol)
                : "memory");

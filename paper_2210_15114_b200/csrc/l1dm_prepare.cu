@@ -431,13 +431,16 @@ __global__ void __launch_bounds__(256)
   const int64_t r0 = (int64_t)blockIdx.x * kRankRows;
   const uint32_t *pp = perm + seg * ldn;
   uint32_t *rp = rank + seg * ldn;
+  // the perm stream must not evict the rank row being filled: a sector that leaves L2 before
+  // its 8 words arrive costs a DRAM read-modify-write (ncu: 3x write amplification on c4)
+  const uint64_t pol_stream = l2_policy_evict_first(), pol_keep = l2_policy_evict_last();
   for (int64_t r = r0 + 4 * threadIdx.x; r < r0 + kRankRows && r < n; r += 4 * 256) {
     if (r + 4 <= n) {
-      const uint4 q = ld_stream_u4(pp + r);
-      rp[q.x] = (uint32_t)r;
-      rp[q.y] = (uint32_t)(r + 1);
-      rp[q.z] = (uint32_t)(r + 2);
-      rp[q.w] = (uint32_t)(r + 3);
+      const uint4 q = ld_stream_u4_hint(pp + r, pol_stream);
+      st_u32_hint(rp + q.x, (uint32_t)r, pol_keep);
+      st_u32_hint(rp + q.y, (uint32_t)(r + 1), pol_keep);
+      st_u32_hint(rp + q.z, (uint32_t)(r + 2), pol_keep);
+      st_u32_hint(rp + q.w, (uint32_t)(r + 3), pol_keep);
     } else {
       for (int64_t u = r; u < n; ++u) rp[pp[u]] = (uint32_t)u;
     }
