@@ -6,6 +6,8 @@ $B --workload c2 --steps 10 > gpurun_out/r_c2.log 2>&1
 $B --workload c4 --steps 2 > gpurun_out/r_c4.log 2>&1
 $B --workload c5 --steps 3 > gpurun_out/r_c5.log 2>&1
 $B --p 3 --steps 2 --no-cpu-baseline > gpurun_out/r_c3_p3.log 2>&1
-$B --workload c5 --p 3 --steps 2 --no-cpu-baseline > gpurun_out/r_c5_p3.log 2>&1
+$B --p 2 --steps 2 --no-cpu-baseline > gpurun_out/r_c3_p2.log 2>&1
+$B --krylov 16 --steps 2 --no-cpu-baseline > gpurun_out/r_c3_krylov16.log 2>&1
+$B --l2approx 0.5 --steps 2 --no-cpu-baseline > gpurun_out/r_c3_l2approx05.log 2>&1
 bash profiles/run_profile.sh c3 "k5_scan_seq|k5_reduce_all"
-bash profiles/run_profile.sh c4 "k5_scan|k6_accumulate"
+bash profiles/run_profile.sh c2 "k5_scan_m1|k2_pass"
