@@ -230,3 +230,16 @@ def test_two_processes_ipc_peer_sum():
     mp.start_processes(ipc_worker, args=(2, free_port(), results), nprocs=2, join=True,
                        start_method="spawn")
     assert results[0] == [True] * 3 and results[1] == [True] * 3
+
+
+def test_peer_sum_more_ranks_than_rows():
+    """G = 5 ranks over n = 3 points: two owners hold no rows (empty inbox slots, reduce kernels
+    that only wait for their flags); the sum is still exact."""
+    rng = np.random.default_rng(3)
+    n, d, m, G = 3, 7, 2, 5
+    Xn = rng.integers(0, 4, size=(n, d)).astype(np.float32)
+    X = torch.from_numpy(Xn).cuda()
+    Zs = [torch.from_numpy(rng.integers(-2, 3, size=(n, m)).astype(np.float32)).cuda()]
+    outs = run_epochs(X, Zs, G, (0, 4), mode="gather")
+    want = oracle.brute(Xn, Zs[0].cpu().numpy())
+    assert np.array_equal(outs[0][0], want) and np.array_equal(outs[0][4], want)
