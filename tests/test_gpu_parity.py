@@ -282,3 +282,30 @@ def test_pinned_host_pipeline_async_queries():
     Yb = l1.l1dm_matvec(h, Zs[0], torch.empty((5000, 7), dtype=torch.float64).pin_memory())
     assert col_rel_l2(Yb.numpy(), oracle.brute(X, Zs[0].numpy())) <= TOL   # block=True default
     l1.l1dm_free(h)
+
+
+def test_handle_utilities_and_block_cache():
+    """l1dm_shape / l1dm_workspace_bytes on a sharded handle; handles recycling each other's
+    device blocks through the library's cache, then l1dm_release_cached, stay exact."""
+    import ctypes
+    rng = np.random.default_rng(77)
+    X = rng.integers(0, 9, size=(3000, 6)).astype(np.float32)
+    Z = rng.integers(-2, 3, size=(3000, 5)).astype(np.float32)
+    want = oracle.brute(X, Z)
+    Xt, Zt = torch.from_numpy(X).cuda(), torch.from_numpy(Z).cuda()
+    lib = l1.load_library()
+    for rep in range(3):
+        h = l1.l1dm_prepare(Xt, 1, 5)
+        vals = [ctypes.c_int64() for _ in range(4)]
+        assert lib.l1dm_shape(h.ptr, *[ctypes.byref(v) for v in vals]) == 0
+        assert [v.value for v in vals] == [3000, 4, 1, 5]  # n, d_local, k_begin, k_end
+        l1.l1dm_set_query_mode(h, "gather")
+        assert l1.l1dm_workspace_bytes(h, 5) >= 3000 * 4 * 5 * 8  # U of the shard
+        l1.l1dm_free(h)
+        h = l1.l1dm_prepare(Xt)
+        Y = l1.l1dm_matvec(h, Zt)
+        torch.cuda.synchronize()
+        assert np.array_equal(Y.cpu().numpy(), want), rep
+        l1.l1dm_free(h)
+        if rep == 1:
+            l1.l1dm_release_cached()
