@@ -42,7 +42,8 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--workload", default="c3",
+                    choices=["c1", "c2", "c3", "c4", "c5", "ctx1", "ctx2", "ctx3"])
     ap.add_argument("--queries", type=int, default=None, help="queries per step (default: recipe)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -641,6 +642,13 @@ def main_ours(args):
                                                          "sample", "per_core_query_updates_per_s")}
         except Exception as e:  # the baseline is reported, never required
             result["cpu_baseline"] = {"value": None, "error": str(e)}
+    if w.name in wl.PAPER_TABLE3:  # context only (SURVEY §8(d) ctx): the paper's M1/Numba times
+        pp, pq = wl.PAPER_TABLE3[w.name]
+        result["paper_context"] = {
+            "paper_prepare_s": pp, "paper_avg_query_s": pq,
+            "paper_hardware": "2021 M1 MacBook Pro, Python 3.9 + NumPy/Numba (P:360)",
+            "this_prepare_s": (prep_ms or 0.0) * 1e-3, "this_avg_query_s": result["query_ms"] * 1e-3,
+            "data": "synthetic stand-in of the same shape (Table 3, P:336-345)"}
     if rank == 0:
         print(json.dumps(result))
     if world > 1:

@@ -41,6 +41,8 @@ class Workload:
 
     @property
     def index(self) -> int:
+        if self.name.startswith("ctx"):
+            return 5 + int(self.name[3:])
         return int(self.name[1:]) if self.name[1:].isdigit() else 9
 
     @property
@@ -54,7 +56,17 @@ CONFIGS = {
     "c3": Workload("c3", 1 << 20, 128, 64, "uniform11", "normal", 2, 100, False),
     "c4": Workload("c4", 1 << 24, 128, 32, "gmm32", "normal", 3, 10, True),
     "c5": Workload("c5", 1 << 23, 96, 16, "int256", "pm1", 4, 10, True),
+    # SURVEY §8(d) "ctx" (optional): the shapes of the paper's Table 3, synthetic
+    # stand-ins, to place B200 times beside the paper's as context only: a 3-cluster Gaussian
+    # mixture in R^50, MNIST-like 8-bit integers in R^784 with 80% zeros (assumed: the paper
+    # does not describe its data), GloVe-like N(0,1) in R^50; m = 1, 10 Gaussian queries
+    "ctx1": Workload("ctx1", 50000, 50, 1, "gmm3", "normal", 5, 10, True),
+    "ctx2": Workload("ctx2", 50000, 784, 1, "mnist80", "normal", 6, 10, True),
+    "ctx3": Workload("ctx3", 1200000, 50, 1, "normal", "normal", 7, 10, True),
 }
+# Table 3's "Ours" rows (2021 M1 MacBook Pro, Python + NumPy/Numba):
+# (preprocessing s, average query s) — context, not a target
+PAPER_TABLE3 = {"ctx1": (0.55, 0.09), "ctx2": (5.5, 1.9), "ctx3": (16.8, 3.4)}
 
 
 def workload(name: str, n: int | None = None, d: int | None = None, m: int | None = None,
@@ -97,6 +109,19 @@ def make_points(w: Workload, device="cpu") -> torch.Tensor:
         X.mul_(0.5)
         X.add_(centres.index_select(0, assign))
         return X
+    if w.x_dist == "gmm3":  # 3 spherical clusters, centres U[-10, 10]^d, sigma 0.5 (as c4)
+        centres = torch.rand((3, d), generator=g, device=device, dtype=torch.float32)
+        centres.mul_(20.0).sub_(10.0)
+        assign = torch.randint(0, 3, (n,), generator=g, device=device)
+        X = torch.randn((n, d), generator=g, device=device, dtype=torch.float32)
+        X.mul_(0.5)
+        X.add_(centres.index_select(0, assign))
+        return X
+    if w.x_dist == "mnist80":  # integers 1..255 with probability 0.2, else 0
+        v = torch.rand((n, d), generator=g, device=device, dtype=torch.float32)
+        keep = torch.rand((n, d), generator=g, device=device, dtype=torch.float32) < 0.2
+        return torch.where(keep, v.mul_(255.0).floor_().add_(1.0).clamp_(1.0, 255.0),
+                           torch.zeros_like(v))
     if w.x_dist == "int256":
         X = torch.rand((n, d), generator=g, device=device, dtype=torch.float32)
         return X.mul_(256.0).floor_().clamp_(0.0, 255.0)
