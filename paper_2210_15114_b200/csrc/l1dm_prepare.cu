@@ -35,32 +35,49 @@ __global__ void __launch_bounds__(256)
   __shared__ float tile[kT0Points][kT0Coords + 1];
   const int64_t i0 = (int64_t)blockIdx.x * kT0Points;
   const int tid = threadIdx.x;
-  double hacc = 0.0;
-  int bad = 0;
-  for (int64_t kt = 0; kt < dl; kt += kT0Coords) {
-    for (int e = tid; e < kT0Points * kT0Coords; e += 256) {
+  constexpr int PER = kT0Points * kT0Coords / 256;  // elements per thread per chunk
+  // the next chunk's values are loaded into registers while the current one is written out
+  float xr[PER];
+  auto load = [&](int64_t kt) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = tid + 256 * u;
       const int p = e / kT0Coords, c = e % kT0Coords;
       const int64_t i = i0 + p, k = kt + c;
-      float x = 0.0f;
-      if (i < n && k < dl) {
-        x = X[i * ldx + k0 + k];
-        if (!isfinite(x)) bad = 1;
-      }
-      tile[p][c] = x;
+      xr[u] = (i < n && k < dl) ? __ldg(X + i * ldx + k0 + k) : 0.0f;
+    }
+  };
+  double hacc = 0.0;  // threads with (tid & 3) == 0: point i0 + tid / 4
+  int bad = 0;
+  load(0);
+  for (int64_t kt = 0; kt < dl; kt += kT0Coords) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = tid + 256 * u;
+      if (!isfinite(xr[u])) bad = 1;
+      tile[e / kT0Coords][e % kT0Coords] = xr[u];
     }
     __syncthreads();
-    if (tid < kT0Points) {
-      const int kmax = (int)((dl - kt) < kT0Coords ? (dl - kt) : kT0Coords);
-      for (int c = 0; c < kmax; ++c) hacc += (double)tile[tid][c];  // fixed order k = 0..dl-1
+    if (kt + kT0Coords < dl) load(kt + kT0Coords);
+    {  // h_i: 4 threads per point, 8 coordinates each, then a fixed 2-level tree
+      const int p = tid >> 2, q = tid & 3;
+      double part = 0.0;
+#pragma unroll
+      for (int c = 0; c < kT0Coords / 4; ++c) part += (double)tile[p][q * (kT0Coords / 4) + c];
+      part += __shfl_xor_sync(0xFFFFFFFFu, part, 1);
+      part += __shfl_xor_sync(0xFFFFFFFFu, part, 2);
+      hacc += part;  // (zero past dl and past n)
     }
-    for (int e = tid; e < kT0Points * kT0Coords; e += 256) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = tid + 256 * u;
       const int c = e / kT0Points, p = e % kT0Points;
       const int64_t i = i0 + p, k = kt + c;
       if (i < n && k < dl) key[k * ldn + i] = float_to_key(tile[p][c]);
     }
     __syncthreads();
   }
-  if (tid < kT0Points && i0 + tid < n) hsum[i0 + tid] = hacc;
+  if ((tid & 3) == 0 && i0 + (tid >> 2) < n) hsum[i0 + (tid >> 2)] = hacc;
   if (__syncthreads_or(bad) && tid == 0) atomicOr(nonfinite, 1u);
 }
 
