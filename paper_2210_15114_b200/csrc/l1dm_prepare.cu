@@ -552,6 +552,10 @@ __global__ void __launch_bounds__(256)
 // runid[k][i] = the index of x_ik among rvals[k][0..R_k) (binary search; -0.0 == +0.0 as in
 // the sort's key canonicalisation).  Tiles of 64 points x 32 coordinates of X staged in shared
 // memory (as K0), so X is read in whole rows and runid written in whole segments.
+// grid (point blocks of kIdPoints, 32-coordinate chunks): a chunk's distinct values are staged
+// once per CTA and serve kIdPoints / 64 point tiles (staging them per 64 points read 32 KB of
+// L2 per 8 KB of X)
+constexpr int kIdPoints = 1024;
 __global__ void __launch_bounds__(256)
     k_runs_ids(const float *__restrict__ X, int64_t n, int64_t ldx, int64_t k0, int64_t dl,
                int64_t ldn, const float *__restrict__ rvals, const uint32_t *__restrict__ nruns,
@@ -559,20 +563,22 @@ __global__ void __launch_bounds__(256)
   __shared__ float tile[kT0Points][kT0Coords + 1];
   __shared__ float s_vals[kT0Coords][256];
   __shared__ uint32_t s_nr[kT0Coords];
-  const int64_t i0 = (int64_t)blockIdx.x * kT0Points;
   const int tid = threadIdx.x;
-  for (int64_t kt = 0; kt < dl; kt += kT0Coords) {
+  const int64_t kt = (int64_t)blockIdx.y * kT0Coords;
+  for (int e = tid; e < kT0Coords * 256; e += 256) {
+    const int c = e / 256, j = e % 256;
+    s_vals[c][j] = (kt + c < dl) ? rvals[(kt + c) * 256 + j] : 0.0f;
+  }
+  if (tid < kT0Coords) s_nr[tid] = (kt + tid < dl) ? nruns[kt + tid] : 1u;
+  for (int sub = 0; sub < kIdPoints / kT0Points; ++sub) {
+    const int64_t i0 = (int64_t)blockIdx.x * kIdPoints + (int64_t)sub * kT0Points;
+    if (i0 >= n) break;
     __syncthreads();
     for (int e = tid; e < kT0Points * kT0Coords; e += 256) {
       const int p = e / kT0Coords, c = e % kT0Coords;
       const int64_t i = i0 + p, k = kt + c;
       tile[p][c] = (i < n && k < dl) ? X[i * ldx + k0 + k] : 0.0f;
     }
-    for (int e = tid; e < kT0Coords * 256; e += 256) {
-      const int c = e / 256, j = e % 256;
-      s_vals[c][j] = (kt + c < dl) ? rvals[(kt + c) * 256 + j] : 0.0f;
-    }
-    if (tid < kT0Coords) s_nr[tid] = (kt + tid < dl) ? nruns[kt + tid] : 1u;
     __syncthreads();
     for (int e = tid; e < kT0Points * kT0Coords; e += 256) {
       const int c = e / kT0Points, p = e % kT0Points;
@@ -605,7 +611,7 @@ void launch_runs_emit(const float *sval, int64_t n, int64_t ldn, int64_t dl,
 
 void launch_runs_ids(const float *X, int64_t n, int64_t ldx, int64_t k0, int64_t dl, int64_t ldn,
                      const float *rvals, const uint32_t *nruns, uint8_t *runid, cudaStream_t s) {
-  dim3 grid((unsigned)((n + kT0Points - 1) / kT0Points));
+  dim3 grid((unsigned)((n + kIdPoints - 1) / kIdPoints), (unsigned)((dl + kT0Coords - 1) / kT0Coords));
   k_runs_ids<<<grid, 256, 0, s>>>(X, n, ldx, k0, dl, ldn, rvals, nruns, runid);
 }
 
