@@ -521,15 +521,30 @@ __global__ void __launch_bounds__(256)
     k_runs_emit(const float *__restrict__ sval, int64_t n, int64_t ldn, int64_t tiles,
                 const uint32_t *__restrict__ tile_off, float *__restrict__ rvals) {
   constexpr int ITEMS = kRunTile / 256;
+  constexpr int PAD = ITEMS + 1;  // padded rows of the staged tile: conflict-free per-thread runs
   const int64_t seg = blockIdx.y, tile = blockIdx.x;
   const float *v = sval + seg * ldn;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int64_t rt = tile * kRunTile + (int64_t)tid * ITEMS;  // this thread's consecutive rows
+  const int64_t r0 = tile * kRunTile;
+  const int64_t rt = r0 + (int64_t)tid * ITEMS;  // this thread's consecutive rows
+  // the tile's values staged with coalesced loads (+ the row before it), then each thread reads
+  // its ITEMS consecutive rows from shared memory
+  __shared__ uint32_t s_v[256 * PAD];
+  __shared__ uint32_t s_prev;
+  for (int e = tid; e < kRunTile; e += 256) {
+    const int64_t r = r0 + e;
+    s_v[(e / ITEMS) * PAD + (e % ITEMS)] = r < n ? __float_as_uint(v[r]) : 0u;
+  }
+  if (tid == 0) s_prev = r0 > 0 ? __float_as_uint(v[r0 - 1]) : 0u;
+  __syncthreads();
   uint32_t f[ITEMS], cnt = 0;
 #pragma unroll
   for (int j = 0; j < ITEMS; ++j) {
     const int64_t r = rt + j;
-    f[j] = (r < n && (r == 0 || __float_as_uint(v[r]) != __float_as_uint(v[r - 1]))) ? 1u : 0u;
+    const uint32_t cur = s_v[tid * PAD + j];
+    const uint32_t prev = j > 0 ? s_v[tid * PAD + j - 1]
+                                : (tid > 0 ? s_v[(tid - 1) * PAD + ITEMS - 1] : s_prev);
+    f[j] = (r < n && (r == 0 || cur != prev)) ? 1u : 0u;
     cnt += f[j];
   }
   if (!__syncthreads_or(cnt)) return;  // no run starts in this tile
@@ -546,7 +561,7 @@ __global__ void __launch_bounds__(256)
   for (int ww = 0; ww < w; ++ww) run += s_w[ww];
 #pragma unroll
   for (int j = 0; j < ITEMS; ++j)
-    if (f[j]) rvals[seg * 256 + run++] = v[rt + j];
+    if (f[j]) rvals[seg * 256 + run++] = __uint_as_float(s_v[tid * PAD + j]);
 }
 
 // runid[k][i] = the index of x_ik among rvals[k][0..R_k) (binary search; -0.0 == +0.0 as in
