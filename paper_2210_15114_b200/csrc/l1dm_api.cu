@@ -220,6 +220,7 @@ struct l1dm_ctx {
   DevBuf<double> hsum;
   // runs of equal values (every coordinate <= 256 distinct values)
   bool has_runs = false;
+  bool rank_ready = false;  // rank = perm^-1 is built on first use (gather-mode queries only)
   DevBuf<uint8_t> runid;   // [dl][ldn] run index of point i
   DevBuf<float> rvals;     // [dl][256] distinct values, ascending
   DevBuf<uint32_t> nruns;  // [dl]
@@ -426,7 +427,6 @@ l1dm_status prepare_impl(const float *X, int64_t n, int64_t ld_x, int64_t k_begi
   DevBuf<unsigned long long> status;
   DevBuf<unsigned> ctrl;  // [0] nonfinite, [1] timeout, [2] ticket
   CUDA_TRY(keyA.ensure(elems, false, s));
-  CUDA_TRY(h->rank.ensure(elems, false, s));
   CUDA_TRY(h->hsum.ensure((size_t)n, false, s));
   CUDA_TRY(hist.ensure((size_t)dl * 1024, true, s));
   CUDA_TRY(ctrl.ensure(4, true, s));
@@ -474,8 +474,10 @@ l1dm_status prepare_impl(const float *X, int64_t n, int64_t ld_x, int64_t k_begi
   if (P == 0) {
     // keyA holds the keys; emit in place (sval bits over keyA), perm into valA.
     CUDA_TRY(valA.ensure(elems, false, s));
+    CUDA_TRY(h->rank.ensure(elems, false, s));
     launch_identity_emit(keyA.p, reinterpret_cast<float *>(keyA.p), valA.p, h->rank.p, n, ldn, dl,
                          s);
+    h->rank_ready = true;
     h->kernel_launches++;
     h->sval_bits.p = keyA.p;
     h->sval_bits.count = keyA.count;
@@ -511,6 +513,7 @@ l1dm_status prepare_impl(const float *X, int64_t n, int64_t ld_x, int64_t k_begi
     const int64_t tiles = (n + kSortTile - 1) / kSortTile;
     CUDA_TRY(status.ensure((size_t)dl * tiles * 256, true, s));
     static const bool fused_rank = getenv("L1DM_FUSED_RANK") != nullptr;  // tuning switch
+    if (fused_rank) CUDA_TRY(h->rank.ensure(elems, false, s));
     lap("alloc sort buffers");
     uint32_t *kb[2] = {keyA.p, keyB.p};
     uint32_t *vb[2] = {valA.p, valB.p};
@@ -525,10 +528,9 @@ l1dm_status prepare_impl(const float *X, int64_t n, int64_t ld_x, int64_t k_begi
       sort_prof_print(s);  // no-op unless built with L1DM_SORT_PROF
       CUDA_TRY(cudaGetLastError());
     }
-    if (!fused_rank) {
-      launch_rank(vb[P & 1], h->rank.p, n, ldn, dl, s);
-      h->kernel_launches++;
-    }
+    // without the fused variant, rank (only gather-mode queries read it) is built lazily by
+    // ensure_rank: scatter and runs queries never pay for it
+    h->rank_ready = fused_rank;
     const int fin = P & 1;
     DevBuf<uint32_t> *kbuf[2] = {&keyA, &keyB};
     DevBuf<uint32_t> *vbuf[2] = {&valA, &valB};
@@ -662,6 +664,18 @@ bool use_runs(const l1dm_ctx *h) {
 
 // blocked (scatter mode, m > 1 only): Y is column-block-major — block cb at Y + cb n mb with
 // row stride mb — and events[cb] is recorded once block cb is final (nblocks = col_blocks).
+// rank[k][perm[k][r]] = r (K3), built the first time a query needs it (gather mode's
+// accumulate, the l_p gather path, debug export): the scatter and runs strategies never read it
+l1dm_status ensure_rank(l1dm_ctx *h, cudaStream_t s) {
+  if (h->rank_ready) return L1DM_OK;
+  CUDA_TRY(h->rank.ensure((size_t)h->dl * (size_t)h->ldn, false, s));
+  launch_rank(h->perm.p, h->rank.p, h->n, h->ldn, h->dl, s);
+  CUDA_TRY(cudaGetLastError());
+  h->kernel_launches++;
+  h->rank_ready = true;
+  return L1DM_OK;
+}
+
 // pd (peer push): the final pass stores each finished row into its owner's inbox
 // slot instead of Y (gather mode's last accumulate, scatter mode's block write-out); Y is then
 // only the gather mode's scratch between coordinate chunks.  Callers pass pd only when
@@ -847,6 +861,10 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
       }
     }
   }
+  if (!p.scatter) {
+    l1dm_status rs = ensure_rank(h, s);
+    if (rs != L1DM_OK) return rs;
+  }
   for (int64_t c = 0; !p.scatter && c < p.chunks; ++c) {
     const int64_t k_first = c * p.kc;
     const int64_t kcc = std::min<int64_t>(p.kc, h->dl - k_first);
@@ -940,8 +958,13 @@ l1dm_status lp_device(l1dm_ctx *h, int lp, const float *Z, int64_t ldz, int64_t 
   CUDA_TRY(h->zt.ensure((size_t)p.zt_floats, false, s));
   CUDA_TRY(h->agg.ensure(p.lb_slots * (size_t)K * p.mb, false, s));
   CUDA_TRY(h->part.ensure((size_t)h->dl * ld_seg, false, s));
-  if (p.scatter) CUDA_TRY(h->yt.ensure((size_t)h->n * p.mb, false, s));
-  else CUDA_TRY(h->U.ensure((size_t)p.kc * (size_t)h->n * (size_t)m, false, s));
+  if (p.scatter) {
+    CUDA_TRY(h->yt.ensure((size_t)h->n * p.mb, false, s));
+  } else {
+    CUDA_TRY(h->U.ensure((size_t)p.kc * (size_t)h->n * (size_t)m, false, s));
+    l1dm_status rs = ensure_rank(h, s);  // the accumulate gathers U at each point's rank
+    if (rs != L1DM_OK) return rs;
+  }
   {
     TimedScope ts(h, kColsums, s);
     launch_zt(Z, ldz, h->n, m, p.mb, h->zt.p, s);
@@ -1755,9 +1778,12 @@ l1dm_status l1dm_debug_export(l1dm_handle h, float *sval, uint32_t *perm, uint32
   if (perm)
     CUDA_TRY(cudaMemcpy2DAsync(perm, row, h->perm.p, pitch, row, (size_t)h->dl, cudaMemcpyDefault,
                                h->stream));
-  if (rank)
+  if (rank) {
+    st = ensure_rank(h, h->stream);
+    if (st != L1DM_OK) return st;
     CUDA_TRY(cudaMemcpy2DAsync(rank, row, h->rank.p, pitch, row, (size_t)h->dl, cudaMemcpyDefault,
                                h->stream));
+  }
   if (hsum)
     CUDA_TRY(cudaMemcpyAsync(hsum, h->hsum.p, (size_t)h->n * sizeof(double), cudaMemcpyDefault,
                              h->stream));
