@@ -68,7 +68,10 @@ typedef enum {
  *   sval[k][r] = x_{perm[k][r], k}   sorted values T_k
  *   perm[k][r]                       the order pi^k induced by T_k
  *   rank[k][i] = r with perm[k][r]=i "position of x_i(k) in T_k"
+ *                (built on the handle's stream by the first query that reads it — gather
+ *                mode — not by prepare: scatter and runs queries never need it)
  *   h[i]       = sum_k x_ik (fp64)   per-point coordinate sum (query epilogue)
+ * plus, when every coordinate takes <= 256 distinct values, the runs tables.
  * Ties are ordered by point index; -0.0 is ordered as +0.0.
  * X: n x d fp32 (ld_x = d), host or device, BORROWED for the call only (the
  * library copies what it needs).  Synchronous: returns when the state is
