@@ -49,6 +49,35 @@ __global__ void __launch_bounds__(256) gather_sectors(const uint32_t *idx, int64
   }
   if (acc == 1.2345f) out[0] = acc;
 }
+// one random 4-byte element per lane (32 rows per warp request): the m = 1 reduce pass's pattern
+__global__ void __launch_bounds__(256) gather_lanes(const uint32_t *idx, int64_t rows,
+                                                    const float *z, uint32_t zwords, float *out) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  float acc = 0.f;
+  for (int64_t r = tid; r < rows; r += nt * 4) {
+    uint32_t p[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) p[u] = (r + u * nt < rows) ? __ldcs(idx + r + u * nt) : 0u;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc += __ldcg(z + (p[u] % zwords));
+  }
+  if (acc == 1.2345f) out[0] = acc;
+}
+// one random fp64 reduction per lane (the m = 1 apply pass's pattern)
+__global__ void __launch_bounds__(256) red_lanes(const uint32_t *idx, int64_t rows, double *y,
+                                                 uint32_t ywords) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = tid; r < rows; r += nt * 4) {
+    uint32_t p[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) p[u] = (r + u * nt < rows) ? __ldcs(idx + r + u * nt) : 0u;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (r + u * nt < rows) atomicAdd(y + (p[u] % ywords), 1.0);
+  }
+}
 __global__ void __launch_bounds__(256) stream_read(const float4 *z, int64_t n4, int reps,
                                                    float *out) {
   float acc = 0.f;
@@ -100,12 +129,16 @@ int main() {
   const uint32_t yrows = (uint32_t)((64ll << 20) / 64), zrows = (uint32_t)((32ll << 20) / 32);
   const float t_red = best_ms([&] { red_rows<<<grid, 256>>>(idx, rows, y, yrows); });
   const float t_gat = best_ms([&] { gather_sectors<<<grid, 256>>>(idx, rows, z, zrows, out); });
+  const float t_gl = best_ms([&] { gather_lanes<<<grid, 256>>>(idx, rows, z, zrows * 8, out); });
+  const float t_rl = best_ms([&] { red_lanes<<<grid, 256>>>(idx, rows, y, yrows * 8); });
   const int reps = 64;
   const float t_str = best_ms([&] {
     stream_read<<<grid, 256>>>(reinterpret_cast<const float4 *>(z), (32ll << 20) / 16, reps, out);
   });
   const cudaError_t e = cudaGetLastError();
-  printf("{\"red_row8_adds_per_s\": %.4g, \"gather_sector_GBps\": %.1f, "
+  printf("{\"gather_lane_per_s\": %.4g, \"red_lane_per_s\": %.4g, ", rows / (t_gl * 1e-3),
+         rows / (t_rl * 1e-3));
+  printf("\"red_row8_adds_per_s\": %.4g, \"gather_sector_GBps\": %.1f, "
          "\"stream_read_GBps\": %.1f, \"sms\": %d, \"l2_bytes\": %d, \"sm_clock_khz\": %d, "
          "\"status\": \"%s\", \"how\": \"tools/l2_probe.cu: 2^27 random rows, L2-resident "
          "buffers (RED 64 MiB, gather 32 MiB), best of 5 CUDA-event timings\"}\n",

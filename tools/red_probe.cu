@@ -65,6 +65,8 @@ int main() {
   fill_idx<<<sms * 8, 256>>>(idx, rows);
   const int grid = sms * 8;
   printf("{");
+  run<double, 1>("f64", idx, rows, y, grid);
+  run<double, 2>("f64", idx, rows, y, grid);
   run<double, 4>("f64", idx, rows, y, grid);
   run<double, 8>("f64", idx, rows, y, grid);
   run<double, 16>("f64", idx, rows, y, grid);
