@@ -461,12 +461,20 @@ def main_ours(args):
             # query makes two random 32-byte sector accesses (the z gather of the reduce pass and
             # the fp64 reduction into Y of the apply pass) — bound by the L2's random-sector
             # rate, measured by tools/l2_probe.cu (profiles/l2_peaks.json gather_sector_GBps)
+            # per (point, coordinate): one random 4-byte z gather (reduce pass) and one random
+            # fp64 reduction into Y (apply pass), each at the L2's measured per-lane rate
+            # (tools/l2_probe.cu: gather_lane_per_s, red_lane_per_s); the passes run in turn,
+            # so the ceiling is the harmonic combination of the two rates
             sc = kern["scan"]
-            secs = agg.get("scan_pairs", 0) * 2 * 32
-            ach = secs / (sc["ms_total"] * 1e-3) / 1e9 if sc["ms_total"] else None
-            peak = l2p.get("gather_sector_GBps", 5712.0)
-            roof = {"bound": "l2_random_sectors", "kernel": "scan (k5_scan_m1 reduce/prefix/apply)",
-                    "achieved": ach, "peak": peak, "unit": "GB/s (32-B sectors)",
+            pairs = agg.get("scan_pairs", 0)
+            g = l2p.get("gather_lane_per_s", 2.69e11)
+            r = l2p.get("red_lane_per_s", 1.745e11)
+            peak = 1.0 / (1.0 / g + 1.0 / r) / 1e9
+            ach = pairs / (sc["ms_total"] * 1e-3) / 1e9 if sc["ms_total"] else None
+            roof = {"bound": "l2_random_access", "kernel": "scan (k5_scan_m1 reduce/prefix/apply)",
+                    "achieved": ach, "peak": peak,
+                    "unit": "G (point, coordinate) pairs/s: one random 4-B gather + one random "
+                            "fp64 reduction each",
                     "peak_kind": "measured (tools/l2_probe.cu -> profiles/l2_peaks.json)",
                     "frac": (ach / peak) if ach else None,
                     "note": "m = 1: L2-resident z and Y; HBM carries only the sorted tables"}

@@ -969,14 +969,14 @@ bool launch_reduce_all(const uint32_t *perm, const float *sval, int64_t ldn, int
 // Each thread owns ITEMS *consecutive* sorted rows (thread-sequential scan, one warp scan per
 // tile); shared-memory rows are padded (4 floats every 32) so its 128-bit reads are
 // bank-conflict free.
-constexpr int kM1Items = 16;
+constexpr int kM1Items = L1DM_M1_ROW_ITEMS;
 constexpr int kM1Rows = 256 * kM1Items;  // rows per tile
 __device__ __forceinline__ int m1_pad(int r) { return r + (r >> 5) * 4; }
 
 enum { M1_REDUCE = 0, M1_APPLY_STORE = 1, M1_APPLY_SCATTER = 2 };
 
 template <int MODE>
-__global__ void __launch_bounds__(256, 4)
+__global__ void __launch_bounds__(256, L1DM_M1_MINB)
     k5_scan_m1(const uint32_t *__restrict__ perm, const float *__restrict__ sval, int64_t ldn,
                int64_t n, const float *__restrict__ Z, int64_t ldz, double *__restrict__ U,
                int64_t ldu, int64_t k_first, int64_t nseg, int64_t tiles_per_seg,

@@ -8,7 +8,7 @@ L2 = 126 << 20
 
 def scan_items(lpr, vc):
     if lpr == 1 and vc == 1:
-        return 16                      # the single-column kernel: 16 consecutive rows per thread
+        return 8                       # the single-column kernel: 8 consecutive rows per thread
     budget = 65536 if lpr == 32 else 98304  # stage bytes per tile (l1dm_internal.h)
     it = (budget // (1024 * vc + 2048 // lpr)) // 4 * 4
     return min(it, 64)
