@@ -71,6 +71,9 @@ void launch_runs_ids(const float *X, int64_t n, int64_t ldx, int64_t k0, int64_t
 #ifndef L1DM_SCAN_SMEM
 #define L1DM_SCAN_SMEM(lpr) ((lpr) == 32 ? 65536 : 98304)
 #endif
+#ifndef L1DM_RA_TILES
+#define L1DM_RA_TILES 2  // 1024-row tiles per reduce-all CTA (a power of two <= 8)
+#endif
 #ifndef L1DM_M1_ROW_ITEMS
 #define L1DM_M1_ROW_ITEMS 8  // m = 1 scan: consecutive rows per thread (tile = 256 x this); 8 measured best (c2: 16 -> 8 cut the scan 0.91 -> 0.72 ms)
 #endif
