@@ -374,6 +374,11 @@ def main_ours(args):
         ach = (red / (sc["ms_total"] * 1e-3) / 1e9) if sc["ms_total"] else None
         peak = l2p.get("red_row8_adds_per_s", 5.88e11) / 1e9
         roof = {"bound": "l2_fp64_reductions",
+                "note": "the histogram's reductions concentrate on a 3 MiB table (dl x 256 x m); "
+                        "every random-row probe of tools/l2_probe.cu (64 MiB or 4 MiB buffers, "
+                        "shallow or deep, hashed or streamed indices, per-table windows) stays "
+                        "at 5.9-6.1e11/s, below what this kernel sustains, so frac can exceed 1: "
+                        "the probe is not a tight ceiling for this pattern",
                 "kernel": "run histogram (k20_runs_hist + the scan over runs)",
                 "achieved": ach, "peak": peak, "unit": "G fp64 reductions/s",
                 "peak_kind": "measured (tools/l2_probe.cu -> profiles/l2_peaks.json)",

@@ -74,6 +74,12 @@ void launch_runs_ids(const float *X, int64_t n, int64_t ldx, int64_t k0, int64_t
 #ifndef L1DM_RA_TILES
 #define L1DM_RA_TILES 2  // 1024-row tiles per reduce-all CTA (a power of two <= 8)
 #endif
+#ifndef L1DM_RUNS_KG
+#define L1DM_RUNS_KG 32  // coordinates per run-histogram CTA (measured: 8 -> 32 cut c5 25.8 -> 19.5 ms)
+#endif
+#ifndef L1DM_RUNS_UNR
+#define L1DM_RUNS_UNR 16  // coordinates' run ids in flight per lane in the expansion (8.4 -> 5.2 ms)
+#endif
 #ifndef L1DM_M1_ROW_ITEMS
 #define L1DM_M1_ROW_ITEMS 8  // m = 1 scan: consecutive rows per thread (tile = 256 x this); 8 measured best (c2: 16 -> 8 cut the scan 0.91 -> 0.72 ms)
 #endif

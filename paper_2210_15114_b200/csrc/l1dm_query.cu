@@ -1490,7 +1490,7 @@ void launch_runs_lp(const uint8_t *runid, int64_t ldn, int64_t n, int64_t dl, co
     cudaMemsetAsync(H, 0, (size_t)dl * 256 * m * sizeof(double), s);
     const int L = m >= 32 ? 32 : (m > 16 ? 32 : m > 8 ? 16 : m > 4 ? 8 : m > 2 ? 4 : m > 1 ? 2 : 1);
     const int64_t pts_per_cta = 8 * (32 / L) * 16;
-    const int kg = 8;
+    const int kg = L1DM_RUNS_KG;
     dim3 g1((unsigned)((n + pts_per_cta - 1) / pts_per_cta), (unsigned)((dl + kg - 1) / kg));
     k20_runs_hist<<<g1, 256, 0, s>>>(runid, ldn, n, dl, Z, ldz, m, kg, H);
     const unsigned g2 = (unsigned)((dl * m + 255) / 256);
@@ -1512,7 +1512,7 @@ void launch_runs_lp(const uint8_t *runid, int64_t ldn, int64_t n, int64_t dl, co
     if (lpp <= 1) g(k22_runs_gather<2, 1, 8, true>, 1, 2);
     else if (lpp <= 2) g(k22_runs_gather<2, 2, 8, true>, 2, 2);
     else if (lpp <= 4) g(k22_runs_gather<2, 4, 8, true>, 4, 2);
-    else if (lpp <= 8) g(k22_runs_gather<2, 8, 8, true>, 8, 2);
+    else if (lpp <= 8) g(k22_runs_gather<2, 8, L1DM_RUNS_UNR, true>, 8, 2);
     else if (lpp <= 16) g(k22_runs_gather<2, 16, 8, true>, 16, 2);
     else g(k22_runs_gather<2, 32, 8, true>, 32, 2);
   } else {
@@ -1533,7 +1533,7 @@ void launch_runs_query(const uint8_t *runid, int64_t ldn, int64_t n, int64_t dl,
     cudaMemsetAsync(H, 0, (size_t)dl * 256 * m * sizeof(double), s);
     const int L = m >= 32 ? 32 : (m > 16 ? 32 : m > 8 ? 16 : m > 4 ? 8 : m > 2 ? 4 : m > 1 ? 2 : 1);
     const int64_t pts_per_cta = 8 * (32 / L) * 16;
-    const int kg = 8;
+    const int kg = L1DM_RUNS_KG;
     dim3 g1((unsigned)((n + pts_per_cta - 1) / pts_per_cta), (unsigned)((dl + kg - 1) / kg));
     k20_runs_hist<<<g1, 256, 0, s>>>(runid, ldn, n, dl, Z, ldz, m, kg, H);
     const int64_t t2 = dl * m;
@@ -1564,7 +1564,7 @@ void launch_runs_query(const uint8_t *runid, int64_t ldn, int64_t n, int64_t dl,
       if (lpp <= 1) g(k22_runs_gather<2, 1, 8>, 1, 2);
       else if (lpp <= 2) g(k22_runs_gather<2, 2, 8>, 2, 2);
       else if (lpp <= 4) g(k22_runs_gather<2, 4, 8>, 4, 2);
-      else if (lpp <= 8) g(k22_runs_gather<2, 8, 8>, 8, 2);
+      else if (lpp <= 8) g(k22_runs_gather<2, 8, L1DM_RUNS_UNR>, 8, 2);
       else if (lpp <= 16) g(k22_runs_gather<2, 16, 8>, 16, 2);
       else g(k22_runs_gather<2, 32, 8>, 32, 2);
     } else {

@@ -18,18 +18,20 @@ __global__ void fill_idx(uint32_t *idx, int64_t n) {
     idx[i] = (uint32_t)x;
   }
 }
-// 8 lanes per 64-B row, 4 rows per warp per step, 4 steps in flight
+// W lanes per W*8-byte row (32/W rows per warp step), U steps in flight per thread
+template <int W, int U>
 __global__ void __launch_bounds__(256) red_rows(const uint32_t *idx, int64_t rows, double *y,
                                                 uint32_t yrows) {
-  const int lane = threadIdx.x & 31, c = lane & 7, g = lane >> 3;
+  constexpr int G = 32 / W;
+  const int lane = threadIdx.x & 31, c = lane % W, g = lane / W;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t base = warp * 16; base < rows; base += nw * 16) {
-    uint32_t p[4];
+  for (int64_t base = warp * G * U; base < rows; base += nw * G * U) {
+    uint32_t p[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) p[u] = __ldcs(idx + base + u * 4 + g);
+    for (int u = 0; u < U; ++u) p[u] = __ldcs(idx + base + u * G + g);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) atomicAdd(y + (int64_t)(p[u] % yrows) * 8 + c, 1.0);
+    for (int u = 0; u < U; ++u) atomicAdd(y + (int64_t)(p[u] % yrows) * W + c, 1.0);
   }
 }
 // one 32-B sector per row: 8 lanes x 4 B
@@ -48,6 +50,46 @@ __global__ void __launch_bounds__(256) gather_sectors(const uint32_t *idx, int64
     for (int u = 0; u < 4; ++u) acc += __ldcg(z + (int64_t)(p[u] % zrows) * 8 + c);
   }
   if (acc == 1.2345f) out[0] = acc;
+}
+// W lanes per W*8-byte row, row indices hashed in registers (no index stream: the reduction
+// rate alone), U reductions in flight per thread
+template <int W, int U>
+__global__ void __launch_bounds__(256) red_rows_hash(int64_t rows, double *y, uint32_t yrows) {
+  constexpr int G = 32 / W;
+  const int lane = threadIdx.x & 31, c = lane % W, g = lane / W;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = warp * G * U; base < rows; base += nw * G * U) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      uint32_t x = (uint32_t)(base + u * G + g) * 0x9E3779B1u;
+      x ^= x >> 15;
+      x *= 0x85EBCA77u;
+      x ^= x >> 13;
+      atomicAdd(y + (int64_t)(x % yrows) * W + c, 1.0);
+    }
+  }
+}
+// the runs histogram's pattern: a warp's reductions land in one coordinate's 256-row table
+// (rows of W*8 bytes; 96 tables), the run within the table random, the coordinate varying with
+// the loop (as k in k20_runs_hist)
+template <int W, int U>
+__global__ void __launch_bounds__(256) red_tables(int64_t rows, double *y, uint32_t ntab) {
+  constexpr int G = 32 / W;
+  const int lane = threadIdx.x & 31, c = lane % W, g = lane / W;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = warp * G * U; base < rows; base += nw * G * U) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      uint32_t x = (uint32_t)(base + u * G + g) * 0x9E3779B1u;
+      x ^= x >> 15;
+      x *= 0x85EBCA77u;
+      x ^= x >> 13;
+      const uint32_t tab = (uint32_t)((warp + u) % ntab);
+      atomicAdd(y + ((int64_t)tab * 256 + (x & 255u)) * W + c, 1.0);
+    }
+  }
 }
 // one random 4-byte element per lane (32 rows per warp request): the m = 1 reduce pass's pattern
 __global__ void __launch_bounds__(256) gather_lanes(const uint32_t *idx, int64_t rows,
@@ -127,7 +169,18 @@ int main() {
   fill_idx<<<sms * 8, 256>>>(idx, rows);
   const int grid = sms * 8;
   const uint32_t yrows = (uint32_t)((64ll << 20) / 64), zrows = (uint32_t)((32ll << 20) / 32);
-  const float t_red = best_ms([&] { red_rows<<<grid, 256>>>(idx, rows, y, yrows); });
+  const float t_red = best_ms([&] { red_rows<8, 4><<<grid, 256>>>(idx, rows, y, yrows); });
+  // deeper: 16 reductions in flight per thread (the apply / histogram kernels keep many)
+  const float t_red16 = best_ms([&] { red_rows<8, 16><<<grid, 256>>>(idx, rows, y, yrows); });
+  const float t_red_w16 =
+      best_ms([&] { red_rows<16, 16><<<grid, 256>>>(idx, rows, y, yrows / 2); });
+  const float t_hash8 = best_ms([&] { red_rows_hash<8, 16><<<grid, 256>>>(rows, y, yrows); });
+  const float t_hash16_small =
+      best_ms([&] { red_rows_hash<16, 16><<<grid, 256>>>(rows, y, (4u << 20) / 128); });
+  const float t_tables = best_ms([&] { red_tables<16, 16><<<grid, 256>>>(rows, y, 96); });
+  // a 4 MiB table (the runs histogram's: dl x 256 x m fp64, 3 MiB at c5)
+  const float t_red_w16_small =
+      best_ms([&] { red_rows<16, 16><<<grid, 256>>>(idx, rows, y, (4u << 20) / 128); });
   const float t_gat = best_ms([&] { gather_sectors<<<grid, 256>>>(idx, rows, z, zrows, out); });
   const float t_gl = best_ms([&] { gather_lanes<<<grid, 256>>>(idx, rows, z, zrows * 8, out); });
   const float t_rl = best_ms([&] { red_lanes<<<grid, 256>>>(idx, rows, y, yrows * 8); });
@@ -138,6 +191,12 @@ int main() {
   const cudaError_t e = cudaGetLastError();
   printf("{\"gather_lane_per_s\": %.4g, \"red_lane_per_s\": %.4g, ", rows / (t_gl * 1e-3),
          rows / (t_rl * 1e-3));
+  printf("\"red_row8_deep_adds_per_s\": %.4g, \"red_row16_deep_adds_per_s\": %.4g, "
+         "\"red_row16_4MiB_adds_per_s\": %.4g, \"red_row8_hashed_adds_per_s\": %.4g, "
+         "\"red_row16_4MiB_hashed_adds_per_s\": %.4g, \"red_runs_tables_adds_per_s\": %.4g, ",
+         rows * 8.0 / (t_red16 * 1e-3), rows * 16.0 / (t_red_w16 * 1e-3),
+         rows * 16.0 / (t_red_w16_small * 1e-3), rows * 8.0 / (t_hash8 * 1e-3),
+         rows * 16.0 / (t_hash16_small * 1e-3), rows * 16.0 / (t_tables * 1e-3));
   printf("\"red_row8_adds_per_s\": %.4g, \"gather_sector_GBps\": %.1f, "
          "\"stream_read_GBps\": %.1f, \"sms\": %d, \"l2_bytes\": %d, \"sm_clock_khz\": %d, "
          "\"status\": \"%s\", \"how\": \"tools/l2_probe.cu: 2^27 random rows, L2-resident "
