@@ -30,6 +30,9 @@ namespace {
 
 constexpr int kTile = 64;    // output tile (rows x columns) of K12 and K14
 constexpr int kStepK = 16;   // coordinates per shared-memory step of K14
+#ifndef L1DM_EVEN_CTAS_PER_SM
+#define L1DM_EVEN_CTAS_PER_SM 2  // K12 split-K: point chunks for ~this many CTAs per SM (one wave; 2 measured best)
+#endif
 #ifndef L1DM_K14_P2_G
 #define L1DM_K14_P2_G 4
 #endif
@@ -658,7 +661,7 @@ size_t lpp_even_workspace(int64_t n, int64_t d, int64_t m, int p, int64_t *nchun
   const int64_t tk = 32 * k12_g(d);
   const int T = p > 1 ? p - 1 : 1;  // moments through DMMA: t = 1 .. p-1 (bilinear: 1)
   const int64_t tiles = ((d + tk - 1) / tk) * ((m + kTile - 1) / kTile) * T;
-  int64_t nchunks = (4 * (int64_t)sms + tiles - 1) / tiles;  // ~4 CTAs per SM over all tiles
+  int64_t nchunks = (L1DM_EVEN_CTAS_PER_SM * (int64_t)sms + tiles - 1) / tiles;  // CTAs per SM
   const int64_t min_pts = 1024;
   if (nchunks * min_pts > n) nchunks = (n + min_pts - 1) / min_pts;
   if (nchunks < 1) nchunks = 1;
