@@ -74,6 +74,9 @@ void launch_runs_ids(const float *X, int64_t n, int64_t ldx, int64_t k0, int64_t
 #ifndef L1DM_RA_TILES
 #define L1DM_RA_TILES 2  // 1024-row tiles per reduce-all CTA (a power of two <= 8)
 #endif
+#ifndef L1DM_ACC_UNR
+#define L1DM_ACC_UNR 8  // gather-mode accumulate: coordinates' rank + U loads in flight per lane
+#endif
 #ifndef L1DM_RUNS_KG
 #define L1DM_RUNS_KG 32  // coordinates per run-histogram CTA (measured: 8 -> 32 cut c5 25.8 -> 19.5 ms)
 #endif

@@ -1785,11 +1785,11 @@ static void launch_acc_t(const QueryPlan &p, const uint32_t *rank, int64_t ldn, 
   constexpr int PPB = 8 * (32 / LPP);
   dim3 grid((unsigned)((i1 - i0 + PPB - 1) / PPB), (unsigned)p.col_groups);
   if (pd && pd->world > 0 && last)
-    k6_accumulate<V6, LPP, 8, true><<<grid, 256, 0, s>>>(
+    k6_accumulate<V6, LPP, L1DM_ACC_UNR, true><<<grid, 256, 0, s>>>(
         rank, ldn, n, U, p.ldu, k_first, kcc, hsum, Sg, Y, ldy, m, first ? 1 : 0, 1, ticket, i0,
         i1, factor, epilogue ? 1 : 0, *pd);
   else
-    k6_accumulate<V6, LPP, 8, false><<<grid, 256, 0, s>>>(
+    k6_accumulate<V6, LPP, L1DM_ACC_UNR, false><<<grid, 256, 0, s>>>(
         rank, ldn, n, U, p.ldu, k_first, kcc, hsum, Sg, Y, ldy, m, first ? 1 : 0, last ? 1 : 0,
         ticket, i0, i1, factor, epilogue ? 1 : 0, PeerDst{});
 }
