@@ -726,10 +726,10 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int q = 0; q < K; ++q) M[q] += s_wt[ww * NP + K * c + q];
     }
-    double Tt[K];  // P > 1: the coordinate's totals T_t of this column (from the prefix pass)
+    double cT[K];  // P > 1: c_t T_t, the coordinate's totals of this column (prefix pass)
 #pragma unroll
     for (int q = 0; q < K; ++q)
-      Tt[q] = (P > 1 && c < mc) ? __ldg(segtot + kk * ld_seg + K * c + q) : 0.0;
+      cT[q] = (P > 1 && c < mc) ? lp_coef<P>(q) * __ldg(segtot + kk * ld_seg + K * c + q) : 0.0;
     if (c < mc) {
 #pragma unroll 4
       for (int j = 0; j < ITEMS; ++j) {
@@ -739,13 +739,11 @@ __global__ void __launch_bounds__(256)
         if constexpr (P == 1) {
           val = 2.0 * fma(v, M[0], -M[1]);  // 2 U_r = 2 (v_r P_r - Q_r)
         } else {
-          double vp[K];  // v^0 .. v^P
-          vp[0] = 1.0;
+          // sum_t c_t v^(P-t) (2 M_t - T_t) in Horner form over descending powers of v:
+          // a_t = 2 c_t M_t - c_t T_t, val = (..(a_0 v + a_1) v + ..) v + a_P
+          val = fma(2.0 * lp_coef<P>(0), M[0], -cT[0]);
 #pragma unroll
-          for (int q = 1; q < K; ++q) vp[q] = vp[q - 1] * v;
-          val = 0.0;
-#pragma unroll
-          for (int q = 0; q < K; ++q) val = fma(lp_coef<P>(q) * vp[P - q], fma(2.0, M[q], -Tt[q]), val);
+          for (int q = 1; q < K; ++q) val = fma(val, v, fma(2.0 * lp_coef<P>(q), M[q], -cT[q]));
         }
         double zv = z;
 #pragma unroll
