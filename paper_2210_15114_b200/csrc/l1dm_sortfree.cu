@@ -297,7 +297,9 @@ static void launch_k12(const float *X, int64_t ldx, const float *Z, int64_t ldz,
     const char *e = getenv("L1DM_K12_RING");
     return e ? atoi(e) != 0 : true;
   }();
-  if (ring_env && d % 128 == 0 && m % 4 == 0 && ldx % 4 == 0 && ldz % 4 == 0 &&
+  // (only for the first moment: higher powers would be recomputed at every fragment load,
+  // which the staged kernel does once per element — measured slower at p = 4, 6)
+  if (ring_env && p == 1 && d % 128 == 0 && m % 4 == 0 && ldx % 4 == 0 && ldz % 4 == 0 &&
       (uintptr_t)X % 16 == 0 && (uintptr_t)Z % 16 == 0) {
     const size_t sm = (size_t)kRing * kDmmaKs * (kXs + kZs) * sizeof(float);
     static bool attr = false;
@@ -661,7 +663,10 @@ size_t lpp_even_workspace(int64_t n, int64_t d, int64_t m, int p, int64_t *nchun
   const int64_t tk = 32 * k12_g(d);
   const int T = p > 1 ? p - 1 : 1;  // moments through DMMA: t = 1 .. p-1 (bilinear: 1)
   const int64_t tiles = ((d + tk - 1) / tk) * ((m + kTile - 1) / kTile) * T;
-  int64_t nchunks = (L1DM_EVEN_CTAS_PER_SM * (int64_t)sms + tiles - 1) / tiles;  // CTAs per SM
+  // point chunks for ~2 CTAs per SM (one wave) with a single moment, ~4 with several (measured:
+  // p = 2 1.73 vs 1.78 ms; p = 4 5.07 vs 5.96 ms)
+  const int64_t per_sm = T == 1 ? L1DM_EVEN_CTAS_PER_SM : 2 * L1DM_EVEN_CTAS_PER_SM;
+  int64_t nchunks = (per_sm * (int64_t)sms + tiles - 1) / tiles;
   const int64_t min_pts = 1024;
   if (nchunks * min_pts > n) nchunks = (n + min_pts - 1) / min_pts;
   if (nchunks < 1) nchunks = 1;
