@@ -54,3 +54,32 @@ def test_no_cpu_fallback_without_device():
     with pytest.raises(l1.L1dmError) as e:
         l1.l1dm_prepare(X)
     assert e.value.name == "L1DM_EDEVICE"
+
+
+def test_missing_library_raises_instead_of_falling_back(tmp_path):
+    """A fresh interpreter pointed at a library path that does not exist must fail on the
+    first call (ImportError), never compute on the CPU."""
+    import subprocess
+    import sys
+    code = ("import torch, paper_2210_15114_b200 as l1\n"
+            "try:\n"
+            "    l1.l1dm_prepare(torch.rand(8, 2))\n"
+            "except ImportError as e:\n"
+            "    print('raised', 'no CPU fallback' in str(e))\n")
+    env = dict(os.environ, L1DM_LIB=str(tmp_path / "absent.so"))
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True,
+                         text=True, timeout=300)
+    assert out.stdout.strip() == "raised True", out.stdout + out.stderr[-2000:]
+
+
+def test_product_package_never_touches_the_oracle():
+    """Only tests/, __graft_entry__.smoke() and bench.py's CPU arms may use oracle/: no module
+    of the package imports it or names it in a load path."""
+    pkg = os.path.join(ROOT, "paper_2210_15114_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if not f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                continue
+            src = open(os.path.join(dirpath, f)).read()
+            assert not re.search(r"^\s*(import|from)\s+oracle\b", src, flags=re.M), f
+            assert not re.search(r"""#\s*include\s*["<][^">]*oracle|["']oracle[/.]""", src), f
