@@ -78,7 +78,7 @@ void launch_runs_ids(const float *X, int64_t n, int64_t ldx, int64_t k0, int64_t
 #define L1DM_ACC_UNR 8  // gather-mode accumulate: coordinates' rank + U loads in flight per lane
 #endif
 #ifndef L1DM_RUNS_KG
-#define L1DM_RUNS_KG 32  // coordinates per run-histogram CTA (measured: 8 -> 32 cut c5 25.8 -> 19.5 ms)
+#define L1DM_RUNS_KG 96  // coordinates per run-histogram CTA (measured c5 step: kg 8 -> 32 cut 366 -> 303 ms; with 16 run ids in flight 32 -> 96: 273 -> 268 ms)
 #endif
 #ifndef L1DM_RUNS_UNR
 #define L1DM_RUNS_UNR 16  // coordinates' run ids in flight per lane in the expansion (8.4 -> 5.2 ms)
