@@ -238,6 +238,8 @@ typedef struct {
   unsigned *flags[L1DM_MAX_PEERS];  /* owner o's 2G flag words as mapped here */
   double *ybuf[L1DM_MAX_PEERS];     /* rank t's result buffer as mapped here, or NULL */
   unsigned *timeout;                /* this rank's timeout word (device, zeroed) */
+  int64_t n;                        /* points and columns the inboxes and result buffers were */
+  int64_t m;                        /* allocated for: every call checks its n, m against them */
 } l1dm_peer_t;
 /* bytes of device memory, zeroed, with its 64-byte CUDA IPC handle in handle[0..64). */
 L1DM_API l1dm_status l1dm_ipc_alloc(size_t bytes, void **dptr, void *handle);
@@ -263,7 +265,10 @@ L1DM_API l1dm_status l1dm_peer_reduce(const l1dm_peer_t *peers, int64_t n, int64
  * n x m result from this rank's ybuf into Y (device, row stride ld_y). */
 L1DM_API l1dm_status l1dm_peer_wait(const l1dm_peer_t *peers, unsigned epoch, int64_t n, int64_t m,
                                     double *Y, int64_t ld_y, void *stream);
-/* Synchronise the stream and report (then clear) a timed-out peer wait: ETIMEOUT. */
+/* Synchronise the stream and report (then clear) a timed-out peer wait: ETIMEOUT.  After a
+ * timeout the epoch-parity reuse argument no longer holds: tear the group down and allocate a
+ * fresh one (the Python PeerGroup does this) rather than continuing with the next epoch.
+ * A timed-out wait ends every other wait of the same rank early (they poll the timeout word). */
 L1DM_API l1dm_status l1dm_peer_check(const l1dm_peer_t *peers, void *stream);
 
 /* Release every buffer the handle owns.  NULL is a no-op.  Synchronises the

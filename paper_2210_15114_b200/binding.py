@@ -60,7 +60,8 @@ class PeerT(ctypes.Structure):
     """l1dm_peer_t (include/l1dm.h): the peer buffers of one rank's group, as mapped here."""
     _fields_ = [("world", ctypes.c_int), ("rank", ctypes.c_int),
                 ("inbox", ctypes.c_void_p * MAX_PEERS), ("flags", ctypes.c_void_p * MAX_PEERS),
-                ("ybuf", ctypes.c_void_p * MAX_PEERS), ("timeout", ctypes.c_void_p)]
+                ("ybuf", ctypes.c_void_p * MAX_PEERS), ("timeout", ctypes.c_void_p),
+                ("n", ctypes.c_int64), ("m", ctypes.c_int64)]
 
 
 class TimingT(ctypes.Structure):

@@ -83,7 +83,7 @@ class BlockCache {
       auto it = m.lower_bound(bytes);
       if (it != m.end() && it->first <= bytes + bytes / 4) {
         *p = it->second;
-        sizes_[*p] = it->first;
+        sizes_[*p] = {it->first, dev};
         cached_[dev] -= it->first;
         m.erase(it);
         return cudaSuccess;
@@ -103,27 +103,31 @@ class BlockCache {
     }
     if (e == cudaSuccess) {
       std::lock_guard<std::mutex> g(mu_);
-      sizes_[*p] = rounded;
+      sizes_[*p] = {rounded, dev};
     }
     return e;
   }
-  // p must not be in use by any queued work (callers synchronise first)
+  // p must not be in use by any queued work (callers synchronise first).  The block is filed
+  // under the device it was allocated on (recorded at alloc), whatever device is current.
   void free(void *p) {
     if (!p) return;
-    int dev = 0;
-    cudaGetDevice(&dev);
     std::lock_guard<std::mutex> g(mu_);
     auto sz = sizes_.find(p);
     if (sz == sizes_.end()) {
       cudaFree(p);
       return;
     }
-    const size_t bytes = sz->second;
+    const size_t bytes = sz->second.first;
+    const int dev = sz->second.second;
     sizes_.erase(sz);
     if (limit_[dev] == 0) {
+      int cur = 0;
+      cudaGetDevice(&cur);
+      if (cur != dev) cudaSetDevice(dev);
       size_t fr = 0, tot = 0;
       cudaMemGetInfo(&fr, &tot);
       limit_[dev] = tot / 2;
+      if (cur != dev) cudaSetDevice(cur);
     }
     if (cached_[dev] + bytes > limit_[dev]) {
       if (debug()) fprintf(stderr, "[l1dm] cache full: cudaFree %zu B\n", bytes);
@@ -135,7 +139,11 @@ class BlockCache {
   }
   void release_all(int dev) {
     std::lock_guard<std::mutex> g(mu_);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != dev && !free_[dev].empty()) cudaSetDevice(dev);
     for (auto &kv : free_[dev]) cudaFree(kv.second);
+    if (cur != dev && !free_[dev].empty()) cudaSetDevice(cur);
     free_[dev].clear();
     cached_[dev] = 0;
   }
@@ -148,7 +156,7 @@ class BlockCache {
   std::mutex mu_;
   std::map<int, std::multimap<size_t, void *>> free_;
   std::map<int, size_t> cached_, limit_;
-  std::unordered_map<void *, size_t> sizes_;
+  std::unordered_map<void *, std::pair<size_t, int>> sizes_;  // block -> (bytes, device)
 };
 
 template <typename T>
@@ -303,6 +311,19 @@ struct TimedScope {
   }
 };
 
+// Makes h's device current for a scope (calls that only synchronise or release a handle's
+// resources may come from a thread whose current device is another one).
+struct DeviceGuard {
+  int prev = -1, dev = -1;
+  explicit DeviceGuard(int d) : dev(d) {
+    cudaGetDevice(&prev);
+    if (dev >= 0 && prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (dev >= 0 && prev >= 0 && prev != dev) cudaSetDevice(prev);
+  }
+};
+
 l1dm_status check_device(l1dm_ctx *h) {
   int cur = -1;
   CUDA_TRY(cudaGetDevice(&cur));
@@ -334,6 +355,11 @@ l1dm_status check_arch(int *dev_out) {
 
 void destroy(l1dm_ctx *h) {
   if (!h) return;
+  // a handle may be freed (or garbage-collected) while another device is current: every
+  // stream, event and block below belongs to h->device
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (h->device >= 0 && cur != h->device) cudaSetDevice(h->device);
   cudaStreamSynchronize(h->stream);
   if (h->last_stream != h->stream) cudaStreamSynchronize(h->last_stream);
   for (auto &p : h->pending) {
@@ -373,7 +399,9 @@ void destroy(l1dm_ctx *h) {
   h->zt.release();
   h->yt.release();
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  const int hdev = h->device;
   delete h;
+  if (hdev >= 0 && cur >= 0 && cur != hdev) cudaSetDevice(cur);
 }
 
 // --------------------------------------------------------------------- prepare
@@ -1448,8 +1476,11 @@ l1dm_status l1dm_ipc_close(void *dptr) {
 }
 
 namespace {
-l1dm_status check_peers(const l1dm_peer_t *pr) {
+l1dm_status check_peers(const l1dm_peer_t *pr, int64_t n, int64_t m) {
   if (!pr) return fail(L1DM_EINVAL, "peers is NULL");
+  if (pr->n < 1 || pr->m < 1 || n != pr->n || m != pr->m)
+    return fail(L1DM_EINVAL, "n=%lld m=%lld do not match the peer buffers (n=%lld m=%lld)",
+                (long long)n, (long long)m, (long long)pr->n, (long long)pr->m);
   if (pr->world < 1 || pr->world > L1DM_MAX_PEERS || pr->rank < 0 || pr->rank >= pr->world)
     return fail(L1DM_EINVAL, "world=%d rank=%d invalid (1 <= world <= %d)", pr->world, pr->rank,
                 L1DM_MAX_PEERS);
@@ -1467,7 +1498,7 @@ l1dm_status l1dm_matvec_push(l1dm_handle h, const float *Z, int64_t ld_z, int64_
   if (!h || !Z) return fail(L1DM_EINVAL, "handle or Z is NULL");
   if (m < 1 || ld_z < m) return fail(L1DM_EINVAL, "m=%lld ld_z=%lld invalid", (long long)m,
                                      (long long)ld_z);
-  l1dm_status st = check_peers(peers);
+  l1dm_status st = check_peers(peers, h->n, m);
   if (st != L1DM_OK) return st;
   if (epoch == 0) return fail(L1DM_EINVAL, "epoch 0 is reserved (the flags' initial value)");
   st = check_device(h);
@@ -1513,7 +1544,7 @@ l1dm_status l1dm_matvec_push(l1dm_handle h, const float *Z, int64_t ld_z, int64_
 l1dm_status l1dm_peer_reduce(const l1dm_peer_t *peers, int64_t n, int64_t m, unsigned epoch,
                              unsigned targets, void *stream) {
   g_err.clear();
-  l1dm_status st = check_peers(peers);
+  l1dm_status st = check_peers(peers, n, m);
   if (st != L1DM_OK) return st;
   if (n < 1 || m < 1 || epoch == 0) return fail(L1DM_EINVAL, "n, m >= 1 and epoch > 0 required");
   const int G = peers->world, g = peers->rank;
@@ -1542,7 +1573,7 @@ l1dm_status l1dm_peer_reduce(const l1dm_peer_t *peers, int64_t n, int64_t m, uns
 l1dm_status l1dm_peer_wait(const l1dm_peer_t *peers, unsigned epoch, int64_t n, int64_t m,
                            double *Y, int64_t ld_y, void *stream) {
   g_err.clear();
-  l1dm_status st = check_peers(peers);
+  l1dm_status st = check_peers(peers, n, m);
   if (st != L1DM_OK) return st;
   if (epoch == 0) return fail(L1DM_EINVAL, "epoch 0 is reserved");
   const int G = peers->world, g = peers->rank;
@@ -1645,6 +1676,7 @@ void l1dm_free(l1dm_handle h) { destroy(h); }
 l1dm_status l1dm_sync(l1dm_handle h) {
   g_err.clear();
   if (!h) return fail(L1DM_EINVAL, "handle is NULL");
+  DeviceGuard dg(h->device);
   if (h->cp_in) CUDA_TRY(cudaStreamSynchronize(h->cp_in));
   if (h->cp_out) CUDA_TRY(cudaStreamSynchronize(h->cp_out));
   CUDA_TRY(cudaStreamSynchronize(h->stream));

@@ -60,14 +60,18 @@ __global__ void k31_peer_signal(FlagTab flags, int world, int index, unsigned ep
 
 __device__ __forceinline__ void wait_flags(const unsigned *flags, int count, unsigned epoch,
                                            unsigned *timeout) {
+  // One bound for the whole wait (not per flag), and any waiter that sees the rank's timeout
+  // word raised (by another CTA, or an earlier wait) gives up at once: a dead peer costs one
+  // kSpinLimit, not one per CTA and flag.
+  uint32_t spins = 0;
   for (int g = 0; g < count; ++g) {
-    uint32_t spins = 0;
     // epochs only grow: a flag already past this epoch (a fast peer's next query) counts
     while ((int)(ld_acquire_sys_u32(flags + g) - epoch) < 0) {
       if (++spins > kSpinLimit) {
         atomicOr(timeout, 1u);
-        break;
+        return;
       }
+      if ((spins & 63u) == 0 && *(volatile unsigned *)timeout) return;
       if (spins > 16) __nanosleep(128);
     }
   }

@@ -1479,6 +1479,13 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Coordinates per run-histogram CTA: at most L1DM_RUNS_KG, balanced over the grid.y slices so
+// no slice is a thin tail (dl = 128 -> 2 x 64, not 96 + 32; dl = 97 -> 49 + 48).
+static int runs_kg(int64_t dl) {
+  const int64_t slices = (dl + L1DM_RUNS_KG - 1) / L1DM_RUNS_KG;
+  return (int)((dl + slices - 1) / (slices < 1 ? 1 : slices));
+}
+
 void launch_runs_lp(const uint8_t *runid, int64_t ldn, int64_t n, int64_t dl, const float *rvals,
                     const uint32_t *nruns, const float *Z, int64_t ldz, int64_t m, int lp,
                     double *H, double *Y, int64_t ldy, int phase, cudaStream_t s) {
@@ -1488,7 +1495,7 @@ void launch_runs_lp(const uint8_t *runid, int64_t ldn, int64_t n, int64_t dl, co
     cudaMemsetAsync(H, 0, (size_t)dl * 256 * m * sizeof(double), s);
     const int L = m >= 32 ? 32 : (m > 16 ? 32 : m > 8 ? 16 : m > 4 ? 8 : m > 2 ? 4 : m > 1 ? 2 : 1);
     const int64_t pts_per_cta = 8 * (32 / L) * 16;
-    const int kg = L1DM_RUNS_KG;
+    const int kg = runs_kg(dl);
     dim3 g1((unsigned)((n + pts_per_cta - 1) / pts_per_cta), (unsigned)((dl + kg - 1) / kg));
     k20_runs_hist<<<g1, 256, 0, s>>>(runid, ldn, n, dl, Z, ldz, m, kg, H);
     const unsigned g2 = (unsigned)((dl * m + 255) / 256);
@@ -1531,7 +1538,7 @@ void launch_runs_query(const uint8_t *runid, int64_t ldn, int64_t n, int64_t dl,
     cudaMemsetAsync(H, 0, (size_t)dl * 256 * m * sizeof(double), s);
     const int L = m >= 32 ? 32 : (m > 16 ? 32 : m > 8 ? 16 : m > 4 ? 8 : m > 2 ? 4 : m > 1 ? 2 : 1);
     const int64_t pts_per_cta = 8 * (32 / L) * 16;
-    const int kg = L1DM_RUNS_KG;
+    const int kg = runs_kg(dl);
     dim3 g1((unsigned)((n + pts_per_cta - 1) / pts_per_cta), (unsigned)((dl + kg - 1) / kg));
     k20_runs_hist<<<g1, 256, 0, s>>>(runid, ldn, n, dl, Z, ldz, m, kg, H);
     const int64_t t2 = dl * m;

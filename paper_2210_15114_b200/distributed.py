@@ -66,6 +66,7 @@ class PeerGroup:
         self.mapped = []  # pointers this process opened (closed in close())
         pt = binding.PeerT()
         pt.world, pt.rank = G, g
+        pt.n, pt.m = n, m
         for o in range(G):
             for key, arr in (("inbox", pt.inbox), ("flags", pt.flags), ("ybuf", pt.ybuf)):
                 if o == g:
@@ -135,7 +136,8 @@ class ShardedL1DM:
         return self._matvec(self.handle, Z, Y, stream=self.stream)
 
     def matvec(self, Z: torch.Tensor, Y: Optional[torch.Tensor] = None, *, root: Optional[int] = 0,
-               async_op: bool = False, overlap_blocks: int = 1, collective: str = "nccl"):
+               async_op: bool = False, overlap_blocks: int = 1, collective: str = "nccl",
+               check: bool = True):
         """A·Z summed over ranks: on `root` only (reduce) or on every rank (root=None).
 
         overlap_blocks > 1 (CUDA, C-ABI handle): the last accumulate runs per point block and
@@ -144,9 +146,11 @@ class ShardedL1DM:
         collective="peer" (CUDA, l1 handle): the sum runs over peer memory in this library's
         kernels — the query's final pass stores rows straight into their owners' inboxes
         (l1dm_matvec_push), owners reduce and store into the result ranks (l1dm_peer_reduce),
-        result ranks wait (l1dm_peer_wait); no NCCL on the data path."""
+        result ranks wait (l1dm_peer_wait); no NCCL on the data path.  check=True (default)
+        synchronises the stream after the query and raises L1dmError(ETIMEOUT) if any of this
+        rank's bounded peer waits gave up (the group is then rebuilt on the next call)."""
         if collective == "peer":
-            return self._matvec_peer(Z, Y, root)
+            return self._matvec_peer(Z, Y, root, check)
         if (overlap_blocks > 1 and self.world > 1 and self.handle is not None and Z.is_cuda
                 and self._matvec is binding.l1dm_matvec):
             return self._matvec_overlapped(Z, Y, root, async_op, overlap_blocks)
@@ -198,7 +202,7 @@ class ShardedL1DM:
             w.wait()
         return Y
 
-    def _matvec_peer(self, Z, Y, root):
+    def _matvec_peer(self, Z, Y, root, check=True):
         if self.handle is None or self._matvec is not binding.l1dm_matvec or not Z.is_cuda:
             raise ValueError("collective='peer' needs a CUDA Z and an l1 C-ABI handle on every rank")
         n, m = Z.shape[0], Z.shape[1]
@@ -220,6 +224,18 @@ class ShardedL1DM:
             if Y is None:
                 Y = torch.empty((n, m), dtype=torch.float64, device=Z.device)
             binding.l1dm_peer_wait(pg.peers, pg.epoch, n, m, Y, stream=stream)
+        if check:
+            # a bounded flag wait that gave up leaves Y invalid: raise instead of returning it,
+            # and drop the group — after a timeout the epoch-parity reuse argument is void
+            try:
+                binding.l1dm_peer_check(pg.peers, stream=stream if stream is not None
+                                        else torch.cuda.current_stream(Z.device))
+            except binding.L1dmError:
+                if self._peer_owned:
+                    torch.cuda.synchronize(Z.device)
+                    pg.close()
+                self._peer = None
+                raise
         return Y
 
     def _collective(self, T, root):

@@ -44,6 +44,7 @@ class EmulatedGroup:
         for g in range(G):
             pt = binding.PeerT()
             pt.world, pt.rank = G, g
+            pt.n, pt.m = n, m
             for o in range(G):
                 pt.inbox[o] = self.bufs[o]["inbox"]
                 pt.flags[o] = self.bufs[o]["flags"]
@@ -174,6 +175,14 @@ def test_peer_args_rejected():
             binding.l1dm_matvec_push(h, Z, bad, 1)
         with pytest.raises(binding.L1dmError):  # rank 1 has no result buffer
             binding.l1dm_peer_reduce(grp.peers[0], 100, 2, 1, 0b10)
+        # n or m differing from the inbox geometry would store past the owners' slots
+        Z3 = torch.rand(100, 3, device="cuda")
+        with pytest.raises(binding.L1dmError):
+            binding.l1dm_matvec_push(h, Z3, grp.peers[0], 1)
+        with pytest.raises(binding.L1dmError):
+            binding.l1dm_peer_reduce(grp.peers[0], 101, 2, 1, 0b01)
+        with pytest.raises(binding.L1dmError):
+            binding.l1dm_peer_wait(grp.peers[0], 1, 100, 3)
         grp.free()
     finally:
         l1.l1dm_free(h)
