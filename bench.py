@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-shard-proxy", action="store_true")
     ap.add_argument("--reduce", default="reduce", choices=["reduce", "allreduce"])
     ap.add_argument("--p", type=int, default=1, choices=[1, 2, 3, 4, 5, 6, 7],
                     help="l_p^p query: odd p sort-based (NEXT-1), even p sort-free (NEXT-4); "
@@ -137,6 +138,54 @@ def load_l2_peaks():
 def model_b_bytes(n, d, m):
     """SURVEY §8(d) Model B algorithmic bytes per query: n d (12 + 20 m) + n (12 m + 8)."""
     return n * d * (12 + 20 * m) + n * (12 * m + 8)
+
+
+def q12_rows(X, count=64, seed=12):
+    """SURVEY §8(c) SAMPLE rows (Q12): `count` seeded random rows plus rows 0, n-1, argmin h and
+    argmax h (h_i = sum_k x_ik), as row ids on X's device."""
+    n = X.shape[0]
+    h = X.double().sum(dim=1)
+    g = np.random.default_rng(seed)
+    r = set(g.integers(0, n, size=count).tolist())
+    r |= {0, n - 1, int(torch.argmin(h).item()), int(torch.argmax(h).item())}
+    return torch.tensor(sorted(r), dtype=torch.long, device=X.device)
+
+
+def definition_rows(X, Z, rows, p=1, chunk=1 << 21):
+    """y_i = sum_j z_j sum_k |x_ik - x_jk|^p for the listed rows: the definition (P:149, P:171;
+    P:35 for p > 1) in fp64 with plain torch ops on X's device (|R| n d work, no sort, no prefix
+    sums): the bench's check of what it timed (the CPU oracle re-checks the same rows at N = 1
+    in the cpu_baseline leg)."""
+    n = X.shape[0]
+    XR = X[rows].double()
+    acc = torch.zeros((rows.numel(), Z.shape[1]), dtype=torch.float64, device=X.device)
+    for j0 in range(0, n, chunk):
+        j1 = min(n, j0 + chunk)
+        Xc = X[j0:j1].double()
+        Zc = Z[j0:j1].double()
+        for r in range(rows.numel()):
+            D = (Xc - XR[r]).abs_()
+            if p != 1:
+                D.pow_(p)
+            acc[r] += D.sum(dim=1) @ Zc
+        del Xc, Zc
+    return acc
+
+
+def col_rel_l2(Y, Yref):
+    """Max over columns of ||Y[:,c] - Yref[:,c]||_2 / ||Yref[:,c]||_2 (0/0 = 0, x/0 = inf)."""
+    num = torch.linalg.vector_norm((Y - Yref).double(), dim=0)
+    den = torch.linalg.vector_norm(Yref.double(), dim=0)
+    worst = 0.0
+    for a, b in zip(num.tolist(), den.tolist()):
+        worst = max(worst, a / b if b > 0 else (0.0 if a == 0 else float("inf")))
+    return worst
+
+
+def sha256_of(t):
+    import hashlib
+    a = t.detach().cpu().contiguous().numpy()
+    return hashlib.sha256(memoryview(a).cast("B")).hexdigest()
 
 
 # --------------------------------------------------------------------------- reference arm
@@ -250,6 +299,7 @@ def main_ours(args):
 
     # inputs resident in HBM before timing: full X regenerated per rank from the seed
     Xfull = wl.make_points(w, dev)
+    x_sha = sha256_of(Xfull) if rank == 0 else None
     k0, k1 = shard_range(d, rank, world)
     X = Xfull[:, k0:k1].contiguous() if world > 1 else Xfull
     del Xfull
@@ -258,12 +308,19 @@ def main_ours(args):
         Zs = [wl.make_query(w, t, dev) for t in range(Q)]
     else:
         Zs = [wl.make_query(w, 0, dev)]
+    z_sha = None
+    if rank == 0:
+        import hashlib
+        hz = hashlib.sha256()
+        for z in Zs:
+            hz.update(sha256_of(z).encode())
+        z_sha = hz.hexdigest() if len(Zs) > 1 else sha256_of(Zs[0])
     Y = torch.empty((n, m), dtype=torch.float64, device=dev)
     kr = (0, k1 - k0)
 
     peer = {}  # collective="peer": the symmetric buffers are set up once, reused every step
 
-    def one_step(timing=False):
+    def one_step(timing=False, qev=None):
         if args.collective == "peer" and world > 1 and not peer:
             from paper_2210_15114_b200.distributed import PeerGroup
             peer["g"] = PeerGroup(n, m, result_ranks=(tuple(range(world))
@@ -274,8 +331,12 @@ def main_ours(args):
         if timing and sh.handle is not None and args.p % 2 == 1:
             l1.l1dm_timing_enable(sh.handle, True)
         for q in range(Q):
+            if qev is not None:
+                qev[2 * q].record(stream)
             sh.matvec(Zs[q % len(Zs)], Y, root=None if args.reduce == "allreduce" else 0,
                       overlap_blocks=args.overlap_blocks, collective=args.collective)
+            if qev is not None:
+                qev[2 * q + 1].record(stream)
         return sh
 
     for _ in range(args.warmup):
@@ -295,15 +356,23 @@ def main_ours(args):
     hl0 = l1.l1dm_handleless_launches()
     step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
     ev0.record(stream)
+    # per-query events in the last timed step (median / spread of the query time)
+    qev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * Q)]
+    torch.cuda.nvtx.range_push(f"bench {args.workload}: {args.steps} timed steps")
     for s in range(args.steps):
+        last = s == args.steps - 1
         step_ev[2 * s].record(stream)
-        sh = one_step(timing=True)
+        torch.cuda.nvtx.range_push(f"step {s}")
+        sh = one_step(timing=True, qev=qev if last else None)
+        torch.cuda.nvtx.range_pop()
         step_ev[2 * s + 1].record(stream)
         if sh.handle is not None and args.p % 2 == 1:
             timings.append(l1.l1dm_timing_read(sh.handle))  # syncs the stream (host only)
         if sh.handle is not None and args.p % 2 == 1:
             strategy = l1.l1dm_query_strategy(sh.handle, m)  # (runs serves every odd p)
-        sh.close()
+        if not last:
+            sh.close()  # the last step's handle is validated after the timed region
+    torch.cuda.nvtx.range_pop()
     ev1.record(stream)
     hl_launches = l1.l1dm_handleless_launches() - hl0
     torch.cuda.synchronize()
@@ -312,6 +381,38 @@ def main_ours(args):
     clk = clocks.stop() if rank == 0 else None
     ms_total = ev0.elapsed_time(ev1)
     step_ms = [step_ev[2 * s].elapsed_time(step_ev[2 * s + 1]) for s in range(args.steps)]
+    q_ms = [qev[2 * q].elapsed_time(qev[2 * q + 1]) for q in range(Q)]
+
+    # ---- what was timed, validated (queries 0 and Q-1): Y still
+    # holds query Q-1 of the last timed step; query 0 is re-run on the same handle (same
+    # strategy, recycled workspace).  Checked on SURVEY's rows against the definition in fp64.
+    root_has_y = rank == 0
+    Ylast = Y.clone() if root_has_y else None
+    sh.matvec(Zs[0], Y, root=None if args.reduce == "allreduce" else 0,
+              overlap_blocks=args.overlap_blocks, collective=args.collective)
+    torch.cuda.synchronize()
+    sh.close()
+    parity = parity_inputs = None
+    if root_has_y:
+        Xv = wl.make_points(w, dev)          # the full X (every rank holds only its shard)
+        rows = q12_rows(Xv)
+        checks = []
+        for label, Yq, Zq in ((f"query {Q - 1} (last timed)", Ylast, Zs[(Q - 1) % len(Zs)]),
+                              ("query 0 (re-run on the timed handle)", Y, Zs[0])):
+            want = definition_rows(Xv, Zq, rows, p=args.p)
+            got = Yq[rows]
+            checks.append({"query": label, "max_col_rel_l2": col_rel_l2(got, want),
+                           "bit_exact": bool(torch.equal(got, want))})
+        exact_required = w.x_dist == "int256" and w.z_dist == "pm1"  # c5: integers < 2^53
+        worst = max(c["max_col_rel_l2"] for c in checks)
+        parity = {"rows": int(rows.numel()),
+                  "row_set": "64 seeded random + {0, n-1, argmin h, argmax h} (SURVEY Q12)",
+                  "reference": "definition P:149/P:171 in fp64 on the device (torch, |R| n d)",
+                  "queries": checks, "max_col_rel_l2": worst, "tolerance": 1e-9,
+                  "exact_required": exact_required,
+                  "pass": (all(c["bit_exact"] for c in checks) if exact_required
+                           else worst <= 1e-9)}
+        parity_inputs = (Xv, rows, [(Ylast, Zs[(Q - 1) % len(Zs)]), (Y, Zs[0])])
     t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -522,7 +623,12 @@ def main_ours(args):
                      "frac_76B_of_hbm_peak": 76.0 * n * dl / (prep_ms * 1e-3) / 1e9 / hbm_peak}
                     if prep_ms else None),
         "step_ms_each": step_ms,
+        "ms_per_step_median": statistics.median(step_ms),
         "query_ms": (ms_step - (prep_ms or 0.0)) / Q,
+        "query_ms_last_step": {"median": statistics.median(q_ms), "min": min(q_ms),
+                               "max": max(q_ms), "mean": statistics.mean(q_ms)},
+        "inputs_sha256": {"X": x_sha, "Z": z_sha},
+        "parity": parity,
         "query_kernel_ms": query_kernel_ms,
         "kernels": kern,
         "colsums_ms_per_launch": (agg["colsums_ms"] / max(agg["colsums_launches"], 1)
@@ -531,6 +637,34 @@ def main_ours(args):
         "roofline": roof,
         "clocks": clk,
     }
+    # ---- multi-GPU readiness on one GPU (compute only): one step of a G = 8 coordinate shard
+    # (ceil(d/8) coordinates: prepare + the same queries) against the full step; t1 / (G t_G)
+    # is the efficiency an 8-GPU run could reach before any collective cost
+    if world == 1 and args.p % 2 == 1 and d >= 8 and not args.no_shard_proxy:
+        G = 8
+        kk = -(-d // G)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        Ys = torch.empty_like(Y)  # Y still holds the validated query-0 rows
+        for _ in range(2):  # one untimed, one timed
+            torch.cuda.synchronize()
+            a.record(stream)
+            hs = l1.l1dm_prepare(X, 0, kk, stream=stream)
+            l1.l1dm_set_query_mode(hs, args.mode)
+            for q in range(Q):
+                if args.p == 1:
+                    l1.l1dm_matvec(hs, Zs[q % len(Zs)], Ys, stream=stream)
+                else:
+                    l1.l1dm_matvec_lp(hs, args.p, Zs[q % len(Zs)], Ys, stream=stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            l1.l1dm_free(hs)
+        t_shard = a.elapsed_time(b)
+        del Ys
+        result["shard_proxy"] = {
+            "G": G, "coords_per_shard": kk, "t1_ms_per_step": ms_step,
+            "t_shard_ms_per_step": t_shard, "compute_efficiency": ms_step / (G * t_shard),
+            "note": "one B200: a step (prepare + the same queries) on coordinates [0, ceil(d/8)) "
+                    "vs the full step; excludes the cross-GPU sum (DESIGN.md §8)"}
     # ---- e2e through the public API with HOST buffers (pinned), N=1 only
     if world == 1 and not args.no_e2e:
         Xh = X.cpu().pin_memory()
@@ -647,7 +781,8 @@ def main_ours(args):
                                  "memory; 1 untimed step, then the mean over --steps steps, "
                                  "wall time, max over ranks"}
         del Xh, Zh, Yh, Zd
-    # ---- CPU baseline: the oracle on the host cores, bounded sample, rank 0 at N=1
+    # ---- CPU baseline: the oracle on the host cores, bounded sample, rank 0 at N=1; the same
+    # leg re-checks the validated rows with the oracle itself (the definition, in C, long double)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             cb = cpu_oracle_sample(w, Q, budget_dims=(64, 16))
@@ -655,6 +790,25 @@ def main_ours(args):
                                                          "sample", "per_core_query_updates_per_s")}
         except Exception as e:  # the baseline is reported, never required
             result["cpu_baseline"] = {"value": None, "error": str(e)}
+        if parity is not None and args.p % 2 == 1:
+            import oracle
+            Xv, rows, pairs = parity_inputs
+            Xh, rh = Xv.cpu().numpy(), rows.cpu().numpy()
+            Zcat = np.concatenate([zq.cpu().numpy() for _, zq in pairs], axis=1)
+            t0 = time.perf_counter()
+            Yr = (oracle.rows(Xh, Zcat, rh) if args.p == 1 else oracle.rows_lp(Xh, Zcat, args.p, rh))
+            worst_o, exact_o = 0.0, True
+            for i, (yq, _) in enumerate(pairs):
+                want = torch.from_numpy(np.ascontiguousarray(Yr[:, i * m:(i + 1) * m])).to(dev)
+                got = yq[rows]
+                worst_o = max(worst_o, col_rel_l2(got, want))
+                exact_o = exact_o and bool(torch.equal(got, want))
+            parity["oracle"] = {"max_col_rel_l2": worst_o, "bit_exact": exact_o,
+                                "seconds": time.perf_counter() - t0,
+                                "reference": "oracle.rows (C, long double): the same rows"}
+            parity["pass"] = parity["pass"] and (exact_o if parity["exact_required"]
+                                                 else worst_o <= 1e-9)
+    parity_inputs = None
     if w.name in wl.PAPER_TABLE3:  # context only (SURVEY §8(d) ctx): the paper's M1/Numba times
         pp, pq = wl.PAPER_TABLE3[w.name]
         result["paper_context"] = {
@@ -667,6 +821,9 @@ def main_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+    if rank == 0 and parity is not None and not parity["pass"]:
+        print(f"bench: PARITY FAILED on the timed work: {json.dumps(parity)}", file=sys.stderr)
+        return 1
     return 0
 
 

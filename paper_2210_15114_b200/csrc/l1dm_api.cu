@@ -21,6 +21,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "l1dm.h"
 #include "l1dm_internal.h"
 
@@ -309,6 +311,13 @@ struct TimedScope {
       h->pending.push_back({kind, a, b});
     }
   }
+};
+
+// NVTX range over an entry point (named ranges for profilers; header-only NVTX 3,
+// a no-op unless a tool is attached).
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
 };
 
 // Makes h's device current for a scope (calls that only synchronise or release a handle's
@@ -1064,6 +1073,7 @@ extern "C" {
 
 l1dm_status l1dm_prepare_ex(const float *X, int64_t n, int64_t ld_x, int64_t k_begin,
                             int64_t k_end, void *stream, l1dm_handle *out) {
+  NvtxRange nvtx_("l1dm_prepare_ex");
   g_err.clear();
   if (!out) return fail(L1DM_EINVAL, "out is NULL");
   *out = nullptr;
@@ -1260,11 +1270,13 @@ extern "C" {
 
 l1dm_status l1dm_matvec_ex(l1dm_handle h, const float *Z, int64_t ld_z, int64_t m, double *Y,
                            int64_t ld_y, void *stream) {
+  NvtxRange nvtx_("l1dm_matvec_ex");
   return query_entry(h, kQueryL1, 1, Z, ld_z, m, Y, ld_y, stream);
 }
 
 l1dm_status l1dm_matvec_lp_ex(l1dm_handle h, int p, const float *Z, int64_t ld_z, int64_t m,
                               double *Y, int64_t ld_y, void *stream) {
+  NvtxRange nvtx_("l1dm_matvec_lp_ex");
   return query_entry(h, kQueryLp, p, Z, ld_z, m, Y, ld_y, stream);
 }
 
@@ -1275,6 +1287,7 @@ l1dm_status l1dm_matvec_lp(l1dm_handle h, int p, const float *Z, int64_t m, doub
 
 l1dm_status l1dm_tv_matvec_ex(l1dm_handle h, const float *Z, int64_t ld_z, int64_t m, double *Y,
                               int64_t ld_y, void *stream) {
+  NvtxRange nvtx_("l1dm_tv_matvec_ex");
   return query_entry(h, kQueryTV, 1, Z, ld_z, m, Y, ld_y, stream);
 }
 
@@ -1381,6 +1394,7 @@ extern "C" {
 l1dm_status l1dm_lpp_even_matvec(const float *X, int64_t n, int64_t ld_x, int64_t d, int p,
                                  const float *Z, int64_t ld_z, int64_t m, double *Y, int64_t ld_y,
                                  void *stream) {
+  NvtxRange nvtx_("l1dm_lpp_even_matvec");
   if (p == 0) return fail(L1DM_EINVAL, "p=0: even p in {2, 4, 6} only");
   return sortfree_entry(X, n, ld_x, d, p, nullptr, Z, ld_z, m, Y, ld_y, stream);
 }
@@ -1388,11 +1402,13 @@ l1dm_status l1dm_lpp_even_matvec(const float *X, int64_t n, int64_t ld_x, int64_
 l1dm_status l1dm_bilinear_matvec(const float *X, int64_t n, int64_t ld_x, int64_t d,
                                  const double *M, const float *Z, int64_t ld_z, int64_t m,
                                  double *Y, int64_t ld_y, void *stream) {
+  NvtxRange nvtx_("l1dm_bilinear_matvec");
   return sortfree_entry(X, n, ld_x, d, 0, M, Z, ld_z, m, Y, ld_y, stream);
 }
 
 l1dm_status l1dm_l2_embed(const float *X, int64_t n, int64_t ld_x, int64_t d, const float *G,
                           int64_t k, float *Xp, int64_t ld_p, void *stream) {
+  NvtxRange nvtx_("l1dm_l2_embed");
   g_err.clear();
   if (!X || !G || !Xp) return fail(L1DM_EINVAL, "X, G or Xp is NULL");
   if (n < 1 || d < 1 || k < 1 || ld_x < d || ld_p < k)
@@ -1412,6 +1428,7 @@ l1dm_status l1dm_l2_embed(const float *X, int64_t n, int64_t ld_x, int64_t d, co
 l1dm_status l1dm_matvec_pipelined(l1dm_handle h, const float *Z, int64_t ld_z, int64_t m,
                                   double *Y, int64_t ld_y, void *stream, int64_t point_blocks,
                                   void *const *block_events) {
+  NvtxRange nvtx_("l1dm_matvec_pipelined");
   g_err.clear();
   if (!h) return fail(L1DM_EINVAL, "handle is NULL");
   if (!Z || !Y) return fail(L1DM_EINVAL, "Z or Y is NULL");
@@ -1494,6 +1511,7 @@ l1dm_status check_peers(const l1dm_peer_t *pr, int64_t n, int64_t m) {
 
 l1dm_status l1dm_matvec_push(l1dm_handle h, const float *Z, int64_t ld_z, int64_t m,
                              const l1dm_peer_t *peers, unsigned epoch, void *stream) {
+  NvtxRange nvtx_("l1dm_matvec_push");
   g_err.clear();
   if (!h || !Z) return fail(L1DM_EINVAL, "handle or Z is NULL");
   if (m < 1 || ld_z < m) return fail(L1DM_EINVAL, "m=%lld ld_z=%lld invalid", (long long)m,
@@ -1543,6 +1561,7 @@ l1dm_status l1dm_matvec_push(l1dm_handle h, const float *Z, int64_t ld_z, int64_
 
 l1dm_status l1dm_peer_reduce(const l1dm_peer_t *peers, int64_t n, int64_t m, unsigned epoch,
                              unsigned targets, void *stream) {
+  NvtxRange nvtx_("l1dm_peer_reduce");
   g_err.clear();
   l1dm_status st = check_peers(peers, n, m);
   if (st != L1DM_OK) return st;
@@ -1572,6 +1591,7 @@ l1dm_status l1dm_peer_reduce(const l1dm_peer_t *peers, int64_t n, int64_t m, uns
 
 l1dm_status l1dm_peer_wait(const l1dm_peer_t *peers, unsigned epoch, int64_t n, int64_t m,
                            double *Y, int64_t ld_y, void *stream) {
+  NvtxRange nvtx_("l1dm_peer_wait");
   g_err.clear();
   l1dm_status st = check_peers(peers, n, m);
   if (st != L1DM_OK) return st;
@@ -1632,6 +1652,7 @@ l1dm_status l1dm_query_strategy(l1dm_handle h, int64_t m, int *strategy) {
 l1dm_status l1dm_matvec_colblocks(l1dm_handle h, const float *Z, int64_t ld_z, int64_t m,
                                   double *Yb, void *stream, int64_t nevents,
                                   void *const *events) {
+  NvtxRange nvtx_("l1dm_matvec_colblocks");
   g_err.clear();
   if (!h) return fail(L1DM_EINVAL, "handle is NULL");
   if (!Z || !Yb || m < 2 || ld_z < m)

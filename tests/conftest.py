@@ -61,3 +61,15 @@ def col_rel_l2(Y, Yref, floor=0.0):
         den = max(den, floor)
         worst = max(worst, num / den if den > 0 else (0.0 if num == 0 else float("inf")))
     return worst
+
+
+def q12_rows(X, count=64, seed=12):
+    """SURVEY §8(c) SAMPLE rows (Q12): `count` seeded random rows plus rows 0 and n-1 and the
+    points with the smallest and largest coordinate sum (the extremes of |x|, where the
+    prefix sums' cancellation is largest)."""
+    X = np.asarray(X)
+    n = X.shape[0]
+    h = X.astype(np.float64).sum(axis=1)
+    r = set(np.random.default_rng(seed).integers(0, n, size=count).tolist())
+    r |= {0, n - 1, int(np.argmin(h)), int(np.argmax(h))}
+    return np.array(sorted(r), dtype=np.int64)

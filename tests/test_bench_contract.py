@@ -42,6 +42,10 @@ def check_ours(d, n_gpus):
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
     assert d["e2e"]["d2h_bytes_per_step"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+    # the timed work is validated (queries 0 and Q-1) and the inputs hashed
+    assert d["parity"]["pass"] and d["parity"]["max_col_rel_l2"] <= 1e-9
+    assert len(d["parity"]["queries"]) == 2 and d["parity"]["rows"] >= 4
+    assert len(d["inputs_sha256"]["X"]) == 64
 
 
 @pytest.mark.gpu

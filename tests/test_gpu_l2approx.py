@@ -1,8 +1,9 @@
 """Approximate l2 through the l1 engine on the GPU.  Parity: the library's
 embedding equals the oracle's (same G from workloads.gaussian_embedding; fp64 accumulation on
 both sides, one fp32 rounding: equal up to an fp32 ulp where the fp64 and long-double sums
-round differently); the full chain B Z against oracle.brute on the oracle's X' (1e-9, the l1
-bar); and the approximation quality against the exact l2 product (Thm. l2_approx)."""
+round differently); the full chain B Z against oracle.brute on the oracle's X' (1e-6: the two X' differ
+by fp32 ulps, so B differs by up to 2k ulps per entry); the chain's l1 stage on the oracle's X'
+at the l1 bar (1e-9); and the approximation quality against the exact l2 product (Thm. l2_approx)."""
 import numpy as np
 import pytest
 import torch
@@ -42,4 +43,12 @@ def test_chain_parity_and_approximation_quality():
     assert col_rel_l2(Yg.cpu().numpy(), oracle.brute(Xp, Z)) <= 1e-6   # fp32-ulp X' differences
     exact = oracle.brute_l2(X, Z)
     assert col_rel_l2(Yg.cpu().numpy(), exact) <= eps                   # ||(A - B) z|| <= eps-ish
+    # the chain's l1 stage at the l1 bar: the oracle's own X' (never an output of the CUDA
+    # path) through the library's prepare + query, against the oracle's product on it
+    h = l1.l1dm_prepare(torch.from_numpy(Xp).cuda())
+    Yc = l1.l1dm_matvec(h, torch.from_numpy(Z).cuda())
+    torch.cuda.synchronize()
+    l1.l1dm_sync(h)
+    assert col_rel_l2(Yc.cpu().numpy(), oracle.brute(Xp, Z)) <= 1e-9
+    l1.l1dm_free(h)
     eng.close()
