@@ -271,6 +271,99 @@ L1DM_API l1dm_status l1dm_peer_wait(const l1dm_peer_t *peers, unsigned epoch, in
  * A timed-out wait ends every other wait of the same rank early (they poll the timeout word). */
 L1DM_API l1dm_status l1dm_peer_check(const l1dm_peer_t *peers, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * Matrix-free consumers of the block product (PAPER.md "Applications",
+ * P:727-817): everything between the products runs in this library too (fp64 tensor-core
+ * GEMMs, a device Jacobi eigensolver, device-scalar conjugate gradients); DESIGN.md §2d.
+ *
+ * An operator names the matrix A the consumers touch only through products A V:
+ *   L1DM_OP_SORTED    a prepared handle h, p in {1, 3, 5, 7}: A_ij = ||x_i - x_j||_p^p
+ *                     (l1dm_matvec / l1dm_matvec_lp; n = the handle's points)
+ *   L1DM_OP_EVEN      X (n x ld_x fp32, d coordinates, device), p in {2, 4, 6}:
+ *                     A_ij = ||x_i - x_j||_p^p sort-free (l1dm_lpp_even_matvec)
+ *   L1DM_OP_BILINEAR  X as above and M (d x d fp64, device): A_ij = x_i^T M x_j
+ *                     (l1dm_bilinear_matvec; PSD when M is, the CG case of Thm. linear_system)
+ * The products take fp32 blocks (BASELINE.json); an fp64 block V is applied as
+ * A fp32(V) + A fp32(V - fp32(V)) in one product of width 2b (linearity, R21).
+ * Every buffer below is DEVICE memory; every call is stream-ordered on `stream` unless it says
+ * otherwise, and uses the stream-ordered allocator for its scratch. */
+#define L1DM_OP_SORTED 0
+#define L1DM_OP_EVEN 1
+#define L1DM_OP_BILINEAR 2
+typedef struct {
+  int kind;            /* L1DM_OP_* */
+  int p;               /* exponent (SORTED: 1, 3, 5, 7; EVEN: 2, 4, 6; BILINEAR: ignored) */
+  l1dm_handle h;       /* SORTED */
+  const float *X;      /* EVEN, BILINEAR: n x ld_x fp32 */
+  int64_t n, ld_x, d;  /* EVEN, BILINEAR (SORTED: n is taken from the handle) */
+  const double *M;     /* BILINEAR: d x d fp64 row-major */
+} l1dm_operator_t;
+
+/* C (M x N, ldc) = alpha op(A) B + beta C in fp64 on the tensor cores (DMMA), deterministic:
+ *   trans_a = 0: op(A) = A, A is M x K (lda);  trans_a = 1: op(A) = A^T, A is K x M (lda);
+ *   B is K x N (ldb); all row-major.  beta = 0 never reads C.  Errors: EINVAL (null, sizes,
+ *   leading dimensions), EDEVICE, ENOMEM, ECUDA. */
+L1DM_API l1dm_status l1dm_gemm(int trans_a, int64_t M, int64_t N, int64_t K, double alpha,
+                               const double *A, int64_t lda, const double *B, int64_t ldb,
+                               double beta, double *C, int64_t ldc, void *stream);
+
+/* Symmetric eigen-decomposition by cyclic Jacobi (round-robin parallel ordering): A (N x N,
+ * lda, symmetric; only read) -> W (N eigenvalues, in no particular order) and V (N x N, ldv;
+ * column j is the unit eigenvector of W[j]).  Errors: EINVAL, EDEVICE, ENOMEM, ECUDA. */
+L1DM_API l1dm_status l1dm_syevj(int64_t N, const double *A, int64_t lda, double *W, double *V,
+                                int64_t ldv, void *stream);
+
+/* Y (n x b, ldy) = A V for an fp64 block V (n x b, ldv) through the operator's fp32 product
+ * (hi/lo split, one product of 2b columns).  Errors: EINVAL (operator, sizes), as the
+ * operator's product. */
+L1DM_API l1dm_status l1dm_op_apply(const l1dm_operator_t *op, const double *V, int64_t ldv,
+                                   int64_t b, double *Y, int64_t ldy, void *stream);
+
+/* Randomized block Krylov for the k largest |eigenvalues| of the symmetric A = its top-k
+ * singular values (Thm. musco; Thm. bakshi22 P:727-731 via Thm. opt_lowrank_p
+ * P:757-766): K = [A Pi, A^2 Pi, ..., A^q Pi], each new block orthonormalised
+ * against the earlier ones (block classical Gram-Schmidt: against the last two blocks, then
+ * against the whole basis) and within itself (CholeskyQR2 with column dropping: columns whose
+ * residual is below 1e-7 of the block's largest column norm are dropped as zero columns: the
+ * Krylov space is exhausted), the Rayleigh quotient T = Q^T A Q
+ * assembled from the orthogonalisation coefficients (block Lanczos with full
+ * re-orthogonalisation), T = V diag(lam) V^T by Jacobi, sigma = |lam| in nonincreasing order,
+ * Z = Q V_k.  q + 1 block products of width 2b.
+ * Pi: the n x b start block (the method's random draw; the caller passes it, e.g. i.i.d.
+ * N(0,1) from a seeded generator).  1 <= k <= b <= 96, q >= 1, q b <= n.
+ * Outputs: sigma[k], lam[k] (signed Ritz values), Z (n x k, ldz, orthonormal columns); any
+ * output may be NULL except sigma.  Synchronous (returns when the outputs are ready).
+ * Errors: EINVAL, as l1dm_op_apply, ENOMEM, ECUDA. */
+typedef struct {
+  int64_t products;   /* block products A V */
+  int64_t columns;    /* fp32 columns through the product (2b per product) */
+  int64_t block, depth;
+  double product_ms;  /* device time in the products (CUDA events on `stream`) */
+  double total_ms;    /* device time of the whole call */
+} l1dm_krylov_info_t;
+L1DM_API l1dm_status l1dm_block_krylov(const l1dm_operator_t *op, int64_t k, int64_t block,
+                                       int64_t depth, const double *Pi, double *sigma,
+                                       double *lam, double *Z, int64_t ldz, void *stream,
+                                       l1dm_krylov_info_t *info);
+
+/* Conjugate gradients for A x = b (Thm. linear_system) with every scalar on the
+ * device: the host only looks at the convergence flag every 8 iterations (asynchronous copy,
+ * one chunk in flight), iterations after convergence leave x unchanged.  A must be symmetric
+ * positive definite; normal_equations = 1 solves A^2 x = A b instead (symmetric indefinite A,
+ * such as l1 distance matrices), two products per iteration.  Stops when
+ * ||r|| <= tol ||rhs|| or after maxit iterations (then converged = 0: reported, never silent,
+ * SPEC S:361).  b, x: n fp64 (device).  Synchronous.
+ * info: iterations, relative residual ||A x - b|| / ||b|| (one more product), converged. */
+typedef struct {
+  int64_t iterations;
+  double residual;
+  int converged;
+  int64_t products;
+} l1dm_cg_info_t;
+L1DM_API l1dm_status l1dm_cg(const l1dm_operator_t *op, const double *b, double *x, double tol,
+                             int64_t maxit, int normal_equations, void *stream,
+                             l1dm_cg_info_t *info);
+
 /* Release every buffer the handle owns.  NULL is a no-op.  Synchronises the
  * handle's stream first. */
 L1DM_API void l1dm_free(l1dm_handle h);

@@ -37,6 +37,7 @@ EXPORTS = [
     "l1dm_ipc_alloc", "l1dm_ipc_free", "l1dm_ipc_open", "l1dm_ipc_close", "l1dm_matvec_push",
     "l1dm_peer_reduce", "l1dm_peer_wait", "l1dm_peer_check",
     "l1dm_last_error", "l1dm_handleless_launches", "l1dm_version",
+    "l1dm_gemm", "l1dm_syevj", "l1dm_op_apply", "l1dm_block_krylov", "l1dm_cg",
 ]
 
 
@@ -62,6 +63,24 @@ class PeerT(ctypes.Structure):
                 ("inbox", ctypes.c_void_p * MAX_PEERS), ("flags", ctypes.c_void_p * MAX_PEERS),
                 ("ybuf", ctypes.c_void_p * MAX_PEERS), ("timeout", ctypes.c_void_p),
                 ("n", ctypes.c_int64), ("m", ctypes.c_int64)]
+
+
+class OperatorT(ctypes.Structure):
+    """l1dm_operator_t (include/l1dm.h): the matrix the NEXT-2 consumers apply."""
+    _fields_ = [("kind", ctypes.c_int), ("p", ctypes.c_int), ("h", ctypes.c_void_p),
+                ("X", ctypes.c_void_p), ("n", ctypes.c_int64), ("ld_x", ctypes.c_int64),
+                ("d", ctypes.c_int64), ("M", ctypes.c_void_p)]
+
+
+class KrylovInfoT(ctypes.Structure):
+    _fields_ = [("products", ctypes.c_int64), ("columns", ctypes.c_int64),
+                ("block", ctypes.c_int64), ("depth", ctypes.c_int64),
+                ("product_ms", ctypes.c_double), ("total_ms", ctypes.c_double)]
+
+
+class CGInfoT(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int64), ("residual", ctypes.c_double),
+                ("converged", ctypes.c_int), ("products", ctypes.c_int64)]
 
 
 class TimingT(ctypes.Structure):
@@ -136,6 +155,16 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.l1dm_peer_check.argtypes = [ctypes.POINTER(PeerT), vp]
     for name in ("l1dm_ipc_alloc", "l1dm_ipc_free", "l1dm_ipc_open", "l1dm_ipc_close",
                  "l1dm_matvec_push", "l1dm_peer_reduce", "l1dm_peer_wait", "l1dm_peer_check"):
+        getattr(lib, name).restype = st
+    dbl = ctypes.c_double
+    lib.l1dm_gemm.argtypes = [i32, i64, i64, i64, dbl, vp, i64, vp, i64, dbl, vp, i64, vp]
+    lib.l1dm_syevj.argtypes = [i64, vp, i64, vp, vp, i64, vp]
+    lib.l1dm_op_apply.argtypes = [ctypes.POINTER(OperatorT), vp, i64, i64, vp, i64, vp]
+    lib.l1dm_block_krylov.argtypes = [ctypes.POINTER(OperatorT), i64, i64, i64, vp, vp, vp, vp,
+                                      i64, vp, ctypes.POINTER(KrylovInfoT)]
+    lib.l1dm_cg.argtypes = [ctypes.POINTER(OperatorT), vp, vp, dbl, i64, i32, vp,
+                            ctypes.POINTER(CGInfoT)]
+    for name in ("l1dm_gemm", "l1dm_syevj", "l1dm_op_apply", "l1dm_block_krylov", "l1dm_cg"):
         getattr(lib, name).restype = st
     lib.l1dm_handleless_launches.argtypes = []
     lib.l1dm_handleless_launches.restype = i64
@@ -558,3 +587,143 @@ def l1dm_handleless_launches() -> int:
 
 def l1dm_version() -> str:
     return load_library().l1dm_version().decode()
+
+
+# ------------------------------------------------------------ matrix-free consumers (NEXT-2)
+OP_SORTED, OP_EVEN, OP_BILINEAR = 0, 1, 2
+
+
+class Operator:
+    """The matrix A of a NEXT-2 consumer (include/l1dm.h l1dm_operator_t), touched only through
+    the library's block product: a prepared handle (l1 or odd l_p^p), sort-free even l_p^p on
+    device X, or the bilinear form x_i^T M x_j.  Keeps its tensors alive."""
+
+    def __init__(self, kind: int, n: int, device, *, handle: Handle | None = None, p: int = 1,
+                 X: torch.Tensor | None = None, M: torch.Tensor | None = None):
+        self.kind, self.n, self.device = kind, n, torch.device(device)
+        self._keep = (handle, X, M)
+        o = OperatorT()
+        o.kind, o.p = kind, int(p)
+        o.h = handle.ptr if handle is not None else None
+        if X is not None:
+            o.X = X.data_ptr()
+            o.n, o.ld_x, o.d = X.shape[0], X.stride(0), X.shape[1]
+        if M is not None:
+            o.M = M.data_ptr()
+        self.c = o
+
+    @classmethod
+    def sorted(cls, h: Handle, p: int = 1) -> "Operator":
+        return cls(OP_SORTED, h.n, torch.device("cuda", h.device), handle=h, p=p)
+
+    @classmethod
+    def even(cls, X: torch.Tensor, p: int) -> "Operator":
+        X = _as_f32_2d(X, "X")
+        if not X.is_cuda:
+            raise ValueError("the even-p operator needs a CUDA X")
+        return cls(OP_EVEN, X.shape[0], X.device, X=X, p=p)
+
+    @classmethod
+    def bilinear(cls, X: torch.Tensor, M: torch.Tensor) -> "Operator":
+        X = _as_f32_2d(X, "X")
+        M = torch.as_tensor(M, dtype=torch.float64, device=X.device).contiguous()
+        if not X.is_cuda or tuple(M.shape) != (X.shape[1], X.shape[1]):
+            raise ValueError("the bilinear operator needs a CUDA X and a d x d M")
+        return cls(OP_BILINEAR, X.shape[0], X.device, X=X, M=M)
+
+
+def _f64_dev(t, name, device):
+    t = torch.as_tensor(t)
+    if t.device.type != "cuda":
+        raise ValueError(f"{name} must be a CUDA tensor (the dense steps run only in the library)")
+    if t.dtype != torch.float64:
+        raise TypeError(f"{name} must be float64")
+    if t.device != device:
+        raise ValueError(f"{name} must be on {device}")
+    if t.dim() == 1:
+        t = t.view(-1, 1)
+    if t.stride(-1) != 1:
+        t = t.contiguous()
+    return t
+
+
+def l1dm_gemm(A: torch.Tensor, B: torch.Tensor, C: torch.Tensor | None = None, *,
+              trans_a: bool = False, alpha: float = 1.0, beta: float = 0.0, stream=None):
+    """C = alpha op(A) B + beta C in fp64 on the tensor cores (device tensors, row-major)."""
+    dev = A.device
+    A, B = _f64_dev(A, "A", dev), _f64_dev(B, "B", dev)
+    M = A.shape[1] if trans_a else A.shape[0]
+    K = A.shape[0] if trans_a else A.shape[1]
+    if B.shape[0] != K:
+        raise ValueError(f"inner dimensions differ: op(A) is {M} x {K}, B is {tuple(B.shape)}")
+    N = B.shape[1]
+    if C is None:
+        if beta != 0.0:
+            raise ValueError("beta != 0 needs C")
+        C = torch.empty((M, N), dtype=torch.float64, device=dev)
+    C = _f64_dev(C, "C", dev)
+    with torch.cuda.device(dev):
+        _check(load_library().l1dm_gemm(1 if trans_a else 0, M, N, K, float(alpha), _ptr(A),
+                                        A.stride(0), _ptr(B), B.stride(0), float(beta), _ptr(C),
+                                        C.stride(0), _stream_of(C, stream)), "l1dm_gemm")
+    return C
+
+
+def l1dm_syevj(A: torch.Tensor, stream=None):
+    """Symmetric eigen-decomposition (device Jacobi): returns (W, V), A V = V diag(W)."""
+    dev = A.device
+    A = _f64_dev(A, "A", dev)
+    N = A.shape[0]
+    if A.shape != (N, N):
+        raise ValueError("A must be square")
+    W = torch.empty(N, dtype=torch.float64, device=dev)
+    V = torch.empty((N, N), dtype=torch.float64, device=dev)
+    with torch.cuda.device(dev):
+        _check(load_library().l1dm_syevj(N, _ptr(A), A.stride(0), _ptr(W), _ptr(V), V.stride(0),
+                                         _stream_of(A, stream)), "l1dm_syevj")
+    return W, V
+
+
+def l1dm_op_apply(op: Operator, V: torch.Tensor, Y: torch.Tensor | None = None, stream=None):
+    """A V for an fp64 block V (n x b) through the fp32 product (hi/lo split)."""
+    squeeze = V.dim() == 1
+    V = _f64_dev(V, "V", op.device)
+    n, b = V.shape
+    if n != op.n:
+        raise ValueError(f"V has {n} rows, the operator {op.n}")
+    if Y is None:
+        Y = torch.empty((n, b), dtype=torch.float64, device=op.device)
+    with torch.cuda.device(op.device):
+        _check(load_library().l1dm_op_apply(ctypes.byref(op.c), _ptr(V), V.stride(0), b, _ptr(Y),
+                                            Y.stride(0), _stream_of(V, stream)), "l1dm_op_apply")
+    return Y.view(-1) if squeeze else Y
+
+
+def l1dm_block_krylov(op: Operator, k: int, Pi: torch.Tensor, depth: int, stream=None):
+    """Top-k |eigenvalues| (= singular values) of A by block Krylov from the start block Pi
+    (n x b fp64); returns (sigma, lam, Z, info dict)."""
+    Pi = _f64_dev(Pi, "Pi", op.device).contiguous()
+    n, b = Pi.shape
+    sigma = torch.empty(k, dtype=torch.float64, device=op.device)
+    lam = torch.empty(k, dtype=torch.float64, device=op.device)
+    Z = torch.empty((n, k), dtype=torch.float64, device=op.device)
+    info = KrylovInfoT()
+    with torch.cuda.device(op.device):
+        _check(load_library().l1dm_block_krylov(ctypes.byref(op.c), k, b, depth, _ptr(Pi),
+                                                _ptr(sigma), _ptr(lam), _ptr(Z), k,
+                                                _stream_of(Pi, stream), ctypes.byref(info)),
+               "l1dm_block_krylov")
+    return sigma, lam, Z, {f: getattr(info, f) for f, _ in KrylovInfoT._fields_}
+
+
+def l1dm_cg(op: Operator, b: torch.Tensor, *, tol: float = 1e-8, maxit: int = 500,
+            normal_equations: bool = False, stream=None):
+    """Conjugate gradients with device scalars; returns (x, info dict)."""
+    b = _f64_dev(b, "b", op.device).reshape(-1).contiguous()
+    x = torch.empty_like(b)
+    info = CGInfoT()
+    with torch.cuda.device(op.device):
+        _check(load_library().l1dm_cg(ctypes.byref(op.c), _ptr(b), _ptr(x), float(tol), int(maxit),
+                                      1 if normal_equations else 0, _stream_of(b, stream),
+                                      ctypes.byref(info)), "l1dm_cg")
+    return x, {f: getattr(info, f) for f, _ in CGInfoT._fields_}

@@ -1858,3 +1858,471 @@ int64_t l1dm_handleless_launches(void) { return g_handleless_launches.load(); }
 const char *l1dm_version(void) { return "l1dm 0.1.0 (sm_100a)"; }
 
 }  // extern "C"
+
+// ============================================================================================
+// Matrix-free consumers (include/l1dm.h): block Krylov and
+// conjugate gradients with every dense step on the device (l1dm_dense.cu) and A touched only
+// through the operator's block product.
+// ============================================================================================
+namespace {
+
+// One stream-ordered scratch allocation carved into aligned pieces; freed (stream-ordered) on
+// scope exit.
+struct Scratch {
+  cudaStream_t s;
+  char *base = nullptr;
+  size_t used = 0, cap = 0;
+  explicit Scratch(cudaStream_t s_) : s(s_) {}
+  ~Scratch() {
+    if (base) cudaFreeAsync(base, s);
+  }
+  cudaError_t reserve(size_t bytes) {
+    cap = bytes;
+    return cudaMallocAsync(reinterpret_cast<void **>(&base), bytes ? bytes : 256, s);
+  }
+  template <typename T>
+  T *take(size_t count) {
+    const size_t off = (used + 255) & ~(size_t)255;
+    used = off + count * sizeof(T);
+    return reinterpret_cast<T *>(base + off);
+  }
+  static size_t bytes_for(size_t count, size_t elem) { return ((count * elem + 255) & ~(size_t)255); }
+};
+
+l1dm_status op_check(const l1dm_operator_t *op, int64_t *n_out) {
+  if (!op) return fail(L1DM_EINVAL, "operator is NULL");
+  switch (op->kind) {
+    case L1DM_OP_SORTED: {
+      if (!op->h) return fail(L1DM_EINVAL, "sorted operator without a handle");
+      if (op->p != 1 && op->p != 3 && op->p != 5 && op->p != 7)
+        return fail(L1DM_EINVAL, "sorted operator: p=%d not in {1, 3, 5, 7}", op->p);
+      l1dm_status st = check_device(op->h);
+      if (st != L1DM_OK) return st;
+      *n_out = op->h->n;
+      return L1DM_OK;
+    }
+    case L1DM_OP_EVEN:
+    case L1DM_OP_BILINEAR:
+      if (!op->X || (op->kind == L1DM_OP_BILINEAR && !op->M))
+        return fail(L1DM_EINVAL, "operator X (or M) is NULL");
+      if (op->n < 1 || op->d < 1 || op->ld_x < op->d)
+        return fail(L1DM_EINVAL, "operator n=%lld d=%lld ld_x=%lld invalid", (long long)op->n,
+                    (long long)op->d, (long long)op->ld_x);
+      if (op->kind == L1DM_OP_EVEN && op->p != 2 && op->p != 4 && op->p != 6)
+        return fail(L1DM_EINVAL, "even operator: p=%d not in {2, 4, 6}", op->p);
+      if (!is_device_pointer(op->X) || (op->kind == L1DM_OP_BILINEAR && !is_device_pointer(op->M)))
+        return fail(L1DM_EINVAL, "operator X and M must be device memory");
+      *n_out = op->n;
+      return L1DM_OK;
+    default:
+      return fail(L1DM_EINVAL, "unknown operator kind %d", op->kind);
+  }
+}
+
+// Y = A Z for an fp32 block (the operator's own product, stream-ordered)
+l1dm_status op_apply_f32(const l1dm_operator_t *op, const float *Z, int64_t ldz, int64_t m,
+                         double *Y, int64_t ldy, cudaStream_t s) {
+  switch (op->kind) {
+    case L1DM_OP_SORTED:
+      return op->p == 1 ? l1dm_matvec_ex(op->h, Z, ldz, m, Y, ldy, s)
+                        : l1dm_matvec_lp_ex(op->h, op->p, Z, ldz, m, Y, ldy, s);
+    case L1DM_OP_EVEN:
+      return l1dm_lpp_even_matvec(op->X, op->n, op->ld_x, op->d, op->p, Z, ldz, m, Y, ldy, s);
+    default:
+      return l1dm_bilinear_matvec(op->X, op->n, op->ld_x, op->d, op->M, Z, ldz, m, Y, ldy, s);
+  }
+}
+
+// Y = A V for fp64 V through the fp32 product: [hi | lo] in one product of 2b columns
+l1dm_status op_apply_f64(const l1dm_operator_t *op, int64_t n, const double *V, int64_t ldv,
+                         int64_t b, double *Y, int64_t ldy, float *zs, double *yr,
+                         cudaStream_t s) {
+  launch_split_hilo(n, b, V, ldv, zs, s);
+  l1dm_status st = op_apply_f32(op, zs, 2 * b, 2 * b, yr, 2 * b, s);
+  if (st != L1DM_OK) return st;
+  launch_combine_hilo(n, b, yr, Y, ldy, s);
+  return L1DM_OK;
+}
+
+int device_sms() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+}  // namespace
+
+extern "C" {
+
+l1dm_status l1dm_gemm(int trans_a, int64_t M, int64_t N, int64_t K, double alpha, const double *A,
+                      int64_t lda, const double *B, int64_t ldb, double beta, double *C,
+                      int64_t ldc, void *stream) {
+  NvtxRange nvtx_("l1dm_gemm");
+  g_err.clear();
+  if (!C || (K > 0 && (!A || !B))) return fail(L1DM_EINVAL, "A, B or C is NULL");
+  if (M < 1 || N < 1 || K < 0 || ldc < N || (K > 0 && (ldb < N || lda < (trans_a ? M : K))))
+    return fail(L1DM_EINVAL, "gemm sizes M=%lld N=%lld K=%lld lda=%lld ldb=%lld ldc=%lld invalid",
+                (long long)M, (long long)N, (long long)K, (long long)lda, (long long)ldb,
+                (long long)ldc);
+  int dev = 0;
+  l1dm_status st = check_arch(&dev);
+  if (st != L1DM_OK) return st;
+  if ((K > 0 && (!is_device_pointer(A) || !is_device_pointer(B))) || !is_device_pointer(C))
+    return fail(L1DM_EINVAL, "l1dm_gemm takes device pointers");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int sms = device_sms();
+  Scratch sc(s);
+  CUDA_TRY(sc.reserve(gemm_workspace(trans_a ? 1 : 0, M, N, K, sms)));
+  g_handleless_launches += launch_gemm(trans_a ? 1 : 0, M, N, K, alpha, A, lda, B, ldb, beta, C,
+                                       ldc, reinterpret_cast<double *>(sc.base), sms, s);
+  CUDA_TRY(cudaGetLastError());
+  return L1DM_OK;
+}
+
+l1dm_status l1dm_syevj(int64_t N, const double *A, int64_t lda, double *W, double *V, int64_t ldv,
+                       void *stream) {
+  NvtxRange nvtx_("l1dm_syevj");
+  g_err.clear();
+  if (!A || !W || !V) return fail(L1DM_EINVAL, "A, W or V is NULL");
+  if (N < 1 || lda < N || ldv < N || N > (1 << 15))
+    return fail(L1DM_EINVAL, "syevj N=%lld lda=%lld ldv=%lld invalid", (long long)N,
+                (long long)lda, (long long)ldv);
+  int dev = 0;
+  l1dm_status st = check_arch(&dev);
+  if (st != L1DM_OK) return st;
+  if (!is_device_pointer(A) || !is_device_pointer(W) || !is_device_pointer(V))
+    return fail(L1DM_EINVAL, "l1dm_syevj takes device pointers");
+  cudaStream_t s = (cudaStream_t)stream;
+  Scratch sc(s);
+  const bool big = false;  // both Jacobi variants only read A
+  CUDA_TRY(sc.reserve(Scratch::bytes_for(jacobi_workspace(N), 1) +
+                      (big ? Scratch::bytes_for((size_t)N * N, sizeof(double)) : 0) + 512));
+  double *ws = sc.take<double>(jacobi_workspace(N) / sizeof(double) + 1);
+  double *Acp = const_cast<double *>(A);
+  int64_t ld = lda;
+  if (big) {
+    Acp = sc.take<double>((size_t)N * N);
+    CUDA_TRY(cudaMemcpy2DAsync(Acp, N * sizeof(double), A, lda * sizeof(double),
+                               N * sizeof(double), N, cudaMemcpyDeviceToDevice, s));
+    ld = N;
+  }
+  static const bool dbg = getenv("L1DM_DEBUG_JACOBI") != nullptr;
+  int *stats = dbg ? sc.take<int>(4) : nullptr;
+  g_handleless_launches += launch_jacobi(N, Acp, ld, W, V, ldv, ws, device_sms(), s, stats);
+  CUDA_TRY(cudaGetLastError());
+  if (dbg) {
+    int hs = -1;
+    cudaMemcpyAsync(&hs, stats, sizeof(int), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    fprintf(stderr, "[l1dm] syevj N=%lld sweeps=%d\n", (long long)N, hs);
+  }
+  return L1DM_OK;
+}
+
+l1dm_status l1dm_op_apply(const l1dm_operator_t *op, const double *V, int64_t ldv, int64_t b,
+                          double *Y, int64_t ldy, void *stream) {
+  NvtxRange nvtx_("l1dm_op_apply");
+  g_err.clear();
+  int64_t n = 0;
+  l1dm_status st = op_check(op, &n);
+  if (st != L1DM_OK) return st;
+  if (!V || !Y || b < 1 || ldv < b || ldy < b)
+    return fail(L1DM_EINVAL, "V/Y NULL or b=%lld ldv=%lld ldy=%lld invalid", (long long)b,
+                (long long)ldv, (long long)ldy);
+  if (!is_device_pointer(V) || !is_device_pointer(Y))
+    return fail(L1DM_EINVAL, "l1dm_op_apply takes device pointers");
+  cudaStream_t s = (cudaStream_t)stream;
+  Scratch sc(s);
+  CUDA_TRY(sc.reserve(Scratch::bytes_for((size_t)n * 2 * b, sizeof(float)) +
+                      Scratch::bytes_for((size_t)n * 2 * b, sizeof(double))));
+  float *zs = sc.take<float>((size_t)n * 2 * b);
+  double *yr = sc.take<double>((size_t)n * 2 * b);
+  g_handleless_launches += 2;
+  return op_apply_f64(op, n, V, ldv, b, Y, ldy, zs, yr, s);
+}
+
+l1dm_status l1dm_block_krylov(const l1dm_operator_t *op, int64_t k, int64_t block, int64_t depth,
+                              const double *Pi, double *sigma, double *lam, double *Z,
+                              int64_t ldz, void *stream, l1dm_krylov_info_t *info) {
+  NvtxRange nvtx_("l1dm_block_krylov");
+  g_err.clear();
+  int64_t n = 0;
+  l1dm_status st = op_check(op, &n);
+  if (st != L1DM_OK) return st;
+  const int64_t b = block, q = depth, Qw = block * depth;
+  if (!Pi || !sigma) return fail(L1DM_EINVAL, "Pi or sigma is NULL");
+  if (k < 1 || b < k || b > 96 || q < 1 || Qw > n || (Z && ldz < k))
+    return fail(L1DM_EINVAL, "krylov k=%lld block=%lld depth=%lld (n=%lld) invalid: need 1 <= k "
+                "<= block <= 96, depth >= 1, block*depth <= n", (long long)k, (long long)b,
+                (long long)q, (long long)n);
+  for (const void *ptr : {(const void *)Pi, (const void *)sigma, (const void *)lam,
+                          (const void *)Z})
+    if (ptr && !is_device_pointer(ptr)) return fail(L1DM_EINVAL, "krylov buffers must be device memory");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int sms = device_sms();
+  // scratch: basis, Krylov block, orthogonalisation temporaries, T and its eigenvectors
+  const size_t gws = std::max({gemm_workspace(1, Qw, b, n, sms), gemm_workspace(1, b, b, n, sms)});
+  size_t bytes = 0;
+  auto add = [&](size_t count, size_t el) { bytes += Scratch::bytes_for(count, el); };
+  add((size_t)n * Qw, 8);                    // Qb
+  add((size_t)n * b, 8);                     // W
+  add((size_t)n * b, 8);                     // Vt
+  add((size_t)n * 2 * b, 4);                 // zs
+  add((size_t)n * 2 * b, 8);                 // yr
+  for (int i = 0; i < 4; ++i) add((size_t)b * b, 8);  // G0, G, Gv, S
+  add((size_t)b, 8);                         // lamb
+  add((size_t)Qw * b, 8);                    // Ct
+  add((size_t)Qw * Qw, 8);                   // T
+  add((size_t)Qw * Qw, 8);                   // TV
+  add((size_t)Qw, 8);                        // TW
+  add((size_t)Qw * k, 8);                    // Vs
+  add((size_t)k, 4);                         // order
+  add(gws / 8 + 1, 8);
+  add(jacobi_workspace(std::max(Qw, b)) / 8 + 1, 8);
+  Scratch sc(s);
+  CUDA_TRY(sc.reserve(bytes));
+  double *Qb = sc.take<double>((size_t)n * Qw), *W = sc.take<double>((size_t)n * b);
+  double *Vt = sc.take<double>((size_t)n * b);
+  float *zs = sc.take<float>((size_t)n * 2 * b);
+  double *yr = sc.take<double>((size_t)n * 2 * b);
+  double *G0 = sc.take<double>(b * b), *G = sc.take<double>(b * b);
+  double *Gv = sc.take<double>(b * b), *S = sc.take<double>(b * b);
+  double *lamb = sc.take<double>(b), *Ct = sc.take<double>(Qw * b);
+  double *T = sc.take<double>(Qw * Qw), *TV = sc.take<double>(Qw * Qw), *TW = sc.take<double>(Qw);
+  double *Vs = sc.take<double>(Qw * k);
+  int *order = sc.take<int>(k);
+  double *gw = sc.take<double>(gws / 8 + 1);
+  double *jw = sc.take<double>(jacobi_workspace(std::max(Qw, b)) / 8 + 1);
+  CUDA_TRY(cudaMemsetAsync(T, 0, (size_t)Qw * Qw * sizeof(double), s));
+
+  std::vector<cudaEvent_t> evs;
+  auto ev = [&]() {
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    evs.push_back(e);
+  };
+  auto release_events = [&]() {
+    for (auto e : evs) cudaEventDestroy(e);
+    evs.clear();
+  };
+  int64_t launches = 0, products = 0;
+  std::vector<std::pair<size_t, size_t>> prod_ev;
+  auto apply = [&](const double *V, int64_t ldv, double *Y) -> l1dm_status {
+    const size_t e0 = evs.size();
+    ev();
+    l1dm_status r = op_apply_f64(op, n, V, ldv, b, Y, b, zs, yr, s);
+    ev();
+    prod_ev.push_back({e0, e0 + 1});
+    ++products;
+    launches += 2;
+    return r;
+  };
+  auto gemm = [&](int ta, int64_t M, int64_t N, int64_t K, double alpha, const double *A,
+                  int64_t lda, const double *B, int64_t ldb, double beta, double *C, int64_t ldc) {
+    launches += launch_gemm(ta, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, gw, sms, s);
+  };
+  // Gram-based orthonormalisation (CholeskyQR) resolves column residuals down to ~sqrt(eps) of
+  // the block's largest column norm; columns whose residual is below kDropRtol of it are
+  // rounding noise (a rank-deficient block: Krylov space exhausted), dropped as zero columns
+  constexpr double kDropRtol = 1e-7;
+  ev();  // total start
+  st = apply(Pi, b, W);  // A Pi: the first Krylov block
+  int64_t cols = 0;
+  for (int64_t j = 0; j < q && st == L1DM_OK; ++j) {
+    gemm(1, b, b, n, 1.0, W, b, W, b, 0.0, G0, b);  // column norms before projection (drop floor)
+    if (cols > 0) {
+      // block Gram-Schmidt against the basis, twice: first against the last two blocks (the
+      // block Lanczos three-term recurrence: in exact arithmetic A Q_{j-1} has no component on
+      // older blocks), then against the whole basis (full re-orthogonalisation).  The
+      // coefficients add up to column block j-1 of T = Q^T A Q (rows 0..cols): W = A Q_{j-1}.
+      for (int pass = 0; pass < 2; ++pass) {
+        const int64_t c0 = pass == 0 ? std::max<int64_t>(0, cols - 2 * b) : 0, cw = cols - c0;
+        gemm(1, cw, b, n, 1.0, Qb + c0, Qw, W, b, 0.0, Ct, b);
+        gemm(0, n, b, cw, -1.0, Qb + c0, Qw, Ct, b, 1.0, W, b);
+        launch_axpy2d(cw, b, 1.0, Ct, b, T + c0 * Qw + (j - 1) * b, Qw, s);
+        ++launches;
+      }
+    }
+    // orthonormal basis of the block's column space: CholeskyQR with column dropping, twice
+    // (CholeskyQR2)
+    const double *src = W;
+    double *dst = Vt;
+    int64_t ldd = b;
+    for (int rep = 0; rep < 2; ++rep) {
+      gemm(1, b, b, n, 1.0, src, b, src, b, 0.0, G, b);
+      launch_chol_orth(b, G, b, rep == 0 ? G0 : nullptr, b, kDropRtol, 0.25, S, s);
+      gemm(0, n, b, b, 1.0, src, b, S, b, 0.0, dst, ldd);
+      launches += 1;
+      src = Vt;
+      dst = Qb + cols;
+      ldd = Qw;
+    }
+    if (cols > 0)  // R = Q_j^T W: rows cols..cols+b of T's column block j-1
+      gemm(1, b, b, n, 1.0, Qb + cols, Qw, W, b, 0.0, T + cols * Qw + (j - 1) * b, Qw);
+    cols += b;
+    st = apply(Qb + (cols - b), Qw, W);  // A Q_j: next Krylov block and T's column block j
+  }
+  if (st != L1DM_OK) {
+    cudaStreamSynchronize(s);
+    release_events();
+    return st;
+  }
+  gemm(1, Qw, b, n, 1.0, Qb, Qw, W, b, 0.0, T + (q - 1) * b, Qw);  // last column block of T
+  launch_symmetrize(Qw, T, Qw, s);
+  launches += 1 + launch_jacobi(Qw, T, Qw, TW, TV, Qw, jw, sms, s);
+  launch_select(Qw, k, TW, TV, Qw, lam, sigma, Vs, order, s);
+  ++launches;
+  if (Z) gemm(0, n, k, Qw, 1.0, Qb, Qw, Vs, k, 0.0, Z, ldz);
+  ev();  // total end
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    release_events();
+    return fail(L1DM_ECUDA, "block krylov: %s", cudaGetErrorString(e));
+  }
+  if (info) {
+    info->products = products;
+    info->columns = products * 2 * b;
+    info->block = b;
+    info->depth = q;
+    float ms = 0.0f;
+    double pm = 0.0;
+    for (auto &pe : prod_ev) {
+      cudaEventElapsedTime(&ms, evs[pe.first], evs[pe.second]);
+      pm += ms;
+    }
+    info->product_ms = pm;
+    cudaEventElapsedTime(&ms, evs.front(), evs.back());
+    info->total_ms = ms;
+  }
+  g_handleless_launches += launches;
+  release_events();
+  return L1DM_OK;
+}
+
+l1dm_status l1dm_cg(const l1dm_operator_t *op, const double *bvec, double *x, double tol,
+                    int64_t maxit, int normal_equations, void *stream, l1dm_cg_info_t *info) {
+  NvtxRange nvtx_("l1dm_cg");
+  g_err.clear();
+  int64_t n = 0;
+  l1dm_status st = op_check(op, &n);
+  if (st != L1DM_OK) return st;
+  if (!bvec || !x || maxit < 0 || !(tol >= 0.0))
+    return fail(L1DM_EINVAL, "b/x NULL, maxit < 0 or tol invalid");
+  if (!is_device_pointer(bvec) || !is_device_pointer(x))
+    return fail(L1DM_EINVAL, "l1dm_cg takes device b and x");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nb = cg_dot_blocks();
+  Scratch sc(s);
+  CUDA_TRY(sc.reserve(4 * Scratch::bytes_for(n, 8) + Scratch::bytes_for(n * 2, 4) +
+                      Scratch::bytes_for(n * 2, 8) + Scratch::bytes_for(nb, 8) +
+                      Scratch::bytes_for(16, 8)));
+  double *r = sc.take<double>(n), *p = sc.take<double>(n), *Ap = sc.take<double>(n);
+  double *tmp = sc.take<double>(n);
+  float *zs = sc.take<float>(n * 2);
+  double *yr = sc.take<double>(n * 2);
+  double *part = sc.take<double>(nb);
+  double *stv = sc.take<double>(16);
+  double *hflag = nullptr;  // pinned: [chunk parity][conv, it]
+  CUDA_TRY(cudaHostAlloc(reinterpret_cast<void **>(&hflag), 4 * sizeof(double), 0));
+  cudaEvent_t cev[2] = {nullptr, nullptr};
+  cudaEventCreateWithFlags(&cev[0], cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&cev[1], cudaEventDisableTiming);
+  auto cleanup = [&]() {
+    cudaStreamSynchronize(s);
+    cudaFreeHost(hflag);
+    cudaEventDestroy(cev[0]);
+    cudaEventDestroy(cev[1]);
+  };
+  int64_t products = 0, launches = 0;
+  auto A = [&](const double *v, double *out) -> l1dm_status {
+    ++products;
+    launches += 2;
+    return op_apply_f64(op, n, v, 1, 1, out, 1, zs, yr, s);
+  };
+  // rhs into r (normal equations: A b), x = 0, p = r
+  if (normal_equations) st = A(bvec, r);
+  else if (cudaMemcpyAsync(r, bvec, n * sizeof(double), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    st = fail(L1DM_ECUDA, "cg: copy of b failed");
+  if (st != L1DM_OK) {
+    cleanup();
+    return st;
+  }
+  cudaMemsetAsync(x, 0, n * sizeof(double), s);
+  cudaMemcpyAsync(p, r, n * sizeof(double), cudaMemcpyDeviceToDevice, s);
+  launch_dot(n, r, r, part, s);
+  launch_cg_scalars(0, part, tol, stv, s);
+  launches += 2;
+  constexpr int64_t kChunk = 8;  // iterations between host looks at the flag
+  int64_t issued = 0, chunk = 0;
+  bool stop = false;
+  while (!stop && issued < maxit) {
+    const int64_t it_here = std::min(kChunk, maxit - issued);
+    for (int64_t i = 0; i < it_here && st == L1DM_OK; ++i) {
+      if (normal_equations) {
+        st = A(p, tmp);
+        if (st == L1DM_OK) st = A(tmp, Ap);
+      } else {
+        st = A(p, Ap);
+      }
+      launch_dot(n, p, Ap, part, s);
+      launch_cg_scalars(1, part, tol, stv, s);
+      launch_cg_xr(n, stv, p, Ap, x, r, s);
+      launch_dot(n, r, r, part, s);
+      launch_cg_scalars(2, part, tol, stv, s);
+      launch_cg_p(n, stv, r, p, s);
+      launches += 6;
+    }
+    if (st != L1DM_OK) break;
+    issued += it_here;
+    const int slot = (int)(chunk & 1);
+    cudaMemcpyAsync(hflag + 2 * slot, stv + CG_CONV_INDEX, 2 * sizeof(double),
+                    cudaMemcpyDeviceToHost, s);
+    cudaEventRecord(cev[slot], s);
+    if (chunk > 0) {  // the previous chunk's flag (this chunk is already queued behind it)
+      cudaEventSynchronize(cev[slot ^ 1]);
+      if (hflag[2 * (slot ^ 1)] != 0.0) stop = true;
+    }
+    ++chunk;
+  }
+  if (st != L1DM_OK) {
+    cleanup();
+    return st;
+  }
+  // final state and the true residual ||A x - b|| / ||b||
+  double hst[2] = {0.0, 0.0};
+  cudaMemcpyAsync(hst, stv + CG_CONV_INDEX, 2 * sizeof(double), cudaMemcpyDeviceToHost, s);
+  st = A(x, tmp);
+  if (st != L1DM_OK) {
+    cleanup();
+    return st;
+  }
+  launch_sub(n, tmp, bvec, tmp, s);
+  std::vector<double> hp(2 * nb);
+  launch_dot(n, tmp, tmp, part, s);
+  cudaMemcpyAsync(hp.data(), part, nb * sizeof(double), cudaMemcpyDeviceToHost, s);
+  launch_dot(n, bvec, bvec, part, s);
+  cudaMemcpyAsync(hp.data() + nb, part, nb * sizeof(double), cudaMemcpyDeviceToHost, s);
+  launches += 3;
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  cleanup();
+  if (e != cudaSuccess) return fail(L1DM_ECUDA, "cg: %s", cudaGetErrorString(e));
+  double rr = 0.0, bb = 0.0;
+  for (int i = 0; i < nb; ++i) {
+    rr += hp[i];
+    bb += hp[nb + i];
+  }
+  if (info) {
+    info->iterations = (int64_t)hst[1];
+    info->converged = hst[0] != 0.0;
+    info->residual = std::sqrt(rr) / std::max(std::sqrt(bb), 1e-300);
+    info->products = products;
+  }
+  g_handleless_launches += launches;
+  return L1DM_OK;
+}
+
+}  // extern "C"

@@ -262,4 +262,35 @@ int launch_bilinear(const float *X, int64_t ldx, const double *M, const float *Z
 int launch_embed(const float *X, int64_t ldx, int64_t n, int64_t d, const float *G, int64_t ldg,
                   int64_t k, float *Xp, int64_t ldp, cudaStream_t s);
 
+// ---------------- dense fp64 steps of the matrix-free consumers (l1dm_dense.cu, NEXT-2) ----
+size_t gemm_workspace(int ta, int64_t M, int64_t N, int64_t K, int sms);
+int launch_gemm(int ta, int64_t M, int64_t N, int64_t K, double alpha, const double *A,
+                int64_t lda, const double *B, int64_t ldb, double beta, double *C, int64_t ldc,
+                double *ws, int sms, cudaStream_t s);
+size_t jacobi_workspace(int64_t N);
+int launch_jacobi(int64_t N, double *A, int64_t lda, double *W, double *V, int64_t ldv,
+                  double *ws, int sms, cudaStream_t s, int *stats = nullptr);
+void launch_chol_orth(int64_t b, const double *G, int64_t ldg, const double *G0, int64_t ldg0,
+                      double rtol, double floor_abs, double *S, cudaStream_t s);
+void launch_select(int64_t N, int64_t k, const double *W, const double *V, int64_t ldv,
+                   double *lam, double *sigma, double *Vs, int *order, cudaStream_t s);
+void launch_scale_cols(int64_t b, const double *V, const double *lam, const double *G0,
+                       int64_t ldg0, double rtol, double floor_abs, double *S, cudaStream_t s);
+void launch_split_hilo(int64_t n, int64_t b, const double *V, int64_t ldv, float *Zs,
+                       cudaStream_t s);
+void launch_combine_hilo(int64_t n, int64_t b, const double *Yr, double *Y, int64_t ldy,
+                         cudaStream_t s);
+void launch_axpy2d(int64_t rows, int64_t cols, double alpha, const double *S, int64_t lds,
+                   double *D, int64_t ldd, cudaStream_t s);
+void launch_symmetrize(int64_t N, double *T, int64_t ldt, cudaStream_t s);
+int cg_dot_blocks();
+// CG device state: doubles [CG_CONV_INDEX] = converged flag, [CG_CONV_INDEX + 1] = iterations
+constexpr int CG_CONV_INDEX = 6;
+void launch_dot(int64_t n, const double *x, const double *y, double *part, cudaStream_t s);
+void launch_cg_scalars(int phase, const double *part, double tol, double *st, cudaStream_t s);
+void launch_cg_xr(int64_t n, const double *st, const double *p, const double *Ap, double *x,
+                  double *r, cudaStream_t s);
+void launch_cg_p(int64_t n, const double *st, const double *r, double *p, cudaStream_t s);
+void launch_sub(int64_t n, const double *a, const double *b, double *d, cudaStream_t s);
+
 }  // namespace l1dm

@@ -1,61 +1,167 @@
-"""Matrix-free consumers on the GPU: the block product is this
-package's C-ABI library; the reference spectrum is numpy.linalg.eigh of the oracle's dense A
-(oracle.brute / brute_lp with Z = I)."""
+"""Matrix-free consumers on the GPU, every step in the library:
+  * the fp64 tensor-core GEMM (l1dm_gemm) against numpy's matmul, with a rounding bound,
+  * the Jacobi eigensolver (l1dm_syevj) against numpy.linalg.eigh (a library routine),
+  * block Krylov (l1dm_block_krylov) against numpy.linalg.eigh of the oracle's dense A
+    (oracle.brute / brute_lp / lp_even / brute_bilinear with Z = I, pinned in test_oracle_*),
+  * conjugate gradients (l1dm_cg) by its residual and against numpy.linalg.solve."""
 import numpy as np
 import pytest
 import torch
 
 import oracle
 import paper_2210_15114_b200 as l1
-from paper_2210_15114_b200.krylov import block_krylov, cg_solve, fp64_product
+from paper_2210_15114_b200 import binding
+from paper_2210_15114_b200.binding import Operator
+from paper_2210_15114_b200.krylov import block_krylov, cg_solve, fp64_product, lowrank_error
 
 pytestmark = pytest.mark.gpu
 
 
-def l1_engine(X, p=1):
-    h = l1.l1dm_prepare(torch.from_numpy(X).cuda())
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+# ------------------------------------------------------------------------------------ GEMM
+@pytest.mark.parametrize("ta", [False, True])
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (7, 3, 5), (64, 64, 16), (130, 33, 1000),
+                                   (33, 130, 257), (640, 32, 70001), (20000, 32, 640),
+                                   (5, 96, 100000), (3, 2, 0)])
+def test_gemm_against_numpy(ta, M, N, K):
+    rng = np.random.default_rng(M * 7 + N * 3 + K + ta)
+    A = rng.standard_normal((K, M) if ta else (M, K))
+    B = rng.standard_normal((K, N))
+    C0 = rng.standard_normal((M, N))
+    opA = A.T if ta else A
+    want = 0.5 * (opA @ B) - 2.0 * C0
+    got = binding.l1dm_gemm(dev(A), dev(B), dev(C0), trans_a=ta, alpha=0.5, beta=-2.0)
+    # fp64 rounding bound: |err| <= K eps sum_k |a_mk b_kn| (+ the beta term's rounding)
+    bound = 4 * max(K, 1) * 2.2e-16 * (0.5 * (np.abs(opA) @ np.abs(B)) + 2.0 * np.abs(C0)) + 1e-300
+    assert np.all(np.abs(got.cpu().numpy() - want) <= bound)
+
+
+def test_gemm_strided_views_and_beta_zero_ignores_nan():
+    rng = np.random.default_rng(3)
+    big = dev(rng.standard_normal((300, 50)))
+    A = big[:, 5:25]                      # lda = 50
+    B = dev(rng.standard_normal((20, 9)))
+    Cw = torch.full((300, 16), float("nan"), dtype=torch.float64, device="cuda")
+    C = Cw[:, 2:11]                       # ldc = 16, beta = 0 never reads the NaNs
+    binding.l1dm_gemm(A, B, C)
+    want = A.cpu().numpy() @ B.cpu().numpy()
+    assert np.allclose(C.cpu().numpy(), want, rtol=1e-13, atol=1e-13)
+    assert torch.isnan(Cw[:, :2]).all() and torch.isnan(Cw[:, 11:]).all()
+
+
+# ----------------------------------------------------------------------------------- Jacobi
+def check_eig(A, W, V, tol=1e-12):
+    A = np.asarray(A)
+    N = A.shape[0]
+    W, V = W.cpu().numpy(), V.cpu().numpy()
+    scale = max(np.linalg.norm(A), 1e-300)
+    ref = np.linalg.eigvalsh(A)
+    assert np.allclose(np.sort(W), ref, rtol=0, atol=tol * scale)
+    assert np.abs(V.T @ V - np.eye(N)).max() <= tol * max(N, 10)
+    assert np.linalg.norm(A @ V - V * W[None, :]) <= tol * scale * max(N, 10)
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 17, 64, 96, 97, 200, 333])
+def test_syevj_random_symmetric(N):
+    rng = np.random.default_rng(N)
+    B = rng.standard_normal((N, N))
+    A = B + B.T
+    W, V = binding.l1dm_syevj(dev(A))
+    check_eig(A, W, V)
+
+
+@pytest.mark.parametrize("N", [5, 40, 150])
+def test_syevj_degenerate_spectra(N):
+    rng = np.random.default_rng(N + 1)
+    u = rng.standard_normal((N, 1))
+    for A in (np.eye(N) + u @ u.T,                      # N-1 equal eigenvalues
+              np.zeros((N, N)),                         # all zero
+              np.diag(np.arange(N, dtype=np.float64)),  # already diagonal
+              np.ones((N, N))):                         # rank one, zero diagonal gap
+        W, V = binding.l1dm_syevj(dev(A))
+        check_eig(A, W, V)
+
+
+def test_syevj_l1_distance_matrix_zero_diagonal():
+    """An l1 distance matrix (zero diagonal, one positive and n-1 negative eigenvalues)."""
+    X = np.random.default_rng(2).standard_normal((120, 4)).astype(np.float32)
+    A = oracle.brute(X, np.eye(120, dtype=np.float32))
+    W, V = binding.l1dm_syevj(dev(A))
+    check_eig(A, W, V)
+
+
+# ----------------------------------------------------------------------------------- Krylov
+def dense(X, p):
+    n = X.shape[0]
+    I = np.eye(n, dtype=np.float32)
     if p == 1:
-        return h, (lambda V: l1.l1dm_matvec(h, V.cuda()))
-    return h, (lambda V: l1.l1dm_matvec_lp(h, p, V.cuda()))
+        return oracle.brute(X, I)
+    if p % 2:
+        return oracle.brute_lp(X, I, p)
+    return oracle.lp_even(X, I, p)
 
 
 @pytest.mark.parametrize("p", [1, 3])
 def test_topk_singular_values_vs_dense_spectrum(p):
     rng = np.random.default_rng(10 + p)
     X = rng.standard_normal((1500, 6)).astype(np.float32)
-    A = oracle.brute_lp(X, np.eye(1500, dtype=np.float32), p)
+    A = dense(X, p)
     sv = np.sort(np.abs(np.linalg.eigvalsh(A)))[::-1]
-    h, mv = l1_engine(X, p)
-    r = block_krylov(mv, 1500, 8, eps=0.5, seed=1, device="cuda")
-    l1.l1dm_free(h)
+    h = l1.l1dm_prepare(dev(X))
+    op = Operator.sorted(h, p)
+    r = block_krylov(op, 8, eps=0.5, seed=1)
+    assert r.products == r.info["depth"] + 1
     assert np.allclose(r.sigma.cpu().numpy(), sv[:8], rtol=1e-8)
     Z = r.Z.cpu().numpy()
     assert np.abs(Z.T @ Z - np.eye(8)).max() <= 1e-10
     k = 8
     best = np.sqrt(np.sort(np.linalg.eigvalsh(A) ** 2)[:-k].sum())
     assert np.linalg.norm(A - (A @ Z) @ Z.T) <= 1.05 * best         # (1 + eps) bound, eps = 0.05
+    est = np.sqrt(lowrank_error(op, r.Z, probes=64))
+    err = np.linalg.norm(A - (A @ Z) @ Z.T)
+    assert 0.5 * err <= est <= 2 * err                               # Hutchinson estimate
+    l1.l1dm_free(h)
 
 
-def test_cg_on_gram_engine():
-    """PSD engine: the bilinear form with M = I + ridge-free Gram is PSD; solve A x = b."""
-    rng = np.random.default_rng(3)
-    X = rng.standard_normal((800, 900)).astype(np.float32)      # n < d: X X^T full rank
-    M = torch.eye(900, dtype=torch.float64, device="cuda")
-    Xd = torch.from_numpy(X).cuda()
-    mv = lambda V: l1.l1dm_bilinear_matvec(Xd, M, V.cuda())
-    b = torch.from_numpy(rng.standard_normal(800)).cuda()
-    res = cg_solve(mv, b, tol=1e-10, maxit=2000)
-    assert res.converged and res.residual <= 1e-8
+def test_topk_sort_free_and_bilinear_operators():
+    rng = np.random.default_rng(21)
+    X = rng.standard_normal((900, 5)).astype(np.float32)
+    A2 = dense(X, 2)
+    r = block_krylov(Operator.even(dev(X), 2), 4, seed=2)
+    assert np.allclose(r.sigma.cpu().numpy(), np.sort(np.abs(np.linalg.eigvalsh(A2)))[::-1][:4],
+                       rtol=1e-9)
+    M = rng.standard_normal((5, 5))
+    M = M + M.T
+    AB = oracle.brute_bilinear(X, M, np.eye(900, dtype=np.float32))
+    r = block_krylov(Operator.bilinear(dev(X), dev(M)), 3, seed=3)
+    assert np.allclose(r.sigma.cpu().numpy(), np.sort(np.abs(np.linalg.eigvalsh(AB)))[::-1][:3],
+                       rtol=1e-9)
+
+
+def test_exact_rank_one_operator():
+    """Points on a line, Gram form (M = I, d = 1): A = x x^T has rank 1 — the Krylov space is
+    exhausted after one direction; the dropped directions must not disturb sigma_1."""
+    n = 120
+    x = np.arange(n, dtype=np.float32)[:, None]
+    r = block_krylov(Operator.bilinear(dev(x), torch.eye(1, dtype=torch.float64)), 1, seed=5)
+    want = float((x.astype(np.float64) ** 2).sum())
+    assert abs(r.sigma[0].item() - want) <= 1e-10 * want
+    z = r.Z.cpu().numpy()[:, 0]
+    xd = x[:, 0].astype(np.float64)
+    assert abs(abs(z @ xd) / np.linalg.norm(xd) - 1.0) <= 1e-10
 
 
 def test_fp64_product_split_accuracy():
     rng = np.random.default_rng(4)
     X = rng.standard_normal((2000, 4)).astype(np.float32)
-    h, mv = l1_engine(X)
-    V = torch.from_numpy(rng.standard_normal((2000, 3))).cuda()
+    h = l1.l1dm_prepare(dev(X))
+    V = dev(rng.standard_normal((2000, 3)))
     A = oracle.brute(X, np.eye(2000, dtype=np.float32))
     want = A @ V.cpu().numpy()
-    got = fp64_product(mv, V).cpu().numpy()
+    got = fp64_product(Operator.sorted(h), V).cpu().numpy()
     assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
     l1.l1dm_free(h)
 
@@ -67,13 +173,50 @@ def test_c3_scale_ritz_residuals():
     w = wl.workload("c3")
     X = wl.make_points(w, "cuda")
     h = l1.l1dm_prepare(X)
-    mv = lambda V: l1.l1dm_matvec(h, V.cuda())
-    r = block_krylov(mv, w.n, 4, block=12, depth=6, seed=2, device="cuda")
-    AZ = fp64_product(mv, r.Z)
+    op = Operator.sorted(h)
+    r = block_krylov(op, 4, block=12, depth=6, seed=2)
+    AZ = fp64_product(op, r.Z)
     res = torch.linalg.norm(AZ - r.Z * r.lam[None, :], dim=0) / r.sigma
     l1.l1dm_free(h)
     assert float(res[0]) <= 1e-8          # the dominant pair converges fast (gap sigma1/sigma2)
     # the next pairs sit in a clustered part of the spectrum (U[-1,1)^128 points): at depth 6
-    # they are approximate (measured ~2e-2), still far better than the random start (~1)
+    # they are approximate (measured ~2e-2 in round 1), far better than the random start (~1)
     assert bool(torch.all(res <= 0.1))
     assert bool(torch.all(r.sigma[:-1] >= r.sigma[1:]))
+    assert r.info["product_ms"] > 0 and r.info["total_ms"] >= r.info["product_ms"]
+
+
+# --------------------------------------------------------------------------------------- CG
+def test_cg_on_gram_engine():
+    """PSD engine: the bilinear form with M = I and n < d (X X^T full rank); solve A x = b."""
+    rng = np.random.default_rng(3)
+    X = rng.standard_normal((800, 900)).astype(np.float32)
+    op = Operator.bilinear(dev(X), torch.eye(900, dtype=torch.float64, device="cuda"))
+    b = dev(rng.standard_normal(800))
+    res = cg_solve(op, b, tol=1e-10, maxit=2000)
+    assert res.converged and res.residual <= 1e-8
+    G = X.astype(np.float64) @ X.astype(np.float64).T
+    want = np.linalg.solve(G, b.cpu().numpy())
+    assert np.linalg.norm(res.x.cpu().numpy() - want) <= 1e-6 * np.linalg.norm(want)
+
+
+def test_cg_normal_equations_on_l1_matrix():
+    rng = np.random.default_rng(7)
+    X = rng.standard_normal((150, 4)).astype(np.float32)
+    h = l1.l1dm_prepare(dev(X))
+    b = dev(rng.standard_normal(150))
+    res = cg_solve(Operator.sorted(h), b, tol=1e-9, maxit=5000, normal_equations=True)
+    assert res.residual <= 1e-6
+    assert res.products >= 2 * res.iterations
+    l1.l1dm_free(h)
+
+
+def test_cg_non_convergence_reported():
+    rng = np.random.default_rng(6)
+    X = rng.standard_normal((200, 240)).astype(np.float32)
+    op = Operator.bilinear(dev(X), torch.eye(240, dtype=torch.float64, device="cuda"))
+    b = dev(rng.standard_normal(200))
+    bad = cg_solve(op, b, tol=1e-14, maxit=2)
+    assert not bad.converged and bad.iterations == 2
+    zero = cg_solve(op, torch.zeros(200, dtype=torch.float64, device="cuda"), maxit=10)
+    assert zero.converged and zero.iterations == 0 and float(zero.x.abs().max()) == 0.0
