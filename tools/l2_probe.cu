@@ -131,6 +131,28 @@ __global__ void __launch_bounds__(256) stream_read(const float4 *z, int64_t n4, 
     }
   if (acc == 1.2345f) out[0] = acc;
 }
+// the ceiling sweep: W lanes per W*8-byte row, U reductions in flight per thread, hashed rows of
+// a ytab-row buffer; `local` > 0 confines each warp's reductions to one of `local` sub-tables of
+// 256 rows (the locality of the runs histogram's per-coordinate tables)
+template <int W, int U>
+__global__ void __launch_bounds__(256) red_sweep(int64_t rows, double *y, uint32_t ytab,
+                                                 uint32_t local) {
+  constexpr int G = 32 / W;
+  const int lane = threadIdx.x & 31, c = lane % W, g = lane / W;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = warp * G * U; base < rows; base += nw * G * U) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      uint32_t x = (uint32_t)(base + u * G + g) * 0x9E3779B1u;
+      x ^= x >> 15;
+      x *= 0x85EBCA77u;
+      x ^= x >> 13;
+      const uint32_t row = local ? (uint32_t)((warp + u) % local) * 256u + (x & 255u) : x % ytab;
+      atomicAdd(y + (int64_t)row * W + c, 1.0);
+    }
+  }
+}
 template <typename F>
 static float best_ms(F f) {
   cudaEvent_t a, b;
@@ -188,8 +210,44 @@ int main() {
   const float t_str = best_ms([&] {
     stream_read<<<grid, 256>>>(reinterpret_cast<const float4 *>(z), (32ll << 20) / 16, reps, out);
   });
+  // ceiling sweep over row width (32-256 B), buffer size (1-64 MiB), locality and grid size:
+  // the largest fp64 reduction rate any pattern reaches is the L2 reduction ceiling
+  double best_rate = 0.0;
+  char best_cfg[160] = "";
+  printf("{\"sweep\": [");
+  bool first = true;
+  auto rec = [&](const char *name, int w, double mib, int loc, int gmul, float ms) {
+    const double rate = rows * (double)w / (ms * 1e-3);
+    printf("%s{\"kernel\": \"%s\", \"row_bytes\": %d, \"MiB\": %.3g, \"local_tables\": %d, "
+           "\"ctas_per_sm\": %d, \"adds_per_s\": %.4g}",
+           first ? "" : ", ", name, w * 8, mib, loc, gmul, rate);
+    first = false;
+    if (rate > best_rate) {
+      best_rate = rate;
+      snprintf(best_cfg, sizeof(best_cfg), "%s, %d-B rows, %.3g MiB, local %d, %d CTAs/SM", name,
+               w * 8, mib, loc, gmul);
+    }
+  };
+  for (int gmul : {4, 8, 16}) {
+    const int gg = sms * gmul;
+    for (double mib : {1.0, 3.0, 8.0, 32.0, 64.0}) {
+      const uint32_t b = (uint32_t)(mib * (1 << 20));
+      rec("hashed", 4, mib, 0, gmul, best_ms([&] { red_sweep<4, 16><<<gg, 256>>>(rows, y, b / 32, 0); }));
+      rec("hashed", 8, mib, 0, gmul, best_ms([&] { red_sweep<8, 16><<<gg, 256>>>(rows, y, b / 64, 0); }));
+      rec("hashed", 16, mib, 0, gmul, best_ms([&] { red_sweep<16, 16><<<gg, 256>>>(rows, y, b / 128, 0); }));
+      rec("hashed", 32, mib, 0, gmul, best_ms([&] { red_sweep<32, 8><<<gg, 256>>>(rows, y, b / 256, 0); }));
+    }
+    for (int loc : {16, 96, 256}) {
+      rec("local_tables", 8, loc * 256 * 64 / 1048576.0, loc, gmul,
+          best_ms([&] { red_sweep<8, 16><<<gg, 256>>>(rows, y, 0, (uint32_t)loc); }));
+      rec("local_tables", 16, loc * 256 * 128 / 1048576.0, loc, gmul,
+          best_ms([&] { red_sweep<16, 16><<<gg, 256>>>(rows, y, 0, (uint32_t)loc); }));
+    }
+  }
+  printf("], \"red_ceiling_adds_per_s\": %.4g, \"red_ceiling_config\": \"%s\", ", best_rate,
+         best_cfg);
   const cudaError_t e = cudaGetLastError();
-  printf("{\"gather_lane_per_s\": %.4g, \"red_lane_per_s\": %.4g, ", rows / (t_gl * 1e-3),
+  printf("\"gather_lane_per_s\": %.4g, \"red_lane_per_s\": %.4g, ", rows / (t_gl * 1e-3),
          rows / (t_rl * 1e-3));
   printf("\"red_row8_deep_adds_per_s\": %.4g, \"red_row16_deep_adds_per_s\": %.4g, "
          "\"red_row16_4MiB_adds_per_s\": %.4g, \"red_row8_hashed_adds_per_s\": %.4g, "
