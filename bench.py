@@ -579,8 +579,8 @@ def main_ours(args):
             # so the ceiling is the harmonic combination of the two rates
             sc = kern["scan"]
             pairs = agg.get("scan_pairs", 0)
-            g = l2p.get("gather_lane_per_s", 2.69e11)
-            r = l2p.get("red_lane_per_s", 1.745e11)
+            g = max(l2p.get("gather_lane_per_s", 2.69e11), l2p.get("gather_lane_4MiB_per_s", 0))
+            r = max(l2p.get("red_lane_per_s", 1.745e11), l2p.get("red_lane_8MiB_per_s", 0))
             peak = 1.0 / (1.0 / g + 1.0 / r) / 1e9
             ach = pairs / (sc["ms_total"] * 1e-3) / 1e9 if sc["ms_total"] else None
             roof = {"bound": "l2_random_access", "kernel": "scan (k5_scan_m1 reduce/prefix/apply)",

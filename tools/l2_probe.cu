@@ -206,6 +206,9 @@ int main() {
   const float t_gat = best_ms([&] { gather_sectors<<<grid, 256>>>(idx, rows, z, zrows, out); });
   const float t_gl = best_ms([&] { gather_lanes<<<grid, 256>>>(idx, rows, z, zrows * 8, out); });
   const float t_rl = best_ms([&] { red_lanes<<<grid, 256>>>(idx, rows, y, yrows * 8); });
+  // c2's exact buffer sizes (m = 1 scatter: z is 4 MiB, Y is 8 MiB)
+  const float t_gl4 = best_ms([&] { gather_lanes<<<grid, 256>>>(idx, rows, z, 1u << 20, out); });
+  const float t_rl8 = best_ms([&] { red_lanes<<<grid, 256>>>(idx, rows, y, 1u << 20); });
   const int reps = 64;
   const float t_str = best_ms([&] {
     stream_read<<<grid, 256>>>(reinterpret_cast<const float4 *>(z), (32ll << 20) / 16, reps, out);
@@ -249,6 +252,8 @@ int main() {
   const cudaError_t e = cudaGetLastError();
   printf("\"gather_lane_per_s\": %.4g, \"red_lane_per_s\": %.4g, ", rows / (t_gl * 1e-3),
          rows / (t_rl * 1e-3));
+  printf("\"gather_lane_4MiB_per_s\": %.4g, \"red_lane_8MiB_per_s\": %.4g, ",
+         rows / (t_gl4 * 1e-3), rows / (t_rl8 * 1e-3));
   printf("\"red_row8_deep_adds_per_s\": %.4g, \"red_row16_deep_adds_per_s\": %.4g, "
          "\"red_row16_4MiB_adds_per_s\": %.4g, \"red_row8_hashed_adds_per_s\": %.4g, "
          "\"red_row16_4MiB_hashed_adds_per_s\": %.4g, \"red_runs_tables_adds_per_s\": %.4g, ",
