@@ -15,8 +15,6 @@
 //                  epoch-tagged flags, tiles claimed by atomic ticket), then U.
 //   K6 accumulate  per point: gather U rows at rank[k][i] for every k of the chunk
 //                  and accumulate in registers (no atomics); epilogue writes Y.
-#include <cuda.h>
-#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -937,205 +935,10 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// TMA variant of k5_reduce_all (m <= 64, m % 8 == 0; SURVEY K5's "tile::gather4" proposal):
-// the Z rows of each 64-row chunk of sorted order arrive by cp.async.bulk.tensor ... gather4
-// (4 rows of m floats per instruction, row indices = perm) into a 4-stage shared-memory ring
-// with mbarrier completion; one thread issues, the 8 warps sum 8 rows each per chunk.  A CTA
-// covers two 1024-row tiles of one coordinate, like k5_reduce_all.
-constexpr int kRaChunk = 64, kRaStages = 4;
-
-__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
-  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
-               "r"(count)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(
-                   (unsigned)__cvta_generic_to_shared(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
-  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
-  unsigned done = 0;
-  while (!done) {
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(done)
-        : "r"(a), "r"(parity)
-        : "memory");
-  }
-}
-__device__ __forceinline__ void tma_gather4(void *dst, const CUtensorMap *tm, uint64_t *bar, int col,
-                                            int r0, int r1, int r2, int r3) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"((unsigned)__cvta_generic_to_shared(bar)), "r"(col),
-      "r"(r0), "r"(r1), "r"(r2), "r"(r3)
-      : "memory");
-}
-
-template <int NCL>
-__global__ void __launch_bounds__(256)
-    k5_reduce_all_tma(const __grid_constant__ CUtensorMap tm, const uint32_t *__restrict__ perm,
-                      const float *__restrict__ sval, int64_t ldn, int64_t n, int64_t m,
-                      int64_t nseg, int64_t tiles_per_seg, double *__restrict__ agg) {
-  constexpr int R = 1024, NW = 8, TPC = 2, ROWS = TPC * R, NCH = ROWS / kRaChunk;
-  constexpr int RPW = kRaChunk / NW;  // rows per warp per chunk
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  // the bulk-tensor destination must be 128-byte aligned (the dynamic base is not, after the
-  // static mbarriers): round up inside the 128 bytes of slack the launch adds
-  float *ring = reinterpret_cast<float *>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~(uintptr_t)127);  // [stages][chunk][m]
-  uint32_t *sp = reinterpret_cast<uint32_t *>(ring + (size_t)kRaStages * kRaChunk * m);  // [ROWS]
-  float *sv = reinterpret_cast<float *>(sp + ROWS);                  // [ROWS]
-  double *s_part = reinterpret_cast<double *>(sv + ROWS);            // [TPC][NW][2m]
-  __shared__ __align__(8) uint64_t bar[kRaStages];
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int64_t t = blockIdx.x;
-  const int64_t pair = t / nseg;
-  const int64_t kk = t - pair * nseg;
-  const int64_t row0 = pair * ROWS;
-  const int64_t nvalid = (n - row0 < ROWS) ? (n - row0) : ROWS;
-  const uint32_t *pp = perm + kk * ldn + row0;
-  const float *vp = sval + kk * ldn + row0;
-  for (int q = tid; q < ROWS / 4; q += 256) {  // the CTA's perm and sval (rows padded to ldn)
-    const bool ok = row0 + 4 * q < ldn;
-    cp_async<16>(sp + 4 * q, ok ? (const void *)(pp + 4 * q) : (const void *)perm, ok);
-    cp_async<16>(sv + 4 * q, ok ? (const void *)(vp + 4 * q) : (const void *)sval, ok);
-  }
-  cp_async_commit();
-  if (tid == 0) {
-    for (int b = 0; b < kRaStages; ++b) mbar_init(&bar[b], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  cp_async_wait_all();
-  __syncthreads();
-  const unsigned chunk_bytes = (unsigned)(kRaChunk * m * 4);
-  auto issue = [&](int c) {  // thread 0: chunk c into stage c % kRaStages
-    if (c >= NCH) return;
-    const int st = c % kRaStages;
-    float *dst = ring + (size_t)st * kRaChunk * m;
-    mbar_expect_tx(&bar[st], chunk_bytes);
-    for (int q = 0; q < kRaChunk / 4; ++q) {
-      int rr[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int r = c * kRaChunk + 4 * q + u;
-        rr[u] = r < nvalid ? (int)sp[r] : 0;  // rows past n: any valid row, not summed
-      }
-      tma_gather4(dst + (size_t)4 * q * m, &tm, &bar[st], 0, rr[0], rr[1], rr[2], rr[3]);
-    }
-  };
-  if (tid == 0)
-    for (int c = 0; c < kRaStages; ++c) issue(c);
-  double cs[NCL], ct[NCL];
-#pragma unroll
-  for (int j = 0; j < NCL; ++j) cs[j] = ct[j] = 0.0;
-  for (int c = 0; c < NCH; ++c) {
-    const int st = c % kRaStages;
-    mbar_wait(&bar[st], (unsigned)((c / kRaStages) & 1));
-    const float *zb = ring + (size_t)st * kRaChunk * m;
-#pragma unroll
-    for (int u = 0; u < RPW; ++u) {
-      const int rl = w * RPW + u, r = c * kRaChunk + rl;
-      if (r < nvalid) {
-        const double v = (double)sv[r];
-#pragma unroll
-        for (int j = 0; j < NCL; ++j) {
-          const int col = lane + 32 * j;
-          const double z = col < m ? (double)zb[(size_t)rl * m + col] : 0.0;
-          cs[j] += z;
-          ct[j] = fma(v, z, ct[j]);
-        }
-      }
-    }
-    if ((c + 1) % (NCH / TPC) == 0) {  // end of a 1024-row tile: park this warp's partial
-      const int tile = c / (NCH / TPC);
-#pragma unroll
-      for (int j = 0; j < NCL; ++j) {
-        const int col = lane + 32 * j;
-        if (col < m) {
-          s_part[((size_t)tile * NW + w) * 2 * m + 2 * col] = cs[j];
-          s_part[((size_t)tile * NW + w) * 2 * m + 2 * col + 1] = ct[j];
-        }
-        cs[j] = ct[j] = 0.0;
-      }
-    }
-    __syncthreads();  // stage st is free
-    if (tid == 0) issue(c + kRaStages);
-  }
-  __syncthreads();
-  for (int half = 0; half < TPC; ++half) {
-    const int64_t tile = TPC * pair + half;
-    if (tile >= tiles_per_seg) break;
-    double *ag = agg + (kk * tiles_per_seg + tile) * 2 * m;
-    for (int64_t e = tid; e < 2 * m; e += 256) {
-      double a = 0.0;
-#pragma unroll
-      for (int ww = 0; ww < NW; ++ww) a += s_part[((size_t)half * NW + ww) * 2 * m + e];
-      ag[e] = a;
-    }
-  }
-}
-
-static bool ra_tma_enabled() {
-  static const bool on = [] {
-    const char *e = getenv("L1DM_RA_TMA");
-    return e && atoi(e) != 0;
-  }();
-  return on;
-}
-
-static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
-    void *f = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      f = nullptr;
-    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
-  }();
-  return fn;
-}
-
 bool launch_reduce_all(const uint32_t *perm, const float *sval, int64_t ldn, int64_t n,
                        const float *Z, int64_t ldz, int64_t m, int64_t kcc, int64_t tiles_per_seg,
                        double *agg, double *segtot, cudaStream_t s) {
   if (m > 256) return false;
-  if (ra_tma_enabled() && m <= 64 && m % 8 == 0 && (ldz * 4) % 16 == 0 &&
-      ((uintptr_t)Z & 15) == 0 && tensor_map_encoder() && n < (1ll << 31)) {
-    CUtensorMap tm;
-    cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)n};
-    cuuint64_t strides[1] = {(cuuint64_t)ldz * 4};
-    cuuint32_t box[2] = {(cuuint32_t)m, 1};
-    cuuint32_t es[2] = {1, 1};
-    if (tensor_map_encoder()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)Z, dims, strides, box,
-                             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
-      const int64_t total = kcc * ((tiles_per_seg + 1) / 2);
-      const size_t smem = 128 + (size_t)kRaStages * kRaChunk * m * 4 + 2 * 2048 * 4 +
-                          (size_t)2 * 8 * 2 * m * sizeof(double);
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(k5_reduce_all_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(k5_reduce_all_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-      }
-      if (m <= 32)
-        k5_reduce_all_tma<1><<<(unsigned)total, 256, smem, s>>>(tm, perm, sval, ldn, n, m, kcc,
-                                                                tiles_per_seg, agg);
-      else
-        k5_reduce_all_tma<2><<<(unsigned)total, 256, smem, s>>>(tm, perm, sval, ldn, n, m, kcc,
-                                                                tiles_per_seg, agg);
-      const int64_t warps = kcc * 2 * m;
-      k5_seq_prefix<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(agg, kcc, tiles_per_seg,
-                                                                (int)(2 * m), 2 * m, segtot, 2 * m);
-      return true;
-    }
-  }
   const int64_t total = kcc * ((tiles_per_seg + L1DM_RA_TILES - 1) / L1DM_RA_TILES);
   const size_t smem = (size_t)8 * 2 * m * sizeof(double);
 #define L1DM_RA(NCL)                                                                            \
