@@ -313,6 +313,14 @@ L1DM_API l1dm_status l1dm_gemm(int trans_a, int64_t M, int64_t N, int64_t K, dou
 L1DM_API l1dm_status l1dm_syevj(int64_t N, const double *A, int64_t lda, double *W, double *V,
                                 int64_t ldv, void *stream);
 
+/* The k eigenpairs of largest |lambda| of a symmetric A (N x N, lda; only read): Householder
+ * tridiagonalisation on a cooperative grid, Sturm bisection, inverse iteration with
+ * re-orthogonalisation inside eigenvalue clusters, back-transformation.  lam[k] in
+ * nonincreasing |lambda| order (ties: smaller eigenvalue index first), V (N x k, ldv) the unit
+ * eigenvectors.  N <= 4096, k <= min(N, 96).  Errors: EINVAL, EDEVICE, ENOMEM, ECUDA. */
+L1DM_API l1dm_status l1dm_syev_topk(int64_t N, const double *A, int64_t lda, int64_t k,
+                                    double *lam, double *V, int64_t ldv, void *stream);
+
 /* Y (n x b, ldy) = A V for an fp64 block V (n x b, ldv) through the operator's fp32 product
  * (hi/lo split, one product of 2b columns).  Errors: EINVAL (operator, sizes), as the
  * operator's product. */
@@ -327,10 +335,10 @@ L1DM_API l1dm_status l1dm_op_apply(const l1dm_operator_t *op, const double *V, i
  * residual is below 1e-7 of the block's largest column norm are dropped as zero columns: the
  * Krylov space is exhausted), the Rayleigh quotient T = Q^T A Q
  * assembled from the orthogonalisation coefficients (block Lanczos with full
- * re-orthogonalisation), T = V diag(lam) V^T by Jacobi, sigma = |lam| in nonincreasing order,
- * Z = Q V_k.  q + 1 block products of width 2b.
+ * re-orthogonalisation), its k eigenpairs of largest |lambda| (as l1dm_syev_topk), sigma = |lam|
+ * in nonincreasing order, Z = Q V_k.  q + 1 block products of width 2b.
  * Pi: the n x b start block (the method's random draw; the caller passes it, e.g. i.i.d.
- * N(0,1) from a seeded generator).  1 <= k <= b <= 96, q >= 1, q b <= n.
+ * N(0,1) from a seeded generator).  1 <= k <= b <= 96, q >= 1, q b <= min(n, 4096).
  * Outputs: sigma[k], lam[k] (signed Ritz values), Z (n x k, ldz, orthonormal columns); any
  * output may be NULL except sigma.  Synchronous (returns when the outputs are ready).
  * Errors: EINVAL, as l1dm_op_apply, ENOMEM, ECUDA. */

@@ -37,7 +37,7 @@ EXPORTS = [
     "l1dm_ipc_alloc", "l1dm_ipc_free", "l1dm_ipc_open", "l1dm_ipc_close", "l1dm_matvec_push",
     "l1dm_peer_reduce", "l1dm_peer_wait", "l1dm_peer_check",
     "l1dm_last_error", "l1dm_handleless_launches", "l1dm_version",
-    "l1dm_gemm", "l1dm_syevj", "l1dm_op_apply", "l1dm_block_krylov", "l1dm_cg",
+    "l1dm_gemm", "l1dm_syevj", "l1dm_syev_topk", "l1dm_op_apply", "l1dm_block_krylov", "l1dm_cg",
 ]
 
 
@@ -159,12 +159,14 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     dbl = ctypes.c_double
     lib.l1dm_gemm.argtypes = [i32, i64, i64, i64, dbl, vp, i64, vp, i64, dbl, vp, i64, vp]
     lib.l1dm_syevj.argtypes = [i64, vp, i64, vp, vp, i64, vp]
+    lib.l1dm_syev_topk.argtypes = [i64, vp, i64, i64, vp, vp, i64, vp]
     lib.l1dm_op_apply.argtypes = [ctypes.POINTER(OperatorT), vp, i64, i64, vp, i64, vp]
     lib.l1dm_block_krylov.argtypes = [ctypes.POINTER(OperatorT), i64, i64, i64, vp, vp, vp, vp,
                                       i64, vp, ctypes.POINTER(KrylovInfoT)]
     lib.l1dm_cg.argtypes = [ctypes.POINTER(OperatorT), vp, vp, dbl, i64, i32, vp,
                             ctypes.POINTER(CGInfoT)]
-    for name in ("l1dm_gemm", "l1dm_syevj", "l1dm_op_apply", "l1dm_block_krylov", "l1dm_cg"):
+    for name in ("l1dm_gemm", "l1dm_syevj", "l1dm_syev_topk", "l1dm_op_apply", "l1dm_block_krylov",
+                 "l1dm_cg"):
         getattr(lib, name).restype = st
     lib.l1dm_handleless_launches.argtypes = []
     lib.l1dm_handleless_launches.restype = i64
@@ -682,6 +684,19 @@ def l1dm_syevj(A: torch.Tensor, stream=None):
         _check(load_library().l1dm_syevj(N, _ptr(A), A.stride(0), _ptr(W), _ptr(V), V.stride(0),
                                          _stream_of(A, stream)), "l1dm_syevj")
     return W, V
+
+
+def l1dm_syev_topk(A: torch.Tensor, k: int, stream=None):
+    """The k eigenpairs of largest |lambda| of a symmetric device matrix: (lam, V), A V = V lam."""
+    dev = A.device
+    A = _f64_dev(A, "A", dev)
+    N = A.shape[0]
+    lam = torch.empty(k, dtype=torch.float64, device=dev)
+    V = torch.empty((N, k), dtype=torch.float64, device=dev)
+    with torch.cuda.device(dev):
+        _check(load_library().l1dm_syev_topk(N, _ptr(A), A.stride(0), k, _ptr(lam), _ptr(V), k,
+                                             _stream_of(A, stream)), "l1dm_syev_topk")
+    return lam, V
 
 
 def l1dm_op_apply(op: Operator, V: torch.Tensor, Y: torch.Tensor | None = None, stream=None):

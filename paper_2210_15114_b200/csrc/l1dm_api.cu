@@ -2020,6 +2020,32 @@ l1dm_status l1dm_syevj(int64_t N, const double *A, int64_t lda, double *W, doubl
   return L1DM_OK;
 }
 
+l1dm_status l1dm_syev_topk(int64_t N, const double *A, int64_t lda, int64_t k, double *lam,
+                           double *V, int64_t ldv, void *stream) {
+  NvtxRange nvtx_("l1dm_syev_topk");
+  g_err.clear();
+  if (!A || !lam || !V) return fail(L1DM_EINVAL, "A, lam or V is NULL");
+  if (N < 1 || N > 4096 || k < 1 || k > 96 || k > N || lda < N || ldv < k)
+    return fail(L1DM_EINVAL, "syev_topk N=%lld k=%lld lda=%lld ldv=%lld invalid (N <= 4096, "
+                "k <= min(N, 96))", (long long)N, (long long)k, (long long)lda, (long long)ldv);
+  int dev = 0;
+  l1dm_status st = check_arch(&dev);
+  if (st != L1DM_OK) return st;
+  if (!is_device_pointer(A) || !is_device_pointer(lam) || !is_device_pointer(V))
+    return fail(L1DM_EINVAL, "l1dm_syev_topk takes device pointers");
+  cudaStream_t s = (cudaStream_t)stream;
+  Scratch sc(s);
+  CUDA_TRY(sc.reserve(Scratch::bytes_for(topk_workspace(N), 1) +
+                      Scratch::bytes_for((size_t)N * k, sizeof(double)) + 512));
+  double *ws = sc.take<double>(topk_workspace(N) / sizeof(double) + 1);
+  double *Vs = sc.take<double>((size_t)N * k);
+  g_handleless_launches += launch_sym_topk(N, A, lda, k, lam, nullptr, Vs, ws, device_sms(), s);
+  CUDA_TRY(cudaMemcpy2DAsync(V, ldv * sizeof(double), Vs, k * sizeof(double), k * sizeof(double),
+                             N, cudaMemcpyDeviceToDevice, s));
+  CUDA_TRY(cudaGetLastError());
+  return L1DM_OK;
+}
+
 l1dm_status l1dm_op_apply(const l1dm_operator_t *op, const double *V, int64_t ldv, int64_t b,
                           double *Y, int64_t ldy, void *stream) {
   NvtxRange nvtx_("l1dm_op_apply");
@@ -2052,9 +2078,9 @@ l1dm_status l1dm_block_krylov(const l1dm_operator_t *op, int64_t k, int64_t bloc
   if (st != L1DM_OK) return st;
   const int64_t b = block, q = depth, Qw = block * depth;
   if (!Pi || !sigma) return fail(L1DM_EINVAL, "Pi or sigma is NULL");
-  if (k < 1 || b < k || b > 96 || q < 1 || Qw > n || (Z && ldz < k))
+  if (k < 1 || b < k || b > 96 || q < 1 || Qw > n || Qw > 4096 || (Z && ldz < k))
     return fail(L1DM_EINVAL, "krylov k=%lld block=%lld depth=%lld (n=%lld) invalid: need 1 <= k "
-                "<= block <= 96, depth >= 1, block*depth <= n", (long long)k, (long long)b,
+                "<= block <= 96, depth >= 1, block*depth <= min(n, 4096)", (long long)k, (long long)b,
                 (long long)q, (long long)n);
   for (const void *ptr : {(const void *)Pi, (const void *)sigma, (const void *)lam,
                           (const void *)Z})
@@ -2074,12 +2100,9 @@ l1dm_status l1dm_block_krylov(const l1dm_operator_t *op, int64_t k, int64_t bloc
   add((size_t)b, 8);                         // lamb
   add((size_t)Qw * b, 8);                    // Ct
   add((size_t)Qw * Qw, 8);                   // T
-  add((size_t)Qw * Qw, 8);                   // TV
-  add((size_t)Qw, 8);                        // TW
   add((size_t)Qw * k, 8);                    // Vs
-  add((size_t)k, 4);                         // order
   add(gws / 8 + 1, 8);
-  add(jacobi_workspace(std::max(Qw, b)) / 8 + 1, 8);
+  add(topk_workspace(Qw) / 8 + 1, 8);
   Scratch sc(s);
   CUDA_TRY(sc.reserve(bytes));
   double *Qb = sc.take<double>((size_t)n * Qw), *W = sc.take<double>((size_t)n * b);
@@ -2089,11 +2112,10 @@ l1dm_status l1dm_block_krylov(const l1dm_operator_t *op, int64_t k, int64_t bloc
   double *G0 = sc.take<double>(b * b), *G = sc.take<double>(b * b);
   double *Gv = sc.take<double>(b * b), *S = sc.take<double>(b * b);
   double *lamb = sc.take<double>(b), *Ct = sc.take<double>(Qw * b);
-  double *T = sc.take<double>(Qw * Qw), *TV = sc.take<double>(Qw * Qw), *TW = sc.take<double>(Qw);
+  double *T = sc.take<double>(Qw * Qw);
   double *Vs = sc.take<double>(Qw * k);
-  int *order = sc.take<int>(k);
   double *gw = sc.take<double>(gws / 8 + 1);
-  double *jw = sc.take<double>(jacobi_workspace(std::max(Qw, b)) / 8 + 1);
+  double *tw = sc.take<double>(topk_workspace(Qw) / 8 + 1);
   CUDA_TRY(cudaMemsetAsync(T, 0, (size_t)Qw * Qw * sizeof(double), s));
 
   std::vector<cudaEvent_t> evs;
@@ -2171,9 +2193,9 @@ l1dm_status l1dm_block_krylov(const l1dm_operator_t *op, int64_t k, int64_t bloc
   }
   gemm(1, Qw, b, n, 1.0, Qb, Qw, W, b, 0.0, T + (q - 1) * b, Qw);  // last column block of T
   launch_symmetrize(Qw, T, Qw, s);
-  launches += 1 + launch_jacobi(Qw, T, Qw, TW, TV, Qw, jw, sms, s);
-  launch_select(Qw, k, TW, TV, Qw, lam, sigma, Vs, order, s);
-  ++launches;
+  // the k Ritz pairs of largest |lambda|: Householder tridiagonalisation, bisection, inverse
+  // iteration, back-transformation (l1dm_dense.cu)
+  launches += 1 + launch_sym_topk(Qw, T, Qw, k, lam, sigma, Vs, tw, sms, s);
   if (Z) gemm(0, n, k, Qw, 1.0, Qb, Qw, Vs, k, 0.0, Z, ldz);
   ev();  // total end
   cudaError_t e = cudaStreamSynchronize(s);

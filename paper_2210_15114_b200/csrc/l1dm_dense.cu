@@ -617,6 +617,351 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ------------------------------------------------------------------------ top-k eigenpairs
+// The Rayleigh-Ritz step needs only the k eigenpairs of largest |lambda| of the (q b)^2 matrix T:
+//   k55_tridiag     Householder reduction T = H^T Tri H on a cooperative grid (two grid barriers
+//                   per column: p = tau A22 v, then the rank-2 update A22 -= v w^T + w v^T),
+//   k56_tri_topk    one CTA: Sturm-count bisection for the k smallest and k largest eigenvalues
+//                   of the tridiagonal, the k of largest |lambda|, inverse iteration (tridiagonal
+//                   LU with partial pivoting) with modified Gram-Schmidt inside eigenvalue
+//                   clusters (|dl| <= 1e-3 ||Tri||_1, LAPACK dstein's grouping),
+//   k57_back        one CTA per vector: y <- H_0 ... H_{N-3} y (reflectors in reverse order).
+// ws layout (doubles): A copy N*N | p N | reflectors N*N | tau N | d N | e N
+__global__ void __launch_bounds__(512)
+    k55_tridiag(int N, double *__restrict__ A, double *__restrict__ p, double *__restrict__ H,
+                double *__restrict__ tau, double *__restrict__ d, double *__restrict__ e) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[512];
+  const int tid = threadIdx.x;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  const int lane = tid & 31;
+  const int64_t gwarp = gtid >> 5, nwarps = nth >> 5;
+  auto block_sum = [&](double v) -> double {  // fixed tree
+    red[tid] = v;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o; o >>= 1) {
+      if (tid < o) red[tid] += red[tid + o];
+      __syncthreads();
+    }
+    const double r = red[0];
+    __syncthreads();
+    return r;
+  };
+  for (int j = 0; j < N - 2; ++j) {
+    const int m = N - j - 1;           // length of x = A[j][j+1 .. N-1] (row j = column j)
+    const double *x = A + (int64_t)j * N + j + 1;
+    // every CTA computes the reflector's scalars from row j (unchanged during this step)
+    double part = 0.0;
+    for (int i = 1 + tid; i < m; i += blockDim.x) part += x[i] * x[i];
+    const double sigma = block_sum(part);
+    const double x0 = x[0];
+    double alpha, t, v0;
+    if (sigma == 0.0) {  // already tridiagonal in this column
+      alpha = x0;
+      t = 0.0;
+      v0 = 0.0;
+    } else {
+      const double nrm = sqrt(fma(x0, x0, sigma));
+      alpha = x0 >= 0.0 ? -nrm : nrm;
+      v0 = x0 - alpha;
+      t = 2.0 / fma(v0, v0, sigma);   // H = I - t v v^T, v = (v0, x_1, ..., x_{m-1})
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+      d[j] = A[(int64_t)j * N + j];
+      e[j] = alpha;
+      tau[j] = t;
+    }
+    for (int i = gtid; i < m; i += nth) H[(int64_t)j * N + i] = (i == 0) ? v0 : x[i];
+    if (t != 0.0) {
+      // p = t A22 v: one warp per row of the trailing block
+      for (int64_t r = gwarp; r < m; r += nwarps) {
+        const double *ar = A + (int64_t)(j + 1 + r) * N + j + 1;
+        double acc = 0.0;
+        for (int c = lane; c < m; c += 32) acc = fma(ar[c], c == 0 ? v0 : x[c], acc);
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+        if (lane == 0) p[r] = t * acc;
+      }
+    }
+    grid.sync();
+    if (t != 0.0) {
+      // K = t/2 v^T p; w = p - K v; A22 -= v w^T + w v^T
+      double kp = 0.0;
+      for (int i = tid; i < m; i += blockDim.x) kp = fma(i == 0 ? v0 : x[i], p[i], kp);
+      const double K = 0.5 * t * block_sum(kp);
+      for (int64_t q = gtid; q < (int64_t)m * m; q += nth) {
+        const int r = (int)(q / m), c = (int)(q - (q / m) * m);
+        const double vr = r == 0 ? v0 : x[r], vc = c == 0 ? v0 : x[c];
+        const double wr = p[r] - K * vr, wc = p[c] - K * vc;
+        double *a = A + (int64_t)(j + 1 + r) * N + j + 1 + c;
+        *a -= fma(vr, wc, wr * vc);
+      }
+    }
+    grid.sync();
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    if (N >= 2) {
+      d[N - 2] = A[(int64_t)(N - 2) * N + N - 2];
+      e[N - 2] = A[(int64_t)(N - 1) * N + N - 2];
+    }
+    d[N - 1] = A[(int64_t)(N - 1) * N + N - 1];
+  }
+}
+
+// number of eigenvalues of the tridiagonal (d, e) below x (Sturm count via the LDL^T pivots)
+__device__ __forceinline__ int sturm_count(const double *d, const double *e2, int N, double x,
+                                           double pivmin) {
+  int cnt = 0;
+  double q = d[0] - x;
+  if (fabs(q) < pivmin) q = -pivmin;
+  cnt += q < 0.0;
+  for (int i = 1; i < N; ++i) {
+    q = d[i] - x - e2[i - 1] / q;
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += q < 0.0;
+  }
+  return cnt;
+}
+
+// One CTA (256 threads).  Y (N x k, ldy = k): the tridiagonal's eigenvectors of the k eigenvalues
+// of largest |lambda| (ties by index), in that order; lam[k], sigma[k] = |lam|.
+// smem: d, e, e2 (N each) + LU factors 5N + work 2N + the k vectors live in Y (global).
+__global__ void __launch_bounds__(256)
+    k56_tri_topk(int N, int k, const double *__restrict__ dg, const double *__restrict__ eg,
+                 double *__restrict__ lam, double *__restrict__ sigma, double *__restrict__ Y) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double *d = reinterpret_cast<double *>(smem_raw);
+  double *e = d + N, *e2 = e + N;
+  double *lu_d = e2 + N, *lu_u1 = lu_d + N, *lu_u2 = lu_u1 + N, *lu_l = lu_u2 + N;
+  int *piv = reinterpret_cast<int *>(lu_l + N);
+  double *y = reinterpret_cast<double *>(piv + N + (N & 1));
+  double *cand = y + N;                    // [2k] candidate eigenvalues
+  int *cidx = reinterpret_cast<int *>(cand + 2 * k);  // [2k] their eigenvalue indices
+  int *sel = cidx + 2 * k;                 // [k] chosen candidates, by |lambda| desc
+  __shared__ double s_lo, s_hi, s_norm, s_red[256];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < N; i += blockDim.x) {
+    d[i] = dg[i];
+    e[i] = i < N - 1 ? eg[i] : 0.0;
+    e2[i] = e[i] * e[i];
+  }
+  __syncthreads();
+  if (tid == 0) {  // Gershgorin interval and ||Tri||_1
+    double lo = d[0], hi = d[0], nrm = 0.0;
+    for (int i = 0; i < N; ++i) {
+      const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i < N - 1 ? fabs(e[i]) : 0.0);
+      lo = fmin(lo, d[i] - r);
+      hi = fmax(hi, d[i] + r);
+      nrm = fmax(nrm, fabs(d[i]) + r);
+    }
+    s_lo = lo;
+    s_hi = hi;
+    s_norm = nrm;
+  }
+  __syncthreads();
+  const double tnorm = s_norm > 0.0 ? s_norm : 1.0;
+  const double pivmin = fmax(1e-300, 1e-300 * tnorm);
+  // bisection for eigenvalue indices 0..k-1 and N-k..N-1 (2k candidates, duplicates when 2k > N)
+  const int nc = 2 * k;
+  for (int c = tid; c < nc; c += blockDim.x) {
+    int idx = c < k ? c : N - nc + c;
+    if (idx < 0) idx = 0;
+    if (idx >= N) idx = N - 1;
+    double lo = s_lo - 2.2e-16 * tnorm - pivmin, hi = s_hi + 2.2e-16 * tnorm + pivmin;
+    for (int it = 0; it < 200; ++it) {
+      const double mid = 0.5 * (lo + hi);
+      if (mid <= lo || mid >= hi) break;
+      if (hi - lo <= 2.2e-16 * fmax(fabs(lo), fabs(hi)) + pivmin) break;
+      if (sturm_count(d, e2, N, mid, pivmin) > idx) hi = mid;
+      else lo = mid;
+    }
+    cand[c] = 0.5 * (lo + hi);
+    cidx[c] = idx;
+  }
+  __syncthreads();
+  if (tid == 0) {  // the k distinct eigenvalue indices of largest |lambda| (ties: smaller index)
+    int nsel = 0;
+    bool used[2 * 96 + 2];  // k <= 96
+    for (int c = 0; c < nc; ++c) used[c] = false;
+    for (int c = 0; c < nc; ++c)  // candidates with the same index are one eigenvalue
+      for (int c2 = 0; c2 < c; ++c2)
+        if (cidx[c2] == cidx[c]) used[c] = true;
+    while (nsel < k) {
+      int best = -1;
+      for (int c = 0; c < nc; ++c) {
+        if (used[c]) continue;
+        if (best < 0 || fabs(cand[c]) > fabs(cand[best]) ||
+            (fabs(cand[c]) == fabs(cand[best]) && cidx[c] < cidx[best]))
+          best = c;
+      }
+      if (best < 0) break;
+      used[best] = true;
+      sel[nsel++] = best;
+    }
+    for (int r = nsel; r < k; ++r) sel[r] = sel[0];
+  }
+  __syncthreads();
+  // inverse iteration, vectors processed in ascending eigenvalue order so clusters are adjacent
+  for (int rr = 0; rr < k; ++rr) {
+    // position rr in ascending-lambda order among the selected
+    __shared__ int s_r;
+    __shared__ double s_lam;
+    if (tid == 0) {
+      int chosen = -1;
+      for (int a = 0; a < k; ++a) {  // rank by (lambda, index)
+        int rank = 0;
+        for (int b2 = 0; b2 < k; ++b2)
+          rank += (cand[sel[b2]] < cand[sel[a]]) ||
+                  (cand[sel[b2]] == cand[sel[a]] && cidx[sel[b2]] < cidx[sel[a]]) ||
+                  (cand[sel[b2]] == cand[sel[a]] && cidx[sel[b2]] == cidx[sel[a]] && b2 < a);
+        if (rank == rr) chosen = a;
+      }
+      s_r = chosen;
+      double lm = cand[sel[chosen]];
+      s_lam = lm;
+    }
+    __syncthreads();
+    const int r = s_r;
+    double shift = s_lam;
+    // LU of (Tri - shift I) with partial pivoting (thread 0; O(N))
+    if (tid == 0) {
+      const double tiny = 2.2e-16 * tnorm;
+      double a = d[0] - shift, b = N > 1 ? e[0] : 0.0;
+      for (int i = 0; i < N - 1; ++i) {
+        const double c = e[i], dn = d[i + 1] - shift, bn = i + 1 < N - 1 ? e[i + 1] : 0.0;
+        if (fabs(a) >= fabs(c)) {  // no swap: rows (a b 0), (c dn bn)
+          piv[i] = 0;
+          const double l = (a != 0.0) ? c / a : 0.0;
+          lu_d[i] = a;
+          lu_u1[i] = b;
+          lu_u2[i] = 0.0;
+          lu_l[i] = l;
+          a = dn - l * b;
+          b = bn;
+        } else {  // swap: pivot row (c dn bn)
+          piv[i] = 1;
+          const double l = a / c;
+          lu_d[i] = c;
+          lu_u1[i] = dn;
+          lu_u2[i] = bn;
+          lu_l[i] = l;
+          a = b - l * dn;
+          b = -l * bn;
+        }
+        if (lu_d[i] == 0.0) lu_d[i] = tiny;
+      }
+      lu_d[N - 1] = (a == 0.0) ? tiny : a;
+      if (fabs(lu_d[N - 1]) < tiny) lu_d[N - 1] = lu_d[N - 1] < 0 ? -tiny : tiny;
+    }
+    for (int i = tid; i < N; i += blockDim.x)  // deterministic start: 1 + small index ramp
+      y[i] = 1.0 + 1e-3 * (double)((i * 7 + r * 13) % 17);
+    __syncthreads();
+    for (int iter = 0; iter < 4; ++iter) {
+      if (tid == 0) {  // solve L U y = y
+        for (int i = 0; i < N - 1; ++i) {
+          if (piv[i]) {
+            const double t0 = y[i];
+            y[i] = y[i + 1];
+            y[i + 1] = t0 - lu_l[i] * y[i + 1];
+          } else {
+            y[i + 1] -= lu_l[i] * y[i];
+          }
+        }
+        y[N - 1] /= lu_d[N - 1];
+        if (N >= 2) y[N - 2] = (y[N - 2] - lu_u1[N - 2] * y[N - 1]) / lu_d[N - 2];
+        for (int i = N - 3; i >= 0; --i)
+          y[i] = (y[i] - lu_u1[i] * y[i + 1] - lu_u2[i] * y[i + 2]) / lu_d[i];
+      }
+      __syncthreads();
+      // MGS against earlier vectors of the same cluster (ascending order: the last few)
+      for (int q = 0; q < rr; ++q) {
+        // vector processed at position q: find its selection slot
+        __shared__ int s_q;
+        __shared__ bool s_close;
+        if (tid == 0) {
+          int slot = -1;
+          for (int a = 0; a < k; ++a) {
+            int rank = 0;
+            for (int b2 = 0; b2 < k; ++b2)
+              rank += (cand[sel[b2]] < cand[sel[a]]) ||
+                      (cand[sel[b2]] == cand[sel[a]] && cidx[sel[b2]] < cidx[sel[a]]) ||
+                      (cand[sel[b2]] == cand[sel[a]] && cidx[sel[b2]] == cidx[sel[a]] && b2 < a);
+            if (rank == q) slot = a;
+          }
+          s_q = slot;
+          s_close = fabs(cand[sel[slot]] - shift) <= 1e-3 * tnorm;
+        }
+        __syncthreads();
+        if (s_close) {
+          const double *yq = Y + s_q;  // column s_q of Y (ld k)
+          double part = 0.0;
+          for (int i = tid; i < N; i += blockDim.x) part = fma(yq[(int64_t)i * k], y[i], part);
+          s_red[tid] = part;
+          __syncthreads();
+          for (int o = 128; o; o >>= 1) {
+            if (tid < o) s_red[tid] += s_red[tid + o];
+            __syncthreads();
+          }
+          const double dot = s_red[0];
+          __syncthreads();
+          for (int i = tid; i < N; i += blockDim.x) y[i] -= dot * yq[(int64_t)i * k];
+          __syncthreads();
+        }
+      }
+      // normalise
+      double part = 0.0;
+      for (int i = tid; i < N; i += blockDim.x) part = fma(y[i], y[i], part);
+      s_red[tid] = part;
+      __syncthreads();
+      for (int o = 128; o; o >>= 1) {
+        if (tid < o) s_red[tid] += s_red[tid + o];
+        __syncthreads();
+      }
+      const double nrm = sqrt(s_red[0]);
+      __syncthreads();
+      const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
+      for (int i = tid; i < N; i += blockDim.x) y[i] *= inv;
+      __syncthreads();
+    }
+    for (int i = tid; i < N; i += blockDim.x) Y[(int64_t)i * k + r] = y[i];
+    if (tid == 0) {
+      if (lam) lam[r] = cand[sel[r]];
+      if (sigma) sigma[r] = fabs(cand[sel[r]]);
+    }
+    __syncthreads();
+  }
+}
+
+// one CTA per vector: y <- H_0 H_1 ... H_{N-3} y, H_j = I - tau_j v_j v_j^T acting on [j+1, N)
+__global__ void __launch_bounds__(256)
+    k57_back(int N, int k, const double *__restrict__ H, const double *__restrict__ tau,
+             double *__restrict__ Y) {
+  __shared__ double red[256];
+  __shared__ double yv[4096];  // N <= 4096
+  const int tid = threadIdx.x, col = blockIdx.x;
+  for (int i = tid; i < N; i += 256) yv[i] = Y[(int64_t)i * k + col];
+  __syncthreads();
+  for (int j = N - 3; j >= 0; --j) {
+    const double t = tau[j];
+    if (t == 0.0) continue;
+    const int m = N - j - 1;
+    const double *v = H + (int64_t)j * N;
+    double part = 0.0;
+    for (int i = tid; i < m; i += 256) part = fma(v[i], yv[j + 1 + i], part);
+    red[tid] = part;
+    __syncthreads();
+    for (int o = 128; o; o >>= 1) {
+      if (tid < o) red[tid] += red[tid + o];
+      __syncthreads();
+    }
+    const double f = t * red[0];
+    __syncthreads();
+    for (int i = tid; i < m; i += 256) yv[j + 1 + i] -= f * v[i];
+    __syncthreads();
+  }
+  for (int i = tid; i < N; i += 256) Y[(int64_t)i * k + col] = yv[i];
+}
+
 // ------------------------------------------------------------------------------- small kernels
 // order[r] = index of the r-th largest |W| (ties by index), r < k; lam/sigma of the selection;
 // Vs (N x k) = V[:, order].
@@ -867,6 +1212,51 @@ int launch_jacobi(int64_t N, double *A, int64_t lda, double *W, double *V, int64
   cudaLaunchCooperativeKernel((void *)k42_jacobi_grid, dim3((unsigned)blocks), dim3(512), args, 0,
                               s);
   return 1;
+}
+
+size_t topk_workspace(int64_t N) { return (size_t)(2 * N * N + 5 * N + 8) * sizeof(double); }
+
+// The k eigenpairs of largest |lambda| of the symmetric A (N x N, lda; read only):
+// lam[k], sigma[k] = |lam| in nonincreasing |lambda| order, Vs (N x k, ld k) the unit
+// eigenvectors.  N <= 4096, k <= 96.  Returns the number of launches.
+int launch_sym_topk(int64_t N, const double *A, int64_t lda, int64_t k, double *lam,
+                    double *sigma, double *Vs, double *ws, int sms, cudaStream_t s) {
+  if (N < 1 || k < 1) return 0;
+  double *Ac = ws, *p = Ac + N * N, *H = p + N, *tau = H + N * N, *d = tau + N, *e = d + N;
+  cudaMemcpy2DAsync(Ac, N * sizeof(double), A, lda * sizeof(double), N * sizeof(double), N,
+                    cudaMemcpyDeviceToDevice, s);
+  int launches = 1;
+  if (N > 2) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k55_tridiag, 512, 0);
+    if (per_sm < 1) per_sm = 1;
+    int64_t blocks = (int64_t)sms * per_sm;
+    const int64_t want = (N * N + 511) / 512;
+    if (blocks > want) blocks = want;
+    if (blocks < 1) blocks = 1;
+    int Ni = (int)N;
+    void *args[] = {&Ni, &Ac, &p, &H, &tau, &d, &e};
+    cudaLaunchCooperativeKernel((void *)k55_tridiag, dim3((unsigned)blocks), dim3(512), args, 0, s);
+    ++launches;
+  } else {
+    // N <= 2: the matrix is already tridiagonal
+    double *dd = d, *ee = e;
+    cudaMemcpy2DAsync(dd, sizeof(double), Ac, (N + 1) * sizeof(double), sizeof(double), N,
+                      cudaMemcpyDeviceToDevice, s);
+    if (N == 2)
+      cudaMemcpyAsync(ee, Ac + N, sizeof(double), cudaMemcpyDeviceToDevice, s);
+    cudaMemsetAsync(tau, 0, N * sizeof(double), s);
+  }
+  const size_t sm = (size_t)(8 * N + 2) * sizeof(double) + (size_t)(4 * k) * sizeof(double) +
+                    (size_t)(N + 1) * sizeof(int) + (size_t)(5 * k) * sizeof(int) + 64;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k56_tri_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k56_tri_topk<<<1, 256, sm, s>>>((int)N, (int)k, d, e, lam, sigma, Vs);
+  if (N > 2) k57_back<<<(unsigned)k, 256, 0, s>>>((int)N, (int)k, H, tau, Vs);
+  return launches + 2;
 }
 
 // S (b x b) with V S orthonormal (CholeskyQR with column dropping, k43_chol_orth)

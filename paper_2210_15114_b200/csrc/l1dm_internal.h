@@ -270,6 +270,9 @@ int launch_gemm(int ta, int64_t M, int64_t N, int64_t K, double alpha, const dou
 size_t jacobi_workspace(int64_t N);
 int launch_jacobi(int64_t N, double *A, int64_t lda, double *W, double *V, int64_t ldv,
                   double *ws, int sms, cudaStream_t s, int *stats = nullptr);
+size_t topk_workspace(int64_t N);
+int launch_sym_topk(int64_t N, const double *A, int64_t lda, int64_t k, double *lam,
+                    double *sigma, double *Vs, double *ws, int sms, cudaStream_t s);
 void launch_chol_orth(int64_t b, const double *G, int64_t ldg, const double *G0, int64_t ldg0,
                       double rtol, double floor_abs, double *S, cudaStream_t s);
 void launch_select(int64_t N, int64_t k, const double *W, const double *V, int64_t ldv,

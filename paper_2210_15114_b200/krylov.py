@@ -4,8 +4,9 @@ P:727-817): randomized block Krylov for the top-k singular values / a rank-k app
 SPEC S:340-357) and conjugate gradients (Thm. linear_system).
 
 Every step runs in libl1dm.so (include/l1dm.h "Matrix-free consumers"): the products, the fp64
-tensor-core GEMMs of the block Gram-Schmidt, the Jacobi eigensolver of the Gram matrices and of
-the Rayleigh quotient, and CG's dot products and updates with device scalars.  This module only
+tensor-core GEMMs of the block Gram-Schmidt, CholeskyQR2 inside each block, the top-k
+eigensolver of the Rayleigh quotient (Householder tridiagonalisation, bisection, inverse
+iteration), and CG's dot products and updates with device scalars.  This module only
 chooses the parameters, draws the start block (the method's random numbers, an input to the
 library) and marshals results.  There is no host or torch fallback: without the library and a
 B200 the calls raise.
@@ -13,9 +14,10 @@ B200 the calls raise.
 Block Krylov (Musco & Musco's block Krylov iteration for symmetric A, whose singular values
 are |eigenvalues|):
   K = [A Pi, A^2 Pi, ..., A^q Pi]  built block by block, each new block orthonormalised
-  against all previous ones (two passes of block classical Gram-Schmidt) and within itself;
-  Rayleigh-Ritz: T = Q^T (A Q) from the orthogonalisation coefficients (block Lanczos with full
-  re-orthogonalisation), T = V diag(lam) V^T, sigma_i = |lam_i| sorted, Z = Q V_k.
+  against the previous ones (block Gram-Schmidt: the last two blocks, then the whole basis) and
+  within itself (CholeskyQR2); Rayleigh-Ritz: T = Q^T (A Q) from the orthogonalisation
+  coefficients (block Lanczos with full re-orthogonalisation), its k eigenpairs of largest
+  |lambda|, sigma_i = |lam_i| sorted, Z = Q V_k.
 """
 from __future__ import annotations
 
@@ -42,14 +44,14 @@ class KrylovResult:
 def krylov_params(n: int, k: int, block: Optional[int] = None, depth: Optional[int] = None,
                   eps: float = 0.5) -> tuple[int, int]:
     """(b, q): block b = k + 8 and depth q = max(4, ceil(log(n) / sqrt(eps))) by default
-    (SPEC S:343), capped so that the basis (q b columns) fits in n and b <= 96."""
+    (SPEC S:343), capped so that the basis (q b columns) fits in n and 4096, and b <= 96."""
     if not (1 <= k < n):
         raise ValueError(f"need 1 <= k < n (k={k}, n={n})")
     b = block or min(n, k + 8)
     if not (k <= b <= 96):
         raise ValueError(f"need k <= block <= 96 (k={k}, block={b})")
     q = depth or max(4, math.ceil(math.log(max(n, 2)) / math.sqrt(eps)))
-    q = max(1, min(q, n // b))
+    q = max(1, min(q, n // b, 4096 // b))
     return b, q
 
 

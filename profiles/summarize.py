@@ -19,12 +19,21 @@ for r in rows[hi + 1:]:
     scale = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1, "msecond": 1}.get(r[ui], 1)
     agg[name][0] += 1
     agg[name][1] += float(r[vi].replace(",", "")) * scale
-tot = sum(v[1] for v in agg.values())
+# shares over the library's kernels (l1dm::); torch's kernels (the inputs' RNG and the bench's
+# after-the-timed-region parity check, definition in fp64) are listed apart
+lib = {k: v for k, v in agg.items() if k.startswith("l1dm::")}
+tot = sum(v[1] for v in lib.values())
 out = [f"# ncu launch list (gpu__time_duration.sum, --clock-control none; cold-cache, serialised)",
        f"# workload {w}: bench.py --workload {w} --steps 1 --warmup 1 --queries 3 (profiles/run_profile.sh)",
+       f"# share = of the library's (l1dm::) kernel time {tot:.3f} ms",
        f"{'kernel':60s} {'launches':>8s} {'total_ms':>10s} {'share':>7s}"]
-for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
+for k, v in sorted(lib.items(), key=lambda x: -x[1][1]):
     out.append(f"{k[:60]:60s} {v[0]:8d} {v[1]:10.3f} {v[1] / tot * 100:6.1f}%")
+other = {k: v for k, v in agg.items() if not k.startswith("l1dm::")}
+if other:
+    out.append("# not the library's (input generation, parity check after the timed region):")
+    for k, v in sorted(other.items(), key=lambda x: -x[1][1]):
+        out.append(f"{k[:60]:60s} {v[0]:8d} {v[1]:10.3f}")
 open(f"profiles/{tag}_{w}_launch_shares.txt", "w").write("\n".join(out) + "\n")
 
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,

@@ -93,6 +93,44 @@ def test_syevj_l1_distance_matrix_zero_diagonal():
     check_eig(A, W, V)
 
 
+@pytest.mark.parametrize("N,k", [(1, 1), (2, 2), (3, 1), (17, 5), (96, 16), (97, 8), (640, 16),
+                                 (1000, 32)])
+def test_syev_topk_against_eigh(N, k):
+    rng = np.random.default_rng(N * 3 + k)
+    B = rng.standard_normal((N, N))
+    A = B + B.T
+    lam, V = binding.l1dm_syev_topk(dev(A), k)
+    lam, V = lam.cpu().numpy(), V.cpu().numpy()
+    w = np.linalg.eigvalsh(A)
+    want = w[np.argsort(-np.abs(w), kind="stable")][:k]
+    scale = np.linalg.norm(A)
+    assert np.allclose(np.abs(lam), np.abs(want), rtol=0, atol=1e-12 * scale)
+    assert np.allclose(lam, want, rtol=0, atol=1e-12 * scale) or N < 3
+    assert np.abs(V.T @ V - np.eye(k)).max() <= 1e-9
+    assert np.linalg.norm(A @ V - V * lam[None, :]) <= 1e-10 * scale
+
+
+def test_syev_topk_clustered_and_krylov_like_spectra():
+    """An l1 distance matrix (one dominant eigenvalue, a cluster of negative ones) and a matrix
+    with exactly repeated eigenvalues (identity plus rank 2)."""
+    X = np.random.default_rng(8).standard_normal((300, 5)).astype(np.float32)
+    A = oracle.brute(X, np.eye(300, dtype=np.float32))
+    lam, V = binding.l1dm_syev_topk(dev(A), 12)
+    lam, V = lam.cpu().numpy(), V.cpu().numpy()
+    w = np.linalg.eigvalsh(A)
+    want = w[np.argsort(-np.abs(w), kind="stable")][:12]
+    assert np.allclose(lam, want, rtol=1e-12, atol=1e-12 * np.linalg.norm(A))
+    assert np.abs(V.T @ V - np.eye(12)).max() <= 1e-9
+    assert np.linalg.norm(A @ V - V * lam[None, :]) <= 1e-9 * np.linalg.norm(A)
+    u = np.random.default_rng(9).standard_normal((200, 2))
+    R = 3.0 * np.eye(200) + u @ u.T
+    lam, V = binding.l1dm_syev_topk(dev(R), 5)
+    lam, V = lam.cpu().numpy(), V.cpu().numpy()
+    assert np.allclose(np.sort(lam)[:3], 3.0, rtol=1e-12)
+    assert np.abs(V.T @ V - np.eye(5)).max() <= 1e-9
+    assert np.linalg.norm(R @ V - V * lam[None, :]) <= 1e-10 * np.linalg.norm(R)
+
+
 # ----------------------------------------------------------------------------------- Krylov
 def dense(X, p):
     n = X.shape[0]
