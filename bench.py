@@ -657,11 +657,14 @@ def main_ours(args):
         G = 8
         kk = -(-d // G)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c_ = torch.cuda.Event(enable_timing=True)
         Ys = torch.empty_like(Y)  # Y still holds the validated query-0 rows
+        Xs = X[:, :kk].contiguous()  # what a rank holds at N > 1 (its slice, made contiguous)
         for _ in range(2):  # one untimed, one timed
             torch.cuda.synchronize()
             a.record(stream)
-            hs = l1.l1dm_prepare(X, 0, kk, stream=stream)
+            hs = l1.l1dm_prepare(Xs, stream=stream)
+            c_.record(stream)
             l1.l1dm_set_query_mode(hs, args.mode)
             for q in range(Q):
                 if args.p == 1:
@@ -672,10 +675,14 @@ def main_ours(args):
             torch.cuda.synchronize()
             l1.l1dm_free(hs)
         t_shard = a.elapsed_time(b)
-        del Ys
+        t_shard_prep = a.elapsed_time(c_)
+        del Ys, Xs
         result["shard_proxy"] = {
             "G": G, "coords_per_shard": kk, "t1_ms_per_step": ms_step,
             "t_shard_ms_per_step": t_shard, "compute_efficiency": ms_step / (G * t_shard),
+            "t1_prepare_ms": prep_ms, "t_shard_prepare_ms": t_shard_prep,
+            "t1_query_ms": (ms_step - (prep_ms or 0.0)) / Q,
+            "t_shard_query_ms": (t_shard - t_shard_prep) / Q,
             "note": "one B200: a step (prepare + the same queries) on coordinates [0, ceil(d/8)) "
                     "vs the full step; excludes the cross-GPU sum (DESIGN.md §8)"}
     # ---- e2e through the public API with HOST buffers (pinned), N=1 only

@@ -2,7 +2,7 @@
 
 Tolerance (R18): the query evaluates sum_t c_t x^(p-t) (2 M_t - T_t) with fp64
 moments M_t of z x^t.  For |x| ~ 1 data the moments are O(n) and cancel to the O(n) result
-only mildly: measured max column relative l2 error ~6e-16 for p = 3, 5, 7 (scratch/lp_probe.py),
+only mildly: measured max column relative l2 error ~6e-16 for p = 3, 5, 7 (a round-1 probe script, in git history),
 so the l1 bar of 1e-9 holds with ~6 orders of margin.  Integer data with small moments is exact
 (every partial sum is an integer < 2^53) and is checked bit-for-bit.  TV is half the l1
 product: same 1e-9 bar."""
