@@ -185,7 +185,8 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
   __shared__ uint32_t s_vals[kSortTile];
   __shared__ uint32_t s_whist[W][256];   // per-warp digit counts, then warp-exclusive offsets
   __shared__ uint32_t s_tstart[256];     // tile-local start of each digit
-  __shared__ uint64_t s_gbase[256];      // global start of this tile's run of each digit
+  __shared__ uint32_t s_gbase[256];      // segment-relative start of this tile's run of each digit
+                                         // (n < 2^32: every in-segment offset fits 32 bits)
   __shared__ uint32_t s_wsum[W];
   __shared__ unsigned s_tk[2];
 
@@ -227,21 +228,24 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
     const int64_t seg = t_cur - tile * nseg;
     const int64_t base = tile * kSortTile;
     const int64_t seg_off = seg * ldn;
-    const int64_t tile_valid = (n - base < kSortTile) ? (n - base) : kSortTile;
+    const int tile_valid = (int)((n - base < kSortTile) ? (n - base) : kSortTile);
+    // 32-bit tile-local indices from here on (the pass is instruction-bound: ncu shows the SM
+    // issuing integer ALU most of the time, so 64-bit index arithmetic per key is not free)
+    const uint32_t base32 = (uint32_t)base;
 
     // ---- items (warp-striped: warp w owns [w*32*ITEMS, (w+1)*32*ITEMS), item j at +j*32+lane)
     uint32_t keys[kSortItems];
     uint32_t vals[kSortItems];
     uint16_t lrank[kSortItems];
-    const int64_t wbase = base + (int64_t)w * 32 * kSortItems;
+    const int wbase = w * 32 * kSortItems;
     {
       const uint32_t *sk = s_in + (size_t)cur * 2 * kSortTile, *sv = sk + kSortTile;
 #pragma unroll
       for (int j = 0; j < kSortItems; ++j) {
-        const int e = w * 32 * kSortItems + j * 32 + lane;
-        const bool valid = base + e < n;
+        const int e = wbase + j * 32 + lane;
+        const bool valid = e < tile_valid;
         keys[j] = valid ? sk[e] : 0u;
-        vals[j] = FIRST ? (uint32_t)(base + e) : (valid ? sv[e] : 0u);
+        vals[j] = FIRST ? base32 + (uint32_t)e : (valid ? sv[e] : 0u);
       }
     }
     // ---- warp multisplit: stable rank of each key among equal digits of its warp
@@ -252,13 +256,13 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
     uint32_t peers[kSortItems];
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
-      const bool valid = wbase + j * 32 + lane < n;
+      const bool valid = wbase + j * 32 + lane < tile_valid;
       const uint32_t dgt = (keys[j] >> shift) & 255u;
 #ifdef L1DM_SORT_MATCH
       // invalid lanes match only themselves (256 + lane is no digit)
       const uint32_t pm = __match_any_sync(0xFFFFFFFFu, valid ? dgt : 256u + lane);
 #else
-      uint32_t pm = __ballot_sync(0xFFFFFFFFu, valid);
+      uint32_t pm = (tile_valid == kSortTile) ? 0xFFFFFFFFu : __ballot_sync(0xFFFFFFFFu, valid);
 #pragma unroll
       for (int b = 0; b < 8; ++b) {
         const uint32_t bit = (dgt >> b) & 1u;
@@ -337,7 +341,7 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
       st_relaxed_u64(&st[tile * 256 + dgt], pack_status(kFlagInclusive, epoch,
                                                         (uint32_t)(excl + cnt)));
     }
-    s_gbase[dgt] = (uint64_t)digit_base[seg * 256 + dgt] + excl;
+    s_gbase[dgt] = digit_base[seg * 256 + dgt] + (uint32_t)excl;
     SORT_T(3);
 
     // ---- block exclusive scan of the tile's digit counts -> s_tstart
@@ -360,8 +364,8 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
     // ---- stage the tile in digit order (stable: warp order, then item, then lane)
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
-      const int64_t idx = wbase + j * 32 + lane;
-      if (idx < n) {
+      const int idx = wbase + j * 32 + lane;
+      if (idx < tile_valid) {
         const uint32_t d = (keys[j] >> shift) & 255u;
         const uint32_t lp = s_tstart[d] + s_whist[w][d] + lrank[j];
         s_keys[lp] = keys[j];
@@ -372,18 +376,22 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
     SORT_T(5);
 
     // ---- scatter: consecutive e inside a digit run go to consecutive global slots
-    for (int e = tid; e < tile_valid; e += kSortThreads) {
-      const uint32_t k = s_keys[e];
-      const uint32_t v = s_vals[e];
-      const uint32_t d = (k >> shift) & 255u;
-      const int64_t gpos = (int64_t)(s_gbase[d] + (uint64_t)(e - s_tstart[d]));
-      if (LAST) {
-        kout[seg_off + gpos] = __float_as_uint(key_to_float(k));  // sval
-        vout[seg_off + gpos] = v;                                 // perm
-        if (rank) rank[seg_off + v] = (uint32_t)gpos;             // rank = perm^-1 (K3 fused)
-      } else {
-        kout[seg_off + gpos] = k;
-        vout[seg_off + gpos] = v;
+    {
+      uint32_t *ko = kout + seg_off, *vo = vout + seg_off;
+      uint32_t *ro = rank ? rank + seg_off : nullptr;
+      for (int e = tid; e < tile_valid; e += kSortThreads) {
+        const uint32_t k = s_keys[e];
+        const uint32_t v = s_vals[e];
+        const uint32_t d = (k >> shift) & 255u;
+        const uint32_t gpos = s_gbase[d] + ((uint32_t)e - s_tstart[d]);
+        if (LAST) {
+          ko[gpos] = __float_as_uint(key_to_float(k));  // sval
+          vo[gpos] = v;                                 // perm
+          if (ro) ro[v] = gpos;                         // rank = perm^-1 (K3 fused)
+        } else {
+          ko[gpos] = k;
+          vo[gpos] = v;
+        }
       }
     }
     SORT_T(6);
