@@ -477,6 +477,20 @@ L1DM_API const char *l1dm_last_error(void);
  * counted per handle in l1dm_timing_t.kernel_launches.  Never fails. */
 L1DM_API int64_t l1dm_handleless_launches(void);
 
+/* Environment variables (read once per process; testing and tuning hooks — the defaults are
+ * the measured choices of DESIGN.md §6 and per-handle control is l1dm_set_query_mode):
+ *   L1DM_SCATTER=0|1        planner default for handles left in L1DM_MODE_AUTO (gather/scatter)
+ *   L1DM_SCATTER_MB=k       scatter column-block width override
+ *   L1DM_REDUCE_ALL=0       scatter tile totals by a reduce pass per column block
+ *   L1DM_RUNS=0             prepare never builds the runs tables (§2f)
+ *   L1DM_RUNS_GATHER=0      the shared-memory-staged runs expansion
+ *   L1DM_FUSED_RANK=1       the last sort pass scatters the inverse ranks eagerly
+ *   L1DM_SCAN_SEGMENTS=k    gather-mode scan: split columns until k segments per chunk
+ *   L1DM_K12_RING=0|1       even-p moment reduce staging variant
+ *   L1DM_DEBUG_ALLOC, L1DM_DEBUG_PREP, L1DM_DEBUG_JACOBI   diagnostics to stderr
+ * None changes a result beyond floating-point summation order (every path is held to the same
+ * parity bar by tests/). */
+
 /* Library version string. */
 L1DM_API const char *l1dm_version(void);
 
