@@ -22,6 +22,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 #include <cstdint>
@@ -247,11 +248,18 @@ int gemm_t(int64_t M, int64_t N, int64_t K, double alpha, const double *A, int64
   return 2;
 }
 
+// Split-K factor of the TN reduction (A^T B over the n points): enough CTAs to hide the
+// operand loads' latency — measured on B200, the tall basis products (M > 64, N = 32) run best
+// with ~8 CTAs per SM (2.13 ms vs 3.48 ms at 2 per SM for 608 x 32 x 2^20), the Gram-sized
+// ones with ~2.
 int64_t gemm_splits(int ta, int64_t M, int64_t N, int64_t K, int sms) {
   if (!ta) return 1;  // A W: K is a basis width (small); M (points) gives the parallelism
-  const int64_t bm = (M <= 32 && N <= 32) ? 32 : 64, bn = N <= 32 ? 32 : 64;
+  const bool narrow = N <= 32;
+  const int64_t bm = (M <= 32 && narrow) ? 32 : (M <= 64 && narrow) ? 64 : narrow ? 128 : 64;
+  const int64_t bn = narrow ? 32 : 64;
+  const int64_t per_sm = (narrow && M > 64) ? 8 : 2;
   const int64_t tiles = ((M + bm - 1) / bm) * ((N + bn - 1) / bn);
-  int64_t sp = (2 * (int64_t)sms + tiles - 1) / tiles;
+  int64_t sp = (per_sm * (int64_t)sms + tiles - 1) / tiles;
   const int64_t kmax = (K + 255) / 256;  // at least 256 rows per split
   if (sp > kmax) sp = kmax;
   return sp < 1 ? 1 : sp;
@@ -1162,9 +1170,11 @@ int launch_gemm(int ta, int64_t M, int64_t N, int64_t K, double alpha, const dou
   }
   const int64_t sp = gemm_splits(ta, M, N, K, sms);
   const bool narrow = N <= 32;
-  if (ta) {
+  if (ta) {  // tile choice measured on B200 (profiles/r02e_gemm_tn_sweep.json)
     if (M <= 32 && narrow)  // Gram-sized: 32 x 32 tile, the 8 warps split K four ways
       return gemm_t<1, 2, 1, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, sp, s);
+    if (M <= 64 && narrow)  // 64 x 32 tile, K split two ways inside the CTA
+      return gemm_t<1, 4, 1, 2>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, sp, s);
     return narrow ? gemm_t<1, 8, 1, 1>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, sp, s)
                   : gemm_t<1, 4, 2, 1>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, sp, s);
   }
