@@ -19,13 +19,13 @@ constexpr uint32_t kSpinLimit = 1u << 26;
 // ---------------- prepare (Alg. 1) ----------------
 constexpr int kSortThreads = 256;
 #ifndef L1DM_SORT_ITEMS
-#define L1DM_SORT_ITEMS 12
+#define L1DM_SORT_ITEMS 16  // keys per thread per onesweep tile (16: c3 prepare 5.92 -> 5.66 ms vs 12, round 2)
 #endif
 #ifndef L1DM_SORT_MINB
-#define L1DM_SORT_MINB 2  // with 12 items per thread: 2 CTAs per SM, measured best on B200
+#define L1DM_SORT_MINB 2  // 2 CTAs per SM (128 registers); 3 with 8-10 items measured no better
 #endif
 constexpr int kSortItems = L1DM_SORT_ITEMS;             // keys per thread per onesweep tile
-constexpr int kSortTile = kSortThreads * kSortItems;    // 3072 keys
+constexpr int kSortTile = kSortThreads * kSortItems;    // 4096 keys
 constexpr int kHistChunk = 16384;                       // keys per histogram CTA
 
 void launch_keys(const float *X, int64_t n, int64_t ldx, int64_t k0, int64_t dl, int64_t ldn,
