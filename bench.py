@@ -240,7 +240,7 @@ def sha256_of(t):
 
 
 # --------------------------------------------------------------------------- reference arm
-def cpu_oracle_sample(w, queries, budget_dims=None):
+def cpu_oracle_sample(w, queries, budget_dims=None, per_core=True):
     """Time the oracle (as it stands) on a bounded sample: full n, d' coordinates, m' columns."""
     import oracle
     from paper_2210_15114_b200 import workloads as wl
@@ -260,15 +260,17 @@ def cpu_oracle_sample(w, queries, budget_dims=None):
     upd = n * d_s * m_s
     value = upd * queries / (t_prep + queries * t_q)
     # a single-thread Alg. 2 run gives the per-core rate (2 coordinates, 1 column)
-    t0 = time.perf_counter()
-    oracle.alg2(np.ascontiguousarray(X[:, :2]), np.ascontiguousarray(order[:2]),
-                np.ascontiguousarray(Z[:, :1]), nthreads=1)
-    per_core = n * 2 / (time.perf_counter() - t0)
+    per_core_rate = None
+    if per_core:
+        t0 = time.perf_counter()
+        oracle.alg2(np.ascontiguousarray(X[:, :2]), np.ascontiguousarray(order[:2]),
+                    np.ascontiguousarray(Z[:, :1]), nthreads=1)
+        per_core_rate = n * 2 / (time.perf_counter() - t0)
     return {"value": value, "unit": "updates/s", "cores": cores, "kind": "oracle",
             "sample": (f"n={n} (full), d'={d_s} of {w.d} coords, m'={m_s} of {w.m} cols; Alg.1 "
                        f"{t_prep:.2f}s + Alg.2 {t_q:.2f}s per query, step = prep + {queries} "
                        f"queries (query time x{queries})"),
-            "per_core_query_updates_per_s": per_core,
+            "per_core_query_updates_per_s": per_core_rate,
             "prep_s": t_prep, "query_s": t_q}
 
 
@@ -295,23 +297,30 @@ def run_reference(args):
     from paper_2210_15114_b200 import workloads as wl
     w = wl.workload(args.workload)
     Q = args.queries or w.queries
-    vals = []
+    vals, sample_ms = [], []
     info = None
     for i in range(args.warmup + args.steps):
-        info = cpu_oracle_sample(w, Q, budget_dims=(64, 16))
+        t0 = time.perf_counter()
+        info = cpu_oracle_sample(w, Q, budget_dims=(64, 16), per_core=(i == 0))
+        if i == 0:
+            per_core_rate = info["per_core_query_updates_per_s"]
         if i >= args.warmup:
             vals.append(info["value"])
+            sample_ms.append((time.perf_counter() - t0) * 1e3)
     value = statistics.mean(vals)
-    ms = w.n * w.d * w.m * Q / value * 1e3
+    # ms_per_step is the wall time of the bounded sample each step actually ran (what the
+    # driver's clock sees); the full workload's step at this rate is reported beside it
     line = {
         "impl": "reference", "metric": METRIC, "value": value,
         "unit": "updates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "ms_per_step": statistics.mean(sample_ms),
+        "full_step_ms_at_this_rate": w.n * w.d * w.m * Q / value * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64 (long double accumulation) over f32 inputs", "data": "synthetic",
         "config": {"workload": args.workload, "n": w.n, "d": w.d, "m": w.m, "queries": Q},
-        "cpu_baseline": {k: info[k] for k in ("kind", "cores", "sample",
-                                              "per_core_query_updates_per_s")}
-                        | {"value": value, "unit": "updates/s"},
+        "cpu_baseline": {k: info[k] for k in ("kind", "cores", "sample")}
+                        | {"value": value, "unit": "updates/s",
+                           "per_core_query_updates_per_s": per_core_rate},
         "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
