@@ -859,6 +859,12 @@ def main_ours(args):
             cb = cpu_oracle_sample(w, Q, budget_dims=(64, 16))
             result["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind",
                                                          "sample", "per_core_query_updates_per_s")}
+            if w.n <= 4096:  # c1 also times BRUTE, O(n^2 (d + m))
+                import oracle
+                Xb, Zb = X.cpu().numpy(), Zs[0].cpu().numpy()
+                t0 = time.perf_counter()
+                oracle.brute(Xb, Zb)
+                result["cpu_baseline"]["brute_s_per_query"] = time.perf_counter() - t0
         except Exception as e:  # the baseline is reported, never required
             result["cpu_baseline"] = {"value": None, "error": str(e)}
         if parity is not None and args.p % 2 == 1:
