@@ -322,3 +322,29 @@ def test_handle_utilities_and_block_cache():
         l1.l1dm_free(h)
         if rep == 1:
             l1.l1dm_release_cached()
+
+
+def test_empty_and_invalid_sizes_rejected():
+    """SURVEY A9 / include/l1dm.h: n, d, m >= 1 — empty inputs are rejected with EINVAL (no
+    kernel runs), an empty coordinate range too; n = 1 is the smallest valid case (Y = 0)."""
+    with pytest.raises(l1.L1dmError) as e:
+        l1.l1dm_prepare(torch.zeros((0, 3), device="cuda"))
+    assert e.value.name == "L1DM_EINVAL"
+    with pytest.raises(l1.L1dmError) as e:
+        l1.l1dm_prepare(torch.zeros((5, 0), device="cuda"))
+    assert e.value.name == "L1DM_EINVAL"
+    X = torch.rand((7, 3), device="cuda")
+    with pytest.raises(l1.L1dmError) as e:
+        l1.l1dm_prepare(X, 2, 2)
+    assert e.value.name == "L1DM_EINVAL"
+    h = l1.l1dm_prepare(X)
+    with pytest.raises((l1.L1dmError, ValueError)):
+        l1.l1dm_matvec(h, torch.zeros((7, 0), device="cuda"))
+    with pytest.raises((l1.L1dmError, ValueError)):
+        l1.l1dm_matvec(h, torch.zeros((6, 2), device="cuda"))   # wrong number of rows
+    l1.l1dm_free(h)
+    h1 = l1.l1dm_prepare(torch.tensor([[1.5, -2.0]], device="cuda"))
+    Y = l1.l1dm_matvec(h1, torch.tensor([[3.0]], device="cuda"))
+    torch.cuda.synchronize()
+    assert float(Y.abs().max()) == 0.0
+    l1.l1dm_free(h1)
