@@ -35,6 +35,8 @@ if other:
     for k, v in sorted(other.items(), key=lambda x: -x[1][1]):
         out.append(f"{k[:60]:60s} {v[0]:8d} {v[1]:10.3f}")
 open(f"profiles/{tag}_{w}_launch_shares.txt", "w").write("\n".join(out) + "\n")
+if rep == "-":  # launch list only
+    sys.exit(0)
 
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                      text=True).stdout
