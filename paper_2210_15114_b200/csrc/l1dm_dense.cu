@@ -50,10 +50,11 @@ __device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double
 //   Bs[k][n] (row stride BN + 8)
 constexpr int GK = 16;
 
-template <int TA, int WM, int WN, int KS = 1>
+template <int TA, int WM, int WN, int KS = 1, int MI = 2>
 struct GemmCfg {
   static_assert(WM * WN * KS == 8, "8 warps per CTA");
-  static constexpr int BM = 16 * WM, BN = 32 * WN, SK = GK * KS;  // SK: rows per stage
+  // warp tile (8 MI) x 32: MI x 4 DMMA 8x8 tiles
+  static constexpr int BM = 8 * MI * WM, BN = 32 * WN, SK = GK * KS;  // SK: rows per stage
   static constexpr int ALD = TA ? BM + 8 : SK + 4;   // As row stride (doubles)
   static constexpr int AROWS = TA ? SK : BM;
   static constexpr int BLD = BN + 8;
@@ -65,12 +66,12 @@ struct GemmCfg {
 
 // KS > 1 (small M x N, long K): the 8 warps split each stage's rows into KS slices of 16 and
 // their partial tiles are summed through shared memory at the end (fixed order).
-template <int TA, int WM, int WN, int KS>
+template <int TA, int WM, int WN, int KS, int MI>
 __global__ void __launch_bounds__(256)
     k40_gemm(int64_t M, int64_t N, int64_t K, const double *__restrict__ A, int64_t lda,
              const double *__restrict__ B, int64_t ldb, int64_t kchunk, double *__restrict__ C,
              int64_t ldc, double alpha, double beta, int direct) {
-  using Cf = GemmCfg<TA, WM, WN, KS>;
+  using Cf = GemmCfg<TA, WM, WN, KS, MI>;
   constexpr int BM = Cf::BM, BN = Cf::BN, ALD = Cf::ALD, BLD = Cf::BLD, AROWS = Cf::AROWS;
   constexpr int AL = Cf::AL, BL = Cf::BL, SK = Cf::SK;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -115,9 +116,9 @@ __global__ void __launch_bounds__(256)
       bs[(e / BN) * BLD + (e % BN)] = rb[i];
     }
   };
-  double acc[2][4][2];
+  double acc[MI][4][2];
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
@@ -135,16 +136,16 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int ks = 0; ks < GK / 4; ++ks) {
       const int kk = wk * GK + ks * 4 + (lane & 3);
-      double a[2], b[4];
+      double a[MI], b[4];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int mm = wm * 16 + i * 8 + (lane >> 2);
+      for (int i = 0; i < MI; ++i) {
+        const int mm = wm * 8 * MI + i * 8 + (lane >> 2);
         a[i] = TA ? as[kk * ALD + mm] : as[mm * ALD + kk];
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) b[j] = bs[kk * BLD + wn * 32 + j * 8 + (lane >> 2)];
 #pragma unroll
-      for (int i = 0; i < 2; ++i)
+      for (int i = 0; i < MI; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
@@ -159,35 +160,35 @@ __global__ void __launch_bounds__(256)
     double *red = As;  // [KS-1][BM][BN]
     if (wk > 0) {
 #pragma unroll
-      for (int i = 0; i < 2; ++i)
+      for (int i = 0; i < MI; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const int r = wm * 16 + i * 8 + (lane >> 2), c = wn * 32 + j * 8 + (lane & 3) * 2 + h;
+            const int r = wm * 8 * MI + i * 8 + (lane >> 2), c = wn * 32 + j * 8 + (lane & 3) * 2 + h;
             red[((size_t)(wk - 1) * BM + r) * BN + c] = acc[i][j][h];
           }
     }
     __syncthreads();
     if (wk > 0) return;
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < MI; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int r = wm * 16 + i * 8 + (lane >> 2), c = wn * 32 + j * 8 + (lane & 3) * 2 + h;
+          const int r = wm * 8 * MI + i * 8 + (lane >> 2), c = wn * 32 + j * 8 + (lane & 3) * 2 + h;
           for (int q = 0; q < KS - 1; ++q) acc[i][j][h] += red[((size_t)q * BM + r) * BN + c];
         }
   }
   // epilogue: lane holds C[row][col], C[row][col + 1] of each 8x8 tile
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int64_t r = m0 + wm * 16 + i * 8 + (lane >> 2);
+        const int64_t r = m0 + wm * 8 * MI + i * 8 + (lane >> 2);
         const int64_t c = n0 + wn * 32 + j * 8 + (lane & 3) * 2 + h;
         if (r >= M || c >= N) continue;
         if (direct) {
@@ -216,14 +217,14 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-template <int TA, int WM, int WN, int KS>
+template <int TA, int WM, int WN, int KS, int MI = 2>
 int gemm_t(int64_t M, int64_t N, int64_t K, double alpha, const double *A, int64_t lda,
            const double *B, int64_t ldb, double beta, double *C, int64_t ldc, double *ws,
            int64_t splits, cudaStream_t s) {
-  using Cf = GemmCfg<TA, WM, WN, KS>;
+  using Cf = GemmCfg<TA, WM, WN, KS, MI>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k40_gemm<TA, WM, WN, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k40_gemm<TA, WM, WN, KS, MI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Cf::SMEM);
     attr = true;
   }
@@ -234,11 +235,11 @@ int gemm_t(int64_t M, int64_t N, int64_t K, double alpha, const double *A, int64
   if (splits < 1) splits = 1;
   dim3 g((unsigned)mt, (unsigned)nt, (unsigned)splits);
   if (splits == 1) {
-    k40_gemm<TA, WM, WN, KS><<<g, 256, Cf::SMEM, s>>>(M, N, K, A, lda, B, ldb, kchunk, C, ldc,
+    k40_gemm<TA, WM, WN, KS, MI><<<g, 256, Cf::SMEM, s>>>(M, N, K, A, lda, B, ldb, kchunk, C, ldc,
                                                       alpha, beta, 1);
     return 1;
   }
-  k40_gemm<TA, WM, WN, KS><<<g, 256, Cf::SMEM, s>>>(M, N, K, A, lda, B, ldb, kchunk, ws, N, 1.0,
+  k40_gemm<TA, WM, WN, KS, MI><<<g, 256, Cf::SMEM, s>>>(M, N, K, A, lda, B, ldb, kchunk, ws, N, 1.0,
                                                     0.0, 0);
   const int64_t tot = M * N;
   int64_t fb = (tot + 255) / 256;
@@ -1178,8 +1179,10 @@ int launch_gemm(int ta, int64_t M, int64_t N, int64_t K, double alpha, const dou
     return narrow ? gemm_t<1, 8, 1, 1>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, sp, s)
                   : gemm_t<1, 4, 2, 1>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, sp, s);
   }
-  return narrow ? gemm_t<0, 8, 1, 1>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, sp, s)
-                : gemm_t<0, 4, 2, 1>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, sp, s);
+  // the tall updates A W: 32 x 32 warp tiles (4 x 4 DMMA tiles per 8 fragment loads; measured
+  // 1M x 64 x 640: 3.73 -> 3.09 ms, 1M x 32 x 32: 0.36 -> 0.23 ms in the same run)
+  return narrow ? gemm_t<0, 8, 1, 1, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, sp, s)
+                : gemm_t<0, 4, 2, 1, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, sp, s);
 }
 
 size_t jacobi_workspace(int64_t N) {
