@@ -354,6 +354,19 @@ L1DM_API l1dm_status l1dm_block_krylov(const l1dm_operator_t *op, int64_t k, int
                                        double *lam, double *Z, int64_t ldz, void *stream,
                                        l1dm_krylov_info_t *info);
 
+/* The same with a caller-supplied product instead of an operator, e.g. a coordinate-sharded
+ * partial product followed by the cross-GPU all-reduce (A = sum_g A^(K_g)): every dense
+ * step still runs in this library, identically on every rank (deterministic kernels), and only
+ * the products go through the callback.  apply(user, V, ldv, b, Y, ldy, stream) must enqueue
+ * Y (n x b fp64, ldy) = A V (n x b fp64, ldv) on `stream` (device pointers) and return 0 (a
+ * negative l1dm_status otherwise, passed through).  Errors: as l1dm_block_krylov. */
+typedef int (*l1dm_apply_fn)(void *user, const double *V, int64_t ldv, int64_t b, double *Y,
+                             int64_t ldy, void *stream);
+L1DM_API l1dm_status l1dm_block_krylov_cb(int64_t n, l1dm_apply_fn apply, void *user, int64_t k,
+                                          int64_t block, int64_t depth, const double *Pi,
+                                          double *sigma, double *lam, double *Z, int64_t ldz,
+                                          void *stream, l1dm_krylov_info_t *info);
+
 /* Conjugate gradients for A x = b (Thm. linear_system) with every scalar on the
  * device: the host only looks at the convergence flag every 8 iterations (asynchronous copy,
  * one chunk in flight), iterations after convergence leave x unchanged.  A must be symmetric
@@ -371,6 +384,10 @@ typedef struct {
 L1DM_API l1dm_status l1dm_cg(const l1dm_operator_t *op, const double *b, double *x, double tol,
                              int64_t maxit, int normal_equations, void *stream,
                              l1dm_cg_info_t *info);
+/* CG with a caller-supplied product (see l1dm_block_krylov_cb; b = 1 column per call). */
+L1DM_API l1dm_status l1dm_cg_cb(int64_t n, l1dm_apply_fn apply, void *user, const double *b,
+                                double *x, double tol, int64_t maxit, int normal_equations,
+                                void *stream, l1dm_cg_info_t *info);
 
 /* Release every buffer the handle owns.  NULL is a no-op.  Synchronises the
  * handle's stream first. */

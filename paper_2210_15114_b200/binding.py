@@ -38,6 +38,7 @@ EXPORTS = [
     "l1dm_peer_reduce", "l1dm_peer_wait", "l1dm_peer_check",
     "l1dm_last_error", "l1dm_handleless_launches", "l1dm_version",
     "l1dm_gemm", "l1dm_syevj", "l1dm_syev_topk", "l1dm_op_apply", "l1dm_block_krylov", "l1dm_cg",
+    "l1dm_block_krylov_cb", "l1dm_cg_cb",
 ]
 
 
@@ -81,6 +82,10 @@ class KrylovInfoT(ctypes.Structure):
 class CGInfoT(ctypes.Structure):
     _fields_ = [("iterations", ctypes.c_int64), ("residual", ctypes.c_double),
                 ("converged", ctypes.c_int), ("products", ctypes.c_int64)]
+
+
+APPLY_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                            ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p)
 
 
 class TimingT(ctypes.Structure):
@@ -165,8 +170,11 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                       i64, vp, ctypes.POINTER(KrylovInfoT)]
     lib.l1dm_cg.argtypes = [ctypes.POINTER(OperatorT), vp, vp, dbl, i64, i32, vp,
                             ctypes.POINTER(CGInfoT)]
+    lib.l1dm_block_krylov_cb.argtypes = [i64, APPLY_FN, vp, i64, i64, i64, vp, vp, vp, vp, i64, vp,
+                                         ctypes.POINTER(KrylovInfoT)]
+    lib.l1dm_cg_cb.argtypes = [i64, APPLY_FN, vp, vp, vp, dbl, i64, i32, vp, ctypes.POINTER(CGInfoT)]
     for name in ("l1dm_gemm", "l1dm_syevj", "l1dm_syev_topk", "l1dm_op_apply", "l1dm_block_krylov",
-                 "l1dm_cg"):
+                 "l1dm_cg", "l1dm_block_krylov_cb", "l1dm_cg_cb"):
         getattr(lib, name).restype = st
     lib.l1dm_handleless_launches.argtypes = []
     lib.l1dm_handleless_launches.restype = i64
@@ -741,4 +749,69 @@ def l1dm_cg(op: Operator, b: torch.Tensor, *, tol: float = 1e-8, maxit: int = 50
         _check(load_library().l1dm_cg(ctypes.byref(op.c), _ptr(b), _ptr(x), float(tol), int(maxit),
                                       1 if normal_equations else 0, _stream_of(b, stream),
                                       ctypes.byref(info)), "l1dm_cg")
+    return x, {f: getattr(info, f) for f, _ in CGInfoT._fields_}
+
+
+class _DeviceView:
+    """A zero-copy torch view of a device buffer the library hands to a callback."""
+
+    def __init__(self, ptr: int, rows: int, cols: int, ld: int):
+        self.__cuda_array_interface__ = {"shape": (rows, cols), "typestr": "<f8",
+                                         "data": (int(ptr), False), "strides": (ld * 8, 8),
+                                         "version": 2}
+
+
+def device_view(ptr: int, rows: int, cols: int, ld: int, device) -> torch.Tensor:
+    return torch.as_tensor(_DeviceView(ptr, rows, cols, ld), device=device)
+
+
+def _callback(apply, n: int, device):
+    """Wrap apply(V, Y, stream) -> None (torch views of the library's buffers; enqueue Y = A V on
+    `stream`) as an l1dm_apply_fn.  Exceptions become a nonzero status (never cross the ABI)."""
+    def cb(user, vptr, ldv, b, yptr, ldy, sptr):
+        try:
+            V = device_view(vptr, n, b, ldv, device)
+            Y = device_view(yptr, n, b, ldy, device)
+            st = torch.cuda.ExternalStream(sptr, device=device) if sptr else \
+                torch.cuda.default_stream(device)
+            with torch.cuda.stream(st):
+                apply(V, Y, st)
+            return 0
+        except Exception:  # noqa: BLE001 — reported as a status through the C ABI
+            import traceback
+            traceback.print_exc()
+            return -4
+    return APPLY_FN(cb)
+
+
+def l1dm_block_krylov_cb(n: int, apply, k: int, Pi: torch.Tensor, depth: int, stream=None):
+    """Block Krylov with a caller-supplied product apply(V, Y, stream) (Y = A V, fp64 n x b
+    views): every dense step in the library; returns (sigma, lam, Z, info dict)."""
+    device = Pi.device
+    Pi = _f64_dev(Pi, "Pi", device).contiguous()
+    b = Pi.shape[1]
+    sigma = torch.empty(k, dtype=torch.float64, device=device)
+    lam = torch.empty(k, dtype=torch.float64, device=device)
+    Z = torch.empty((n, k), dtype=torch.float64, device=device)
+    info = KrylovInfoT()
+    fn = _callback(apply, n, device)
+    with torch.cuda.device(device):
+        _check(load_library().l1dm_block_krylov_cb(n, fn, None, k, b, depth, _ptr(Pi), _ptr(sigma),
+                                                   _ptr(lam), _ptr(Z), k, _stream_of(Pi, stream),
+                                                   ctypes.byref(info)), "l1dm_block_krylov_cb")
+    return sigma, lam, Z, {f: getattr(info, f) for f, _ in KrylovInfoT._fields_}
+
+
+def l1dm_cg_cb(n: int, apply, b: torch.Tensor, *, tol: float = 1e-8, maxit: int = 500,
+               normal_equations: bool = False, stream=None):
+    """CG with a caller-supplied product apply(V, Y, stream); returns (x, info dict)."""
+    device = b.device
+    b = _f64_dev(b, "b", device).reshape(-1).contiguous()
+    x = torch.empty_like(b)
+    info = CGInfoT()
+    fn = _callback(apply, n, device)
+    with torch.cuda.device(device):
+        _check(load_library().l1dm_cg_cb(n, fn, None, _ptr(b), _ptr(x), float(tol), int(maxit),
+                                         1 if normal_equations else 0, _stream_of(b, stream),
+                                         ctypes.byref(info)), "l1dm_cg_cb")
     return x, {f: getattr(info, f) for f, _ in CGInfoT._fields_}

@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <unordered_map>
@@ -2068,24 +2069,18 @@ l1dm_status l1dm_op_apply(const l1dm_operator_t *op, const double *V, int64_t ld
   return op_apply_f64(op, n, V, ldv, b, Y, ldy, zs, yr, s);
 }
 
-l1dm_status l1dm_block_krylov(const l1dm_operator_t *op, int64_t k, int64_t block, int64_t depth,
-                              const double *Pi, double *sigma, double *lam, double *Z,
-                              int64_t ldz, void *stream, l1dm_krylov_info_t *info) {
-  NvtxRange nvtx_("l1dm_block_krylov");
-  g_err.clear();
-  int64_t n = 0;
-  l1dm_status st = op_check(op, &n);
-  if (st != L1DM_OK) return st;
+}  // extern "C"
+
+namespace {
+// Y = A V (n x b fp64 blocks, leading dimensions given), stream-ordered on the core's stream
+using ApplyF64 = std::function<l1dm_status(const double *V, int64_t ldv, int64_t b, double *Y,
+                                           int64_t ldy)>;
+
+l1dm_status krylov_core(int64_t n, const ApplyF64 &apply_f64, int64_t k, int64_t block,
+                        int64_t depth, const double *Pi, double *sigma, double *lam, double *Z,
+                        int64_t ldz, cudaStream_t s, l1dm_krylov_info_t *info) {
+  l1dm_status st = L1DM_OK;  // (arguments checked by the entry points: krylov_args)
   const int64_t b = block, q = depth, Qw = block * depth;
-  if (!Pi || !sigma) return fail(L1DM_EINVAL, "Pi or sigma is NULL");
-  if (k < 1 || b < k || b > 96 || q < 1 || Qw > n || Qw > 4096 || (Z && ldz < k))
-    return fail(L1DM_EINVAL, "krylov k=%lld block=%lld depth=%lld (n=%lld) invalid: need 1 <= k "
-                "<= block <= 96, depth >= 1, block*depth <= min(n, 4096)", (long long)k, (long long)b,
-                (long long)q, (long long)n);
-  for (const void *ptr : {(const void *)Pi, (const void *)sigma, (const void *)lam,
-                          (const void *)Z})
-    if (ptr && !is_device_pointer(ptr)) return fail(L1DM_EINVAL, "krylov buffers must be device memory");
-  cudaStream_t s = (cudaStream_t)stream;
   const int sms = device_sms();
   // scratch: basis, Krylov block, orthogonalisation temporaries, T and its eigenvectors
   const size_t gws = std::max({gemm_workspace(1, Qw, b, n, sms), gemm_workspace(1, b, b, n, sms)});
@@ -2094,8 +2089,6 @@ l1dm_status l1dm_block_krylov(const l1dm_operator_t *op, int64_t k, int64_t bloc
   add((size_t)n * Qw, 8);                    // Qb
   add((size_t)n * b, 8);                     // W
   add((size_t)n * b, 8);                     // Vt
-  add((size_t)n * 2 * b, 4);                 // zs
-  add((size_t)n * 2 * b, 8);                 // yr
   for (int i = 0; i < 4; ++i) add((size_t)b * b, 8);  // G0, G, Gv, S
   add((size_t)b, 8);                         // lamb
   add((size_t)Qw * b, 8);                    // Ct
@@ -2107,8 +2100,6 @@ l1dm_status l1dm_block_krylov(const l1dm_operator_t *op, int64_t k, int64_t bloc
   CUDA_TRY(sc.reserve(bytes));
   double *Qb = sc.take<double>((size_t)n * Qw), *W = sc.take<double>((size_t)n * b);
   double *Vt = sc.take<double>((size_t)n * b);
-  float *zs = sc.take<float>((size_t)n * 2 * b);
-  double *yr = sc.take<double>((size_t)n * 2 * b);
   double *G0 = sc.take<double>(b * b), *G = sc.take<double>(b * b);
   double *Gv = sc.take<double>(b * b), *S = sc.take<double>(b * b);
   double *lamb = sc.take<double>(b), *Ct = sc.take<double>(Qw * b);
@@ -2134,7 +2125,7 @@ l1dm_status l1dm_block_krylov(const l1dm_operator_t *op, int64_t k, int64_t bloc
   auto apply = [&](const double *V, int64_t ldv, double *Y) -> l1dm_status {
     const size_t e0 = evs.size();
     ev();
-    l1dm_status r = op_apply_f64(op, n, V, ldv, b, Y, b, zs, yr, s);
+    l1dm_status r = apply_f64(V, ldv, b, Y, b);
     ev();
     prod_ev.push_back({e0, e0 + 1});
     ++products;
@@ -2224,27 +2215,16 @@ l1dm_status l1dm_block_krylov(const l1dm_operator_t *op, int64_t k, int64_t bloc
   return L1DM_OK;
 }
 
-l1dm_status l1dm_cg(const l1dm_operator_t *op, const double *bvec, double *x, double tol,
-                    int64_t maxit, int normal_equations, void *stream, l1dm_cg_info_t *info) {
-  NvtxRange nvtx_("l1dm_cg");
-  g_err.clear();
-  int64_t n = 0;
-  l1dm_status st = op_check(op, &n);
-  if (st != L1DM_OK) return st;
-  if (!bvec || !x || maxit < 0 || !(tol >= 0.0))
-    return fail(L1DM_EINVAL, "b/x NULL, maxit < 0 or tol invalid");
-  if (!is_device_pointer(bvec) || !is_device_pointer(x))
-    return fail(L1DM_EINVAL, "l1dm_cg takes device b and x");
-  cudaStream_t s = (cudaStream_t)stream;
+l1dm_status cg_core(int64_t n, const ApplyF64 &apply_f64, const double *bvec, double *x,
+                    double tol, int64_t maxit, int normal_equations, cudaStream_t s,
+                    l1dm_cg_info_t *info) {
+  l1dm_status st = L1DM_OK;
   const int nb = cg_dot_blocks();
   Scratch sc(s);
-  CUDA_TRY(sc.reserve(4 * Scratch::bytes_for(n, 8) + Scratch::bytes_for(n * 2, 4) +
-                      Scratch::bytes_for(n * 2, 8) + Scratch::bytes_for(nb, 8) +
+  CUDA_TRY(sc.reserve(4 * Scratch::bytes_for(n, 8) + Scratch::bytes_for(nb, 8) +
                       Scratch::bytes_for(16, 8)));
   double *r = sc.take<double>(n), *p = sc.take<double>(n), *Ap = sc.take<double>(n);
   double *tmp = sc.take<double>(n);
-  float *zs = sc.take<float>(n * 2);
-  double *yr = sc.take<double>(n * 2);
   double *part = sc.take<double>(nb);
   double *stv = sc.take<double>(16);
   double *hflag = nullptr;  // pinned: [chunk parity][conv, it]
@@ -2262,7 +2242,7 @@ l1dm_status l1dm_cg(const l1dm_operator_t *op, const double *bvec, double *x, do
   auto A = [&](const double *v, double *out) -> l1dm_status {
     ++products;
     launches += 2;
-    return op_apply_f64(op, n, v, 1, 1, out, 1, zs, yr, s);
+    return apply_f64(v, 1, 1, out, 1);
   };
   // rhs into r (normal equations: A b), x = 0, p = r
   if (normal_equations) st = A(bvec, r);
@@ -2345,6 +2325,129 @@ l1dm_status l1dm_cg(const l1dm_operator_t *op, const double *bvec, double *x, do
   }
   g_handleless_launches += launches;
   return L1DM_OK;
+}
+
+
+// The fp64 product of an l1dm_operator_t: the hi/lo split through the operator's own product,
+// with scratch for blocks up to bmax columns
+struct OpApply {
+  const l1dm_operator_t *op;
+  int64_t n;
+  cudaStream_t s;
+  Scratch sc;
+  float *zs = nullptr;
+  double *yr = nullptr;
+  int64_t bmax = 0;
+  OpApply(const l1dm_operator_t *o, int64_t n_, cudaStream_t s_) : op(o), n(n_), s(s_), sc(s_) {}
+  cudaError_t reserve(int64_t b) {
+    bmax = b;
+    cudaError_t e = sc.reserve(Scratch::bytes_for((size_t)n * 2 * b, sizeof(float)) +
+                               Scratch::bytes_for((size_t)n * 2 * b, sizeof(double)));
+    if (e != cudaSuccess) return e;
+    zs = sc.take<float>((size_t)n * 2 * b);
+    yr = sc.take<double>((size_t)n * 2 * b);
+    return cudaSuccess;
+  }
+  ApplyF64 fn() {
+    return [this](const double *V, int64_t ldv, int64_t b, double *Y, int64_t ldy) {
+      return op_apply_f64(op, n, V, ldv, b, Y, ldy, zs, yr, s);
+    };
+  }
+};
+
+// a caller-supplied product (l1dm_apply_fn): e.g. a coordinate-sharded partial plus the
+// cross-GPU all-reduce
+ApplyF64 callback_apply(l1dm_apply_fn fn, void *user, cudaStream_t s) {
+  return [fn, user, s](const double *V, int64_t ldv, int64_t b, double *Y, int64_t ldy) {
+    const int rc = fn(user, V, ldv, b, Y, ldy, (void *)s);
+    return rc == 0 ? L1DM_OK : fail(rc < 0 && rc >= L1DM_ENOTSIMPLEX ? (l1dm_status)rc : L1DM_ECUDA,
+                                    "the caller's product callback returned %d", rc);
+  };
+}
+
+l1dm_status krylov_args(int64_t n, int64_t k, int64_t b, int64_t q, const double *Pi,
+                        const double *sigma, const double *lam, const double *Z, int64_t ldz) {
+  if (!Pi || !sigma) return fail(L1DM_EINVAL, "Pi or sigma is NULL");
+  const int64_t Qw = b * q;
+  if (n < 1 || k < 1 || b < k || b > 96 || q < 1 || Qw > n || Qw > 4096 || (Z && ldz < k))
+    return fail(L1DM_EINVAL, "krylov k=%lld block=%lld depth=%lld (n=%lld) invalid: need 1 <= k "
+                "<= block <= 96, depth >= 1, block*depth <= min(n, 4096)", (long long)k, (long long)b,
+                (long long)q, (long long)n);
+  for (const void *ptr : {(const void *)Pi, (const void *)sigma, (const void *)lam,
+                          (const void *)Z})
+    if (ptr && !is_device_pointer(ptr)) return fail(L1DM_EINVAL, "krylov buffers must be device memory");
+  return L1DM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+l1dm_status l1dm_block_krylov(const l1dm_operator_t *op, int64_t k, int64_t block, int64_t depth,
+                              const double *Pi, double *sigma, double *lam, double *Z,
+                              int64_t ldz, void *stream, l1dm_krylov_info_t *info) {
+  NvtxRange nvtx_("l1dm_block_krylov");
+  g_err.clear();
+  int64_t n = 0;
+  l1dm_status st = op_check(op, &n);
+  if (st != L1DM_OK) return st;
+  st = krylov_args(n, k, block, depth, Pi, sigma, lam, Z, ldz);
+  if (st != L1DM_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  OpApply oa(op, n, s);
+  CUDA_TRY(oa.reserve(block));
+  return krylov_core(n, oa.fn(), k, block, depth, Pi, sigma, lam, Z, ldz, s, info);
+}
+
+l1dm_status l1dm_block_krylov_cb(int64_t n, l1dm_apply_fn apply, void *user, int64_t k,
+                                 int64_t block, int64_t depth, const double *Pi, double *sigma,
+                                 double *lam, double *Z, int64_t ldz, void *stream,
+                                 l1dm_krylov_info_t *info) {
+  NvtxRange nvtx_("l1dm_block_krylov_cb");
+  g_err.clear();
+  if (!apply) return fail(L1DM_EINVAL, "apply callback is NULL");
+  int dev = 0;
+  l1dm_status st = check_arch(&dev);
+  if (st != L1DM_OK) return st;
+  st = krylov_args(n, k, block, depth, Pi, sigma, lam, Z, ldz);
+  if (st != L1DM_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  return krylov_core(n, callback_apply(apply, user, s), k, block, depth, Pi, sigma, lam, Z, ldz,
+                     s, info);
+}
+
+l1dm_status l1dm_cg(const l1dm_operator_t *op, const double *bvec, double *x, double tol,
+                    int64_t maxit, int normal_equations, void *stream, l1dm_cg_info_t *info) {
+  NvtxRange nvtx_("l1dm_cg");
+  g_err.clear();
+  int64_t n = 0;
+  l1dm_status st = op_check(op, &n);
+  if (st != L1DM_OK) return st;
+  if (!bvec || !x || maxit < 0 || !(tol >= 0.0))
+    return fail(L1DM_EINVAL, "b/x NULL, maxit < 0 or tol invalid");
+  if (!is_device_pointer(bvec) || !is_device_pointer(x))
+    return fail(L1DM_EINVAL, "l1dm_cg takes device b and x");
+  cudaStream_t s = (cudaStream_t)stream;
+  OpApply oa(op, n, s);
+  CUDA_TRY(oa.reserve(1));
+  return cg_core(n, oa.fn(), bvec, x, tol, maxit, normal_equations, s, info);
+}
+
+l1dm_status l1dm_cg_cb(int64_t n, l1dm_apply_fn apply, void *user, const double *bvec, double *x,
+                       double tol, int64_t maxit, int normal_equations, void *stream,
+                       l1dm_cg_info_t *info) {
+  NvtxRange nvtx_("l1dm_cg_cb");
+  g_err.clear();
+  if (!apply || !bvec || !x || n < 1 || maxit < 0 || !(tol >= 0.0))
+    return fail(L1DM_EINVAL, "apply/b/x NULL, n < 1, maxit < 0 or tol invalid");
+  int dev = 0;
+  l1dm_status st = check_arch(&dev);
+  if (st != L1DM_OK) return st;
+  if (!is_device_pointer(bvec) || !is_device_pointer(x))
+    return fail(L1DM_EINVAL, "l1dm_cg_cb takes device b and x");
+  cudaStream_t s = (cudaStream_t)stream;
+  return cg_core(n, callback_apply(apply, user, s), bvec, x, tol, maxit, normal_equations, s,
+                 info);
 }
 
 }  // extern "C"

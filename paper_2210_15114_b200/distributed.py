@@ -103,6 +103,7 @@ class ShardedL1DM:
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         d = X.shape[1]
+        self.n, self.p = X.shape[0], p
         self.k_begin, self.k_end = k_range if k_range is not None else shard_range(
             d, self.rank, self.world)
         if local_matvec is None and p % 2 == 1 and p != 1:  # odd l_p^p (Thm. odd_p): A = sum_k A^(k)
@@ -237,6 +238,52 @@ class ShardedL1DM:
                 self._peer = None
                 raise
         return Y
+
+    # ---- matrix-free consumers over the shards ("needs all-reduce")
+    def _fp64_product(self, V: torch.Tensor, Y: torch.Tensor, stream) -> None:
+        """Y = A V for an fp64 block on every rank: this rank's partial A^(K_g) V through the
+        library (hi/lo split), then an all-reduce (sum over the coordinate shards)."""
+        if self.handle is None:
+            part = torch.zeros_like(Y)
+        else:
+            part = binding.l1dm_op_apply(self._operator(), V, stream=stream)
+        if self.world > 1:
+            dist.all_reduce(part, op=dist.ReduceOp.SUM, group=self.group)
+        Y.copy_(part)
+
+    def _operator(self):
+        if getattr(self, "_op", None) is None:
+            if self._prepare is not binding.l1dm_prepare:
+                raise ValueError("the consumers need the library's handle on every rank")
+            p = getattr(self, "p", 1)
+            self._op = binding.Operator.sorted(self.handle, p)
+        return self._op
+
+    def krylov(self, k: int, *, block: Optional[int] = None, depth: Optional[int] = None,
+               eps: float = 0.5, seed: int = 0):
+        """Top-k singular values of A (Thm. musco) with the products sharded over
+        the ranks and all-reduced; every dense step in the library, identical on every rank
+        (the same start block from the seed, deterministic kernels, all-reduced products)."""
+        from .krylov import KrylovResult, krylov_params
+        n = self.n
+        b, q = krylov_params(n, k, block, depth, eps)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        gen = torch.Generator(device=dev).manual_seed(seed)
+        Pi = torch.randn((n, b), generator=gen, dtype=torch.float64, device=dev)
+        sigma, lam, Z, info = binding.l1dm_block_krylov_cb(
+            n, lambda V, Y, st: self._fp64_product(V, Y, st), k, Pi, q)
+        return KrylovResult(sigma=sigma, Z=Z, lam=lam, products=info["products"],
+                            columns=info["columns"], info=info)
+
+    def cg(self, b: torch.Tensor, *, tol: float = 1e-8, maxit: int = 500,
+           normal_equations: bool = False):
+        """Conjugate gradients (Thm. linear_system) on the sharded operator."""
+        from .krylov import CGResult
+        x, info = binding.l1dm_cg_cb(self.n, lambda V, Y, st: self._fp64_product(V, Y, st),
+                                     b.to(torch.float64), tol=tol, maxit=maxit,
+                                     normal_equations=normal_equations)
+        return CGResult(x=x, iterations=int(info["iterations"]), residual=float(info["residual"]),
+                        converged=bool(info["converged"]), products=int(info["products"]))
 
     def _collective(self, T, root):
         if root is None:
