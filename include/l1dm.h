@@ -418,8 +418,10 @@ L1DM_API l1dm_status l1dm_set_workspace_limit(l1dm_handle h, size_t bytes);
  *   GATHER  the scan stores U = v*P - Q per (coordinate, sorted row) in a workspace and a
  *           per-point pass gathers U at rank_k(i) for every k (Y written once, no atomics);
  *   SCATTER the scan adds 2U straight into Y[perm_k(r)] with fp64 L2 atomics, one column
- *           block of Y at a time (no U workspace, no rank gather; the order of the d terms
- *           of y_i then varies run to run at the ulp level on float data — DESIGN.md R16).
+ *           block of Y at a time (no U workspace, no rank gather).  For m > 1 the block
+ *           accumulator is 64-bit fixed point at a per-query scale bounded from Z and the
+ *           sorted values, so Y is bitwise reproducible; for m = 1 the fp64 reductions'
+ *           order varies run to run at the ulp level on float data (R16).
  *   RUNS    tie-heavy data only (every prepared coordinate takes <= 256 distinct values,
  *           detected by prepare): Alg. 2 over the distinct values — per coordinate the run
  *           sums of Z by fp64 L2 reductions in point order, a prefix over the runs, then each

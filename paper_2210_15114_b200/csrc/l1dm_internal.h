@@ -181,7 +181,8 @@ void launch_totals(const double *segtot, int64_t ld_seg, int64_t dl, int64_t mc,
 // (S == nullptr: Y[i][c] = Yt[i][c]).
 void launch_block_out(const double *yt, int mb, int64_t mc, const double *hsum, const double *S,
                       const double *g, double *Y, int64_t ldy, int64_t i0, int64_t i1,
-                      cudaStream_t s, const PeerDst *pd = nullptr, int64_t pc0 = 0);
+                      cudaStream_t s, const PeerDst *pd = nullptr, int64_t pc0 = 0,
+                      const double *fx = nullptr);
 // (pd: the rows go to their owners' inbox slots at column pc0 instead of Y.)
 // segtot: per-coordinate rows of ld_seg doubles ((S, T) per column); zs: m == 1 only, kc x ldn
 // floats (z in sorted order between the reduce and apply passes).
@@ -200,7 +201,12 @@ void launch_scan(const QueryPlan &p, const uint32_t *perm, const float *sval, in
 void launch_scan_seq(const QueryPlan &p, int lp, const uint32_t *perm, const float *sval,
                      int64_t ldn, int64_t n, const float *zt, int64_t mc, double *out,
                      int64_t ldo, bool store, int64_t kcc, double *agg, double *segtot,
-                     int64_t ld_seg, int phase, cudaStream_t s, int64_t agg_ld = 0);
+                     int64_t ld_seg, int phase, cudaStream_t s, int64_t agg_ld = 0,
+                     const double *fx = nullptr);
+// (fx: lp = 1 apply in deterministic fixed point — out is an int64 block, fx = {2^F, 2^-F}.)
+// fx = {2^F, 2^-F} for the query: F from a bound on |Yt| (column |z| sums and the shard's |x|).
+void launch_fx_scale(const float *Z, int64_t ldz, int64_t n, int64_t m, const uint32_t *sval_bits,
+                     int64_t ldn, int64_t dl, double *colabs, double *fx, cudaStream_t s);
 // (agg_ld: the apply's stride between tiles in agg, 0 = the block's own payload (lp+1) mb.)
 // P = 1, m <= 256: tile totals of all m columns in one pass over full Z rows + the prefix
 // (agg: kcc x tiles x 2m, segtot rows of 2m).  The per-block apply then reads agg + 2 c0 with

@@ -612,7 +612,11 @@ struct SeqCfg {
   static constexpr int CH = MB * 4 >= 16 ? 16 : MB * 4;  // bytes per cp.async of a Z row
   static constexpr size_t SMEM = (size_t)G * GS * 4 + (size_t)G * PS * 4 * 2;
 };
-enum { SEQ_REDUCE = 0, SEQ_APPLY_RED = 1, SEQ_APPLY_STORE = 2 };
+enum { SEQ_REDUCE = 0, SEQ_APPLY_RED = 1, SEQ_APPLY_STORE = 2, SEQ_APPLY_FX = 3 };
+// SEQ_APPLY_FX (P = 1): the 2U values are added into Yt as 64-bit fixed-point integers,
+// q = rint(2U 2^F) with the query's scale 2^F = fx[0] (l1dm_fx_scale below), by integer L2
+// reductions — integer addition is associative, so Yt (and Y) are bitwise reproducible whatever
+// the order of the reductions (R16); the block write-out scales back by fx[1] = 2^-F.
 
 // c_t = C(P, t) (-1)^t
 template <int P>
@@ -627,7 +631,8 @@ __global__ void __launch_bounds__(256)
     k5_scan_seq(const uint32_t *__restrict__ perm, const float *__restrict__ sval, int64_t ldn,
                 int64_t n, const float *__restrict__ zt, int64_t mc, double *__restrict__ out,
                 int64_t ldo, int64_t nseg, int64_t tiles_per_seg, double *__restrict__ agg,
-                int64_t agg_ld, const double *__restrict__ segtot, int64_t ld_seg) {
+                int64_t agg_ld, const double *__restrict__ segtot, int64_t ld_seg,
+                const double *__restrict__ fx) {
   using C = SeqCfg<MB, P>;
   constexpr int NT = C::NT, NW = C::NW, ITEMS = C::ITEMS, R = C::R, GPW = C::GPW, GS = C::GS,
                 PS = C::PS, K = C::K, NP = C::NP, CH = C::CH, CPR = MB * 4 / CH;
@@ -726,6 +731,8 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int q = 0; q < K; ++q) M[q] += s_wt[ww * NP + K * c + q];
     }
+    double fxs = 0.0;  // SEQ_APPLY_FX: the fixed-point scale 2^F
+    if constexpr (MODE == SEQ_APPLY_FX) fxs = __ldg(fx);
     double cT[K];  // P > 1: c_t T_t, the coordinate's totals of this column (prefix pass)
 #pragma unroll
     for (int q = 0; q < K; ++q)
@@ -753,6 +760,12 @@ __global__ void __launch_bounds__(256)
         }
         if constexpr (MODE == SEQ_APPLY_RED) {
           red_add_f64(out + (int64_t)pg[j] * ldo + c, val, pol_keep);
+        } else if constexpr (MODE == SEQ_APPLY_FX) {
+          const unsigned long long q = (unsigned long long)__double2ll_rn(val * fxs);
+          asm volatile("red.global.add.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(
+                           reinterpret_cast<unsigned long long *>(out) + (int64_t)pg[j] * ldo + c),
+                       "l"(q), "l"(pol_keep)
+                       : "memory");
         } else {
           __stcs(out + (kk * n + row0 + rl0 + j) * ldo + c, val);  // U[kk][r][c]
         }
@@ -792,7 +805,7 @@ template <int MB, int P>
 static void launch_seq_t(const QueryPlan &p, const uint32_t *perm, const float *sval, int64_t ldn,
                          int64_t n, const float *zt, int64_t mc, double *out, int64_t ldo,
                          bool store, int64_t kcc, double *agg, int64_t agg_ld, double *segtot,
-                         int64_t ld_seg, int phase, cudaStream_t s) {
+                         int64_t ld_seg, int phase, cudaStream_t s, const double *fx) {
   using C = SeqCfg<MB, P>;
   static bool attr = false;
   if (!attr) {
@@ -802,32 +815,38 @@ static void launch_seq_t(const QueryPlan &p, const uint32_t *perm, const float *
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     cudaFuncSetAttribute(k5_scan_seq<MB, SEQ_APPLY_STORE, P>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (P == 1)
+      cudaFuncSetAttribute(k5_scan_seq<MB, SEQ_APPLY_FX, P>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     attr = true;
   }
   const int64_t total = kcc * p.tiles_per_segment;
   if (phase != 1) {
     k5_scan_seq<MB, SEQ_REDUCE, P><<<(unsigned)total, C::NT, C::SMEM, s>>>(
         perm, sval, ldn, n, zt, mc, out, ldo, kcc, p.tiles_per_segment, agg, C::NP, segtot,
-        ld_seg);
+        ld_seg, nullptr);
     const int64_t warps = kcc * C::NP;
     k5_seq_prefix<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(agg, kcc, p.tiles_per_segment,
                                                               C::NP, C::K * mc, segtot, ld_seg);
   }
   if (phase != 0) {
-    auto kern = store ? k5_scan_seq<MB, SEQ_APPLY_STORE, P> : k5_scan_seq<MB, SEQ_APPLY_RED, P>;
+    auto kern = store ? k5_scan_seq<MB, SEQ_APPLY_STORE, P>
+                      : (P == 1 && fx) ? k5_scan_seq<MB, SEQ_APPLY_FX, P>
+                                       : k5_scan_seq<MB, SEQ_APPLY_RED, P>;
     kern<<<(unsigned)total, C::NT, C::SMEM, s>>>(perm, sval, ldn, n, zt, mc, out, ldo, kcc,
                                                  p.tiles_per_segment, agg,
-                                                 agg_ld > 0 ? agg_ld : C::NP, segtot, ld_seg);
+                                                 agg_ld > 0 ? agg_ld : C::NP, segtot, ld_seg, fx);
   }
 }
 
 void launch_scan_seq(const QueryPlan &p, int lp, const uint32_t *perm, const float *sval,
                      int64_t ldn, int64_t n, const float *zt, int64_t mc, double *out,
                      int64_t ldo, bool store, int64_t kcc, double *agg, double *segtot,
-                     int64_t ld_seg, int phase, cudaStream_t s, int64_t agg_ld) {
+                     int64_t ld_seg, int phase, cudaStream_t s, int64_t agg_ld,
+                     const double *fx) {
 #define L1DM_SEQ(MB, P)                                                                         \
   launch_seq_t<MB, P>(p, perm, sval, ldn, n, zt, mc, out, ldo, store, kcc, agg, agg_ld, segtot, \
-                      ld_seg, phase, s)
+                      ld_seg, phase, s, fx)
 #define L1DM_SEQ_P(MB)                         \
   switch (lp) {                                \
     case 1: L1DM_SEQ(MB, 1); break;            \
@@ -1252,12 +1271,15 @@ template <bool PUSH>
 __global__ void __launch_bounds__(256)
     k9_block_out(const double *__restrict__ yt, int mb, int64_t mc, const double *__restrict__ hsum,
                  const double *__restrict__ S, const double *__restrict__ g, double *__restrict__ Y,
-                 int64_t ldy, int64_t i0, int64_t i1, PeerDst pd, int64_t pc0) {
+                 int64_t ldy, int64_t i0, int64_t i1, PeerDst pd, int64_t pc0,
+                 const double *__restrict__ fx) {
   const int64_t total = (i1 - i0) * mc;
+  const double inv = fx ? __ldg(fx + 1) : 0.0;  // fixed-point Yt (SEQ_APPLY_FX): 2^-F
   for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * 256) {
     const int64_t i = i0 + e / mc, c = e - (e / mc) * mc;
-    const double v = yt[i * mb + c];
+    const double v = fx ? (double)reinterpret_cast<const long long *>(yt)[i * mb + c] * inv
+                        : yt[i * mb + c];
     const double out = S ? v + fma(-hsum[i], S[c], g[c]) : v;
     if constexpr (PUSH) {
       peer_row(pd, i)[pc0 + c] = out;
@@ -1270,16 +1292,75 @@ __global__ void __launch_bounds__(256)
 
 void launch_block_out(const double *yt, int mb, int64_t mc, const double *hsum, const double *S,
                       const double *g, double *Y, int64_t ldy, int64_t i0, int64_t i1,
-                      cudaStream_t s, const PeerDst *pd, int64_t pc0) {
+                      cudaStream_t s, const PeerDst *pd, int64_t pc0, const double *fx) {
   if (i1 <= i0) return;
   int64_t blocks = ((i1 - i0) * mc + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (pd && pd->world > 0)
     k9_block_out<true><<<(unsigned)blocks, 256, 0, s>>>(yt, mb, mc, hsum, S, g, Y, ldy, i0, i1,
-                                                        *pd, pc0);
+                                                        *pd, pc0, fx);
   else
     k9_block_out<false><<<(unsigned)blocks, 256, 0, s>>>(yt, mb, mc, hsum, S, g, Y, ldy, i0, i1,
-                                                         PeerDst{}, 0);
+                                                         PeerDst{}, 0, fx);
+}
+
+// The fixed-point scale of a query (SEQ_APPLY_FX).  Every term 2U^k_r = 2 (v_r P_r - Q_r)
+// satisfies |2U| <= 4 max|v| sum_j |z_j| (|P_r| and |Q_r / max|v|| are partial sums of |z|),
+// so a point's block row, a sum of dl such terms, is below B = 4 dl Mx Sz with Mx the largest
+// |x| of the shard's coordinates (the ends of the sorted rows) and Sz the largest column sum of
+// |z| (k8b_colabs; x 1.0001 for its own rounding).  F = 61 - ceil(log2 B) keeps every partial
+// sum below 2^61 in magnitude: fx[0] = 2^F, fx[1] = 2^-F.  Each term is rounded once to 2^-F
+// (<= 2^-F-1 absolute; relative to B about dl 2^-63), the sum is exact.
+__global__ void __launch_bounds__(256)
+    k8b_colabs(const float *__restrict__ Z, int64_t ldz, int64_t n, int64_t m,
+               double *__restrict__ colabs) {
+  if (m <= 256) {  // 256 / m rows per CTA step, one column per thread
+    const int64_t c = threadIdx.x % m;
+    const int64_t rpb = 256 / m;
+    const int64_t r0 = threadIdx.x / m;
+    if (r0 >= rpb) return;
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * rpb + r0; i < n; i += (int64_t)gridDim.x * rpb)
+      acc += fabs((double)__ldg(Z + i * ldz + c));
+    atomicAdd(colabs + c, acc);  // a bound only: the order of these additions does not matter
+    return;
+  }
+  for (int64_t c = threadIdx.x; c < m; c += 256) {  // wide blocks: one row per CTA step
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x; i < n; i += gridDim.x) acc += fabs((double)__ldg(Z + i * ldz + c));
+    atomicAdd(colabs + c, acc);
+  }
+}
+
+__global__ void k8c_fx_scale(const double *__restrict__ colabs, int64_t m,
+                             const uint32_t *__restrict__ sval_bits, int64_t ldn, int64_t n,
+                             int64_t dl, double *__restrict__ fx) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double sz = 0.0, mx = 0.0;
+  for (int64_t c = 0; c < m; ++c) sz = fmax(sz, colabs[c]);
+  for (int64_t k = 0; k < dl; ++k) {
+    mx = fmax(mx, fabs((double)__uint_as_float(sval_bits[k * ldn])));
+    mx = fmax(mx, fabs((double)__uint_as_float(sval_bits[k * ldn + n - 1])));
+  }
+  const double B = 4.0 * (double)dl * mx * sz * 1.0001;
+  int F = 60;
+  if (B > 0.0 && isfinite(B)) {
+    F = 61 - ilogb(B) - 1;  // 2^ilogb(B) <= B < 2^(ilogb+1): B < 2^(61 - F)
+    if (F > 60) F = 60;
+    if (F < -1000) F = -1000;
+  }
+  fx[0] = ldexp(1.0, F);
+  fx[1] = ldexp(1.0, -F);
+}
+
+void launch_fx_scale(const float *Z, int64_t ldz, int64_t n, int64_t m, const uint32_t *sval_bits,
+                     int64_t ldn, int64_t dl, double *colabs, double *fx, cudaStream_t s) {
+  cudaMemsetAsync(colabs, 0, (size_t)m * sizeof(double), s);
+  int64_t blocks = 148 * 4;
+  const int64_t rpb = m <= 256 ? 256 / m : 1;
+  if (blocks * rpb > n) blocks = (n + rpb - 1) / rpb;
+  k8b_colabs<<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(Z, ldz, n, m, colabs);
+  k8c_fx_scale<<<1, 32, 0, s>>>(colabs, m, sval_bits, ldn, n, dl, fx);
 }
 
 // ------------------------------------------------------------------ runs mode
