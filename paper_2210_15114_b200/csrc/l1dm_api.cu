@@ -244,7 +244,7 @@ struct l1dm_ctx {
   DevBuf<float> zs;            // m == 1: gathered z in sorted order (reduce -> apply pass)
   DevBuf<float> zt;            // scatter mode, m > 1: column-block-major copy of Z
   DevBuf<double> yt;           // scatter mode, m > 1: one column block's accumulator (n x mb)
-  DevBuf<double> fxbuf;        // scatter mode, m > 1: column |z| sums (m) + fixed-point scale (2)
+  DevBuf<double> fxbuf;        // scatter mode, m > 1: fixed-point scales (2m) + their scratch
   DevBuf<unsigned> ctr;        // [0] colsum done counter, [1] timeout flag, [2..] scan tickets
   size_t ws_limit = 0;
   int mode = 0;  // L1DM_MODE_*
@@ -860,11 +860,11 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
     // deterministic accumulation (R16): the block accumulator Yt holds 64-bit fixed
     // point at a per-query scale from a bound on |Yt|; integer reductions are associative, so Y
     // is bitwise reproducible run to run
-    CUDA_TRY(h->fxbuf.ensure((size_t)m + 2, false, s));
-    double *fx = h->fxbuf.p + m;
+    CUDA_TRY(h->fxbuf.ensure(2 * (size_t)m + fx_scale_part_doubles(m), false, s));
+    double *fx = h->fxbuf.p;
     {
       TimedScope ts(h, kColsums, s);
-      launch_fx_scale(Z, ldz, h->n, m, h->sval_bits.p, h->ldn, h->dl, h->fxbuf.p, fx, s);
+      launch_fx_scale(Z, ldz, h->n, m, h->sval_bits.p, h->ldn, h->dl, h->fxbuf.p + 2 * m, fx, s);
       h->kernel_launches += 2;
     }
     for (int cb = 0; cb < p.col_blocks; ++cb) {
@@ -885,7 +885,7 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
         CUDA_TRY(cudaMemsetAsync(h->yt.p, 0, (size_t)h->n * p.mb * sizeof(double), s));
         launch_scan_seq(p, 1, h->perm.p, sval, h->ldn, h->n, ztb, mc, h->yt.p, p.mb, false,
                         h->dl, all ? h->agg.p + 2 * c0 : h->agg.p, h->part.p + 2 * c0, 2 * m, 1,
-                        s, all ? 2 * m : 0, fx);
+                        s, all ? 2 * m : 0, fx + c0);
         h->kernel_launches++;  // apply
         h->launches[kAcc]++;
         if (h->timing) h->acc_pairs += h->n * h->dl;
@@ -896,14 +896,14 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
         const int64_t nb = last ? nblocks : 1;
         if (blocked) {
           launch_block_out(h->yt.p, p.mb, mc, h->hsum.p, h->Sg.p + c0, h->Sg.p + m + c0,
-                           Y + (size_t)cb * h->n * p.mb, p.mb, 0, h->n, s, nullptr, 0, fx);
+                           Y + (size_t)cb * h->n * p.mb, p.mb, 0, h->n, s, nullptr, 0, fx + m + c0);
           if (events && events[cb]) CUDA_TRY(cudaEventRecord((cudaEvent_t)events[cb], s));
         }
         for (int64_t b = 0; !blocked && b < nb; ++b) {
           int64_t i0 = 0, i1 = h->n;
           if (last) block_range(b, i0, i1);
           launch_block_out(h->yt.p, p.mb, mc, h->hsum.p, h->Sg.p + c0, h->Sg.p + m + c0, Y + c0,
-                           ldy, i0, i1, s, pd, c0, fx);
+                           ldy, i0, i1, s, pd, c0, fx + m + c0);
           if (last && events && events[b]) CUDA_TRY(cudaEventRecord((cudaEvent_t)events[b], s));
         }
         h->kernel_launches += 1 + nb;  // totals, block out(s)

@@ -203,10 +203,14 @@ void launch_scan_seq(const QueryPlan &p, int lp, const uint32_t *perm, const flo
                      int64_t ldo, bool store, int64_t kcc, double *agg, double *segtot,
                      int64_t ld_seg, int phase, cudaStream_t s, int64_t agg_ld = 0,
                      const double *fx = nullptr);
-// (fx: lp = 1 apply in deterministic fixed point — out is an int64 block, fx = {2^F, 2^-F}.)
-// fx = {2^F, 2^-F} for the query: F from a bound on |Yt| (column |z| sums and the shard's |x|).
+// (fx: lp = 1 apply in deterministic fixed point — out is an int64 block, fx = the block's
+//  per-column scales 2^F_c.)
+// fx[c] = 2^F_c, fx[m + c] = 2^-F_c for the query: F_c from a bound on column c of Yt (the
+// column's |z| sum and the shard's |x|), computed in a fixed order; part holds
+// fx_scale_part_doubles(m) doubles of scratch.
+size_t fx_scale_part_doubles(int64_t m);
 void launch_fx_scale(const float *Z, int64_t ldz, int64_t n, int64_t m, const uint32_t *sval_bits,
-                     int64_t ldn, int64_t dl, double *colabs, double *fx, cudaStream_t s);
+                     int64_t ldn, int64_t dl, double *part, double *fx, cudaStream_t s);
 // (agg_ld: the apply's stride between tiles in agg, 0 = the block's own payload (lp+1) mb.)
 // P = 1, m <= 256: tile totals of all m columns in one pass over full Z rows + the prefix
 // (agg: kcc x tiles x 2m, segtot rows of 2m).  The per-block apply then reads agg + 2 c0 with

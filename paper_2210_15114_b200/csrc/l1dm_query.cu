@@ -614,9 +614,10 @@ struct SeqCfg {
 };
 enum { SEQ_REDUCE = 0, SEQ_APPLY_RED = 1, SEQ_APPLY_STORE = 2, SEQ_APPLY_FX = 3 };
 // SEQ_APPLY_FX (P = 1): the 2U values are added into Yt as 64-bit fixed-point integers,
-// q = rint(2U 2^F) with the query's scale 2^F = fx[0] (l1dm_fx_scale below), by integer L2
-// reductions — integer addition is associative, so Yt (and Y) are bitwise reproducible whatever
-// the order of the reductions (R16); the block write-out scales back by fx[1] = 2^-F.
+// q = rint(2U 2^F_c) with column c's scale 2^F_c = fx[c] (launch_fx_scale below; fx points at
+// the block's first column), by integer L2 reductions — integer addition is associative, so Yt
+// (and Y) are bitwise reproducible whatever the order of the reductions (R16); the
+// block write-out scales back by 2^-F_c.
 
 // c_t = C(P, t) (-1)^t
 template <int P>
@@ -731,8 +732,8 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int q = 0; q < K; ++q) M[q] += s_wt[ww * NP + K * c + q];
     }
-    double fxs = 0.0;  // SEQ_APPLY_FX: the fixed-point scale 2^F
-    if constexpr (MODE == SEQ_APPLY_FX) fxs = __ldg(fx);
+    double fxs = 0.0;  // SEQ_APPLY_FX: this column's fixed-point scale 2^F_c
+    if constexpr (MODE == SEQ_APPLY_FX) fxs = c < mc ? __ldg(fx + c) : 0.0;
     double cT[K];  // P > 1: c_t T_t, the coordinate's totals of this column (prefix pass)
 #pragma unroll
     for (int q = 0; q < K; ++q)
@@ -1274,11 +1275,11 @@ __global__ void __launch_bounds__(256)
                  int64_t ldy, int64_t i0, int64_t i1, PeerDst pd, int64_t pc0,
                  const double *__restrict__ fx) {
   const int64_t total = (i1 - i0) * mc;
-  const double inv = fx ? __ldg(fx + 1) : 0.0;  // fixed-point Yt (SEQ_APPLY_FX): 2^-F
   for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * 256) {
     const int64_t i = i0 + e / mc, c = e - (e / mc) * mc;
-    const double v = fx ? (double)reinterpret_cast<const long long *>(yt)[i * mb + c] * inv
+    // fixed-point Yt (SEQ_APPLY_FX): fx = the block's inverse scales 2^-F_c
+    const double v = fx ? (double)reinterpret_cast<const long long *>(yt)[i * mb + c] * __ldg(fx + c)
                         : yt[i * mb + c];
     const double out = S ? v + fma(-hsum[i], S[c], g[c]) : v;
     if constexpr (PUSH) {
@@ -1304,63 +1305,87 @@ void launch_block_out(const double *yt, int mb, int64_t mc, const double *hsum, 
                                                          PeerDst{}, 0, fx);
 }
 
-// The fixed-point scale of a query (SEQ_APPLY_FX).  Every term 2U^k_r = 2 (v_r P_r - Q_r)
-// satisfies |2U| <= 4 max|v| sum_j |z_j| (|P_r| and |Q_r / max|v|| are partial sums of |z|),
-// so a point's block row, a sum of dl such terms, is below B = 4 dl Mx Sz with Mx the largest
-// |x| of the shard's coordinates (the ends of the sorted rows) and Sz the largest column sum of
-// |z| (k8b_colabs; x 1.0001 for its own rounding).  F = 61 - ceil(log2 B) keeps every partial
-// sum below 2^61 in magnitude: fx[0] = 2^F, fx[1] = 2^-F.  Each term is rounded once to 2^-F
-// (<= 2^-F-1 absolute; relative to B about dl 2^-63), the sum is exact.
+// The fixed-point scales of a query (SEQ_APPLY_FX), one per column c.  Every term
+// 2U^k_r = 2 (v_r P_r - Q_r) satisfies |2U^k| <= 4 Mx_k Sz_c (|P_r| and |Q_r| / Mx_k are partial
+// sums of |z|), Mx_k the largest |x| of coordinate k (the ends of its sorted row) and Sz_c the
+// column sum of |z|; a point's block row, a sum over the dl coordinates, stays below
+// B_c = 4 Sz_c sum_k Mx_k (x 1.0001 for the bound's own rounding).  F_c = 61 - ceil(log2 B_c)
+// keeps every partial sum below 2^61 in magnitude: fx[c] = 2^F_c, fx[m + c] = 2^-F_c.  Each
+// term is rounded once to 2^-F_c (<= 2^-(F_c+1) absolute, about 2^-63 B_c), the sum is exact.
+// The scale itself must not depend on the order of any floating-point sum (else F_c could flip
+// at a power of two from run to run): k8b writes per-CTA partial sums (its row lanes folded in
+// order), k8c adds them in CTA order.
 __global__ void __launch_bounds__(256)
     k8b_colabs(const float *__restrict__ Z, int64_t ldz, int64_t n, int64_t m,
-               double *__restrict__ colabs) {
+               double *__restrict__ part) {
   if (m <= 256) {  // 256 / m rows per CTA step, one column per thread
+    __shared__ double s_acc[256];
     const int64_t c = threadIdx.x % m;
     const int64_t rpb = 256 / m;
     const int64_t r0 = threadIdx.x / m;
-    if (r0 >= rpb) return;
     double acc = 0.0;
-    for (int64_t i = (int64_t)blockIdx.x * rpb + r0; i < n; i += (int64_t)gridDim.x * rpb)
-      acc += fabs((double)__ldg(Z + i * ldz + c));
-    atomicAdd(colabs + c, acc);  // a bound only: the order of these additions does not matter
+    if (r0 < rpb)
+      for (int64_t i = (int64_t)blockIdx.x * rpb + r0; i < n; i += (int64_t)gridDim.x * rpb)
+        acc += fabs((double)__ldg(Z + i * ldz + c));
+    s_acc[threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.x < m) {  // the CTA's row lanes, folded in order
+      for (int64_t r = 1; r < rpb; ++r) acc += s_acc[r * m + threadIdx.x];
+      part[(int64_t)blockIdx.x * m + c] = acc;
+    }
     return;
   }
   for (int64_t c = threadIdx.x; c < m; c += 256) {  // wide blocks: one row per CTA step
     double acc = 0.0;
     for (int64_t i = blockIdx.x; i < n; i += gridDim.x) acc += fabs((double)__ldg(Z + i * ldz + c));
-    atomicAdd(colabs + c, acc);
+    part[(int64_t)blockIdx.x * m + c] = acc;
   }
 }
 
-__global__ void k8c_fx_scale(const double *__restrict__ colabs, int64_t m,
-                             const uint32_t *__restrict__ sval_bits, int64_t ldn, int64_t n,
-                             int64_t dl, double *__restrict__ fx) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double sz = 0.0, mx = 0.0;
-  for (int64_t c = 0; c < m; ++c) sz = fmax(sz, colabs[c]);
-  for (int64_t k = 0; k < dl; ++k) {
-    mx = fmax(mx, fabs((double)__uint_as_float(sval_bits[k * ldn])));
-    mx = fmax(mx, fabs((double)__uint_as_float(sval_bits[k * ldn + n - 1])));
+__global__ void __launch_bounds__(256)
+    k8c_fx_scale(const double *__restrict__ part, int64_t nparts, int64_t m,
+                 const uint32_t *__restrict__ sval_bits, int64_t ldn, int64_t n, int64_t dl,
+                 double *__restrict__ fx) {
+  __shared__ double s_mx;
+  if (threadIdx.x < 32) {  // sum_k Mx_k, warp lanes over k, folded in a fixed order
+    double mx = 0.0;
+    for (int64_t k = threadIdx.x; k < dl; k += 32)
+      mx += fmax(fabs((double)__uint_as_float(sval_bits[k * ldn])),
+                 fabs((double)__uint_as_float(sval_bits[k * ldn + n - 1])));
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) mx += __shfl_xor_sync(0xFFFFFFFFu, mx, off);
+    if (threadIdx.x == 0) s_mx = mx;
   }
-  const double B = 4.0 * (double)dl * mx * sz * 1.0001;
-  int F = 60;
-  if (B > 0.0 && isfinite(B)) {
-    F = 61 - ilogb(B) - 1;  // 2^ilogb(B) <= B < 2^(ilogb+1): B < 2^(61 - F)
-    if (F > 60) F = 60;
-    if (F < -1000) F = -1000;
+  __syncthreads();
+  for (int64_t c = (int64_t)blockIdx.x * 256 + threadIdx.x; c < m; c += (int64_t)gridDim.x * 256) {
+    double sz = 0.0;
+    for (int64_t t = 0; t < nparts; ++t) sz += part[t * m + c];
+    const double B = 4.0 * s_mx * sz * 1.0001;
+    int F = 0;  // B = 0: the column is zero, any scale
+    if (B > 0.0 && isfinite(B)) {
+      // 2^ilogb(B) <= B < 2^(ilogb+1): B < 2^(61 - F).  Tiny data take large F (2^F stays
+      // finite up to F = 1000, i.e. B >= 2^-939 keeps the full 61 bits; fp32 inputs give
+      // B >= ~2^-300)
+      F = 61 - ilogb(B) - 1;
+      if (F > 1000) F = 1000;
+      if (F < -1000) F = -1000;
+    }
+    fx[c] = ldexp(1.0, F);
+    fx[m + c] = ldexp(1.0, -F);
   }
-  fx[0] = ldexp(1.0, F);
-  fx[1] = ldexp(1.0, -F);
 }
+
+size_t fx_scale_part_doubles(int64_t m) { return (size_t)148 * 4 * m; }
 
 void launch_fx_scale(const float *Z, int64_t ldz, int64_t n, int64_t m, const uint32_t *sval_bits,
-                     int64_t ldn, int64_t dl, double *colabs, double *fx, cudaStream_t s) {
-  cudaMemsetAsync(colabs, 0, (size_t)m * sizeof(double), s);
+                     int64_t ldn, int64_t dl, double *part, double *fx, cudaStream_t s) {
   int64_t blocks = 148 * 4;
   const int64_t rpb = m <= 256 ? 256 / m : 1;
   if (blocks * rpb > n) blocks = (n + rpb - 1) / rpb;
-  k8b_colabs<<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(Z, ldz, n, m, colabs);
-  k8c_fx_scale<<<1, 32, 0, s>>>(colabs, m, sval_bits, ldn, n, dl, fx);
+  if (blocks < 1) blocks = 1;
+  k8b_colabs<<<(unsigned)blocks, 256, 0, s>>>(Z, ldz, n, m, part);
+  k8c_fx_scale<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(part, blocks, m, sval_bits, ldn,
+                                                           n, dl, fx);
 }
 
 // ------------------------------------------------------------------ runs mode
