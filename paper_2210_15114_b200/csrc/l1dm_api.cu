@@ -465,22 +465,22 @@ l1dm_status prepare_impl(const float *X, int64_t n, int64_t ld_x, int64_t k_begi
   }
   DevBuf<uint32_t> keyA, keyB, valA, valB, hist, dbase;
   DevBuf<unsigned long long> status;
-  DevBuf<unsigned> ctrl;  // [0] nonfinite, [1] timeout, [2] ticket
+  DevBuf<unsigned> ctrl;  // [0] nonfinite [1] timeout [2] ticket [3] runs [4..8) trivial passes
+  CUDA_TRY(ctrl.ensure(8, true, s));
   CUDA_TRY(keyA.ensure(elems, false, s));
   CUDA_TRY(h->hsum.ensure((size_t)n, false, s));
   CUDA_TRY(hist.ensure((size_t)dl * 1024, true, s));
-  CUDA_TRY(ctrl.ensure(4, true, s));
 
   lap("alloc keyA/rank/hsum/hist");
   launch_keys(Xd, n, ld_x, k_begin, dl, ldn, keyA.p, h->hsum.p, ctrl.p + 0, s);
   h->kernel_launches++;
   launch_hist(keyA.p, n, ldn, dl, hist.p, s);
   h->kernel_launches++;
+  CUDA_TRY(dbase.ensure((size_t)4 * dl * 256, false, s));
+  launch_digit_base(hist.p, n, dl, dbase.p, ctrl.p + 4, s);
+  h->kernel_launches++;
   CUDA_TRY(cudaGetLastError());
-  std::vector<uint32_t> hh((size_t)dl * 1024);
-  unsigned flags_h[4];
-  CUDA_TRY(cudaMemcpyAsync(hh.data(), hist.p, hh.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost,
-                           s));
+  unsigned flags_h[8];
   CUDA_TRY(cudaMemcpyAsync(flags_h, ctrl.p, sizeof(flags_h), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   lap("keys + hist + readback");
@@ -496,20 +496,8 @@ l1dm_status prepare_impl(const float *X, int64_t n, int64_t ld_x, int64_t k_begi
   }
   // Passes whose digit is constant in every segment are the identity: skip them.
   std::vector<int> passes;
-  for (int p = 0; p < 4; ++p) {
-    bool trivial_all = true;
-    for (int64_t k = 0; k < dl && trivial_all; ++k) {
-      const uint32_t *hk = &hh[(size_t)k * 1024 + (size_t)p * 256];
-      bool trivial = false;
-      for (int b = 0; b < 256; ++b)
-        if (hk[b] == (uint32_t)n) {
-          trivial = true;
-          break;
-        }
-      trivial_all = trivial;
-    }
-    if (!trivial_all) passes.push_back(p);
-  }
+  for (int p = 0; p < 4; ++p)
+    if (flags_h[4 + p] != (unsigned)dl) passes.push_back(p);
   const int P = (int)passes.size();
   if (P == 0) {
     // keyA holds the keys; emit in place (sval bits over keyA), perm into valA.
@@ -528,25 +516,6 @@ l1dm_status prepare_impl(const float *X, int64_t n, int64_t ld_x, int64_t k_begi
     valA.p = nullptr;
     valA.count = 0;
   } else {
-    // digit bases: exclusive scan over digits of each segment's histogram, per pass
-    std::vector<uint32_t> db((size_t)dl * 1024);
-    for (int64_t k = 0; k < dl; ++k)
-      for (int p = 0; p < 4; ++p) {
-        uint32_t run = 0;
-        for (int b = 0; b < 256; ++b) {
-          db[(size_t)k * 1024 + (size_t)p * 256 + b] = run;
-          run += hh[(size_t)k * 1024 + (size_t)p * 256 + b];
-        }
-      }
-    // layout for launch: per pass a dl x 256 block
-    std::vector<uint32_t> dbp((size_t)4 * dl * 256);
-    for (int p = 0; p < 4; ++p)
-      for (int64_t k = 0; k < dl; ++k)
-        memcpy(&dbp[((size_t)p * dl + k) * 256], &db[(size_t)k * 1024 + (size_t)p * 256],
-               256 * sizeof(uint32_t));
-    CUDA_TRY(dbase.ensure(dbp.size(), false, s));
-    CUDA_TRY(cudaMemcpyAsync(dbase.p, dbp.data(), dbp.size() * sizeof(uint32_t),
-                             cudaMemcpyHostToDevice, s));
     CUDA_TRY(keyB.ensure(elems, false, s));
     CUDA_TRY(valB.ensure(elems, false, s));
     if (P > 1) CUDA_TRY(valA.ensure(elems, false, s));
@@ -587,7 +556,17 @@ l1dm_status prepare_impl(const float *X, int64_t n, int64_t ld_x, int64_t k_begi
       return e ? atoi(e) != 0 : true;
     }();
     const int64_t rt = runs_tiles(n);
-    if (runs_env && n >= 2) {
+    bool maybe = runs_env && n >= 2;
+    if (maybe) {  // necessary condition on a sample first (ctrl[3]: 1 = too many values)
+      launch_runs_sample(reinterpret_cast<const float *>(h->sval_bits.p), n, ldn, dl, ctrl.p + 3,
+                         s);
+      h->kernel_launches++;
+      unsigned too_many = 0;
+      CUDA_TRY(cudaMemcpyAsync(&too_many, ctrl.p + 3, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaStreamSynchronize(s));
+      maybe = too_many == 0;
+    }
+    if (maybe) {
       DevBuf<uint32_t> rcnt;
       CUDA_TRY(rcnt.ensure((size_t)dl * rt, false, s));
       launch_runs_count(reinterpret_cast<const float *>(h->sval_bits.p), n, ldn, dl, rcnt.p, s);

@@ -30,6 +30,10 @@ constexpr int kHistChunk = 16384;                       // keys per histogram CT
 
 void launch_keys(const float *X, int64_t n, int64_t ldx, int64_t k0, int64_t dl, int64_t ldn,
                  uint32_t *key, double *hsum, unsigned *nonfinite, cudaStream_t s);
+// per (segment, pass): exclusive digit scan -> dbase (pass-major dl x 256 blocks); ntrivial[p]
+// counts the segments whose pass-p digit is constant (zeroed by the caller)
+void launch_digit_base(const uint32_t *hist, int64_t n, int64_t dl, uint32_t *dbase,
+                       unsigned *ntrivial, cudaStream_t s);
 void launch_hist(const uint32_t *key, int64_t n, int64_t ldn, int64_t dl, uint32_t *hist,
                  cudaStream_t s);
 // One stable LSD pass over all dl segments.  first: values are implicit point indices.
@@ -51,6 +55,9 @@ void launch_identity_emit(const uint32_t *key, float *sval, uint32_t *perm, uint
 // tile (cnt: dl x runs_tiles(n)); then, given exclusive per-tile offsets, runid[k][i] (u8,
 // point order) and rvals[k][0..R_k) (the distinct values, ascending; R_k <= 256).
 int64_t runs_tiles(int64_t n);
+// flag |= 1 when some coordinate has > 256 distinct values among 4096 sampled sorted positions
+void launch_runs_sample(const float *sval, int64_t n, int64_t ldn, int64_t dl, unsigned *flag,
+                        cudaStream_t s);
 void launch_runs_count(const float *sval, int64_t n, int64_t ldn, int64_t dl, uint32_t *cnt,
                        cudaStream_t s);
 void launch_runs_emit(const float *sval, int64_t n, int64_t ldn, int64_t dl,

@@ -130,6 +130,35 @@ void launch_hist(const uint32_t *key, int64_t n, int64_t ldn, int64_t dl, uint32
   k1_hist<<<grid, 256, 0, s>>>(key, n, ldn, hist);
 }
 
+// Digit bases on the device: per (segment k, pass p) the exclusive scan of the 256-bin histogram
+// -> dbase[(p dl + k) 256 + b] (the layout k2_pass reads), and ntrivial[p] += 1 when the digit
+// is constant over the segment (some bin holds all n keys).  The host reads back four words.
+__global__ void __launch_bounds__(256)
+    k1b_digit_base(const uint32_t *__restrict__ hist, int64_t n, int64_t dl,
+                   uint32_t *__restrict__ dbase, unsigned *__restrict__ ntrivial) {
+  const int64_t k = blockIdx.x;
+  const int p = blockIdx.y, b = threadIdx.x, lane = b & 31, w = b >> 5;
+  const uint32_t c = hist[k * 1024 + p * 256 + b];
+  uint32_t incl = c;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+    if (lane >= off) incl += y;
+  }
+  __shared__ uint32_t s_w[8];
+  if (lane == 31) s_w[w] = incl;
+  const int triv = __syncthreads_or(c == (uint32_t)n);
+  uint32_t pre = 0;
+  for (int ww = 0; ww < w; ++ww) pre += s_w[ww];
+  dbase[((int64_t)p * dl + k) * 256 + b] = pre + incl - c;
+  if (b == 0 && triv) atomicAdd(ntrivial + p, 1u);
+}
+
+void launch_digit_base(const uint32_t *hist, int64_t n, int64_t dl, uint32_t *dbase,
+                       unsigned *ntrivial, cudaStream_t s) {
+  k1b_digit_base<<<dim3((unsigned)dl, 4), 256, 0, s>>>(hist, n, dl, dbase, ntrivial);
+}
+
 // ------------------------------------------------------------------ K2
 #ifdef L1DM_SORT_PROF
 // debug build only: per-phase SM cycles of k2_pass summed over CTAs (thread 0's view)
@@ -616,6 +645,36 @@ __global__ void __launch_bounds__(256)
       runid[k * ldn + i] = (uint8_t)lo;
     }
   }
+}
+
+// A cheap necessary test before the exact count: the distinct values among 4096 evenly spaced
+// sorted positions of a coordinate are a subset of its distinct values, so more than 256 of them
+// rules runs mode out for the shard (float data: one small kernel instead of a full read of
+// sval).  flag |= 1 when some coordinate fails.
+__global__ void __launch_bounds__(256)
+    k_runs_sample(const float *__restrict__ sval, int64_t n, int64_t ldn,
+                  unsigned *__restrict__ flag) {
+  constexpr int S = 4096;
+  const float *v = sval + (int64_t)blockIdx.x * ldn;
+  uint32_t c = 0;
+  for (int j = threadIdx.x; j < S; j += 256) {
+    const int64_t r = (int64_t)j * n / S, rp = (int64_t)(j - 1) * n / S;
+    c += (j == 0 || (r != rp && __float_as_uint(v[r]) != __float_as_uint(v[rp]))) ? 1u : 0u;
+  }
+  c = __reduce_add_sync(0xFFFFFFFFu, c);
+  __shared__ uint32_t s_c[8];
+  if ((threadIdx.x & 31) == 0) s_c[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < 8; ++w) t += s_c[w];
+    if (t > 256) atomicOr(flag, 1u);
+  }
+}
+
+void launch_runs_sample(const float *sval, int64_t n, int64_t ldn, int64_t dl, unsigned *flag,
+                        cudaStream_t s) {
+  k_runs_sample<<<(unsigned)dl, 256, 0, s>>>(sval, n, ldn, flag);
 }
 
 int64_t runs_tiles(int64_t n) { return (n + kRunTile - 1) / kRunTile; }
