@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <type_traits>
 
 #include "l1dm_device.cuh"
 #include "l1dm_internal.h"
@@ -262,6 +263,10 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
     // issuing integer ALU most of the time, so 64-bit index arithmetic per key is not free)
     const uint32_t base32 = (uint32_t)base;
 
+    // the tile body, specialised for full tiles (no per-item validity tests: only the last tile
+    // of a segment is partial)
+    auto tile_body = [&](auto full_c) {
+    constexpr bool FULL = decltype(full_c)::value;
     // ---- items (warp-striped: warp w owns [w*32*ITEMS, (w+1)*32*ITEMS), item j at +j*32+lane)
     uint32_t keys[kSortItems];
     uint32_t vals[kSortItems];
@@ -272,7 +277,7 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
 #pragma unroll
       for (int j = 0; j < kSortItems; ++j) {
         const int e = wbase + j * 32 + lane;
-        const bool valid = e < tile_valid;
+        const bool valid = FULL || e < tile_valid;
         keys[j] = valid ? sk[e] : 0u;
         vals[j] = FIRST ? base32 + (uint32_t)e : (valid ? sv[e] : 0u);
       }
@@ -285,18 +290,23 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
     uint32_t peers[kSortItems];
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
-      const bool valid = wbase + j * 32 + lane < tile_valid;
+      const bool valid = FULL || wbase + j * 32 + lane < tile_valid;
       const uint32_t dgt = (keys[j] >> shift) & 255u;
 #ifdef L1DM_SORT_MATCH
       // invalid lanes match only themselves (256 + lane is no digit)
       const uint32_t pm = __match_any_sync(0xFFFFFFFFu, valid ? dgt : 256u + lane);
 #else
-      uint32_t pm = (tile_valid == kSortTile) ? 0xFFFFFFFFu : __ballot_sync(0xFFFFFFFFu, valid);
+      uint32_t pm = FULL ? 0xFFFFFFFFu : __ballot_sync(0xFFFFFFFFu, valid);
 #pragma unroll
       for (int b = 0; b < 8; ++b) {
-        const uint32_t bit = (dgt >> b) & 1u;
-        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, bit);
-        pm &= bit ? bal : ~bal;
+        // one LOP3 to a predicate, the vote, a select and a 3-input LOP3 per bit
+        uint32_t bal, m;
+        asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+            "and.b32 t, %2, %3;\n\tsetp.ne.u32 p, t, 0;\n\t"
+            "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\tselp.b32 %1, 0, 0xffffffff, p;\n\t}"
+            : "=r"(bal), "=r"(m)
+            : "r"(dgt), "r"(1u << b));
+        pm &= bal ^ m;
       }
 #endif
       peers[j] = valid ? pm : 0u;
@@ -307,9 +317,9 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
       const uint32_t pm = peers[j];
-      const int leader = pm ? __ffs(pm) - 1 : lane;
+      const int leader = (FULL || pm) ? __ffs(pm) - 1 : lane;
       uint32_t old = 0;
-      if (pm && lane == leader)
+      if ((FULL || pm) && lane == leader)
         old = atomicAdd(&s_whist[w][(keys[j] >> shift) & 255u], (uint32_t)__popc(pm));
       old = __shfl_sync(0xFFFFFFFFu, old, leader);
       lrank[j] = (uint16_t)(old + __popc(pm & lt));
@@ -394,7 +404,7 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
       const int idx = wbase + j * 32 + lane;
-      if (idx < tile_valid) {
+      if (FULL || idx < tile_valid) {
         const uint32_t d = (keys[j] >> shift) & 255u;
         const uint32_t lp = s_tstart[d] + s_whist[w][d] + lrank[j];
         s_keys[lp] = keys[j];
@@ -403,6 +413,11 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
     }
     __syncthreads();
     SORT_T(5);
+    };
+    if (tile_valid == kSortTile)
+      tile_body(std::true_type{});
+    else
+      tile_body(std::false_type{});
 
     // ---- scatter: consecutive e inside a digit run go to consecutive global slots
     {
