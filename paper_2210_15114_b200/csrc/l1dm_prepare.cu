@@ -214,8 +214,8 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
   __shared__ uint32_t s_keys[kSortTile];
   __shared__ uint32_t s_vals[kSortTile];
   __shared__ uint32_t s_whist[W][256];   // per-warp digit counts, then warp-exclusive offsets
-  __shared__ uint32_t s_tstart[256];     // tile-local start of each digit
-  __shared__ uint32_t s_gbase[256];      // segment-relative start of this tile's run of each digit
+  __shared__ uint32_t s_gbase[256];      // segment-relative start of this tile's run of each
+                                         // digit minus its tile-local start
                                          // (n < 2^32: every in-segment offset fits 32 bits)
   __shared__ uint32_t s_wsum[W];
   __shared__ unsigned s_tk[2];
@@ -380,10 +380,10 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
       st_relaxed_u64(&st[tile * 256 + dgt], pack_status(kFlagInclusive, epoch,
                                                         (uint32_t)(excl + cnt)));
     }
-    s_gbase[dgt] = digit_base[seg * 256 + dgt] + (uint32_t)excl;
+    const uint32_t gb = digit_base[seg * 256 + dgt] + (uint32_t)excl;
     SORT_T(3);
 
-    // ---- block exclusive scan of the tile's digit counts -> s_tstart
+    // ---- block exclusive scan of the tile's digit counts -> the tile start of each digit
     uint32_t incl_scan = cnt;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -396,7 +396,12 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
 #pragma unroll
     for (int ww = 0; ww < W; ++ww)
       if (ww < w) wpre += s_wsum[ww];
-    s_tstart[dgt] = wpre + incl_scan - cnt;
+    // fold the tile start into this digit's per-warp offsets (staging: one shared load per key)
+    // and into the global base (scatter: gpos = s_gbase[d] + e, modulo 2^32)
+    const uint32_t ts = wpre + incl_scan - cnt;
+#pragma unroll
+    for (int ww = 0; ww < W; ++ww) s_whist[ww][dgt] += ts;
+    s_gbase[dgt] = gb - ts;
     __syncthreads();
     SORT_T(4);
 
@@ -406,7 +411,7 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
       const int idx = wbase + j * 32 + lane;
       if (FULL || idx < tile_valid) {
         const uint32_t d = (keys[j] >> shift) & 255u;
-        const uint32_t lp = s_tstart[d] + s_whist[w][d] + lrank[j];
+        const uint32_t lp = s_whist[w][d] + lrank[j];
         s_keys[lp] = keys[j];
         s_vals[lp] = vals[j];
       }
@@ -423,11 +428,12 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
     {
       uint32_t *ko = kout + seg_off, *vo = vout + seg_off;
       uint32_t *ro = rank ? rank + seg_off : nullptr;
+#pragma unroll 4
       for (int e = tid; e < tile_valid; e += kSortThreads) {
         const uint32_t k = s_keys[e];
         const uint32_t v = s_vals[e];
         const uint32_t d = (k >> shift) & 255u;
-        const uint32_t gpos = s_gbase[d] + ((uint32_t)e - s_tstart[d]);
+        const uint32_t gpos = s_gbase[d] + (uint32_t)e;
         if (LAST) {
           ko[gpos] = __float_as_uint(key_to_float(k));  // sval
           vo[gpos] = v;                                 // perm
@@ -442,7 +448,7 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
     // claim the tile after next only now: a CTA holds at most two tickets (the one it works on
     // and the one in flight), which keeps the tiles a look-back may wait for close behind
     if (tid == 0) s_tk[0] = atomicAdd(ticket, 1u);
-    __syncthreads();  // s_keys / s_vals / s_gbase / s_tstart are reused by the next tile
+    __syncthreads();  // s_keys / s_vals / s_gbase are reused by the next tile
     const int64_t t_nn = s_tk[0];
     issue(t_nn, cur);
     t_cur = t_nxt;
