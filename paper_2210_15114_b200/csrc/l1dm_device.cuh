@@ -117,6 +117,10 @@ __device__ __forceinline__ uint4 ld_stream_u4_hint(const void *p, uint64_t pol) 
                : "l"(p), "l"(pol));
   return v;
 }
+// a global-space store through a pointer the compiler cannot see is global (opaque pointers)
+__device__ __forceinline__ void st_global_u32(uint32_t *p, uint32_t v) {
+  asm volatile("st.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void st_u32_hint(uint32_t *p, uint32_t v, uint64_t pol) {
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v),
                "l"(pol)

@@ -22,7 +22,7 @@ constexpr int kSortThreads = 256;
 #define L1DM_SORT_ITEMS 16  // keys per thread per onesweep tile (16: c3 prepare 5.92 -> 5.66 ms vs 12, round 2)
 #endif
 #ifndef L1DM_SORT_MINB
-#define L1DM_SORT_MINB 2  // 2 CTAs per SM (128 registers); 3 with 8-10 items measured no better
+#define L1DM_SORT_MINB 3  // 3 CTAs per SM (80 registers, the stage in the consumed input half): c3 3.82 -> 3.77 ms, c4 59.2 -> 57.2
 #endif
 constexpr int kSortItems = L1DM_SORT_ITEMS;             // keys per thread per onesweep tile
 constexpr int kSortTile = kSortThreads * kSortItems;    // 4096 keys

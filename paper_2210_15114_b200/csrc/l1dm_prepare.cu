@@ -211,8 +211,6 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
   constexpr int W = kSortThreads / 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t *s_in = reinterpret_cast<uint32_t *>(smem_raw);  // [2][2][kSortTile] keys | vals
-  __shared__ uint32_t s_keys[kSortTile];
-  __shared__ uint32_t s_vals[kSortTile];
   __shared__ uint32_t s_whist[W][256];   // per-warp digit counts, then warp-exclusive offsets
   __shared__ uint32_t s_gbase[256];      // segment-relative start of this tile's run of each
                                          // digit minus its tile-local start
@@ -263,6 +261,9 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
     // issuing integer ALU most of the time, so 64-bit index arithmetic per key is not free)
     const uint32_t base32 = (uint32_t)base;
 
+    // the digit-ordered stage: the input half this tile was loaded from (free once every thread
+    // holds its items in registers)
+    uint32_t *s_keys = s_in + (size_t)cur * 2 * kSortTile, *s_vals = s_keys + kSortTile;
     // the tile body, specialised for full tiles (no per-item validity tests: only the last tile
     // of a segment is partial)
     auto tile_body = [&](auto full_c) {
@@ -428,6 +429,9 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
     {
       uint32_t *ko = kout + seg_off, *vo = vout + seg_off;
       uint32_t *ro = rank ? rank + seg_off : nullptr;
+      // opaque segment pointers: each store address is then one IMAD.WIDE.U32 of the 32-bit
+      // slot (ncu: the compiler otherwise re-derived seg * ldn + gpos in 64 bits per store)
+      asm("" : "+l"(ko), "+l"(vo));
 #pragma unroll 4
       for (int e = tid; e < tile_valid; e += kSortThreads) {
         const uint32_t k = s_keys[e];
@@ -435,12 +439,12 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
         const uint32_t d = (k >> shift) & 255u;
         const uint32_t gpos = s_gbase[d] + (uint32_t)e;
         if (LAST) {
-          ko[gpos] = __float_as_uint(key_to_float(k));  // sval
-          vo[gpos] = v;                                 // perm
+          st_global_u32(ko + gpos, __float_as_uint(key_to_float(k)));  // sval
+          st_global_u32(vo + gpos, v);                                 // perm
           if (ro) ro[v] = gpos;                         // rank = perm^-1 (K3 fused)
         } else {
-          ko[gpos] = k;
-          vo[gpos] = v;
+          st_global_u32(ko + gpos, k);
+          st_global_u32(vo + gpos, v);
         }
       }
     }
