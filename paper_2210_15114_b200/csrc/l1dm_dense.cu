@@ -640,20 +640,18 @@ __global__ void __launch_bounds__(512)
     k55_tridiag(int N, double *__restrict__ A, double *__restrict__ p, double *__restrict__ H,
                 double *__restrict__ tau, double *__restrict__ d, double *__restrict__ e) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ double red[512];
+  __shared__ double red[32];
   const int tid = threadIdx.x;
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid;
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
   const int lane = tid & 31;
   const int64_t gwarp = gtid >> 5, nwarps = nth >> 5;
-  auto block_sum = [&](double v) -> double {  // fixed tree
-    red[tid] = v;
+  auto block_sum = [&](double v) -> double {  // fixed order: lanes (butterfly), then warps
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    if (lane == 0) red[tid >> 5] = v;
     __syncthreads();
-    for (int o = blockDim.x / 2; o; o >>= 1) {
-      if (tid < o) red[tid] += red[tid + o];
-      __syncthreads();
-    }
-    const double r = red[0];
+    double r = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) r += red[q];
     __syncthreads();
     return r;
   };
@@ -698,8 +696,9 @@ __global__ void __launch_bounds__(512)
       double kp = 0.0;
       for (int i = tid; i < m; i += blockDim.x) kp = fma(i == 0 ? v0 : x[i], p[i], kp);
       const double K = 0.5 * t * block_sum(kp);
-      for (int64_t q = gtid; q < (int64_t)m * m; q += nth) {
-        const int r = (int)(q / m), c = (int)(q - (q / m) * m);
+      const uint32_t mm = (uint32_t)m * (uint32_t)m;  // N <= 4096: fits 32 bits
+      for (uint32_t q = (uint32_t)gtid; q < mm; q += (uint32_t)nth) {
+        const uint32_t r = q / (uint32_t)m, c = q - r * (uint32_t)m;
         const double vr = r == 0 ? v0 : x[r], vc = c == 0 ? v0 : x[c];
         const double wr = p[r] - K * vr, wc = p[c] - K * vc;
         double *a = A + (int64_t)(j + 1 + r) * N + j + 1 + c;
@@ -732,24 +731,35 @@ __device__ __forceinline__ int sturm_count(const double *d, const double *e2, in
   return cnt;
 }
 
-// One CTA (256 threads).  Y (N x k, ldy = k): the tridiagonal's eigenvectors of the k eigenvalues
+// One CTA of 1024 threads.  Y (N x k, ldy = k): the tridiagonal's eigenvectors of the k eigenvalues
 // of largest |lambda| (ties by index), in that order; lam[k], sigma[k] = |lam|.
-// smem: d, e, e2 (N each) + LU factors 5N + work 2N + the k vectors live in Y (global).
-__global__ void __launch_bounds__(256)
+// Eigenvalues: multisection — one warp per candidate index, its 32 lanes take Sturm counts at 32
+// interior points of the bracket each round, so a round shrinks it 33-fold (12 rounds to full
+// precision instead of ~60 bisection steps).
+// Eigenvectors: inverse iteration (tridiagonal LU with partial pivoting, reciprocal pivots):
+// three iterations of every vector concurrently (thread per vector; LU factors in lw, interleaved
+// [i][r] so the k threads read adjacent words), then, in ascending eigenvalue order, two more with
+// modified Gram-Schmidt against the earlier vectors of the same cluster (|dl| <= 1e-3 ||Tri||_1,
+// LAPACK dstein's grouping) — the concurrent phase takes the long serial chains off the one-vector-
+// at-a-time path.
+// smem: d, e, e2 (later one vector's LU factors, 4.5 N), y (N) + candidates.  lw: 4 N k
+// doubles + N k ints.
+__global__ void __launch_bounds__(1024)
     k56_tri_topk(int N, int k, const double *__restrict__ dg, const double *__restrict__ eg,
-                 double *__restrict__ lam, double *__restrict__ sigma, double *__restrict__ Y) {
+                 double *__restrict__ lam, double *__restrict__ sigma, double *__restrict__ Y,
+                 double *__restrict__ lw) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double *d = reinterpret_cast<double *>(smem_raw);
   double *e = d + N, *e2 = e + N;
-  double *lu_d = e2 + N, *lu_u1 = lu_d + N, *lu_u2 = lu_u1 + N, *lu_l = lu_u2 + N;
-  int *piv = reinterpret_cast<int *>(lu_l + N);
-  double *y = reinterpret_cast<double *>(piv + N + (N & 1));
-  double *cand = y + N;                    // [2k] candidate eigenvalues
-  int *cidx = reinterpret_cast<int *>(cand + 2 * k);  // [2k] their eigenvalue indices
-  int *sel = cidx + 2 * k;                 // [k] chosen candidates, by |lambda| desc
-  __shared__ double s_lo, s_hi, s_norm, s_red[256];
-  const int tid = threadIdx.x;
-  for (int i = tid; i < N; i += blockDim.x) {
+  double *y = d + (9 * (int64_t)N + 1) / 2;               // after 4.5 N: d, e, e2 | one LU
+  double *cand = y + N;                                   // [2k] candidate eigenvalues
+  int *cidx = reinterpret_cast<int *>(cand + 2 * k);      // [2k] their eigenvalue indices
+  int *sel = cidx + 2 * k;                                // [k] chosen candidates, |lambda| desc
+  int *ord = sel + k;                                     // [k] slots in ascending (lambda, index)
+  __shared__ double s_lo, s_hi, s_norm, s_red[32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int nth = blockDim.x, nw = nth >> 5;
+  for (int i = tid; i < N; i += nth) {
     d[i] = dg[i];
     e[i] = i < N - 1 ? eg[i] : 0.0;
     e2[i] = e[i] * e[i];
@@ -770,22 +780,36 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   const double tnorm = s_norm > 0.0 ? s_norm : 1.0;
   const double pivmin = fmax(1e-300, 1e-300 * tnorm);
-  // bisection for eigenvalue indices 0..k-1 and N-k..N-1 (2k candidates, duplicates when 2k > N)
+  // eigenvalue indices 0..k-1 and N-k..N-1 (2k candidates, duplicates when 2k > N)
   const int nc = 2 * k;
-  for (int c = tid; c < nc; c += blockDim.x) {
+  for (int c = w; c < nc; c += nw) {
     int idx = c < k ? c : N - nc + c;
     if (idx < 0) idx = 0;
     if (idx >= N) idx = N - 1;
     double lo = s_lo - 2.2e-16 * tnorm - pivmin, hi = s_hi + 2.2e-16 * tnorm + pivmin;
-    for (int it = 0; it < 200; ++it) {
-      const double mid = 0.5 * (lo + hi);
-      if (mid <= lo || mid >= hi) break;
+    for (int round = 0; round < 64; ++round) {
       if (hi - lo <= 2.2e-16 * fmax(fabs(lo), fabs(hi)) + pivmin) break;
-      if (sturm_count(d, e2, N, mid, pivmin) > idx) hi = mid;
-      else lo = mid;
+      const double x = lo + (hi - lo) * ((double)(lane + 1) / 33.0);
+      const bool above = x > lo && x < hi && sturm_count(d, e2, N, x, pivmin) > idx;
+      // lanes whose point lies above eigenvalue idx; points are nondecreasing in the lane
+      const unsigned b = __ballot_sync(0xFFFFFFFFu, above);
+      const unsigned inside = __ballot_sync(0xFFFFFFFFu, x > lo && x < hi);
+      if (!inside) break;  // no representable interior point left
+      const int f = b ? __ffs(b) - 1 : 32;  // first lane above
+      // the bracket becomes (x_{f-1}, x_f]: the largest interior point below, the first above
+      const unsigned below = inside & ~b & ((f == 32) ? 0xFFFFFFFFu : ((1u << f) - 1u));
+      const int g = below ? 31 - __clz(below) : -1;
+      const double xf = __shfl_sync(0xFFFFFFFFu, x, f & 31);
+      const double xg = __shfl_sync(0xFFFFFFFFu, x, g < 0 ? 0 : g);
+      const double nlo = g >= 0 ? xg : lo, nhi = f < 32 ? xf : hi;
+      if (nlo == lo && nhi == hi) break;
+      lo = nlo;
+      hi = nhi;
     }
-    cand[c] = 0.5 * (lo + hi);
-    cidx[c] = idx;
+    if (lane == 0) {
+      cand[c] = 0.5 * (lo + hi);
+      cidx[c] = idx;
+    }
   }
   __syncthreads();
   if (tid == 0) {  // the k distinct eigenvalue indices of largest |lambda| (ties: smaller index)
@@ -808,131 +832,158 @@ __global__ void __launch_bounds__(256)
       sel[nsel++] = best;
     }
     for (int r = nsel; r < k; ++r) sel[r] = sel[0];
+    for (int a = 0; a < k; ++a) {  // ascending (lambda, index, slot) order of the selection
+      int rank = 0;
+      for (int b2 = 0; b2 < k; ++b2)
+        rank += (cand[sel[b2]] < cand[sel[a]]) ||
+                (cand[sel[b2]] == cand[sel[a]] && cidx[sel[b2]] < cidx[sel[a]]) ||
+                (cand[sel[b2]] == cand[sel[a]] && cidx[sel[b2]] == cidx[sel[a]] && b2 < a);
+      ord[rank] = a;
+    }
   }
   __syncthreads();
-  // inverse iteration, vectors processed in ascending eigenvalue order so clusters are adjacent
+  // LU factors of (Tri - lambda_r I), vector r at [i * k + r]
+  double *lu_r = lw, *lu_u1 = lu_r + (int64_t)N * k, *lu_u2 = lu_u1 + (int64_t)N * k;
+  double *lu_l = lu_u2 + (int64_t)N * k;
+  int *piv = reinterpret_cast<int *>(lu_l + (int64_t)N * k);
+  const double tiny = 2.2e-16 * tnorm;
+  // solve L U v = v for vector r (one thread); v at stride vs
+  auto solve = [&](int r, double *v, int64_t vs) {
+    for (int i = 0; i < N - 1; ++i) {
+      const int64_t o = (int64_t)i * k + r;
+      const double l = lu_l[o];
+      if (piv[o]) {
+        const double t0 = v[i * vs];
+        const double t1 = v[(i + 1) * vs];
+        v[i * vs] = t1;
+        v[(i + 1) * vs] = t0 - l * t1;
+      } else {
+        v[(i + 1) * vs] -= l * v[i * vs];
+      }
+    }
+    double y1 = v[(N - 1) * vs] * lu_r[(int64_t)(N - 1) * k + r], y2 = 0.0;
+    v[(N - 1) * vs] = y1;
+    for (int i = N - 2; i >= 0; --i) {
+      const int64_t o = (int64_t)i * k + r;
+      const double yi = (v[i * vs] - lu_u1[o] * y1 - lu_u2[o] * y2) * lu_r[o];
+      v[i * vs] = yi;
+      y2 = y1;
+      y1 = yi;
+    }
+  };
+  if (tid < k) {  // concurrent phase: factor, then three plain inverse iterations per vector
+    const int r = tid;
+    const double shift = cand[sel[r]];
+    double a = d[0] - shift, b = N > 1 ? e[0] : 0.0;
+    for (int i = 0; i < N - 1; ++i) {
+      const int64_t o = (int64_t)i * k + r;
+      const double c = e[i], dn = d[i + 1] - shift, bn = i + 1 < N - 1 ? e[i + 1] : 0.0;
+      double piv_d;
+      if (fabs(a) >= fabs(c)) {  // no swap: rows (a b 0), (c dn bn)
+        piv[o] = 0;
+        const double l = (a != 0.0) ? c / a : 0.0;
+        piv_d = a;
+        lu_u1[o] = b;
+        lu_u2[o] = 0.0;
+        lu_l[o] = l;
+        a = dn - l * b;
+        b = bn;
+      } else {  // swap: pivot row (c dn bn)
+        piv[o] = 1;
+        const double l = a / c;
+        piv_d = c;
+        lu_u1[o] = dn;
+        lu_u2[o] = bn;
+        lu_l[o] = l;
+        a = b - l * dn;
+        b = -l * bn;
+      }
+      if (piv_d == 0.0) piv_d = tiny;
+      lu_r[o] = 1.0 / piv_d;
+    }
+    double last = (a == 0.0) ? tiny : a;
+    if (fabs(last) < tiny) last = last < 0 ? -tiny : tiny;
+    lu_r[(int64_t)(N - 1) * k + r] = 1.0 / last;
+    double *v = Y + r;  // column r of Y (ld k)
+    for (int i = 0; i < N; ++i)  // deterministic start: 1 + small index ramp
+      v[(int64_t)i * k] = 1.0 + 1e-3 * (double)((i * 7 + r * 13) % 17);
+    for (int iter = 0; iter < 3; ++iter) {
+      solve(r, v, k);
+      double s = 0.0;
+      for (int i = 0; i < N; ++i) s = fma(v[(int64_t)i * k], v[(int64_t)i * k], s);
+      const double inv = s > 0.0 ? 1.0 / sqrt(s) : 0.0;
+      for (int i = 0; i < N; ++i) v[(int64_t)i * k] *= inv;
+    }
+  }
+  __syncthreads();
+  auto block_sum = [&](double v) -> double {  // fixed order: lanes, then warps
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    if (lane == 0) s_red[w] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int q = 0; q < nw; ++q) t += s_red[q];
+    __syncthreads();
+    return t;
+  };
+  // serial phase, ascending eigenvalue order: two iterations with MGS inside the cluster.  The
+  // vector's LU factors are staged in shared memory over d, e, e2 (no longer needed), so the
+  // serial solve runs on shared-memory latencies
+  double *sl_r = d, *sl_u1 = sl_r + N, *sl_u2 = sl_u1 + N, *sl_l = sl_u2 + N;
+  int *sl_p = reinterpret_cast<int *>(sl_l + N);
+  auto solve_s = [&]() {  // thread 0: L U y = y from the staged factors
+    for (int i = 0; i < N - 1; ++i) {
+      const double l = sl_l[i];
+      if (sl_p[i]) {
+        const double t0 = y[i], t1 = y[i + 1];
+        y[i] = t1;
+        y[i + 1] = t0 - l * t1;
+      } else {
+        y[i + 1] -= l * y[i];
+      }
+    }
+    double y1 = y[N - 1] * sl_r[N - 1], y2 = 0.0;
+    y[N - 1] = y1;
+    for (int i = N - 2; i >= 0; --i) {
+      const double yi = (y[i] - sl_u1[i] * y1 - sl_u2[i] * y2) * sl_r[i];
+      y[i] = yi;
+      y2 = y1;
+      y1 = yi;
+    }
+  };
   for (int rr = 0; rr < k; ++rr) {
-    // position rr in ascending-lambda order among the selected
-    __shared__ int s_r;
-    __shared__ double s_lam;
-    if (tid == 0) {
-      int chosen = -1;
-      for (int a = 0; a < k; ++a) {  // rank by (lambda, index)
-        int rank = 0;
-        for (int b2 = 0; b2 < k; ++b2)
-          rank += (cand[sel[b2]] < cand[sel[a]]) ||
-                  (cand[sel[b2]] == cand[sel[a]] && cidx[sel[b2]] < cidx[sel[a]]) ||
-                  (cand[sel[b2]] == cand[sel[a]] && cidx[sel[b2]] == cidx[sel[a]] && b2 < a);
-        if (rank == rr) chosen = a;
-      }
-      s_r = chosen;
-      double lm = cand[sel[chosen]];
-      s_lam = lm;
+    const int r = ord[rr];
+    const double shift = cand[sel[r]];
+    for (int i = tid; i < N; i += nth) {
+      const int64_t o = (int64_t)i * k + r;
+      y[i] = Y[o];
+      sl_r[i] = lu_r[o];
+      sl_u1[i] = lu_u1[o];
+      sl_u2[i] = lu_u2[o];
+      sl_l[i] = lu_l[o];
+      sl_p[i] = piv[o];
     }
     __syncthreads();
-    const int r = s_r;
-    double shift = s_lam;
-    // LU of (Tri - shift I) with partial pivoting (thread 0; O(N))
-    if (tid == 0) {
-      const double tiny = 2.2e-16 * tnorm;
-      double a = d[0] - shift, b = N > 1 ? e[0] : 0.0;
-      for (int i = 0; i < N - 1; ++i) {
-        const double c = e[i], dn = d[i + 1] - shift, bn = i + 1 < N - 1 ? e[i + 1] : 0.0;
-        if (fabs(a) >= fabs(c)) {  // no swap: rows (a b 0), (c dn bn)
-          piv[i] = 0;
-          const double l = (a != 0.0) ? c / a : 0.0;
-          lu_d[i] = a;
-          lu_u1[i] = b;
-          lu_u2[i] = 0.0;
-          lu_l[i] = l;
-          a = dn - l * b;
-          b = bn;
-        } else {  // swap: pivot row (c dn bn)
-          piv[i] = 1;
-          const double l = a / c;
-          lu_d[i] = c;
-          lu_u1[i] = dn;
-          lu_u2[i] = bn;
-          lu_l[i] = l;
-          a = b - l * dn;
-          b = -l * bn;
-        }
-        if (lu_d[i] == 0.0) lu_d[i] = tiny;
-      }
-      lu_d[N - 1] = (a == 0.0) ? tiny : a;
-      if (fabs(lu_d[N - 1]) < tiny) lu_d[N - 1] = lu_d[N - 1] < 0 ? -tiny : tiny;
-    }
-    for (int i = tid; i < N; i += blockDim.x)  // deterministic start: 1 + small index ramp
-      y[i] = 1.0 + 1e-3 * (double)((i * 7 + r * 13) % 17);
-    __syncthreads();
-    for (int iter = 0; iter < 4; ++iter) {
-      if (tid == 0) {  // solve L U y = y
-        for (int i = 0; i < N - 1; ++i) {
-          if (piv[i]) {
-            const double t0 = y[i];
-            y[i] = y[i + 1];
-            y[i + 1] = t0 - lu_l[i] * y[i + 1];
-          } else {
-            y[i + 1] -= lu_l[i] * y[i];
-          }
-        }
-        y[N - 1] /= lu_d[N - 1];
-        if (N >= 2) y[N - 2] = (y[N - 2] - lu_u1[N - 2] * y[N - 1]) / lu_d[N - 2];
-        for (int i = N - 3; i >= 0; --i)
-          y[i] = (y[i] - lu_u1[i] * y[i + 1] - lu_u2[i] * y[i + 2]) / lu_d[i];
-      }
+    for (int iter = 0; iter < 2; ++iter) {
+      if (tid == 0) solve_s();
       __syncthreads();
-      // MGS against earlier vectors of the same cluster (ascending order: the last few)
       for (int q = 0; q < rr; ++q) {
-        // vector processed at position q: find its selection slot
-        __shared__ int s_q;
-        __shared__ bool s_close;
-        if (tid == 0) {
-          int slot = -1;
-          for (int a = 0; a < k; ++a) {
-            int rank = 0;
-            for (int b2 = 0; b2 < k; ++b2)
-              rank += (cand[sel[b2]] < cand[sel[a]]) ||
-                      (cand[sel[b2]] == cand[sel[a]] && cidx[sel[b2]] < cidx[sel[a]]) ||
-                      (cand[sel[b2]] == cand[sel[a]] && cidx[sel[b2]] == cidx[sel[a]] && b2 < a);
-            if (rank == q) slot = a;
-          }
-          s_q = slot;
-          s_close = fabs(cand[sel[slot]] - shift) <= 1e-3 * tnorm;
-        }
+        const int sq = ord[q];
+        if (fabs(cand[sel[sq]] - shift) > 1e-3 * tnorm) continue;  // (uniform over the CTA)
+        const double *yq = Y + sq;
+        double part = 0.0;
+        for (int i = tid; i < N; i += nth) part = fma(yq[(int64_t)i * k], y[i], part);
+        const double dot = block_sum(part);
+        for (int i = tid; i < N; i += nth) y[i] -= dot * yq[(int64_t)i * k];
         __syncthreads();
-        if (s_close) {
-          const double *yq = Y + s_q;  // column s_q of Y (ld k)
-          double part = 0.0;
-          for (int i = tid; i < N; i += blockDim.x) part = fma(yq[(int64_t)i * k], y[i], part);
-          s_red[tid] = part;
-          __syncthreads();
-          for (int o = 128; o; o >>= 1) {
-            if (tid < o) s_red[tid] += s_red[tid + o];
-            __syncthreads();
-          }
-          const double dot = s_red[0];
-          __syncthreads();
-          for (int i = tid; i < N; i += blockDim.x) y[i] -= dot * yq[(int64_t)i * k];
-          __syncthreads();
-        }
       }
-      // normalise
       double part = 0.0;
-      for (int i = tid; i < N; i += blockDim.x) part = fma(y[i], y[i], part);
-      s_red[tid] = part;
-      __syncthreads();
-      for (int o = 128; o; o >>= 1) {
-        if (tid < o) s_red[tid] += s_red[tid + o];
-        __syncthreads();
-      }
-      const double nrm = sqrt(s_red[0]);
-      __syncthreads();
+      for (int i = tid; i < N; i += nth) part = fma(y[i], y[i], part);
+      const double nrm = sqrt(block_sum(part));
       const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
-      for (int i = tid; i < N; i += blockDim.x) y[i] *= inv;
+      for (int i = tid; i < N; i += nth) y[i] *= inv;
       __syncthreads();
     }
-    for (int i = tid; i < N; i += blockDim.x) Y[(int64_t)i * k + r] = y[i];
+    for (int i = tid; i < N; i += nth) Y[(int64_t)i * k + r] = y[i];
     if (tid == 0) {
       if (lam) lam[r] = cand[sel[r]];
       if (sigma) sigma[r] = fabs(cand[sel[r]]);
@@ -1227,7 +1278,10 @@ int launch_jacobi(int64_t N, double *A, int64_t lda, double *W, double *V, int64
   return 1;
 }
 
-size_t topk_workspace(int64_t N) { return (size_t)(2 * N * N + 5 * N + 8) * sizeof(double); }
+// (+ the inverse iteration's LU factors: 5 N k doubles and N k ints, k <= 96)
+size_t topk_workspace(int64_t N) {
+  return (size_t)(2 * N * N + 5 * N + 8 + 6 * N * 96) * sizeof(double);
+}
 
 // The k eigenpairs of largest |lambda| of the symmetric A (N x N, lda; read only):
 // lam[k], sigma[k] = |lam| in nonincreasing |lambda| order, Vs (N x k, ld k) the unit
@@ -1244,6 +1298,11 @@ int launch_sym_topk(int64_t N, const double *A, int64_t lda, int64_t k, double *
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k55_tridiag, 512, 0);
     if (per_sm < 1) per_sm = 1;
     int64_t blocks = (int64_t)sms * per_sm;
+    static const int64_t cap = [] {
+      const char *v = getenv("L1DM_TRIDIAG_CTAS");
+      return v ? (int64_t)atoll(v) : (int64_t)0;
+    }();
+    if (cap > 0 && blocks > cap) blocks = cap;
     const int64_t want = (N * N + 511) / 512;
     if (blocks > want) blocks = want;
     if (blocks < 1) blocks = 1;
@@ -1260,14 +1319,15 @@ int launch_sym_topk(int64_t N, const double *A, int64_t lda, int64_t k, double *
       cudaMemcpyAsync(ee, Ac + N, sizeof(double), cudaMemcpyDeviceToDevice, s);
     cudaMemsetAsync(tau, 0, N * sizeof(double), s);
   }
-  const size_t sm = (size_t)(8 * N + 2) * sizeof(double) + (size_t)(4 * k) * sizeof(double) +
-                    (size_t)(N + 1) * sizeof(int) + (size_t)(5 * k) * sizeof(int) + 64;
+  const size_t sm = (size_t)((9 * N + 1) / 2 + N) * sizeof(double) +
+                    (size_t)(2 * k) * sizeof(double) + (size_t)(4 * k) * sizeof(int) + 64;
+  double *lw = e + N;  // LU factors of the inverse iteration (topk_workspace)
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k56_tri_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  k56_tri_topk<<<1, 256, sm, s>>>((int)N, (int)k, d, e, lam, sigma, Vs);
+  k56_tri_topk<<<1, 1024, sm, s>>>((int)N, (int)k, d, e, lam, sigma, Vs, lw);
   if (N > 2) k57_back<<<(unsigned)k, 256, 0, s>>>((int)N, (int)k, H, tau, Vs);
   return launches + 2;
 }
