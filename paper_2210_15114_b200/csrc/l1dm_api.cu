@@ -814,10 +814,16 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
     // reduce + prefix (tile totals), accumulate = apply (U and the reductions into Yt),
     // colsums = Zt, totals and the block write-out.
     const float *sval = reinterpret_cast<const float *>(h->sval_bits.p);
+    // deterministic accumulation (DESIGN.md R16): the block accumulator Yt holds 64-bit fixed
+    // point at per-column scales from a bound on |Yt|; integer reductions are associative, so Y
+    // is bitwise reproducible run to run.  The Zt pass also sums |z| per column for the bound.
+    CUDA_TRY(h->fxbuf.ensure(2 * (size_t)m + (size_t)zt_max_ctas(m, p.mb) * m, false, s));
+    double *fx = h->fxbuf.p;
     {
       TimedScope ts(h, kColsums, s);
-      launch_zt(Z, ldz, h->n, m, p.mb, h->zt.p, s);
-      h->kernel_launches++;
+      const int64_t nparts = launch_zt(Z, ldz, h->n, m, p.mb, h->zt.p, s, h->fxbuf.p + 2 * m);
+      launch_fx_scale(h->fxbuf.p + 2 * m, nparts, m, h->sval_bits.p, h->ldn, h->n, h->dl, fx, s);
+      h->kernel_launches += 2;
       h->launches[kColsums]++;
     }
     // tile totals: one pass over full Z rows for every column block at once (m <= 256), else a
@@ -835,16 +841,6 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
       h->kernel_launches += 2;  // reduce-all, prefix
       h->launches[kScan]++;
       if (h->timing) h->scan_pairs += h->n * h->dl * p.col_blocks;
-    }
-    // deterministic accumulation (DESIGN.md R16): the block accumulator Yt holds 64-bit fixed
-    // point at a per-query scale from a bound on |Yt|; integer reductions are associative, so Y
-    // is bitwise reproducible run to run
-    CUDA_TRY(h->fxbuf.ensure(2 * (size_t)m + fx_scale_part_doubles(m), false, s));
-    double *fx = h->fxbuf.p;
-    {
-      TimedScope ts(h, kColsums, s);
-      launch_fx_scale(Z, ldz, h->n, m, h->sval_bits.p, h->ldn, h->dl, h->fxbuf.p + 2 * m, fx, s);
-      h->kernel_launches += 2;
     }
     for (int cb = 0; cb < p.col_blocks; ++cb) {
       const int64_t c0 = (int64_t)cb * p.mb;

@@ -209,7 +209,169 @@ __global__ void __launch_bounds__(256)
   for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * 256) {
     double s = 0.0;
-    for (int64_t z = 0; z < S; ++z) s += P[z * total + e];
+    int64_t z = 0;
+    for (; z + 8 <= S; z += 8) {  // eight loads in flight, added in index order
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = P[(z + u) * total + e];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; z < S; ++z) s += P[z * total + e];
+    const int64_t r = e / N, c = e - (e / N) * N;
+    double *p = C + r * ldc + c;
+    const double v = alpha * s;
+    *p = (beta != 0.0) ? fma(beta, *p, v) : v;
+  }
+}
+
+// ---- skinny GEMMs of the Krylov block steps (one dimension = the n points, the others <= 96)
+// Bandwidth-bound shapes, so no shared-memory staging: DMMA fragments are loaded straight from
+// global memory (lane l: rows k0 + l % 4, columns 8 t + l / 4 — four 64-byte row pieces per load
+// instruction), several k-steps of loads in flight per warp.
+//
+// k44_skinny_tn<MT, NT>: partial C (M x N, M <= 8 MT, N <= 8 NT) = A^T B over a contiguous row
+// range per warp; the 8 warps' tiles are summed in a fixed order through shared memory and each
+// CTA writes its partial to P[blockIdx.x][M][N] (folded by k41_gemm_fold in CTA order).
+template <int MT, int NT>
+__global__ void __launch_bounds__(256)
+    k44_skinny_tn(int64_t M, int64_t N, int64_t K, const double *__restrict__ A, int64_t lda,
+                  const double *__restrict__ B, int64_t ldb, int64_t rows_per_warp,
+                  double *__restrict__ P) {
+  constexpr int U = MT * NT > 16 ? 2 : 4;  // k-steps (of 4 rows) in flight per warp
+  __shared__ double red[MT * 8][NT * 8 + 1];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * 8 + w;
+  const int64_t r0 = gw * rows_per_warp;
+  const int64_t r1 = (r0 + rows_per_warp < K) ? r0 + rows_per_warp : K;
+  const int kr = lane & 3, cl = lane >> 2;
+  bool mok[MT], nok[NT];
+#pragma unroll
+  for (int t = 0; t < MT; ++t) mok[t] = 8 * t + cl < M;
+#pragma unroll
+  for (int t = 0; t < NT; ++t) nok[t] = 8 * t + cl < N;
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int64_t k0 = r0; k0 < r1; k0 += 4 * U) {
+    double a[U][MT], b[U][NT];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t k = k0 + 4 * u + kr;
+      const bool ok = k < r1;
+#pragma unroll
+      for (int t = 0; t < MT; ++t) a[u][t] = (ok && mok[t]) ? __ldg(A + k * lda + 8 * t + cl) : 0.0;
+#pragma unroll
+      for (int t = 0; t < NT; ++t) b[u][t] = (ok && nok[t]) ? __ldg(B + k * ldb + 8 * t + cl) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[u][i], b[u][j]);
+  }
+  // lane holds C[8 i + l / 4][8 j + 2 (l % 4) + h]; the warps add theirs in index order
+  for (int q = 0; q < 8; ++q) {
+    if (w == q) {
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            double &r = red[8 * i + cl][8 * j + 2 * kr + h];
+            r = (q == 0) ? acc[i][j][h] : r + acc[i][j][h];
+          }
+    }
+    __syncthreads();
+  }
+  const int64_t tot = M * N;
+  for (int64_t e = threadIdx.x; e < tot; e += 256) {
+    const int r = (int)(e / N), c = (int)(e - (e / N) * N);
+    P[(int64_t)blockIdx.x * tot + e] = red[r][c];
+  }
+}
+
+// k45_skinny_nn<NT>: C (M x N, N <= 8 NT) = alpha A (M x K) B (K x N) + beta C with K <= 96 and M
+// the n points: B staged in shared memory once per CTA; each warp computes 8-row tiles of C
+// (grid-stride), its A fragments loaded straight from global memory.
+template <int NT>
+__global__ void __launch_bounds__(256)
+    k45_skinny_nn(int64_t M, int64_t N, int64_t K, const double *__restrict__ A, int64_t lda,
+                  const double *__restrict__ B, int64_t ldb, double alpha, double beta,
+                  double *__restrict__ C, int64_t ldc) {
+  constexpr int KMAX = 96;
+  __shared__ double bs[KMAX][NT * 8 + 1];
+  for (int e = threadIdx.x; e < KMAX * NT * 8; e += 256) {
+    const int kk = e / (NT * 8), nn = e - (e / (NT * 8)) * (NT * 8);
+    bs[kk][nn] = (kk < K && nn < N) ? B[(int64_t)kk * ldb + nn] : 0.0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int kr = lane & 3, cl = lane >> 2;
+  const int ksteps = (int)((K + 3) / 4);
+  const bool vec2 = (ldc % 2 == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
+  const int64_t tiles = (M + 7) / 8;
+  for (int64_t t = (int64_t)blockIdx.x * 8 + w; t < tiles; t += (int64_t)gridDim.x * 8) {
+    const int64_t row = 8 * t + cl;  // A fragment row of this lane
+    const bool rok = row < M;
+    double acc[NT][2];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = 0.0;
+    double a[KMAX / 4];
+#pragma unroll
+    for (int q = 0; q < KMAX / 4; ++q) {
+      const int kk = 4 * q + kr;
+      a[q] = (q < ksteps && rok && kk < K) ? __ldg(A + row * lda + kk) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < KMAX / 4; ++q) {
+      if (q >= ksteps) break;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) dmma884(acc[j][0], acc[j][1], a[q], bs[4 * q + kr][8 * j + cl]);
+    }
+    if (row < M) {
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const int64_t c = 8 * j + 2 * kr;
+        double *p = C + row * ldc + c;
+        if (vec2 && c + 1 < N) {  // whole 16-byte pairs: every warp store fills 32-byte sectors
+          double2 v = make_double2(alpha * acc[j][0], alpha * acc[j][1]);
+          if (beta != 0.0) {
+            const double2 o = *reinterpret_cast<const double2 *>(p);
+            v.x = fma(beta, o.x, v.x);
+            v.y = fma(beta, o.y, v.y);
+          }
+          *reinterpret_cast<double2 *>(p) = v;
+        } else {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (c + h >= N) continue;
+            const double v = alpha * acc[j][h];
+            p[h] = (beta != 0.0) ? fma(beta, p[h], v) : v;
+          }
+        }
+      }
+    }
+  }
+}
+
+// The same fold for many partials (the skinny TN's one per CTA): a warp per element, lane l
+// summing partials l, l + 32, ... in order, then a fixed butterfly (deterministic).
+__global__ void __launch_bounds__(256)
+    k41b_gemm_fold_warp(int64_t M, int64_t N, int64_t S, const double *__restrict__ P, double *C,
+                        int64_t ldc, double alpha, double beta) {
+  const int lane = threadIdx.x & 31;
+  const int64_t e = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5), total = M * N;
+  if (e >= total) return;
+  double s = 0.0;
+  for (int64_t z = lane; z < S; z += 32) s += P[z * total + e];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+  if (lane == 0) {
     const int64_t r = e / N, c = e - (e / N) * N;
     double *p = C + r * ldc + c;
     const double v = alpha * s;
@@ -242,6 +404,11 @@ int gemm_t(int64_t M, int64_t N, int64_t K, double alpha, const double *A, int64
   k40_gemm<TA, WM, WN, KS, MI><<<g, 256, Cf::SMEM, s>>>(M, N, K, A, lda, B, ldb, kchunk, ws, N, 1.0,
                                                     0.0, 0);
   const int64_t tot = M * N;
+  if (splits >= 64 && tot <= 148 * 64) {  // many partials of a small C: a warp per element
+    k41b_gemm_fold_warp<<<(unsigned)((tot + 7) / 8), 256, 0, s>>>(M, N, splits, ws, C, ldc,
+                                                                  alpha, beta);
+    return 2;
+  }
   int64_t fb = (tot + 255) / 256;
   if (fb > 148 * 8) fb = 148 * 8;
   k41_gemm_fold<<<(unsigned)(fb < 1 ? 1 : fb), 256, 0, s>>>(M, N, splits, ws, C, ldc, alpha,
@@ -1206,9 +1373,48 @@ int grid1d(int64_t elems, int cap = 148 * 8) {
 }  // namespace
 
 // ------------------------------------------------------------------------------- launchers
+// the skinny kernels' shapes: TN with M <= 64, N <= 32 and a long K; NN with K <= 96, N <= 32
+static bool skinny_tn(int ta, int64_t M, int64_t N, int64_t K) {
+  return ta && M <= 64 && N <= 32 && K >= 4096;
+}
+static bool skinny_nn(int ta, int64_t N, int64_t K) { return !ta && K <= 96 && N <= 32; }
+static int64_t skinny_tn_ctas(int64_t K, int sms) {
+  int64_t c = (int64_t)sms * 4;
+  const int64_t cap = (K + 8 * 64 - 1) / (8 * 64);  // at least 64 rows per warp
+  return c < cap ? c : (cap < 1 ? 1 : cap);
+}
+
 size_t gemm_workspace(int ta, int64_t M, int64_t N, int64_t K, int sms) {
   const int64_t sp = gemm_splits(ta, M, N, K, sms);
-  return sp > 1 ? (size_t)sp * (size_t)M * (size_t)N * sizeof(double) : 0;
+  size_t b = sp > 1 ? (size_t)sp * (size_t)M * (size_t)N * sizeof(double) : 0;
+  if (skinny_tn(ta, M, N, K))
+    b = std::max(b, (size_t)skinny_tn_ctas(K, sms) * (size_t)M * (size_t)N * sizeof(double));
+  return b;
+}
+
+template <int MT, int NT>
+static int skinny_tn_t(int64_t M, int64_t N, int64_t K, double alpha, const double *A,
+                       int64_t lda, const double *B, int64_t ldb, double beta, double *C,
+                       int64_t ldc, double *ws, int sms, cudaStream_t s) {
+  const int64_t ctas = skinny_tn_ctas(K, sms);
+  int64_t rpw = (K + ctas * 8 - 1) / (ctas * 8);
+  rpw = (rpw + 15) / 16 * 16;
+  k44_skinny_tn<MT, NT><<<(unsigned)ctas, 256, 0, s>>>(M, N, K, A, lda, B, ldb, rpw, ws);
+  const int64_t tot = M * N;
+  k41b_gemm_fold_warp<<<(unsigned)((tot + 7) / 8), 256, 0, s>>>(M, N, ctas, ws, C, ldc, alpha,
+                                                                beta);
+  return 2;
+}
+
+template <int NT>
+static int skinny_nn_t(int64_t M, int64_t N, int64_t K, double alpha, const double *A,
+                       int64_t lda, const double *B, int64_t ldb, double beta, double *C,
+                       int64_t ldc, int sms, cudaStream_t s) {
+  int64_t ctas = (int64_t)sms * 8;
+  const int64_t need = ((M + 7) / 8 + 7) / 8;
+  if (ctas > need) ctas = need < 1 ? 1 : need;
+  k45_skinny_nn<NT><<<(unsigned)ctas, 256, 0, s>>>(M, N, K, A, lda, B, ldb, alpha, beta, C, ldc);
+  return 1;
 }
 
 int launch_gemm(int ta, int64_t M, int64_t N, int64_t K, double alpha, const double *A,
@@ -1219,6 +1425,29 @@ int launch_gemm(int ta, int64_t M, int64_t N, int64_t K, double alpha, const dou
     const int64_t tot = M * N;
     k41_gemm_fold<<<grid1d(tot), 256, 0, s>>>(M, N, 0, nullptr, C, ldc, 0.0, beta);
     return 1;
+  }
+  static const bool skinny_on = [] {
+    const char *v = getenv("L1DM_SKINNY_GEMM");
+    return v ? atoi(v) != 0 : true;
+  }();
+  if (skinny_on && skinny_tn(ta, M, N, K)) {
+    const int mt = (int)((M + 7) / 8), nt = (int)((N + 7) / 8);
+#define L1DM_TN(MT_, NT_) \
+  if (mt == MT_ && nt == NT_) \
+    return skinny_tn_t<MT_, NT_>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, sms, s);
+#define L1DM_TN_M(MT_) L1DM_TN(MT_, 1) L1DM_TN(MT_, 2) L1DM_TN(MT_, 3) L1DM_TN(MT_, 4)
+    L1DM_TN_M(1) L1DM_TN_M(2) L1DM_TN_M(3) L1DM_TN_M(4) L1DM_TN_M(5) L1DM_TN_M(6) L1DM_TN_M(7)
+    L1DM_TN_M(8)
+#undef L1DM_TN_M
+#undef L1DM_TN
+  }
+  if (skinny_on && skinny_nn(ta, N, K)) {
+    switch ((N + 7) / 8) {
+      case 1: return skinny_nn_t<1>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, sms, s);
+      case 2: return skinny_nn_t<2>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, sms, s);
+      case 3: return skinny_nn_t<3>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, sms, s);
+      default: return skinny_nn_t<4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, sms, s);
+    }
   }
   const int64_t sp = gemm_splits(ta, M, N, K, sms);
   const bool narrow = N <= 32;

@@ -213,11 +213,10 @@ void launch_scan_seq(const QueryPlan &p, int lp, const uint32_t *perm, const flo
 // (fx: lp = 1 apply in deterministic fixed point — out is an int64 block, fx = the block's
 //  per-column scales 2^F_c.)
 // fx[c] = 2^F_c, fx[m + c] = 2^-F_c for the query: F_c from a bound on column c of Yt (the
-// column's |z| sum and the shard's |x|), computed in a fixed order; part holds
-// fx_scale_part_doubles(m) doubles of scratch.
-size_t fx_scale_part_doubles(int64_t m);
-void launch_fx_scale(const float *Z, int64_t ldz, int64_t n, int64_t m, const uint32_t *sval_bits,
-                     int64_t ldn, int64_t dl, double *part, double *fx, cudaStream_t s);
+// column's |z| sum, from the nparts x m per-CTA partials launch_zt wrote, and the shard's |x|),
+// every sum in a fixed order.
+void launch_fx_scale(const double *part, int64_t nparts, int64_t m, const uint32_t *sval_bits,
+                     int64_t ldn, int64_t n, int64_t dl, double *fx, cudaStream_t s);
 // (agg_ld: the apply's stride between tiles in agg, 0 = the block's own payload (lp+1) mb.)
 // P = 1, m <= 256: tile totals of all m columns in one pass over full Z rows + the prefix
 // (agg: kcc x tiles x 2m, segtot rows of 2m).  The per-block apply then reads agg + 2 c0 with
@@ -226,8 +225,11 @@ bool launch_reduce_all(const uint32_t *perm, const float *sval, int64_t ldn, int
                        const float *Z, int64_t ldz, int64_t m, int64_t kcc, int64_t tiles_per_seg,
                        double *agg, double *segtot, cudaStream_t s);
 // Zt[cb][i][0..mb) = Z[i][cb*mb + ..] (zero-padded past m): the scatter mode's per-block Z.
-void launch_zt(const float *Z, int64_t ldz, int64_t n, int64_t m, int mb, float *zt,
-               cudaStream_t s);
+// With colabs_part (zt_max_ctas(m, mb) x m doubles) also the per-CTA column sums of |z| for
+// launch_fx_scale; returns the number of CTAs (partials).
+int64_t launch_zt(const float *Z, int64_t ldz, int64_t n, int64_t m, int mb, float *zt,
+                  cudaStream_t s, double *colabs_part = nullptr);
+int64_t zt_max_ctas(int64_t m, int mb);
 void launch_accumulate(const QueryPlan &p, const uint32_t *rank, int64_t ldn, int64_t n,
                        const double *U, int64_t k_first, int64_t kcc, const double *hsum,
                        const double *Sg, double *Y, int64_t ldy, int64_t m, bool first_chunk,

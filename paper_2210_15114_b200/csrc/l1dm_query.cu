@@ -1313,54 +1313,28 @@ void launch_block_out(const double *yt, int mb, int64_t mc, const double *hsum, 
 // keeps every partial sum below 2^61 in magnitude: fx[c] = 2^F_c, fx[m + c] = 2^-F_c.  Each
 // term is rounded once to 2^-F_c (<= 2^-(F_c+1) absolute, about 2^-63 B_c), the sum is exact.
 // The scale itself must not depend on the order of any floating-point sum (else F_c could flip
-// at a power of two from run to run): k8b writes per-CTA partial sums (its row lanes folded in
-// order), k8c adds them in CTA order.
-__global__ void __launch_bounds__(256)
-    k8b_colabs(const float *__restrict__ Z, int64_t ldz, int64_t n, int64_t m,
-               double *__restrict__ part) {
-  if (m <= 256) {  // 256 / m rows per CTA step, one column per thread
-    __shared__ double s_acc[256];
-    const int64_t c = threadIdx.x % m;
-    const int64_t rpb = 256 / m;
-    const int64_t r0 = threadIdx.x / m;
-    double acc = 0.0;
-    if (r0 < rpb)
-      for (int64_t i = (int64_t)blockIdx.x * rpb + r0; i < n; i += (int64_t)gridDim.x * rpb)
-        acc += fabs((double)__ldg(Z + i * ldz + c));
-    s_acc[threadIdx.x] = acc;
-    __syncthreads();
-    if (threadIdx.x < m) {  // the CTA's row lanes, folded in order
-      for (int64_t r = 1; r < rpb; ++r) acc += s_acc[r * m + threadIdx.x];
-      part[(int64_t)blockIdx.x * m + c] = acc;
-    }
-    return;
-  }
-  for (int64_t c = threadIdx.x; c < m; c += 256) {  // wide blocks: one row per CTA step
-    double acc = 0.0;
-    for (int64_t i = blockIdx.x; i < n; i += gridDim.x) acc += fabs((double)__ldg(Z + i * ldz + c));
-    part[(int64_t)blockIdx.x * m + c] = acc;
-  }
-}
-
+// at a power of two from run to run): k8_zt writes per-CTA partial sums (its threads folded in
+// order) while it builds the Zt blocks, k8c adds them in a fixed lane/butterfly order.
 __global__ void __launch_bounds__(256)
     k8c_fx_scale(const double *__restrict__ part, int64_t nparts, int64_t m,
                  const uint32_t *__restrict__ sval_bits, int64_t ldn, int64_t n, int64_t dl,
                  double *__restrict__ fx) {
-  __shared__ double s_mx;
-  if (threadIdx.x < 32) {  // sum_k Mx_k, warp lanes over k, folded in a fixed order
-    double mx = 0.0;
-    for (int64_t k = threadIdx.x; k < dl; k += 32)
-      mx += fmax(fabs((double)__uint_as_float(sval_bits[k * ldn])),
-                 fabs((double)__uint_as_float(sval_bits[k * ldn + n - 1])));
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // sum_k Mx_k: lanes over k, a fixed butterfly (every warp computes it)
+  double mx = 0.0;
+  for (int64_t k = lane; k < dl; k += 32)
+    mx += fmax(fabs((double)__uint_as_float(sval_bits[k * ldn])),
+               fabs((double)__uint_as_float(sval_bits[k * ldn + n - 1])));
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) mx += __shfl_xor_sync(0xFFFFFFFFu, mx, off);
-    if (threadIdx.x == 0) s_mx = mx;
-  }
-  __syncthreads();
-  for (int64_t c = (int64_t)blockIdx.x * 256 + threadIdx.x; c < m; c += (int64_t)gridDim.x * 256) {
+  for (int off = 16; off > 0; off >>= 1) mx += __shfl_xor_sync(0xFFFFFFFFu, mx, off);
+  // column c: lanes over the CTA partials (strided, in order), then a fixed butterfly
+  for (int64_t c = (int64_t)blockIdx.x * 8 + w; c < m; c += (int64_t)gridDim.x * 8) {
     double sz = 0.0;
-    for (int64_t t = 0; t < nparts; ++t) sz += part[t * m + c];
-    const double B = 4.0 * s_mx * sz * 1.0001;
+    for (int64_t t = lane; t < nparts; t += 32) sz += part[t * m + c];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sz += __shfl_xor_sync(0xFFFFFFFFu, sz, off);
+    if (lane != 0) continue;
+    const double B = 4.0 * mx * sz * 1.0001;
     int F = 0;  // B = 0: the column is zero, any scale
     if (B > 0.0 && isfinite(B)) {
       // 2^ilogb(B) <= B < 2^(ilogb+1): B < 2^(61 - F).  Tiny data take large F (2^F stays
@@ -1375,17 +1349,10 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-size_t fx_scale_part_doubles(int64_t m) { return (size_t)148 * 4 * m; }
-
-void launch_fx_scale(const float *Z, int64_t ldz, int64_t n, int64_t m, const uint32_t *sval_bits,
-                     int64_t ldn, int64_t dl, double *part, double *fx, cudaStream_t s) {
-  int64_t blocks = 148 * 4;
-  const int64_t rpb = m <= 256 ? 256 / m : 1;
-  if (blocks * rpb > n) blocks = (n + rpb - 1) / rpb;
-  if (blocks < 1) blocks = 1;
-  k8b_colabs<<<(unsigned)blocks, 256, 0, s>>>(Z, ldz, n, m, part);
-  k8c_fx_scale<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(part, blocks, m, sval_bits, ldn,
-                                                           n, dl, fx);
+void launch_fx_scale(const double *part, int64_t nparts, int64_t m, const uint32_t *sval_bits,
+                     int64_t ldn, int64_t n, int64_t dl, double *fx, cudaStream_t s) {
+  k8c_fx_scale<<<(unsigned)((m + 7) / 8), 256, 0, s>>>(part, nparts, m, sval_bits, ldn, n, dl,
+                                                       fx);
 }
 
 // ------------------------------------------------------------------ runs mode
@@ -1766,44 +1733,104 @@ void launch_simplex_stats(const double *hsum, int64_t n, const float *sval, int6
 // ------------------------------------------------------------------ scatter-mode Z blocks
 // Zt[cb][i][0..mb) = Z[i][cb*mb ..] zero-padded past m.  Thread e -> (row i = e / cb_count,
 // block cb = e % cb_count): a warp reads whole Z rows and writes full sectors of each block.
+// With part != nullptr (scatter m > 1: the fixed-point scales, launch_fx_scale) the pass also
+// sums |z| per column: the grid is a multiple of cb_count threads, so a thread's block is fixed;
+// each CTA folds its threads' sums per column in thread order into part[blockIdx][m].
 template <int MB>
 __global__ void __launch_bounds__(256)
     k8_zt(const float *__restrict__ Z, int64_t ldz, int64_t n, int64_t m, int64_t ncb,
-          float *__restrict__ zt, int vec4) {
+          float *__restrict__ zt, int vec4, double *__restrict__ part) {
   const int64_t total = n * ncb;
+  float acc[MB];
+#pragma unroll
+  for (int q = 0; q < MB; ++q) acc[q] = 0.0f;
+  double dacc[MB];
+#pragma unroll
+  for (int q = 0; q < MB; ++q) dacc[q] = 0.0;
+  int cnt = 0;
   for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * 256) {
     const int64_t i = e / ncb, cb = e - (e / ncb) * ncb;
     const int64_t c0 = cb * MB;
     const float *src = Z + i * ldz + c0;
     float *dst = zt + (cb * n + i) * MB;
+    float v[MB];
+    bool done = false;
     if constexpr (MB % 4 == 0) {
       if (vec4 && c0 + MB <= m) {
 #pragma unroll
-        for (int q = 0; q < MB; q += 4)
-          reinterpret_cast<float4 *>(dst)[q / 4] = __ldcs(reinterpret_cast<const float4 *>(src + q));
-        continue;
+        for (int q = 0; q < MB; q += 4) {
+          const float4 t = __ldcs(reinterpret_cast<const float4 *>(src + q));
+          reinterpret_cast<float4 *>(dst)[q / 4] = t;
+          v[q] = t.x; v[q + 1] = t.y; v[q + 2] = t.z; v[q + 3] = t.w;
+        }
+        done = true;
       }
     }
+    if (!done) {
 #pragma unroll
-    for (int q = 0; q < MB; ++q) dst[q] = (c0 + q < m) ? __ldcs(src + q) : 0.0f;
+      for (int q = 0; q < MB; ++q) {
+        v[q] = (c0 + q < m) ? __ldcs(src + q) : 0.0f;
+        dst[q] = v[q];
+      }
+    }
+    if (part) {  // |z| sums: fp32 runs of 64 rows, folded into fp64 (a bound only)
+#pragma unroll
+      for (int q = 0; q < MB; ++q) acc[q] += fabsf(v[q]);
+      if (++cnt == 64) {
+#pragma unroll
+        for (int q = 0; q < MB; ++q) {
+          dacc[q] += (double)acc[q];
+          acc[q] = 0.0f;
+        }
+        cnt = 0;
+      }
+    }
+  }
+  if (!part) return;
+  constexpr int QC = MB < 16 ? MB : 16;  // columns of a block per shared-memory round
+  __shared__ double s_acc[256 * QC];
+  const int64_t base = (int64_t)blockIdx.x * 256;
+#pragma unroll
+  for (int q0 = 0; q0 < MB; q0 += QC) {
+#pragma unroll
+    for (int q = 0; q < QC; ++q) s_acc[threadIdx.x * QC + q] = dacc[q0 + q] + (double)acc[q0 + q];
+    __syncthreads();
+    for (int64_t c = threadIdx.x; c < m; c += 256) {
+      const int64_t cb = c / MB, q = c - cb * MB;
+      if (q < q0 || q >= q0 + QC) continue;
+      int64_t t0 = (cb - base % ncb) % ncb;  // first thread of this CTA on block cb
+      if (t0 < 0) t0 += ncb;
+      double sum = 0.0;
+      for (int64_t t = t0; t < 256; t += ncb) sum += s_acc[t * QC + (q - q0)];
+      part[(int64_t)blockIdx.x * m + c] = sum;
+    }
+    __syncthreads();
   }
 }
 
-void launch_zt(const float *Z, int64_t ldz, int64_t n, int64_t m, int mb, float *zt,
-               cudaStream_t s) {
+int64_t launch_zt(const float *Z, int64_t ldz, int64_t n, int64_t m, int mb, float *zt,
+                  cudaStream_t s, double *colabs_part) {
   const int64_t ncb = (m + mb - 1) / mb;
   const int vec4 = (ldz % 4 == 0 && reinterpret_cast<uintptr_t>(Z) % 16 == 0) ? 1 : 0;
   int64_t blocks = (n * ncb + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
+  // with the |z| sums: whole multiples of ncb CTAs keep every thread on one block
+  if (colabs_part) blocks = (blocks + ncb - 1) / ncb * ncb;
   switch (mb) {
-    case 2: k8_zt<2><<<(unsigned)blocks, 256, 0, s>>>(Z, ldz, n, m, ncb, zt, vec4); break;
-    case 4: k8_zt<4><<<(unsigned)blocks, 256, 0, s>>>(Z, ldz, n, m, ncb, zt, vec4); break;
-    case 8: k8_zt<8><<<(unsigned)blocks, 256, 0, s>>>(Z, ldz, n, m, ncb, zt, vec4); break;
-    case 16: k8_zt<16><<<(unsigned)blocks, 256, 0, s>>>(Z, ldz, n, m, ncb, zt, vec4); break;
-    case 32: k8_zt<32><<<(unsigned)blocks, 256, 0, s>>>(Z, ldz, n, m, ncb, zt, vec4); break;
+    case 2: k8_zt<2><<<(unsigned)blocks, 256, 0, s>>>(Z, ldz, n, m, ncb, zt, vec4, colabs_part); break;
+    case 4: k8_zt<4><<<(unsigned)blocks, 256, 0, s>>>(Z, ldz, n, m, ncb, zt, vec4, colabs_part); break;
+    case 8: k8_zt<8><<<(unsigned)blocks, 256, 0, s>>>(Z, ldz, n, m, ncb, zt, vec4, colabs_part); break;
+    case 16: k8_zt<16><<<(unsigned)blocks, 256, 0, s>>>(Z, ldz, n, m, ncb, zt, vec4, colabs_part); break;
+    case 32: k8_zt<32><<<(unsigned)blocks, 256, 0, s>>>(Z, ldz, n, m, ncb, zt, vec4, colabs_part); break;
     default: break;
   }
+  return blocks;
+}
+
+int64_t zt_max_ctas(int64_t m, int mb) {
+  const int64_t ncb = (m + mb - 1) / mb;
+  return (148 * 16 + ncb - 1) / ncb * ncb;
 }
 
 // ------------------------------------------------------------------ K6

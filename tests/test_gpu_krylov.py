@@ -25,7 +25,12 @@ def dev(a):
 @pytest.mark.parametrize("ta", [False, True])
 @pytest.mark.parametrize("M,N,K", [(1, 1, 1), (7, 3, 5), (64, 64, 16), (130, 33, 1000),
                                    (33, 130, 257), (640, 32, 70001), (20000, 32, 640),
-                                   (5, 96, 100000), (3, 2, 0)])
+                                   (5, 96, 100000), (3, 2, 0),
+                                   # the skinny kernels (TN: M <= 48, N <= 32, long K; NN:
+                                   # K <= 96, N <= 32), full and ragged fragments
+                                   (24, 24, 100003), (48, 24, 70001), (64, 32, 65537), (1, 1, 4096),
+                                   (17, 31, 9999), (40, 8, 5001), (100003, 24, 24),
+                                   (9999, 32, 96), (50001, 5, 48), (13, 17, 3)])
 def test_gemm_against_numpy(ta, M, N, K):
     rng = np.random.default_rng(M * 7 + N * 3 + K + ta)
     A = rng.standard_normal((K, M) if ta else (M, K))
