@@ -233,11 +233,13 @@ __global__ void __launch_bounds__(256)
 // k44_skinny_tn<MT, NT>: partial C (M x N, M <= 8 MT, N <= 8 NT) = A^T B over a contiguous row
 // range per warp; the 8 warps' tiles are summed in a fixed order through shared memory and each
 // CTA writes its partial to P[blockIdx.x][M][N] (folded by k41_gemm_fold in CTA order).
-template <int MT, int NT>
+// SYM (a Gram matrix: B = A, M = N): only the tiles i <= j are computed and the rest mirrored.
+template <int MT, int NT, bool SYM = false>
 __global__ void __launch_bounds__(256)
     k44_skinny_tn(int64_t M, int64_t N, int64_t K, const double *__restrict__ A, int64_t lda,
                   const double *__restrict__ B, int64_t ldb, int64_t rows_per_warp,
                   double *__restrict__ P) {
+  static_assert(!SYM || MT == NT, "a Gram matrix is square");
   constexpr int U = MT * NT > 16 ? 2 : 4;  // k-steps (of 4 rows) in flight per warp
   __shared__ double red[MT * 8][NT * 8 + 1];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -264,14 +266,16 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int t = 0; t < MT; ++t) a[u][t] = (ok && mok[t]) ? __ldg(A + k * lda + 8 * t + cl) : 0.0;
 #pragma unroll
-      for (int t = 0; t < NT; ++t) b[u][t] = (ok && nok[t]) ? __ldg(B + k * ldb + 8 * t + cl) : 0.0;
+      for (int t = 0; t < NT; ++t)
+        b[u][t] = SYM ? a[u][t < MT ? t : 0] : ((ok && nok[t]) ? __ldg(B + k * ldb + 8 * t + cl) : 0.0);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int i = 0; i < MT; ++i)
 #pragma unroll
-        for (int j = 0; j < NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[u][i], b[u][j]);
+        for (int j = 0; j < NT; ++j)
+          if (!SYM || i <= j) dmma884(acc[i][j][0], acc[i][j][1], a[u][i], b[u][j]);
   }
   // lane holds C[8 i + l / 4][8 j + 2 (l % 4) + h]; the warps add theirs in index order
   for (int q = 0; q < 8; ++q) {
@@ -282,6 +286,7 @@ __global__ void __launch_bounds__(256)
         for (int j = 0; j < NT; ++j)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
+            if (SYM && i > j) continue;
             double &r = red[8 * i + cl][8 * j + 2 * kr + h];
             r = (q == 0) ? acc[i][j][h] : r + acc[i][j][h];
           }
@@ -291,21 +296,21 @@ __global__ void __launch_bounds__(256)
   const int64_t tot = M * N;
   for (int64_t e = threadIdx.x; e < tot; e += 256) {
     const int r = (int)(e / N), c = (int)(e - (e / N) * N);
-    P[(int64_t)blockIdx.x * tot + e] = red[r][c];
+    P[(int64_t)blockIdx.x * tot + e] = (SYM && r / 8 > c / 8) ? red[c][r] : red[r][c];
   }
 }
 
-// k45_skinny_nn<NT>: C (M x N, N <= 8 NT) = alpha A (M x K) B (K x N) + beta C with K <= 96 and M
-// the n points: B staged in shared memory once per CTA; each warp computes 8-row tiles of C
-// (grid-stride), its A fragments loaded straight from global memory.
-template <int NT>
+// k45_skinny_nn<NT, KQ, TU>: C (M x N, N <= 8 NT) = alpha A (M x K) B (K x N) + beta C with
+// K <= 4 KQ and M the n points: B staged in shared memory once per CTA; each warp computes TU
+// 8-row tiles of C per step (grid-stride), all their A fragments loaded straight from global
+// memory before any DMMA (TU x KQ loads in flight per lane).
+template <int NT, int KQ, int TU>
 __global__ void __launch_bounds__(256)
     k45_skinny_nn(int64_t M, int64_t N, int64_t K, const double *__restrict__ A, int64_t lda,
                   const double *__restrict__ B, int64_t ldb, double alpha, double beta,
                   double *__restrict__ C, int64_t ldc) {
-  constexpr int KMAX = 96;
-  __shared__ double bs[KMAX][NT * 8 + 1];
-  for (int e = threadIdx.x; e < KMAX * NT * 8; e += 256) {
+  __shared__ double bs[4 * KQ][NT * 8 + 1];
+  for (int e = threadIdx.x; e < 4 * KQ * NT * 8; e += 256) {
     const int kk = e / (NT * 8), nn = e - (e / (NT * 8)) * (NT * 8);
     bs[kk][nn] = (kk < K && nn < N) ? B[(int64_t)kk * ldb + nn] : 0.0;
   }
@@ -315,25 +320,33 @@ __global__ void __launch_bounds__(256)
   const int ksteps = (int)((K + 3) / 4);
   const bool vec2 = (ldc % 2 == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
   const int64_t tiles = (M + 7) / 8;
-  for (int64_t t = (int64_t)blockIdx.x * 8 + w; t < tiles; t += (int64_t)gridDim.x * 8) {
-    const int64_t row = 8 * t + cl;  // A fragment row of this lane
-    const bool rok = row < M;
-    double acc[NT][2];
+  const int64_t stride = (int64_t)gridDim.x * 8;
+  for (int64_t t0 = (int64_t)blockIdx.x * 8 + w; t0 < tiles; t0 += stride * TU) {
+    double a[TU][KQ];
 #pragma unroll
-    for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = 0.0;
-    double a[KMAX / 4];
+    for (int u = 0; u < TU; ++u) {
+      const int64_t row = 8 * (t0 + u * stride) + cl;
+      const bool rok = row < M;
 #pragma unroll
-    for (int q = 0; q < KMAX / 4; ++q) {
-      const int kk = 4 * q + kr;
-      a[q] = (q < ksteps && rok && kk < K) ? __ldg(A + row * lda + kk) : 0.0;
+      for (int q = 0; q < KQ; ++q) {
+        const int kk = 4 * q + kr;
+        a[u][q] = (rok && kk < K) ? __ldg(A + row * lda + kk) : 0.0;
+      }
     }
 #pragma unroll
-    for (int q = 0; q < KMAX / 4; ++q) {
-      if (q >= ksteps) break;
+    for (int u = 0; u < TU; ++u) {
+      const int64_t row = 8 * (t0 + u * stride) + cl;
+      double acc[NT][2];
 #pragma unroll
-      for (int j = 0; j < NT; ++j) dmma884(acc[j][0], acc[j][1], a[q], bs[4 * q + kr][8 * j + cl]);
-    }
-    if (row < M) {
+      for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll
+      for (int q = 0; q < KQ; ++q) {
+        if (q >= ksteps) break;
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+          dmma884(acc[j][0], acc[j][1], a[u][q], bs[4 * q + kr][8 * j + cl]);
+      }
+      if (row >= M) continue;
 #pragma unroll
       for (int j = 0; j < NT; ++j) {
         const int64_t c = 8 * j + 2 * kr;
@@ -1399,22 +1412,40 @@ static int skinny_tn_t(int64_t M, int64_t N, int64_t K, double alpha, const doub
   const int64_t ctas = skinny_tn_ctas(K, sms);
   int64_t rpw = (K + ctas * 8 - 1) / (ctas * 8);
   rpw = (rpw + 15) / 16 * 16;
-  k44_skinny_tn<MT, NT><<<(unsigned)ctas, 256, 0, s>>>(M, N, K, A, lda, B, ldb, rpw, ws);
+  if constexpr (MT == NT) {
+    if (A == B && lda == ldb && M == N)
+      k44_skinny_tn<MT, NT, true><<<(unsigned)ctas, 256, 0, s>>>(M, N, K, A, lda, B, ldb, rpw, ws);
+    else
+      k44_skinny_tn<MT, NT><<<(unsigned)ctas, 256, 0, s>>>(M, N, K, A, lda, B, ldb, rpw, ws);
+  } else {
+    k44_skinny_tn<MT, NT><<<(unsigned)ctas, 256, 0, s>>>(M, N, K, A, lda, B, ldb, rpw, ws);
+  }
   const int64_t tot = M * N;
   k41b_gemm_fold_warp<<<(unsigned)((tot + 7) / 8), 256, 0, s>>>(M, N, ctas, ws, C, ldc, alpha,
                                                                 beta);
   return 2;
 }
 
+template <int NT, int KQ, int TU>
+static int skinny_nn_kt(int64_t M, int64_t N, int64_t K, double alpha, const double *A,
+                        int64_t lda, const double *B, int64_t ldb, double beta, double *C,
+                        int64_t ldc, int sms, cudaStream_t s) {
+  int64_t ctas = (int64_t)sms * 4;
+  const int64_t need = ((M + 7) / 8 + 8 * TU - 1) / (8 * TU);
+  if (ctas > need) ctas = need < 1 ? 1 : need;
+  k45_skinny_nn<NT, KQ, TU><<<(unsigned)ctas, 256, 0, s>>>(M, N, K, A, lda, B, ldb, alpha, beta,
+                                                           C, ldc);
+  return 1;
+}
 template <int NT>
 static int skinny_nn_t(int64_t M, int64_t N, int64_t K, double alpha, const double *A,
                        int64_t lda, const double *B, int64_t ldb, double beta, double *C,
                        int64_t ldc, int sms, cudaStream_t s) {
-  int64_t ctas = (int64_t)sms * 8;
-  const int64_t need = ((M + 7) / 8 + 7) / 8;
-  if (ctas > need) ctas = need < 1 ? 1 : need;
-  k45_skinny_nn<NT><<<(unsigned)ctas, 256, 0, s>>>(M, N, K, A, lda, B, ldb, alpha, beta, C, ldc);
-  return 1;
+  if (K <= 32)
+    return skinny_nn_kt<NT, 8, 4>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, sms, s);
+  if (K <= 64)
+    return skinny_nn_kt<NT, 16, 2>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, sms, s);
+  return skinny_nn_kt<NT, 24, 1>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, sms, s);
 }
 
 int launch_gemm(int ta, int64_t M, int64_t N, int64_t K, double alpha, const double *A,

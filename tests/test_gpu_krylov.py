@@ -44,6 +44,20 @@ def test_gemm_against_numpy(ta, M, N, K):
     assert np.all(np.abs(got.cpu().numpy() - want) <= bound)
 
 
+@pytest.mark.parametrize("M,K", [(24, 100003), (32, 65536), (5, 9001), (17, 4099)])
+def test_gram_symmetric_path(M, K):
+    """A^T A with B = A (the skinny kernel computes the upper tiles and mirrors them): equal
+    to numpy within the rounding bound and exactly symmetric."""
+    rng = np.random.default_rng(M + K)
+    A = dev(rng.standard_normal((K, M)))
+    G = binding.l1dm_gemm(A, A, trans_a=True).cpu().numpy()
+    An = A.cpu().numpy()
+    want = An.T @ An
+    bound = 4 * K * 2.2e-16 * (np.abs(An).T @ np.abs(An))
+    assert np.all(np.abs(G - want) <= bound)
+    assert np.array_equal(G, G.T)
+
+
 def test_gemm_strided_views_and_beta_zero_ignores_nan():
     rng = np.random.default_rng(3)
     big = dev(rng.standard_normal((300, 50)))
