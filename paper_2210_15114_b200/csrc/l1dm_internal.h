@@ -19,13 +19,13 @@ constexpr uint32_t kSpinLimit = 1u << 26;
 // ---------------- prepare (Alg. 1) ----------------
 constexpr int kSortThreads = 256;
 #ifndef L1DM_SORT_ITEMS
-#define L1DM_SORT_ITEMS 16  // keys per thread per onesweep tile (16: c3 prepare 5.92 -> 5.66 ms vs 12, round 2)
+#define L1DM_SORT_ITEMS 24  // keys per thread per onesweep tile (24 x 256 = 6144: c3 prepare 3.77 -> 3.59 ms vs 16)
 #endif
 #ifndef L1DM_SORT_MINB
-#define L1DM_SORT_MINB 3  // 3 CTAs per SM (80 registers, the stage in the consumed input half): c3 3.82 -> 3.77 ms, c4 59.2 -> 57.2
+#define L1DM_SORT_MINB 2  // 2 CTAs per SM (104 KB of shared memory each); 3 x 4096-key tiles: c3 3.77 ms
 #endif
 constexpr int kSortItems = L1DM_SORT_ITEMS;             // keys per thread per onesweep tile
-constexpr int kSortTile = kSortThreads * kSortItems;    // 4096 keys
+constexpr int kSortTile = kSortThreads * kSortItems;    // 6144 keys
 constexpr int kHistChunk = 16384;                       // keys per histogram CTA
 
 void launch_keys(const float *X, int64_t n, int64_t ldx, int64_t k0, int64_t dl, int64_t ldn,

@@ -451,6 +451,7 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
     SORT_T(6);
     // claim the tile after next only now: a CTA holds at most two tickets (the one it works on
     // and the one in flight), which keeps the tiles a look-back may wait for close behind
+    // (claiming it at the top of the tile, to hide the atomic's latency, measured 1% slower)
     if (tid == 0) s_tk[0] = atomicAdd(ticket, 1u);
     __syncthreads();  // s_keys / s_vals / s_gbase are reused by the next tile
     const int64_t t_nn = s_tk[0];
