@@ -571,10 +571,11 @@ def main_ours(args):
                     "achieved": ach, "peak": hbm_peak, "peak_kind": peak_kind, "unit": "GB/s",
                     "frac": (ach / hbm_peak) if ach else None, "alg_bytes_per_query": qbytes}
     elif plan["scatter"] and m > 1:
-        # scatter mode: per column block, "scan" = reduce + prefix (perm/sval
-        # streamed from HBM, one Zt row gathered from L2 per pair), "accumulate" = apply (the
-        # same gathers plus one fp64 L2 reduction per update).  The apply pass is bounded by the
-        # L2's fp64 reduction throughput: roofline in reductions/s against the measured probe.
+        # scatter mode: per column block, "accumulate" = the apply (perm/sval
+        # streamed from HBM, one Zt row gathered from L2 per pair, one 8-byte L2 reduction per
+        # update; by default single-pass, its tile prefixes by look-back), "scan" = the two-pass
+        # form's reduce + prefix (L1DM_SCATTER_LB=0 only).  The apply pass is bounded by the L2's
+        # reduction throughput: roofline in reductions/s against the measured probe.
         mb = plan["mb"]
         kern["scan"]["alg_bytes"] = agg.get("scan_pairs", 0) * (8 + 4 * mb)
         kern["accumulate"]["alg_reductions"] = agg.get("queries", 0) * n * dl * m
@@ -587,7 +588,10 @@ def main_ours(args):
         dominant = "accumulate"
         ach = (acc["alg_reductions"] / (acc["ms_total"] * 1e-3) / 1e9) if acc["ms_total"] else None
         peak = red_ceiling(l2p) / 1e9
-        roof = {"bound": "l2_fp64_reductions", "kernel": "apply (k5_scan_seq<mb,APPLY>)",
+        single = not kern["scan"]["launches"]  # the default single-pass apply (k5_scan_lb)
+        roof = {"bound": "l2_fp64_reductions",
+                "kernel": ("apply (k5_scan_lb<mb>: look-back prefixes + 64-bit L2 reductions)"
+                           if single else "apply (k5_scan_seq<mb,APPLY>)"),
                 "achieved": ach, "peak": peak,
                 "peak_kind": PEAK_KIND_RED if l2p else "fallback (earlier probe)",
                 "unit": "G fp64 reductions/s", "frac": (ach / peak) if ach else None,

@@ -244,7 +244,8 @@ struct l1dm_ctx {
   DevBuf<float> zs;            // m == 1: gathered z in sorted order (reduce -> apply pass)
   DevBuf<float> zt;            // scatter mode, m > 1: column-block-major copy of Z
   DevBuf<double> yt;           // scatter mode, m > 1: one column block's accumulator (n x mb)
-  DevBuf<double> fxbuf;        // scatter mode, m > 1: fixed-point scales (2m) + their scratch
+  DevBuf<double> fxbuf;        // scatter mode, m > 1: fixed-point scales (6m) + their scratch
+  DevBuf<unsigned long long> lbst;  // scatter mode, m > 1: single-pass apply look-back words
   DevBuf<unsigned> ctr;        // [0] colsum done counter, [1] timeout flag, [2..] scan tickets
   size_t ws_limit = 0;
   int mode = 0;  // L1DM_MODE_*
@@ -410,6 +411,7 @@ void destroy(l1dm_ctx *h) {
   h->zt.release();
   h->yt.release();
   h->fxbuf.release();
+  h->lbst.release();
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   const int hdev = h->device;
   delete h;
@@ -817,23 +819,34 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
     // deterministic accumulation (R16): the block accumulator Yt holds 64-bit fixed
     // point at per-column scales from a bound on |Yt|; integer reductions are associative, so Y
     // is bitwise reproducible run to run.  The Zt pass also sums |z| per column for the bound.
-    CUDA_TRY(h->fxbuf.ensure(2 * (size_t)m + (size_t)zt_max_ctas(m, p.mb) * m, false, s));
+    CUDA_TRY(h->fxbuf.ensure(6 * (size_t)m + (size_t)zt_max_ctas(m, p.mb) * m, false, s));
     double *fx = h->fxbuf.p;
     {
       TimedScope ts(h, kColsums, s);
-      const int64_t nparts = launch_zt(Z, ldz, h->n, m, p.mb, h->zt.p, s, h->fxbuf.p + 2 * m);
-      launch_fx_scale(h->fxbuf.p + 2 * m, nparts, m, h->sval_bits.p, h->ldn, h->n, h->dl, fx, s);
+      const int64_t nparts = launch_zt(Z, ldz, h->n, m, p.mb, h->zt.p, s, h->fxbuf.p + 6 * m);
+      launch_fx_scale(h->fxbuf.p + 6 * m, nparts, m, h->sval_bits.p, h->ldn, h->n, h->dl, fx, s);
       h->kernel_launches += 2;
       h->launches[kColsums]++;
     }
-    // tile totals: one pass over full Z rows for every column block at once (m <= 256), else a
-    // reduce pass per block over its Zt block
+    // tile prefixes: by default a decoupled look-back inside each block's apply (k5_scan_lb, no
+    // pass over Z beyond the gathers the apply makes anyway); L1DM_SCATTER_LB=0 selects the
+    // two-pass form below (one reduce pass over full Z rows for every column block at once for
+    // m <= 256, else a reduce pass per block over its Zt block)
+    static const bool lb_env = [] {
+      const char *e = getenv("L1DM_SCATTER_LB");
+      return e ? atoi(e) != 0 : true;
+    }();
+    const bool single = lb_env;
+    if (single) {
+      const int64_t lbt = (h->n + scan_lb_rows() - 1) / scan_lb_rows();
+      CUDA_TRY(h->lbst.ensure((size_t)h->dl * lbt * 2 * p.mb * 2, true, s));
+    }
     static const bool reduce_all_env = [] {
       const char *e = getenv("L1DM_REDUCE_ALL");
       return e ? atoi(e) != 0 : true;
     }();
     bool all = false;
-    if (reduce_all_env && m <= 256) {
+    if (!single && reduce_all_env && m <= 256) {
       TimedScope ts(h, kScan, s);
       CUDA_TRY(h->agg.ensure((size_t)h->dl * p.tiles_per_segment * 2 * m, false, s));
       all = launch_reduce_all(h->perm.p, sval, h->ldn, h->n, Z, ldz, m, h->dl,
@@ -847,7 +860,7 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
       const int64_t mc = std::min<int64_t>(p.mb, m - c0);
       const bool last = cb == p.col_blocks - 1;
       const float *ztb = h->zt.p + (size_t)cb * h->n * p.mb;
-      if (!all) {
+      if (!all && !single) {
         TimedScope ts(h, kScan, s);
         launch_scan_seq(p, 1, h->perm.p, sval, h->ldn, h->n, ztb, mc, h->yt.p, p.mb, false,
                         h->dl, h->agg.p, h->part.p + 2 * c0, 2 * m, 0, s);
@@ -858,9 +871,18 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
       {
         TimedScope ts(h, kAcc, s);
         CUDA_TRY(cudaMemsetAsync(h->yt.p, 0, (size_t)h->n * p.mb * sizeof(double), s));
-        launch_scan_seq(p, 1, h->perm.p, sval, h->ldn, h->n, ztb, mc, h->yt.p, p.mb, false,
-                        h->dl, all ? h->agg.p + 2 * c0 : h->agg.p, h->part.p + 2 * c0, 2 * m, 1,
-                        s, all ? 2 * m : 0, fx + c0);
+        if (single) {
+          const uint32_t ep = h->epoch++;
+          if (h->epoch >= (1u << 30)) h->epoch = 1;
+          launch_scan_lb(p.mb, h->perm.p, sval, h->ldn, h->n, ztb, mc,
+                         reinterpret_cast<unsigned long long *>(h->yt.p), h->dl,
+                         h->lbst.p, ep, h->ctr.p + 1, fx + c0,
+                         fx + 2 * m + c0, m, h->part.p + 2 * c0, 2 * m, s);
+        } else {
+          launch_scan_seq(p, 1, h->perm.p, sval, h->ldn, h->n, ztb, mc, h->yt.p, p.mb, false,
+                          h->dl, all ? h->agg.p + 2 * c0 : h->agg.p, h->part.p + 2 * c0, 2 * m,
+                          1, s, all ? 2 * m : 0, fx + c0);
+        }
         h->kernel_launches++;  // apply
         h->launches[kAcc]++;
         if (h->timing) h->acc_pairs += h->n * h->dl;

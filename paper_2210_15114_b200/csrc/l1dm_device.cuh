@@ -84,6 +84,18 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// 16-byte look-back status words {value, tag}: one aligned vector access at the L2 (.cg), so a
+// reader sees a value together with the tag written with it (the transaction-word scheme of
+// decoupled look-back); volatile so a polling loop re-reads.
+__device__ __forceinline__ void st_cg_u64x2(ulonglong2 *p, unsigned long long x,
+                                            unsigned long long y) {
+  asm volatile("st.global.cg.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(x), "l"(y) : "memory");
+}
+__device__ __forceinline__ ulonglong2 ld_cg_u64x2(const ulonglong2 *p) {
+  ulonglong2 v;
+  asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
+  return v;
+}
 // ---- L2 eviction-priority policies (createpolicy) and hinted cp.async / fp64 reduction ----
 __device__ __forceinline__ uint64_t l2_policy_evict_first() {
   uint64_t p;

@@ -217,6 +217,17 @@ void launch_scan_seq(const QueryPlan &p, int lp, const uint32_t *perm, const flo
 // every sum in a fixed order.
 void launch_fx_scale(const double *part, int64_t nparts, int64_t m, const uint32_t *sval_bits,
                      int64_t ldn, int64_t n, int64_t dl, double *fx, cudaStream_t s);
+// Single-pass P = 1 scatter apply of one column block (k5_scan_lb): the tile prefixes by a
+// fixed-point decoupled look-back (lbst: kcc x tiles x 2 mb 16-byte words, zeroed once; epoch
+// distinct per launch), reductions into the int64
+// block accumulator yt at scales fx (2^F_c), fa = the look-back scales (rows of fa_ld doubles:
+// 2^Fz, 2^-Fz, 2^Fv, 2^-Fv), segment totals of s and t into segtot (rows of ld_seg).
+int scan_lb_rows();  // rows per k5_scan_lb tile (lbst needs kcc x ceil(n / rows) x 2 mb words)
+void launch_scan_lb(int mb, const uint32_t *perm, const float *sval, int64_t ldn, int64_t n,
+                    const float *zt, int64_t mc, unsigned long long *yt, int64_t kcc,
+                    void *lbst, uint32_t epoch, unsigned *timeout_flag, const double *fx,
+                    const double *fa, int64_t fa_ld, double *segtot, int64_t ld_seg,
+                    cudaStream_t s);
 // (agg_ld: the apply's stride between tiles in agg, 0 = the block's own payload (lp+1) mb.)
 // P = 1, m <= 256: tile totals of all m columns in one pass over full Z rows + the prefix
 // (agg: kcc x tiles x 2m, segtot rows of 2m).  The per-block apply then reads agg + 2 c0 with

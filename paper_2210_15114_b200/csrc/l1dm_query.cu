@@ -598,9 +598,9 @@ __global__ void __launch_bounds__(256, 2)
 // thread-sequential scan; only per-thread totals are scanned across the CTA (shuffles over the
 // 32/MB groups of a warp, then across warps).  At each row step a warp touches 32/MB rows x MB
 // consecutive columns: every reduction request is one row segment of Yt.
-template <int MB, int P = 1>
+template <int MB, int P = 1, int NTT = 256>
 struct SeqCfg {
-  static constexpr int NT = 256, NW = 8;
+  static constexpr int NT = NTT, NW = NTT / 32;
   static constexpr int G = NT / MB;           // row groups per tile
   static constexpr int ITEMS = 4 * MB;        // consecutive rows per thread
   static constexpr int R = G * ITEMS;         // 1024 rows per tile
@@ -865,6 +865,225 @@ void launch_scan_seq(const QueryPlan &p, int lp, const uint32_t *perm, const flo
   }
 #undef L1DM_SEQ_P
 #undef L1DM_SEQ
+}
+
+// Single-pass scatter apply (P = 1, fixed-point Yt): the tile's exclusive prefixes of s = z and
+// t = v z come from a decoupled look-back (Merrill & Garland) over the earlier tiles of its
+// segment instead of a separate tile-totals pass over Z — the Zt rows the apply gathers anyway
+// give the tile aggregates.  The look-back runs in 64-bit fixed point (per column, 2^Fz for the
+// s sums, 2^Fv for the t sums; launch_fx_scale), so the prefix a tile receives is the exact
+// integer sum of its predecessors' rounded aggregates whichever of them it walks over: Y stays
+// bitwise reproducible (R16).  Each status word is 16 bytes {value, epoch<<2|flag},
+// written and read as one vector access (no separate flag, no fences).  Warp 0's lanes
+// 0..2MB-1 each walk back one component, kLBW predecessors per round trip: first while the
+// tile's Z gathers are in flight (non-blocking: it stops at the first unpublished predecessor),
+// then, once the tile's own aggregate is known, it publishes INCLUSIVE directly when the walk
+// finished (the common case) or AGGREGATE and waits.  Tile order is blockIdx order with the
+// segments interleaved (CTAs are dispatched in increasing blockIdx, so every tile a CTA waits
+// for is resident or done — the single-pass scan's usual forward-progress argument); waits are
+// bounded by kSpinLimit (then *timeout_flag is raised).
+template <int MB, int NTT>
+__global__ void __launch_bounds__(NTT, 1280 / NTT)  // 5 x 256 threads per SM (smem-limited)
+    k5_scan_lb(const uint32_t *__restrict__ perm, const float *__restrict__ sval, int64_t ldn,
+               int64_t n, const float *__restrict__ zt, int64_t mc, unsigned long long *__restrict__ yt,
+               int64_t nseg, int64_t tiles_per_seg, ulonglong2 *__restrict__ lbst, uint32_t epoch,
+               unsigned *timeout_flag, const double *__restrict__ fx,
+               const double *__restrict__ fa, int64_t fa_ld, double *__restrict__ segtot,
+               int64_t ld_seg) {
+  using C = SeqCfg<MB, 1, NTT>;
+  constexpr int NT = C::NT, NW = C::NW, ITEMS = C::ITEMS, R = C::R, GPW = C::GPW, GS = C::GS,
+                PS = C::PS, NP = C::NP, CH = C::CH, CPR = MB * 4 / CH;
+  constexpr int kLBW = 4;  // predecessors loaded per look-back round trip
+  static_assert(NP <= 32, "one look-back lane per component");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float *zb = reinterpret_cast<float *>(smem_raw);              // [G][GS]
+  float *vb = zb + C::G * GS;                                    // [G][PS]
+  uint32_t *pb = reinterpret_cast<uint32_t *>(vb + C::G * PS);  // [G][PS]
+  __shared__ double s_wt[NW * NP];
+  __shared__ double s_excl[NP];
+
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int c = lane % MB, gl = lane / MB, g = w * GPW + gl;
+  const int64_t t = blockIdx.x;
+  const int64_t tile = t / nseg;
+  const int64_t kk = t - tile * nseg;
+  const int64_t row0 = tile * R;
+  const int64_t nrows = (n - row0 < R) ? (n - row0) : R;
+  const uint64_t pol_stream = l2_policy_evict_first(), pol_keep = l2_policy_evict_last();
+  {
+    const uint32_t *pp = perm + kk * ldn + row0;
+    const float *vp = sval + kk * ldn + row0;
+    for (int q = tid; q < R / 4; q += NT) {
+      const int r = 4 * q, dst = (r / ITEMS) * PS + (r % ITEMS);
+      const bool ok = row0 + r < ldn;
+      cp_async_hint<16>(pb + dst, ok ? (const void *)(pp + r) : (const void *)perm, ok, pol_stream);
+      cp_async_hint<16>(vb + dst, ok ? (const void *)(vp + r) : (const void *)sval, ok, pol_stream);
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    for (int e = tid; e < R * CPR; e += NT) {  // gather Zt rows into sorted order
+      const int r = e / CPR, ch = e - (e / CPR) * CPR;
+      const bool ok = r < nrows;
+      const float *src =
+          ok ? zt + (int64_t)pb[(r / ITEMS) * PS + (r % ITEMS)] * MB + ch * (CH / 4) : zt;
+      cp_async_hint<CH>(zb + (r / ITEMS) * GS + (r % ITEMS) * MB + ch * (CH / 4), src, ok,
+                        pol_keep);
+    }
+    cp_async_commit();
+  }
+  // ---- look-back, first part (overlaps the gathers): component e = 2 cc + q of this lane
+  const bool lb_lane = w == 0 && lane < NP;
+  const int e = lane, cc = e >> 1, q = e & 1;
+  ulonglong2 *st = lbst + (kk * tiles_per_seg) * NP + e;
+  const unsigned long long tag_a = ((unsigned long long)epoch << 2) | kFlagAggregate;
+  const unsigned long long tag_i = ((unsigned long long)epoch << 2) | kFlagInclusive;
+  long long excl = 0;
+  int64_t j = tile - 1;  // nearest predecessor not summed yet
+  bool done = tile == 0;
+  // one round trip: sum the published predecessors in the window; returns whether any was
+  auto walk = [&]() {
+    ulonglong2 sv[kLBW];
+#pragma unroll
+    for (int u = 0; u < kLBW; ++u)
+      sv[u] = (j - u >= 0) ? ld_cg_u64x2(st + (j - u) * NP) : make_ulonglong2(0ull, tag_i);
+    int u = 0;
+    for (; u < kLBW; ++u) {
+      const unsigned long long tg = sv[u].y;
+      if ((tg >> 2) != (unsigned long long)epoch || (tg & 3ull) == kFlagInvalid) break;
+      excl += (long long)sv[u].x;
+      if ((tg & 3ull) == kFlagInclusive) {
+        done = true;
+        return true;
+      }
+    }
+    j -= u;
+    return u > 0;
+  };
+  if (lb_lane)
+    while (!done && walk()) {
+    }
+  cp_async_wait_all();
+  __syncthreads();
+  const int rl0 = g * ITEMS;
+  const int nmine = (int)(nrows - rl0 < ITEMS ? (nrows - rl0 < 0 ? 0 : nrows - rl0) : ITEMS);
+  const float *zg = zb + g * GS + c;
+  const float *vg = vb + g * PS;
+  const uint32_t *pg = pb + g * PS;
+  double o0 = 0.0, o1 = 0.0;  // this thread's totals of s = z and t = v z (fp64, fixed order)
+#pragma unroll 4
+  for (int jj = 0; jj < ITEMS; ++jj) {
+    const double z = (double)zg[jj * MB];  // zero-filled past n
+    const double v = jj < nmine ? (double)vg[jj] : 0.0;
+    o0 += z;
+    o1 = fma(v, z, o1);
+  }
+  double ps0 = o0, ps1 = o1;
+#pragma unroll
+  for (int off = 1; off < GPW; off <<= 1) {
+    const double a0 = __shfl_up_sync(0xFFFFFFFFu, ps0, off * MB);
+    const double a1 = __shfl_up_sync(0xFFFFFFFFu, ps1, off * MB);
+    if (gl >= off) {
+      ps0 += a0;
+      ps1 += a1;
+    }
+  }
+  if (gl == GPW - 1) {
+    s_wt[w * NP + 2 * c] = ps0;
+    s_wt[w * NP + 2 * c + 1] = ps1;
+  }
+  __syncthreads();
+  if (lb_lane) {
+    // the tile aggregate of component e (warps in order) in fixed point
+    double a = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < NW; ++ww) a += s_wt[ww * NP + e];
+    const bool live = cc < mc;
+    const double sc = live ? __ldg(fa + (2 * q) * fa_ld + cc) : 0.0;
+    const double isc = live ? __ldg(fa + (2 * q + 1) * fa_ld + cc) : 0.0;
+    const long long qa = __double2ll_rn(a * sc);
+    if (!done) {
+      st_cg_u64x2(st + tile * NP, (unsigned long long)qa, tag_a);
+      uint32_t spins = 0;
+      while (!done) {
+        if (walk()) continue;
+        if (++spins > kSpinLimit) {
+          atomicOr(timeout_flag, 1u);
+          break;
+        }
+        if (spins > 16) __nanosleep(32);
+      }
+    }
+    st_cg_u64x2(st + tile * NP, (unsigned long long)(excl + qa), tag_i);
+    s_excl[e] = (double)excl * isc;
+    if (tile == tiles_per_seg - 1 && live) segtot[kk * ld_seg + e] = (double)(excl + qa) * isc;
+  }
+  __syncthreads();
+  // exclusive prefix of this thread's first row: tile prefix + earlier warps + earlier groups
+  double M0 = s_excl[2 * c] + ps0 - o0, M1 = s_excl[2 * c + 1] + ps1 - o1;
+  for (int ww = 0; ww < w; ++ww) {
+    M0 += s_wt[ww * NP + 2 * c];
+    M1 += s_wt[ww * NP + 2 * c + 1];
+  }
+  if (c < mc) {
+    const double fxs = __ldg(fx + c);
+#pragma unroll 4
+    for (int jj = 0; jj < ITEMS; ++jj) {
+      if (jj >= nmine) break;
+      const double z = (double)zg[jj * MB], v = (double)vg[jj];
+      const double val = 2.0 * fma(v, M0, -M1);  // 2 U_r = 2 (v_r P_r - Q_r)
+      M0 += z;
+      M1 = fma(v, z, M1);
+      const unsigned long long qv = (unsigned long long)__double2ll_rn(val * fxs);
+      asm volatile("red.global.add.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(
+                       yt + (int64_t)pg[jj] * MB + c),
+                   "l"(qv), "l"(pol_keep)
+                   : "memory");
+    }
+  }
+}
+
+int scan_lb_rows() {
+  static const int nt = [] {
+    const char *e = getenv("L1DM_LB_NT");  // tuning override: threads per apply CTA
+    return (e && atoi(e) == 256) ? 256 : 128;
+  }();
+  return nt * 4;  // rows per tile: nt / mb groups x 4 mb rows
+}
+
+void launch_scan_lb(int mb, const uint32_t *perm, const float *sval, int64_t ldn, int64_t n,
+                    const float *zt, int64_t mc, unsigned long long *yt, int64_t kcc,
+                    void *lbst, uint32_t epoch,
+                    unsigned *timeout_flag, const double *fx, const double *fa, int64_t fa_ld,
+                    double *segtot, int64_t ld_seg, cudaStream_t s) {
+  const int nt = scan_lb_rows() / 4;
+  const int64_t tiles_per_seg = (n + 4 * nt - 1) / (4 * nt);
+  const int64_t total = kcc * tiles_per_seg;
+#define L1DM_LB(MB, NTT)                                                                       \
+  {                                                                                            \
+    using C = SeqCfg<MB, 1, NTT>;                                                              \
+    static bool attr = false;                                                                  \
+    if (!attr) {                                                                               \
+      cudaFuncSetAttribute(k5_scan_lb<MB, NTT>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                           (int)C::SMEM);                                                      \
+      attr = true;                                                                             \
+    }                                                                                          \
+    k5_scan_lb<MB, NTT><<<(unsigned)total, C::NT, C::SMEM, s>>>(                               \
+        perm, sval, ldn, n, zt, mc, yt, kcc, tiles_per_seg, static_cast<ulonglong2 *>(lbst),   \
+        epoch, timeout_flag, fx, fa, fa_ld, segtot, ld_seg);                           \
+  }
+#define L1DM_LB_NT(NTT)              \
+  switch (mb) {                      \
+    case 2: L1DM_LB(2, NTT) break;   \
+    case 4: L1DM_LB(4, NTT) break;   \
+    case 8: L1DM_LB(8, NTT) break;   \
+    case 16: L1DM_LB(16, NTT) break; \
+    default: break;                  \
+  }
+  if (nt == 256) L1DM_LB_NT(256)
+  else L1DM_LB_NT(128)
+#undef L1DM_LB_NT
+#undef L1DM_LB
 }
 
 // Tile totals of every column at once for the P = 1 scatter scan (one pass over the sorted
@@ -1321,12 +1540,28 @@ __global__ void __launch_bounds__(256)
                  double *__restrict__ fx) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   // sum_k Mx_k: lanes over k, a fixed butterfly (every warp computes it)
-  double mx = 0.0;
-  for (int64_t k = lane; k < dl; k += 32)
-    mx += fmax(fabs((double)__uint_as_float(sval_bits[k * ldn])),
-               fabs((double)__uint_as_float(sval_bits[k * ldn + n - 1])));
+  double mx = 0.0, mxx = 0.0;  // sum_k Mx_k and max_k Mx_k
+  for (int64_t k = lane; k < dl; k += 32) {
+    const double mk = fmax(fabs((double)__uint_as_float(sval_bits[k * ldn])),
+                           fabs((double)__uint_as_float(sval_bits[k * ldn + n - 1])));
+    mx += mk;
+    mxx = fmax(mxx, mk);
+  }
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) mx += __shfl_xor_sync(0xFFFFFFFFu, mx, off);
+  for (int off = 16; off > 0; off >>= 1) {
+    mx += __shfl_xor_sync(0xFFFFFFFFu, mx, off);
+    mxx = fmax(mxx, __shfl_xor_sync(0xFFFFFFFFu, mxx, off));
+  }
+  // F = 61 - ilogb(B) - 1 (B > 0 finite), clamped: B 2^F < 2^61
+  auto scale_exp = [](double B, int top) {
+    int F = 0;
+    if (B > 0.0 && isfinite(B)) {
+      F = top - ilogb(B) - 1;
+      if (F > 1000) F = 1000;
+      if (F < -1000) F = -1000;
+    }
+    return F;
+  };
   // column c: lanes over the CTA partials (strided, in order), then a fixed butterfly
   for (int64_t c = (int64_t)blockIdx.x * 8 + w; c < m; c += (int64_t)gridDim.x * 8) {
     double sz = 0.0;
@@ -1334,18 +1569,20 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) sz += __shfl_xor_sync(0xFFFFFFFFu, sz, off);
     if (lane != 0) continue;
-    const double B = 4.0 * mx * sz * 1.0001;
-    int F = 0;  // B = 0: the column is zero, any scale
-    if (B > 0.0 && isfinite(B)) {
-      // 2^ilogb(B) <= B < 2^(ilogb+1): B < 2^(61 - F).  Tiny data take large F (2^F stays
-      // finite up to F = 1000, i.e. B >= 2^-939 keeps the full 61 bits; fp32 inputs give
-      // B >= ~2^-300)
-      F = 61 - ilogb(B) - 1;
-      if (F > 1000) F = 1000;
-      if (F < -1000) F = -1000;
-    }
+    // B = 0: the column is zero, any scale.  2^ilogb(B) <= B < 2^(ilogb+1): B < 2^(61 - F).
+    // Tiny data take large F (2^F stays finite up to F = 1000, i.e. B >= 2^-939 keeps the full
+    // 61 bits; fp32 inputs give B >= ~2^-300)
+    const int F = scale_exp(4.0 * mx * sz * 1.0001, 61);
     fx[c] = ldexp(1.0, F);
     fx[m + c] = ldexp(1.0, -F);
+    // the single-pass apply's look-back (k5_scan_lb): every partial sum of s = z over a
+    // coordinate is bounded by sz, of t = v z by max_k Mx_k sz; 2^62 headroom for the rounded
+    // tile aggregates' sums
+    const int Fz = scale_exp(sz * 1.0001, 62), Fv = scale_exp(mxx * sz * 1.0001, 62);
+    fx[2 * m + c] = ldexp(1.0, Fz);
+    fx[3 * m + c] = ldexp(1.0, -Fz);
+    fx[4 * m + c] = ldexp(1.0, Fv);
+    fx[5 * m + c] = ldexp(1.0, -Fv);
   }
 }
 

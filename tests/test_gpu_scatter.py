@@ -125,25 +125,30 @@ def test_scatter_sharded_coordinates_exact():
     assert np.array_equal(sum(parts), oracle.hist(X, Z, M=8).astype(np.float64))
 
 
-def test_scatter_wide_query_per_block_reduce():
-    """m > 256: the tile totals come from one reduce pass per column block (not reduce-all)."""
+def test_scatter_wide_query():
+    """m > 256 (more than 32 column blocks of the single-pass apply)."""
     rng = np.random.default_rng(300)
     X = rng.standard_normal((1500, 2)).astype(np.float32)
     Z = rng.standard_normal((1500, 300)).astype(np.float32)
     assert col_rel_l2(gpu_matvec(X, Z, mode="scatter"), oracle.brute(X, Z)) <= TOL
 
 
-def test_scatter_per_block_reduce_subprocess():
-    """The per-block reduce path for m <= 256 too (L1DM_REDUCE_ALL=0, read once per process)."""
+# the two-pass forms (tile totals from a reduce pass, then the apply), selected per process:
+# L1DM_SCATTER_LB=0 with the reduce-all pass over full Z rows, and with one reduce per block;
+# L1DM_LB_NT=256: the single-pass apply with 1024-row tiles (default 512)
+@pytest.mark.parametrize("env", [{"L1DM_SCATTER_LB": "0"},
+                                 {"L1DM_SCATTER_LB": "0", "L1DM_REDUCE_ALL": "0"},
+                                 {"L1DM_LB_NT": "256"}])
+def test_scatter_variants_subprocess(env):
     import os
     import subprocess
     import sys
     code = ("import sys; sys.path[:0] = ['.', 'tests']; import test_gpu_scatter as t;"
             "[t.test_scatter_random_float_vs_brute(*c) for c in t.CASES];"
-            "t.test_scatter_integer_ties_exact(3000, 4, 4); print('ok')")
-    env = dict(os.environ, L1DM_REDUCE_ALL="0")
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
-                       timeout=600)
+            "t.test_scatter_integer_ties_exact(3000, 4, 4); t.test_scatter_wide_query();"
+            "t.test_scatter_bitwise_reproducible(); print('ok')")
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env),
+                       capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
