@@ -246,6 +246,8 @@ struct l1dm_ctx {
   DevBuf<double> yt;           // scatter mode, m > 1: one column block's accumulator (n x mb)
   DevBuf<double> fxbuf;        // scatter mode, m > 1: fixed-point scales (6m) + their scratch
   DevBuf<unsigned long long> lbst;  // scatter mode, m > 1: single-pass apply look-back words
+  uint32_t lb_epoch = 0;            // k5_scan_lb launches (their words carry it mod 4)
+  int64_t lb_geom = -1;             // slot geometry the words were written with
   DevBuf<unsigned> ctr;        // [0] colsum done counter, [1] timeout flag, [2..] scan tickets
   size_t ws_limit = 0;
   int mode = 0;  // L1DM_MODE_*
@@ -412,6 +414,7 @@ void destroy(l1dm_ctx *h) {
   h->yt.release();
   h->fxbuf.release();
   h->lbst.release();
+  h->lb_geom = -1;
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   const int hdev = h->device;
   delete h;
@@ -838,8 +841,16 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
     }();
     const bool single = lb_env;
     if (single) {
+      // every launch rewrites all dl x tiles x 2mb words, so a stale word on the same geometry is
+      // the previous launch's (another epoch mod 4); on a new geometry the words are zeroed
       const int64_t lbt = (h->n + scan_lb_rows() - 1) / scan_lb_rows();
-      CUDA_TRY(h->lbst.ensure((size_t)h->dl * lbt * 2 * p.mb * 2, true, s));
+      const size_t words = (size_t)h->dl * lbt * 2 * p.mb;
+      const int64_t geom = (int64_t)words * 64 + p.mb;
+      CUDA_TRY(h->lbst.ensure(words, false, s));
+      if (geom != h->lb_geom) {
+        CUDA_TRY(cudaMemsetAsync(h->lbst.p, 0, words * sizeof(unsigned long long), s));
+        h->lb_geom = geom;
+      }
     }
     static const bool reduce_all_env = [] {
       const char *e = getenv("L1DM_REDUCE_ALL");
@@ -872,8 +883,7 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
         TimedScope ts(h, kAcc, s);
         CUDA_TRY(cudaMemsetAsync(h->yt.p, 0, (size_t)h->n * p.mb * sizeof(double), s));
         if (single) {
-          const uint32_t ep = h->epoch++;
-          if (h->epoch >= (1u << 30)) h->epoch = 1;
+          const uint32_t ep = ++h->lb_epoch;
           launch_scan_lb(p.mb, h->perm.p, sval, h->ldn, h->n, ztb, mc,
                          reinterpret_cast<unsigned long long *>(h->yt.p), h->dl,
                          h->lbst.p, ep, h->ctr.p + 1, fx + c0,

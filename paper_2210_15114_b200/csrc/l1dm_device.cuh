@@ -84,18 +84,6 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-// 16-byte look-back status words {value, tag}: one aligned vector access at the L2 (.cg), so a
-// reader sees a value together with the tag written with it (the transaction-word scheme of
-// decoupled look-back); volatile so a polling loop re-reads.
-__device__ __forceinline__ void st_cg_u64x2(ulonglong2 *p, unsigned long long x,
-                                            unsigned long long y) {
-  asm volatile("st.global.cg.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(x), "l"(y) : "memory");
-}
-__device__ __forceinline__ ulonglong2 ld_cg_u64x2(const ulonglong2 *p) {
-  ulonglong2 v;
-  asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
-  return v;
-}
 // ---- L2 eviction-priority policies (createpolicy) and hinted cp.async / fp64 reduction ----
 __device__ __forceinline__ uint64_t l2_policy_evict_first() {
   uint64_t p;
@@ -136,6 +124,20 @@ __device__ __forceinline__ void st_global_u32(uint32_t *p, uint32_t v) {
 __device__ __forceinline__ void st_u32_hint(uint32_t *p, uint32_t v, uint64_t pol) {
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v),
                "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64_hint(const unsigned long long *p,
+                                                                  uint64_t pol) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.L2::cache_hint.u64 %0, [%1], %2;"
+               : "=l"(v)
+               : "l"(p), "l"(pol)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64_hint(unsigned long long *p, unsigned long long v,
+                                                    uint64_t pol) {
+  asm volatile("st.relaxed.gpu.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol)
                : "memory");
 }
 __device__ __forceinline__ void st_f64_hint(double *p, double v, uint64_t pol) {

@@ -867,14 +867,24 @@ void launch_scan_seq(const QueryPlan &p, int lp, const uint32_t *perm, const flo
 #undef L1DM_SEQ
 }
 
+// Look-back status word of k5_scan_lb: [63:4] the 60-bit signed fixed-point value, [3:2] the
+// launch's epoch mod 4, [1:0] the flag (0 = not published).  One 8-byte access: a reader sees a
+// value with its own tag.  Every launch rewrites every word of its geometry (and the words are
+// zeroed when the geometry changes), so a stale word is from the previous launch: two epoch
+// bits tell them apart with margin.
+__device__ __forceinline__ unsigned long long lb_word(long long v, uint32_t ep, uint32_t flag) {
+  return ((unsigned long long)v << 4) | (unsigned long long)((ep << 2) | flag);
+}
+
 // Single-pass scatter apply (P = 1, fixed-point Yt): the tile's exclusive prefixes of s = z and
 // t = v z come from a decoupled look-back (Merrill & Garland) over the earlier tiles of its
 // segment instead of a separate tile-totals pass over Z — the Zt rows the apply gathers anyway
 // give the tile aggregates.  The look-back runs in 64-bit fixed point (per column, 2^Fz for the
 // s sums, 2^Fv for the t sums; launch_fx_scale), so the prefix a tile receives is the exact
 // integer sum of its predecessors' rounded aggregates whichever of them it walks over: Y stays
-// bitwise reproducible (R16).  Each status word is 16 bytes {value, epoch<<2|flag},
-// written and read as one vector access (no separate flag, no fences).  Warp 0's lanes
+// bitwise reproducible (R16).  Each status word is 8 bytes {value, epoch, flag}
+// (lb_word; no separate flag, no fences; epochs count this kernel's launches per handle, and
+// the words are zeroed whenever the slot geometry changes).  Warp 0's lanes
 // 0..2MB-1 each walk back one component, kLBW predecessors per round trip: first while the
 // tile's Z gathers are in flight (non-blocking: it stops at the first unpublished predecessor),
 // then, once the tile's own aggregate is known, it publishes INCLUSIVE directly when the walk
@@ -886,7 +896,8 @@ template <int MB, int NTT>
 __global__ void __launch_bounds__(NTT, 1280 / NTT)  // 5 x 256 threads per SM (smem-limited)
     k5_scan_lb(const uint32_t *__restrict__ perm, const float *__restrict__ sval, int64_t ldn,
                int64_t n, const float *__restrict__ zt, int64_t mc, unsigned long long *__restrict__ yt,
-               int64_t nseg, int64_t tiles_per_seg, ulonglong2 *__restrict__ lbst, uint32_t epoch,
+               int64_t nseg, int64_t tiles_per_seg, unsigned long long *__restrict__ lbst,
+               uint32_t epoch,
                unsigned *timeout_flag, const double *__restrict__ fx,
                const double *__restrict__ fa, int64_t fa_ld, double *__restrict__ segtot,
                int64_t ld_seg) {
@@ -935,24 +946,25 @@ __global__ void __launch_bounds__(NTT, 1280 / NTT)  // 5 x 256 threads per SM (s
   // ---- look-back, first part (overlaps the gathers): component e = 2 cc + q of this lane
   const bool lb_lane = w == 0 && lane < NP;
   const int e = lane, cc = e >> 1, q = e & 1;
-  ulonglong2 *st = lbst + (kk * tiles_per_seg) * NP + e;
-  const unsigned long long tag_a = ((unsigned long long)epoch << 2) | kFlagAggregate;
-  const unsigned long long tag_i = ((unsigned long long)epoch << 2) | kFlagInclusive;
+  unsigned long long *st = lbst + (kk * tiles_per_seg) * NP + e;
+  const uint32_t ep2 = epoch & 3u;
+  const uint64_t pol_lb = pol_stream;  // status words are read back within a few tiles
   long long excl = 0;
   int64_t j = tile - 1;  // nearest predecessor not summed yet
   bool done = tile == 0;
   // one round trip: sum the published predecessors in the window; returns whether any was
   auto walk = [&]() {
-    ulonglong2 sv[kLBW];
+    unsigned long long sv[kLBW];
 #pragma unroll
     for (int u = 0; u < kLBW; ++u)
-      sv[u] = (j - u >= 0) ? ld_cg_u64x2(st + (j - u) * NP) : make_ulonglong2(0ull, tag_i);
+      sv[u] = (j - u >= 0) ? ld_relaxed_u64_hint(st + (j - u) * NP, pol_lb)
+                           : lb_word(0, ep2, kFlagInclusive);
     int u = 0;
     for (; u < kLBW; ++u) {
-      const unsigned long long tg = sv[u].y;
-      if ((tg >> 2) != (unsigned long long)epoch || (tg & 3ull) == kFlagInvalid) break;
-      excl += (long long)sv[u].x;
-      if ((tg & 3ull) == kFlagInclusive) {
+      const uint32_t tg = (uint32_t)sv[u] & 0xFu;
+      if ((tg >> 2) != ep2 || (tg & 3u) == kFlagInvalid) break;
+      excl += (long long)sv[u] >> 4;  // the 60-bit signed value
+      if ((tg & 3u) == kFlagInclusive) {
         done = true;
         return true;
       }
@@ -1003,7 +1015,7 @@ __global__ void __launch_bounds__(NTT, 1280 / NTT)  // 5 x 256 threads per SM (s
     const double isc = live ? __ldg(fa + (2 * q + 1) * fa_ld + cc) : 0.0;
     const long long qa = __double2ll_rn(a * sc);
     if (!done) {
-      st_cg_u64x2(st + tile * NP, (unsigned long long)qa, tag_a);
+      st_relaxed_u64_hint(st + tile * NP, lb_word(qa, ep2, kFlagAggregate), pol_lb);
       uint32_t spins = 0;
       while (!done) {
         if (walk()) continue;
@@ -1014,7 +1026,7 @@ __global__ void __launch_bounds__(NTT, 1280 / NTT)  // 5 x 256 threads per SM (s
         if (spins > 16) __nanosleep(32);
       }
     }
-    st_cg_u64x2(st + tile * NP, (unsigned long long)(excl + qa), tag_i);
+    st_relaxed_u64_hint(st + tile * NP, lb_word(excl + qa, ep2, kFlagInclusive), pol_lb);
     s_excl[e] = (double)excl * isc;
     if (tile == tiles_per_seg - 1 && live) segtot[kk * ld_seg + e] = (double)(excl + qa) * isc;
   }
@@ -1069,7 +1081,8 @@ void launch_scan_lb(int mb, const uint32_t *perm, const float *sval, int64_t ldn
       attr = true;                                                                             \
     }                                                                                          \
     k5_scan_lb<MB, NTT><<<(unsigned)total, C::NT, C::SMEM, s>>>(                               \
-        perm, sval, ldn, n, zt, mc, yt, kcc, tiles_per_seg, static_cast<ulonglong2 *>(lbst),   \
+        perm, sval, ldn, n, zt, mc, yt, kcc, tiles_per_seg,                                    \
+        static_cast<unsigned long long *>(lbst),                                               \
         epoch, timeout_flag, fx, fa, fa_ld, segtot, ld_seg);                           \
   }
 #define L1DM_LB_NT(NTT)              \
@@ -1576,9 +1589,9 @@ __global__ void __launch_bounds__(256)
     fx[c] = ldexp(1.0, F);
     fx[m + c] = ldexp(1.0, -F);
     // the single-pass apply's look-back (k5_scan_lb): every partial sum of s = z over a
-    // coordinate is bounded by sz, of t = v z by max_k Mx_k sz; 2^62 headroom for the rounded
-    // tile aggregates' sums
-    const int Fz = scale_exp(sz * 1.0001, 62), Fv = scale_exp(mxx * sz * 1.0001, 62);
+    // coordinate is bounded by sz, of t = v z by max_k Mx_k sz; the rounded tile aggregates'
+    // sums stay below 2^58 (the look-back words carry 60-bit signed values)
+    const int Fz = scale_exp(sz * 1.0001, 58), Fv = scale_exp(mxx * sz * 1.0001, 58);
     fx[2 * m + c] = ldexp(1.0, Fz);
     fx[3 * m + c] = ldexp(1.0, -Fz);
     fx[4 * m + c] = ldexp(1.0, Fv);
