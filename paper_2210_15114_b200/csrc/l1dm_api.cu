@@ -840,6 +840,7 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
       return e ? atoi(e) != 0 : true;
     }();
     const bool single = lb_env;
+
     if (single) {
       // every launch rewrites all dl x tiles x 2mb words, so a stale word on the same geometry is
       // the previous launch's (another epoch mod 4); on a new geometry the words are zeroed
@@ -881,6 +882,8 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
       }
       {
         TimedScope ts(h, kAcc, s);
+        // (clearing Yt in the write-out's pass instead, as it reads it, measured 7x slower for
+        // that kernel than this memset: c3 G = 8 shard query 3.94 vs 2.77 ms)
         CUDA_TRY(cudaMemsetAsync(h->yt.p, 0, (size_t)h->n * p.mb * sizeof(double), s));
         if (single) {
           const uint32_t ep = ++h->lb_epoch;
@@ -897,7 +900,27 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
         h->launches[kAcc]++;
         if (h->timing) h->acc_pairs += h->n * h->dl;
       }
-      {
+      if (single) {
+        // S, g of the block folded into the write-out (no k4_totals launch)
+        TimedScope ts(h, kColsums, s);
+        unsigned long long *ytq = reinterpret_cast<unsigned long long *>(h->yt.p);
+        const int64_t nb = last ? nblocks : 1;
+        if (blocked) {
+          launch_block_out_fx(ytq, p.mb, mc, h->hsum.p, h->part.p + 2 * c0, 2 * m, h->dl,
+                              h->Sg.p + c0, m, Y + (size_t)cb * h->n * p.mb, p.mb, 0, h->n, s,
+                              nullptr, 0, fx + m + c0);
+          if (events && events[cb]) CUDA_TRY(cudaEventRecord((cudaEvent_t)events[cb], s));
+        }
+        for (int64_t b = 0; !blocked && b < nb; ++b) {
+          int64_t i0 = 0, i1 = h->n;
+          if (last) block_range(b, i0, i1);
+          launch_block_out_fx(ytq, p.mb, mc, h->hsum.p, h->part.p + 2 * c0, 2 * m, h->dl,
+                              h->Sg.p + c0, m, Y + c0, ldy, i0, i1, s, pd, c0, fx + m + c0);
+          if (last && events && events[b]) CUDA_TRY(cudaEventRecord((cudaEvent_t)events[b], s));
+        }
+        h->kernel_launches += blocked ? 1 : nb;  // block out(s)
+        h->launches[kColsums]++;
+      } else {
         TimedScope ts(h, kColsums, s);
         launch_totals(h->part.p + 2 * c0, 2 * m, h->dl, mc, h->Sg.p + c0, h->Sg.p + m + c0, s);
         const int64_t nb = last ? nblocks : 1;

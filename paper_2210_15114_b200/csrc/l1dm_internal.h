@@ -222,6 +222,13 @@ void launch_fx_scale(const double *part, int64_t nparts, int64_t m, const uint32
 // distinct per launch), reductions into the int64
 // block accumulator yt at scales fx (2^F_c), fa = the look-back scales (rows of fa_ld doubles:
 // 2^Fz, 2^-Fz, 2^Fv, 2^-Fv), segment totals of s and t into segtot (rows of ld_seg).
+// Block write-out after k5_scan_lb (mb even): S and g of the block from segtot (rows of ld_seg,
+// dl coordinates) stored to Sg[c] / Sg[m_all + c], Y rows [i0, i1) = Yt 2^-F + g - h S (or the
+// owners' inbox rows with pd).
+void launch_block_out_fx(const unsigned long long *yt, int mb, int64_t mc, const double *hsum,
+                         const double *segtot, int64_t ld_seg, int64_t dl, double *Sg,
+                         int64_t m_all, double *Y, int64_t ldy, int64_t i0, int64_t i1,
+                         cudaStream_t s, const PeerDst *pd, int64_t pc0, const double *fx_inv);
 int scan_lb_rows();  // rows per k5_scan_lb tile (lbst needs kcc x ceil(n / rows) x 2 mb words)
 void launch_scan_lb(int mb, const uint32_t *perm, const float *sval, int64_t ldn, int64_t n,
                     const float *zt, int64_t mc, unsigned long long *yt, int64_t kcc,

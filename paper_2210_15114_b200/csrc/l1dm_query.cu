@@ -1537,6 +1537,85 @@ void launch_block_out(const double *yt, int mb, int64_t mc, const double *hsum, 
                                                          PeerDst{}, 0, fx);
 }
 
+// Block write-out of the single-pass fixed-point apply (k5_scan_lb), with the block's query totals
+// folded in (no k4_totals launch): S_c = coordinate 0's segment total of s, g_c = sum_k T_kc
+// (warp per column, lanes over k, a fixed butterfly: every CTA derives the same values; CTA 0
+// also stores them to Sg), then Y[i][c0 + c] = Yt[i][c] 2^-F_c + g_c - h_i S_c for rows
+// [i0, i1), two columns per thread (16-byte loads, and stores when Y allows).
+template <bool PUSH>
+__global__ void __launch_bounds__(256)
+    k9f_block_out(const unsigned long long *__restrict__ yt, int mb, int64_t mc,
+                  const double *__restrict__ hsum, const double *__restrict__ segtot,
+                  int64_t ld_seg, int64_t dl, double *__restrict__ Sg, int64_t m_all,
+                  double *__restrict__ Y, int64_t ldy, int64_t i0, int64_t i1, PeerDst pd,
+                  int64_t pc0, const double *__restrict__ fx_inv, int vec) {
+  __shared__ double s_S[32], s_g[32], s_f[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int c = w; c < mb; c += 8) {
+    double gk = 0.0;
+    if (c < mc)
+      for (int64_t k = lane; k < dl; k += 32) gk += __ldg(segtot + k * ld_seg + 2 * c + 1);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) gk += __shfl_xor_sync(0xFFFFFFFFu, gk, off);
+    if (lane == 0) {
+      const double S = c < mc ? __ldg(segtot + 2 * c) : 0.0;
+      s_S[c] = S;
+      s_g[c] = gk;
+      s_f[c] = c < mc ? __ldg(fx_inv + c) : 0.0;
+      if (blockIdx.x == 0 && c < mc) {
+        Sg[c] = S;
+        Sg[m_all + c] = gk;
+      }
+    }
+  }
+  __syncthreads();
+  const int hp = mb >> 1;  // column pairs per row
+  const int64_t total = (i1 - i0) * hp;
+  for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * 256) {
+    const int64_t i = i0 + e / hp;
+    const int c = 2 * (int)(e - (e / hp) * hp);
+    const ulonglong2 *yp = reinterpret_cast<const ulonglong2 *>(yt + i * mb + c);
+    const ulonglong2 q = *yp;
+    if (c >= mc) continue;
+    const double h = __ldg(hsum + i);
+    const double o0 = (double)(long long)q.x * s_f[c] + fma(-h, s_S[c], s_g[c]);
+    const double o1 = (double)(long long)q.y * s_f[c + 1] + fma(-h, s_S[c + 1], s_g[c + 1]);
+    if constexpr (PUSH) {
+      double *row = peer_row(pd, i) + pc0 + c;
+      row[0] = o0;
+      if (c + 1 < mc) row[1] = o1;
+    } else {
+      double *yo = Y + i * ldy + c;
+      if (vec && c + 1 < mc) {
+        __stcs(reinterpret_cast<double2 *>(yo), make_double2(o0, o1));
+      } else {
+        __stcs(yo, o0);
+        if (c + 1 < mc) __stcs(yo + 1, o1);
+      }
+    }
+  }
+  if constexpr (PUSH) __threadfence_system();  // the sends precede the signal kernel's flag
+}
+
+void launch_block_out_fx(const unsigned long long *yt, int mb, int64_t mc, const double *hsum,
+                         const double *segtot, int64_t ld_seg, int64_t dl, double *Sg,
+                         int64_t m_all, double *Y, int64_t ldy, int64_t i0, int64_t i1,
+                         cudaStream_t s, const PeerDst *pd, int64_t pc0, const double *fx_inv) {
+  if (i1 <= i0) return;
+  int64_t blocks = ((i1 - i0) * (mb / 2) + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  const int vec = (reinterpret_cast<uintptr_t>(Y) % 16 == 0 && ldy % 2 == 0) ? 1 : 0;
+  if (pd && pd->world > 0)
+    k9f_block_out<true><<<(unsigned)blocks, 256, 0, s>>>(yt, mb, mc, hsum, segtot, ld_seg, dl,
+                                                         Sg, m_all, Y, ldy, i0, i1, *pd, pc0,
+                                                         fx_inv, vec);
+  else
+    k9f_block_out<false><<<(unsigned)blocks, 256, 0, s>>>(yt, mb, mc, hsum, segtot, ld_seg, dl,
+                                                          Sg, m_all, Y, ldy, i0, i1, PeerDst{}, 0,
+                                                          fx_inv, vec);
+}
+
 // The fixed-point scales of a query (SEQ_APPLY_FX), one per column c.  Every term
 // 2U^k_r = 2 (v_r P_r - Q_r) satisfies |2U^k| <= 4 Mx_k Sz_c (|P_r| and |Q_r| / Mx_k are partial
 // sums of |z|), Mx_k the largest |x| of coordinate k (the ends of its sorted row) and Sz_c the
@@ -1998,8 +2077,49 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
   for (int q = 0; q < MB; ++q) dacc[q] = 0.0;
   int cnt = 0;
-  for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * 256) {
+  const int64_t stride = (int64_t)gridDim.x * 256;
+  int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if constexpr (MB % 4 == 0) {
+    // whole-block rows, 4 rows in flight per thread (loads of all four issued first); the
+    // stride is a multiple of ncb, so a thread stays on one column block
+    if (vec4 && m % MB == 0) {
+      for (; e + 3 * stride < total; e += 4 * stride) {
+        float4 t[4][MB / 4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t eu = e + u * stride, i = eu / ncb, cb = eu - i * ncb;
+          const float4 *src = reinterpret_cast<const float4 *>(Z + i * ldz + cb * MB);
+#pragma unroll
+          for (int q = 0; q < MB / 4; ++q) t[u][q] = __ldcs(src + q);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t eu = e + u * stride, i = eu / ncb, cb = eu - i * ncb;
+          float4 *dst = reinterpret_cast<float4 *>(zt + (cb * n + i) * MB);
+#pragma unroll
+          for (int q = 0; q < MB / 4; ++q) dst[q] = t[u][q];
+          if (part) {
+#pragma unroll
+            for (int q = 0; q < MB / 4; ++q) {
+              acc[4 * q] += fabsf(t[u][q].x);
+              acc[4 * q + 1] += fabsf(t[u][q].y);
+              acc[4 * q + 2] += fabsf(t[u][q].z);
+              acc[4 * q + 3] += fabsf(t[u][q].w);
+            }
+            if (++cnt == 64) {
+#pragma unroll
+              for (int q = 0; q < MB; ++q) {
+                dacc[q] += (double)acc[q];
+                acc[q] = 0.0f;
+              }
+              cnt = 0;
+            }
+          }
+        }
+      }
+    }
+  }
+  for (; e < total; e += stride) {
     const int64_t i = e / ncb, cb = e - (e / ncb) * ncb;
     const int64_t c0 = cb * MB;
     const float *src = Z + i * ldz + c0;
