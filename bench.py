@@ -632,13 +632,16 @@ def main_ours(args):
             # fp64 reduction into Y (apply pass), each at the L2's measured per-lane rate
             # (tools/l2_probe.cu: gather_lane_per_s, red_lane_per_s); the passes run in turn,
             # so the ceiling is the harmonic combination of the two rates
-            sc = kern["scan"]
-            pairs = agg.get("scan_pairs", 0)
+            single = not kern["scan"]["launches"]  # default: the single-pass apply (k5_scan_lb<1>)
+            sc = kern["accumulate"] if single else kern["scan"]
+            pairs = agg.get("accumulate_pairs" if single else "scan_pairs", 0)
             g = max(l2p.get("gather_lane_per_s", 2.69e11), l2p.get("gather_lane_4MiB_per_s", 0))
             r = max(l2p.get("red_lane_per_s", 1.745e11), l2p.get("red_lane_8MiB_per_s", 0))
             peak = 1.0 / (1.0 / g + 1.0 / r) / 1e9
             ach = pairs / (sc["ms_total"] * 1e-3) / 1e9 if sc["ms_total"] else None
-            roof = {"bound": "l2_random_access", "kernel": "scan (k5_scan_m1 reduce/prefix/apply)",
+            roof = {"bound": "l2_random_access",
+                    "kernel": ("apply (k5_scan_lb<1>: gather, look-back, 64-bit reductions)" if single
+                               else "scan (k5_scan_m1 reduce/prefix/apply)"),
                     "achieved": ach, "peak": peak,
                     "unit": "G (point, coordinate) pairs/s: one random 4-B gather + one random "
                             "fp64 reduction each",

@@ -777,9 +777,22 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
     fprintf(stderr, "[l1dm] plan + workspace %.3f ms\n",
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - dbg_t0)
                 .count());
-  if (p.scatter && m == 1) {
-    // scatter mode, m == 1: zero Y, reduce/prefix/apply over every coordinate adding 2U into Y,
-    // then the epilogue g - h_i S
+  // scatter mode: by default the single-pass apply (k5_scan_lb; tile prefixes by a fixed-point
+  // look-back inside the apply, no pass over Z beyond the gathers the apply makes anyway) for
+  // every m, m = 1 included (one 1-column block); L1DM_SCATTER_LB=0 selects the two-pass forms
+  // (m = 1: reduce / prefix / apply with fp64 atomics into Y; m > 1: a reduce pass for the tile
+  // totals, then the apply)
+  static const bool lb_env = [] {
+    const char *e = getenv("L1DM_SCATTER_LB");
+    return e ? atoi(e) != 0 : true;
+  }();
+  if (p.scatter && m == 1 && lb_env) {
+    CUDA_TRY(h->zt.ensure((size_t)h->n, false, s));
+    CUDA_TRY(h->yt.ensure((size_t)h->n, false, s));
+  }
+  if (p.scatter && m == 1 && !lb_env) {
+    // scatter mode, m == 1, two-pass: zero Y, reduce/prefix/apply over every coordinate adding
+    // 2U into Y, then the epilogue g - h_i S
     CUDA_TRY(cudaMemset2DAsync(Y, (size_t)ldy * sizeof(double), 0, sizeof(double), (size_t)h->n, s));
     {
       TimedScope ts(h, kScan, s);
@@ -831,20 +844,15 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
       h->kernel_launches += 2;
       h->launches[kColsums]++;
     }
-    // tile prefixes: by default a decoupled look-back inside each block's apply (k5_scan_lb, no
-    // pass over Z beyond the gathers the apply makes anyway); L1DM_SCATTER_LB=0 selects the
-    // two-pass form below (one reduce pass over full Z rows for every column block at once for
-    // m <= 256, else a reduce pass per block over its Zt block)
-    static const bool lb_env = [] {
-      const char *e = getenv("L1DM_SCATTER_LB");
-      return e ? atoi(e) != 0 : true;
-    }();
+    // tile prefixes: by default a decoupled look-back inside each block's apply (k5_scan_lb);
+    // L1DM_SCATTER_LB=0: the two-pass form below (one reduce pass over full Z rows for every
+    // column block at once for m <= 256, else a reduce pass per block over its Zt block)
     const bool single = lb_env;
 
     if (single) {
       // every launch rewrites all dl x tiles x 2mb words, so a stale word on the same geometry is
       // the previous launch's (another epoch mod 4); on a new geometry the words are zeroed
-      const int64_t lbt = (h->n + scan_lb_rows() - 1) / scan_lb_rows();
+      const int64_t lbt = (h->n + scan_lb_rows(p.mb) - 1) / scan_lb_rows(p.mb);
       const size_t words = (size_t)h->dl * lbt * 2 * p.mb;
       const int64_t geom = (int64_t)words * 64 + p.mb;
       CUDA_TRY(h->lbst.ensure(words, false, s));

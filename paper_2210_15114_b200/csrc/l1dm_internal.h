@@ -229,7 +229,7 @@ void launch_block_out_fx(const unsigned long long *yt, int mb, int64_t mc, const
                          const double *segtot, int64_t ld_seg, int64_t dl, double *Sg,
                          int64_t m_all, double *Y, int64_t ldy, int64_t i0, int64_t i1,
                          cudaStream_t s, const PeerDst *pd, int64_t pc0, const double *fx_inv);
-int scan_lb_rows();  // rows per k5_scan_lb tile (lbst needs kcc x ceil(n / rows) x 2 mb words)
+int scan_lb_rows(int mb);  // rows per k5_scan_lb tile (lbst: kcc x ceil(n / rows) x 2 mb words)
 void launch_scan_lb(int mb, const uint32_t *perm, const float *sval, int64_t ldn, int64_t n,
                     const float *zt, int64_t mc, unsigned long long *yt, int64_t kcc,
                     void *lbst, uint32_t epoch, unsigned *timeout_flag, const double *fx,

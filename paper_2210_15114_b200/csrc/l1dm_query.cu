@@ -602,7 +602,7 @@ template <int MB, int P = 1, int NTT = 256>
 struct SeqCfg {
   static constexpr int NT = NTT, NW = NTT / 32;
   static constexpr int G = NT / MB;           // row groups per tile
-  static constexpr int ITEMS = 4 * MB;        // consecutive rows per thread
+  static constexpr int ITEMS = MB == 1 ? 8 : 4 * MB;  // consecutive rows per thread
   static constexpr int R = G * ITEMS;         // 1024 rows per tile
   static constexpr int GPW = 32 / MB;         // groups per warp
   static constexpr int GS = ITEMS * MB + MB;  // padded floats per group of the Z stage
@@ -1055,21 +1055,26 @@ __global__ void __launch_bounds__(NTT, 1280 / NTT)  // 5 x 256 threads per SM (s
   }
 }
 
-int scan_lb_rows() {
-  static const int nt = [] {
-    const char *e = getenv("L1DM_LB_NT");  // tuning override: threads per apply CTA
-    return (e && atoi(e) == 256) ? 256 : 128;
+// threads per k5_scan_lb CTA: 128 (512-row tiles) for mb >= 2, 256 (2048-row tiles) for mb = 1,
+// or L1DM_LB_NT (tuning override, 128 or 256)
+static int scan_lb_threads(int mb) {
+  static const int env = [] {
+    const char *e = getenv("L1DM_LB_NT");
+    return e ? atoi(e) : 0;
   }();
-  return nt * 4;  // rows per tile: nt / mb groups x 4 mb rows
+  if (env == 128 || env == 256) return env;
+  return mb == 1 ? 256 : 128;
 }
+
+int scan_lb_rows(int mb) { return scan_lb_threads(mb) * (mb == 1 ? 8 : 4); }
 
 void launch_scan_lb(int mb, const uint32_t *perm, const float *sval, int64_t ldn, int64_t n,
                     const float *zt, int64_t mc, unsigned long long *yt, int64_t kcc,
                     void *lbst, uint32_t epoch,
                     unsigned *timeout_flag, const double *fx, const double *fa, int64_t fa_ld,
                     double *segtot, int64_t ld_seg, cudaStream_t s) {
-  const int nt = scan_lb_rows() / 4;
-  const int64_t tiles_per_seg = (n + 4 * nt - 1) / (4 * nt);
+  const int nt = scan_lb_threads(mb);
+  const int64_t tiles_per_seg = (n + scan_lb_rows(mb) - 1) / scan_lb_rows(mb);
   const int64_t total = kcc * tiles_per_seg;
 #define L1DM_LB(MB, NTT)                                                                       \
   {                                                                                            \
@@ -1087,6 +1092,7 @@ void launch_scan_lb(int mb, const uint32_t *perm, const float *sval, int64_t ldn
   }
 #define L1DM_LB_NT(NTT)              \
   switch (mb) {                      \
+    case 1: L1DM_LB(1, NTT) break;   \
     case 2: L1DM_LB(2, NTT) break;   \
     case 4: L1DM_LB(4, NTT) break;   \
     case 8: L1DM_LB(8, NTT) break;   \
@@ -1569,18 +1575,23 @@ __global__ void __launch_bounds__(256)
     }
   }
   __syncthreads();
-  const int hp = mb >> 1;  // column pairs per row
+  const int hp = mb > 1 ? mb >> 1 : 1;  // column pairs per row (mb = 1: one column)
   const int64_t total = (i1 - i0) * hp;
   for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * 256) {
     const int64_t i = i0 + e / hp;
-    const int c = 2 * (int)(e - (e / hp) * hp);
-    const ulonglong2 *yp = reinterpret_cast<const ulonglong2 *>(yt + i * mb + c);
-    const ulonglong2 q = *yp;
+    const int c = mb > 1 ? 2 * (int)(e - (e / hp) * hp) : 0;
+    ulonglong2 q;
+    if (mb > 1)
+      q = *reinterpret_cast<const ulonglong2 *>(yt + i * mb + c);
+    else
+      q = make_ulonglong2(yt[i], 0ull);
     if (c >= mc) continue;
     const double h = __ldg(hsum + i);
     const double o0 = (double)(long long)q.x * s_f[c] + fma(-h, s_S[c], s_g[c]);
-    const double o1 = (double)(long long)q.y * s_f[c + 1] + fma(-h, s_S[c + 1], s_g[c + 1]);
+    const double o1 = c + 1 < mc ? (double)(long long)q.y * s_f[c + 1] +
+                                       fma(-h, s_S[c + 1], s_g[c + 1])
+                                 : 0.0;
     if constexpr (PUSH) {
       double *row = peer_row(pd, i) + pc0 + c;
       row[0] = o0;
@@ -1603,7 +1614,7 @@ void launch_block_out_fx(const unsigned long long *yt, int mb, int64_t mc, const
                          int64_t m_all, double *Y, int64_t ldy, int64_t i0, int64_t i1,
                          cudaStream_t s, const PeerDst *pd, int64_t pc0, const double *fx_inv) {
   if (i1 <= i0) return;
-  int64_t blocks = ((i1 - i0) * (mb / 2) + 255) / 256;
+  int64_t blocks = ((i1 - i0) * (mb > 1 ? mb / 2 : 1) + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
   const int vec = (reinterpret_cast<uintptr_t>(Y) % 16 == 0 && ldy % 2 == 0) ? 1 : 0;
   if (pd && pd->world > 0)
@@ -2188,6 +2199,7 @@ int64_t launch_zt(const float *Z, int64_t ldz, int64_t n, int64_t m, int mb, flo
   // with the |z| sums: whole multiples of ncb CTAs keep every thread on one block
   if (colabs_part) blocks = (blocks + ncb - 1) / ncb * ncb;
   switch (mb) {
+    case 1: k8_zt<1><<<(unsigned)blocks, 256, 0, s>>>(Z, ldz, n, m, ncb, zt, vec4, colabs_part); break;
     case 2: k8_zt<2><<<(unsigned)blocks, 256, 0, s>>>(Z, ldz, n, m, ncb, zt, vec4, colabs_part); break;
     case 4: k8_zt<4><<<(unsigned)blocks, 256, 0, s>>>(Z, ldz, n, m, ncb, zt, vec4, colabs_part); break;
     case 8: k8_zt<8><<<(unsigned)blocks, 256, 0, s>>>(Z, ldz, n, m, ncb, zt, vec4, colabs_part); break;

@@ -18,8 +18,10 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-9
 
 # m spans block widths 2 / 4 / 8 and ragged last blocks; n spans the 1024-row tiles' edges.
+# m = 1 runs the same single-pass kernel with one-column blocks (2048-row tiles).
 CASES = [(1, 1, 2), (2, 1, 3), (3, 2, 2), (100, 3, 4), (1023, 2, 5), (1024, 3, 8), (1025, 2, 9),
-         (2047, 3, 16), (3073, 4, 7), (5000, 2, 17), (700, 5, 64), (1500, 3, 65), (4097, 2, 3)]
+         (2047, 3, 16), (3073, 4, 7), (5000, 2, 17), (700, 5, 64), (1500, 3, 65), (4097, 2, 3),
+         (1, 1, 1), (2049, 3, 1), (5000, 4, 1)]
 
 
 @pytest.mark.parametrize("n,d,m", CASES)
@@ -35,7 +37,8 @@ def test_scatter_random_float_vs_brute(n, d, m):
         assert col_rel_l2(Ys, Yr) <= TOL
 
 
-@pytest.mark.parametrize("n,d,m", [(4099, 3, 2), (3000, 4, 4), (2500, 2, 7), (1500, 3, 32)])
+@pytest.mark.parametrize("n,d,m", [(4099, 3, 2), (3000, 4, 4), (2500, 2, 7), (1500, 3, 32),
+                                   (4100, 3, 1)])
 def test_scatter_integer_ties_exact(n, d, m):
     rng = np.random.default_rng(7 * n + m + 1)
     X = rng.integers(0, 5, size=(n, d)).astype(np.float32)
