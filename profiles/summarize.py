@@ -66,7 +66,9 @@ for r in rows[2:]:
     sc = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}
     rb = float(r[hdr.index("dram__bytes_read.sum")]) * sc[units[hdr.index("dram__bytes_read.sum")]]
     wb = float(r[hdr.index("dram__bytes_write.sum")]) * sc[units[hdr.index("dram__bytes_write.sum")]]
-    if "k5_reduce_all" in name:  # scatter mode: tile totals of every column (timing kind scan)
+    if "k5_scan_lb" in name:  # scatter mode, single pass: the apply (timing kind accumulate)
+        kind = "scatter_accumulate"
+    elif "k5_reduce_all" in name:  # scatter mode: tile totals of every column (timing kind scan)
         kind = "scatter_scan"
     elif "k5_scan_seq" in name:  # scatter mode: <mb, 0> reduce (timing kind scan), <mb, 1> apply
         kind = "scatter_accumulate" if ", 1>" in name or ",1>" in name else "scatter_scan"
