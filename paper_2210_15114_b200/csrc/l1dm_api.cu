@@ -246,6 +246,8 @@ struct l1dm_ctx {
   DevBuf<double> yt;           // scatter mode, m > 1: one column block's accumulator (n x mb)
   DevBuf<double> fxbuf;        // scatter mode, m > 1: fixed-point scales (6m) + their scratch
   DevBuf<unsigned long long> lbst;  // scatter mode, m > 1: single-pass apply look-back words
+  DevBuf<float> xr;                 // X in point order (n x dl), built for odd-p single passes
+  bool xr_ready = false;
   uint32_t lb_epoch = 0;            // k5_scan_lb launches (their words carry it mod 4)
   int64_t lb_geom = -1;             // slot geometry the words were written with
   DevBuf<unsigned> ctr;        // [0] colsum done counter, [1] timeout flag, [2..] scan tickets
@@ -414,6 +416,7 @@ void destroy(l1dm_ctx *h) {
   h->yt.release();
   h->fxbuf.release();
   h->lbst.release();
+  h->xr.release();
   h->lb_geom = -1;
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   const int hdev = h->device;
@@ -1052,6 +1055,67 @@ l1dm_status lp_device(l1dm_ctx *h, int lp, const float *Z, int64_t ldz, int64_t 
     CUDA_TRY(h->U.ensure((size_t)p.kc * (size_t)h->n * (size_t)m, false, s));
     l1dm_status rs = ensure_rank(h, s);  // the accumulate gathers U at each point's rank
     if (rs != L1DM_OK) return rs;
+  }
+  static const bool lb_env = [] {
+    const char *e = getenv("L1DM_SCATTER_LB");
+    return e ? atoi(e) != 0 : true;
+  }();
+  if (p.scatter && lb_env && scan_lb_supported(p.mb, lp)) {
+    // single pass: per column block the apply prefixes all p + 1 moments by the
+    // fixed-point look-back and adds 2 sum_t c_t v^(p-t) M_t; after the last block one DMMA
+    // expansion subtracts the totals' part, sum_k sum_t c_t x_ik^(p-t) T_kt (X rebuilt in point
+    // order from the sorted tables once per handle)
+    if (h->ctr.count < 3) CUDA_TRY(h->ctr.ensure(3, true, s));  // [1]: the timeout word
+    if (!h->xr_ready) {
+      CUDA_TRY(h->xr.ensure((size_t)h->n * h->dl, false, s));
+      launch_unsort(h->perm.p, sval, h->ldn, h->n, h->dl, h->xr.p, s);
+      h->kernel_launches++;
+      h->xr_ready = true;
+    }
+    CUDA_TRY(h->fxbuf.ensure(2 * (size_t)K * m + (size_t)zt_max_ctas(m, p.mb) * m, false, s));
+    double *fa = h->fxbuf.p;
+    {
+      TimedScope ts(h, kColsums, s);
+      const int64_t nparts = launch_zt(Z, ldz, h->n, m, p.mb, h->zt.p, s, fa + 2 * (size_t)K * m);
+      launch_lb_scales(fa + 2 * (size_t)K * m, nparts, m, h->sval_bits.p, h->ldn, h->n, h->dl, lp,
+                       fa, s);
+      h->kernel_launches += 2;
+      h->launches[kColsums]++;
+    }
+    const int64_t lbt = (h->n + scan_lb_rows(p.mb) - 1) / scan_lb_rows(p.mb);
+    const size_t words = (size_t)h->dl * lbt * K * p.mb;
+    const int64_t geom = ((int64_t)words * 64 + p.mb) * 8 + K;
+    CUDA_TRY(h->lbst.ensure(words, false, s));
+    if (geom != h->lb_geom) {
+      CUDA_TRY(cudaMemsetAsync(h->lbst.p, 0, words * sizeof(unsigned long long), s));
+      h->lb_geom = geom;
+    }
+    for (int cb = 0; cb < p.col_blocks; ++cb) {
+      const int64_t c0 = (int64_t)cb * p.mb;
+      const int64_t mc = std::min<int64_t>(p.mb, m - c0);
+      const float *ztb = h->zt.p + (size_t)cb * h->n * p.mb;
+      TimedScope ts(h, kAcc, s);
+      CUDA_TRY(cudaMemsetAsync(h->yt.p, 0, (size_t)h->n * p.mb * sizeof(double), s));
+      const uint32_t ep = ++h->lb_epoch;
+      launch_scan_lb(p.mb, h->perm.p, sval, h->ldn, h->n, ztb, mc,
+                     reinterpret_cast<unsigned long long *>(h->yt.p), h->dl, h->lbst.p, ep,
+                     h->ctr.p + 1, nullptr, fa + c0, m, h->part.p + K * c0, ld_seg, s, lp);
+      launch_block_out(h->yt.p, p.mb, mc, nullptr, nullptr, nullptr, Y + c0, ldy, 0, h->n, s);
+      h->kernel_launches += 2;
+      h->launches[kAcc]++;
+      if (h->timing) h->acc_pairs += h->n * h->dl;
+    }
+    {
+      TimedScope ts(h, kColsums, s);
+      CUDA_TRY(h->agg.ensure(lp_totals_workspace(h->dl, m, lp) / sizeof(double) + 1, false, s));
+      h->kernel_launches += launch_lp_totals_expand(h->xr.p, h->dl, h->n, h->dl, m, h->part.p,
+                                                    ld_seg, lp, h->agg.p, Y, ldy, s);
+      h->launches[kColsums]++;
+    }
+    CUDA_TRY(cudaGetLastError());
+    h->queries++;
+    h->m_last = m;
+    return L1DM_OK;
   }
   {
     TimedScope ts(h, kColsums, s);

@@ -234,7 +234,25 @@ void launch_scan_lb(int mb, const uint32_t *perm, const float *sval, int64_t ldn
                     const float *zt, int64_t mc, unsigned long long *yt, int64_t kcc,
                     void *lbst, uint32_t epoch, unsigned *timeout_flag, const double *fx,
                     const double *fa, int64_t fa_ld, double *segtot, int64_t ld_seg,
-                    cudaStream_t s);
+                    cudaStream_t s, int lp = 1);
+// (lp in {3, 5, 7}: (lp + 1) moments, yt points at a fp64 block accumulator, fx unused, fa rows
+//  (2t, 2t + 1) = the scale of moment t and its inverse; segtot rows of ld_seg hold (lp + 1) mc
+//  moments per coordinate; the totals' part of the value is added by launch_lp_totals_expand.)
+bool scan_lb_supported(int mb, int lp);
+// Odd p in one pass: Y -= E, E_ic = sum_k sum_t C(p,t) (-1)^t x_ik^(p-t) T_ktc from the apply's
+// segment totals (segtot rows of ld_seg, (p+1) moments per column) and X in point order (n x dl,
+// row stride ldx); work: lp_totals_workspace bytes.  Returns the kernels launched.
+size_t lp_totals_workspace(int64_t dl, int64_t m, int p);
+int launch_lp_totals_expand(const float *X, int64_t ldx, int64_t n, int64_t dl, int64_t m,
+                            const double *segtot, int64_t ld_seg, int p, double *work, double *Y,
+                            int64_t ldy, cudaStream_t s);
+// X in point order from the sorted tables: xr[perm[k][r] * dl + k] = sval[k][r] (once per handle).
+void launch_unsort(const uint32_t *perm, const float *sval, int64_t ldn, int64_t n, int64_t dl,
+                   float *xr, cudaStream_t s);
+// Look-back scales of (lp + 1) moments per column (fa rows 2t, 2t + 1: 2^F_t and 2^-F_t, F_t from
+// the bound max_k Mx_k^t sum_i |z_ic| < 2^58), from launch_zt's |z| partials.
+void launch_lb_scales(const double *part, int64_t nparts, int64_t m, const uint32_t *sval_bits,
+                      int64_t ldn, int64_t n, int64_t dl, int lp, double *fa, cudaStream_t s);
 // (agg_ld: the apply's stride between tiles in agg, 0 = the block's own payload (lp+1) mb.)
 // P = 1, m <= 256: tile totals of all m columns in one pass over full Z rows + the prefix
 // (agg: kcc x tiles x 2m, segtot rows of 2m).  The per-block apply then reads agg + 2 c0 with

@@ -892,7 +892,13 @@ __device__ __forceinline__ unsigned long long lb_word(long long v, uint32_t ep, 
 // segments interleaved (CTAs are dispatched in increasing blockIdx, so every tile a CTA waits
 // for is resident or done — the single-pass scan's usual forward-progress argument); waits are
 // bounded by kSpinLimit (then *timeout_flag is raised).
-template <int MB, int NTT>
+//
+// P > 1 (odd l_p^p): K = P + 1 moments z v^t per column, all prefixed by the same
+// look-back (K mb components, one lane each), and each row adds only the prefix part of its term,
+// 2 sum_t c_t v^(P-t) M_t, into a fp64 block accumulator (fp64 reductions, yt points at doubles):
+// the coordinate totals' part, sum_k sum_t c_t x_ik^(P-t) T_kt, is one DMMA expansion after the
+// last block (launch_lp_totals_expand), so no pass has to know the totals before the apply.
+template <int MB, int NTT, int P>
 __global__ void __launch_bounds__(NTT, 1280 / NTT)  // 5 x 256 threads per SM (smem-limited)
     k5_scan_lb(const uint32_t *__restrict__ perm, const float *__restrict__ sval, int64_t ldn,
                int64_t n, const float *__restrict__ zt, int64_t mc, unsigned long long *__restrict__ yt,
@@ -901,9 +907,9 @@ __global__ void __launch_bounds__(NTT, 1280 / NTT)  // 5 x 256 threads per SM (s
                unsigned *timeout_flag, const double *__restrict__ fx,
                const double *__restrict__ fa, int64_t fa_ld, double *__restrict__ segtot,
                int64_t ld_seg) {
-  using C = SeqCfg<MB, 1, NTT>;
+  using C = SeqCfg<MB, P, NTT>;
   constexpr int NT = C::NT, NW = C::NW, ITEMS = C::ITEMS, R = C::R, GPW = C::GPW, GS = C::GS,
-                PS = C::PS, NP = C::NP, CH = C::CH, CPR = MB * 4 / CH;
+                PS = C::PS, NP = C::NP, CH = C::CH, CPR = MB * 4 / CH, K = P + 1;
   constexpr int kLBW = 4;  // predecessors loaded per look-back round trip
   static_assert(NP <= 32, "one look-back lane per component");
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -945,7 +951,7 @@ __global__ void __launch_bounds__(NTT, 1280 / NTT)  // 5 x 256 threads per SM (s
   }
   // ---- look-back, first part (overlaps the gathers): component e = 2 cc + q of this lane
   const bool lb_lane = w == 0 && lane < NP;
-  const int e = lane, cc = e >> 1, q = e & 1;
+  const int e = lane, cc = e / K, q = e - (e / K) * K;
   unsigned long long *st = lbst + (kk * tiles_per_seg) * NP + e;
   const uint32_t ep2 = epoch & 3u;
   const uint64_t pol_lb = pol_stream;  // status words are read back within a few tiles
@@ -982,27 +988,34 @@ __global__ void __launch_bounds__(NTT, 1280 / NTT)  // 5 x 256 threads per SM (s
   const float *zg = zb + g * GS + c;
   const float *vg = vb + g * PS;
   const uint32_t *pg = pb + g * PS;
-  double o0 = 0.0, o1 = 0.0;  // this thread's totals of s = z and t = v z (fp64, fixed order)
+  double o[K];  // this thread's totals of the moments z v^t (P = 1: s = z, t = v z; fp64, fixed order)
+#pragma unroll
+  for (int q = 0; q < K; ++q) o[q] = 0.0;
 #pragma unroll 4
   for (int jj = 0; jj < ITEMS; ++jj) {
     const double z = (double)zg[jj * MB];  // zero-filled past n
     const double v = jj < nmine ? (double)vg[jj] : 0.0;
-    o0 += z;
-    o1 = fma(v, z, o1);
+    double zv = z;
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      o[q] += zv;  // (q = 1: z v is exact in fp64, so this equals fma(v, z, o))
+      zv *= v;
+    }
   }
-  double ps0 = o0, ps1 = o1;
+  double ps[K];
+#pragma unroll
+  for (int q = 0; q < K; ++q) ps[q] = o[q];
 #pragma unroll
   for (int off = 1; off < GPW; off <<= 1) {
-    const double a0 = __shfl_up_sync(0xFFFFFFFFu, ps0, off * MB);
-    const double a1 = __shfl_up_sync(0xFFFFFFFFu, ps1, off * MB);
-    if (gl >= off) {
-      ps0 += a0;
-      ps1 += a1;
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      const double a = __shfl_up_sync(0xFFFFFFFFu, ps[q], off * MB);
+      if (gl >= off) ps[q] += a;
     }
   }
   if (gl == GPW - 1) {
-    s_wt[w * NP + 2 * c] = ps0;
-    s_wt[w * NP + 2 * c + 1] = ps1;
+#pragma unroll
+    for (int q = 0; q < K; ++q) s_wt[w * NP + K * c + q] = ps[q];
   }
   __syncthreads();
   if (lb_lane) {
@@ -1032,25 +1045,42 @@ __global__ void __launch_bounds__(NTT, 1280 / NTT)  // 5 x 256 threads per SM (s
   }
   __syncthreads();
   // exclusive prefix of this thread's first row: tile prefix + earlier warps + earlier groups
-  double M0 = s_excl[2 * c] + ps0 - o0, M1 = s_excl[2 * c + 1] + ps1 - o1;
+  double M[K];
+#pragma unroll
+  for (int q2 = 0; q2 < K; ++q2) M[q2] = s_excl[K * c + q2] + ps[q2] - o[q2];
   for (int ww = 0; ww < w; ++ww) {
-    M0 += s_wt[ww * NP + 2 * c];
-    M1 += s_wt[ww * NP + 2 * c + 1];
+#pragma unroll
+    for (int q2 = 0; q2 < K; ++q2) M[q2] += s_wt[ww * NP + K * c + q2];
   }
   if (c < mc) {
-    const double fxs = __ldg(fx + c);
+    double fxs = 0.0;
+    if constexpr (P == 1) fxs = __ldg(fx + c);
 #pragma unroll 4
     for (int jj = 0; jj < ITEMS; ++jj) {
       if (jj >= nmine) break;
       const double z = (double)zg[jj * MB], v = (double)vg[jj];
-      const double val = 2.0 * fma(v, M0, -M1);  // 2 U_r = 2 (v_r P_r - Q_r)
-      M0 += z;
-      M1 = fma(v, z, M1);
-      const unsigned long long qv = (unsigned long long)__double2ll_rn(val * fxs);
-      asm volatile("red.global.add.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(
-                       yt + (int64_t)pg[jj] * MB + c),
-                   "l"(qv), "l"(pol_keep)
-                   : "memory");
+      if constexpr (P == 1) {
+        const double val = 2.0 * fma(v, M[0], -M[1]);  // 2 U_r = 2 (v_r P_r - Q_r)
+        M[0] += z;
+        M[1] = fma(v, z, M[1]);
+        const unsigned long long qv = (unsigned long long)__double2ll_rn(val * fxs);
+        asm volatile("red.global.add.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(
+                         yt + (int64_t)pg[jj] * MB + c),
+                     "l"(qv), "l"(pol_keep)
+                     : "memory");
+      } else {
+        // 2 sum_t c_t v^(P-t) M_t in Horner form over descending powers of v
+        double val = 2.0 * lp_coef<P>(0) * M[0];
+#pragma unroll
+        for (int q2 = 1; q2 < K; ++q2) val = fma(val, v, 2.0 * lp_coef<P>(q2) * M[q2]);
+        double zv = z;
+#pragma unroll
+        for (int q2 = 0; q2 < K; ++q2) {
+          M[q2] += zv;
+          zv *= v;
+        }
+        red_add_f64(reinterpret_cast<double *>(yt) + (int64_t)pg[jj] * MB + c, val, pol_keep);
+      }
     }
   }
 }
@@ -1072,37 +1102,64 @@ void launch_scan_lb(int mb, const uint32_t *perm, const float *sval, int64_t ldn
                     const float *zt, int64_t mc, unsigned long long *yt, int64_t kcc,
                     void *lbst, uint32_t epoch,
                     unsigned *timeout_flag, const double *fx, const double *fa, int64_t fa_ld,
-                    double *segtot, int64_t ld_seg, cudaStream_t s) {
+                    double *segtot, int64_t ld_seg, cudaStream_t s, int lp) {
   const int nt = scan_lb_threads(mb);
   const int64_t tiles_per_seg = (n + scan_lb_rows(mb) - 1) / scan_lb_rows(mb);
   const int64_t total = kcc * tiles_per_seg;
-#define L1DM_LB(MB, NTT)                                                                       \
+#define L1DM_LB(MB, NTT, P)                                                                    \
   {                                                                                            \
-    using C = SeqCfg<MB, 1, NTT>;                                                              \
+    using C = SeqCfg<MB, P, NTT>;                                                              \
     static bool attr = false;                                                                  \
     if (!attr) {                                                                               \
-      cudaFuncSetAttribute(k5_scan_lb<MB, NTT>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+      cudaFuncSetAttribute(k5_scan_lb<MB, NTT, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,\
                            (int)C::SMEM);                                                      \
       attr = true;                                                                             \
     }                                                                                          \
-    k5_scan_lb<MB, NTT><<<(unsigned)total, C::NT, C::SMEM, s>>>(                               \
+    k5_scan_lb<MB, NTT, P><<<(unsigned)total, C::NT, C::SMEM, s>>>(                            \
         perm, sval, ldn, n, zt, mc, yt, kcc, tiles_per_seg,                                    \
-        static_cast<unsigned long long *>(lbst),                                               \
-        epoch, timeout_flag, fx, fa, fa_ld, segtot, ld_seg);                           \
+        static_cast<unsigned long long *>(lbst), epoch, timeout_flag, fx, fa, fa_ld, segtot,   \
+        ld_seg);                                                                               \
   }
-#define L1DM_LB_NT(NTT)              \
-  switch (mb) {                      \
-    case 1: L1DM_LB(1, NTT) break;   \
-    case 2: L1DM_LB(2, NTT) break;   \
-    case 4: L1DM_LB(4, NTT) break;   \
-    case 8: L1DM_LB(8, NTT) break;   \
-    case 16: L1DM_LB(16, NTT) break; \
-    default: break;                  \
+#define L1DM_LB_NT(NTT)                 \
+  if (lp == 1) {                        \
+    switch (mb) {                       \
+      case 1: L1DM_LB(1, NTT, 1) break; \
+      case 2: L1DM_LB(2, NTT, 1) break; \
+      case 4: L1DM_LB(4, NTT, 1) break; \
+      case 8: L1DM_LB(8, NTT, 1) break; \
+      case 16: L1DM_LB(16, NTT, 1) break; \
+      default: break;                   \
+    }                                   \
+  } else if (lp == 3) {                 \
+    switch (mb) {                       \
+      case 2: L1DM_LB(2, NTT, 3) break; \
+      case 4: L1DM_LB(4, NTT, 3) break; \
+      case 8: L1DM_LB(8, NTT, 3) break; \
+      default: break;                   \
+    }                                   \
+  } else if (lp == 5 || lp == 7) {      \
+    switch (mb) {                       \
+      case 2: if (lp == 5) L1DM_LB(2, NTT, 5) else L1DM_LB(2, NTT, 7) break; \
+      case 4: if (lp == 5) L1DM_LB(4, NTT, 5) else L1DM_LB(4, NTT, 7) break; \
+      default: break;                   \
+    }                                   \
   }
-  if (nt == 256) L1DM_LB_NT(256)
-  else L1DM_LB_NT(128)
+  if (nt == 256) {
+    L1DM_LB_NT(256)
+  } else {
+    L1DM_LB_NT(128)
+  }
 #undef L1DM_LB_NT
 #undef L1DM_LB
+}
+
+// Whether launch_scan_lb has a kernel for (mb, lp): one look-back lane per component, (lp + 1) mb
+// <= 32.
+bool scan_lb_supported(int mb, int lp) {
+  if (lp == 1) return mb == 1 || mb == 2 || mb == 4 || mb == 8 || mb == 16;
+  if (lp == 3) return mb == 2 || mb == 4 || mb == 8;
+  if (lp == 5 || lp == 7) return mb == 2 || mb == 4;
+  return false;
 }
 
 // Tile totals of every column at once for the P = 1 scatter scan (one pass over the sorted
@@ -1687,6 +1744,65 @@ __global__ void __launch_bounds__(256)
     fx[4 * m + c] = ldexp(1.0, Fv);
     fx[5 * m + c] = ldexp(1.0, -Fv);
   }
+}
+
+// Look-back scales for the odd-p single pass: per column c and moment t = 0..lp, 2^F with
+// max_k Mx_k^t sum_i |z_ic| 2^F < 2^58 (every partial sum of z v^t over a coordinate is below the
+// bound), summed in the same fixed orders as k8c_fx_scale.
+__global__ void __launch_bounds__(256)
+    k8e_lb_scales(const double *__restrict__ part, int64_t nparts, int64_t m,
+                  const uint32_t *__restrict__ sval_bits, int64_t ldn, int64_t n, int64_t dl,
+                  int lp, double *__restrict__ fa) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double mxx = 0.0;
+  for (int64_t k = lane; k < dl; k += 32)
+    mxx = fmax(mxx, fmax(fabs((double)__uint_as_float(sval_bits[k * ldn])),
+                         fabs((double)__uint_as_float(sval_bits[k * ldn + n - 1]))));
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) mxx = fmax(mxx, __shfl_xor_sync(0xFFFFFFFFu, mxx, off));
+  for (int64_t c = (int64_t)blockIdx.x * 8 + w; c < m; c += (int64_t)gridDim.x * 8) {
+    double sz = 0.0;
+    for (int64_t t = lane; t < nparts; t += 32) sz += part[t * m + c];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sz += __shfl_xor_sync(0xFFFFFFFFu, sz, off);
+    if (lane != 0) continue;
+    double B = sz * 1.0001;
+    for (int t = 0; t <= lp; ++t) {
+      int F = 0;
+      if (B > 0.0 && isfinite(B)) {
+        F = 58 - ilogb(B) - 1;
+        if (F > 1000) F = 1000;
+        if (F < -1000) F = -1000;
+      }
+      fa[(2 * t) * m + c] = ldexp(1.0, F);
+      fa[(2 * t + 1) * m + c] = ldexp(1.0, -F);
+      B *= mxx;
+    }
+  }
+}
+
+void launch_lb_scales(const double *part, int64_t nparts, int64_t m, const uint32_t *sval_bits,
+                      int64_t ldn, int64_t n, int64_t dl, int lp, double *fa, cudaStream_t s) {
+  k8e_lb_scales<<<(unsigned)((m + 7) / 8), 256, 0, s>>>(part, nparts, m, sval_bits, ldn, n, dl,
+                                                        lp, fa);
+}
+
+// X in point order from the sorted tables, xr[perm[k][r] dl + k] = sval[k][r]: the odd-p single
+// pass needs x_ik^(p-t) by point for its totals expansion (launch_lp_totals_expand); built once
+// per handle on the first such query.
+__global__ void __launch_bounds__(256)
+    k3x_unsort(const uint32_t *__restrict__ perm, const float *__restrict__ sval, int64_t ldn,
+               int64_t n, int64_t dl, float *__restrict__ xr) {
+  const int64_t k = blockIdx.y;
+  for (int64_t r = (int64_t)blockIdx.x * 256 + threadIdx.x; r < n; r += (int64_t)gridDim.x * 256)
+    xr[(int64_t)perm[k * ldn + r] * dl + k] = sval[k * ldn + r];
+}
+
+void launch_unsort(const uint32_t *perm, const float *sval, int64_t ldn, int64_t n, int64_t dl,
+                   float *xr, cudaStream_t s) {
+  int64_t bx = (n + 255) / 256;
+  if (bx > 1024) bx = 1024;
+  k3x_unsort<<<dim3((unsigned)bx, (unsigned)dl), 256, 0, s>>>(perm, sval, ldn, n, dl, xr);
 }
 
 void launch_fx_scale(const double *part, int64_t nparts, int64_t m, const uint32_t *sval_bits,

@@ -333,7 +333,8 @@ static void launch_k12(const float *X, int64_t ldx, const float *Z, int64_t ldz,
 // K14 on DMMA: grid (point tiles, column tiles), 8 warps; warp w owns points 16 (w % 4) .. +16
 // x columns 32 (w / 4) .. +32.  K = (P-1) d: for t = 1..P-1 the A operand is x^(P-t) (staged in
 // shared memory as fp64), B = c_t W_t.  hp_i = sum_k x_ik^P accumulates while staging.
-template <int P, int G, int KS>
+// SUB (odd p's totals term, launch_lp_totals_expand): Y -= the same expansion.
+template <int P, int G, int KS, bool SUB = false>
 __global__ void __launch_bounds__(256)
     k14_moment_expand_dmma(const float *__restrict__ X, int64_t ldx, int64_t n, int64_t d,
                            int64_t m, const double *__restrict__ Wc,
@@ -434,13 +435,19 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int64_t c = c0 + cw + 8 * j + 2 * (lane & 3) + h;
-        if (c < m) Y[i * ldy + c] = fma(S[c], s_hp[r], acc[g][j][h] + G_[c]);
+        if (c < m) {
+          const double e = fma(S[c], s_hp[r], acc[g][j][h] + G_[c]);
+          if constexpr (SUB)
+            Y[i * ldy + c] -= e;
+          else
+            Y[i * ldy + c] = e;
+        }
       }
   }
 }
 
 // launch K14 for P with (G, KS): 32 G points x 64 columns per CTA, KS coordinates per stage
-template <int P, int G, int KS>
+template <int P, int G, int KS, bool SUB = false>
 static void launch_k14(const float *X, int64_t ldx, int64_t n, int64_t d, int64_t m,
                        const double *Wc, const double *S, const double *Gc, double *Y,
                        int64_t ldy, cudaStream_t s) {
@@ -449,12 +456,12 @@ static void launch_k14(const float *X, int64_t ldx, int64_t n, int64_t d, int64_
                     sizeof(double);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k14_moment_expand_dmma<P, G, KS>,
+    cudaFuncSetAttribute(k14_moment_expand_dmma<P, G, KS, SUB>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr = true;
   }
   dim3 g((unsigned)((n + TR - 1) / TR), (unsigned)((m + kTile - 1) / kTile));
-  k14_moment_expand_dmma<P, G, KS><<<g, 256, sm, s>>>(X, ldx, n, d, m, Wc, S, Gc, Y, ldy);
+  k14_moment_expand_dmma<P, G, KS, SUB><<<g, 256, sm, s>>>(X, ldx, n, d, m, Wc, S, Gc, Y, ldy);
 }
 
 // W[t][k][c] = c_t * sum_ch part[ch][t][k][c]  (t = 1..p-1, scaled for the expand), plus
@@ -714,6 +721,55 @@ int launch_lpp_even(const float *X, int64_t ldx, const float *Z, int64_t ldz, in
     default: return 3;
   }
   return fused_g ? 4 : 5;  // k12, (k13 G partials), k13 fold, k13 colsum, k14
+}
+
+// ---- odd p in one pass (DESIGN.md §2b / §6): the coordinate totals' part of each point's value,
+//   E_ic = sum_k sum_t c_t x_ik^(P-t) T_ktc,   c_t = C(P, t) (-1)^t,
+// with T_ktc = sum_j z_jc x_jk^t the segment totals the single-pass apply leaves in segtot (rows of
+// ld_seg: (P+1) moments per column).  t = 0 is S_c hp_i (T_k0c = S_c for every k, hp_i = sum_k
+// x_ik^P), t = P is the constant c_P sum_k T_kPc, 1 <= t < P is the DMMA expansion of K14 with
+// W_t = c_t T_t.  Y -= E.
+__global__ void __launch_bounds__(256)
+    k14b_lp_totals(const double *__restrict__ segtot, int64_t ld_seg, int64_t dl, int64_t m, int P,
+                   double *__restrict__ W, double *__restrict__ S, double *__restrict__ Gc) {
+  const int K = P + 1;
+  const int64_t total = (int64_t)(P - 1) * dl * m;
+  for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total + m;
+       e += (int64_t)gridDim.x * 256) {
+    if (e < total) {  // W[t-1][k][c] = c_t T_ktc
+      const int64_t tt = e / (dl * m), rem = e - tt * dl * m, k = rem / m, c = rem - k * m;
+      const int t = (int)tt + 1;
+      double b = 1.0;  // C(P, t)
+      for (int q = 0; q < t; ++q) b = b * (double)(P - q) / (double)(q + 1);
+      W[e] = ((t & 1) ? -b : b) * segtot[k * ld_seg + K * c + t];
+    } else {  // column c: S_c and c_P sum_k T_kPc (fixed order)
+      const int64_t c = e - total;
+      double g = 0.0;
+      for (int64_t k = 0; k < dl; ++k) g += segtot[k * ld_seg + K * c + P];
+      S[c] = segtot[K * c];
+      Gc[c] = (P & 1) ? -g : g;
+    }
+  }
+}
+
+size_t lp_totals_workspace(int64_t dl, int64_t m, int p) {
+  return ((size_t)(p - 1) * dl * m + 2 * (size_t)m) * sizeof(double);
+}
+
+int launch_lp_totals_expand(const float *X, int64_t ldx, int64_t n, int64_t dl, int64_t m,
+                            const double *segtot, int64_t ld_seg, int p, double *work, double *Y,
+                            int64_t ldy, cudaStream_t s) {
+  double *W = work, *S = W + (size_t)(p - 1) * dl * m, *G = S + m;
+  int64_t b = ((int64_t)(p - 1) * dl * m + m + 255) / 256;
+  if (b > 148 * 8) b = 148 * 8;
+  k14b_lp_totals<<<(unsigned)b, 256, 0, s>>>(segtot, ld_seg, dl, m, p, W, S, G);
+  switch (p) {
+    case 3: launch_k14<3, 4, 16, true>(X, ldx, n, dl, m, W, S, G, Y, ldy, s); break;
+    case 5: launch_k14<5, 4, 16, true>(X, ldx, n, dl, m, W, S, G, Y, ldy, s); break;
+    case 7: launch_k14<7, 2, 16, true>(X, ldx, n, dl, m, W, S, G, Y, ldy, s); break;
+    default: return 1;
+  }
+  return 2;
 }
 
 }  // namespace l1dm

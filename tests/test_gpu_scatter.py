@@ -137,8 +137,9 @@ def test_scatter_wide_query():
 
 
 # the two-pass forms (tile totals from a reduce pass, then the apply), selected per process:
-# L1DM_SCATTER_LB=0 with the reduce-all pass over full Z rows, and with one reduce per block;
-# L1DM_LB_NT=256: the single-pass apply with 1024-row tiles (default 512)
+# L1DM_SCATTER_LB=0 with the reduce-all pass over full Z rows, and with one reduce per block
+# (odd p: the per-block reduce, then the apply with the totals); L1DM_LB_NT=256: the single-pass
+# apply with 1024-row tiles (default 512)
 @pytest.mark.parametrize("env", [{"L1DM_SCATTER_LB": "0"},
                                  {"L1DM_SCATTER_LB": "0", "L1DM_REDUCE_ALL": "0"},
                                  {"L1DM_LB_NT": "256"}])
@@ -149,7 +150,10 @@ def test_scatter_variants_subprocess(env):
     code = ("import sys; sys.path[:0] = ['.', 'tests']; import test_gpu_scatter as t;"
             "[t.test_scatter_random_float_vs_brute(*c) for c in t.CASES];"
             "t.test_scatter_integer_ties_exact(3000, 4, 4); t.test_scatter_wide_query();"
-            "t.test_scatter_bitwise_reproducible(); print('ok')")
+            "t.test_scatter_bitwise_reproducible();"
+            "import test_gpu_lp as lp;"
+            "[lp.test_lp_random_float_vs_oracle(*c, p, 'scatter') for c in lp.CASES for p in (3, 5, 7)];"
+            "[lp.test_lp_integer_ties_exact(p, 'scatter') for p in (3, 5)]; print('ok')")
     r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env),
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
