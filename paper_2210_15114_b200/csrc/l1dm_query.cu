@@ -899,7 +899,7 @@ __device__ __forceinline__ unsigned long long lb_word(long long v, uint32_t ep, 
 // the coordinate totals' part, sum_k sum_t c_t x_ik^(P-t) T_kt, is one DMMA expansion after the
 // last block (launch_lp_totals_expand), so no pass has to know the totals before the apply.
 template <int MB, int NTT, int P>
-__global__ void __launch_bounds__(NTT, 1280 / NTT)  // 5 x 256 threads per SM (smem-limited)
+__global__ void __launch_bounds__(NTT, (P <= 3 ? 1280 : 768) / NTT)  // 5 (3 for P >= 5) x 256 thr/SM
     k5_scan_lb(const uint32_t *__restrict__ perm, const float *__restrict__ sval, int64_t ldn,
                int64_t n, const float *__restrict__ zt, int64_t mc, unsigned long long *__restrict__ yt,
                int64_t nseg, int64_t tiles_per_seg, unsigned long long *__restrict__ lbst,
@@ -911,7 +911,7 @@ __global__ void __launch_bounds__(NTT, 1280 / NTT)  // 5 x 256 threads per SM (s
   constexpr int NT = C::NT, NW = C::NW, ITEMS = C::ITEMS, R = C::R, GPW = C::GPW, GS = C::GS,
                 PS = C::PS, NP = C::NP, CH = C::CH, CPR = MB * 4 / CH, K = P + 1;
   constexpr int kLBW = 4;  // predecessors loaded per look-back round trip
-  static_assert(NP <= 32, "one look-back lane per component");
+  static_assert(NP <= 64 && NT >= 64, "one look-back lane per component (warps 0 and 1)");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float *zb = reinterpret_cast<float *>(smem_raw);              // [G][GS]
   float *vb = zb + C::G * GS;                                    // [G][PS]
@@ -950,8 +950,8 @@ __global__ void __launch_bounds__(NTT, 1280 / NTT)  // 5 x 256 threads per SM (s
     cp_async_commit();
   }
   // ---- look-back, first part (overlaps the gathers): component e = 2 cc + q of this lane
-  const bool lb_lane = w == 0 && lane < NP;
-  const int e = lane, cc = e / K, q = e - (e / K) * K;
+  const int e = NP <= 32 ? lane : 32 * w + lane, cc = e / K, q = e - (e / K) * K;
+  const bool lb_lane = NP <= 32 ? (w == 0 && lane < NP) : (w < 2 && e < NP);
   unsigned long long *st = lbst + (kk * tiles_per_seg) * NP + e;
   const uint32_t ep2 = epoch & 3u;
   const uint64_t pol_lb = pol_stream;  // status words are read back within a few tiles
@@ -1120,29 +1120,38 @@ void launch_scan_lb(int mb, const uint32_t *perm, const float *sval, int64_t ldn
         static_cast<unsigned long long *>(lbst), epoch, timeout_flag, fx, fa, fa_ld, segtot,   \
         ld_seg);                                                                               \
   }
-#define L1DM_LB_NT(NTT)                 \
-  if (lp == 1) {                        \
-    switch (mb) {                       \
-      case 1: L1DM_LB(1, NTT, 1) break; \
-      case 2: L1DM_LB(2, NTT, 1) break; \
-      case 4: L1DM_LB(4, NTT, 1) break; \
-      case 8: L1DM_LB(8, NTT, 1) break; \
-      case 16: L1DM_LB(16, NTT, 1) break; \
-      default: break;                   \
-    }                                   \
-  } else if (lp == 3) {                 \
-    switch (mb) {                       \
-      case 2: L1DM_LB(2, NTT, 3) break; \
-      case 4: L1DM_LB(4, NTT, 3) break; \
-      case 8: L1DM_LB(8, NTT, 3) break; \
-      default: break;                   \
-    }                                   \
-  } else if (lp == 5 || lp == 7) {      \
-    switch (mb) {                       \
-      case 2: if (lp == 5) L1DM_LB(2, NTT, 5) else L1DM_LB(2, NTT, 7) break; \
-      case 4: if (lp == 5) L1DM_LB(4, NTT, 5) else L1DM_LB(4, NTT, 7) break; \
-      default: break;                   \
-    }                                   \
+#define L1DM_LB_NT(NTT)                                                      \
+  if (lp == 1) {                                                             \
+    switch (mb) {                                                            \
+      case 1: L1DM_LB(1, NTT, 1) break;                                      \
+      case 2: L1DM_LB(2, NTT, 1) break;                                      \
+      case 4: L1DM_LB(4, NTT, 1) break;                                      \
+      case 8: L1DM_LB(8, NTT, 1) break;                                      \
+      case 16: L1DM_LB(16, NTT, 1) break;                                    \
+      default: break;                                                        \
+    }                                                                        \
+  } else if (lp == 3) {                                                      \
+    switch (mb) {                                                            \
+      case 2: L1DM_LB(2, NTT, 3) break;                                      \
+      case 4: L1DM_LB(4, NTT, 3) break;                                      \
+      case 8: L1DM_LB(8, NTT, 3) break;                                      \
+      case 16: L1DM_LB(16, NTT, 3) break;                                    \
+      default: break;                                                        \
+    }                                                                        \
+  } else if (lp == 5) {                                                      \
+    switch (mb) {                                                            \
+      case 2: L1DM_LB(2, NTT, 5) break;                                      \
+      case 4: L1DM_LB(4, NTT, 5) break;                                      \
+      case 8: L1DM_LB(8, NTT, 5) break;                                      \
+      default: break;                                                        \
+    }                                                                        \
+  } else if (lp == 7) {                                                      \
+    switch (mb) {                                                            \
+      case 2: L1DM_LB(2, NTT, 7) break;                                      \
+      case 4: L1DM_LB(4, NTT, 7) break;                                      \
+      case 8: L1DM_LB(8, NTT, 7) break;                                      \
+      default: break;                                                        \
+    }                                                                        \
   }
   if (nt == 256) {
     L1DM_LB_NT(256)
@@ -1153,12 +1162,11 @@ void launch_scan_lb(int mb, const uint32_t *perm, const float *sval, int64_t ldn
 #undef L1DM_LB
 }
 
-// Whether launch_scan_lb has a kernel for (mb, lp): one look-back lane per component, (lp + 1) mb
-// <= 32.
+// Whether launch_scan_lb has a kernel for (mb, lp): one look-back lane per component in warps 0
+// and 1, (lp + 1) mb <= 64.
 bool scan_lb_supported(int mb, int lp) {
-  if (lp == 1) return mb == 1 || mb == 2 || mb == 4 || mb == 8 || mb == 16;
-  if (lp == 3) return mb == 2 || mb == 4 || mb == 8;
-  if (lp == 5 || lp == 7) return mb == 2 || mb == 4;
+  if (lp == 1 || lp == 3) return mb == 1 || mb == 2 || mb == 4 || mb == 8 || mb == 16;
+  if (lp == 5 || lp == 7) return mb == 2 || mb == 4 || mb == 8;
   return false;
 }
 
