@@ -718,22 +718,40 @@ def main_ours(args):
         c_ = torch.cuda.Event(enable_timing=True)
         Ys = torch.empty_like(Y)  # Y still holds the validated query-0 rows
         Xs = X[:, :kk].contiguous()  # what a rank holds at N > 1 (its slice, made contiguous)
-        for _ in range(2):  # one untimed, one timed
-            torch.cuda.synchronize()
-            a.record(stream)
-            hs = l1.l1dm_prepare(Xs, stream=stream)
-            c_.record(stream)
-            l1.l1dm_set_query_mode(hs, args.mode)
-            for q in range(Q):
-                if args.p == 1:
-                    l1.l1dm_matvec(hs, Zs[q % len(Zs)], Ys, stream=stream)
-                else:
-                    l1.l1dm_matvec_lp(hs, args.p, Zs[q % len(Zs)], Ys, stream=stream)
-            b.record(stream)
-            torch.cuda.synchronize()
-            l1.l1dm_free(hs)
-        t_shard = a.elapsed_time(b)
-        t_shard_prep = a.elapsed_time(c_)
+
+        def shard_step(colblocks):
+            """prepare + Q queries on the shard; colblocks: the call each rank makes at N > 1
+            (scatter strategy, --overlap-blocks > 1: column-block-major output, one event per
+            block for the per-block reduce) instead of the row-major l1dm_matvec"""
+            times = None
+            for _ in range(2):  # one untimed, one timed
+                torch.cuda.synchronize()
+                a.record(stream)
+                hs = l1.l1dm_prepare(Xs, stream=stream)
+                c_.record(stream)
+                l1.l1dm_set_query_mode(hs, args.mode)
+                if colblocks:
+                    sc_, mb_, ncb_ = l1.binding.l1dm_query_layout(hs, m)
+                    if not (sc_ and m > 1):
+                        l1.l1dm_free(hs)
+                        return None
+                    Yb = torch.empty((ncb_, n, mb_), dtype=torch.float64, device=dev)
+                    evs = [torch.cuda.Event() for _ in range(ncb_)]
+                for q in range(Q):
+                    if colblocks:
+                        l1.binding.l1dm_matvec_colblocks(hs, Zs[q % len(Zs)], Yb, evs, stream=stream)
+                    elif args.p == 1:
+                        l1.l1dm_matvec(hs, Zs[q % len(Zs)], Ys, stream=stream)
+                    else:
+                        l1.l1dm_matvec_lp(hs, args.p, Zs[q % len(Zs)], Ys, stream=stream)
+                b.record(stream)
+                torch.cuda.synchronize()
+                l1.l1dm_free(hs)
+                times = (a.elapsed_time(b), a.elapsed_time(c_))
+            return times
+
+        t_shard, t_shard_prep = shard_step(False)
+        cb_times = shard_step(True) if args.p == 1 and args.overlap_blocks > 1 else None
         del Ys, Xs
         result["shard_proxy"] = {
             "G": G, "coords_per_shard": kk, "t1_ms_per_step": ms_step,
@@ -743,6 +761,16 @@ def main_ours(args):
             "t_shard_query_ms": (t_shard - t_shard_prep) / Q,
             "note": "one B200: a step (prepare + the same queries) on coordinates [0, ceil(d/8)) "
                     "vs the full step; excludes the cross-GPU sum (DESIGN.md §8)"}
+        if cb_times:
+            # what each rank computes at N > 1 in the scatter strategy (bench.py --gpus N runs
+            # ShardedL1DM.matvec with --overlap-blocks 4: l1dm_matvec_colblocks, then the
+            # per-block reduce and the root's l1dm_unblock, both part of the collective phase)
+            result["shard_proxy"].update({
+                "t_shard_colblocks_ms_per_step": cb_times[0],
+                "t_shard_colblocks_query_ms": (cb_times[0] - cb_times[1]) / Q,
+                "compute_efficiency_colblocks": ms_step / (G * cb_times[0]),
+                "note_colblocks": "per-rank call of the N > 1 scatter path (column-block-major "
+                                  "output for the per-block reduce)"})
     # ---- e2e through the public API with HOST buffers (pinned), N=1 only
     if world == 1 and not args.no_e2e:
         Xh = X.cpu().pin_memory()

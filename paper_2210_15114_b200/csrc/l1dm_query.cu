@@ -598,11 +598,14 @@ __global__ void __launch_bounds__(256, 2)
 // thread-sequential scan; only per-thread totals are scanned across the CTA (shuffles over the
 // 32/MB groups of a warp, then across warps).  At each row step a warp touches 32/MB rows x MB
 // consecutive columns: every reduction request is one row segment of Yt.
-template <int MB, int P = 1, int NTT = 256>
+#ifndef L1DM_LB_ITEMS
+#define L1DM_LB_ITEMS 4  // single-pass apply: consecutive rows per thread / mb (mb >= 2)
+#endif
+template <int MB, int P = 1, int NTT = 256, int IM = 4>
 struct SeqCfg {
   static constexpr int NT = NTT, NW = NTT / 32;
   static constexpr int G = NT / MB;           // row groups per tile
-  static constexpr int ITEMS = MB == 1 ? 8 : 4 * MB;  // consecutive rows per thread
+  static constexpr int ITEMS = MB == 1 ? 8 : IM * MB;  // consecutive rows per thread
   static constexpr int R = G * ITEMS;         // 1024 rows per tile
   static constexpr int GPW = 32 / MB;         // groups per warp
   static constexpr int GS = ITEMS * MB + MB;  // padded floats per group of the Z stage
@@ -907,7 +910,7 @@ __global__ void __launch_bounds__(NTT, (P <= 3 ? 1280 : 768) / NTT)  // 5 (3 for
                unsigned *timeout_flag, const double *__restrict__ fx,
                const double *__restrict__ fa, int64_t fa_ld, double *__restrict__ segtot,
                int64_t ld_seg) {
-  using C = SeqCfg<MB, P, NTT>;
+  using C = SeqCfg<MB, P, NTT, L1DM_LB_ITEMS>;
   constexpr int NT = C::NT, NW = C::NW, ITEMS = C::ITEMS, R = C::R, GPW = C::GPW, GS = C::GS,
                 PS = C::PS, NP = C::NP, CH = C::CH, CPR = MB * 4 / CH, K = P + 1;
   constexpr int kLBW = 4;  // predecessors loaded per look-back round trip
@@ -1096,7 +1099,7 @@ static int scan_lb_threads(int mb) {
   return mb == 1 ? 256 : 128;
 }
 
-int scan_lb_rows(int mb) { return scan_lb_threads(mb) * (mb == 1 ? 8 : 4); }
+int scan_lb_rows(int mb) { return scan_lb_threads(mb) * (mb == 1 ? 8 : L1DM_LB_ITEMS); }
 
 void launch_scan_lb(int mb, const uint32_t *perm, const float *sval, int64_t ldn, int64_t n,
                     const float *zt, int64_t mc, unsigned long long *yt, int64_t kcc,
@@ -1108,7 +1111,7 @@ void launch_scan_lb(int mb, const uint32_t *perm, const float *sval, int64_t ldn
   const int64_t total = kcc * tiles_per_seg;
 #define L1DM_LB(MB, NTT, P)                                                                    \
   {                                                                                            \
-    using C = SeqCfg<MB, P, NTT>;                                                              \
+    using C = SeqCfg<MB, P, NTT, L1DM_LB_ITEMS>;                                               \
     static bool attr = false;                                                                  \
     if (!attr) {                                                                               \
       cudaFuncSetAttribute(k5_scan_lb<MB, NTT, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,\
