@@ -417,11 +417,15 @@ L1DM_API l1dm_status l1dm_set_workspace_limit(l1dm_handle h, size_t bytes);
 /* Query strategy.  Both compute the same Y = A*Z:
  *   GATHER  the scan stores U = v*P - Q per (coordinate, sorted row) in a workspace and a
  *           per-point pass gathers U at rank_k(i) for every k (Y written once, no atomics);
- *   SCATTER the scan adds 2U straight into Y[perm_k(r)] with fp64 L2 atomics, one column
- *           block of Y at a time (no U workspace, no rank gather).  For m > 1 the block
- *           accumulator is 64-bit fixed point at a per-query scale bounded from Z and the
- *           sorted values, so Y is bitwise reproducible; for m = 1 the fp64 reductions'
- *           order varies run to run at the ulp level on float data (R16).
+ *   SCATTER one pass per column block of Y (every m, m = 1 included): the scan's tile
+ *           prefixes come from a decoupled look-back over the earlier tiles of the same
+ *           coordinate (Alg. 2's partial sums in sorted order; bounded waits, else
+ *           ETIMEOUT) and it adds 2U straight into Y[perm_k(r)] with L2 reductions into a
+ *           compact block accumulator (no U workspace, no rank gather).  Both the look-back
+ *           prefixes and the accumulator are 64-bit fixed point at per-query scales bounded
+ *           from Z and the sorted values, so Y is bitwise reproducible (R16); odd
+ *           p > 1 accumulates in fp64 (summation order varies at the ulp level) and subtracts
+ *           the coordinate totals' part with one fp64 tensor-core expansion.
  *   RUNS    tie-heavy data only (every prepared coordinate takes <= 256 distinct values,
  *           detected by prepare): Alg. 2 over the distinct values — per coordinate the run
  *           sums of Z by fp64 L2 reductions in point order, a prefix over the runs, then each
@@ -449,7 +453,7 @@ typedef struct {
   int64_t chunks;
   int64_t l2_resident;
   int64_t workspace_bytes;
-  int64_t scatter;      /* 1: scatter mode, the scan adds 2U into an L2-resident Y block with atomics */
+  int64_t scatter;      /* 1: scatter mode, the scan adds 2U into an L2-resident Y block with reductions */
 } l1dm_plan_t;
 L1DM_API l1dm_status l1dm_plan(int64_t n, int64_t d_local, int64_t m, int64_t l2_bytes,
                       int64_t workspace_limit, l1dm_plan_t *out);
@@ -500,7 +504,10 @@ L1DM_API int64_t l1dm_handleless_launches(void);
  * the measured choices of DESIGN.md §6 and per-handle control is l1dm_set_query_mode):
  *   L1DM_SCATTER=0|1        planner default for handles left in L1DM_MODE_AUTO (gather/scatter)
  *   L1DM_SCATTER_MB=k       scatter column-block width override
- *   L1DM_REDUCE_ALL=0       scatter tile totals by a reduce pass per column block
+ *   L1DM_SCATTER_LB=0       scatter mode in two passes per column block (a reduce pass for
+ *                           the tile totals, then the apply) instead of the look-back apply
+ *   L1DM_REDUCE_ALL=0       (with L1DM_SCATTER_LB=0) tile totals by a reduce pass per block
+ *   L1DM_LB_NT=128|256      threads per look-back apply CTA (tiles of 4 rows per thread)
  *   L1DM_RUNS=0             prepare never builds the runs tables (§2f)
  *   L1DM_RUNS_GATHER=0      the shared-memory-staged runs expansion
  *   L1DM_FUSED_RANK=1       the last sort pass scatters the inverse ranks eagerly
