@@ -560,17 +560,55 @@ void launch_identity_emit(const uint32_t *key, float *sval, uint32_t *perm, uint
 // into per-tile offsets and decides (every coordinate needs <= 256 runs); K_r2 emits both.
 constexpr int kRunTile = 4096;
 
+// A thread's 16 consecutive sorted values of a 4096-row tile (four 16-byte loads; zero past n)
+// and the value before its first row (the previous lane's last, the previous tile's last row for
+// lane 0 of warp 0, a shared-memory hand-off between warps).
+struct RunRows {
+  uint32_t v[16];
+  uint32_t prev;
+};
+__device__ __forceinline__ void load_run_rows(const float *v, int64_t n, int64_t r0, RunRows &o,
+                                              uint32_t *s_last) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t rt = r0 + (int64_t)tid * 16;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int64_t r = rt + 4 * q;
+    if (r + 4 <= n) {  // rows are 128-byte aligned (ldn) and r is a multiple of 4
+      const uint4 u = *reinterpret_cast<const uint4 *>(v + r);
+      o.v[4 * q] = u.x;
+      o.v[4 * q + 1] = u.y;
+      o.v[4 * q + 2] = u.z;
+      o.v[4 * q + 3] = u.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) o.v[4 * q + u] = r + u < n ? __float_as_uint(v[r + u]) : 0u;
+    }
+  }
+  uint32_t p = __shfl_up_sync(0xFFFFFFFFu, o.v[15], 1);
+  if (lane == 31) s_last[w] = o.v[15];
+  __syncthreads();
+  if (lane == 0) p = w > 0 ? s_last[w - 1] : (r0 > 0 ? __float_as_uint(v[r0 - 1]) : 0u);
+  o.prev = p;
+}
+
 __global__ void __launch_bounds__(256)
     k_runs_count(const float *__restrict__ sval, int64_t n, int64_t ldn, int64_t tiles,
                  uint32_t *__restrict__ cnt) {
+  static_assert(kRunTile == 256 * 16, "16 rows per thread");
+  __shared__ uint32_t s_last[8], s_c[8];
   const int64_t seg = blockIdx.y, tile = blockIdx.x;
-  const float *v = sval + seg * ldn;
   const int64_t r0 = tile * kRunTile;
-  uint32_t c = 0;
-  for (int64_t r = r0 + threadIdx.x; r < r0 + kRunTile && r < n; r += 256)
-    c += (r == 0 || __float_as_uint(v[r]) != __float_as_uint(v[r - 1])) ? 1u : 0u;
-  for (int off = 16; off; off >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, off);
-  __shared__ uint32_t s_c[8];
+  RunRows rr;
+  load_run_rows(sval + seg * ldn, n, r0, rr, s_last);
+  const int64_t rt = r0 + (int64_t)threadIdx.x * 16;
+  uint32_t c = 0, prev = rr.prev;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    c += (rt + j < n && (rt + j == 0 || rr.v[j] != prev)) ? 1u : 0u;
+    prev = rr.v[j];
+  }
+  c = __reduce_add_sync(0xFFFFFFFFu, c);
   if ((threadIdx.x & 31) == 0) s_c[threadIdx.x >> 5] = c;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -583,32 +621,21 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(256)
     k_runs_emit(const float *__restrict__ sval, int64_t n, int64_t ldn, int64_t tiles,
                 const uint32_t *__restrict__ tile_off, float *__restrict__ rvals) {
-  constexpr int ITEMS = kRunTile / 256;
-  constexpr int PAD = ITEMS + 1;  // padded rows of the staged tile: conflict-free per-thread runs
+  __shared__ uint32_t s_last[8], s_w[8];
   const int64_t seg = blockIdx.y, tile = blockIdx.x;
-  const float *v = sval + seg * ldn;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t r0 = tile * kRunTile;
-  const int64_t rt = r0 + (int64_t)tid * ITEMS;  // this thread's consecutive rows
-  // the tile's values staged with coalesced loads (+ the row before it), then each thread reads
-  // its ITEMS consecutive rows from shared memory
-  __shared__ uint32_t s_v[256 * PAD];
-  __shared__ uint32_t s_prev;
-  for (int e = tid; e < kRunTile; e += 256) {
-    const int64_t r = r0 + e;
-    s_v[(e / ITEMS) * PAD + (e % ITEMS)] = r < n ? __float_as_uint(v[r]) : 0u;
-  }
-  if (tid == 0) s_prev = r0 > 0 ? __float_as_uint(v[r0 - 1]) : 0u;
-  __syncthreads();
-  uint32_t f[ITEMS], cnt = 0;
+  RunRows rr;
+  load_run_rows(sval + seg * ldn, n, r0, rr, s_last);
+  const int64_t rt = r0 + (int64_t)tid * 16;
+  uint32_t f = 0, cnt = 0, prev = rr.prev;  // f: bit j = row rt + j starts a run
 #pragma unroll
-  for (int j = 0; j < ITEMS; ++j) {
-    const int64_t r = rt + j;
-    const uint32_t cur = s_v[tid * PAD + j];
-    const uint32_t prev = j > 0 ? s_v[tid * PAD + j - 1]
-                                : (tid > 0 ? s_v[(tid - 1) * PAD + ITEMS - 1] : s_prev);
-    f[j] = (r < n && (r == 0 || cur != prev)) ? 1u : 0u;
-    cnt += f[j];
+  for (int j = 0; j < 16; ++j) {
+    if (rt + j < n && (rt + j == 0 || rr.v[j] != prev)) {
+      f |= 1u << j;
+      ++cnt;
+    }
+    prev = rr.v[j];
   }
   if (!__syncthreads_or(cnt)) return;  // no run starts in this tile
   uint32_t inc = cnt;  // block exclusive scan of the per-thread counts
@@ -617,14 +644,13 @@ __global__ void __launch_bounds__(256)
     const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, off);
     if (lane >= off) inc += y;
   }
-  __shared__ uint32_t s_w[8];
   if (lane == 31) s_w[w] = inc;
   __syncthreads();
   uint32_t run = tile_off[seg * tiles + tile] + inc - cnt;  // run starts before this thread
   for (int ww = 0; ww < w; ++ww) run += s_w[ww];
 #pragma unroll
-  for (int j = 0; j < ITEMS; ++j)
-    if (f[j]) rvals[seg * 256 + run++] = __uint_as_float(s_v[tid * PAD + j]);
+  for (int j = 0; j < 16; ++j)
+    if (f & (1u << j)) rvals[seg * 256 + run++] = __uint_as_float(rr.v[j]);
 }
 
 // runid[k][i] = the index of x_ik among rvals[k][0..R_k) (binary search; -0.0 == +0.0 as in
@@ -639,13 +665,14 @@ __global__ void __launch_bounds__(256)
                int64_t ldn, const float *__restrict__ rvals, const uint32_t *__restrict__ nruns,
                uint8_t *__restrict__ runid) {
   __shared__ float tile[kT0Points][kT0Coords + 1];
-  __shared__ float s_vals[kT0Coords][256];
+  // padded rows (one float per 32): the search's power-of-two strides spread over the banks
+  __shared__ float s_vals[kT0Coords][256 + 8];
   __shared__ uint32_t s_nr[kT0Coords];
   const int tid = threadIdx.x;
   const int64_t kt = (int64_t)blockIdx.y * kT0Coords;
   for (int e = tid; e < kT0Coords * 256; e += 256) {
     const int c = e / 256, j = e % 256;
-    s_vals[c][j] = (kt + c < dl) ? rvals[(kt + c) * 256 + j] : 0.0f;
+    s_vals[c][j + (j >> 5)] = (kt + c < dl) ? rvals[(kt + c) * 256 + j] : 0.0f;
   }
   if (tid < kT0Coords) s_nr[tid] = (kt + tid < dl) ? nruns[kt + tid] : 1u;
   for (int sub = 0; sub < kIdPoints / kT0Points; ++sub) {
@@ -658,17 +685,34 @@ __global__ void __launch_bounds__(256)
       tile[p][c] = (i < n && k < dl) ? X[i * ldx + k0 + k] : 0.0f;
     }
     __syncthreads();
-    for (int e = tid; e < kT0Points * kT0Coords; e += 256) {
+    // the largest j with rvals[j] <= x (== x: present): a fixed 8-step branchless search per
+    // element, the 8 elements of a thread interleaved (independent shared-memory chains)
+    constexpr int PE = kT0Points * kT0Coords / 256;
+    float xs[PE];
+    int pos[PE], nr[PE];
+#pragma unroll
+    for (int u = 0; u < PE; ++u) {
+      const int e = tid + 256 * u;
+      const int c = e / kT0Points, p = e % kT0Points;
+      xs[u] = tile[p][c];
+      nr[u] = (int)s_nr[c];
+      pos[u] = 0;
+    }
+#pragma unroll
+    for (int step = 128; step > 0; step >>= 1) {
+#pragma unroll
+      for (int u = 0; u < PE; ++u) {
+        const int c = (tid + 256 * u) / kT0Points;
+        const int t = pos[u] + step;
+        if (t < nr[u] && s_vals[c][t + (t >> 5)] <= xs[u]) pos[u] = t;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < PE; ++u) {
+      const int e = tid + 256 * u;
       const int c = e / kT0Points, p = e % kT0Points;
       const int64_t i = i0 + p, k = kt + c;
-      if (i >= n || k >= dl) continue;
-      const float x = tile[p][c];
-      int lo = 0, hi = (int)s_nr[c] - 1;  // the largest j with rvals[j] <= x (== x: present)
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (s_vals[c][mid] <= x) lo = mid; else hi = mid - 1;
-      }
-      runid[k * ldn + i] = (uint8_t)lo;
+      if (i < n && k < dl) runid[k * ldn + i] = (uint8_t)pos[u];
     }
   }
 }
