@@ -101,7 +101,8 @@ L1DM_API l1dm_status l1dm_prepare_ex(const float *X, int64_t n, int64_t ld_x, in
  * Z: n x m fp32 (ld_z = m); Y: n x m fp64 (ld_y = m), OVERWRITTEN.
  * Device Z/Y: stream-ordered on the handle's (prepare) stream; Z and Y must stay valid
  * until the stream reaches the end of the call.  Host Z/Y: synchronous.
- * NaN/Inf in Z are not checked; they propagate into Y by IEEE rules.
+ * NaN/Inf in Z are not checked; they propagate into Y by IEEE rules (in the fixed-point scatter
+ * mode: a column of Z holding a NaN or Inf gives a NaN column of Y).
  * Errors: EINVAL (null, m < 1), EDEVICE, ENOMEM (workspace), ECUDA. */
 L1DM_API l1dm_status l1dm_matvec(l1dm_handle h, const float *Z, int64_t m, double *Y);
 

@@ -16,6 +16,7 @@
 //   K6 accumulate  per point: gather U rows at rank[k][i] for every k of the chunk
 //                  and accumulate in registers (no atomics); epilogue writes Y.
 #include <cuda_runtime.h>
+#include <math_constants.h>
 
 #include <cstdlib>
 
@@ -1746,14 +1747,19 @@ __global__ void __launch_bounds__(256)
     const int F = scale_exp(4.0 * mx * sz * 1.0001, 61);
     fx[c] = ldexp(1.0, F);
     fx[m + c] = ldexp(1.0, -F);
+    const bool bad = !isfinite(sz);  // a NaN / Inf in column c: the column's Y is NaN (the
+    if (bad) {                       // fixed-point path would otherwise hide it)
+      fx[c] = 0.0;
+      fx[m + c] = CUDART_NAN;
+    }
     // the single-pass apply's look-back (k5_scan_lb): every partial sum of s = z over a
     // coordinate is bounded by sz, of t = v z by max_k Mx_k sz; the rounded tile aggregates'
     // sums stay below 2^58 (the look-back words carry 60-bit signed values)
     const int Fz = scale_exp(sz * 1.0001, 58), Fv = scale_exp(mxx * sz * 1.0001, 58);
     fx[2 * m + c] = ldexp(1.0, Fz);
-    fx[3 * m + c] = ldexp(1.0, -Fz);
+    fx[3 * m + c] = bad ? CUDART_NAN : ldexp(1.0, -Fz);
     fx[4 * m + c] = ldexp(1.0, Fv);
-    fx[5 * m + c] = ldexp(1.0, -Fv);
+    fx[5 * m + c] = bad ? CUDART_NAN : ldexp(1.0, -Fv);
   }
 }
 
@@ -1777,6 +1783,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) sz += __shfl_xor_sync(0xFFFFFFFFu, sz, off);
     if (lane != 0) continue;
+    const bool bad = !isfinite(sz);  // NaN / Inf in column c: NaN prefixes, so Y's column is NaN
     double B = sz * 1.0001;
     for (int t = 0; t <= lp; ++t) {
       int F = 0;
@@ -1786,7 +1793,7 @@ __global__ void __launch_bounds__(256)
         if (F < -1000) F = -1000;
       }
       fa[(2 * t) * m + c] = ldexp(1.0, F);
-      fa[(2 * t + 1) * m + c] = ldexp(1.0, -F);
+      fa[(2 * t + 1) * m + c] = bad ? CUDART_NAN : ldexp(1.0, -F);
       B *= mxx;
     }
   }

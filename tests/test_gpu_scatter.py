@@ -228,3 +228,22 @@ def test_scatter_columns_of_different_scales(xscale, zscales):
             assert not Y[:, c].any()
         else:
             assert col_rel_l2(Y[:, c:c + 1], Yr[:, c:c + 1]) <= TOL, c
+
+
+@pytest.mark.parametrize("m", [1, 5])
+def test_scatter_nonfinite_z_column_is_nan(m):
+    """A NaN / Inf in a column of Z is not hidden by the fixed-point accumulation: that column of
+    Y comes out NaN (include/l1dm.h), the other columns are unaffected."""
+    rng = np.random.default_rng(5)
+    X = rng.standard_normal((3000, 3)).astype(np.float32)
+    Z = rng.standard_normal((3000, m)).astype(np.float32)
+    Zb = Z.copy()
+    Zb[17, 0] = np.nan
+    if m > 1:
+        Zb[5, m - 1] = np.inf
+    Y = gpu_matvec(X, Zb, mode="scatter")
+    assert np.all(np.isnan(Y[:, 0]))
+    if m > 1:
+        assert not np.any(np.isfinite(Y[:, m - 1]))
+        Yr = oracle.brute(X, Z)
+        assert col_rel_l2(Y[:, 1:m - 1], Yr[:, 1:m - 1]) <= TOL
