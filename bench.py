@@ -66,6 +66,8 @@ def parse():
     ap.add_argument("--collective", default="nccl", choices=["nccl", "peer"],
                     help="N > 1: NCCL per point/column block, or this library's peer-memory sum "
                          "(final pass stores into the owners' inboxes; DESIGN.md §8)")
+    ap.add_argument("--no-pattern-probe", action="store_true",
+                    help="skip the apply-pattern ceiling probe (tools/apply_probe.cu)")
     ap.add_argument("--overlap-blocks", type=int, default=4,
                     help="N>1: point blocks whose reduce overlaps the remaining accumulate")
     return ap.parse_args()
@@ -184,6 +186,26 @@ def red_ceiling(l2p):
     tools/l2_probe.cu's sweep reaches (row widths 32-256 B, buffers 1-64 MiB, localised tables,
     4-16 CTAs per SM); falls back to the earlier single-pattern probe."""
     return float(l2p.get("red_ceiling_adds_per_s", l2p.get("red_row8_adds_per_s", 5.88e11)))
+
+
+def apply_pattern_probe(n, d):
+    """The memory-system ceiling of the scatter apply's own access pattern (tools/apply_probe.cu:
+    the perm/sval stream, the Zt row gathers and the 64-bit reductions into Yt, without the scan
+    arithmetic or the look-back), compiled and run on this GPU right after the timed region:
+    {"best_ms", "median_ms", ...} per launch, or None when nvcc or the probe fails."""
+    import subprocess
+    import tempfile
+    src = os.path.join(ROOT, "tools", "apply_probe.cu")
+    try:
+        exe = os.path.join(tempfile.gettempdir(), f"l1dm_apply_probe_{os.getpid()}")
+        subprocess.run(["nvcc", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-o", exe,
+                        src], check=True, capture_output=True, timeout=180)
+        out = subprocess.run([exe, str(n), str(d)], check=True, capture_output=True, text=True,
+                             timeout=120).stdout
+        os.remove(exe)
+        return json.loads(out.strip().splitlines()[-1])
+    except Exception:
+        return None
 
 
 def model_b_bytes(n, d, m):
@@ -665,6 +687,23 @@ def main_ours(args):
     if traffic and dk and dk.get("ms_per_launch"):
         roof["dram_GBps"] = traffic / (dk["ms_per_launch"] * 1e-3) / 1e9
         roof["dram_frac_of_hbm_peak"] = roof["dram_GBps"] / hbm_peak
+    # the apply's own access pattern without its arithmetic (tools/apply_probe.cu), on this GPU
+    # after the timed region: the fraction of that pattern's ceiling the kernel reaches
+    if (plan and plan.get("scatter") and m > 1 and plan.get("mb") == 8 and args.p == 1
+            and dominant == "accumulate" and not kern["scan"]["launches"] and world == 1
+            and not args.no_pattern_probe):
+        pr = apply_pattern_probe(n, dl)
+        acc_ms = kern["accumulate"].get("ms_per_launch")
+        if pr and acc_ms and pr.get("n") == n:
+            roof["pattern_ceiling"] = {
+                "ms_per_launch_best": pr["apply_pattern_ms"],
+                "ms_per_launch_median": pr["apply_pattern_median_ms"],
+                "frac_of_best": pr["apply_pattern_ms"] / acc_ms,
+                "frac_of_median": pr["apply_pattern_median_ms"] / acc_ms,
+                "how": "tools/apply_probe.cu: the apply's perm/sval stream, Zt row gathers and "
+                       "64-bit L2 reductions (same tiles, grid and L2 hints) without the scan "
+                       "arithmetic or the look-back; best, and median of the last 32 of 800 "
+                       "back-to-back launches with their clears (sustained, as in a step)"}
     # the U-materialising design's HBM floor (Model B bytes) over the measured query time:
     # above 1.0 means the query beats that design's roofline
     roof["model_b_hbm_equivalent_frac"] = (qb / (query_kernel_ms * 1e-3) / 1e9 / hbm_peak
