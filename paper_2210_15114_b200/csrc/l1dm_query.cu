@@ -1057,17 +1057,17 @@ __global__ void __launch_bounds__(NTT, (P <= 3 ? 1280 : 768) / NTT)  // 5 (3 for
     for (int q2 = 0; q2 < K; ++q2) M[q2] += s_wt[ww * NP + K * c + q2];
   }
   if (c < mc) {
-    double fxs = 0.0;
-    if constexpr (P == 1) fxs = __ldg(fx + c);
+    double fxs2 = 0.0;  // P = 1: 2 2^F_c (the factor 2 of 2U folded into the exact scaling)
+    if constexpr (P == 1) fxs2 = 2.0 * __ldg(fx + c);
 #pragma unroll 4
     for (int jj = 0; jj < ITEMS; ++jj) {
       if (jj >= nmine) break;
       const double z = (double)zg[jj * MB], v = (double)vg[jj];
       if constexpr (P == 1) {
-        const double val = 2.0 * fma(v, M[0], -M[1]);  // 2 U_r = 2 (v_r P_r - Q_r)
+        const double u = fma(v, M[0], -M[1]);  // U_r = v_r P_r - Q_r; adds 2 U_r
         M[0] += z;
         M[1] = fma(v, z, M[1]);
-        const unsigned long long qv = (unsigned long long)__double2ll_rn(val * fxs);
+        const unsigned long long qv = (unsigned long long)__double2ll_rn(u * fxs2);
         asm volatile("red.global.add.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(
                          yt + (int64_t)pg[jj] * MB + c),
                      "l"(qv), "l"(pol_keep)
