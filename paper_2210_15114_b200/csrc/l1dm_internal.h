@@ -19,13 +19,16 @@ constexpr uint32_t kSpinLimit = 1u << 26;
 // ---------------- prepare (Alg. 1) ----------------
 constexpr int kSortThreads = 256;
 #ifndef L1DM_SORT_ITEMS
-#define L1DM_SORT_ITEMS 24  // keys per thread per onesweep tile (24 x 256 = 6144: c3 prepare 3.77 -> 3.59 ms vs 16)
+#define L1DM_SORT_ITEMS 18  // keys per thread per onesweep tile (18 x 256 = 4608 with the bulk-copy loads: c3 prepare 3.59 -> 3.53 ms; 24 no longer fits ptxas at 2 CTAs/SM)
 #endif
 #ifndef L1DM_SORT_MINB
 #define L1DM_SORT_MINB 2  // 2 CTAs per SM (104 KB of shared memory each); 3 x 4096-key tiles: c3 3.77 ms
 #endif
+#ifndef L1DM_SORT_TMA
+#define L1DM_SORT_TMA 1  // tile loads by 1-D bulk copies (one thread, mbarrier) instead of cp.async
+#endif
 constexpr int kSortItems = L1DM_SORT_ITEMS;             // keys per thread per onesweep tile
-constexpr int kSortTile = kSortThreads * kSortItems;    // 6144 keys
+constexpr int kSortTile = kSortThreads * kSortItems;    // 4608 keys
 constexpr int kHistChunk = 16384;                       // keys per histogram CTA
 
 void launch_keys(const float *X, int64_t n, int64_t ldx, int64_t k0, int64_t dl, int64_t ldn,

@@ -268,6 +268,23 @@ __device__ __forceinline__ unsigned long long pack_status(uint32_t flag, uint32_
          ((unsigned long long)(epoch & 0x3FFFFFFFu) << 32) | (unsigned long long)cnt;
 }
 
+#if L1DM_SORT_TMA
+// thread 0 of a sort CTA: tile t's keys (and values unless vin is null) into dst by 1-D bulk
+// copies completing on bar.  Out of line: inlined into k2_pass, ptxas (12.9) fails register
+// allocation ("register count of 7": the predicate file) under the ballot loop's pressure.
+__device__ __noinline__ void sort_tile_bulk_load(const uint32_t *kin, const uint32_t *vin,
+                                                 uint32_t *dst, uint64_t *bar, int64_t t,
+                                                 int64_t nseg, int64_t ldn) {
+  const int64_t tile = t / nseg, seg = t - tile * nseg;
+  const int64_t base = tile * kSortTile, off = seg * ldn + base;
+  const unsigned bytes = 4u * (unsigned)(ldn - base < kSortTile ? ldn - base : kSortTile);
+  mbar_expect_tx(bar, vin ? 2 * bytes : bytes);
+  bulk_g2s(dst, kin + off, bytes, bar);
+  if (vin) bulk_g2s(dst + kSortTile, vin + off, bytes, bar);
+}
+__device__ __noinline__ void sort_tile_wait(uint64_t *bar, unsigned parity) { mbar_wait(bar, parity); }
+#endif
+
 // Persistent onesweep pass: each CTA loops over tiles claimed by an atomic ticket, and the
 // next tile's keys/values are already in flight (cp.async into the other half of a shared
 // double buffer) while the current one is ranked, looked back and scattered — ncu/clock64
@@ -295,6 +312,20 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t total = nseg * tiles_per_seg;
   // stage tile t (keys, and values unless FIRST) into half b of the input buffer
+#if L1DM_SORT_TMA
+  // one thread moves each contiguous key / value tile with a 1-D bulk copy (TMA engine) that
+  // completes on the half's mbarrier; rows are padded to ldn (a multiple of 32 keys), so every
+  // copy is a multiple of 128 bytes from a 128-byte aligned address
+  __shared__ uint64_t s_bar[2];
+  uint32_t phase = 0;  // bit b: parity of the next completion of half b
+  auto issue = [&](int64_t t, int b) {
+    unsigned tx;  // %tid.x re-read here: a predicate held across the loop exhausts the file
+    asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tx));
+    if (tx == 0 && t < total)
+      sort_tile_bulk_load(kin, FIRST ? nullptr : vin, s_in + (size_t)b * 2 * kSortTile, &s_bar[b],
+                          t, nseg, ldn);
+  };
+#else
   auto issue = [&](int64_t t, int b) {
     if (t < total) {
       const int64_t tile = t / nseg, seg = t - (t / nseg) * nseg;
@@ -309,7 +340,13 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
     }
     cp_async_commit();  // (an empty group past the last ticket keeps the group count uniform)
   };
+#endif
   if (tid == 0) {
+#if L1DM_SORT_TMA
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    mbar_init_fence();
+#endif
     s_tk[0] = atomicAdd(ticket, 1u);
     s_tk[1] = atomicAdd(ticket, 1u);
   }
@@ -322,7 +359,12 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
   long long prof_last = clock64();
 #endif
   while (t_cur < total) {
+#if L1DM_SORT_TMA
+    sort_tile_wait(&s_bar[cur], (phase >> cur) & 1u);  // t_cur's tile (t_nxt's may be in flight)
+    phase ^= 1u << cur;
+#else
     cp_async_wait_group<1>();  // t_cur's group (t_nxt's may still be in flight)
+#endif
     for (int b = tid; b < W * 256; b += kSortThreads) (&s_whist[0][0])[b] = 0;
     __syncthreads();
     SORT_T(0);
@@ -527,6 +569,9 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
     // and the one in flight), which keeps the tiles a look-back may wait for close behind
     // (claiming it at the top of the tile, to hide the atomic's latency, measured 1% slower)
     if (tid == 0) s_tk[0] = atomicAdd(ticket, 1u);
+#if L1DM_SORT_TMA
+    fence_proxy_async_smem();  // this thread's reads of half `cur` before the bulk copy into it
+#endif
     __syncthreads();  // s_keys / s_vals / s_gbase are reused by the next tile
     const int64_t t_nn = s_tk[0];
     issue(t_nn, cur);
@@ -534,7 +579,9 @@ __global__ void __launch_bounds__(kSortThreads, L1DM_SORT_MINB)
     t_nxt = t_nn;
     cur ^= 1;
   }
+#if !L1DM_SORT_TMA
   cp_async_wait_all();
+#endif
 }
 
 void launch_sort_pass(bool first, bool last, const uint32_t *kin, const uint32_t *vin,

@@ -1645,33 +1645,56 @@ __global__ void __launch_bounds__(256)
   }
   __syncthreads();
   const int hp = mb > 1 ? mb >> 1 : 1;  // column pairs per row (mb = 1: one column)
+  // mb is a power of two (the planner's blocks): row and pair by shift and mask — a 64-bit
+  // division per element made this pass ALU-bound
+  const int hsh = __ffs(hp) - 1;
   const int64_t total = (i1 - i0) * hp;
-  for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * 256) {
-    const int64_t i = i0 + e / hp;
-    const int c = mb > 1 ? 2 * (int)(e - (e / hp) * hp) : 0;
-    ulonglong2 q;
-    if (mb > 1)
-      q = *reinterpret_cast<const ulonglong2 *>(yt + i * mb + c);
-    else
-      q = make_ulonglong2(yt[i], 0ull);
-    if (c >= mc) continue;
-    const double h = __ldg(hsum + i);
-    const double o0 = (double)(long long)q.x * s_f[c] + fma(-h, s_S[c], s_g[c]);
-    const double o1 = c + 1 < mc ? (double)(long long)q.y * s_f[c + 1] +
-                                       fma(-h, s_S[c + 1], s_g[c + 1])
-                                 : 0.0;
-    if constexpr (PUSH) {
-      double *row = peer_row(pd, i) + pc0 + c;
-      row[0] = o0;
-      if (c + 1 < mc) row[1] = o1;
-    } else {
-      double *yo = Y + i * ldy + c;
-      if (vec && c + 1 < mc) {
-        __stcs(reinterpret_cast<double2 *>(yo), make_double2(o0, o1));
+  const int64_t stride = (int64_t)gridDim.x * 256;
+  // four elements per thread in flight (loads first): one 16-byte load per iteration left the
+  // pass latency-bound at ~2.8 TB/s
+  constexpr int U = 4;
+  for (int64_t e0 = (int64_t)blockIdx.x * 256 + threadIdx.x; e0 < total; e0 += U * stride) {
+    ulonglong2 q[U];
+    double hv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + u * stride;
+      q[u] = make_ulonglong2(0ull, 0ull);
+      hv[u] = 0.0;
+      if (e < total) {
+        const int64_t i = i0 + (e >> hsh);
+        const int c = mb > 1 ? 2 * (int)(e & (hp - 1)) : 0;
+        if (mb > 1)
+          q[u] = __ldcs(reinterpret_cast<const ulonglong2 *>(yt + i * mb + c));
+        else
+          q[u] = make_ulonglong2(__ldcs(yt + i), 0ull);
+        hv[u] = __ldg(hsum + i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + u * stride;
+      if (e >= total) break;
+      const int64_t i = i0 + (e >> hsh);
+      const int c = mb > 1 ? 2 * (int)(e & (hp - 1)) : 0;
+      if (c >= mc) continue;
+      const double h = hv[u];
+      const double o0 = (double)(long long)q[u].x * s_f[c] + fma(-h, s_S[c], s_g[c]);
+      const double o1 = c + 1 < mc ? (double)(long long)q[u].y * s_f[c + 1] +
+                                         fma(-h, s_S[c + 1], s_g[c + 1])
+                                   : 0.0;
+      if constexpr (PUSH) {
+        double *row = peer_row(pd, i) + pc0 + c;
+        row[0] = o0;
+        if (c + 1 < mc) row[1] = o1;
       } else {
-        __stcs(yo, o0);
-        if (c + 1 < mc) __stcs(yo + 1, o1);
+        double *yo = Y + i * ldy + c;
+        if (vec && c + 1 < mc) {
+          __stcs(reinterpret_cast<double2 *>(yo), make_double2(o0, o1));
+        } else {
+          __stcs(yo, o0);
+          if (c + 1 < mc) __stcs(yo + 1, o1);
+        }
       }
     }
   }
