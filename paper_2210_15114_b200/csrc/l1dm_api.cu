@@ -102,6 +102,11 @@ class BlockCache {
     if (e == cudaErrorMemoryAllocation) {
       cudaGetLastError();
       release_all(dev);
+      cudaMemPool_t pool;  // and what the stream-ordered pool keeps (keep_default_pool)
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        cudaDeviceSynchronize();
+        cudaMemPoolTrimTo(pool, 0);
+      }
       e = cudaMalloc(p, rounded);
     }
     if (e == cudaSuccess) {
@@ -319,6 +324,21 @@ struct TimedScope {
     }
   }
 };
+
+// The device's default stream-ordered pool keeps freed memory (release threshold = max): with
+// the default threshold of 0 every Krylov / CG call re-mapped its multi-GB basis (c3 top-16:
+// ~80-120 ms of host-side cudaMallocAsync per call beside 480 ms of device work).
+static void keep_default_pool() {
+  static bool done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
 
 // NVTX range over an entry point (named ranges for profilers; header-only NVTX 3,
 // a no-op unless a tool is attached).
@@ -1447,6 +1467,7 @@ l1dm_status sortfree_entry(const float *X, int64_t n, int64_t ld_x, int64_t d, i
     for (void *q : {ws, xs, zs, ys, ms})
       if (q) cudaFreeAsync(q, s);
   };
+  keep_default_pool();
   cudaError_t e = cudaMallocAsync(&ws, wsb, s);
   const float *Xd = X, *Zd = Z;
   const double *Md = M;
@@ -1993,6 +2014,7 @@ struct Scratch {
   }
   cudaError_t reserve(size_t bytes) {
     cap = bytes;
+    keep_default_pool();
     return cudaMallocAsync(reinterpret_cast<void **>(&base), bytes ? bytes : 256, s);
   }
   template <typename T>
