@@ -2134,16 +2134,33 @@ void launch_runs_query(const uint8_t *runid, int64_t ldn, int64_t n, int64_t dl,
       dim3 grid((unsigned)((i1 - i0 + ppb - 1) / ppb), (unsigned)((m + V * LPP - 1) / (V * LPP)));
       kern<<<grid, 256, 0, s>>>(runid, ldn, i1, dl, H, m, hsum, Sg, Y, ldy, i0);
     };
+    // narrow coordinate shards (dl < 16, e.g. c5 at G = 8: 12): 4 run ids in flight per step,
+    // so the unrolled body covers the shard instead of the one-at-a-time tail loop
+    const bool narrow = dl < 16;
     if (m % 2 == 0) {
       const int64_t lpp = m / 2;
-      if (lpp <= 1) g(k22_runs_gather<2, 1, 8>, 1, 2);
+      if (narrow) {
+        if (lpp <= 1) g(k22_runs_gather<2, 1, 4>, 1, 2);
+        else if (lpp <= 2) g(k22_runs_gather<2, 2, 4>, 2, 2);
+        else if (lpp <= 4) g(k22_runs_gather<2, 4, 4>, 4, 2);
+        else if (lpp <= 8) g(k22_runs_gather<2, 8, 4>, 8, 2);
+        else if (lpp <= 16) g(k22_runs_gather<2, 16, 4>, 16, 2);
+        else g(k22_runs_gather<2, 32, 4>, 32, 2);
+      } else if (lpp <= 1) g(k22_runs_gather<2, 1, 8>, 1, 2);
       else if (lpp <= 2) g(k22_runs_gather<2, 2, 8>, 2, 2);
       else if (lpp <= 4) g(k22_runs_gather<2, 4, 8>, 4, 2);
       else if (lpp <= 8) g(k22_runs_gather<2, 8, L1DM_RUNS_UNR>, 8, 2);
       else if (lpp <= 16) g(k22_runs_gather<2, 16, 8>, 16, 2);
       else g(k22_runs_gather<2, 32, 8>, 32, 2);
     } else {
-      if (m <= 1) g(k22_runs_gather<1, 1, 8>, 1, 1);
+      if (narrow) {
+        if (m <= 1) g(k22_runs_gather<1, 1, 4>, 1, 1);
+        else if (m <= 2) g(k22_runs_gather<1, 2, 4>, 2, 1);
+        else if (m <= 4) g(k22_runs_gather<1, 4, 4>, 4, 1);
+        else if (m <= 8) g(k22_runs_gather<1, 8, 4>, 8, 1);
+        else if (m <= 16) g(k22_runs_gather<1, 16, 4>, 16, 1);
+        else g(k22_runs_gather<1, 32, 4>, 32, 1);
+      } else if (m <= 1) g(k22_runs_gather<1, 1, 8>, 1, 1);
       else if (m <= 2) g(k22_runs_gather<1, 2, 8>, 2, 1);
       else if (m <= 4) g(k22_runs_gather<1, 4, 8>, 4, 1);
       else if (m <= 8) g(k22_runs_gather<1, 8, 8>, 8, 1);
