@@ -1900,7 +1900,26 @@ __global__ void __launch_bounds__(256)
   const int64_t k = e / m, c = e - (e / m) * m;
   const uint32_t R = nruns[k];
   double P = 0.0, Q = 0.0;
-  for (uint32_t j = 0; j < R; ++j) {
+  uint32_t j = 0;
+  // eight runs' H and values loaded before the in-place stores (the sequential form waits one
+  // L2 round trip per run: 256 of them per query whatever dl is); same order of additions
+  for (; j + 8 <= R; j += 8) {
+    double h8[8];
+    float v8[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      h8[u] = H[(k * 256 + j + u) * m + c];
+      v8[u] = rvals[k * 256 + j + u];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double v = (double)v8[u];
+      H[(k * 256 + j + u) * m + c] = fma(v, P, -Q);
+      P += h8[u];
+      Q = fma(v, h8[u], Q);
+    }
+  }
+  for (; j < R; ++j) {
     double *hp = H + (k * 256 + j) * m + c;
     const double h = *hp, v = (double)rvals[k * 256 + j];
     *hp = fma(v, P, -Q);  // U at run j (exclusive prefixes)
@@ -1989,6 +2008,24 @@ __global__ void __launch_bounds__(256)
       }
     }
   }
+  if constexpr (UNR > 4) {  // the remainder four run ids at a time before the singles
+    for (; k + 4 <= dl; k += 4) {
+      uint32_t r[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) r[u] = __ldg(rp + (k + u) * ldn);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double *p = ub + ((k + u) * 256 + r[u]) * m;
+        if constexpr (V == 2) {
+          const double2 v = __ldg(reinterpret_cast<const double2 *>(p));
+          acc[0] += v.x;
+          acc[1] += v.y;
+        } else {
+          acc[0] += __ldg(p);
+        }
+      }
+    }
+  }
   for (; k < dl; ++k) {
     const double *p = ub + (k * 256 + __ldg(rp + k * ldn)) * m;
 #pragma unroll
@@ -2016,6 +2053,7 @@ __global__ void __launch_bounds__(256)
   double T[K], M[K];
 #pragma unroll
   for (int t = 0; t < K; ++t) T[t] = M[t] = 0.0;
+#pragma unroll 8  // eight runs' loads in flight (no stores in this loop)
   for (uint32_t j = 0; j < R; ++j) {
     const double h = H[(k * 256 + j) * m + c], v = (double)rvals[k * 256 + j];
     double hv = h;
@@ -2025,26 +2063,40 @@ __global__ void __launch_bounds__(256)
       hv *= v;
     }
   }
-  for (uint32_t j = 0; j < R; ++j) {
-    double *hp = H + (k * 256 + j) * m + c;
-    const double h = *hp, v = (double)rvals[k * 256 + j];
-    double vp[K];
-    vp[0] = 1.0;
+  for (uint32_t j0 = 0; j0 < R; j0 += 8) {
+    // the next eight runs' H and values loaded before the in-place stores (as k21_runs_scan)
+    double h8[8];
+    float v8[8];
 #pragma unroll
-    for (int t = 1; t < K; ++t) vp[t] = vp[t - 1] * v;
-    double w = 0.0;
-#pragma unroll
-    for (int t = 0; t < K; ++t) {
-      double b = 1.0;  // c_t = C(P, t) (-1)^t
-      for (int q = 0; q < t; ++q) b = b * (double)(P - q) / (double)(q + 1);
-      w = fma(((t & 1) ? -b : b) * vp[P - t], fma(2.0, M[t], -T[t]), w);
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t ju = j0 + u < R ? j0 + u : R - 1;
+      h8[u] = H[(k * 256 + ju) * m + c];
+      v8[u] = rvals[k * 256 + ju];
     }
-    *hp = w;
-    double hv = h;
 #pragma unroll
-    for (int t = 0; t < K; ++t) {
-      M[t] += hv;
-      hv *= v;
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t j = j0 + u;
+      if (j >= R) break;
+      double *hp = H + (k * 256 + j) * m + c;
+      const double h = h8[u], v = (double)v8[u];
+      double vp[K];
+      vp[0] = 1.0;
+#pragma unroll
+      for (int t = 1; t < K; ++t) vp[t] = vp[t - 1] * v;
+      double w = 0.0;
+#pragma unroll
+      for (int t = 0; t < K; ++t) {
+        double b = 1.0;  // c_t = C(P, t) (-1)^t
+        for (int q = 0; q < t; ++q) b = b * (double)(P - q) / (double)(q + 1);
+        w = fma(((t & 1) ? -b : b) * vp[P - t], fma(2.0, M[t], -T[t]), w);
+      }
+      *hp = w;
+      double hv = h;
+#pragma unroll
+      for (int t = 0; t < K; ++t) {
+        M[t] += hv;
+        hv *= v;
+      }
     }
   }
 }
@@ -2143,7 +2195,10 @@ void launch_runs_query(const uint8_t *runid, int64_t ldn, int64_t n, int64_t dl,
         if (lpp <= 1) g(k22_runs_gather<2, 1, 4>, 1, 2);
         else if (lpp <= 2) g(k22_runs_gather<2, 2, 4>, 2, 2);
         else if (lpp <= 4) g(k22_runs_gather<2, 4, 4>, 4, 2);
-        else if (lpp <= 8) g(k22_runs_gather<2, 8, 4>, 8, 2);
+        else if (lpp <= 8) {
+          if (dl >= 8) g(k22_runs_gather<2, 8, 8>, 8, 2);  // 8 + a 4-wide remainder (c5 at G = 8: 12)
+          else g(k22_runs_gather<2, 8, 4>, 8, 2);
+        }
         else if (lpp <= 16) g(k22_runs_gather<2, 16, 4>, 16, 2);
         else g(k22_runs_gather<2, 32, 4>, 32, 2);
       } else if (lpp <= 1) g(k22_runs_gather<2, 1, 8>, 1, 2);

@@ -71,7 +71,8 @@ def test_lp_integer_ties_exact(p, mode):
 # runs mode (<= 256 distinct values per coordinate) for odd p: float values,
 # ragged n, m across the expansion's lane layouts (even / odd, > 32)
 @pytest.mark.parametrize("p", [3, 5, 7])
-@pytest.mark.parametrize("n,d,m", [(2, 1, 1), (999, 3, 2), (4097, 5, 7), (2500, 2, 40)])
+@pytest.mark.parametrize("n,d,m", [(2, 1, 1), (999, 3, 2), (4097, 5, 7), (2500, 2, 40),
+                                   (4100, 4, 8), (4099, 3, 6)])
 def test_lp_runs_float_few_values(n, d, m, p):
     rng = np.random.default_rng(n + 3 * d + 11 * m + p)
     X = (rng.integers(-40, 41, size=(n, d)) / 9.0).astype(np.float32)

@@ -16,7 +16,11 @@ TOL = 1e-9
 
 @pytest.mark.parametrize("n,d,m", [(2, 1, 1), (1000, 3, 1), (40000, 12, 16), (5001, 4, 3),
                                    (3000, 5, 17), (2500, 2, 40), (1500, 3, 66), (1200, 2, 71),
-                                   (777, 9, 2)])
+                                   (777, 9, 2),
+                                   # the expansion's run-id loop: 16-, 8- and 4-wide steps
+                                   # with 4-wide and single remainders, narrow and wide shards
+                                   (8000, 3, 66), (9000, 14, 8), (4500, 28, 4), (4500, 29, 4),
+                                   (4097, 1, 4), (5000, 6, 16), (4100, 12, 12)])
 def test_runs_integer_exact(n, d, m):
     rng = np.random.default_rng(n + 7 * m)
     X = rng.integers(0, 256, size=(n, d)).astype(np.float32)
