@@ -240,7 +240,7 @@ struct l1dm_ctx {
   DevBuf<uint8_t> runid;   // [dl][ldn] run index of point i
   DevBuf<float> rvals;     // [dl][256] distinct values, ascending
   DevBuf<uint32_t> nruns;  // [dl]
-  DevBuf<double> rtab;     // [dl][256][m] query table: H, then U in place
+  DevBuf<double> rtab;     // [copies][dl][256][m] query table: H (replicas folded into the first), then U in place
   // query workspace
   DevBuf<double> U;
   DevBuf<uint32_t> flags;
@@ -738,7 +738,7 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
   };
   if (!blocked && use_runs(h)) {
     // runs mode: tie-heavy coordinates, no sorted-order gather at all
-    CUDA_TRY(h->rtab.ensure((size_t)h->dl * 256 * m, false, s));
+    CUDA_TRY(h->rtab.ensure((size_t)runs_copies(h->dl, m) * h->dl * 256 * m, false, s));
     CUDA_TRY(h->part.ensure((size_t)h->dl * 2 * m, false, s));
     CUDA_TRY(h->Sg.ensure((size_t)2 * m, false, s));
     {
@@ -1025,7 +1025,7 @@ l1dm_status matvec_device(l1dm_ctx *h, const float *Z, int64_t ldz, int64_t m, d
 l1dm_status lp_device(l1dm_ctx *h, int lp, const float *Z, int64_t ldz, int64_t m, double *Y,
                       int64_t ldy, cudaStream_t s) {
   if (use_runs(h)) {  // tie-heavy data: the run-level form serves every odd p
-    CUDA_TRY(h->rtab.ensure((size_t)h->dl * 256 * m, false, s));
+    CUDA_TRY(h->rtab.ensure((size_t)runs_copies(h->dl, m) * h->dl * 256 * m, false, s));
     {
       TimedScope ts(h, kScan, s);
       launch_runs_lp(h->runid.p, h->ldn, h->n, h->dl, h->rvals.p, h->nruns.p, Z, ldz, m, lp,

@@ -90,6 +90,9 @@ void launch_runs_ids(const float *X, int64_t n, int64_t ldx, int64_t k0, int64_t
 #ifndef L1DM_RUNS_KG
 #define L1DM_RUNS_KG 96  // coordinates per run-histogram CTA (measured c5 step: kg 8 -> 32 cut 366 -> 303 ms; with 16 run ids in flight 32 -> 96: 273 -> 268 ms)
 #endif
+#ifndef L1DM_RUNS_COPIES
+#define L1DM_RUNS_COPIES 1  // replicate narrow run tables for the histogram's reductions (runs_copies)
+#endif
 #ifndef L1DM_RUNS_UNR
 #define L1DM_RUNS_UNR 16  // coordinates' run ids in flight per lane in the expansion (8.4 -> 5.2 ms)
 #endif
@@ -282,6 +285,7 @@ bool make_lp_plan(int64_t n, int64_t dl, int64_t m, int lp, int64_t l2_bytes, in
 // Runs mode.  phase 0: H (dl x 256 x m, zeroed here) <- run sums of Z, then U
 // in place and segtot (rows of 2m: S, T_k); phase 1: Y = 2 sum_k U[k][runid] + g - h S with
 // Sg = (S, g) from launch_totals.
+int runs_copies(int64_t dl, int64_t m);  // replicas of the [dl][256][m] run table the histogram needs
 void launch_runs_query(const uint8_t *runid, int64_t ldn, int64_t n, int64_t dl, const float *rvals,
                        const uint32_t *nruns, const float *Z, int64_t ldz, int64_t m, double *H,
                        double *segtot, const double *hsum, double *Sg, double *Y, int64_t ldy,

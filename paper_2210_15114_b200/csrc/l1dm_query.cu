@@ -1865,7 +1865,7 @@ void launch_fx_scale(const double *part, int64_t nparts, int64_t m, const uint32
 __global__ void __launch_bounds__(256)
     k20_runs_hist(const uint8_t *__restrict__ runid, int64_t ldn, int64_t n, int64_t dl,
                   const float *__restrict__ Z, int64_t ldz, int64_t m, int kg,
-                  double *__restrict__ H) {
+                  double *__restrict__ H, int copies) {
   // lane -> (point p within the warp's group of 32/L, column c), L = min(32, pow2 >= m)
   const int L = m >= 32 ? 32 : (m > 16 ? 32 : m > 8 ? 16 : m > 4 ? 8 : m > 2 ? 4 : m > 1 ? 2 : 1);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1876,6 +1876,10 @@ __global__ void __launch_bounds__(256)
   const int64_t pts_per_cta = 8 * ppw * 16;  // 16 steps per warp
   const int64_t i_base = (int64_t)blockIdx.x * pts_per_cta + (int64_t)w * ppw * 16;
   const uint64_t pol = l2_policy_evict_last();
+  // narrow tables (few coordinates) are spread over `copies` replicas, a warp on one of them:
+  // a table of a few thousand 128-byte lines loads the L2 slices unevenly, and how unevenly
+  // depends on where the allocation landed (runs_copies); folded by k20b_fold before the scan
+  H += (int64_t)((blockIdx.x * 8 + w) % (unsigned)copies) * (dl * 256 * m);
   for (int step = 0; step < 16; ++step) {
     const int64_t i = i_base + (int64_t)step * ppw + pg;
     if (i >= n) break;
@@ -1889,6 +1893,30 @@ __global__ void __launch_bounds__(256)
       }
     }
   }
+}
+
+// H[e] += H[e + r T] for the replicas r = 1 .. copies - 1 (in that order), T = dl 256 m.
+__global__ void __launch_bounds__(256)
+    k20b_fold(double *__restrict__ H, int64_t T, int copies) {
+  const int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (e >= T) return;
+  double a = H[e];
+  for (int r = 1; r < copies; ++r) a += H[e + (int64_t)r * T];
+  H[e] = a;
+}
+
+// Replicas of the run table for the histogram's reductions: enough that they spread over
+// ~24 k 128-byte lines (the G = 1 c5 table, which runs at the L2 reduction ceiling), at most 8.
+int runs_copies(int64_t dl, int64_t m) {
+#if L1DM_RUNS_COPIES
+  const int64_t lines = dl * 256 * m * 8 / 128;
+  int c = 1;
+  while (c < 8 && lines * c * 2 <= 24576) c *= 2;
+  return c;
+#else
+  (void)dl; (void)m;
+  return 1;
+#endif
 }
 
 __global__ void __launch_bounds__(256)
@@ -2114,12 +2142,15 @@ void launch_runs_lp(const uint8_t *runid, int64_t ldn, int64_t n, int64_t dl, co
   // phase 0: R1 as for l1 (the run sums of z), then the p-moment scan over runs in place of
   // the l1 prefix; phase 1: the expansion without the l1 epilogue (no g - h S for p > 1)
   if (phase == 0) {
-    cudaMemsetAsync(H, 0, (size_t)dl * 256 * m * sizeof(double), s);
+    const int copies = runs_copies(dl, m);
+    cudaMemsetAsync(H, 0, (size_t)copies * dl * 256 * m * sizeof(double), s);
     const int L = m >= 32 ? 32 : (m > 16 ? 32 : m > 8 ? 16 : m > 4 ? 8 : m > 2 ? 4 : m > 1 ? 2 : 1);
     const int64_t pts_per_cta = 8 * (32 / L) * 16;
     const int kg = runs_kg(dl);
     dim3 g1((unsigned)((n + pts_per_cta - 1) / pts_per_cta), (unsigned)((dl + kg - 1) / kg));
-    k20_runs_hist<<<g1, 256, 0, s>>>(runid, ldn, n, dl, Z, ldz, m, kg, H);
+    k20_runs_hist<<<g1, 256, 0, s>>>(runid, ldn, n, dl, Z, ldz, m, kg, H, copies);
+    if (copies > 1)
+      k20b_fold<<<(unsigned)((dl * 256 * m + 255) / 256), 256, 0, s>>>(H, dl * 256 * m, copies);
     const unsigned g2 = (unsigned)((dl * m + 255) / 256);
     switch (lp) {
       case 3: k21_runs_scan_lp<3><<<g2, 256, 0, s>>>(H, rvals, nruns, dl, m); break;
@@ -2157,12 +2188,15 @@ void launch_runs_query(const uint8_t *runid, int64_t ldn, int64_t n, int64_t dl,
                        double *segtot, const double *hsum, double *Sg, double *Y, int64_t ldy,
                        int phase, cudaStream_t s, int64_t i0, int64_t i1) {
   if (phase == 0) {
-    cudaMemsetAsync(H, 0, (size_t)dl * 256 * m * sizeof(double), s);
+    const int copies = runs_copies(dl, m);
+    cudaMemsetAsync(H, 0, (size_t)copies * dl * 256 * m * sizeof(double), s);
     const int L = m >= 32 ? 32 : (m > 16 ? 32 : m > 8 ? 16 : m > 4 ? 8 : m > 2 ? 4 : m > 1 ? 2 : 1);
     const int64_t pts_per_cta = 8 * (32 / L) * 16;
     const int kg = runs_kg(dl);
     dim3 g1((unsigned)((n + pts_per_cta - 1) / pts_per_cta), (unsigned)((dl + kg - 1) / kg));
-    k20_runs_hist<<<g1, 256, 0, s>>>(runid, ldn, n, dl, Z, ldz, m, kg, H);
+    k20_runs_hist<<<g1, 256, 0, s>>>(runid, ldn, n, dl, Z, ldz, m, kg, H, copies);
+    if (copies > 1)
+      k20b_fold<<<(unsigned)((dl * 256 * m + 255) / 256), 256, 0, s>>>(H, dl * 256 * m, copies);
     const int64_t t2 = dl * m;
     k21_runs_scan<<<(unsigned)((t2 + 255) / 256), 256, 0, s>>>(H, rvals, nruns, dl, m, segtot);
     return;
