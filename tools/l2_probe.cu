@@ -156,12 +156,15 @@ __global__ void __launch_bounds__(256) red_sweep(int64_t rows, double *y, uint32
 // the runs histogram's own reduction stream (k20_runs_hist at c5: m = 16 columns, 16 lanes per
 // 128-B row, 2 points per warp step, the point's 96 coordinates in turn, each into its 256-row
 // table at a pseudo-random run id): run ids hashed, z = 1 (no loads), tables dl x 256 x m
-__global__ void __launch_bounds__(256) red_runs_exact(int64_t npts, int dl, double *H) {
+__global__ void __launch_bounds__(256) red_runs_exact(int64_t npts, int dl, double *H,
+                                                      int copies = 1) {
   constexpr int L = 16, m = 16, ppw = 2;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int pg = lane / L, cl = lane % L;
   const int64_t pts_per_cta = 8 * ppw * 16;
   const int64_t i_base = (int64_t)blockIdx.x * pts_per_cta + (int64_t)w * ppw * 16;
+  // replicated tables (runs_copies in the library): a warp on replica (8 blockIdx.x + w) % copies
+  H += (int64_t)((blockIdx.x * 8 + w) % (unsigned)copies) * ((int64_t)dl * 256 * m);
   for (int step = 0; step < 16; ++step) {
     const int64_t i = i_base + (int64_t)step * ppw + pg;
     if (i >= npts) break;
@@ -277,6 +280,22 @@ int main() {
     if (rate > best_rate) {
       best_rate = rate;
       snprintf(best_cfg, sizeof(best_cfg), "runs_histogram_exact (k20's stream, 3 MiB tables)");
+    }
+    // the same stream on replicated tables, as the library runs it (runs_copies): 96 coordinates
+    // x 4 and 8 replicas, and a G = 8 shard's 12 coordinates x 1 and 8 replicas
+    for (int cfg = 0; cfg < 4; ++cfg) {
+      const int dlc = cfg < 2 ? 96 : 12, cp = cfg == 0 ? 4 : (cfg == 2 ? 1 : 8);
+      const float msr = best_ms(
+          [&] { red_runs_exact<<<(unsigned)(npts / 256), 256>>>(npts, dlc, y, cp); });
+      const double r = (double)npts * dlc * 16 / (msr * 1e-3);
+      printf(", {\"kernel\": \"runs_histogram_replicas\", \"row_bytes\": 128, \"coords\": %d, "
+             "\"replicas\": %d, \"MiB\": %.3g, \"adds_per_s\": %.4g}", dlc, cp,
+             dlc * 256 * 128.0 * cp / 1048576.0, r);
+      if (r > best_rate) {
+        best_rate = r;
+        snprintf(best_cfg, sizeof(best_cfg),
+                 "runs_histogram_replicas (k20's stream, %d coordinates x %d replicas)", dlc, cp);
+      }
     }
   }
   printf("], \"red_ceiling_adds_per_s\": %.4g, \"red_ceiling_config\": \"%s\", ", best_rate,
